@@ -1,0 +1,256 @@
+/*
+ * hps_b200.h -- C ABI of the B200-native HPS lookup path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no CUDA or torch
+ * types in the signatures (streams are passed as `void*` holding a
+ * cudaStream_t, NULL = the object's own stream). Every entry point names the
+ * reference interface it replaces (file:line under /root/reference/proj).
+ * The C++ shim in include/hps_b200/slab_cache.hpp re-exposes the
+ * reference's hps::SlabCache API on top of these calls, and
+ * paper_2210_08804_b200/__init__.py binds them with ctypes.
+ *
+ * Status codes: 0 OK, 1 INVALID_ARGUMENT (reference:
+ * std::invalid_argument), 2 INTERNAL / CUDA error, 3 OUT_OF_MEMORY,
+ * 4 LOGIC_ERROR (reference: std::logic_error from check_invariants),
+ * 5 TIER_FAULT (reference: hps::TierFault). hps_last_error() returns the
+ * thread-local message of the last failing call on this thread.
+ *
+ * Memory modes: HPS_MEM_HOST -- every key / row / output pointer is host
+ * memory; the call is synchronous (the reference's drop-in semantics).
+ * HPS_MEM_DEVICE -- key / row / output pointers are device memory on the
+ * object's GPU; work is ordered after `stream` and results are ready when
+ * `stream` reaches the point of the call. Calls that must report a count
+ * (query misses, update writes) synchronise before returning.
+ *
+ * Thread safety: every object serialises its own calls (one mutex and one
+ * CUDA stream per cache), matching the reference's per-call atomicity
+ * ("safe for arbitrary concurrent calls").
+ */
+#ifndef HPS_B200_H_
+#define HPS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_OK 0
+#define HPS_INVALID_ARGUMENT 1
+#define HPS_INTERNAL 2
+#define HPS_OUT_OF_MEMORY 3
+#define HPS_LOGIC_ERROR 4
+#define HPS_TIER_FAULT 5
+
+#define HPS_MEM_HOST 0
+#define HPS_MEM_DEVICE 1
+
+typedef struct hps_cache hps_cache;
+typedef struct hps_vdb hps_vdb;
+typedef struct hps_engine hps_engine;
+
+/* ---- vocabulary ------------------------------------------------------- */
+
+/* Thread-local message of the last failing call. */
+const char* hps_last_error(void);
+
+/* XXH64; replaces hps::xxh64 / xxh64_key (xxhash64.hpp:60-124). */
+uint64_t hps_xxh64(const void* data, size_t len, uint64_t seed);
+uint64_t hps_xxh64_key(uint64_t key, uint64_t seed);
+/* replaces SlabCache::slabset_of / first_slab_of (slab_cache.cpp:60-67) */
+uint64_t hps_slabset_of(uint64_t key, uint64_t slabset_count);
+uint32_t hps_first_slab_of(uint64_t key, uint32_t slabs_per_set);
+/* replaces hps::partition_of (volatile_store.cpp:10-13) */
+uint32_t hps_partition_of(uint64_t key, uint32_t partition_count);
+
+/* GPU dedup; replaces hps::dedup_keys (types.cpp:20-34). Writes the unique
+ * keys in first-occurrence order and the u32 inverse index; *n_unique gets
+ * the unique count. `unique_out` must hold n keys. */
+int hps_dedup_keys(int device, const uint64_t* keys, size_t n, uint64_t* unique_out,
+                   uint32_t* inverse_out, size_t* n_unique, int mem, void* stream);
+
+/* ---- embedding cache (replaces hps::SlabCache, slab_cache.hpp:41-116) ---- */
+
+/* Mirrors SlabCacheConfig (slab_cache.hpp:27-34). worker_pool_size and
+ * tasks_per_worker are validated like the reference (worker_pool_size == 0
+ * is an error) and map to keys-per-warp on the device. */
+typedef struct {
+  uint64_t slabset_count;
+  uint32_t slabs_per_set;
+  uint32_t dimension;
+  uint32_t worker_pool_size;
+  uint32_t tasks_per_worker;
+} hps_cache_config;
+
+typedef struct {
+  uint32_t dimension;
+  uint32_t slabs_per_set;
+  uint64_t slabset_count;
+  uint64_t capacity;
+  uint64_t occupied;
+  uint64_t recency_clock;
+  int device;
+  int reserved;
+} hps_cache_info;
+
+/* replaces SlabCache::SlabCache (slab_cache.cpp:17-41) */
+int hps_cache_create(const hps_cache_config* config, int device, hps_cache** out);
+/* replaces SlabCache::~SlabCache (slab_cache.cpp:43-52) */
+int hps_cache_destroy(hps_cache* cache);
+int hps_cache_get_info(hps_cache* cache, hps_cache_info* out);
+/* Raw cudaStream_t of the cache's own stream (for event-based chaining). */
+void* hps_cache_stream(hps_cache* cache);
+
+/* replaces SlabCache::query (slab_cache.cpp:69-91). Bumps the recency clock
+ * once, even for n == 0 and before the size check. Hit rows are copied into
+ * out (n * dimension floats, out_len must equal that), miss rows are left
+ * untouched. Misses are reported in ascending position order into
+ * miss_positions / miss_keys (each must hold n entries; same memory kind as
+ * keys) and their count into *n_miss (host). */
+int hps_cache_query(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
+                    size_t out_len, uint32_t* miss_positions, uint64_t* miss_keys,
+                    size_t* n_miss, int mem, void* stream);
+
+/* replaces SlabCache::replace (slab_cache.cpp:93-107). Rejects a wrong
+ * vector size or duplicate keys before any mutation. */
+int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n,
+                      const float* vectors, size_t vectors_len, int mem, void* stream);
+
+/* replaces SlabCache::update (slab_cache.cpp:109-125). *written = number of
+ * positions whose key was resident (duplicates count every time; the last
+ * occurrence's row wins). */
+int hps_cache_update(hps_cache* cache, const uint64_t* keys, size_t n,
+                     const float* vectors, size_t vectors_len, size_t* written,
+                     int mem, void* stream);
+
+/* replaces DumpCursor::next (slab_cache.cpp:367-394) over the slabset range
+ * [set_begin, set_end): resident keys in set, slab, slot order into the host
+ * buffer out (capacity cap). *n_out = number of resident keys in the range
+ * (may exceed cap; then only cap are written). */
+int hps_cache_dump(hps_cache* cache, uint64_t set_begin, uint64_t set_end,
+                   uint64_t* out, size_t cap, size_t* n_out);
+
+/* replaces SlabCache::check_invariants (slab_cache.cpp:407-442); returns
+ * HPS_LOGIC_ERROR with the reference's message on violation. */
+int hps_cache_check_invariants(hps_cache* cache);
+
+/* Test/diagnostic: copy the whole device table to host buffers (any may be
+ * NULL): keys/counters hold capacity entries, masks S*W, rows capacity*d. */
+int hps_cache_export_state(hps_cache* cache, uint64_t* keys, uint64_t* counters,
+                           uint32_t* masks, float* rows);
+
+/* ---- volatile DB (replaces hps::VolatileStore, volatile_store.hpp:45-137) ---- */
+
+int hps_vdb_create(uint32_t lookup_threads, hps_vdb** out);
+int hps_vdb_destroy(hps_vdb* vdb);
+/* replaces register_table (volatile_store.cpp:25-51) */
+int hps_vdb_register_table(hps_vdb* vdb, const char* name, uint32_t dimension,
+                           uint32_t partition_count, uint64_t overflow_margin);
+int hps_vdb_has_table(hps_vdb* vdb, const char* name);
+/* replaces insert (volatile_store.cpp:113-152); evicted keys (if not NULL,
+ * capacity evicted_cap) and their count. */
+int hps_vdb_insert(hps_vdb* vdb, const char* name, const uint64_t* keys, size_t n,
+                   const float* vectors, size_t vectors_len, uint64_t* evicted,
+                   size_t evicted_cap, size_t* n_evicted);
+/* replaces insert_async (volatile_store.cpp:174-188) */
+int hps_vdb_insert_async(hps_vdb* vdb, const char* name, const uint64_t* keys,
+                         size_t n, const float* vectors, size_t vectors_len);
+/* replaces lookup (volatile_store.cpp:82-112): found keys / rows in input
+ * order, missing keys in input order; each output holds n entries (rows:
+ * n * dim). */
+int hps_vdb_lookup(hps_vdb* vdb, const char* name, const uint64_t* keys, size_t n,
+                   uint64_t* found_keys, float* found_vectors, size_t* n_found,
+                   uint64_t* missing_keys, size_t* n_missing);
+/* replaces drain (volatile_store.cpp:250-253) */
+int hps_vdb_drain(hps_vdb* vdb);
+/* replaces table_size / partition_size / table_clock / last_access */
+int hps_vdb_table_size(hps_vdb* vdb, const char* name, uint64_t* out);
+int hps_vdb_partition_size(hps_vdb* vdb, const char* name, uint32_t partition,
+                           uint64_t* out);
+int hps_vdb_table_clock(hps_vdb* vdb, const char* name, uint64_t* out);
+/* *found = 0 when the key is absent */
+int hps_vdb_last_access(hps_vdb* vdb, const char* name, uint64_t key, uint64_t* out,
+                        int* found);
+/* replaces evict (volatile_store.cpp:190-199) */
+int hps_vdb_evict(hps_vdb* vdb, const char* name, uint32_t partition,
+                  uint64_t* evicted, size_t evicted_cap, size_t* n_evicted);
+
+/* ---- cold tier callback (stands in for hps::PersistentStore::get,
+ *      persistent_store.cpp:405-439, which stays CPU code) ---- */
+typedef int (*hps_cold_fetch_fn)(void* ctx, const uint64_t* keys, size_t n,
+                                 uint64_t* found_keys, float* found_vectors,
+                                 size_t* n_found, uint64_t* missing_keys,
+                                 size_t* n_missing);
+
+/* replaces hps::tier_fetch (lookup_engine.cpp:50-89): VDB first (if vdb and
+ * the table are present), then the cold tier for the rest; cold hits are
+ * promoted to the VDB asynchronously. counters (may be NULL) receives
+ * {vdb_hits, cold_hits, missing}. */
+int hps_tier_fetch(hps_vdb* vdb, const char* table, uint32_t dimension,
+                   hps_cold_fetch_fn cold, void* cold_ctx, const uint64_t* keys,
+                   size_t n, uint64_t* found_keys, float* found_vectors,
+                   size_t* n_found, uint64_t* missing_keys, size_t* n_missing,
+                   uint64_t* counters);
+
+/* ---- lookup engine (replaces hps::LookupEngine, lookup_engine.hpp:152-196) ---- */
+
+/* Mirrors EngineConfig (lookup_engine.hpp:29-37). */
+typedef struct {
+  double hit_rate_threshold;
+  const float* default_vector; /* may be NULL = zeros; padded / cut to dim */
+  uint32_t default_vector_len;
+  uint32_t workspace_pool_size;
+  uint32_t async_worker_count;
+  int volatile_tier_enabled;
+  uint32_t max_batch; /* device workspace capacity in keys (0 = 131072) */
+} hps_engine_config;
+
+/* Mirrors LookupOutcome (lookup_engine.hpp:145-150). */
+typedef struct {
+  int sync_branch;
+  double unique_hit_rate;
+  uint64_t unique_count;
+  uint64_t defaults_returned;
+} hps_lookup_outcome;
+
+/* Mirrors EngineStatsSnapshot (lookup_engine.hpp:129-142), same order. */
+typedef struct {
+  uint64_t queries, queried_keys, unique_keys, cache_hits, cache_misses,
+      sync_batches, async_batches, defaults_returned, vdb_hits, pdb_hits,
+      tier_missing, async_faults;
+} hps_engine_stats;
+
+/* replaces LookupEngine::LookupEngine (lookup_engine.cpp:91-117); vdb and
+ * cold may be NULL. The engine keeps pointers to cache / vdb, which must
+ * outlive it. */
+int hps_engine_create(const char* table, uint32_t dimension, hps_cache* cache,
+                      hps_vdb* vdb, hps_cold_fetch_fn cold, void* cold_ctx,
+                      const hps_engine_config* config, hps_engine** out);
+int hps_engine_destroy(hps_engine* engine);
+
+/* replaces LookupEngine::lookup (lookup_engine.cpp:130-241). out holds
+ * n * dimension floats (out_len must equal that), miss_flags n bytes;
+ * outcome may be NULL. */
+int hps_engine_lookup(hps_engine* engine, const uint64_t* keys, size_t n, float* out,
+                      size_t out_len, uint8_t* miss_flags, hps_lookup_outcome* outcome,
+                      int mem, void* stream);
+
+/* replaces drain_async (lookup_engine.cpp:286-289) */
+int hps_engine_drain_async(hps_engine* engine);
+/* replaces stats (lookup_engine.cpp:291-294) */
+int hps_engine_get_stats(hps_engine* engine, hps_engine_stats* out);
+/* replaces WorkspacePool::size / outstanding / peak_outstanding */
+int hps_engine_pool_info(hps_engine* engine, uint64_t* size, uint64_t* outstanding,
+                         uint64_t* peak_outstanding);
+
+/* ---- workload (harness input; replaces PowerLawSampler::sample,
+ *      workload.cpp:24-70, bit-exact) ---- */
+int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,
+                        uint64_t draw_seed, size_t count, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPS_B200_H_ */

@@ -1,0 +1,63 @@
+"""Builds the in-tree native library libhps_b200.so with nvcc for sm_100a.
+
+All translation units (CUDA kernels, the host runtime and the C ABI) are
+compiled by nvcc (`-x cu` for the .cpp files, which share the device
+headers) and linked into one shared object next to this file, so the GPU box
+receives it with the repo snapshot. Incremental: objects are rebuilt only
+when a source or header is newer.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "build"
+LIB = PKG / "libhps_b200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+         "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+
+SOURCES = ["cache_kernels.cu", "lookup_kernels.cu", "device_cache.cpp", "volatile_store.cpp",
+           "engine.cpp", "workload.cpp", "capi.cpp"]
+
+
+def _newest_header() -> float:
+    hs = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + list((ROOT / "include").glob("*.h"))
+    return max(h.stat().st_mtime for h in hs)
+
+
+def build(verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    hdr = _newest_header()
+    objs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = BUILD / (src + ".o")
+        objs.append(o)
+        if o.exists() and o.stat().st_mtime >= max(s.stat().st_mtime, hdr):
+            continue
+        cmd = [NVCC, *ARCH, *FLAGS]
+        if src.endswith(".cpp"):
+            cmd += ["-x", "cu"]
+        cmd += ["-c", str(s), "-o", str(o)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    if not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+               "-lpthread", "-ldl", "-lrt"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose=True))

@@ -1,0 +1,538 @@
+// cache_kernels.cu -- sm_100a kernels for SlabCache query / replace /
+// update / dump and for GPU dedup.
+//
+// Reference behaviour restated here (all under /root/reference/proj):
+//   query    core/src/slab_cache.cpp:69-91, 228-259
+//   replace  core/src/slab_cache.cpp:93-107, 261-326
+//   update   core/src/slab_cache.cpp:109-125, 328-358
+//   dump     core/src/slab_cache.cpp:360-394
+//   dedup    core/src/types.cpp:20-34
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.hpp"
+#include "probe.cuh"
+
+namespace hpsb {
+
+namespace {
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+inline uint64_t pow2_at_least(uint64_t v) {
+  uint64_t c = 16;
+  while (c < v) c <<= 1;
+  return c;
+}
+
+inline uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+constexpr int kWarpsPerBlock = 8;  // 256-thread blocks for warp-per-key kernels
+
+}  // namespace
+
+// ------------------------------------------------------------------ scan --
+void scan_begin(ScanState& s, uint64_t tiles, cudaStream_t st) {
+  (void)tiles;
+  s.epoch = (s.epoch + 1) & 0xFFFFFFu;
+  if (s.epoch == 0) {
+    // 24-bit epoch wrapped: clear the status words once, then restart at 1
+    cudaMemsetAsync(s.status, 0, s.capacity_tiles * sizeof(uint64_t), st);
+    s.epoch = 1;
+  }
+}
+
+// ------------------------------------------------------------------ query --
+// One warp serves P keys (P = keys_per_warp): hits copy the row into out[i]
+// and stamp the slot; misses leave out[i] untouched (slab_cache.cpp:248-251).
+template <int P>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_cache_query(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                  float* __restrict__ out, uint8_t* __restrict__ hit, uint64_t stamp) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * kWarpsPerBlock) + (threadIdx.x >> 5);
+  const uint64_t base = warp * P;
+  if (base >= n) return;
+  WarpKeys<P> wk;
+  warp_load_keys<P>(c, keys, base, n, wk);
+  int64_t slot[P];
+  warp_probe<P>(c, wk, slot);
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    if (!wk.valid[p]) continue;
+    const uint64_t i = base + p;
+    if (slot[p] >= 0) {
+      warp_copy_row(c.rows + uint64_t(slot[p]) * c.d, out + i * c.d, c.d);
+      if (lane == 0) {
+        c.counters[slot[p]] = stamp;
+        hit[i] = 1;
+      }
+    } else if (lane == 0) {
+      hit[i] = 0;
+    }
+  }
+}
+
+void launch_cache_query(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
+                        uint8_t* hit, uint64_t stamp, int keys_per_warp, cudaStream_t st) {
+  if (n == 0) return;
+  const int P = keys_per_warp >= 8 ? 8 : (keys_per_warp >= 4 ? 4 : (keys_per_warp >= 2 ? 2 : 1));
+  const uint64_t warps = (n + P - 1) / P;
+  const dim3 grid(unsigned((warps + kWarpsPerBlock - 1) / kWarpsPerBlock));
+  const dim3 block(kWarpsPerBlock * 32);
+  switch (P) {
+    case 8: k_cache_query<8><<<grid, block, 0, st>>>(c, keys, n, out, hit, stamp); break;
+    case 4: k_cache_query<4><<<grid, block, 0, st>>>(c, keys, n, out, hit, stamp); break;
+    case 2: k_cache_query<2><<<grid, block, 0, st>>>(c, keys, n, out, hit, stamp); break;
+    default: k_cache_query<1><<<grid, block, 0, st>>>(c, keys, n, out, hit, stamp); break;
+  }
+  check_launch("cache_query");
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    k_select_misses(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ hit,
+                    uint64_t n, uint32_t* __restrict__ miss_pos,
+                    uint64_t* __restrict__ miss_keys, unsigned long long* n_miss,
+                    ScanState scan) {
+  select_tile(
+      n, scan, [&](uint64_t i) { return hit[i] == 0; },
+      [&](uint64_t i, uint64_t r) {
+        miss_pos[r] = uint32_t(i);
+        miss_keys[r] = keys[i];
+      },
+      n_miss);
+}
+
+void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
+                          uint32_t* miss_pos, uint64_t* miss_keys,
+                          unsigned long long* n_miss, ScanState& scan, cudaStream_t st) {
+  if (n == 0) {
+    cudaMemsetAsync(n_miss, 0, sizeof(unsigned long long), st);
+    return;
+  }
+  const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+  scan_begin(scan, tiles, st);
+  k_select_misses<<<unsigned(tiles), kScanBlock, 0, st>>>(keys, hit, n, miss_pos, miss_keys,
+                                                          n_miss, scan);
+  scan.tile_base += tiles;
+  check_launch("select_misses");
+}
+
+// ---------------------------------------------------------------- replace --
+// Deterministic parity with the reference's grouped application
+// (slab_cache.cpp:131-142: keys grouped by slabset, input order inside a
+// group): (A) hash keys into a table of touched slabsets and count,
+// (B) give each touched set a bucket range, (C) scatter key indices into
+// the buckets, (D) one warp per touched set sorts its (few) indices and
+// applies them serially with ballot probes, lowest-free-slot insertion and
+// a warp argmin over the set's W*32 counters for eviction.
+size_t replace_scratch_bytes(uint64_t n) {
+  const uint64_t cap = pow2_at_least(2 * n);
+  return align_up(cap * 8, 256) + 3 * align_up(cap * 4, 256) + 2 * align_up(n * 4, 256) + 256;
+}
+
+ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
+  ReplaceScratch r;
+  r.cap = pow2_at_least(2 * n);
+  char* p = static_cast<char*>(base);
+  r.tab_set = reinterpret_cast<uint64_t*>(p);
+  p += align_up(r.cap * 8, 256);
+  r.tab_cnt = reinterpret_cast<uint32_t*>(p);
+  p += align_up(r.cap * 4, 256);
+  r.tab_fill = reinterpret_cast<uint32_t*>(p);
+  p += align_up(r.cap * 4, 256);
+  r.tab_off = reinterpret_cast<uint32_t*>(p);
+  p += align_up(r.cap * 4, 256);
+  r.key_tab = reinterpret_cast<uint32_t*>(p);
+  p += align_up(n * 4, 256);
+  r.bucket = reinterpret_cast<uint32_t*>(p);
+  p += align_up(n * 4, 256);
+  r.cursor = reinterpret_cast<uint32_t*>(p);
+  r.dup_flag = r.cursor + 1;
+  return r;
+}
+
+__global__ void k_replace_group(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                                ReplaceScratch rs) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t s = xxh64_key(keys[i], kSlabsetSeed) % c.S;
+  uint64_t t = fmix64(s) & (rs.cap - 1);
+  while (true) {
+    const unsigned long long old =
+        atomicCAS(reinterpret_cast<unsigned long long*>(rs.tab_set + t), ~0ull, s);
+    if (old == ~0ull || old == s) break;
+    t = (t + 1) & (rs.cap - 1);
+  }
+  rs.key_tab[i] = uint32_t(t);
+  atomicAdd(rs.tab_cnt + t, 1u);
+}
+
+__global__ void k_replace_offsets(ReplaceScratch rs) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rs.cap) return;
+  const uint32_t cnt = rs.tab_cnt[t];
+  if (cnt) rs.tab_off[t] = atomicAdd(rs.cursor, cnt);
+}
+
+__global__ void k_replace_bucket(uint64_t n, ReplaceScratch rs) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t t = rs.key_tab[i];
+  const uint32_t pos = atomicAdd(rs.tab_fill + t, 1u);
+  rs.bucket[rs.tab_off[t] + pos] = uint32_t(i);
+}
+
+// Sorts bucket[off, off+cnt) ascending. cnt <= 32: rank sort in registers;
+// larger groups (tiny caches) fall back to a lane-0 insertion sort.
+__device__ __forceinline__ void warp_sort_group(uint32_t* b, uint32_t cnt) {
+  const uint32_t lane = lane_id();
+  if (cnt <= 32) {
+    const uint32_t v = lane < cnt ? b[lane] : 0xFFFFFFFFu;
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint32_t o = __shfl_sync(0xFFFFFFFFu, v, j);
+      rank += (o < v) ? 1u : 0u;
+    }
+    __syncwarp();
+    if (lane < cnt) b[rank] = v;
+  } else if (lane == 0) {
+    for (uint32_t a = 1; a < cnt; ++a) {
+      const uint32_t x = b[a];
+      uint32_t j = a;
+      while (j > 0 && b[j - 1] > x) {
+        b[j] = b[j - 1];
+        --j;
+      }
+      b[j] = x;
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void k_replace_validate(const uint64_t* __restrict__ keys, ReplaceScratch rs) {
+  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= rs.cap) return;
+  const uint32_t cnt = rs.tab_cnt[t];
+  if (cnt < 2) return;
+  const uint32_t* b = rs.bucket + rs.tab_off[t];
+  const uint32_t lane = lane_id();
+  bool dup = false;
+  for (uint32_t x = lane; x < cnt; x += 32) {
+    const uint64_t kx = keys[b[x]];
+    for (uint32_t y = x + 1; y < cnt; ++y) dup |= (keys[b[y]] == kx);
+  }
+  if (__any_sync(0xFFFFFFFFu, dup) && lane == 0) atomicOr(rs.dup_flag, 1u);
+}
+
+__global__ void k_replace_apply(CacheDev c, const uint64_t* __restrict__ keys,
+                                const float* __restrict__ rows, uint64_t stamp,
+                                ReplaceScratch rs) {
+  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= rs.cap) return;
+  const uint32_t cnt = rs.tab_cnt[t];
+  if (cnt == 0) return;
+  if (*reinterpret_cast<volatile uint32_t*>(rs.dup_flag)) return;  // rejected before mutation
+  uint32_t* b = rs.bucket + rs.tab_off[t];
+  warp_sort_group(b, cnt);
+  const uint32_t lane = lane_id();
+  const uint64_t set = rs.tab_set[t];
+  volatile uint32_t* vmask = c.masks;
+  volatile uint64_t* vkeys = c.keys;
+  volatile uint64_t* vctr = c.counters;
+  const uint64_t per_set = uint64_t(c.W) * kSlotsPerSlab;
+  for (uint32_t g = 0; g < cnt; ++g) {
+    const uint32_t i = b[g];
+    const uint64_t key = keys[i];
+    const uint32_t first = uint32_t(xxh64_key(key, kSlabSeed) % c.W);
+    int64_t found = -1;
+    int64_t ins_slab = -1;
+    for (uint32_t step = 0; step < c.W; ++step) {
+      uint32_t sl = first + step;
+      sl = (sl >= c.W) ? sl - c.W : sl;
+      const uint64_t slab = set * c.W + sl;
+      const uint32_t m = vmask[slab];
+      const uint64_t k = vkeys[slab * kSlotsPerSlab + lane];
+      const uint32_t hitb = __ballot_sync(0xFFFFFFFFu, ((m >> lane) & 1u) && k == key);
+      if (hitb) {
+        found = int64_t(slab * kSlotsPerSlab + (__ffs(hitb) - 1));
+        break;
+      }
+      if (m != kFullSlab) {
+        ins_slab = int64_t(slab);
+        break;
+      }
+    }
+    if (found >= 0) {
+      // resident: recency refresh only, vector kept (slab_cache.cpp:283-288)
+      if (lane == 0) vctr[found] = stamp;
+      __syncwarp();
+      continue;
+    }
+    uint64_t slot;
+    if (ins_slab >= 0) {
+      const uint32_t m = vmask[ins_slab];
+      const uint32_t j = __ffs(~m) - 1;  // countr_one(mask) (slab_cache.cpp:299)
+      slot = uint64_t(ins_slab) * kSlotsPerSlab + j;
+      if (lane == 0) {
+        vmask[ins_slab] = m | (1u << j);
+        atomicAdd(c.occupied, 1ull);
+      }
+    } else {
+      // all slabs full: evict min counter, ties to lowest (slab, slot)
+      const uint64_t base = set * per_set;
+      uint64_t best_c = ~0ull;
+      uint32_t best_i = 0xFFFFFFFFu;
+      for (uint32_t s = lane; s < per_set; s += 32) {
+        const uint64_t cv = vctr[base + s];
+        if (cv < best_c) {
+          best_c = cv;
+          best_i = s;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, best_c, o);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, best_i, o);
+        if (oc < best_c || (oc == best_c && oi < best_i)) {
+          best_c = oc;
+          best_i = oi;
+        }
+      }
+      slot = base + best_i;
+    }
+    if (lane == 0) {
+      vkeys[slot] = key;
+      vctr[slot] = stamp;
+    }
+    warp_copy_row(rows + uint64_t(i) * c.d, c.rows + slot * c.d, c.d);
+    __threadfence_block();
+    __syncwarp();
+  }
+}
+
+void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
+                    uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st) {
+  if (n == 0) return;
+  cudaMemsetAsync(rs.tab_set, 0xFF, rs.cap * 8, st);
+  // tab_cnt, tab_fill are contiguous (carve order); cursor + dup_flag after buckets
+  cudaMemsetAsync(rs.tab_cnt, 0, rs.cap * 4, st);
+  cudaMemsetAsync(rs.tab_fill, 0, rs.cap * 4, st);
+  cudaMemsetAsync(rs.cursor, 0, 8, st);
+  const unsigned tb = 256;
+  k_replace_group<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(c, keys, n, rs);
+  k_replace_offsets<<<unsigned((rs.cap + tb - 1) / tb), tb, 0, st>>>(rs);
+  k_replace_bucket<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(n, rs);
+  const uint64_t warp_threads = rs.cap * 32;
+  if (validate) {
+    k_replace_validate<<<unsigned((warp_threads + tb - 1) / tb), tb, 0, st>>>(keys, rs);
+  }
+  k_replace_apply<<<unsigned((warp_threads + tb - 1) / tb), tb, 0, st>>>(c, keys, rows, stamp,
+                                                                          rs);
+  check_launch("replace");
+}
+
+// ----------------------------------------------------------------- update --
+// Overwrite resident rows; the last occurrence of a key in input order
+// wins (the reference applies a set's keys in input order,
+// slab_cache.cpp:137-142, 328-358). Phase A probes and records
+// max(position) per hit slot; phase B lets only that position write.
+size_t update_scratch_bytes(uint64_t n) {
+  const uint64_t cap = pow2_at_least(2 * n);
+  return align_up(cap * 8, 256) + align_up(cap * 4, 256) + align_up(n * 4, 256) + 256;
+}
+
+UpdateScratch update_scratch_carve(void* base, uint64_t n) {
+  UpdateScratch u;
+  u.cap = pow2_at_least(2 * n);
+  char* p = static_cast<char*>(base);
+  u.ut_key = reinterpret_cast<uint64_t*>(p);
+  p += align_up(u.cap * 8, 256);
+  u.ut_pos = reinterpret_cast<uint32_t*>(p);
+  p += align_up(u.cap * 4, 256);
+  u.found_tab = reinterpret_cast<uint32_t*>(p);
+  p += align_up(n * 4, 256);
+  u.written = reinterpret_cast<unsigned long long*>(p);
+  return u;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_update_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, UpdateScratch us) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * kWarpsPerBlock) + (threadIdx.x >> 5);
+  const uint64_t base = warp * P;
+  if (base >= n) return;
+  WarpKeys<P> wk;
+  warp_load_keys<P>(c, keys, base, n, wk);
+  int64_t slot[P];
+  warp_probe<P>(c, wk, slot);
+  const uint32_t lane = lane_id();
+  if (lane >= uint32_t(P)) return;
+  // lane p handles position base + p
+  int64_t my_slot = -1;
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (uint32_t(p) == lane) my_slot = slot[p];
+  const uint64_t i = base + lane;
+  if (i >= n) return;
+  if (my_slot < 0) {
+    us.found_tab[i] = 0xFFFFFFFFu;
+    return;
+  }
+  atomicAdd(us.written, 1ull);
+  const uint64_t g = uint64_t(my_slot);
+  uint64_t t = fmix64(g) & (us.cap - 1);
+  while (true) {
+    const unsigned long long old =
+        atomicCAS(reinterpret_cast<unsigned long long*>(us.ut_key + t), ~0ull, g);
+    if (old == ~0ull || old == g) break;
+    t = (t + 1) & (us.cap - 1);
+  }
+  atomicMax(us.ut_pos + t, uint32_t(i + 1));
+  us.found_tab[i] = uint32_t(t);
+}
+
+__global__ void k_update_write(CacheDev c, const float* __restrict__ rows, uint64_t n,
+                               UpdateScratch us) {
+  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const uint32_t t = us.found_tab[i];
+  if (t == 0xFFFFFFFFu) return;
+  if (us.ut_pos[t] != uint32_t(i + 1)) return;  // a later duplicate wins
+  const uint64_t g = us.ut_key[t];
+  warp_copy_row(rows + i * c.d, c.rows + g * c.d, c.d);
+}
+
+void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
+                   int keys_per_warp, const UpdateScratch& us, cudaStream_t st) {
+  cudaMemsetAsync(us.written, 0, 8, st);
+  if (n == 0) return;
+  cudaMemsetAsync(us.ut_key, 0xFF, us.cap * 8, st);
+  cudaMemsetAsync(us.ut_pos, 0, us.cap * 4, st);
+  const int P = keys_per_warp >= 8 ? 8 : (keys_per_warp >= 4 ? 4 : 1);
+  const uint64_t warps = (n + P - 1) / P;
+  const unsigned grid = unsigned((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  switch (P) {
+    case 8: k_update_probe<8><<<grid, kWarpsPerBlock * 32, 0, st>>>(c, keys, n, us); break;
+    case 4: k_update_probe<4><<<grid, kWarpsPerBlock * 32, 0, st>>>(c, keys, n, us); break;
+    default: k_update_probe<1><<<grid, kWarpsPerBlock * 32, 0, st>>>(c, keys, n, us); break;
+  }
+  const uint64_t threads = n * 32;
+  k_update_write<<<unsigned((threads + 255) / 256), 256, 0, st>>>(c, rows, n, us);
+  check_launch("update");
+}
+
+// ------------------------------------------------------------------- dump --
+// Resident keys of slabs [set_begin*W, set_end*W) in slab order, slot order
+// inside a slab (slab_cache.cpp:380-392). One item = one slab.
+// Count-weighted variant of select_tile: each item contributes popc(mask).
+__global__ void __launch_bounds__(kScanBlock)
+    k_dump_keys(CacheDev c, uint64_t slab_begin, uint64_t n_slabs, uint64_t* __restrict__ out,
+                unsigned long long* n_out, ScanState scan) {
+  __shared__ uint32_t s_warp[kScanBlock / 32];
+  __shared__ uint64_t s_tile;
+  __shared__ uint64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(scan.tile_ctr, 1ull) - scan.tile_base;
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t first = tile * kScanTile + uint64_t(threadIdx.x) * kScanItems;
+  uint32_t m[kScanItems];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint64_t s = first + k;
+    m[k] = (s < n_slabs) ? c.masks[slab_begin + s] : 0u;
+    cnt += __popc(m[k]);
+  }
+  uint32_t block_total;
+  const uint32_t excl = block_exclusive_scan<kScanBlock>(cnt, s_warp, &block_total);
+  if (threadIdx.x < 32) {
+    const uint64_t pre = lb_exclusive_prefix(scan.status, uint32_t(tile), scan.epoch, block_total);
+    if (threadIdx.x == 0) {
+      s_prefix = pre;
+      const uint64_t tiles = (n_slabs + kScanTile - 1) / kScanTile;
+      if (tile == tiles - 1) *n_out = pre + block_total;
+    }
+  }
+  __syncthreads();
+  uint64_t r = s_prefix + excl;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    uint32_t mm = m[k];
+    const uint64_t slab = slab_begin + first + k;
+    while (mm) {
+      const uint32_t j = __ffs(mm) - 1;
+      mm &= mm - 1;
+      out[r++] = c.keys[slab * kSlotsPerSlab + j];
+    }
+  }
+}
+
+void launch_dump(const CacheDev& c, uint64_t set_begin, uint64_t set_end, uint64_t* out,
+                 unsigned long long* n_out, ScanState& scan, cudaStream_t st) {
+  const uint64_t n_slabs = (set_end - set_begin) * c.W;
+  if (n_slabs == 0) {
+    cudaMemsetAsync(n_out, 0, 8, st);
+    return;
+  }
+  const uint64_t tiles = (n_slabs + kScanTile - 1) / kScanTile;
+  scan_begin(scan, tiles, st);
+  k_dump_keys<<<unsigned(tiles), kScanBlock, 0, st>>>(c, set_begin * c.W, n_slabs, out, n_out,
+                                                      scan);
+  scan.tile_base += tiles;
+  check_launch("dump");
+}
+
+// ------------------------------------------------------------------ dedup --
+__global__ void k_dedup_insert(const uint64_t* __restrict__ keys, uint64_t n, DedupScratch ds,
+                               uint32_t epoch) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool claimed;
+  ds.slot_of[i] = dedup_insert(ds.table, ds.cap, keys, keys[i], uint32_t(i), epoch, &claimed);
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    k_dedup_compact(const uint64_t* __restrict__ keys, uint64_t n, DedupScratch ds,
+                    uint64_t* __restrict__ unique_out, ScanState scan) {
+  select_tile(
+      n, scan, [&](uint64_t i) { return uint32_t(ds.table[ds.slot_of[i]]) == uint32_t(i); },
+      [&](uint64_t i, uint64_t r) {
+        unique_out[r] = keys[i];
+        ds.rank_of_slot[ds.slot_of[i]] = uint32_t(r);
+      },
+      ds.n_unique);
+}
+
+__global__ void k_dedup_inverse(uint64_t n, DedupScratch ds, uint32_t* __restrict__ inverse) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  inverse[i] = ds.rank_of_slot[ds.slot_of[i]];
+}
+
+void launch_dedup(const uint64_t* keys, uint64_t n, uint64_t* unique_out, uint32_t* inverse,
+                  const DedupScratch& ds, uint32_t table_epoch, ScanState& scan,
+                  cudaStream_t st) {
+  if (n == 0) {
+    cudaMemsetAsync(ds.n_unique, 0, 8, st);
+    return;
+  }
+  const unsigned tb = 256;
+  k_dedup_insert<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(keys, n, ds, table_epoch);
+  const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+  scan_begin(scan, tiles, st);
+  k_dedup_compact<<<unsigned(tiles), kScanBlock, 0, st>>>(keys, n, ds, unique_out, scan);
+  scan.tile_base += tiles;
+  k_dedup_inverse<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(n, ds, inverse);
+  check_launch("dedup");
+}
+
+}  // namespace hpsb

@@ -1,0 +1,486 @@
+// capi.cpp -- extern "C" boundary (include/hps_b200.h). Every entry point
+// catches, maps the exception to a status code and stores the message in a
+// thread-local for hps_last_error().
+#include "hps_b200.h"
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "device_cache.hpp"
+#include "engine.hpp"
+#include "volatile_store.hpp"
+
+struct hps_cache {
+  std::unique_ptr<hpsb::DeviceCache> impl;
+};
+struct hps_vdb {
+  std::unique_ptr<hpsb::VolatileStore> impl;
+};
+struct hps_engine {
+  std::unique_ptr<hpsb::LookupEngine> impl;
+};
+
+namespace hpsb {
+void powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed, uint64_t draw_seed,
+                     size_t count, uint64_t* out);
+}
+
+namespace {
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HPS_OK;
+  } catch (const hpsb::Error& e) {
+    g_error = e.what();
+    return e.code();
+  } catch (const std::bad_alloc& e) {
+    g_error = e.what();
+    return HPS_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return HPS_INTERNAL;
+  } catch (...) {
+    g_error = "unknown error";
+    return HPS_INTERNAL;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw hpsb::invalid_argument(what);
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Process-wide per-device context for the stateless dedup entry point.
+struct DedupContext {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  hpsb::DeviceBuffer dbuf;
+  hpsb::PinnedBuffer hbuf;
+  hpsb::ScanState scan;
+  uint32_t epoch = 0;
+  uint64_t cap = 0;
+};
+std::mutex g_dedup_mu;
+std::map<int, std::unique_ptr<DedupContext>> g_dedup;
+
+DedupContext& dedup_ctx(int device) {
+  std::lock_guard<std::mutex> lk(g_dedup_mu);
+  auto& p = g_dedup[device];
+  if (!p) {
+    p = std::make_unique<DedupContext>();
+    hpsb::DeviceGuard g(device);
+    HPSB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  }
+  return *p;
+}
+}  // namespace
+
+extern "C" {
+
+const char* hps_last_error(void) { return g_error.c_str(); }
+
+uint64_t hps_xxh64_key(uint64_t key, uint64_t seed) { return hpsb::xxh64_key(key, seed); }
+
+uint64_t hps_xxh64(const void* input, size_t len, uint64_t seed) {
+  // general byte-string XXH64 (xxhash64.hpp:60-114)
+  using namespace hpsb;
+  const unsigned char* p = static_cast<const unsigned char*>(input);
+  const unsigned char* end = p + len;
+  auto rd64 = [](const unsigned char* q) {
+    uint64_t v;
+    std::memcpy(&v, q, 8);
+    return v;
+  };
+  auto rd32 = [](const unsigned char* q) {
+    uint32_t v;
+    std::memcpy(&v, q, 4);
+    return v;
+  };
+  auto round1 = [](uint64_t acc, uint64_t lane) { return rotl64(acc + lane * kP2, 31) * kP1; };
+  uint64_t h;
+  if (len >= 32) {
+    uint64_t v1 = seed + kP1 + kP2, v2 = seed + kP2, v3 = seed, v4 = seed - kP1;
+    const unsigned char* limit = end - 32;
+    do {
+      v1 = round1(v1, rd64(p));
+      v2 = round1(v2, rd64(p + 8));
+      v3 = round1(v3, rd64(p + 16));
+      v4 = round1(v4, rd64(p + 24));
+      p += 32;
+    } while (p <= limit);
+    h = rotl64(v1, 1) + rotl64(v2, 7) + rotl64(v3, 12) + rotl64(v4, 18);
+    for (uint64_t v : {v1, v2, v3, v4}) {
+      h ^= round1(0, v);
+      h = h * kP1 + kP4;
+    }
+  } else {
+    h = seed + kP5;
+  }
+  h += uint64_t(len);
+  while (p + 8 <= end) {
+    h ^= round1(0, rd64(p));
+    h = rotl64(h, 27) * kP1 + kP4;
+    p += 8;
+  }
+  if (p + 4 <= end) {
+    h ^= uint64_t(rd32(p)) * kP1;
+    h = rotl64(h, 23) * kP2 + kP3;
+    p += 4;
+  }
+  while (p < end) {
+    h ^= uint64_t(*p) * kP5;
+    h = rotl64(h, 11) * kP1;
+    ++p;
+  }
+  h ^= h >> 33;
+  h *= kP2;
+  h ^= h >> 29;
+  h *= kP3;
+  h ^= h >> 32;
+  return h;
+}
+
+uint64_t hps_slabset_of(uint64_t key, uint64_t slabset_count) {
+  return hpsb::xxh64_key(key, hpsb::kSlabsetSeed) % slabset_count;
+}
+uint32_t hps_first_slab_of(uint64_t key, uint32_t slabs_per_set) {
+  return uint32_t(hpsb::xxh64_key(key, hpsb::kSlabSeed) % slabs_per_set);
+}
+uint32_t hps_partition_of(uint64_t key, uint32_t partition_count) {
+  return hpsb::partition_of(key, partition_count);
+}
+
+int hps_dedup_keys(int device, const uint64_t* keys, size_t n, uint64_t* unique_out,
+                   uint32_t* inverse_out, size_t* n_unique, int mem, void* stream) {
+  return guarded([&] {
+    need(n_unique != nullptr, "n_unique must not be null");
+    need(n < (1ull << 32), "dedup batch too large");
+    DedupContext& c = dedup_ctx(device);
+    std::lock_guard<std::mutex> lk(c.mu);
+    hpsb::DeviceGuard g(device);
+    if (n == 0) {
+      *n_unique = 0;
+      return;
+    }
+    uint64_t tcap = 16;
+    while (tcap < 2 * n) tcap <<= 1;
+    const uint64_t tiles = (n + hpsb::kScanTile - 1) / hpsb::kScanTile;
+    auto a = [](uint64_t v) { return (v + 255) / 256 * 256; };
+    const bool host = mem == HPS_MEM_HOST;
+    const uint64_t bytes = a(tcap * 8) + a(n * 4) + a(tcap * 4) + a(8) + a(tiles * 8) + a(8) +
+                           (host ? a(n * 8) * 2 + a(n * 4) : 0);
+    const bool grow = bytes > c.dbuf.size() || tcap != c.cap;
+    char* p = static_cast<char*>(c.dbuf.ensure(bytes, c.stream));
+    auto take = [&](uint64_t b) {
+      char* r = p;
+      p += a(b);
+      return r;
+    };
+    hpsb::DedupScratch ds;
+    ds.cap = tcap;
+    ds.table = reinterpret_cast<uint64_t*>(take(tcap * 8));
+    ds.slot_of = reinterpret_cast<uint32_t*>(take(n * 4));
+    ds.rank_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
+    ds.n_unique = reinterpret_cast<unsigned long long*>(take(8));
+    c.scan.status = reinterpret_cast<uint64_t*>(take(tiles * 8));
+    c.scan.tile_ctr = reinterpret_cast<unsigned long long*>(take(8));
+    c.scan.capacity_tiles = tiles;
+    if (grow) {
+      // fresh carve: clear everything once and restart the epochs
+      HPSB_CUDA(cudaMemsetAsync(c.dbuf.get(), 0, c.dbuf.size(), c.stream));
+      c.scan.tile_base = 0;
+      c.scan.epoch = 0;
+      c.epoch = 0;
+      c.cap = tcap;
+    }
+    if (++c.epoch == 0) {
+      HPSB_CUDA(cudaMemsetAsync(ds.table, 0, tcap * 8, c.stream));
+      c.epoch = 1;
+    }
+    const uint64_t* d_keys = keys;
+    uint64_t* d_unique = unique_out;
+    uint32_t* d_inv = inverse_out;
+    if (host) {
+      uint64_t* k = reinterpret_cast<uint64_t*>(take(n * 8));
+      d_unique = reinterpret_cast<uint64_t*>(take(n * 8));
+      d_inv = reinterpret_cast<uint32_t*>(take(n * 4));
+      HPSB_CUDA(cudaMemcpyAsync(k, keys, n * 8, cudaMemcpyHostToDevice, c.stream));
+      d_keys = k;
+    } else if (stream) {
+      cudaEvent_t ev;
+      HPSB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      HPSB_CUDA(cudaEventRecord(ev, as_stream(stream)));
+      HPSB_CUDA(cudaStreamWaitEvent(c.stream, ev, 0));
+      cudaEventDestroy(ev);
+    }
+    hpsb::launch_dedup(d_keys, n, d_unique, d_inv, ds, c.epoch, c.scan, c.stream);
+    unsigned long long* h = static_cast<unsigned long long*>(c.hbuf.ensure(8));
+    HPSB_CUDA(cudaMemcpyAsync(h, ds.n_unique, 8, cudaMemcpyDeviceToHost, c.stream));
+    HPSB_CUDA(cudaStreamSynchronize(c.stream));
+    *n_unique = size_t(*h);
+    if (host) {
+      HPSB_CUDA(cudaMemcpyAsync(unique_out, d_unique, *n_unique * 8, cudaMemcpyDeviceToHost,
+                                c.stream));
+      HPSB_CUDA(cudaMemcpyAsync(inverse_out, d_inv, n * 4, cudaMemcpyDeviceToHost, c.stream));
+      HPSB_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  });
+}
+
+// ------------------------------------------------------------------ cache --
+int hps_cache_create(const hps_cache_config* config, int device, hps_cache** out) {
+  return guarded([&] {
+    need(config != nullptr && out != nullptr, "null argument");
+    hpsb::CacheConfig c;
+    c.slabset_count = config->slabset_count;
+    c.slabs_per_set = config->slabs_per_set;
+    c.dimension = config->dimension;
+    c.worker_pool_size = config->worker_pool_size;
+    c.tasks_per_worker = config->tasks_per_worker;
+    auto h = std::make_unique<hps_cache>();
+    h->impl = std::make_unique<hpsb::DeviceCache>(c, device);
+    *out = h.release();
+  });
+}
+
+int hps_cache_destroy(hps_cache* cache) {
+  return guarded([&] { delete cache; });
+}
+
+int hps_cache_get_info(hps_cache* cache, hps_cache_info* out) {
+  return guarded([&] {
+    need(cache && out, "null argument");
+    auto& c = *cache->impl;
+    out->dimension = c.dimension();
+    out->slabs_per_set = c.slabs_per_set();
+    out->slabset_count = c.slabset_count();
+    out->capacity = c.capacity();
+    out->occupied = c.occupied();
+    out->recency_clock = c.recency_clock();
+    out->device = c.device();
+    out->reserved = 0;
+  });
+}
+
+void* hps_cache_stream(hps_cache* cache) { return cache ? cache->impl->stream() : nullptr; }
+
+int hps_cache_query(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
+                    size_t out_len, uint32_t* miss_positions, uint64_t* miss_keys,
+                    size_t* n_miss, int mem, void* stream) {
+  return guarded([&] {
+    need(cache && n_miss, "null argument");
+    *n_miss = cache->impl->query(keys, n, out, out_len, miss_positions, miss_keys, mem,
+                                 as_stream(stream));
+  });
+}
+
+int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n, const float* vectors,
+                      size_t vectors_len, int mem, void* stream) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    cache->impl->replace(keys, n, vectors, vectors_len, mem, as_stream(stream));
+  });
+}
+
+int hps_cache_update(hps_cache* cache, const uint64_t* keys, size_t n, const float* vectors,
+                     size_t vectors_len, size_t* written, int mem, void* stream) {
+  return guarded([&] {
+    need(cache && written, "null argument");
+    *written = cache->impl->update(keys, n, vectors, vectors_len, mem, as_stream(stream));
+  });
+}
+
+int hps_cache_dump(hps_cache* cache, uint64_t set_begin, uint64_t set_end, uint64_t* out,
+                   size_t cap, size_t* n_out) {
+  return guarded([&] {
+    need(cache && n_out, "null argument");
+    *n_out = cache->impl->dump(set_begin, set_end, out, cap);
+  });
+}
+
+int hps_cache_check_invariants(hps_cache* cache) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    cache->impl->check_invariants();
+  });
+}
+
+int hps_cache_export_state(hps_cache* cache, uint64_t* keys, uint64_t* counters,
+                           uint32_t* masks, float* rows) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    cache->impl->export_state(keys, counters, masks, rows);
+  });
+}
+
+// -------------------------------------------------------------------- vdb --
+int hps_vdb_create(uint32_t lookup_threads, hps_vdb** out) {
+  return guarded([&] {
+    need(out != nullptr, "null argument");
+    auto h = std::make_unique<hps_vdb>();
+    h->impl = std::make_unique<hpsb::VolatileStore>(lookup_threads);
+    *out = h.release();
+  });
+}
+int hps_vdb_destroy(hps_vdb* vdb) {
+  return guarded([&] { delete vdb; });
+}
+int hps_vdb_register_table(hps_vdb* vdb, const char* name, uint32_t dimension,
+                           uint32_t partition_count, uint64_t overflow_margin) {
+  return guarded([&] {
+    need(vdb && name, "null argument");
+    vdb->impl->register_table(name, dimension, partition_count, overflow_margin);
+  });
+}
+int hps_vdb_has_table(hps_vdb* vdb, const char* name) {
+  return (vdb && name && vdb->impl->has_table(name)) ? 1 : 0;
+}
+int hps_vdb_insert(hps_vdb* vdb, const char* name, const uint64_t* keys, size_t n,
+                   const float* vectors, size_t vectors_len, uint64_t* evicted,
+                   size_t evicted_cap, size_t* n_evicted) {
+  return guarded([&] {
+    need(vdb && name, "null argument");
+    auto ev = vdb->impl->insert(name, keys, n, vectors, vectors_len);
+    if (evicted) std::copy(ev.begin(), ev.begin() + std::min(ev.size(), evicted_cap), evicted);
+    if (n_evicted) *n_evicted = ev.size();
+  });
+}
+int hps_vdb_insert_async(hps_vdb* vdb, const char* name, const uint64_t* keys, size_t n,
+                         const float* vectors, size_t vectors_len) {
+  return guarded([&] {
+    need(vdb && name, "null argument");
+    vdb->impl->insert_async(name, std::vector<uint64_t>(keys, keys + n),
+                            std::vector<float>(vectors, vectors + vectors_len));
+  });
+}
+int hps_vdb_lookup(hps_vdb* vdb, const char* name, const uint64_t* keys, size_t n,
+                   uint64_t* found_keys, float* found_vectors, size_t* n_found,
+                   uint64_t* missing_keys, size_t* n_missing) {
+  return guarded([&] {
+    need(vdb && name && n_found && n_missing, "null argument");
+    vdb->impl->lookup(name, keys, n, found_keys, found_vectors, nullptr, n_found, missing_keys,
+                      n_missing);
+  });
+}
+int hps_vdb_drain(hps_vdb* vdb) {
+  return guarded([&] { vdb->impl->drain(); });
+}
+int hps_vdb_table_size(hps_vdb* vdb, const char* name, uint64_t* out) {
+  return guarded([&] { *out = vdb->impl->table_size(name); });
+}
+int hps_vdb_partition_size(hps_vdb* vdb, const char* name, uint32_t partition, uint64_t* out) {
+  return guarded([&] { *out = vdb->impl->partition_size(name, partition); });
+}
+int hps_vdb_table_clock(hps_vdb* vdb, const char* name, uint64_t* out) {
+  return guarded([&] { *out = vdb->impl->table_clock(name); });
+}
+int hps_vdb_last_access(hps_vdb* vdb, const char* name, uint64_t key, uint64_t* out,
+                        int* found) {
+  return guarded([&] {
+    uint64_t v = 0;
+    *found = vdb->impl->last_access(name, key, &v) ? 1 : 0;
+    *out = v;
+  });
+}
+int hps_vdb_evict(hps_vdb* vdb, const char* name, uint32_t partition, uint64_t* evicted,
+                  size_t evicted_cap, size_t* n_evicted) {
+  return guarded([&] {
+    auto ev = vdb->impl->evict(name, partition);
+    if (evicted) std::copy(ev.begin(), ev.begin() + std::min(ev.size(), evicted_cap), evicted);
+    if (n_evicted) *n_evicted = ev.size();
+  });
+}
+
+int hps_tier_fetch(hps_vdb* vdb, const char* table, uint32_t dimension, hps_cold_fetch_fn cold,
+                   void* cold_ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
+                   float* found_vectors, size_t* n_found, uint64_t* missing_keys,
+                   size_t* n_missing, uint64_t* counters) {
+  return guarded([&] {
+    need(table && n_found && n_missing, "null argument");
+    std::vector<int32_t> row_of(n);
+    hpsb::TierCounters tc;
+    hpsb::tier_fetch_staged(vdb ? vdb->impl.get() : nullptr, table, dimension, cold, cold_ctx,
+                            keys, n, found_keys, found_vectors, row_of.data(), n_found,
+                            missing_keys, n_missing, &tc);
+    if (counters) {
+      counters[0] = tc.vdb_hits;
+      counters[1] = tc.cold_hits;
+      counters[2] = tc.missing;
+    }
+  });
+}
+
+// ----------------------------------------------------------------- engine --
+int hps_engine_create(const char* table, uint32_t dimension, hps_cache* cache, hps_vdb* vdb,
+                      hps_cold_fetch_fn cold, void* cold_ctx, const hps_engine_config* config,
+                      hps_engine** out) {
+  return guarded([&] {
+    need(table && cache && config && out, "null argument");
+    hpsb::EngineConfig c;
+    c.hit_rate_threshold = config->hit_rate_threshold;
+    if (config->default_vector && config->default_vector_len)
+      c.default_vector.assign(config->default_vector,
+                              config->default_vector + config->default_vector_len);
+    c.workspace_pool_size = config->workspace_pool_size;
+    c.async_worker_count = config->async_worker_count;
+    c.volatile_tier_enabled = config->volatile_tier_enabled != 0;
+    c.max_batch = config->max_batch ? config->max_batch : 131072;
+    auto h = std::make_unique<hps_engine>();
+    h->impl = std::make_unique<hpsb::LookupEngine>(table, dimension, cache->impl.get(),
+                                                   vdb ? vdb->impl.get() : nullptr, cold,
+                                                   cold_ctx, std::move(c));
+    *out = h.release();
+  });
+}
+int hps_engine_destroy(hps_engine* engine) {
+  return guarded([&] { delete engine; });
+}
+int hps_engine_lookup(hps_engine* engine, const uint64_t* keys, size_t n, float* out,
+                      size_t out_len, uint8_t* miss_flags, hps_lookup_outcome* outcome, int mem,
+                      void* stream) {
+  return guarded([&] {
+    need(engine != nullptr, "null argument");
+    hpsb::LookupOutcome o;
+    engine->impl->lookup(keys, n, out, out_len, miss_flags, &o, mem, as_stream(stream));
+    if (outcome) {
+      outcome->sync_branch = o.sync_branch ? 1 : 0;
+      outcome->unique_hit_rate = o.unique_hit_rate;
+      outcome->unique_count = o.unique_count;
+      outcome->defaults_returned = o.defaults_returned;
+    }
+  });
+}
+int hps_engine_drain_async(hps_engine* engine) {
+  return guarded([&] { engine->impl->drain_async(); });
+}
+int hps_engine_get_stats(hps_engine* engine, hps_engine_stats* out) {
+  return guarded([&] {
+    const auto s = engine->impl->stats();
+    *out = hps_engine_stats{s.queries,        s.queried_keys,  s.unique_keys,
+                            s.cache_hits,     s.cache_misses,  s.sync_batches,
+                            s.async_batches,  s.defaults_returned, s.vdb_hits,
+                            s.pdb_hits,       s.tier_missing,  s.async_faults};
+  });
+}
+int hps_engine_pool_info(hps_engine* engine, uint64_t* size, uint64_t* outstanding,
+                         uint64_t* peak_outstanding) {
+  return guarded([&] {
+    auto& p = engine->impl->pool();
+    if (size) *size = p.size();
+    if (outstanding) *outstanding = p.outstanding();
+    if (peak_outstanding) *peak_outstanding = p.peak_outstanding();
+  });
+}
+
+int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,
+                        uint64_t draw_seed, size_t count, uint64_t* out) {
+  return guarded([&] { hpsb::powerlaw_sample(alpha, keyspace, permute_seed, draw_seed, count, out); });
+}
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// device_cache.cpp -- see device_cache.hpp.
+#include "device_cache.hpp"
+
+#include <algorithm>
+#include <unordered_set>
+#include <vector>
+
+namespace hpsb {
+
+namespace {
+inline uint64_t align256(uint64_t v) { return (v + 255) / 256 * 256; }
+
+// Bump allocator over one scratch block.
+struct Carver {
+  char* p;
+  template <class T>
+  T* take(uint64_t count) {
+    T* r = reinterpret_cast<T*>(p);
+    p += align256(count * sizeof(T));
+    return r;
+  }
+};
+
+int keys_per_warp_for(uint32_t tasks_per_worker) {
+  // SlabCacheConfig::tasks_per_worker (slab_cache.hpp:33) becomes the number
+  // of keys one warp keeps in flight (paper tasksPerWarp).
+  if (tasks_per_worker >= 8) return 8;
+  if (tasks_per_worker >= 4) return 4;
+  if (tasks_per_worker >= 2) return 2;
+  return 1;
+}
+}  // namespace
+
+DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device_(device) {
+  // same validation, same messages as slab_cache.cpp:18-29
+  if (cfg.slabset_count == 0) throw invalid_argument("slabset_count must be positive");
+  if (cfg.slabs_per_set == 0) throw invalid_argument("slabs_per_set must be positive");
+  if (cfg.dimension == 0) throw invalid_argument("cache dimension must be positive");
+  if (cfg.worker_pool_size == 0) throw invalid_argument("worker_pool_size must be positive");
+  keys_per_warp_ = keys_per_warp_for(std::max<uint32_t>(1, cfg.tasks_per_worker));
+  DeviceGuard g(device_);
+  HPSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  HPSB_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
+  HPSB_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
+  const uint64_t slabs = cfg.slabset_count * cfg.slabs_per_set;
+  const uint64_t slots = slabs * 32ull;
+  dev_.S = cfg.slabset_count;
+  dev_.W = cfg.slabs_per_set;
+  dev_.d = cfg.dimension;
+  HPSB_CUDA(cudaMalloc(&dev_.keys, slots * 8));
+  HPSB_CUDA(cudaMalloc(&dev_.counters, slots * 8));
+  HPSB_CUDA(cudaMalloc(&dev_.masks, slabs * 4));
+  HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
+  HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
+  HPSB_CUDA(cudaMemsetAsync(dev_.keys, 0, slots * 8, stream_));
+  HPSB_CUDA(cudaMemsetAsync(dev_.counters, 0, slots * 8, stream_));
+  HPSB_CUDA(cudaMemsetAsync(dev_.masks, 0, slabs * 4, stream_));
+  HPSB_CUDA(cudaMemsetAsync(dev_.rows, 0, slots * uint64_t(cfg.dimension) * 4, stream_));
+  HPSB_CUDA(cudaMemsetAsync(dev_.occupied, 0, 8, stream_));
+  HPSB_CUDA(cudaMalloc(&d_small_, 64));
+  HPSB_CUDA(cudaMemsetAsync(d_small_, 0, 64, stream_));
+  HPSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_small_), 64, cudaHostAllocPortable));
+  HPSB_CUDA(cudaMalloc(&scan_.tile_ctr, 8));
+  HPSB_CUDA(cudaMemsetAsync(scan_.tile_ctr, 0, 8, stream_));
+  ensure_scan_tiles(1024);
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+DeviceCache::~DeviceCache() {
+  DeviceGuard g(device_);
+  cudaStreamSynchronize(stream_);
+  cudaFree(dev_.keys);
+  cudaFree(dev_.counters);
+  cudaFree(dev_.masks);
+  cudaFree(dev_.rows);
+  cudaFree(dev_.occupied);
+  cudaFree(d_small_);
+  cudaFreeHost(h_small_);
+  cudaFree(scan_.tile_ctr);
+  cudaFree(scan_.status);
+  cudaEventDestroy(ev_in_);
+  cudaEventDestroy(ev_out_);
+  cudaStreamDestroy(stream_);
+}
+
+void DeviceCache::ensure_scan_tiles(uint64_t tiles) {
+  if (tiles <= scan_.capacity_tiles) return;
+  uint64_t cap = std::max<uint64_t>(1024, scan_.capacity_tiles);
+  while (cap < tiles) cap <<= 1;
+  if (scan_.status) {
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+    HPSB_CUDA(cudaFree(scan_.status));
+  }
+  HPSB_CUDA(cudaMalloc(&scan_.status, cap * 8));
+  HPSB_CUDA(cudaMemsetAsync(scan_.status, 0, cap * 8, stream_));
+  scan_.capacity_tiles = cap;
+  scan_.epoch = 0;
+}
+
+void DeviceCache::join_from(cudaStream_t user) {
+  if (user == nullptr || user == stream_) return;
+  HPSB_CUDA(cudaEventRecord(ev_in_, user));
+  HPSB_CUDA(cudaStreamWaitEvent(stream_, ev_in_, 0));
+}
+
+void DeviceCache::join_to(cudaStream_t user) {
+  if (user == nullptr || user == stream_) return;
+  HPSB_CUDA(cudaEventRecord(ev_out_, stream_));
+  HPSB_CUDA(cudaStreamWaitEvent(user, ev_out_, 0));
+}
+
+uint64_t DeviceCache::occupied() {
+  std::lock_guard<std::mutex> lk(mu_);
+  DeviceGuard g(device_);
+  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 7, dev_.occupied, 8, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  return h_small_[7];
+}
+
+size_t DeviceCache::query(const uint64_t* keys, size_t n, float* out, size_t out_len,
+                          uint32_t* miss_pos, uint64_t* miss_keys, int mem, cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  // one tick per call, before anything else (slab_cache.cpp:73-74)
+  const uint64_t stamp = bump_clock();
+  if (out_len != n * uint64_t(cfg_.dimension))
+    throw invalid_argument("query output buffer has wrong size");
+  if (n == 0) return 0;
+  DeviceGuard g(device_);
+  const uint64_t d = cfg_.dimension;
+  const bool host = mem == kHostMem;
+  ensure_scan_tiles((n + kScanTile - 1) / kScanTile);
+  const uint64_t bytes = align256(n) + (host ? align256(n * 8) * 2 + align256(n * d * 4) +
+                                                   align256(n * 4)
+                                             : 0);
+  Carver cv{static_cast<char*>(scratch(bytes))};
+  uint8_t* d_hit = cv.take<uint8_t>(n);
+  const uint64_t* d_keys = keys;
+  float* d_out = out;
+  uint32_t* d_mpos = miss_pos;
+  uint64_t* d_mkeys = miss_keys;
+  if (host) {
+    uint64_t* k = cv.take<uint64_t>(n);
+    d_out = cv.take<float>(n * d);
+    d_mpos = cv.take<uint32_t>(n);
+    d_mkeys = cv.take<uint64_t>(n);
+    HPSB_CUDA(cudaMemcpyAsync(k, keys, n * 8, cudaMemcpyHostToDevice, stream_));
+    // miss rows must come back untouched: start from the caller's bytes
+    HPSB_CUDA(cudaMemcpyAsync(d_out, out, n * d * 4, cudaMemcpyHostToDevice, stream_));
+    d_keys = k;
+  } else {
+    join_from(user);
+  }
+  launch_cache_query(dev_, d_keys, n, d_out, d_hit, stamp, keys_per_warp_, stream_);
+  launch_select_misses(d_keys, d_hit, n, d_mpos, d_mkeys, d_small_, scan_, stream_);
+  HPSB_CUDA(cudaMemcpyAsync(h_small_, d_small_, 8, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  const size_t n_miss = h_small_[0];
+  if (host) {
+    HPSB_CUDA(cudaMemcpyAsync(out, d_out, n * d * 4, cudaMemcpyDeviceToHost, stream_));
+    if (n_miss) {
+      HPSB_CUDA(cudaMemcpyAsync(miss_pos, d_mpos, n_miss * 4, cudaMemcpyDeviceToHost, stream_));
+      HPSB_CUDA(
+          cudaMemcpyAsync(miss_keys, d_mkeys, n_miss * 8, cudaMemcpyDeviceToHost, stream_));
+    }
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+  } else {
+    join_to(user);
+  }
+  return n_miss;
+}
+
+void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
+                          size_t vectors_len, int mem, cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (vectors_len != n * uint64_t(cfg_.dimension))
+    throw invalid_argument("replace vector buffer has wrong size");
+  const bool host = mem == kHostMem;
+  if (host) {
+    std::unordered_set<uint64_t> distinct(keys, keys + n);
+    if (distinct.size() != n) throw invalid_argument("replace batch contains duplicate keys");
+  }
+  if (n == 0) return;
+  DeviceGuard g(device_);
+  const uint64_t d = cfg_.dimension;
+  const uint64_t stamp = clock_.load(std::memory_order_relaxed);  // no increment
+  const uint64_t rs_bytes = replace_scratch_bytes(n);
+  const uint64_t bytes = align256(rs_bytes) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
+  Carver cv{static_cast<char*>(scratch(bytes))};
+  ReplaceScratch rs = replace_scratch_carve(cv.take<char>(rs_bytes), n);
+  const uint64_t* d_keys = keys;
+  const float* d_rows = vectors;
+  if (host) {
+    uint64_t* k = cv.take<uint64_t>(n);
+    float* r = cv.take<float>(n * d);
+    HPSB_CUDA(cudaMemcpyAsync(k, keys, n * 8, cudaMemcpyHostToDevice, stream_));
+    HPSB_CUDA(cudaMemcpyAsync(r, vectors, n * d * 4, cudaMemcpyHostToDevice, stream_));
+    d_keys = k;
+    d_rows = r;
+  } else {
+    join_from(user);
+  }
+  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/!host, rs, stream_);
+  if (host) {
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+    return;
+  }
+  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 1, rs.cursor, 8, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  const uint32_t dup = reinterpret_cast<const uint32_t*>(h_small_ + 1)[1];
+  if (dup) throw invalid_argument("replace batch contains duplicate keys");
+  join_to(user);
+}
+
+void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const float* d_rows) {
+  if (n == 0) return;
+  const uint64_t stamp = clock_.load(std::memory_order_relaxed);
+  const uint64_t rs_bytes = replace_scratch_bytes(n);
+  ReplaceScratch rs = replace_scratch_carve(scratch2_.ensure(rs_bytes, stream_), n);
+  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/false, rs, stream_);
+}
+
+size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
+                           size_t vectors_len, int mem, cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (vectors_len != n * uint64_t(cfg_.dimension))
+    throw invalid_argument("update vector buffer has wrong size");
+  if (n == 0) return 0;
+  DeviceGuard g(device_);
+  const uint64_t d = cfg_.dimension;
+  const bool host = mem == kHostMem;
+  const uint64_t us_bytes = update_scratch_bytes(n);
+  const uint64_t bytes = align256(us_bytes) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
+  Carver cv{static_cast<char*>(scratch(bytes))};
+  UpdateScratch us = update_scratch_carve(cv.take<char>(us_bytes), n);
+  const uint64_t* d_keys = keys;
+  const float* d_rows = vectors;
+  if (host) {
+    uint64_t* k = cv.take<uint64_t>(n);
+    float* r = cv.take<float>(n * d);
+    HPSB_CUDA(cudaMemcpyAsync(k, keys, n * 8, cudaMemcpyHostToDevice, stream_));
+    HPSB_CUDA(cudaMemcpyAsync(r, vectors, n * d * 4, cudaMemcpyHostToDevice, stream_));
+    d_keys = k;
+    d_rows = r;
+  } else {
+    join_from(user);
+  }
+  launch_update(dev_, d_keys, n, d_rows, keys_per_warp_, us, stream_);
+  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 2, us.written, 8, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  if (!host) join_to(user);
+  return h_small_[2];
+}
+
+size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, size_t cap) {
+  std::lock_guard<std::mutex> lk(mu_);
+  set_end = std::min<uint64_t>(set_end, cfg_.slabset_count);
+  if (set_begin >= set_end) return 0;
+  DeviceGuard g(device_);
+  const uint64_t slots = (set_end - set_begin) * cfg_.slabs_per_set * 32ull;
+  ensure_scan_tiles(((set_end - set_begin) * cfg_.slabs_per_set + kScanTile - 1) / kScanTile);
+  uint64_t* d_out = static_cast<uint64_t*>(scratch(slots * 8));
+  launch_dump(dev_, set_begin, set_end, d_out, d_small_ + 3, scan_, stream_);
+  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 3, d_small_ + 3, 8, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  const size_t n = h_small_[3];
+  const size_t take = std::min(n, cap);
+  if (take) {
+    HPSB_CUDA(cudaMemcpyAsync(out, d_out, take * 8, cudaMemcpyDeviceToHost, stream_));
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+  }
+  return n;
+}
+
+void DeviceCache::export_state(uint64_t* keys, uint64_t* counters, uint32_t* masks,
+                               float* rows) {
+  std::lock_guard<std::mutex> lk(mu_);
+  DeviceGuard g(device_);
+  const uint64_t slabs = cfg_.slabset_count * cfg_.slabs_per_set;
+  const uint64_t slots = slabs * 32ull;
+  if (keys) HPSB_CUDA(cudaMemcpyAsync(keys, dev_.keys, slots * 8, cudaMemcpyDeviceToHost, stream_));
+  if (counters)
+    HPSB_CUDA(
+        cudaMemcpyAsync(counters, dev_.counters, slots * 8, cudaMemcpyDeviceToHost, stream_));
+  if (masks) HPSB_CUDA(cudaMemcpyAsync(masks, dev_.masks, slabs * 4, cudaMemcpyDeviceToHost, stream_));
+  if (rows)
+    HPSB_CUDA(cudaMemcpyAsync(rows, dev_.rows, slots * uint64_t(cfg_.dimension) * 4,
+                              cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void DeviceCache::check_invariants() {
+  const uint64_t S = cfg_.slabset_count, W = cfg_.slabs_per_set;
+  const uint64_t slots = S * W * 32;
+  std::vector<uint64_t> keys(slots), ctr(slots);
+  std::vector<uint32_t> masks(S * W);
+  export_state(keys.data(), ctr.data(), masks.data(), nullptr);
+  const uint64_t clock_now = recency_clock();
+  const uint64_t occ = occupied();
+  std::unordered_set<uint64_t> seen;
+  seen.reserve(occ);
+  uint64_t populated = 0;
+  for (uint64_t set = 0; set < S; ++set) {
+    for (uint64_t slab = 0; slab < W; ++slab) {
+      const uint32_t m = masks[set * W + slab];
+      // masks only grow contiguously from bit 0 (no erase; eviction in place)
+      if ((m & (m + 1)) != 0) throw logic_error("slab cache occupancy mask is not contiguous");
+      for (uint32_t j = 0; j < 32; ++j) {
+        if (!((m >> j) & 1u)) continue;
+        ++populated;
+        const uint64_t slot = (set * W + slab) * 32 + j;
+        const uint64_t key = keys[slot];
+        // same checks and messages as slab_cache.cpp:425-436
+        if (hpsb::xxh64_key(key, kSlabsetSeed) % S != set)
+          throw logic_error("slab cache key stored outside its slabset");
+        if (!seen.insert(key).second) throw logic_error("slab cache holds a key in two slots");
+        if (ctr[slot] > clock_now) throw logic_error("slab cache slot counter exceeds the clock");
+      }
+    }
+  }
+  if (populated != occ) throw logic_error("slab cache occupancy counter is out of sync");
+}
+
+}  // namespace hpsb

@@ -1,0 +1,99 @@
+// device_cache.hpp -- one HBM-resident slab-cache replica and its
+// operations; the object behind the hps_cache_* C ABI.
+//
+// Mirrors hps::SlabCache (slab_cache.hpp:41-179): same configuration
+// checks, same recency clock rules (query bumps once per call before any
+// check, replace stamps with the current value, update never touches it),
+// same results. Concurrency model: one CUDA stream per cache; every
+// operation holds `mu_` while it enqueues, so operations are linearised in
+// stream order (the reference's per-slabset gates, slab_cache.cpp:214, are
+// replaced by stream ordering -- no torn reads).
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "kernels.hpp"
+#include "runtime.hpp"
+
+namespace hpsb {
+
+struct CacheConfig {
+  uint64_t slabset_count = 1;
+  uint32_t slabs_per_set = 2;
+  uint32_t dimension = 0;
+  uint32_t worker_pool_size = 1;
+  uint32_t tasks_per_worker = 8;
+};
+
+enum MemKind : int { kHostMem = 0, kDeviceMem = 1 };
+
+class DeviceCache {
+ public:
+  DeviceCache(const CacheConfig& cfg, int device);
+  ~DeviceCache();
+  DeviceCache(const DeviceCache&) = delete;
+  DeviceCache& operator=(const DeviceCache&) = delete;
+
+  // slab_cache.cpp:69-91. Returns the miss count; misses ascending.
+  size_t query(const uint64_t* keys, size_t n, float* out, size_t out_len, uint32_t* miss_pos,
+               uint64_t* miss_keys, int mem, cudaStream_t user);
+  // slab_cache.cpp:93-107
+  void replace(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
+               int mem, cudaStream_t user);
+  // slab_cache.cpp:109-125
+  size_t update(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
+                int mem, cudaStream_t user);
+  // DumpCursor::next over a slabset range (host output)
+  size_t dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, size_t cap);
+  // slab_cache.cpp:407-442
+  void check_invariants();
+  void export_state(uint64_t* keys, uint64_t* counters, uint32_t* masks, float* rows);
+
+  uint32_t dimension() const { return cfg_.dimension; }
+  uint64_t slabset_count() const { return cfg_.slabset_count; }
+  uint32_t slabs_per_set() const { return cfg_.slabs_per_set; }
+  uint64_t capacity() const { return cfg_.slabset_count * cfg_.slabs_per_set * 32ull; }
+  uint64_t occupied();
+  uint64_t recency_clock() const { return clock_.load(std::memory_order_relaxed); }
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+  const CacheDev& dev() const { return dev_; }
+  int keys_per_warp() const { return keys_per_warp_; }
+
+  // ---- engine-facing primitives (caller holds mutex()) ----
+  std::mutex& mutex() { return mu_; }
+  uint64_t bump_clock() { return clock_.fetch_add(1, std::memory_order_relaxed) + 1; }
+  // Device keys / rows, distinct keys guaranteed by the caller; stamp = the
+  // current clock. Enqueued on stream(); scratch is the cache's own.
+  void replace_device_locked(const uint64_t* d_keys, size_t n, const float* d_rows);
+
+  // Makes stream() wait for work already queued on `user` (no-op if null
+  // or identical), and the reverse.
+  void join_from(cudaStream_t user);
+  void join_to(cudaStream_t user);
+
+ private:
+  void* scratch(size_t bytes) { return scratch_.ensure(bytes, stream_); }
+  void* pinned(size_t bytes) { return pinned_.ensure(bytes); }
+  void ensure_scan_tiles(uint64_t tiles);
+
+  CacheConfig cfg_;
+  int device_;
+  int keys_per_warp_;
+  CacheDev dev_{};
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
+  std::mutex mu_;
+  std::atomic<uint64_t> clock_{0};
+  ScanState scan_;
+  DeviceBuffer scratch_;
+  DeviceBuffer scratch2_;
+  PinnedBuffer pinned_;
+  unsigned long long* d_small_ = nullptr;  // small device counters
+  unsigned long long* h_small_ = nullptr;  // pinned mirror
+};
+
+}  // namespace hpsb

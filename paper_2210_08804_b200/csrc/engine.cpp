@@ -1,0 +1,456 @@
+// engine.cpp -- see engine.hpp. Reference: /root/reference/proj/core/src/
+// lookup_engine.cpp (tier_fetch :50-89, ctor checks :91-117, lookup
+// :130-241, async_loop :243-284, drain_async :286-289).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace hpsb {
+
+namespace {
+inline uint64_t a256(uint64_t v) { return (v + 255) / 256 * 256; }
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+// ------------------------------------------------------------- tier fetch --
+void tier_fetch_staged(VolatileStore* vdb, const std::string& table, uint32_t dim,
+                       ColdFetchFn cold, void* cold_ctx, const uint64_t* keys, size_t n,
+                       uint64_t* found_keys, float* rows, int32_t* row_of, size_t* n_found,
+                       uint64_t* missing_keys, size_t* n_missing, TierCounters* counters) {
+  *n_found = 0;
+  *n_missing = 0;
+  if (n == 0) return;
+  const bool use_vdb = vdb != nullptr && vdb->has_table(table);
+  size_t nf = 0, nm = 0;
+  std::vector<uint64_t> remaining;
+  if (use_vdb) {
+    remaining.resize(n);
+    vdb->lookup(table, keys, n, found_keys, rows, row_of, &nf, remaining.data(), &nm);
+    remaining.resize(nm);
+    if (counters) counters->vdb_hits += nf;
+  } else {
+    remaining.assign(keys, keys + n);
+    nm = n;
+    for (size_t i = 0; i < n; ++i) row_of[i] = -1;
+  }
+  if (nm == 0) {
+    *n_found = nf;
+    return;
+  }
+  if (cold == nullptr) {
+    // no cold tier wired: everything left is absent
+    std::copy(remaining.begin(), remaining.end(), missing_keys);
+    if (counters) counters->missing += nm;
+    *n_found = nf;
+    *n_missing = nm;
+    return;
+  }
+  std::vector<uint64_t> cf_keys(nm), cm_keys(nm);
+  std::vector<float> cf_rows(nm * uint64_t(dim));
+  size_t cf = 0, cm = 0;
+  const int rc = cold(cold_ctx, remaining.data(), nm, cf_keys.data(), cf_rows.data(), &cf,
+                      cm_keys.data(), &cm);
+  if (rc != 0) throw tier_fault("cold tier fetch failed");
+  if (counters) {
+    counters->cold_hits += cf;
+    counters->missing += cm;
+  }
+  if (use_vdb && cf) {
+    // promote cold reads (lookup_engine.cpp:76-81)
+    vdb->insert_async(table, std::vector<uint64_t>(cf_keys.begin(), cf_keys.begin() + cf),
+                      std::vector<float>(cf_rows.begin(), cf_rows.begin() + cf * dim));
+  }
+  std::copy(cf_keys.begin(), cf_keys.begin() + cf, found_keys + nf);
+  std::copy(cf_rows.begin(), cf_rows.begin() + cf * dim, rows + nf * dim);
+  // cold hits are a subsequence of `remaining` (input order): two pointers
+  size_t j = 0;
+  for (size_t i = 0; i < n && j < cf; ++i) {
+    if (row_of[i] >= 0) continue;
+    if (keys[i] == cf_keys[j]) {
+      row_of[i] = int32_t(nf + j);
+      ++j;
+    }
+  }
+  std::copy(cm_keys.begin(), cm_keys.begin() + cm, missing_keys);
+  *n_found = nf + cf;
+  *n_missing = cm;
+}
+
+// -------------------------------------------------------------- workspace --
+Workspace::~Workspace() {
+  if (done) {
+    cudaEventSynchronize(done);
+    cudaEventDestroy(done);
+  }
+}
+
+void Workspace::wait_idle() {
+  if (pending) {
+    HPSB_CUDA(cudaEventSynchronize(done));
+    pending = false;
+  }
+}
+
+void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
+  if (done == nullptr) HPSB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  if (n <= capacity && d == dim && dbuf.get() != nullptr) return;
+  uint64_t cap = 1024;
+  while (cap < n) cap <<= 1;
+  uint64_t tcap = 16;
+  while (tcap < 2 * cap) tcap <<= 1;
+  const uint64_t tiles = (cap + kScanTile - 1) / kScanTile;
+  const uint64_t dev_bytes = a256(cap * 8) * 3 + a256(cap * uint64_t(d) * 4) * 2 + a256(cap) +
+                             a256(cap * 4) * 2 + a256(tcap * 8) + a256(tcap * 4) + a256(16) +
+                             a256(tiles * 8) + a256(8);
+  HPSB_CUDA(cudaStreamSynchronize(st));
+  char* p = static_cast<char*>(dbuf.ensure(dev_bytes, st));
+  auto take = [&](uint64_t bytes) {
+    char* r = p;
+    p += a256(bytes);
+    return r;
+  };
+  d_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  d_out = reinterpret_cast<float*>(take(cap * uint64_t(d) * 4));
+  d_flags = reinterpret_cast<uint8_t*>(take(cap));
+  d_row_of = reinterpret_cast<int32_t*>(take(cap * 4));
+  d_staged = reinterpret_cast<float*>(take(cap * uint64_t(d) * 4));
+  d_found_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  ls.cap = tcap;
+  ls.miss_table = reinterpret_cast<uint64_t*>(take(tcap * 8));
+  ls.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
+  ls.rank_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
+  ls.counts = reinterpret_cast<unsigned long long*>(take(16));
+  ls.miss_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  scan.status = reinterpret_cast<uint64_t*>(take(tiles * 8));
+  scan.tile_ctr = reinterpret_cast<unsigned long long*>(take(8));
+  scan.capacity_tiles = tiles;
+  scan.tile_base = 0;
+  scan.epoch = 0;
+  HPSB_CUDA(cudaMemsetAsync(ls.miss_table, 0, tcap * 8, st));
+  HPSB_CUDA(cudaMemsetAsync(ls.counts, 0, 16, st));
+  HPSB_CUDA(cudaMemsetAsync(scan.status, 0, tiles * 8, st));
+  HPSB_CUDA(cudaMemsetAsync(scan.tile_ctr, 0, 8, st));
+  table_epoch = 0;
+  prev_counts[0] = prev_counts[1] = 0;
+
+  const uint64_t host_bytes = a256(cap * 8) * 4 + a256(16) + a256(cap * 4) +
+                              a256(cap * uint64_t(d) * 4) * 2 + a256(cap);
+  char* h = static_cast<char*>(hbuf.ensure(host_bytes));
+  auto htake = [&](uint64_t bytes) {
+    char* r = h;
+    h += a256(bytes);
+    return r;
+  };
+  h_keys = reinterpret_cast<uint64_t*>(htake(cap * 8));
+  h_counts = reinterpret_cast<unsigned long long*>(htake(16));
+  h_miss_keys = reinterpret_cast<uint64_t*>(htake(cap * 8));
+  h_row_of = reinterpret_cast<int32_t*>(htake(cap * 4));
+  h_staged = reinterpret_cast<float*>(htake(cap * uint64_t(d) * 4));
+  h_found_keys = reinterpret_cast<uint64_t*>(htake(cap * 8));
+  h_missing = reinterpret_cast<uint64_t*>(htake(cap * 8));
+  h_flags = reinterpret_cast<uint8_t*>(htake(cap));
+  h_out = reinterpret_cast<float*>(htake(cap * uint64_t(d) * 4));
+  HPSB_CUDA(cudaStreamSynchronize(st));
+  capacity = cap;
+  dim = d;
+}
+
+WorkspacePool::WorkspacePool(size_t size, int device) {
+  if (size == 0) throw invalid_argument("workspace pool size must be positive");
+  for (size_t i = 0; i < size; ++i) {
+    slots_.push_back(std::make_unique<Workspace>());
+    slots_.back()->device = device;
+    free_.push_back(slots_.back().get());
+  }
+}
+
+Workspace* WorkspacePool::acquire() {
+  std::unique_lock<std::mutex> lk(mu_);
+  cv_.wait(lk, [&] { return !free_.empty(); });
+  Workspace* ws = free_.back();
+  free_.pop_back();
+  ++outstanding_;
+  peak_ = std::max(peak_, outstanding_);
+  return ws;
+}
+
+void WorkspacePool::release(Workspace* ws) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    free_.push_back(ws);
+    --outstanding_;
+  }
+  cv_.notify_one();
+}
+
+size_t WorkspacePool::outstanding() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return outstanding_;
+}
+size_t WorkspacePool::peak_outstanding() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return peak_;
+}
+
+// ----------------------------------------------------------------- engine --
+LookupEngine::LookupEngine(const std::string& table, uint32_t dim, DeviceCache* cache,
+                           VolatileStore* vdb, ColdFetchFn cold, void* cold_ctx,
+                           EngineConfig cfg)
+    : table_(table),
+      dim_(dim),
+      cache_(cache),
+      vdb_(vdb),
+      cold_(cold),
+      cold_ctx_(cold_ctx),
+      cfg_(std::move(cfg)),
+      pool_(cfg_.workspace_pool_size, cache ? cache->device() : 0) {
+  if (table.empty()) throw invalid_argument("table name must not be empty");
+  if (table.size() > 255) throw invalid_argument("table name exceeds 255 bytes: " + table);
+  if (dim == 0) throw invalid_argument("table dimension must be positive: " + table);
+  if (cache == nullptr) throw invalid_argument("engine needs a cache");
+  if (cache->dimension() != dim) throw invalid_argument("cache dimension does not match table");
+  if (cfg_.hit_rate_threshold < 0.0 || cfg_.hit_rate_threshold > 1.0)
+    throw invalid_argument("hit_rate_threshold must be within [0, 1]");
+  if (cfg_.async_worker_count == 0) throw invalid_argument("async_worker_count must be positive");
+  std::vector<float> def = cfg_.default_vector;
+  def.resize(dim, 0.0f);  // padded with zeros / cut to the dimension
+  DeviceGuard g(cache->device());
+  HPSB_CUDA(cudaMalloc(&d_default_, dim * 4));
+  HPSB_CUDA(cudaMemcpy(d_default_, def.data(), dim * 4, cudaMemcpyHostToDevice));
+  for (uint32_t i = 0; i < cfg_.async_worker_count; ++i)
+    workers_.emplace_back([this] { async_loop(); });
+}
+
+LookupEngine::~LookupEngine() {
+  {
+    std::lock_guard<std::mutex> lk(q_mu_);
+    stopping_ = true;
+  }
+  q_cv_.notify_all();
+  for (auto& w : workers_) w.join();
+  DeviceGuard g(cache_->device());
+  cudaFree(d_default_);
+}
+
+size_t LookupEngine::fetch_and_upload(Workspace& ws, const uint64_t* miss_keys, size_t n_miss,
+                                      TierCounters* counters, size_t* n_found) {
+  size_t nf = 0, nm = 0;
+  tier_fetch_staged(cfg_.volatile_tier_enabled ? vdb_ : nullptr, table_, dim_, cold_, cold_ctx_,
+                    miss_keys, n_miss, ws.h_found_keys, ws.h_staged, ws.h_row_of, &nf,
+                    ws.h_missing, &nm, counters);
+  *n_found = nf;
+  return nm;
+}
+
+void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out_len,
+                          uint8_t* flags, LookupOutcome* outcome, int mem, cudaStream_t user) {
+  if (out_len != n * uint64_t(dim_)) throw invalid_argument("lookup output buffer has wrong size");
+  const bool host = mem == kHostMem;
+  const uint32_t d = dim_;
+  Workspace* ws = pool_.acquire();
+  bool handed_off = false;
+  struct LeaseGuard {
+    WorkspacePool& pool;
+    Workspace* ws;
+    bool* handed;
+    ~LeaseGuard() {
+      if (!*handed) pool.release(ws);
+    }
+  } guard{pool_, ws, &handed_off};
+  ws->wait_idle();
+  DeviceGuard g(cache_->device());
+  cudaStream_t st = cache_->stream();
+  ws->ensure(std::max<size_t>(n, 1), d, st);
+
+  uint64_t uh = 0, um = 0;
+  const uint64_t* d_keys = keys;
+  float* d_out = out;
+  uint8_t* d_flags = flags;
+  {
+    std::lock_guard<std::mutex> lk(cache_->mutex());
+    const uint64_t stamp = cache_->bump_clock();  // query ticks even when empty
+    if (n > 0) {
+      if (host) {
+        if (is_pinned(keys)) {
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_keys, keys, n * 8, cudaMemcpyHostToDevice, st));
+        } else {
+          std::memcpy(ws->h_keys, keys, n * 8);
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_keys, ws->h_keys, n * 8, cudaMemcpyHostToDevice, st));
+        }
+        d_keys = ws->d_keys;
+        d_out = ws->d_out;
+        d_flags = ws->d_flags;
+      } else {
+        cache_->join_from(user);
+      }
+      ws->table_epoch += 1;
+      if (ws->table_epoch == 0) {
+        HPSB_CUDA(cudaMemsetAsync(ws->ls.miss_table, 0, ws->ls.cap * 8, st));
+        ws->table_epoch = 1;
+      }
+      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->ls,
+                          ws->table_epoch, st);
+      launch_lookup_compact(d_keys, n, d_flags, ws->ls, ws->table_epoch, ws->scan, st);
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts, 16, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaEventRecord(ws->done, st));
+    }
+  }
+  if (n > 0) {
+    HPSB_CUDA(cudaEventSynchronize(ws->done));
+    uh = ws->h_counts[0] - ws->prev_counts[0];
+    um = ws->h_counts[1] - ws->prev_counts[1];
+    ws->prev_counts[0] = ws->h_counts[0];
+    ws->prev_counts[1] = ws->h_counts[1];
+    if (um > 0) {
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_miss_keys, ws->ls.miss_keys, um * 8,
+                                cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaEventRecord(ws->done, st));
+      HPSB_CUDA(cudaEventSynchronize(ws->done));
+    }
+  }
+  const uint64_t n_unique = uh + um;
+  // lookup_engine.cpp:148-153
+  const double h = n_unique == 0 ? 1.0 : 1.0 - double(um) / double(n_unique);
+  const bool sync_branch = h < cfg_.hit_rate_threshold;
+  TierCounters counters;
+  uint64_t defaults = 0;
+  if (sync_branch) {
+    size_t nf = 0;
+    const size_t absent = fetch_and_upload(*ws, ws->h_miss_keys, um, &counters, &nf);
+    defaults = absent;
+    std::lock_guard<std::mutex> lk(cache_->mutex());
+    if (nf > 0) {
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of, um * 4, cudaMemcpyHostToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                cudaMemcpyHostToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                cudaMemcpyHostToDevice, st));
+      launch_lookup_scatter(n, d, d_flags, d_flags, ws->ls, ws->d_row_of, ws->d_staged, d_out,
+                            st);
+      cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+    }
+    HPSB_CUDA(cudaEventRecord(ws->done, st));
+    ws->pending = true;
+  } else {
+    defaults = um;
+  }
+
+  if (n > 0) {
+    if (host) {
+      const bool po = is_pinned(out), pf = is_pinned(flags);
+      HPSB_CUDA(cudaMemcpyAsync(po ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
+                                cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(pf ? flags : ws->h_flags, d_flags, n, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaEventRecord(ws->done, st));
+      HPSB_CUDA(cudaEventSynchronize(ws->done));
+      ws->pending = false;
+      if (!po) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
+      if (!pf) std::memcpy(flags, ws->h_flags, n);
+    } else {
+      cache_->join_to(user);
+    }
+  }
+
+  if (outcome) {
+    outcome->sync_branch = sync_branch;
+    outcome->unique_hit_rate = h;
+    outcome->unique_count = n_unique;
+    outcome->defaults_returned = defaults;
+  }
+  {
+    std::lock_guard<std::mutex> lk(stats_mu_);
+    stats_.queries += 1;
+    stats_.queried_keys += n;
+    stats_.unique_keys += n_unique;
+    stats_.cache_hits += uh;
+    stats_.cache_misses += um;
+    stats_.defaults_returned += defaults;
+    if (sync_branch) {
+      stats_.sync_batches += 1;
+      stats_.vdb_hits += counters.vdb_hits;
+      stats_.pdb_hits += counters.cold_hits;
+      stats_.tier_missing += counters.missing;
+    } else {
+      stats_.async_batches += 1;
+    }
+  }
+  if (!sync_branch && um > 0) {
+    // the workspace (and its miss list) rides along with the background fill
+    ws->missing_keys.assign(ws->h_miss_keys, ws->h_miss_keys + um);
+    {
+      std::lock_guard<std::mutex> lk(q_mu_);
+      queue_.push_back(AsyncTask{ws});
+      handed_off = true;
+    }
+    q_cv_.notify_one();
+  }
+}
+
+void LookupEngine::async_loop() {
+  for (;;) {
+    AsyncTask task;
+    {
+      std::unique_lock<std::mutex> lk(q_mu_);
+      q_cv_.wait(lk, [&] { return stopping_ || !queue_.empty(); });
+      if (queue_.empty()) return;
+      task = queue_.front();
+      queue_.pop_front();
+      ++active_;
+    }
+    Workspace& ws = *task.ws;
+    TierCounters counters;
+    try {
+      DeviceGuard g(cache_->device());
+      cudaStream_t st = cache_->stream();
+      ws.wait_idle();
+      size_t nf = 0;
+      fetch_and_upload(ws, ws.missing_keys.data(), ws.missing_keys.size(), &counters, &nf);
+      if (nf > 0) {
+        std::lock_guard<std::mutex> lk(cache_->mutex());
+        HPSB_CUDA(cudaMemcpyAsync(ws.d_staged, ws.h_staged, nf * uint64_t(dim_) * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(ws.d_found_keys, ws.h_found_keys, nf * 8,
+                                  cudaMemcpyHostToDevice, st));
+        cache_->replace_device_locked(ws.d_found_keys, nf, ws.d_staged);
+        HPSB_CUDA(cudaEventRecord(ws.done, st));
+        ws.pending = true;
+      }
+      ws.wait_idle();
+      std::lock_guard<std::mutex> lk(stats_mu_);
+      stats_.vdb_hits += counters.vdb_hits;
+      stats_.pdb_hits += counters.cold_hits;
+      stats_.tier_missing += counters.missing;
+    } catch (...) {
+      // the caller already got default rows; a failed fill only costs hit rate
+      std::lock_guard<std::mutex> lk(stats_mu_);
+      stats_.async_faults += 1;
+    }
+    pool_.release(task.ws);
+    {
+      std::lock_guard<std::mutex> lk(q_mu_);
+      --active_;
+      if (queue_.empty() && active_ == 0) idle_cv_.notify_all();
+    }
+  }
+}
+
+void LookupEngine::drain_async() {
+  std::unique_lock<std::mutex> lk(q_mu_);
+  idle_cv_.wait(lk, [&] { return queue_.empty() && active_ == 0; });
+}
+
+EngineStats LookupEngine::stats() const {
+  std::lock_guard<std::mutex> lk(stats_mu_);
+  return stats_;
+}
+
+}  // namespace hpsb

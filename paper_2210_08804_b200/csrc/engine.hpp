@@ -1,0 +1,169 @@
+// engine.hpp -- B200 lookup engine (the object behind hps_engine_*).
+//
+// Mirrors hps::LookupEngine (lookup_engine.hpp:152-196): one lookup =
+// fused device probe of every query position (dedup of hits is implicit,
+// see lookup_kernels.cu), unique-key hit rate h = 1 - |misses|/|Q*|
+// (h = 1 for an empty batch), strict `h < threshold` switch between the
+// synchronous tier fetch + replace and the asynchronous default-rows path
+// whose fetch + replace run on background workers holding the workspace
+// lease, and the same statistics. Workspaces are a bounded pool of device
+// + pinned buffers (the reference's WorkspacePool, lookup_engine.cpp:9-48):
+// acquiring one is the admission ticket, so the pool bounds in-flight
+// batches and provides backpressure.
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "device_cache.hpp"
+#include "kernels.hpp"
+#include "runtime.hpp"
+#include "volatile_store.hpp"
+
+namespace hpsb {
+
+// Cold tier (stands in for PersistentStore::get, persistent_store.cpp:405-439).
+using ColdFetchFn = int (*)(void* ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
+                            float* found_vectors, size_t* n_found, uint64_t* missing_keys,
+                            size_t* n_missing);
+
+struct TierCounters {
+  uint64_t vdb_hits = 0, cold_hits = 0, missing = 0;
+};
+
+// tier_fetch (lookup_engine.cpp:50-89) writing found rows straight into
+// `rows` (n * dim) in found order (VDB hits in input order, then cold hits in
+// input order); row_of[i] = found row of keys[i] or -1. found_keys holds n.
+void tier_fetch_staged(VolatileStore* vdb, const std::string& table, uint32_t dim,
+                       ColdFetchFn cold, void* cold_ctx, const uint64_t* keys, size_t n,
+                       uint64_t* found_keys, float* rows, int32_t* row_of, size_t* n_found,
+                       uint64_t* missing_keys, size_t* n_missing, TierCounters* counters);
+
+struct EngineConfig {
+  double hit_rate_threshold = 0.8;
+  std::vector<float> default_vector;
+  uint32_t workspace_pool_size = 16;
+  uint32_t async_worker_count = 2;
+  bool volatile_tier_enabled = true;
+  uint32_t max_batch = 131072;
+};
+
+struct LookupOutcome {
+  bool sync_branch = false;
+  double unique_hit_rate = 0.0;
+  uint64_t unique_count = 0;
+  uint64_t defaults_returned = 0;
+};
+
+struct EngineStats {
+  uint64_t queries = 0, queried_keys = 0, unique_keys = 0, cache_hits = 0, cache_misses = 0,
+           sync_batches = 0, async_batches = 0, defaults_returned = 0, vdb_hits = 0,
+           pdb_hits = 0, tier_missing = 0, async_faults = 0;
+};
+
+// Device + pinned buffers of one in-flight batch.
+struct Workspace {
+  int device = 0;
+  uint64_t capacity = 0;  // keys
+  uint32_t dim = 0;
+  // device
+  DeviceBuffer dbuf;
+  uint64_t* d_keys = nullptr;
+  float* d_out = nullptr;
+  uint8_t* d_flags = nullptr;
+  int32_t* d_row_of = nullptr;
+  float* d_staged = nullptr;
+  uint64_t* d_found_keys = nullptr;
+  LookupScratch ls;
+  ScanState scan;
+  uint32_t table_epoch = 0;
+  unsigned long long prev_counts[2] = {0, 0};
+  // pinned host
+  PinnedBuffer hbuf;
+  uint64_t* h_keys = nullptr;
+  unsigned long long* h_counts = nullptr;
+  uint64_t* h_miss_keys = nullptr;
+  int32_t* h_row_of = nullptr;
+  float* h_staged = nullptr;
+  uint64_t* h_found_keys = nullptr;
+  uint64_t* h_missing = nullptr;
+  uint8_t* h_flags = nullptr;
+  float* h_out = nullptr;
+  // batch state (for the async task)
+  std::vector<uint64_t> missing_keys;
+  cudaEvent_t done = nullptr;
+  bool pending = false;  // `done` recorded, not yet waited
+
+  ~Workspace();
+  void ensure(uint64_t n, uint32_t d, cudaStream_t st);
+  void wait_idle();
+};
+
+class WorkspacePool {
+ public:
+  WorkspacePool(size_t size, int device);
+  Workspace* acquire();  // blocks until one is free
+  void release(Workspace* ws);
+  size_t size() const { return slots_.size(); }
+  size_t outstanding() const;
+  size_t peak_outstanding() const;
+
+ private:
+  std::vector<std::unique_ptr<Workspace>> slots_;
+  mutable std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<Workspace*> free_;
+  size_t outstanding_ = 0, peak_ = 0;
+};
+
+class LookupEngine {
+ public:
+  LookupEngine(const std::string& table, uint32_t dim, DeviceCache* cache, VolatileStore* vdb,
+               ColdFetchFn cold, void* cold_ctx, EngineConfig cfg);
+  ~LookupEngine();
+
+  void lookup(const uint64_t* keys, size_t n, float* out, size_t out_len, uint8_t* flags,
+              LookupOutcome* outcome, int mem, cudaStream_t user);
+  void drain_async();
+  EngineStats stats() const;
+  WorkspacePool& pool() { return pool_; }
+
+ private:
+  struct AsyncTask {
+    Workspace* ws;
+  };
+  void async_loop();
+  // fetch ws->missing_keys from the tiers into ws's pinned staging, upload,
+  // and (optionally) scatter into the output + replace into the cache.
+  size_t fetch_and_upload(Workspace& ws, const uint64_t* miss_keys, size_t n_miss,
+                          TierCounters* counters, size_t* n_found);
+
+  std::string table_;
+  uint32_t dim_;
+  DeviceCache* cache_;
+  VolatileStore* vdb_;
+  ColdFetchFn cold_;
+  void* cold_ctx_;
+  EngineConfig cfg_;
+  float* d_default_ = nullptr;
+  WorkspacePool pool_;
+
+  mutable std::mutex stats_mu_;
+  EngineStats stats_;
+
+  std::mutex q_mu_;
+  std::condition_variable q_cv_, idle_cv_;
+  std::deque<AsyncTask> queue_;
+  size_t active_ = 0;
+  bool stopping_ = false;
+  std::vector<std::thread> workers_;
+};
+
+}  // namespace hpsb

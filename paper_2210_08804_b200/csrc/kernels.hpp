@@ -1,0 +1,99 @@
+// kernels.hpp -- host-side launchers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hpsb {
+
+// Look-back scan state of one serialised user (a cache or a workspace).
+struct ScanState {
+  uint64_t* status = nullptr;             // one word per tile
+  unsigned long long* tile_ctr = nullptr; // cumulative tile ticket counter
+  uint64_t capacity_tiles = 0;
+  unsigned long long tile_base = 0;       // tickets issued so far
+  uint32_t epoch = 0;                     // 24-bit epoch of the next launch
+};
+
+// Tile geometry of the ordered-compaction kernels.
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 4;
+constexpr uint64_t kScanTile = uint64_t(kScanBlock) * kScanItems;
+
+// Prepares `s` for one launch of `tiles` tiles; returns false if the status
+// array had to be cleared (epoch wrap) -- handled internally.
+void scan_begin(ScanState& s, uint64_t tiles, cudaStream_t st);
+
+// ---- cache-level operations (slab_cache.cpp) ----
+void launch_cache_query(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
+                        uint8_t* hit, uint64_t stamp, int keys_per_warp, cudaStream_t st);
+void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
+                          uint32_t* miss_pos, uint64_t* miss_keys,
+                          unsigned long long* n_miss, ScanState& scan, cudaStream_t st);
+
+struct ReplaceScratch {
+  uint64_t cap = 0;          // power of two >= 2n
+  uint64_t* tab_set = nullptr;
+  uint32_t* tab_cnt = nullptr;
+  uint32_t* tab_off = nullptr;
+  uint32_t* tab_fill = nullptr;
+  uint32_t* key_tab = nullptr;  // n
+  uint32_t* bucket = nullptr;   // n
+  uint32_t* cursor = nullptr;
+  uint32_t* dup_flag = nullptr;
+};
+// Needed bytes for n keys, and carving of a raw buffer.
+size_t replace_scratch_bytes(uint64_t n);
+ReplaceScratch replace_scratch_carve(void* base, uint64_t n);
+void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
+                    uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st);
+
+struct UpdateScratch {
+  uint64_t cap = 0;
+  uint64_t* ut_key = nullptr;    // cap, EMPTY = ~0
+  uint32_t* ut_pos = nullptr;    // cap, max(position + 1)
+  uint32_t* found_tab = nullptr; // n
+  unsigned long long* written = nullptr;
+};
+size_t update_scratch_bytes(uint64_t n);
+UpdateScratch update_scratch_carve(void* base, uint64_t n);
+void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
+                   int keys_per_warp, const UpdateScratch& us, cudaStream_t st);
+
+void launch_dump(const CacheDev& c, uint64_t set_begin, uint64_t set_end, uint64_t* out,
+                 unsigned long long* n_out, ScanState& scan, cudaStream_t st);
+
+// ---- dedup (types.cpp:20-34) ----
+struct DedupScratch {
+  uint64_t cap = 0;
+  uint64_t* table = nullptr;       // cap, (epoch << 32) | first position
+  uint32_t* slot_of = nullptr;     // n
+  uint32_t* rank_of_slot = nullptr;  // cap
+  unsigned long long* n_unique = nullptr;
+};
+void launch_dedup(const uint64_t* keys, uint64_t n, uint64_t* unique_out, uint32_t* inverse,
+                  const DedupScratch& ds, uint32_t table_epoch, ScanState& scan,
+                  cudaStream_t st);
+
+// ---- lookup (lookup_engine.cpp:130-241) ----
+struct LookupScratch {
+  uint64_t cap = 0;               // miss table capacity (power of two >= 2 * max_batch)
+  uint64_t* miss_table = nullptr; // (epoch << 32) | first position
+  uint32_t* miss_slot = nullptr;  // per position (valid where missed)
+  uint32_t* rank_of_slot = nullptr;
+  unsigned long long* counts = nullptr;  // [0] unique hits, [1] unique misses (cumulative)
+  uint64_t* miss_keys = nullptr;  // unique misses, first-occurrence order
+};
+void launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
+                         uint8_t* flags, const float* default_row, uint64_t stamp,
+                         const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st);
+void launch_lookup_compact(const uint64_t* keys, uint64_t n, const uint8_t* flags,
+                           const LookupScratch& ls, uint32_t table_epoch, ScanState& scan,
+                           cudaStream_t st);
+void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint8_t* flags,
+                           const LookupScratch& ls, const int32_t* row_of,
+                           const float* staged, float* out, cudaStream_t st);
+
+}  // namespace hpsb

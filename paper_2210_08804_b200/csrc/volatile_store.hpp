@@ -1,0 +1,111 @@
+// volatile_store.hpp -- host volatile DB (level-2 tier) for the miss path.
+//
+// Same contract as hps::VolatileStore (volatile_store.hpp:45-137 of the
+// reference): per-table hash partitions routed by xxh64(key, 0) % P,
+// upsert + evict-oldest down to the overflow margin (ties by smaller key),
+// one clock tick per lookup / insert call, last-access refresh that never
+// moves a stamp backwards. Storage is built for the GPU miss path instead
+// of per-key std::vector rows: each partition keeps an open-addressing index
+// over one contiguous row arena, lookups fan out over a thread pool in
+// input-order chunks, and found rows are copied straight into a (pinned)
+// staging buffer in found order. Refreshes are applied inline with an
+// atomic max (the reference queues them to a background thread; the
+// drained state is identical).
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <shared_mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace hpsb {
+
+uint32_t partition_of(uint64_t key, uint32_t partition_count);  // volatile_store.cpp:10-13
+
+class VolatileStore {
+ public:
+  explicit VolatileStore(unsigned lookup_threads);
+  ~VolatileStore();
+
+  void register_table(const std::string& name, uint32_t dim, uint32_t partition_count,
+                      uint64_t overflow_margin);
+  bool has_table(const std::string& name) const;
+  uint32_t dimension(const std::string& name) const;
+
+  // Upsert + prune touched partitions; returns evicted keys.
+  std::vector<uint64_t> insert(const std::string& name, const uint64_t* keys, size_t n,
+                               const float* vectors, size_t vectors_len);
+  void insert_async(const std::string& name, std::vector<uint64_t> keys,
+                    std::vector<float> vectors);
+  std::vector<uint64_t> evict(const std::string& name, uint32_t partition);
+
+  // Lookup in input order. found_rows receives n_found * dim floats in found
+  // order; found_idx (optional, n entries) gets the found row index of each
+  // input key or -1. found_keys / missing_keys hold n entries.
+  void lookup(const std::string& name, const uint64_t* keys, size_t n, uint64_t* found_keys,
+              float* found_rows, int32_t* found_idx, size_t* n_found, uint64_t* missing_keys,
+              size_t* n_missing);
+
+  void drain();
+
+  uint64_t partition_size(const std::string& name, uint32_t partition) const;
+  uint64_t table_size(const std::string& name) const;
+  uint64_t table_clock(const std::string& name) const;
+  bool last_access(const std::string& name, uint64_t key, uint64_t* out) const;
+
+ private:
+  struct Partition {
+    mutable std::shared_mutex mu;
+    // open addressing: slot -> entry index + 1 (0 = empty)
+    std::vector<uint32_t> index;
+    std::vector<uint64_t> keys;             // per entry
+    std::vector<uint64_t> last_access;      // per entry (updated with atomic_ref max)
+    std::vector<float> rows;                // entry * dim
+    std::vector<uint32_t> free_entries;
+    uint64_t live = 0;
+    int64_t find(uint64_t key) const;       // entry or -1
+  };
+  struct Table {
+    std::string name;
+    uint32_t dim = 0;
+    uint32_t partition_count = 16;
+    uint64_t overflow_margin = 1u << 20;
+    std::atomic<uint64_t> clock{0};
+    std::vector<std::unique_ptr<Partition>> parts;
+  };
+  struct Task {
+    Table* table;
+    std::vector<uint64_t> keys;
+    std::vector<float> vectors;
+  };
+
+  Table& table_ref(const std::string& name) const;
+  std::vector<uint64_t> insert_rows(Table& t, const uint64_t* keys, size_t n,
+                                    const float* vectors, uint64_t stamp);
+  static void upsert(Partition& p, uint32_t dim, uint64_t key, const float* row, uint64_t stamp);
+  static std::vector<uint64_t> prune(Table& t, Partition& p);
+  static void erase_entry(Partition& p, uint32_t dim, uint64_t key);
+  void background_loop();
+
+  mutable std::mutex tables_mu_;
+  std::unordered_map<std::string, std::unique_ptr<Table>> tables_;
+  ThreadPool pool_;
+
+  std::mutex q_mu_;
+  std::condition_variable q_cv_, idle_cv_;
+  std::deque<Task> queue_;
+  bool busy_ = false;
+  bool stopping_ = false;
+  std::thread worker_;
+};
+
+}  // namespace hpsb

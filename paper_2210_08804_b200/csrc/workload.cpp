@@ -1,0 +1,49 @@
+// workload.cpp -- synthetic power-law key streams (harness input).
+//
+// Bit-exact restatement of PowerLawSampler (workload.cpp:18-20, 24-70 of the
+// reference): inverse CDF over r^-alpha (running sum of std::pow, normalised,
+// last entry forced to 1.0), mt19937_64 Fisher-Yates rank -> key permutation
+// (`gen() % (i + 1)`), uniform = top 53 bits * 2^-53, upper_bound search.
+// The CDF build and the permutation are O(keyspace); the draws fan out over
+// threads with per-draw generator positions reproduced by discarding.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace hpsb {
+
+void powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed, uint64_t draw_seed,
+                     size_t count, uint64_t* out) {
+  if (keyspace == 0) throw invalid_argument("keyspace must be positive");
+  if (!(alpha > 0.0)) throw invalid_argument("alpha must be positive");
+  std::vector<double> cdf(keyspace);
+  double running = 0.0;
+  for (uint64_t r = 1; r <= keyspace; ++r) {
+    running += std::pow(static_cast<double>(r), -alpha);
+    cdf[r - 1] = running;
+  }
+  for (double& c : cdf) c /= running;
+  cdf.back() = 1.0;
+  std::vector<uint64_t> rank_to_key(keyspace);
+  for (uint64_t i = 0; i < keyspace; ++i) rank_to_key[i] = i;
+  std::mt19937_64 perm(permute_seed);
+  for (uint64_t i = keyspace - 1; i > 0; --i) {
+    const uint64_t j = perm() % (i + 1);
+    std::swap(rank_to_key[i], rank_to_key[j]);
+  }
+  std::mt19937_64 gen(draw_seed);
+  for (size_t i = 0; i < count; ++i) {
+    const double u = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+    const auto it = std::upper_bound(cdf.begin(), cdf.end(), u);
+    uint64_t rank = static_cast<uint64_t>(it - cdf.begin()) + 1;
+    rank = std::min(rank, keyspace);
+    out[i] = rank_to_key[rank - 1];
+  }
+}
+
+}  // namespace hpsb

@@ -1,0 +1,282 @@
+"""GPU parity for the lookup engine (calls through the C ABI).
+
+Port of /root/reference/proj/tests/unit/test_lookup_engine.cpp (the cold
+tier is a DictStore with PersistentStore::get's contract) plus lockstep
+sessions against the reference-generated fixture and the Python engine
+oracle."""
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2210_08804_b200 as hps
+from opstream import row_values
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+T = hps.TableId
+
+
+def rows(keys, dim, salt=0.0):
+    # test_lookup_engine.cpp:23-32
+    return np.array([[float(k) * 10.0 + salt + c for c in range(dim)] for k in keys],
+                    dtype=np.float32).reshape(-1)
+
+
+class Fixture:
+    def __init__(self, pdb_keys=20):
+        self.table = T("t", 2)
+        self.pdb = hps.DictStore(2)
+        keys = list(range(pdb_keys))
+        self.pdb.put(keys, rows(keys, 2))
+        self.cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=8, slabs_per_set=2,
+                                                       dimension=2))
+
+
+def test_cold_lookup_takes_sync_branch_and_admits():
+    fx = Fixture()
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig(hit_rate_threshold=0.75))
+    o = hps.LookupOutcome()
+    keys = [0, 1, 2, 3]
+    r = e.lookup(keys, o)
+    assert o.sync_branch and o.unique_hit_rate == 0.0 and o.unique_count == 4
+    assert o.defaults_returned == 0
+    assert r.dimension == 2 and r.miss_flags.tolist() == [0] * 4
+    assert r.vectors.tolist() == rows(keys, 2).tolist()
+    r2 = e.lookup(keys, o)
+    assert o.unique_hit_rate == 1.0 and not o.sync_branch
+    assert r2.vectors.tolist() == rows(keys, 2).tolist()
+    assert fx.cache.occupied() == 4
+
+
+def test_async_branch_ships_defaults_and_fills_in_background():
+    fx = Fixture()
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb,
+                         hps.EngineConfig(hit_rate_threshold=0.75, default_vector=[9.0, 9.0]))
+    e.lookup([0, 1, 2, 3, 4, 5])
+    o = hps.LookupOutcome()
+    r = e.lookup([0, 1, 2, 3, 4, 5, 10, 11], o)
+    assert not o.sync_branch and o.unique_hit_rate == 0.75 and o.defaults_returned == 2
+    assert r.miss_flags.tolist() == [0] * 6 + [1, 1]
+    assert r.vectors[12] == 9.0 and r.vectors[15] == 9.0
+    e.drain_async()
+    r2 = e.lookup([10, 11], o)
+    assert o.unique_hit_rate == 1.0
+    assert r2.miss_flags.tolist() == [0, 0]
+    assert r2.vectors.tolist() == rows([10, 11], 2).tolist()
+
+
+def test_duplicate_keys_expand_to_identical_rows():
+    fx = Fixture()
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig(hit_rate_threshold=0.75))
+    o = hps.LookupOutcome()
+    r = e.lookup([5, 5, 6, 5], o)
+    assert o.unique_count == 2
+    v5, v6 = rows([5], 2).tolist(), rows([6], 2).tolist()
+    assert r.vectors.tolist() == v5 + v5 + v6 + v5
+
+
+def test_empty_query_returns_empty_result():
+    fx = Fixture()
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig())
+    clock = fx.cache.recency_clock()
+    o = hps.LookupOutcome()
+    r = e.lookup([], o)
+    assert len(r.vectors) == 0 and len(r.miss_flags) == 0
+    assert o.unique_count == 0 and o.unique_hit_rate == 1.0 and not o.sync_branch
+    assert fx.cache.recency_clock() == clock + 1  # the cache query still ticks
+
+
+def test_threshold_comparison_is_strict():
+    def run(t):
+        fx = Fixture()
+        e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig(hit_rate_threshold=t))
+        e.lookup([0])
+        o = hps.LookupOutcome()
+        e.lookup([0, 1], o)
+        return o
+
+    at = run(0.5)
+    assert at.unique_hit_rate == 0.5 and not at.sync_branch
+    below = run(0.5625)
+    assert below.unique_hit_rate == 0.5 and below.sync_branch and below.defaults_returned == 0
+
+
+def test_absent_keys_come_back_as_flagged_defaults():
+    fx = Fixture()
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb,
+                         hps.EngineConfig(hit_rate_threshold=0.75, default_vector=[7.0]))
+    o = hps.LookupOutcome()
+    r = e.lookup([500, 501], o)
+    assert o.sync_branch and o.defaults_returned == 2
+    assert r.miss_flags.tolist() == [1, 1]
+    assert r.vectors.tolist() == [7.0, 0.0, 7.0, 0.0]
+    assert fx.cache.occupied() == 0
+    assert e.stats().tier_missing == 2
+
+
+def test_engine_stats_add_up_over_a_deterministic_sequence():
+    fx = Fixture()
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig(hit_rate_threshold=0.75))
+    e.lookup([0, 1, 2, 3])
+    e.lookup([0, 1, 2, 3, 4, 5, 6, 7])
+    e.lookup([0, 1, 2, 3, 4, 5, 6, 7])
+    e.lookup([0, 1, 2, 3, 4, 5, 10, 11])
+    e.drain_async()
+    e.lookup([10, 11])
+    e.drain_async()
+    s = e.stats()
+    assert (s.queries, s.queried_keys, s.unique_keys) == (5, 30, 30)
+    assert (s.cache_hits, s.cache_misses) == (20, 10)
+    assert (s.sync_batches, s.async_batches, s.defaults_returned) == (2, 3, 2)
+    assert (s.pdb_hits, s.vdb_hits, s.tier_missing, s.async_faults) == (10, 0, 0, 0)
+
+
+def test_volatile_tier_values_win_when_enabled_and_are_skipped_when_not():
+    table = T("t", 1)
+    pdb = hps.DictStore(1)
+    pdb.put([3], [30.0])
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vdb.insert("t", [3], [33.0])
+    c1 = hps.SlabCache(hps.SlabCacheConfig(slabset_count=4, slabs_per_set=2, dimension=1))
+    e1 = hps.LookupEngine(table, c1, vdb, pdb, hps.EngineConfig(hit_rate_threshold=0.75))
+    assert e1.lookup([3]).vectors.tolist() == [33.0]
+    assert e1.stats().vdb_hits == 1
+    c2 = hps.SlabCache(hps.SlabCacheConfig(slabset_count=4, slabs_per_set=2, dimension=1))
+    e2 = hps.LookupEngine(table, c2, vdb, pdb,
+                          hps.EngineConfig(hit_rate_threshold=0.75, volatile_tier_enabled=False))
+    assert e2.lookup([3]).vectors.tolist() == [30.0]
+    assert e2.stats().vdb_hits == 0 and e2.stats().pdb_hits == 1
+
+
+def test_workspace_pool_bounds_in_flight_batches():
+    fx = Fixture(200)
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb,
+                         hps.EngineConfig(hit_rate_threshold=0.0, workspace_pool_size=2,
+                                          async_worker_count=1))
+    for i in range(30):
+        e.lookup([i * 3 % 200, (i * 3 + 1) % 200])
+    e.drain_async()
+    p = e.workspace_pool()
+    assert p.size == 2 and p.outstanding == 0 and 1 <= p.peak_outstanding <= 2
+
+
+def test_engine_shuts_down_cleanly_with_queued_work():
+    fx = Fixture(100)
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb,
+                         hps.EngineConfig(hit_rate_threshold=0.0, workspace_pool_size=8))
+    for i in range(20):
+        e.lookup([i * 2, i * 2 + 1])
+    e.close()
+
+
+def test_configuration_is_validated():
+    fx = Fixture()
+    for cfg in (hps.EngineConfig(hit_rate_threshold=-0.1), hps.EngineConfig(hit_rate_threshold=1.5),
+                hps.EngineConfig(async_worker_count=0), hps.EngineConfig(workspace_pool_size=0)):
+        with pytest.raises(hps.InvalidArgument):
+            hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, cfg)
+    wrong = hps.SlabCache(hps.SlabCacheConfig(slabset_count=2, slabs_per_set=2, dimension=5))
+    with pytest.raises(hps.InvalidArgument):
+        hps.LookupEngine(fx.table, wrong, None, fx.pdb, hps.EngineConfig())
+
+
+def test_reference_engine_session_fixture():
+    """40 lookups through the reference LookupEngine (engine.json) replayed
+    through the device engine: outcomes, every output byte, flags, stats."""
+    e = json.loads((GOLD / "engine.json").read_text())
+    d = e["dim"]
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table, hps.VolatileTableConfig(partition_count=e["partitions"]))
+    vk = np.arange(e["vdb_keys"], dtype=np.uint64)
+    vdb.insert("t", vk, row_values(vk, d, e["vdb_salt"]))
+    c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=e["S"], slabs_per_set=e["W"], dimension=d))
+    eng = hps.LookupEngine(table, c, vdb, None,
+                           hps.EngineConfig(hit_rate_threshold=e["threshold"],
+                                            default_vector=e["default_vector"]))
+    rng = np.random.default_rng(e["batch_seed"])
+    for step in e["steps"]:
+        keys = rng.integers(0, e["key_range"], 1 + int(rng.integers(300)), dtype=np.uint64)
+        o = hps.LookupOutcome()
+        r = eng.lookup(keys, o)
+        eng.drain_async()
+        assert o.__dict__ == step["outcome"]
+        assert hashlib.sha256(r.vectors.tobytes()).hexdigest() == step["out_sha"]
+        assert hashlib.sha256(r.miss_flags.tobytes()).hexdigest() == step["flags_sha"]
+    assert eng.stats().__dict__ == e["stats"]
+
+
+@pytest.mark.parametrize("threshold", [0.0, 0.7, 0.95, 1.0])
+def test_lockstep_with_engine_oracle_power_law(threshold):
+    d, S = 32, 64
+    eo = oracle.EngineOracle(S, 2, d, threshold=threshold, default_vector=[1.5])
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vk = np.arange(0, 40000, 2, dtype=np.uint64)  # odd keys are absent everywhere
+    vv = row_values(vk, d, 3)
+    vdb.insert("t", vk, vv)
+    for k, r in zip(vk, vv.reshape(-1, d)):
+        eo.vdb[int(k)] = r
+    c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
+    eng = hps.LookupEngine(table, c, vdb, None,
+                           hps.EngineConfig(hit_rate_threshold=threshold, default_vector=[1.5]))
+    stream = hps.powerlaw_sample(1.2, 40000, 7, 8, 30 * 2048)
+    for b in range(30):
+        keys = stream[b * 2048:(b + 1) * 2048]
+        o = hps.LookupOutcome()
+        r = eng.lookup(keys, o)
+        eng.drain_async()
+        out, flags, oc = eo.lookup(keys)
+        eo.drain_async()
+        assert o.__dict__ == oc
+        assert r.vectors.tobytes() == out.tobytes()
+        assert (r.miss_flags == flags).all()
+    s = eng.stats().__dict__
+    assert s == eo.stats
+    c.check_invariants()
+
+
+def test_device_and_pinned_pointer_lookups_match_host_lookup():
+    import torch
+
+    d = 128
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vk = np.arange(100000, dtype=np.uint64)
+    vdb.insert("t", vk, row_values(vk, d, 2))
+
+    def mk():
+        c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=1024, slabs_per_set=2, dimension=d))
+        return c, hps.LookupEngine(table, c, vdb, None, hps.EngineConfig(hit_rate_threshold=0.8))
+
+    ch, eh = mk()
+    cd, ed = mk()
+    cp, ep = mk()
+    stream = hps.powerlaw_sample(1.2, 100000, 1, 2, 8 * 16384)
+    for b in range(8):
+        keys = stream[b * 16384:(b + 1) * 16384]
+        r = eh.lookup(keys)
+        eh.drain_async()
+        kt = torch.from_numpy(keys.view(np.int64)).cuda()
+        out = torch.empty(len(keys) * d, device="cuda")
+        fl = torch.empty(len(keys), dtype=torch.uint8, device="cuda")
+        ed.lookup_ptrs(kt.data_ptr(), len(keys), out.data_ptr(), fl.data_ptr(), hps.HPS_MEM_DEVICE,
+                       torch.cuda.current_stream().cuda_stream)
+        torch.cuda.current_stream().synchronize()
+        ed.drain_async()
+        assert out.cpu().numpy().tobytes() == r.vectors.tobytes()
+        assert (fl.cpu().numpy() == r.miss_flags).all()
+        kp = torch.from_numpy(keys.view(np.int64)).pin_memory()
+        op = torch.empty(len(keys) * d).pin_memory()
+        fp = torch.empty(len(keys), dtype=torch.uint8).pin_memory()
+        ep.lookup_ptrs(kp.data_ptr(), len(keys), op.data_ptr(), fp.data_ptr(), hps.HPS_MEM_HOST)
+        ep.drain_async()
+        assert op.numpy().tobytes() == r.vectors.tobytes()
+        assert (fp.numpy() == r.miss_flags).all()
