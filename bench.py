@@ -1,0 +1,577 @@
+#!/usr/bin/env python
+"""bench.py -- HPS embedding-cache lookup on B200 (BASELINE.json configs[1]).
+
+Workload (cfg 2): 10M-key table, dim 128, f32 rows, cache 20%
+of the table (S = 31,250 slabsets x 2 slabs x 32 slots = 2,000,000 slots),
+batch 65,536 keys drawn power-law (alpha 1.2). The cache is preloaded with
+the hottest 2.2M keys through replace; the resident set is read back with
+dump_all; each batch position is drawn from the resident set with
+probability p (power-law over resident ranks) else from the non-resident
+keys (power-law over their ranks), p calibrated so the measured UNIQUE-key
+hit rate (lookup_engine.cpp:148-152) hits the target. Headline h = 0.90;
+the sweep adds 0.50 and 0.99. Data are synthetic.
+
+One step = one lookup of one 65,536-key batch:
+  value -- hps_cache_lookup_device (probe + gather + expand + unique counts
+           + ordered unique-miss list) on keys already in HBM, CUDA events on
+           the cache stream, query-only so h stays fixed;
+  e2e   -- hps_engine_lookup (the reference-facing LookupEngine call) with
+           pinned HOST keys / rows / flags: H2D keys, device lookup, hit-rate
+           switch, async VDB fill + replace of misses, D2H rows + flags;
+           wall clock with a final drain of the async fills.
+L2 policy: inputs larger than L2 -- the cache table is 1.06 GB, keys come
+from a pool of 32 distinct batches and outputs rotate over 8 x 33.5 MB.
+
+Multi-GPU: one process per GPU (torchrun), each rank an independent cache
+replica serving its own stream (weak scaling); no collective on the data
+path; timing = max over ranks.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference/proj sources) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+P1 = np.uint64(0x9E3779B185EBCA87)
+P2 = np.uint64(0xC2B2AE3D27D4EB4F)
+P3 = np.uint64(0x165667B19E3779F9)
+P4 = np.uint64(0x85EBCA77C2B2AE63)
+P5 = np.uint64(0x27D4EB2F165667C5)
+
+
+def np_xxh64_key(keys: np.ndarray, seed: int) -> np.ndarray:
+    """Vectorised xxh64 of 8-byte LE keys (xxhash64.hpp:86-113, length 8)."""
+    with np.errstate(over="ignore"):
+        k = keys.astype(np.uint64)
+
+        def rotl(x, r):
+            return (x << np.uint64(r)) | (x >> np.uint64(64 - r))
+
+        h = np.uint64(seed) + P5 + np.uint64(8)
+        h = h ^ (rotl(k * P2, 31) * P1)
+        h = rotl(h, 27) * P1 + P4
+        h ^= h >> np.uint64(33)
+        h *= P2
+        h ^= h >> np.uint64(29)
+        h *= P3
+        h ^= h >> np.uint64(32)
+        return h
+
+
+def table_rows(keys: np.ndarray, d: int) -> np.ndarray:
+    """Deterministic synthetic table rows in [-1, 1) (stand-in for gen_table)."""
+    with np.errstate(over="ignore"):
+        k = keys.astype(np.uint64)[:, None] * np.uint64(0x9E3779B1)
+        c = np.arange(d, dtype=np.uint64)[None, :] * np.uint64(0x85EBCA77)
+        v = ((k + c) & np.uint64(0xFFFFFF)).astype(np.float32)
+    return (v / np.float32(8388608.0) - np.float32(1.0)).reshape(-1)
+
+
+class Workload:
+    """cfg-2 geometry + hit-rate-calibrated power-law batches."""
+
+    def __init__(self, keyspace=10_000_000, dim=128, cache_frac=0.2, slabs_per_set=2,
+                 batch=65536, alpha=1.2, seed=42):
+        self.keyspace = keyspace
+        self.dim = dim
+        self.W = slabs_per_set
+        # bench.cpp:63-69 sizing rule: ceil(keys * frac / (W * 32))
+        self.S = int(-(-int(keyspace * cache_frac) // (slabs_per_set * 32)))
+        self.capacity = self.S * self.W * 32
+        self.batch = batch
+        self.alpha = alpha
+        self.seed = seed
+        rng = np.random.default_rng(seed)
+        self.rank_to_key = rng.permutation(keyspace).astype(np.uint64)
+        self.preload = self.rank_to_key[: int(self.capacity * 1.1)]
+
+    def set_resident(self, resident: np.ndarray):
+        """Resident keys ordered by their table rank; the rest likewise."""
+        rank_of = np.empty(self.keyspace, dtype=np.int64)
+        rank_of[self.rank_to_key.astype(np.int64)] = np.arange(self.keyspace)
+        is_res = np.zeros(self.keyspace, dtype=bool)
+        is_res[resident.astype(np.int64)] = True
+        order = self.rank_to_key
+        self.R = order[is_res[order.astype(np.int64)]]
+        self.NR = order[~is_res[order.astype(np.int64)]]
+
+        def cdf(n):
+            w = np.arange(1, n + 1, dtype=np.float64) ** (-self.alpha)
+            c = np.cumsum(w)
+            c /= c[-1]
+            return c
+
+        self.cdf_r = cdf(len(self.R))
+        self.cdf_nr = cdf(len(self.NR))
+
+    def _draw(self, p, u_sel, u_r):
+        is_r = u_sel < p
+        kr = self.R[np.minimum(np.searchsorted(self.cdf_r, u_r, side="right"), len(self.R) - 1)]
+        kn = self.NR[np.minimum(np.searchsorted(self.cdf_nr, u_r, side="right"), len(self.NR) - 1)]
+        return np.where(is_r, kr, kn), is_r
+
+    @staticmethod
+    def unique_hit_rate(keys, is_r):
+        u = np.unique(keys).size
+        ur = np.unique(keys[is_r]).size
+        return 1.0 if u == 0 else ur / u
+
+    def calibrate(self, target: float, seed: int) -> float:
+        rng = np.random.default_rng(seed)
+        u_sel = rng.random(self.batch)
+        u_r = rng.random(self.batch)
+        lo, hi = 0.0, 1.0
+        for _ in range(30):
+            mid = (lo + hi) / 2
+            h = self.unique_hit_rate(*self._draw(mid, u_sel, u_r))
+            if h < target:
+                lo = mid
+            else:
+                hi = mid
+        return hi
+
+    def batches(self, target: float, count: int, seed: int):
+        p = self.calibrate(target, seed)
+        rng = np.random.default_rng(seed + 1)
+        out, hs = [], []
+        for _ in range(count):
+            keys, is_r = self._draw(p, rng.random(self.batch), rng.random(self.batch))
+            out.append(np.ascontiguousarray(keys, dtype=np.uint64))
+            hs.append(self.unique_hit_rate(keys, is_r))
+        return out, p, float(np.mean(hs))
+
+    def algorithmic_bytes(self, keys: np.ndarray, cache_keys: np.ndarray,
+                          masks: np.ndarray) -> tuple:
+        """B = 8|Q| + 260 sum_u s_u + 8H + 4dH + 4d|Q| (lookup
+        level, R_out = |Q|). s_u = slabs probed for unique key u."""
+        u = np.unique(keys)
+        sets = np_xxh64_key(u, 0x5EED5E7) % np.uint64(self.S)
+        first = np_xxh64_key(u, 0x51AB) % np.uint64(self.W)
+        ck = cache_keys.reshape(-1, 32)
+        bits = np.uint32(1) << np.arange(32, dtype=np.uint32)
+        probes = np.zeros(len(u), dtype=np.int64)
+        hit = np.zeros(len(u), dtype=bool)
+        pending = np.ones(len(u), dtype=bool)
+        for step in range(self.W):
+            slab = (sets * np.uint64(self.W) + (first + np.uint64(step)) % np.uint64(self.W)).astype(np.int64)
+            m = masks[slab]
+            occ = (m[:, None] & bits[None, :]) != 0
+            found = ((ck[slab] == u[:, None]) & occ).any(axis=1)
+            probes += pending
+            hit |= pending & found
+            pending &= ~found & (m == np.uint32(0xFFFFFFFF))
+        H = int(hit.sum())
+        q = len(keys)
+        b = 8 * q + 260 * int(probes.sum()) + 8 * H + 4 * self.dim * H + 4 * self.dim * q
+        return b, H, len(u), float(probes.mean())
+
+
+# ---------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the measurement."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int, period_ms: int = 50):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(period_ms)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if not self.samples:
+            return None
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def hbm_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        return float(json.loads(f.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get("lookup_probe_dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------ our arm -----
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2210_08804_b200 as hps
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    wl = Workload(keyspace=args.keyspace, dim=args.dim, cache_frac=args.cache_frac,
+                  batch=args.batch)
+    d, n = wl.dim, wl.batch
+    cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=wl.S, slabs_per_set=wl.W,
+                                              dimension=d, worker_pool_size=8,
+                                              tasks_per_worker=8), device=dev)
+    st = torch.cuda.ExternalStream(cache.stream(), device=dev)
+    # preload the hottest keys through replace (device path, 64K chunks)
+    for i in range(0, len(wl.preload), n):
+        k = wl.preload[i:i + n]
+        kt = torch.from_numpy(k.view(np.int64)).to(dev)
+        rt = torch.from_numpy(table_rows(k, d)).to(dev)
+        cache.replace_device(kt.data_ptr(), len(k), rt.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    resident = cache.dump_all()
+    wl.set_resident(resident)
+    ckeys, _, cmasks, _ = (None, None, None, None)
+    keys_state = np.empty(cache.capacity(), np.uint64)
+    masks_state = np.empty(wl.S * wl.W, np.uint32)
+    hps.lib().hps_cache_export_state(cache.handle, keys_state.ctypes.data, None,
+                                     masks_state.ctypes.data, None)
+
+    default_row = torch.zeros(d, device=dev)
+    pool = 32
+    ring = 8
+    outs = [torch.empty(n * d, device=dev) for _ in range(ring)]
+    flags = [torch.empty(n, dtype=torch.uint8, device=dev) for _ in range(ring)]
+    mkeys = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(ring)]
+
+    def device_run(target, steps, warmup, seed):
+        batches, p, h_draw = wl.batches(target, pool, seed)
+        ab = [wl.algorithmic_bytes(b, keys_state, masks_state) for b in batches]
+        dkeys = [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
+        counts = torch.zeros(max(steps, 1) * 2, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize()
+        sp = st.cuda_stream
+        for s in range(warmup):
+            j = s % pool
+            cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
+                                flags[s % ring].data_ptr(), default_row.data_ptr(),
+                                mkeys[s % ring].data_ptr(), counts.data_ptr(), sp)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        for a, b in kev:  # materialise the cudaEvent_t handles
+            a.record(st)
+            b.record(st)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = hps.kernel_launch_count()
+        with torch.cuda.stream(st):
+            for s in range(steps):
+                j = s % pool
+                ev[s][0].record(st)
+                cache.set_profile_events(kev[s][0].cuda_event, kev[s][1].cuda_event)
+                cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
+                                    flags[s % ring].data_ptr(), default_row.data_ptr(),
+                                    mkeys[s % ring].data_ptr(), counts[2 * s:].data_ptr(), sp)
+                ev[s][1].record(st)
+        torch.cuda.synchronize()
+        launches = hps.kernel_launch_count() - l0
+        cache.set_profile_events(0, 0)
+        if dist:
+            dist.barrier()
+        total_ms = ev[0][0].elapsed_time(ev[-1][1])
+        per = np.array([a.elapsed_time(b) for a, b in ev])
+        k1 = np.array([a.elapsed_time(b) for a, b in kev])
+        c = counts.cpu().numpy().reshape(-1, 2)[:steps]
+        h_meas = float(np.mean(1.0 - c[:, 1] / np.maximum(c.sum(axis=1), 1)))
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        bytes_per = float(np.mean([ab[s % pool][0] for s in range(steps)]))
+        return dict(total_ms=total_ms, p50_us=float(np.median(per) * 1e3),
+                    p99_us=float(np.percentile(per, 99) * 1e3), k1_us=float(k1.mean() * 1e3),
+                    h=h_meas, h_draw=h_draw, p=p, bytes_per_batch=bytes_per,
+                    unique_per_batch=float(np.mean([a[2] for a in ab])),
+                    probes_per_unique=float(np.mean([a[3] for a in ab])), launches=launches)
+
+    clocks = ClockSampler(dev)
+    main = device_run(args.hit, args.steps, args.warmup, seed=1000 + rank)
+    sweep = {}
+    if args.sweep:
+        for h in (0.5, 0.99):
+            r = device_run(h, max(args.steps // 4, 4), args.warmup, seed=2000 + rank + int(h * 100))
+            sweep[f"{h:.2f}"] = {
+                "keys_per_s": world * max(args.steps // 4, 4) * n / (r["total_ms"] / 1e3),
+                "p50_batch_us": r["p50_us"], "measured_unique_hit_rate": r["h"],
+                "probe_kernel_us": r["k1_us"],
+                "probe_kernel_gbs": r["bytes_per_batch"] / (r["k1_us"] * 1e-6) / 1e9}
+    sweep[f"{args.hit:.2f}"] = {
+        "keys_per_s": world * args.steps * n / (main["total_ms"] / 1e3),
+        "p50_batch_us": main["p50_us"], "measured_unique_hit_rate": main["h"],
+        "probe_kernel_us": main["k1_us"],
+        "probe_kernel_gbs": main["bytes_per_batch"] / (main["k1_us"] * 1e-6) / 1e9}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, hps, torch, cache, wl, dev, rank, dist)
+    clk = clocks.stop()
+
+    value = world * args.steps * n / (main["total_ms"] / 1e3)
+    peak, peak_kind = hbm_peak()
+    achieved = main["bytes_per_batch"] / (main["k1_us"] * 1e-6) / 1e9
+    result = None
+    if rank == 0:
+        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args, wl)
+        result = {
+            "metric": "cache lookup keys/sec (steady-state Query, unique-key hit 0.90, batch 65536)",
+            "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main["total_ms"] / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 rows (u64 keys, integer hashing; no FP arithmetic)",
+            "data": "synthetic power-law (alpha 1.2) keys, hash-derived rows",
+            "config": {"workload": "cfg2: 10M-key table, dim 128, cache 20% (31250x2 slabsets), "
+                                   "batch 65536, unique-hit sweep 0.5/0.9/0.99 (headline 0.9)",
+                       "keyspace": wl.keyspace, "dim": d, "slabset_count": wl.S,
+                       "slabs_per_set": wl.W, "batch": n, "target_unique_hit": args.hit,
+                       "parallelism": f"replicas x{world} (no data-path collective)",
+                       "l2": "inputs larger than L2: 1.06 GB table, 32 distinct key batches, "
+                             "outputs rotate over 8 x 33.5 MB"},
+            "p50_batch_latency_us": main["p50_us"], "p99_batch_latency_us": main["p99_us"],
+            "measured_unique_hit_rate": main["h"],
+            "unique_keys_per_batch": main["unique_per_batch"],
+            "slabs_probed_per_unique_key": main["probes_per_unique"],
+            "hit_rate_sweep": sweep,
+            "roofline": {"bound": "hbm", "kernel": "k_lookup_probe", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "algorithmic_bytes_per_launch": main["bytes_per_batch"],
+                         "kernel_us": main["k1_us"],
+                         "frac_of_8tbs_spec": achieved / 8000.0},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": main["launches"],
+        }
+        print(json.dumps(result))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def run_e2e(args, hps, torch, cache, wl, dev, rank, dist):
+    d, n = wl.dim, wl.batch
+    batches, p, _ = wl.batches(args.hit, 32, seed=3000 + rank)
+    vdb = hps.VolatileStore(8)
+    table = hps.TableId("bench", d)
+    vdb.register_table(table, hps.VolatileTableConfig(partition_count=16,
+                                                      overflow_margin=1 << 40))
+    miss_keys = np.unique(np.concatenate([b for b in batches]))
+    miss_keys = miss_keys[~np.isin(miss_keys, wl.R)]
+    for i in range(0, len(miss_keys), 1 << 18):
+        k = miss_keys[i:i + (1 << 18)]
+        vdb.insert("bench", k, table_rows(k, d))
+    eng = hps.LookupEngine(table, cache, vdb, None,
+                           hps.EngineConfig(hit_rate_threshold=0.8, workspace_pool_size=16,
+                                            async_worker_count=2))
+    pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
+    ring = 4
+    po = [torch.empty(n * d).pin_memory() for _ in range(ring)]
+    pf = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(ring)]
+    for s in range(args.warmup):
+        eng.lookup_ptrs(pk[s % 32].data_ptr(), n, po[s % ring].data_ptr(), pf[s % ring].data_ptr(),
+                        hps.HPS_MEM_HOST)
+    eng.drain_async()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    l0 = hps.kernel_launch_count()
+    hs = []
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        o = eng.lookup_ptrs(pk[s % 32].data_ptr(), n, po[s % ring].data_ptr(),
+                            pf[s % ring].data_ptr(), hps.HPS_MEM_HOST)
+        hs.append(o.unique_hit_rate)
+    eng.drain_async()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    launches = hps.kernel_launch_count() - l0
+    if dist:
+        t = torch.tensor([el], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    world = dist.get_world_size() if dist else 1
+    st = eng.stats()
+    eng.close()
+    return {"value": world * args.steps * n / el, "unit": "keys/s",
+            "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * d * 4 + n,
+            "ms_per_step": el * 1e3 / args.steps, "mean_unique_hit_rate": float(np.mean(hs)),
+            "api": "hps_engine_lookup (LookupEngine::lookup), pinned host buffers, "
+                   "threshold 0.8, async VDB fill + replace inside the timed region",
+            "sync_batches": st.sync_batches, "async_batches": st.async_batches,
+            "gpu_launches": launches}
+
+
+# ------------------------------------------------------ reference arm -----
+def ref_session(args, wl, workers):
+    """Reference LookupEngine (oracle/_ref) on the same workload."""
+    import oracle
+
+    d, n = wl.dim, wl.batch
+    eng = oracle.RefEngine(d, S=wl.S, W=wl.W, workers=workers, threshold=0.8, partitions=16)
+    for i in range(0, len(wl.preload), n):
+        k = wl.preload[i:i + n]
+        eng.cache_replace(k, table_rows(k, d))
+    cache_h = oracle.rlib().ref_engine_cache(eng._h)
+    cnt = oracle.rlib().ref_cache_dump_all(cache_h, None, 0)
+    res = np.empty(cnt, dtype=np.uint64)
+    oracle.rlib().ref_cache_dump_all(cache_h, res.ctypes.data, cnt)
+    wl.set_resident(res)
+    return eng
+
+
+def cpu_baseline(args, wl):
+    """Reference LookupEngine on a bounded sample of the same workload
+    (rank 0, N=1): 8 batches of 65,536 keys at the headline hit rate."""
+    try:
+        import oracle
+
+        if not oracle.ref_available():
+            return None
+        cores = os.cpu_count() or 1
+        eng = ref_session(args, wl, cores)
+        batches, _, _ = wl.batches(args.hit, 8, seed=4000)
+        nonres = np.unique(np.concatenate(batches))
+        nonres = nonres[~np.isin(nonres, wl.R)]
+        eng.vdb_insert(nonres, table_rows(nonres, wl.dim))
+        eng.lookup(batches[0])
+        t0 = time.perf_counter()
+        for b in batches:
+            eng.lookup(b)
+        eng.drain()
+        el = time.perf_counter() - t0
+        return {"value": len(batches) * wl.batch / el, "unit": "keys/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"{len(batches)} batches x {wl.batch} keys through the reference "
+                          "LookupEngine (worker_pool_size = cores, threshold 0.8, VDB-backed "
+                          "misses), cfg2 geometry, unique-hit 0.9"}
+    except Exception as e:  # never let the baseline sink the GPU line
+        return {"value": None, "error": str(e)[:200]}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhps_ref.so not built"}))
+        return None
+    wl = Workload(keyspace=args.keyspace, dim=args.dim, cache_frac=args.cache_frac,
+                  batch=args.batch)
+    cores = os.cpu_count() or 1
+    eng = ref_session(args, wl, cores)
+    batches, _, _ = wl.batches(args.hit, 32, seed=3000)
+    nonres = np.unique(np.concatenate(batches))
+    nonres = nonres[~np.isin(nonres, wl.R)]
+    eng.vdb_insert(nonres, table_rows(nonres, wl.dim))
+    for s in range(args.warmup):
+        eng.lookup(batches[s % 32])
+    eng.drain()
+    hs = []
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        _, _, oc = eng.lookup(batches[s % 32])
+        hs.append(oc["unique_hit_rate"])
+    eng.drain()
+    el = time.perf_counter() - t0
+    v = args.steps * wl.batch / el
+    out = {"impl": "reference",
+           "metric": "cache lookup keys/sec (steady-state Query, unique-key hit 0.90, batch 65536)",
+           "value": v, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows (u64 keys)",
+           "data": "synthetic power-law (alpha 1.2) keys, hash-derived rows",
+           "config": {"workload": "cfg2: 10M-key table, dim 128, cache 20% (31250x2 slabsets), "
+                                  "batch 65536, unique-hit 0.9",
+                      "target_unique_hit": args.hit, "parallelism": "CPU reference, rank 0"},
+           "measured_unique_hit_rate": float(np.mean(hs)),
+           "cpu_baseline": {"value": v, "unit": "keys/s", "cores": cores, "kind": "reference",
+                            "sample": f"{args.steps} batches x {wl.batch} keys through the "
+                                      "reference LookupEngine (oracle/_ref), threshold 0.8"},
+           "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--hit", type=float, default=0.9)
+    ap.add_argument("--keyspace", type=int, default=10_000_000)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--cache-frac", type=float, default=0.2)
+    ap.add_argument("--batch", type=int, default=65536)
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -3,7 +3,7 @@
  *
  * This is the drop-in boundary: plain pointers and sizes, no CUDA or torch
  * types in the signatures (streams are passed as `void*` holding a
- * cudaStream_t, NULL = the object's own stream). Every entry point names the
+ * cudaStream_t; NULL = the legacy default stream). Every entry point names the
  * reference interface it replaces (file:line under /root/reference/proj).
  * The C++ shim in include/hps_b200/slab_cache.hpp re-exposes the
  * reference's hps::SlabCache API on top of these calls, and
@@ -54,6 +54,10 @@ typedef struct hps_engine hps_engine;
 
 /* Thread-local message of the last failing call. */
 const char* hps_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process
+ * (diagnostic; bench.py reports it for the timed region). */
+uint64_t hps_kernel_launch_count(void);
 
 /* XXH64; replaces hps::xxh64 / xxh64_key (xxhash64.hpp:60-124). */
 uint64_t hps_xxh64(const void* data, size_t len, uint64_t seed);
@@ -111,6 +115,24 @@ void* hps_cache_stream(hps_cache* cache);
 int hps_cache_query(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
                     size_t out_len, uint32_t* miss_positions, uint64_t* miss_keys,
                     size_t* n_miss, int mem, void* stream);
+
+/* Lookup-level query, device pointers only: the fused hot path of
+ * hps_engine_lookup without the tier logic (LookupEngine::lookup's dedup ->
+ * query -> expand, lookup_engine.cpp:131-153,194-203). Bumps the recency
+ * clock once; out (n * dim) gets every position's row -- the cached row on
+ * a hit, default_row (dim floats, device) on a miss; miss_flags[n] = 1 on a
+ * miss; miss_keys (capacity n) gets the unique missing keys in
+ * first-occurrence order; counts[2] = {unique hits, unique misses} of this
+ * call (so h = 1 - counts[1] / (counts[0] + counts[1])). Stream-ordered:
+ * returns without synchronising. */
+int hps_cache_lookup_device(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
+                            uint8_t* miss_flags, const float* default_row,
+                            uint64_t* miss_keys, uint64_t* counts, void* stream);
+
+/* Diagnostic: record these cudaEvent_t (as void*) on the cache stream right
+ * before / after the probe kernel of subsequent hps_cache_lookup_device
+ * calls; NULL disables. Used by bench.py to time the dominant kernel. */
+int hps_cache_set_profile_events(hps_cache* cache, void* start_event, void* end_event);
 
 /* replaces SlabCache::replace (slab_cache.cpp:93-107). Rejects a wrong
  * vector size or duplicate keys before any mutation. */

@@ -120,6 +120,7 @@ _U64P = C.POINTER(C.c_uint64)
 _SZP = C.POINTER(C.c_size_t)
 SIGNATURES = {
     "hps_last_error": (C.c_char_p, []),
+    "hps_kernel_launch_count": (C.c_uint64, []),
     "hps_xxh64": (C.c_uint64, [_P, C.c_size_t, C.c_uint64]),
     "hps_xxh64_key": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "hps_slabset_of": (C.c_uint64, [C.c_uint64, C.c_uint64]),
@@ -131,6 +132,8 @@ SIGNATURES = {
     "hps_cache_get_info": (C.c_int, [_P, C.POINTER(_CacheInfo)]),
     "hps_cache_stream": (_P, [_P]),
     "hps_cache_query": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P, _SZP, C.c_int, _P]),
+    "hps_cache_lookup_device": (C.c_int, [_P, _P, C.c_size_t, _P, _P, _P, _P, _P, _P]),
+    "hps_cache_set_profile_events": (C.c_int, [_P, _P, _P]),
     "hps_cache_replace": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, C.c_int, _P]),
     "hps_cache_update": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _SZP, C.c_int, _P]),
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
@@ -200,6 +203,11 @@ def _ptr(a: np.ndarray):
 
 
 # ------------------------------------------------------------- vocabulary --
+def kernel_launch_count() -> int:
+    """Kernels launched by libhps_b200 in this process so far."""
+    return int(lib().hps_kernel_launch_count())
+
+
 def xxh64(data: bytes, seed: int = 0) -> int:
     buf = C.create_string_buffer(bytes(data), len(data))
     return int(lib().hps_xxh64(buf, len(data), seed))
@@ -321,6 +329,19 @@ class SlabCache:
                                      miss_keys_ptr, C.byref(nm), HPS_MEM_DEVICE,
                                      stream or None))
         return nm.value
+
+    def lookup_device(self, keys_ptr: int, n: int, out_ptr: int, flags_ptr: int,
+                      default_row_ptr: int, miss_keys_ptr: int, counts_ptr: int,
+                      stream: int = 0) -> None:
+        """hps_cache_lookup_device: the fused lookup hot path on device
+        pointers, stream-ordered (no host sync)."""
+        _check(lib().hps_cache_lookup_device(self._h, keys_ptr, n, out_ptr, flags_ptr,
+                                             default_row_ptr, miss_keys_ptr, counts_ptr,
+                                             stream or None))
+
+    def set_profile_events(self, start_event: int = 0, end_event: int = 0) -> None:
+        _check(lib().hps_cache_set_profile_events(self._h, start_event or None,
+                                                  end_event or None))
 
     def replace(self, keys, vectors) -> None:
         k = _u64(keys)

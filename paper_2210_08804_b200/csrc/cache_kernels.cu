@@ -9,6 +9,7 @@
 //   dedup    core/src/types.cpp:20-34
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -20,7 +21,8 @@ namespace hpsb {
 
 namespace {
 
-inline void check_launch(const char* what) {
+inline void check_launch(const char* what, uint32_t kernels) {
+  note_launches(kernels);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -38,6 +40,10 @@ inline uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 constexpr int kWarpsPerBlock = 8;  // 256-thread blocks for warp-per-key kernels
 
 }  // namespace
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launches(uint32_t kernels) { g_launches.fetch_add(kernels, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 // ------------------------------------------------------------------ scan --
 void scan_begin(ScanState& s, uint64_t tiles, cudaStream_t st) {
@@ -94,7 +100,7 @@ void launch_cache_query(const CacheDev& c, const uint64_t* keys, uint64_t n, flo
     case 2: k_cache_query<2><<<grid, block, 0, st>>>(c, keys, n, out, hit, stamp); break;
     default: k_cache_query<1><<<grid, block, 0, st>>>(c, keys, n, out, hit, stamp); break;
   }
-  check_launch("cache_query");
+  check_launch("cache_query", 1);
 }
 
 __global__ void __launch_bounds__(kScanBlock)
@@ -123,7 +129,7 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
   k_select_misses<<<unsigned(tiles), kScanBlock, 0, st>>>(keys, hit, n, miss_pos, miss_keys,
                                                           n_miss, scan);
   scan.tile_base += tiles;
-  check_launch("select_misses");
+  check_launch("select_misses", 1);
 }
 
 // ---------------------------------------------------------------- replace --
@@ -337,7 +343,7 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
   }
   k_replace_apply<<<unsigned((warp_threads + tb - 1) / tb), tb, 0, st>>>(c, keys, rows, stamp,
                                                                           rs);
-  check_launch("replace");
+  check_launch("replace", validate ? 5 : 4);
 }
 
 // ----------------------------------------------------------------- update --
@@ -427,7 +433,7 @@ void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const fl
   }
   const uint64_t threads = n * 32;
   k_update_write<<<unsigned((threads + 255) / 256), 256, 0, st>>>(c, rows, n, us);
-  check_launch("update");
+  check_launch("update", 2);
 }
 
 // ------------------------------------------------------------------- dump --
@@ -488,7 +494,7 @@ void launch_dump(const CacheDev& c, uint64_t set_begin, uint64_t set_end, uint64
   k_dump_keys<<<unsigned(tiles), kScanBlock, 0, st>>>(c, set_begin * c.W, n_slabs, out, n_out,
                                                       scan);
   scan.tile_base += tiles;
-  check_launch("dump");
+  check_launch("dump", 1);
 }
 
 // ------------------------------------------------------------------ dedup --
@@ -532,7 +538,7 @@ void launch_dedup(const uint64_t* keys, uint64_t n, uint64_t* unique_out, uint32
   k_dedup_compact<<<unsigned(tiles), kScanBlock, 0, st>>>(keys, n, ds, unique_out, scan);
   scan.tile_base += tiles;
   k_dedup_inverse<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(n, ds, inverse);
-  check_launch("dedup");
+  check_launch("dedup", 3);
 }
 
 }  // namespace hpsb

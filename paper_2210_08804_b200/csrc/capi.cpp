@@ -54,7 +54,11 @@ void need(bool ok, const char* what) {
   if (!ok) throw hpsb::invalid_argument(what);
 }
 
-inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+// NULL = the legacy default stream: device-mode work is ordered after it
+// (and the caller's later default-stream work after ours).
+inline cudaStream_t as_stream(void* s) {
+  return s ? static_cast<cudaStream_t>(s) : cudaStreamLegacy;
+}
 
 // Process-wide per-device context for the stateless dedup entry point.
 struct DedupContext {
@@ -65,6 +69,7 @@ struct DedupContext {
   hpsb::ScanState scan;
   uint32_t epoch = 0;
   uint64_t cap = 0;
+  void* last_base = nullptr;
 };
 std::mutex g_dedup_mu;
 std::map<int, std::unique_ptr<DedupContext>> g_dedup;
@@ -84,6 +89,8 @@ DedupContext& dedup_ctx(int device) {
 extern "C" {
 
 const char* hps_last_error(void) { return g_error.c_str(); }
+
+uint64_t hps_kernel_launch_count(void) { return hpsb::launch_count(); }
 
 uint64_t hps_xxh64_key(uint64_t key, uint64_t seed) { return hpsb::xxh64_key(key, seed); }
 
@@ -170,12 +177,15 @@ int hps_dedup_keys(int device, const uint64_t* keys, size_t n, uint64_t* unique_
     }
     uint64_t tcap = 16;
     while (tcap < 2 * n) tcap <<= 1;
-    const uint64_t tiles = (n + hpsb::kScanTile - 1) / hpsb::kScanTile;
+    // regions that persist across calls depend only on tcap and come first,
+    // so their epoch-tagged contents never move between calls
+    const uint64_t tiles = (tcap / 2 + hpsb::kScanTile - 1) / hpsb::kScanTile;
     auto a = [](uint64_t v) { return (v + 255) / 256 * 256; };
     const bool host = mem == HPS_MEM_HOST;
-    const uint64_t bytes = a(tcap * 8) + a(n * 4) + a(tcap * 4) + a(8) + a(tiles * 8) + a(8) +
-                           (host ? a(n * 8) * 2 + a(n * 4) : 0);
-    const bool grow = bytes > c.dbuf.size() || tcap != c.cap;
+    const uint64_t fixed = a(tcap * 8) + a(tcap * 4) + a(8) + a(tiles * 8) + a(8);
+    const uint64_t bytes = fixed + a(n * 4) + (host ? a(n * 8) * 2 + a(n * 4) : 0);
+    if (tcap != c.cap) c.cap = 0;
+    const bool fresh = c.cap == 0;
     char* p = static_cast<char*>(c.dbuf.ensure(bytes, c.stream));
     auto take = [&](uint64_t b) {
       char* r = p;
@@ -185,19 +195,20 @@ int hps_dedup_keys(int device, const uint64_t* keys, size_t n, uint64_t* unique_
     hpsb::DedupScratch ds;
     ds.cap = tcap;
     ds.table = reinterpret_cast<uint64_t*>(take(tcap * 8));
-    ds.slot_of = reinterpret_cast<uint32_t*>(take(n * 4));
     ds.rank_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
     ds.n_unique = reinterpret_cast<unsigned long long*>(take(8));
     c.scan.status = reinterpret_cast<uint64_t*>(take(tiles * 8));
     c.scan.tile_ctr = reinterpret_cast<unsigned long long*>(take(8));
     c.scan.capacity_tiles = tiles;
-    if (grow) {
-      // fresh carve: clear everything once and restart the epochs
-      HPSB_CUDA(cudaMemsetAsync(c.dbuf.get(), 0, c.dbuf.size(), c.stream));
+    ds.slot_of = reinterpret_cast<uint32_t*>(take(n * 4));
+    if (fresh || c.dbuf.get() != c.last_base) {
+      // new carve: clear the persistent regions once and restart the epochs
+      HPSB_CUDA(cudaMemsetAsync(c.dbuf.get(), 0, fixed, c.stream));
       c.scan.tile_base = 0;
       c.scan.epoch = 0;
       c.epoch = 0;
       c.cap = tcap;
+      c.last_base = c.dbuf.get();
     }
     if (++c.epoch == 0) {
       HPSB_CUDA(cudaMemsetAsync(ds.table, 0, tcap * 8, c.stream));
@@ -212,7 +223,7 @@ int hps_dedup_keys(int device, const uint64_t* keys, size_t n, uint64_t* unique_
       d_inv = reinterpret_cast<uint32_t*>(take(n * 4));
       HPSB_CUDA(cudaMemcpyAsync(k, keys, n * 8, cudaMemcpyHostToDevice, c.stream));
       d_keys = k;
-    } else if (stream) {
+    } else {
       cudaEvent_t ev;
       HPSB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       HPSB_CUDA(cudaEventRecord(ev, as_stream(stream)));
@@ -277,6 +288,25 @@ int hps_cache_query(hps_cache* cache, const uint64_t* keys, size_t n, float* out
     need(cache && n_miss, "null argument");
     *n_miss = cache->impl->query(keys, n, out, out_len, miss_positions, miss_keys, mem,
                                  as_stream(stream));
+  });
+}
+
+int hps_cache_lookup_device(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
+                            uint8_t* miss_flags, const float* default_row, uint64_t* miss_keys,
+                            uint64_t* counts, void* stream) {
+  return guarded([&] {
+    need(cache && counts, "null argument");
+    need(n == 0 || (keys && out && miss_flags && default_row && miss_keys), "null argument");
+    cache->impl->lookup_device(keys, n, out, miss_flags, default_row, miss_keys, counts,
+                               as_stream(stream));
+  });
+}
+
+int hps_cache_set_profile_events(hps_cache* cache, void* start_event, void* end_event) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    cache->impl->set_profile_events(static_cast<cudaEvent_t>(start_event),
+                                    static_cast<cudaEvent_t>(end_event));
   });
 }
 

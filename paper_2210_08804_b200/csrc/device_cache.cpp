@@ -169,6 +169,60 @@ size_t DeviceCache::query(const uint64_t* keys, size_t n, float* out, size_t out
   return n_miss;
 }
 
+void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint8_t* flags,
+                                const float* default_row, uint64_t* miss_keys, uint64_t* counts,
+                                cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  const uint64_t stamp = bump_clock();
+  DeviceGuard g(device_);
+  join_from(user);
+  if (n == 0) {
+    HPSB_CUDA(cudaMemsetAsync(counts, 0, 16, stream_));
+    join_to(user);
+    return;
+  }
+  if (n >= (1ull << 32)) throw invalid_argument("lookup batch too large");
+  if (n > lcap_) {
+    // (re)carve: miss table >= 2n entries, per-position slots, scan state
+    uint64_t cap = 1024;
+    while (cap < n) cap <<= 1;
+    uint64_t tcap = 16;
+    while (tcap < 2 * cap) tcap <<= 1;
+    const uint64_t tiles = (cap + kScanTile - 1) / kScanTile;
+    const uint64_t bytes = align256(tcap * 8) + align256(tcap * 4) + align256(cap * 4) +
+                           align256(64) + align256(tiles * 8) + align256(8);
+    Carver cv{static_cast<char*>(lbuf_.ensure(bytes, stream_))};
+    lws_ = LookupScratch{};
+    lws_.cap = tcap;
+    lws_.miss_table = cv.take<uint64_t>(tcap);
+    lws_.rank_of_slot = cv.take<uint32_t>(tcap);
+    lws_.miss_slot = cv.take<uint32_t>(cap);
+    unsigned long long* small = cv.take<unsigned long long>(8);
+    lws_.counts = small;
+    lws_.counts_prev = small + 2;
+    lscan_.status = cv.take<uint64_t>(tiles);
+    lscan_.tile_ctr = cv.take<unsigned long long>(1);
+    lscan_.capacity_tiles = tiles;
+    lscan_.tile_base = 0;
+    lscan_.epoch = 0;
+    HPSB_CUDA(cudaMemsetAsync(lbuf_.get(), 0, bytes, stream_));
+    lepoch_ = 0;
+    lcap_ = cap;
+  }
+  if (++lepoch_ == 0) {
+    HPSB_CUDA(cudaMemsetAsync(lws_.miss_table, 0, lws_.cap * 8, stream_));
+    lepoch_ = 1;
+  }
+  LookupScratch ls = lws_;
+  ls.miss_keys = miss_keys;
+  ls.counts_out = reinterpret_cast<unsigned long long*>(counts);
+  if (prof_start_) HPSB_CUDA(cudaEventRecord(prof_start_, stream_));
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, lepoch_, stream_);
+  if (prof_end_) HPSB_CUDA(cudaEventRecord(prof_end_, stream_));
+  launch_lookup_compact(keys, n, flags, ls, lepoch_, lscan_, stream_);
+  join_to(user);
+}
+
 void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
                           size_t vectors_len, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);

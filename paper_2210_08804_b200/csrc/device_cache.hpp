@@ -46,6 +46,20 @@ class DeviceCache {
   // slab_cache.cpp:109-125
   size_t update(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
                 int mem, cudaStream_t user);
+  // Lookup-level query on device pointers (the engine's fused hot path
+  // without the tier logic): bumps the clock, writes every position's row
+  // (hit: cached row, miss: default_row), miss flags, the unique misses in
+  // first-occurrence order and {unique hits, unique misses} of this call to
+  // device memory. Stream-ordered, no host synchronisation.
+  void lookup_device(const uint64_t* keys, size_t n, float* out, uint8_t* flags,
+                     const float* default_row, uint64_t* miss_keys, uint64_t* counts,
+                     cudaStream_t user);
+  // Diagnostic: events recorded around the probe kernel of the next
+  // lookup_device calls (null = off).
+  void set_profile_events(cudaEvent_t start, cudaEvent_t end) {
+    prof_start_ = start;
+    prof_end_ = end;
+  }
   // DumpCursor::next over a slabset range (host output)
   size_t dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, size_t cap);
   // slab_cache.cpp:407-442
@@ -92,6 +106,13 @@ class DeviceCache {
   DeviceBuffer scratch_;
   DeviceBuffer scratch2_;
   PinnedBuffer pinned_;
+  // lookup_device scratch
+  DeviceBuffer lbuf_;
+  LookupScratch lws_;
+  ScanState lscan_;
+  uint32_t lepoch_ = 0;
+  uint64_t lcap_ = 0;
+  cudaEvent_t prof_start_ = nullptr, prof_end_ = nullptr;
   unsigned long long* d_small_ = nullptr;  // small device counters
   unsigned long long* h_small_ = nullptr;  // pinned mirror
 };

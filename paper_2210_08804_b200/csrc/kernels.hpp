@@ -8,6 +8,11 @@
 
 namespace hpsb {
 
+// Process-wide count of kernels launched by this library (bench.py reports
+// it as gpu_launches for the timed region).
+void note_launches(uint32_t kernels);
+uint64_t launch_count();
+
 // Look-back scan state of one serialised user (a cache or a workspace).
 struct ScanState {
   uint64_t* status = nullptr;             // one word per tile
@@ -85,6 +90,10 @@ struct LookupScratch {
   uint32_t* rank_of_slot = nullptr;
   unsigned long long* counts = nullptr;  // [0] unique hits, [1] unique misses (cumulative)
   uint64_t* miss_keys = nullptr;  // unique misses, first-occurrence order
+  // optional per-call deltas written by the compaction kernel:
+  // counts_out = counts - counts_prev; counts_prev = counts
+  unsigned long long* counts_prev = nullptr;
+  unsigned long long* counts_out = nullptr;
 };
 void launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                          uint8_t* flags, const float* default_row, uint64_t stamp,

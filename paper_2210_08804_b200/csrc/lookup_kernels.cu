@@ -32,7 +32,8 @@
 namespace hpsb {
 
 namespace {
-inline void check_launch(const char* what) {
+inline void check_launch(const char* what, uint32_t kernels) {
+  note_launches(kernels);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -155,12 +156,18 @@ void launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, fl
   const unsigned grid = unsigned((warps + kLookupWarps - 1) / kLookupWarps);
   k_lookup_probe<P><<<grid, kLookupWarps * 32, 0, st>>>(c, keys, n, out, flags, default_row,
                                                         stamp, ls, table_epoch);
-  check_launch("lookup_probe");
+  check_launch("lookup_probe", 1);
 }
 
 __global__ void __launch_bounds__(kScanBlock)
     k_lookup_compact(const uint64_t* __restrict__ keys, uint64_t n,
                      const uint8_t* __restrict__ flags, LookupScratch ls, ScanState scan) {
+  if (ls.counts_out != nullptr && blockIdx.x == 0 && threadIdx.x < 2) {
+    // K1 has fully completed (stream order): publish this call's counts
+    const unsigned long long cum = ls.counts[threadIdx.x];
+    ls.counts_out[threadIdx.x] = cum - ls.counts_prev[threadIdx.x];
+    ls.counts_prev[threadIdx.x] = cum;
+  }
   select_tile(
       n, scan,
       [&](uint64_t i) {
@@ -182,7 +189,7 @@ void launch_lookup_compact(const uint64_t* keys, uint64_t n, const uint8_t* flag
   scan_begin(scan, tiles, st);
   k_lookup_compact<<<unsigned(tiles), kScanBlock, 0, st>>>(keys, n, flags, ls, scan);
   scan.tile_base += tiles;
-  check_launch("lookup_compact");
+  check_launch("lookup_compact", 1);
 }
 
 __global__ void __launch_bounds__(256)
@@ -208,7 +215,7 @@ void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint
   const uint64_t threads = n * 32;
   k_lookup_scatter<<<unsigned((threads + 255) / 256), 256, 0, st>>>(n, d, flags, ls, row_of,
                                                                     staged, out);
-  check_launch("lookup_scatter");
+  check_launch("lookup_scatter", 1);
 }
 
 }  // namespace hpsb
