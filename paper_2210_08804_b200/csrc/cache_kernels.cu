@@ -170,7 +170,7 @@ __global__ void k_replace_group(CacheDev c, const uint64_t* __restrict__ keys, u
                                 ReplaceScratch rs) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t s = xxh64_key(keys[i], kSlabsetSeed) % c.S;
+  const uint64_t s = slabset_of(c, keys[i]);
   uint64_t t = fmix64(s) & (rs.cap - 1);
   while (true) {
     const unsigned long long old =
@@ -258,7 +258,7 @@ __global__ void k_replace_apply(CacheDev c, const uint64_t* __restrict__ keys,
   for (uint32_t g = 0; g < cnt; ++g) {
     const uint32_t i = b[g];
     const uint64_t key = keys[i];
-    const uint32_t first = uint32_t(xxh64_key(key, kSlabSeed) % c.W);
+    const uint32_t first = first_slab_of(c, key);
     int64_t found = -1;
     int64_t ins_slab = -1;
     for (uint32_t step = 0; step < c.W; ++step) {

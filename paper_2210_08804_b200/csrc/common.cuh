@@ -68,7 +68,30 @@ struct CacheDev {
   uint64_t S;
   uint32_t W;
   uint32_t d;
+  uint64_t mS;  // floor((2^64 - 1) / S): Barrett reciprocal for h % S
+  uint64_t mW;  // same for W
 };
+
+// h % m without a 64-bit divide: q = mulhi(h, floor((2^64-1)/m)) is at most
+// two below floor(h / m), so at most two corrections.
+__host__ __device__ __forceinline__ uint64_t fastmod(uint64_t h, uint64_t m, uint64_t recip) {
+#ifdef __CUDA_ARCH__
+  const uint64_t q = __umul64hi(h, recip);
+#else
+  const uint64_t q = uint64_t((unsigned __int128)h * recip >> 64);
+#endif
+  uint64_t r = h - q * m;
+  if (r >= m) r -= m;
+  if (r >= m) r -= m;
+  return r;
+}
+
+__host__ __device__ __forceinline__ uint64_t slabset_of(const CacheDev& c, uint64_t key) {
+  return fastmod(xxh64_key(key, kSlabsetSeed), c.S, c.mS);
+}
+__host__ __device__ __forceinline__ uint32_t first_slab_of(const CacheDev& c, uint64_t key) {
+  return uint32_t(fastmod(xxh64_key(key, kSlabSeed), c.W, c.mW));
+}
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 

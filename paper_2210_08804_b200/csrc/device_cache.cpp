@@ -47,6 +47,8 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device
   dev_.S = cfg.slabset_count;
   dev_.W = cfg.slabs_per_set;
   dev_.d = cfg.dimension;
+  dev_.mS = ~0ull / cfg.slabset_count;
+  dev_.mW = ~0ull / cfg.slabs_per_set;
   HPSB_CUDA(cudaMalloc(&dev_.keys, slots * 8));
   HPSB_CUDA(cudaMalloc(&dev_.counters, slots * 8));
   HPSB_CUDA(cudaMalloc(&dev_.masks, slabs * 4));
@@ -183,29 +185,14 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   }
   if (n >= (1ull << 32)) throw invalid_argument("lookup batch too large");
   if (n > lcap_) {
-    // (re)carve: miss table >= 2n entries, per-position slots, scan state
+    // (re)carve: miss table >= 2n entries, per-position slots, miss list,
+    // ordering bitmap, counters -- zeroed once, then kept clean by the kernel
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
-    uint64_t tcap = 16;
-    while (tcap < 2 * cap) tcap <<= 1;
-    const uint64_t tiles = (cap + kScanTile - 1) / kScanTile;
-    const uint64_t bytes = align256(tcap * 8) + align256(tcap * 4) + align256(cap * 4) +
-                           align256(64) + align256(tiles * 8) + align256(8);
-    Carver cv{static_cast<char*>(lbuf_.ensure(bytes, stream_))};
-    lws_ = LookupScratch{};
-    lws_.cap = tcap;
-    lws_.miss_table = cv.take<uint64_t>(tcap);
-    lws_.rank_of_slot = cv.take<uint32_t>(tcap);
-    lws_.miss_slot = cv.take<uint32_t>(cap);
-    unsigned long long* small = cv.take<unsigned long long>(8);
-    lws_.counts = small;
-    lws_.counts_prev = small + 2;
-    lscan_.status = cv.take<uint64_t>(tiles);
-    lscan_.tile_ctr = cv.take<unsigned long long>(1);
-    lscan_.capacity_tiles = tiles;
-    lscan_.tile_base = 0;
-    lscan_.epoch = 0;
-    HPSB_CUDA(cudaMemsetAsync(lbuf_.get(), 0, bytes, stream_));
+    const uint64_t bytes = lookup_scratch_bytes(cap);
+    void* b = lbuf_.ensure(bytes, stream_);
+    HPSB_CUDA(cudaMemsetAsync(b, 0, bytes, stream_));
+    lws_ = lookup_scratch_carve(b, cap);
     lepoch_ = 0;
     lcap_ = cap;
   }
@@ -217,9 +204,9 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   ls.miss_keys = miss_keys;
   ls.counts_out = reinterpret_cast<unsigned long long*>(counts);
   if (prof_start_) HPSB_CUDA(cudaEventRecord(prof_start_, stream_));
-  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, lepoch_, stream_);
+  lws_.blocks_base +=
+      launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, lepoch_, stream_);
   if (prof_end_) HPSB_CUDA(cudaEventRecord(prof_end_, stream_));
-  launch_lookup_compact(keys, n, flags, ls, lepoch_, lscan_, stream_);
   join_to(user);
 }
 

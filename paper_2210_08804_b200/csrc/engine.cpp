@@ -105,12 +105,9 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   if (n <= capacity && d == dim && dbuf.get() != nullptr) return;
   uint64_t cap = 1024;
   while (cap < n) cap <<= 1;
-  uint64_t tcap = 16;
-  while (tcap < 2 * cap) tcap <<= 1;
-  const uint64_t tiles = (cap + kScanTile - 1) / kScanTile;
+  const uint64_t ls_bytes = lookup_scratch_bytes(cap);
   const uint64_t dev_bytes = a256(cap * 8) * 3 + a256(cap * uint64_t(d) * 4) * 2 + a256(cap) +
-                             a256(cap * 4) * 2 + a256(tcap * 8) + a256(tcap * 4) + a256(16) +
-                             a256(tiles * 8) + a256(8);
+                             a256(cap * 4) + a256(ls_bytes);
   HPSB_CUDA(cudaStreamSynchronize(st));
   char* p = static_cast<char*>(dbuf.ensure(dev_bytes, st));
   auto take = [&](uint64_t bytes) {
@@ -124,21 +121,11 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   d_row_of = reinterpret_cast<int32_t*>(take(cap * 4));
   d_staged = reinterpret_cast<float*>(take(cap * uint64_t(d) * 4));
   d_found_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
-  ls.cap = tcap;
-  ls.miss_table = reinterpret_cast<uint64_t*>(take(tcap * 8));
-  ls.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
-  ls.rank_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
-  ls.counts = reinterpret_cast<unsigned long long*>(take(16));
-  ls.miss_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
-  scan.status = reinterpret_cast<uint64_t*>(take(tiles * 8));
-  scan.tile_ctr = reinterpret_cast<unsigned long long*>(take(8));
-  scan.capacity_tiles = tiles;
-  scan.tile_base = 0;
-  scan.epoch = 0;
-  HPSB_CUDA(cudaMemsetAsync(ls.miss_table, 0, tcap * 8, st));
-  HPSB_CUDA(cudaMemsetAsync(ls.counts, 0, 16, st));
-  HPSB_CUDA(cudaMemsetAsync(scan.status, 0, tiles * 8, st));
-  HPSB_CUDA(cudaMemsetAsync(scan.tile_ctr, 0, 8, st));
+  uint64_t* d_miss_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  char* ls_base = take(ls_bytes);
+  HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
+  ls = lookup_scratch_carve(ls_base, cap);
+  ls.miss_keys = d_miss_keys;
   table_epoch = 0;
   prev_counts[0] = prev_counts[1] = 0;
 
@@ -297,9 +284,8 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
         HPSB_CUDA(cudaMemsetAsync(ws->ls.miss_table, 0, ws->ls.cap * 8, st));
         ws->table_epoch = 1;
       }
-      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->ls,
-                          ws->table_epoch, st);
-      launch_lookup_compact(d_keys, n, d_flags, ws->ls, ws->table_epoch, ws->scan, st);
+      ws->ls.blocks_base += launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags,
+                                                d_default_, stamp, ws->ls, ws->table_epoch, st);
       HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts, 16, cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }

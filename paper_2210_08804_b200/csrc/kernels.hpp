@@ -90,17 +90,29 @@ struct LookupScratch {
   uint32_t* rank_of_slot = nullptr;
   unsigned long long* counts = nullptr;  // [0] unique hits, [1] unique misses (cumulative)
   uint64_t* miss_keys = nullptr;  // unique misses, first-occurrence order
-  // optional per-call deltas written by the compaction kernel:
+  // optional per-call deltas written by the ordering tail:
   // counts_out = counts - counts_prev; counts_prev = counts
   unsigned long long* counts_prev = nullptr;
   unsigned long long* counts_out = nullptr;
+  // unique-miss ordering (fused tail of the probe kernel)
+  uint32_t* list = nullptr;         // miss-table slots claimed this call (capacity n)
+  uint32_t* list_firsts = nullptr;  // their first positions (capacity n)
+  uint32_t* list_ctr = nullptr;     // 1 word, left at 0 by the tail
+  uint32_t* bitmap = nullptr;       // ceil(n/32) words, left zeroed by the tail
+  uint32_t* word_prefix = nullptr;  // ceil(n/32) words
+  unsigned long long* blocks_done = nullptr;  // cumulative block-completion counter
+  unsigned long long blocks_base = 0;         // host: blocks launched before this call
 };
-void launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
-                         uint8_t* flags, const float* default_row, uint64_t stamp,
-                         const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st);
-void launch_lookup_compact(const uint64_t* keys, uint64_t n, const uint8_t* flags,
-                           const LookupScratch& ls, uint32_t table_epoch, ScanState& scan,
-                           cudaStream_t st);
+// Bytes / carving of a LookupScratch for batches of up to `cap` keys (all
+// regions zero-initialised by the caller once).
+size_t lookup_scratch_bytes(uint64_t cap);
+LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
+// One launch per lookup: probe + gather + stamps + miss dedup, and the last
+// block to finish orders the unique misses. Returns the grid size (the
+// caller adds it to ls.blocks_base for the next call).
+unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
+                             uint8_t* flags, const float* default_row, uint64_t stamp,
+                             const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st);
 void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint8_t* flags,
                            const LookupScratch& ls, const int32_t* row_of,
                            const float* staged, float* out, cudaStream_t st);

@@ -1,25 +1,26 @@
 // lookup_kernels.cu -- the fused lookup hot path (sm_100a).
 //
 // Restates LookupEngine::lookup (lookup_engine.cpp:130-241) for a batch of
-// |Q| query positions without materialising the dedup step for hits:
+// |Q| query positions in ONE kernel launch, without materialising the dedup
+// step for hits:
 //
-//   K1 lookup_probe   one warp per P positions: placement hash, ballot probe
-//                     of 32-key slabs, 128-bit gather of the hit row straight
-//                     into the position's output row (the expansion of
-//                     lookup_engine.cpp:194-203 is fused), recency stamp via
-//                     atomicExch -- the exchange that first moves a slot to
-//                     this call's stamp counts one UNIQUE hit, so |Q*| needs
-//                     no dedup of hits. Missing positions get the default row
-//                     (the async branch's answer) and are deduplicated in a
-//                     per-call hash table keeping the first occurrence.
-//   K2 lookup_compact ordered single-pass compaction of the first occurrences
-//                     of missing keys -> the unique miss list in
-//                     first-occurrence order (= reference order of
-//                     CacheMiss after dedup, slab_cache.cpp:84-89), plus the
-//                     rank of every miss-table entry.
-//   K3 lookup_scatter (sync branch only) copies the rows fetched from the
-//                     tiers into every position of their key, clearing the
-//                     default flag (lookup_engine.cpp:165-181).
+//   body  one warp per P positions: placement hash (Barrett modulo), ballot
+//         probe of 32-key slabs, 128-bit gather of the hit row straight into
+//         the position's output row (the expansion of lookup_engine.cpp:
+//         194-203 is fused), recency stamp via atomicExch -- the exchange
+//         that first moves a slot to this call's stamp counts one UNIQUE hit,
+//         so |Q*| needs no dedup of hits. Missing positions get the default
+//         row (the async branch's answer) and are deduplicated in a per-call
+//         hash table that keeps the first occurrence; the claiming position
+//         of every missing key appends the table slot to a short list.
+//   tail  the last block to finish (threadfence + completion counter) orders
+//         the unique misses by first occurrence with a position bitmap and a
+//         block scan -> the unique miss list in first-occurrence order (the
+//         order the reference's dedup + query produce, slab_cache.cpp:84-89)
+//         and the rank of every miss-table entry.
+//   K3    lookup_scatter (sync branch only) copies the rows fetched from the
+//         tiers into every position of their key, clearing the default flag
+//         (lookup_engine.cpp:165-181).
 #include <cuda_runtime.h>
 
 #include <stdexcept>
@@ -39,8 +40,44 @@ inline void check_launch(const char* what, uint32_t kernels) {
     throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
   }
 }
+inline uint64_t a256(uint64_t v) { return (v + 255) / 256 * 256; }
 constexpr int kLookupWarps = 8;
+constexpr int kLookupThreads = kLookupWarps * 32;
 }  // namespace
+
+size_t lookup_scratch_bytes(uint64_t cap) {
+  uint64_t tcap = 16;
+  while (tcap < 2 * cap) tcap <<= 1;
+  const uint64_t words = (cap + 31) / 32;
+  return a256(tcap * 8) + a256(tcap * 4) + a256(cap * 4) * 3 + a256(words * 4) * 2 + a256(64);
+}
+
+LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
+  LookupScratch ls;
+  uint64_t tcap = 16;
+  while (tcap < 2 * cap) tcap <<= 1;
+  const uint64_t words = (cap + 31) / 32;
+  char* p = static_cast<char*>(base);
+  auto take = [&](uint64_t b) {
+    char* r = p;
+    p += a256(b);
+    return r;
+  };
+  ls.cap = tcap;
+  ls.miss_table = reinterpret_cast<uint64_t*>(take(tcap * 8));
+  ls.rank_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
+  ls.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
+  ls.list = reinterpret_cast<uint32_t*>(take(cap * 4));
+  ls.list_firsts = reinterpret_cast<uint32_t*>(take(cap * 4));
+  ls.bitmap = reinterpret_cast<uint32_t*>(take(words * 4));
+  ls.word_prefix = reinterpret_cast<uint32_t*>(take(words * 4));
+  unsigned long long* small = reinterpret_cast<unsigned long long*>(take(64));
+  ls.counts = small;           // [0..1]
+  ls.counts_prev = small + 2;  // [2..3]
+  ls.blocks_done = small + 4;  // [4]
+  ls.list_ctr = reinterpret_cast<uint32_t*>(small + 5);
+  return ls;
+}
 
 __device__ __forceinline__ float4 ld_nc_f4(const float4* p) {
   float4 r;
@@ -55,24 +92,87 @@ __device__ __forceinline__ void st_cs_f4(float4* p, const float4& v) {
                : "memory");
 }
 
+// Orders the unique misses of this call by first occurrence (run by the
+// last block). list[e] = miss-table slot claimed by some position of a
+// missing key; the table entry's low word is that key's first position.
+__device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys, uint64_t n,
+                                               const LookupScratch& ls) {
+  __shared__ uint32_t s_warp[kLookupWarps];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t m = __ldcg(ls.list_ctr);
+  for (uint32_t e = tid; e < m; e += kLookupThreads) {
+    const uint32_t slot = __ldcg(ls.list + e);
+    const uint32_t f = uint32_t(__ldcg(reinterpret_cast<const unsigned long long*>(ls.miss_table) + slot));
+    ls.list_firsts[e] = f;
+    atomicOr(ls.bitmap + (f >> 5), 1u << (f & 31u));
+  }
+  __syncthreads();
+  const uint32_t words = uint32_t((n + 31) / 32);
+  const uint32_t per = (words + kLookupThreads - 1) / kLookupThreads;
+  const uint32_t w0 = min(words, tid * per), w1 = min(words, w0 + per);
+  uint32_t cnt = 0;
+  for (uint32_t w = w0; w < w1; ++w) cnt += __popc(__ldcg(ls.bitmap + w));
+  uint32_t total;
+  uint32_t run = block_exclusive_scan<kLookupThreads>(cnt, s_warp, &total);
+  for (uint32_t w = w0; w < w1; ++w) {
+    ls.word_prefix[w] = run;
+    run += __popc(__ldcg(ls.bitmap + w));
+  }
+  __syncthreads();
+  for (uint32_t e = tid; e < m; e += kLookupThreads) {
+    const uint32_t f = __ldcg(ls.list_firsts + e);
+    const uint32_t w = f >> 5;
+    const uint32_t r =
+        __ldcg(ls.word_prefix + w) + __popc(__ldcg(ls.bitmap + w) & ((1u << (f & 31u)) - 1u));
+    ls.miss_keys[r] = keys[f];
+    ls.rank_of_slot[__ldcg(ls.list + e)] = r;
+  }
+  __syncthreads();
+  for (uint32_t w = w0; w < w1; ++w) ls.bitmap[w] = 0;
+  if (tid == 0) *ls.list_ctr = 0;
+  if (ls.counts_out != nullptr && tid < 2) {
+    const unsigned long long cum = __ldcg(ls.counts + tid);
+    ls.counts_out[tid] = cum - ls.counts_prev[tid];
+    ls.counts_prev[tid] = cum;
+  }
+}
+
 template <int P>
-__global__ void __launch_bounds__(kLookupWarps * 32)
+__global__ void __launch_bounds__(kLookupThreads, 4)
     k_lookup_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                    float* __restrict__ out, uint8_t* __restrict__ flags,
                    const float* __restrict__ default_row, uint64_t stamp, LookupScratch ls,
                    uint32_t epoch) {
   __shared__ unsigned int s_counts[2];
+  __shared__ bool s_last;
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
   __syncthreads();
   const uint64_t warp = (uint64_t(blockIdx.x) * kLookupWarps) + (threadIdx.x >> 5);
   const uint64_t base = warp * P;
   const uint32_t lane = lane_id();
   uint32_t uh = 0, um = 0;
+  bool miss_work = false;
   if (base < n) {
     WarpKeys<P> wk;
     warp_load_keys<P>(c, keys, base, n, wk);
     int64_t slot[P];
     warp_probe<P>(c, wk, slot);
+    // lane p owns position base + p for the bookkeeping
+    int64_t my_slot = -1;
+    uint64_t my_key = 0;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (uint32_t(p) == lane) {
+        my_slot = slot[p];
+        my_key = wk.key[p];
+      }
+    }
+    const uint64_t i = base + lane;
+    const bool mine = lane < uint32_t(P) && i < n;
+    // issue the recency exchange now; its result is consumed at the end
+    unsigned long long old = stamp;
+    if (mine && my_slot >= 0)
+      old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + my_slot), stamp);
     const uint32_t d = c.d;
     if ((d & 3u) == 0) {
       // 128-bit path: the first 32 float4 chunks of every row are loaded for
@@ -108,28 +208,29 @@ __global__ void __launch_bounds__(kLookupWarps * 32)
         for (uint32_t ch = lane; ch < d; ch += 32) out[(base + p) * d + ch] = src[ch];
       }
     }
-    // bookkeeping: lane p owns position base + p
-    if (lane < uint32_t(P)) {
-      int64_t my_slot = -1;
-#pragma unroll
-      for (int p = 0; p < P; ++p)
-        if (uint32_t(p) == lane) my_slot = slot[p];
-      const uint64_t i = base + lane;
-      if (i < n) {
-        if (my_slot >= 0) {
-          const unsigned long long old = atomicExch(
-              reinterpret_cast<unsigned long long*>(c.counters + my_slot), stamp);
-          uh += (old != stamp) ? 1u : 0u;
-          flags[i] = 0;
-        } else {
-          bool claimed;
-          ls.miss_slot[i] =
-              dedup_insert(ls.miss_table, ls.cap, keys, keys[i], uint32_t(i), epoch, &claimed);
-          um += claimed ? 1u : 0u;
-          flags[i] = 1;
-        }
+    bool claimed = false;
+    uint32_t tslot = 0;
+    if (mine) {
+      if (my_slot >= 0) {
+        flags[i] = 0;
+      } else {
+        tslot = dedup_insert(ls.miss_table, ls.cap, keys, my_key, uint32_t(i), epoch, &claimed);
+        ls.miss_slot[i] = tslot;
+        flags[i] = 1;
+        miss_work = true;
       }
     }
+    // claimers append their table slot (one warp-aggregated atomic)
+    const uint32_t cm = __ballot_sync(0xFFFFFFFFu, claimed);
+    if (cm) {
+      const uint32_t leader = __ffs(cm) - 1;
+      uint32_t at = 0;
+      if (lane == leader) at = atomicAdd(ls.list_ctr, uint32_t(__popc(cm)));
+      at = __shfl_sync(0xFFFFFFFFu, at, leader);
+      if (claimed) ls.list[at + __popc(cm & ((1u << lane) - 1u))] = tslot;
+      um = claimed ? 1u : 0u;
+    }
+    if (mine && my_slot >= 0) uh = (old != stamp) ? 1u : 0u;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -140,56 +241,31 @@ __global__ void __launch_bounds__(kLookupWarps * 32)
     atomicAdd(&s_counts[0], uh);
     atomicAdd(&s_counts[1], um);
   }
+  if (miss_work) __threadfence();  // publish table / list writes before completion
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_counts[0]) atomicAdd(ls.counts + 0, (unsigned long long)s_counts[0]);
     if (s_counts[1]) atomicAdd(ls.counts + 1, (unsigned long long)s_counts[1]);
+    __threadfence();
+    const unsigned long long prev = atomicAdd(ls.blocks_done, 1ull);
+    s_last = (prev == ls.blocks_base + gridDim.x - 1);
+    if (s_last) __threadfence();
   }
+  __syncthreads();
+  if (s_last) order_misses_tail(keys, n, ls);
 }
 
-void launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
-                         uint8_t* flags, const float* default_row, uint64_t stamp,
-                         const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st) {
-  if (n == 0) return;
+unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
+                             uint8_t* flags, const float* default_row, uint64_t stamp,
+                             const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st) {
+  if (n == 0) return 0;
   constexpr int P = 4;
   const uint64_t warps = (n + P - 1) / P;
   const unsigned grid = unsigned((warps + kLookupWarps - 1) / kLookupWarps);
-  k_lookup_probe<P><<<grid, kLookupWarps * 32, 0, st>>>(c, keys, n, out, flags, default_row,
-                                                        stamp, ls, table_epoch);
+  k_lookup_probe<P><<<grid, kLookupThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp,
+                                                     ls, table_epoch);
   check_launch("lookup_probe", 1);
-}
-
-__global__ void __launch_bounds__(kScanBlock)
-    k_lookup_compact(const uint64_t* __restrict__ keys, uint64_t n,
-                     const uint8_t* __restrict__ flags, LookupScratch ls, ScanState scan) {
-  if (ls.counts_out != nullptr && blockIdx.x == 0 && threadIdx.x < 2) {
-    // K1 has fully completed (stream order): publish this call's counts
-    const unsigned long long cum = ls.counts[threadIdx.x];
-    ls.counts_out[threadIdx.x] = cum - ls.counts_prev[threadIdx.x];
-    ls.counts_prev[threadIdx.x] = cum;
-  }
-  select_tile(
-      n, scan,
-      [&](uint64_t i) {
-        return flags[i] != 0 && uint32_t(ls.miss_table[ls.miss_slot[i]]) == uint32_t(i);
-      },
-      [&](uint64_t i, uint64_t r) {
-        ls.miss_keys[r] = keys[i];
-        ls.rank_of_slot[ls.miss_slot[i]] = uint32_t(r);
-      },
-      nullptr);
-}
-
-void launch_lookup_compact(const uint64_t* keys, uint64_t n, const uint8_t* flags,
-                           const LookupScratch& ls, uint32_t table_epoch, ScanState& scan,
-                           cudaStream_t st) {
-  (void)table_epoch;
-  if (n == 0) return;
-  const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
-  scan_begin(scan, tiles, st);
-  k_lookup_compact<<<unsigned(tiles), kScanBlock, 0, st>>>(keys, n, flags, ls, scan);
-  scan.tile_base += tiles;
-  check_launch("lookup_compact", 1);
+  return grid;
 }
 
 __global__ void __launch_bounds__(256)

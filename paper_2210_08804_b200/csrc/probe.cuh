@@ -32,8 +32,8 @@ __device__ __forceinline__ void warp_load_keys(const CacheDev& c, const uint64_t
   const bool v = lane < uint32_t(P) && base + lane < n;
   if (v) {
     k = keys[base + lane];
-    s = xxh64_key(k, kSlabsetSeed) % c.S;
-    f = uint32_t(xxh64_key(k, kSlabSeed) % c.W);
+    s = slabset_of(c, k);
+    f = first_slab_of(c, k);
   }
 #pragma unroll
   for (int p = 0; p < P; ++p) {
