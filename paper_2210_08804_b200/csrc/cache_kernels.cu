@@ -68,14 +68,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   if (base >= n) return;
   WarpKeys<P> wk;
   warp_load_keys<P>(c, keys, base, n, wk);
-  int64_t slot[P];
+  uint32_t slot[P];
   warp_probe<P>(c, wk, slot);
   const uint32_t lane = lane_id();
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     if (!wk.valid[p]) continue;
     const uint64_t i = base + p;
-    if (slot[p] >= 0) {
+    if (slot[p] != kNoSlot) {
       warp_copy_row(c.rows + uint64_t(slot[p]) * c.d, out + i * c.d, c.d);
       if (lane == 0) {
         c.counters[slot[p]] = stamp;
@@ -378,18 +378,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   if (base >= n) return;
   WarpKeys<P> wk;
   warp_load_keys<P>(c, keys, base, n, wk);
-  int64_t slot[P];
+  uint32_t slot[P];
   warp_probe<P>(c, wk, slot);
   const uint32_t lane = lane_id();
   if (lane >= uint32_t(P)) return;
   // lane p handles position base + p
-  int64_t my_slot = -1;
+  uint32_t my_slot = kNoSlot;
 #pragma unroll
   for (int p = 0; p < P; ++p)
     if (uint32_t(p) == lane) my_slot = slot[p];
   const uint64_t i = base + lane;
   if (i >= n) return;
-  if (my_slot < 0) {
+  if (my_slot == kNoSlot) {
     us.found_tab[i] = 0xFFFFFFFFu;
     return;
   }

@@ -37,6 +37,10 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device
   if (cfg.slabs_per_set == 0) throw invalid_argument("slabs_per_set must be positive");
   if (cfg.dimension == 0) throw invalid_argument("cache dimension must be positive");
   if (cfg.worker_pool_size == 0) throw invalid_argument("worker_pool_size must be positive");
+  // device slot indices are u32 (probe.cuh); 0xFFFFFFFF is the no-slot mark
+  if (cfg.slabset_count * cfg.slabs_per_set * 32ull >= 0xFFFFFFFFull ||
+      cfg.slabset_count * cfg.slabs_per_set / cfg.slabs_per_set != cfg.slabset_count)
+    throw invalid_argument("cache capacity must stay below 2^32 slots per replica");
   keys_per_warp_ = keys_per_warp_for(std::max<uint32_t>(1, cfg.tasks_per_worker));
   DeviceGuard g(device_);
   HPSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -193,19 +197,14 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     void* b = lbuf_.ensure(bytes, stream_);
     HPSB_CUDA(cudaMemsetAsync(b, 0, bytes, stream_));
     lws_ = lookup_scratch_carve(b, cap);
-    lepoch_ = 0;
     lcap_ = cap;
-  }
-  if (++lepoch_ == 0) {
-    HPSB_CUDA(cudaMemsetAsync(lws_.miss_table, 0, lws_.cap * 8, stream_));
-    lepoch_ = 1;
   }
   LookupScratch ls = lws_;
   ls.miss_keys = miss_keys;
   ls.counts_out = reinterpret_cast<unsigned long long*>(counts);
   if (prof_start_) HPSB_CUDA(cudaEventRecord(prof_start_, stream_));
   lws_.blocks_base +=
-      launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, lepoch_, stream_);
+      launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, stream_);
   if (prof_end_) HPSB_CUDA(cudaEventRecord(prof_end_, stream_));
   join_to(user);
 }

@@ -109,7 +109,6 @@ class DeviceCache {
   // lookup_device scratch
   DeviceBuffer lbuf_;
   LookupScratch lws_;
-  uint32_t lepoch_ = 0;
   uint64_t lcap_ = 0;
   cudaEvent_t prof_start_ = nullptr, prof_end_ = nullptr;
   unsigned long long* d_small_ = nullptr;  // small device counters

@@ -126,7 +126,6 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);
   ls.miss_keys = d_miss_keys;
-  table_epoch = 0;
   prev_counts[0] = prev_counts[1] = 0;
 
   const uint64_t host_bytes = a256(cap * 8) * 4 + a256(16) + a256(cap * 4) +
@@ -279,13 +278,8 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       } else {
         cache_->join_from(user);
       }
-      ws->table_epoch += 1;
-      if (ws->table_epoch == 0) {
-        HPSB_CUDA(cudaMemsetAsync(ws->ls.miss_table, 0, ws->ls.cap * 8, st));
-        ws->table_epoch = 1;
-      }
       ws->ls.blocks_base += launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags,
-                                                d_default_, stamp, ws->ls, ws->table_epoch, st);
+                                                d_default_, stamp, ws->ls, st);
       HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts, 16, cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }

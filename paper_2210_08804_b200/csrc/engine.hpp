@@ -82,7 +82,6 @@ struct Workspace {
   float* d_staged = nullptr;
   uint64_t* d_found_keys = nullptr;
   LookupScratch ls;
-  uint32_t table_epoch = 0;
   unsigned long long prev_counts[2] = {0, 0};
   // pinned host
   PinnedBuffer hbuf;

@@ -85,7 +85,7 @@ void launch_dedup(const uint64_t* keys, uint64_t n, uint64_t* unique_out, uint32
 // ---- lookup (lookup_engine.cpp:130-241) ----
 struct LookupScratch {
   uint64_t cap = 0;               // miss table capacity (power of two >= 2 * max_batch)
-  uint64_t* miss_table = nullptr; // (epoch << 32) | first position
+  uint32_t* miss_table = nullptr; // 0 = empty, else first position + 1 (cleared by the tail)
   uint32_t* miss_slot = nullptr;  // per position (valid where missed)
   uint32_t* rank_of_slot = nullptr;
   unsigned long long* counts = nullptr;  // [0] unique hits, [1] unique misses (cumulative)
@@ -112,7 +112,7 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
 // caller adds it to ls.blocks_base for the next call).
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st);
+                             const LookupScratch& ls, cudaStream_t st);
 void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint8_t* flags,
                            const LookupScratch& ls, const int32_t* row_of,
                            const float* staged, float* out, cudaStream_t st);

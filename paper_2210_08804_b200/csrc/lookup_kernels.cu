@@ -4,25 +4,32 @@
 // |Q| query positions in ONE kernel launch, without materialising the dedup
 // step for hits:
 //
-//   body  one warp per P positions: placement hash (Barrett modulo), ballot
-//         probe of 32-key slabs, 128-bit gather of the hit row straight into
-//         the position's output row (the expansion of lookup_engine.cpp:
-//         194-203 is fused), recency stamp via atomicExch -- the exchange
-//         that first moves a slot to this call's stamp counts one UNIQUE hit,
-//         so |Q*| needs no dedup of hits. Missing positions get the default
-//         row (the async branch's answer) and are deduplicated in a per-call
-//         hash table that keeps the first occurrence; the claiming position
-//         of every missing key appends the table slot to a short list.
+//   body  persistent grid (one wave), one warp per group of P positions per
+//         iteration: placement hash (Barrett modulo), ballot probe of 32-key
+//         slabs, 128-bit gather of the hit row straight into the position's
+//         output row (the expansion of lookup_engine.cpp:194-203 is fused),
+//         recency stamp via atomicExch -- the exchange that first moves a
+//         slot to this call's stamp counts one UNIQUE hit, so |Q*| needs no
+//         dedup of hits. Missing positions get the default row (the async
+//         branch's answer) and are deduplicated in a per-call hash table
+//         that keeps the first occurrence; the claiming position of every
+//         missing key appends the table slot to a short list. The next
+//         group's keys are prefetched and the exchange results are consumed
+//         one iteration late, so neither round trip sits on the warp's
+//         critical path.
 //   tail  the last block to finish (threadfence + completion counter) orders
-//         the unique misses by first occurrence with a position bitmap and a
-//         block scan -> the unique miss list in first-occurrence order (the
-//         order the reference's dedup + query produce, slab_cache.cpp:84-89)
-//         and the rank of every miss-table entry.
+//         the unique misses by first occurrence with a position bitmap (in
+//         shared memory for batches up to 2^18) and a block scan -> the
+//         unique miss list in first-occurrence order (the order the
+//         reference's dedup + query produce, slab_cache.cpp:84-89) and the
+//         rank of every miss-table entry; it also clears the entries it used.
 //   K3    lookup_scatter (sync branch only) copies the rows fetched from the
 //         tiers into every position of their key, clearing the default flag
 //         (lookup_engine.cpp:165-181).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -43,13 +50,15 @@ inline void check_launch(const char* what, uint32_t kernels) {
 inline uint64_t a256(uint64_t v) { return (v + 255) / 256 * 256; }
 constexpr int kLookupWarps = 8;
 constexpr int kLookupThreads = kLookupWarps * 32;
+constexpr uint64_t kSmemBitmapMax = 1u << 18;  // positions ordered in shared memory
+constexpr int kTailBatch = 8;
 }  // namespace
 
 size_t lookup_scratch_bytes(uint64_t cap) {
   uint64_t tcap = 16;
   while (tcap < 2 * cap) tcap <<= 1;
   const uint64_t words = (cap + 31) / 32;
-  return a256(tcap * 8) + a256(tcap * 4) + a256(cap * 4) * 3 + a256(words * 4) * 2 + a256(64);
+  return a256(tcap * 4) + a256(tcap * 4) + a256(cap * 4) * 3 + a256(words * 4) * 2 + a256(64);
 }
 
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
@@ -64,7 +73,7 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
     return r;
   };
   ls.cap = tcap;
-  ls.miss_table = reinterpret_cast<uint64_t*>(take(tcap * 8));
+  ls.miss_table = reinterpret_cast<uint32_t*>(take(tcap * 4));
   ls.rank_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
   ls.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list = reinterpret_cast<uint32_t*>(take(cap * 4));
@@ -94,41 +103,87 @@ __device__ __forceinline__ void st_cs_f4(float4* p, const float4& v) {
 
 // Orders the unique misses of this call by first occurrence (run by the
 // last block). list[e] = miss-table slot claimed by some position of a
-// missing key; the table entry's low word is that key's first position.
+// missing key; the table entry holds that key's first position + 1.
 __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys, uint64_t n,
-                                               const LookupScratch& ls) {
+                                               const LookupScratch& ls, uint32_t* bm,
+                                               bool smem_bm) {
   __shared__ uint32_t s_warp[kLookupWarps];
   const uint32_t tid = threadIdx.x;
   const uint32_t m = __ldcg(ls.list_ctr);
-  for (uint32_t e = tid; e < m; e += kLookupThreads) {
-    const uint32_t slot = __ldcg(ls.list + e);
-    const uint32_t f = uint32_t(__ldcg(reinterpret_cast<const unsigned long long*>(ls.miss_table) + slot));
-    ls.list_firsts[e] = f;
-    atomicOr(ls.bitmap + (f >> 5), 1u << (f & 31u));
+  const uint32_t words = uint32_t((n + 31) / 32);
+  if (smem_bm) {
+    for (uint32_t w = tid; w < words; w += kLookupThreads) bm[w] = 0;
+    __syncthreads();
+  }
+  // 1. first positions -> bitmap (loads batched for memory-level parallelism)
+  for (uint32_t e0 = tid; e0 < m; e0 += kLookupThreads * kTailBatch) {
+    uint32_t s[kTailBatch], f[kTailBatch];
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t e = e0 + j * kLookupThreads;
+      s[j] = e < m ? __ldcg(ls.list + e) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t e = e0 + j * kLookupThreads;
+      f[j] = e < m ? __ldcg(ls.miss_table + s[j]) - 1u : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t e = e0 + j * kLookupThreads;
+      if (e < m) {
+        ls.list_firsts[e] = f[j];
+        atomicOr(bm + (f[j] >> 5), 1u << (f[j] & 31u));
+      }
+    }
   }
   __syncthreads();
-  const uint32_t words = uint32_t((n + 31) / 32);
+  // 2. exclusive popcount prefix per bitmap word
   const uint32_t per = (words + kLookupThreads - 1) / kLookupThreads;
   const uint32_t w0 = min(words, tid * per), w1 = min(words, w0 + per);
   uint32_t cnt = 0;
-  for (uint32_t w = w0; w < w1; ++w) cnt += __popc(__ldcg(ls.bitmap + w));
+  for (uint32_t w = w0; w < w1; ++w) cnt += __popc(smem_bm ? bm[w] : __ldcg(bm + w));
   uint32_t total;
   uint32_t run = block_exclusive_scan<kLookupThreads>(cnt, s_warp, &total);
   for (uint32_t w = w0; w < w1; ++w) {
     ls.word_prefix[w] = run;
-    run += __popc(__ldcg(ls.bitmap + w));
+    run += __popc(smem_bm ? bm[w] : __ldcg(bm + w));
   }
   __syncthreads();
-  for (uint32_t e = tid; e < m; e += kLookupThreads) {
-    const uint32_t f = __ldcg(ls.list_firsts + e);
-    const uint32_t w = f >> 5;
-    const uint32_t r =
-        __ldcg(ls.word_prefix + w) + __popc(__ldcg(ls.bitmap + w) & ((1u << (f & 31u)) - 1u));
-    ls.miss_keys[r] = keys[f];
-    ls.rank_of_slot[__ldcg(ls.list + e)] = r;
+  // 3. rank = prefix(word) + popc(bits below) -> ordered miss keys, ranks
+  for (uint32_t e0 = tid; e0 < m; e0 += kLookupThreads * kTailBatch) {
+    uint32_t s[kTailBatch], f[kTailBatch], r[kTailBatch];
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t e = e0 + j * kLookupThreads;
+      s[j] = e < m ? __ldcg(ls.list + e) : 0u;
+      f[j] = e < m ? __ldcg(ls.list_firsts + e) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t w = f[j] >> 5;
+      const uint32_t word = smem_bm ? bm[w] : __ldcg(bm + w);
+      r[j] = __ldcg(ls.word_prefix + w) + __popc(word & ((1u << (f[j] & 31u)) - 1u));
+    }
+    uint64_t k[kTailBatch];
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t e = e0 + j * kLookupThreads;
+      k[j] = e < m ? keys[f[j]] : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < kTailBatch; ++j) {
+      const uint32_t e = e0 + j * kLookupThreads;
+      if (e < m) {
+        ls.miss_keys[r[j]] = k[j];
+        ls.rank_of_slot[s[j]] = r[j];
+        ls.miss_table[s[j]] = 0u;  // leave the table empty for the next call
+      }
+    }
   }
   __syncthreads();
-  for (uint32_t w = w0; w < w1; ++w) ls.bitmap[w] = 0;
+  if (!smem_bm)
+    for (uint32_t w = w0; w < w1; ++w) bm[w] = 0;
   if (tid == 0) *ls.list_ctr = 0;
   if (ls.counts_out != nullptr && tid < 2) {
     const unsigned long long cum = __ldcg(ls.counts + tid);
@@ -137,43 +192,49 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
   }
 }
 
-template <int P>
-__global__ void __launch_bounds__(kLookupThreads, 4)
+template <int P, int MINB>
+__global__ void __launch_bounds__(kLookupThreads, MINB)
     k_lookup_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                    float* __restrict__ out, uint8_t* __restrict__ flags,
                    const float* __restrict__ default_row, uint64_t stamp, LookupScratch ls,
-                   uint32_t epoch) {
+                   int smem_bm) {
+  extern __shared__ uint32_t s_bitmap[];
   __shared__ unsigned int s_counts[2];
   __shared__ bool s_last;
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t warp = (uint64_t(blockIdx.x) * kLookupWarps) + (threadIdx.x >> 5);
-  const uint64_t base = warp * P;
   const uint32_t lane = lane_id();
+  const uint64_t groups = (n + P - 1) / P;
+  const uint64_t stride = uint64_t(gridDim.x) * kLookupWarps;
+  uint64_t g = uint64_t(blockIdx.x) * kLookupWarps + (threadIdx.x >> 5);
   uint32_t uh = 0, um = 0;
   bool miss_work = false;
-  if (base < n) {
+  // software pipeline state
+  uint64_t next_key = 0;
+  if (g < groups && lane < uint32_t(P) && g * P + lane < n) next_key = keys[g * P + lane];
+  unsigned long long pend_old = 0;
+  bool pend = false;
+  const uint32_t d = c.d;
+  while (g < groups) {
+    const uint64_t base = g * P;
+    const uint64_t k = next_key;
+    const uint64_t gn = g + stride;
+    if (gn < groups && lane < uint32_t(P) && gn * P + lane < n) next_key = keys[gn * P + lane];
     WarpKeys<P> wk;
-    warp_load_keys<P>(c, keys, base, n, wk);
-    int64_t slot[P];
+    warp_place_keys<P>(c, k, base, n, wk);
+    uint32_t slot[P];
     warp_probe<P>(c, wk, slot);
-    // lane p owns position base + p for the bookkeeping
-    int64_t my_slot = -1;
-    uint64_t my_key = 0;
+    // the previous iteration's exchange has long returned by now
+    if (pend) uh += (pend_old != stamp) ? 1u : 0u;
+    uint32_t my_slot = kNoSlot;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      if (uint32_t(p) == lane) {
-        my_slot = slot[p];
-        my_key = wk.key[p];
-      }
-    }
+    for (int p = 0; p < P; ++p)
+      if (uint32_t(p) == lane) my_slot = slot[p];
     const uint64_t i = base + lane;
     const bool mine = lane < uint32_t(P) && i < n;
-    // issue the recency exchange now; its result is consumed at the end
-    unsigned long long old = stamp;
-    if (mine && my_slot >= 0)
-      old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + my_slot), stamp);
-    const uint32_t d = c.d;
+    pend = mine && my_slot != kNoSlot;
+    if (pend)
+      pend_old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + my_slot), stamp);
     if ((d & 3u) == 0) {
       // 128-bit path: the first 32 float4 chunks of every row are loaded for
       // all P positions before any store so P row reads are in flight.
@@ -182,7 +243,7 @@ __global__ void __launch_bounds__(kLookupThreads, 4)
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         if (wk.valid[p] && lane < d4) {
-          const float* src = slot[p] >= 0 ? c.rows + uint64_t(slot[p]) * d : default_row;
+          const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
           v[p] = ld_nc_f4(reinterpret_cast<const float4*>(src) + lane);
         }
       }
@@ -195,7 +256,7 @@ __global__ void __launch_bounds__(kLookupThreads, 4)
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           if (!wk.valid[p]) continue;
-          const float* src = slot[p] >= 0 ? c.rows + uint64_t(slot[p]) * d : default_row;
+          const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
           st_cs_f4(reinterpret_cast<float4*>(out + (base + p) * d) + ch,
                    ld_nc_f4(reinterpret_cast<const float4*>(src) + ch));
         }
@@ -204,17 +265,17 @@ __global__ void __launch_bounds__(kLookupThreads, 4)
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         if (!wk.valid[p]) continue;
-        const float* src = slot[p] >= 0 ? c.rows + uint64_t(slot[p]) * d : default_row;
+        const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
         for (uint32_t ch = lane; ch < d; ch += 32) out[(base + p) * d + ch] = src[ch];
       }
     }
     bool claimed = false;
     uint32_t tslot = 0;
     if (mine) {
-      if (my_slot >= 0) {
+      if (my_slot != kNoSlot) {
         flags[i] = 0;
       } else {
-        tslot = dedup_insert(ls.miss_table, ls.cap, keys, my_key, uint32_t(i), epoch, &claimed);
+        tslot = miss_insert(ls.miss_table, ls.cap, keys, k, uint32_t(i), &claimed);
         ls.miss_slot[i] = tslot;
         flags[i] = 1;
         miss_work = true;
@@ -228,10 +289,11 @@ __global__ void __launch_bounds__(kLookupThreads, 4)
       if (lane == leader) at = atomicAdd(ls.list_ctr, uint32_t(__popc(cm)));
       at = __shfl_sync(0xFFFFFFFFu, at, leader);
       if (claimed) ls.list[at + __popc(cm & ((1u << lane) - 1u))] = tslot;
-      um = claimed ? 1u : 0u;
+      um += claimed ? 1u : 0u;
     }
-    if (mine && my_slot >= 0) uh = (old != stamp) ? 1u : 0u;
+    g = gn;
   }
+  if (pend) uh += (pend_old != stamp) ? 1u : 0u;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     uh += __shfl_xor_sync(0xFFFFFFFFu, uh, o);
@@ -252,18 +314,52 @@ __global__ void __launch_bounds__(kLookupThreads, 4)
     if (s_last) __threadfence();
   }
   __syncthreads();
-  if (s_last) order_misses_tail(keys, n, ls);
+  if (s_last) order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
 }
 
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupScratch& ls, uint32_t table_epoch, cudaStream_t st) {
+                             const LookupScratch& ls, cudaStream_t st) {
   if (n == 0) return 0;
-  constexpr int P = 4;
-  const uint64_t warps = (n + P - 1) / P;
-  const unsigned grid = unsigned((warps + kLookupWarps - 1) / kLookupWarps);
-  k_lookup_probe<P><<<grid, kLookupThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp,
-                                                     ls, table_epoch);
+  // Variant table: (positions per warp, min resident blocks per SM). The
+  // default was chosen from measurements on B200 (profiles/); HPSB_LOOKUP_VARIANT
+  // selects another for experiments.
+  using Kern = void (*)(CacheDev, const uint64_t*, uint64_t, float*, uint8_t*, const float*,
+                        uint64_t, LookupScratch, int);
+  struct Variant {
+    Kern fn;
+    int P;
+    int per_sm;
+  };
+  static Variant variants[] = {{k_lookup_probe<4, 3>, 4, 3}, {k_lookup_probe<2, 4>, 2, 4},
+                               {k_lookup_probe<4, 2>, 4, 2}, {k_lookup_probe<8, 2>, 8, 2},
+                               {k_lookup_probe<1, 6>, 1, 6}, {k_lookup_probe<2, 6>, 2, 6}};
+  static std::once_flag once;
+  static int sms = 148;
+  static int vi = 0;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (const char* e = std::getenv("HPSB_LOOKUP_VARIANT")) vi = std::atoi(e) % 6;
+    for (auto& v : variants) {
+      cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kSmemBitmapMax / 8));
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, v.fn, kLookupThreads, 8192) ==
+              cudaSuccess &&
+          b > 0)
+        v.per_sm = b;
+    }
+  });
+  const Variant& v = variants[vi];
+  const bool smem_bm = n <= kSmemBitmapMax;
+  const size_t dyn = smem_bm ? ((n + 31) / 32) * 4 : 0;
+  const uint64_t groups = (n + v.P - 1) / v.P;
+  const uint64_t need = (groups + kLookupWarps - 1) / kLookupWarps;
+  const unsigned grid = unsigned(std::min<uint64_t>(need, uint64_t(sms) * v.per_sm));
+  v.fn<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp, ls,
+                                          smem_bm ? 1 : 0);
   check_launch("lookup_probe", 1);
   return grid;
 }

@@ -15,24 +15,25 @@ namespace hpsb {
 
 // Per-position placement, computed by lanes 0..P-1 in parallel and
 // broadcast to the warp.
+// Slot indices are u32 (the cache holds < 2^32 slots, checked at creation).
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+
 template <int P>
 struct WarpKeys {
   uint64_t key[P];
-  uint64_t set[P];
+  uint32_t set[P];
   uint32_t first[P];
   bool valid[P];
 };
 
+// Lanes 0..P-1 hash their own key; the placement is broadcast.
 template <int P>
-__device__ __forceinline__ void warp_load_keys(const CacheDev& c, const uint64_t* __restrict__ keys,
-                                               uint64_t base, uint64_t n, WarpKeys<P>& wk) {
+__device__ __forceinline__ void warp_place_keys(const CacheDev& c, uint64_t k, uint64_t base,
+                                                uint64_t n, WarpKeys<P>& wk) {
   const uint32_t lane = lane_id();
-  uint64_t k = 0, s = 0;
-  uint32_t f = 0;
-  const bool v = lane < uint32_t(P) && base + lane < n;
-  if (v) {
-    k = keys[base + lane];
-    s = slabset_of(c, k);
+  uint32_t s = 0, f = 0;
+  if (lane < uint32_t(P)) {
+    s = uint32_t(slabset_of(c, k));
     f = first_slab_of(c, k);
   }
 #pragma unroll
@@ -44,21 +45,29 @@ __device__ __forceinline__ void warp_load_keys(const CacheDev& c, const uint64_t
   }
 }
 
-// slot[p] = global slot index of key p, or -1. Warp-uniform results.
+template <int P>
+__device__ __forceinline__ void warp_load_keys(const CacheDev& c, const uint64_t* __restrict__ keys,
+                                               uint64_t base, uint64_t n, WarpKeys<P>& wk) {
+  const uint32_t lane = lane_id();
+  const uint64_t k = (lane < uint32_t(P) && base + lane < n) ? keys[base + lane] : 0ull;
+  warp_place_keys<P>(c, k, base, n, wk);
+}
+
+// slot[p] = global slot index of key p, or kNoSlot. Warp-uniform results.
 template <int P>
 __device__ __forceinline__ void warp_probe(const CacheDev& c, const WarpKeys<P>& wk,
-                                           int64_t (&slot)[P]) {
+                                           uint32_t (&slot)[P]) {
   const uint32_t lane = lane_id();
   bool pending[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     pending[p] = wk.valid[p];
-    slot[p] = -1;
+    slot[p] = kNoSlot;
   }
   for (uint32_t step = 0; step < c.W; ++step) {
     uint64_t sk[P];
     uint32_t m[P];
-    uint64_t slab[P];
+    uint32_t slab[P];
     bool any = false;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -67,7 +76,7 @@ __device__ __forceinline__ void warp_probe(const CacheDev& c, const WarpKeys<P>&
         sl = (sl >= c.W) ? sl - c.W : sl;
         slab[p] = wk.set[p] * c.W + sl;
         m[p] = c.masks[slab[p]];
-        sk[p] = c.keys[slab[p] * kSlotsPerSlab + lane];
+        sk[p] = c.keys[uint64_t(slab[p]) * kSlotsPerSlab + lane];
         any = true;
       }
     }
@@ -78,7 +87,7 @@ __device__ __forceinline__ void warp_probe(const CacheDev& c, const WarpKeys<P>&
         const uint32_t b =
             __ballot_sync(0xFFFFFFFFu, ((m[p] >> lane) & 1u) && sk[p] == wk.key[p]);
         if (b) {
-          slot[p] = int64_t(slab[p] * kSlotsPerSlab + (__ffs(b) - 1));
+          slot[p] = slab[p] * kSlotsPerSlab + (__ffs(b) - 1);
           pending[p] = false;
         } else if (m[p] != kFullSlab) {
           pending[p] = false;  // a free slot before the key: not resident
@@ -174,5 +183,29 @@ __device__ __forceinline__ uint32_t dedup_insert(uint64_t* table, uint64_t cap,
   }
 }
 
+// Lookup miss table: u32 entries, 0 = empty, else first position + 1. The
+// claimer of an empty entry needs one round trip (a CAS from 0); later
+// positions of the same key compare through the immutable input and keep
+// the minimum position with a fire-and-forget atomicMin. The ordering tail
+// clears every claimed entry, so the table is all-zero between calls.
+__device__ __forceinline__ uint32_t miss_insert(uint32_t* table, uint64_t cap,
+                                                const uint64_t* __restrict__ keys, uint64_t key,
+                                                uint32_t pos, bool* claimed) {
+  uint64_t t = fmix64(key ^ 0x9E3779B97F4A7C15ull) & (cap - 1);
+  const uint32_t mine = pos + 1;
+  while (true) {
+    const uint32_t old = atomicCAS(table + t, 0u, mine);
+    if (old == 0u) {
+      *claimed = true;
+      return uint32_t(t);
+    }
+    if (keys[old - 1] == key) {
+      *claimed = false;
+      if (mine < old) atomicMin(table + t, mine);
+      return uint32_t(t);
+    }
+    t = (t + 1) & (cap - 1);
+  }
+}
 
 }  // namespace hpsb
