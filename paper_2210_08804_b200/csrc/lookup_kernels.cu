@@ -317,6 +317,180 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   if (s_last) order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
 }
 
+__device__ __forceinline__ float4 ld_nc_f4_l1(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Warp-deduplicated variant. Power-law batches repeat their hottest keys
+// thousands of times (alpha 1.2: the top key is ~19% of all positions), and
+// a per-position probe turns every repeat into a read of the same slab,
+// mask and row and an atomic on the same counter -- L2 hot spots that
+// serialise. Here a warp takes 32 consecutive positions, groups equal keys
+// with __match_any_sync, and only the group leader (lowest lane = lowest
+// position) probes, stamps, inserts a miss, and loads the row; the row is
+// then stored from registers to every position of the group.
+template <int P, int MINB>
+__global__ void __launch_bounds__(kLookupThreads, MINB)
+    k_lookup_dedup(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                   float* __restrict__ out, uint8_t* __restrict__ flags,
+                   const float* __restrict__ default_row, uint64_t stamp, LookupScratch ls,
+                   int smem_bm) {
+  extern __shared__ uint32_t s_bitmap[];
+  __shared__ unsigned int s_counts[2];
+  __shared__ bool s_last;
+  if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint64_t tiles = (n + 31) / 32;
+  const uint64_t stride = uint64_t(gridDim.x) * kLookupWarps;
+  uint64_t t = uint64_t(blockIdx.x) * kLookupWarps + (threadIdx.x >> 5);
+  uint32_t uh = 0, um = 0;
+  bool miss_work = false;
+  uint64_t next_key = (t < tiles && t * 32 + lane < n) ? keys[t * 32 + lane] : 0ull;
+  const uint32_t d = c.d;
+  const uint32_t d4 = d >> 2;
+  const bool vec = (d & 3u) == 0;
+  while (t < tiles) {
+    const uint64_t base = t * 32;
+    const uint64_t pos = base + lane;
+    const bool valid = pos < n;
+    const uint64_t key = next_key;
+    const uint64_t tn = t + stride;
+    next_key = (tn < tiles && tn * 32 + lane < n) ? keys[tn * 32 + lane] : 0ull;
+    const uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    uint32_t grp = 1u << lane;
+    if (valid) grp = __match_any_sync(vmask, key);
+    const uint32_t my_leader = __ffs(grp) - 1;
+    const bool leader = valid && my_leader == lane;
+    const uint32_t my_set = uint32_t(slabset_of(c, key));
+    const uint32_t my_first = first_slab_of(c, key);
+    uint32_t L = __ballot_sync(0xFFFFFFFFu, leader);
+    uint32_t my_res = kNoSlot;
+    while (L) {
+      uint32_t ld[P];
+      WarpKeys<P> wk;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        wk.valid[p] = L != 0;
+        ld[p] = L ? __ffs(L) - 1 : 0;
+        L &= L - 1;
+        wk.key[p] = __shfl_sync(0xFFFFFFFFu, key, ld[p]);
+        wk.set[p] = __shfl_sync(0xFFFFFFFFu, my_set, ld[p]);
+        wk.first[p] = __shfl_sync(0xFFFFFFFFu, my_first, ld[p]);
+      }
+      uint32_t slot[P];
+      warp_probe<P>(c, wk, slot);
+      bool stamp_now = false;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (wk.valid[p] && lane == ld[p]) {
+          my_res = slot[p];
+          stamp_now = slot[p] != kNoSlot;
+        }
+      }
+      unsigned long long old = stamp;
+      if (stamp_now)
+        old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + my_res), stamp);
+      if (vec) {
+        float4 v[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          if (wk.valid[p] && lane < d4) {
+            const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
+            v[p] = ld_nc_f4_l1(reinterpret_cast<const float4*>(src) + lane);
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          if (!wk.valid[p]) continue;
+          uint32_t g = __shfl_sync(0xFFFFFFFFu, grp, ld[p]);
+          while (g) {
+            const uint32_t j = __ffs(g) - 1;
+            g &= g - 1;
+            if (lane < d4) st_cs_f4(reinterpret_cast<float4*>(out + (base + j) * d) + lane, v[p]);
+          }
+        }
+        for (uint32_t ch = lane + 32; ch < d4; ch += 32) {
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            if (!wk.valid[p]) continue;
+            const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
+            const float4 x = ld_nc_f4_l1(reinterpret_cast<const float4*>(src) + ch);
+            uint32_t g = __shfl_sync(0xFFFFFFFFu, grp, ld[p]);
+            while (g) {
+              const uint32_t j = __ffs(g) - 1;
+              g &= g - 1;
+              st_cs_f4(reinterpret_cast<float4*>(out + (base + j) * d) + ch, x);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          if (!wk.valid[p]) continue;
+          const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
+          uint32_t g = __shfl_sync(0xFFFFFFFFu, grp, ld[p]);
+          while (g) {
+            const uint32_t j = __ffs(g) - 1;
+            g &= g - 1;
+            for (uint32_t ch = lane; ch < d; ch += 32) out[(base + j) * d + ch] = src[ch];
+          }
+        }
+      }
+      if (stamp_now) uh += (old != stamp) ? 1u : 0u;
+    }
+    // leaders of missing keys insert into the miss table; every position
+    // learns its leader's outcome
+    bool claimed = false;
+    uint32_t tslot = 0;
+    if (leader && my_res == kNoSlot) {
+      tslot = miss_insert(ls.miss_table, ls.cap, keys, key, uint32_t(pos), &claimed);
+      miss_work = true;
+    }
+    const uint32_t res = __shfl_sync(0xFFFFFFFFu, my_res, my_leader);
+    const uint32_t tsl = __shfl_sync(0xFFFFFFFFu, tslot, my_leader);
+    if (valid) {
+      flags[pos] = res == kNoSlot ? 1 : 0;
+      if (res == kNoSlot) ls.miss_slot[pos] = tsl;
+    }
+    const uint32_t cm = __ballot_sync(0xFFFFFFFFu, claimed);
+    if (cm) {
+      const uint32_t first_lane = __ffs(cm) - 1;
+      uint32_t at = 0;
+      if (lane == first_lane) at = atomicAdd(ls.list_ctr, uint32_t(__popc(cm)));
+      at = __shfl_sync(0xFFFFFFFFu, at, first_lane);
+      if (claimed) ls.list[at + __popc(cm & ((1u << lane) - 1u))] = tslot;
+      um += claimed ? 1u : 0u;
+    }
+    t = tn;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uh += __shfl_xor_sync(0xFFFFFFFFu, uh, o);
+    um += __shfl_xor_sync(0xFFFFFFFFu, um, o);
+  }
+  if (lane == 0 && (uh | um)) {
+    atomicAdd(&s_counts[0], uh);
+    atomicAdd(&s_counts[1], um);
+  }
+  if (miss_work) __threadfence();  // publish table / list writes before completion
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_counts[0]) atomicAdd(ls.counts + 0, (unsigned long long)s_counts[0]);
+    if (s_counts[1]) atomicAdd(ls.counts + 1, (unsigned long long)s_counts[1]);
+    __threadfence();
+    const unsigned long long prev = atomicAdd(ls.blocks_done, 1ull);
+    s_last = (prev == ls.blocks_base + gridDim.x - 1);
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  if (s_last) order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+}
+
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
                              const LookupScratch& ls, cudaStream_t st) {
@@ -331,9 +505,14 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     int P;
     int per_sm;
   };
-  static Variant variants[] = {{k_lookup_probe<4, 3>, 4, 3}, {k_lookup_probe<2, 4>, 2, 4},
-                               {k_lookup_probe<4, 2>, 4, 2}, {k_lookup_probe<8, 2>, 8, 2},
-                               {k_lookup_probe<1, 6>, 1, 6}, {k_lookup_probe<2, 6>, 2, 6}};
+  // P = positions per group for the per-position kernels (0-2); for the
+  // warp-dedup kernels (3-6) positions per warp-tile are 32 and P is the
+  // number of group leaders probed concurrently.
+  static Variant variants[] = {{k_lookup_dedup<4, 3>, 32, 3}, {k_lookup_probe<4, 3>, 4, 3},
+                               {k_lookup_probe<4, 2>, 4, 2},  {k_lookup_probe<2, 4>, 2, 4},
+                               {k_lookup_dedup<8, 2>, 32, 2}, {k_lookup_dedup<4, 2>, 32, 2},
+                               {k_lookup_dedup<2, 4>, 32, 4}};
+  constexpr int kVariants = sizeof(variants) / sizeof(variants[0]);
   static std::once_flag once;
   static int sms = 148;
   static int vi = 0;
@@ -341,7 +520,7 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (const char* e = std::getenv("HPSB_LOOKUP_VARIANT")) vi = std::atoi(e) % 6;
+    if (const char* e = std::getenv("HPSB_LOOKUP_VARIANT")) vi = std::atoi(e) % kVariants;
     for (auto& v : variants) {
       cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(kSmemBitmapMax / 8));
