@@ -102,6 +102,7 @@ struct LookupScratch {
   uint32_t* word_prefix = nullptr;  // ceil(n/32) words
   unsigned long long* blocks_done = nullptr;  // cumulative block-completion counter
   unsigned long long blocks_base = 0;         // host: blocks launched before this call
+  unsigned long long* dbg = nullptr;          // diagnostic phase timestamps (HPSB_DEBUG_TIMING)
 };
 // Bytes / carving of a LookupScratch for batches of up to `cap` keys (all
 // regions zero-initialised by the caller once).

@@ -28,6 +28,7 @@
 //         (lookup_engine.cpp:165-181).
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -86,6 +87,12 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   ls.blocks_done = small + 4;  // [4]
   ls.list_ctr = reinterpret_cast<uint32_t*>(small + 5);
   return ls;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ float4 ld_nc_f4(const float4* p) {
@@ -204,6 +211,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
   __syncthreads();
   const uint32_t lane = lane_id();
+  if (ls.dbg && threadIdx.x == 0) atomicMin(ls.dbg + 0, gtimer());
   const uint64_t groups = (n + P - 1) / P;
   const uint64_t stride = uint64_t(gridDim.x) * kLookupWarps;
   uint64_t g = uint64_t(blockIdx.x) * kLookupWarps + (threadIdx.x >> 5);
@@ -294,6 +302,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     g = gn;
   }
   if (pend) uh += (pend_old != stamp) ? 1u : 0u;
+  if (ls.dbg && lane == 0) atomicMax(ls.dbg + 1, gtimer());
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     uh += __shfl_xor_sync(0xFFFFFFFFu, uh, o);
@@ -314,7 +323,12 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     if (s_last) __threadfence();
   }
   __syncthreads();
-  if (s_last) order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+  if (s_last) {
+    if (ls.dbg && threadIdx.x == 0) ls.dbg[2] = gtimer();
+    order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+    __syncthreads();
+    if (ls.dbg && threadIdx.x == 0) ls.dbg[3] = gtimer();
+  }
 }
 
 __device__ __forceinline__ float4 ld_nc_f4_l1(const float4* p) {
@@ -345,6 +359,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
   __syncthreads();
   const uint32_t lane = lane_id();
+  if (ls.dbg && threadIdx.x == 0) atomicMin(ls.dbg + 0, gtimer());
   const uint64_t tiles = (n + 31) / 32;
   const uint64_t stride = uint64_t(gridDim.x) * kLookupWarps;
   uint64_t t = uint64_t(blockIdx.x) * kLookupWarps + (threadIdx.x >> 5);
@@ -468,6 +483,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     }
     t = tn;
   }
+  if (ls.dbg && lane == 0) atomicMax(ls.dbg + 1, gtimer());
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     uh += __shfl_xor_sync(0xFFFFFFFFu, uh, o);
@@ -488,7 +504,12 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     if (s_last) __threadfence();
   }
   __syncthreads();
-  if (s_last) order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+  if (s_last) {
+    if (ls.dbg && threadIdx.x == 0) ls.dbg[2] = gtimer();
+    order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+    __syncthreads();
+    if (ls.dbg && threadIdx.x == 0) ls.dbg[3] = gtimer();
+  }
 }
 
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
@@ -537,9 +558,29 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
   const uint64_t groups = (n + v.P - 1) / v.P;
   const uint64_t need = (groups + kLookupWarps - 1) / kLookupWarps;
   const unsigned grid = unsigned(std::min<uint64_t>(need, uint64_t(sms) * v.per_sm));
-  v.fn<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp, ls,
+  // Diagnostic (HPSB_DEBUG_TIMING=1): globaltimer stamps of kernel start,
+  // last warp out of the body, tail start / end, printed to stderr. Adds a
+  // synchronisation per call; never set for measurements.
+  static unsigned long long* dbg = nullptr;
+  static const bool debug = std::getenv("HPSB_DEBUG_TIMING") != nullptr;
+  LookupScratch lsd = ls;
+  if (debug) {
+    if (!dbg) cudaMalloc(&dbg, 64);
+    const unsigned long long init[4] = {~0ull, 0, 0, 0};
+    cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    lsd.dbg = dbg;
+  }
+  v.fn<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp, lsd,
                                           smem_bm ? 1 : 0);
   check_launch("lookup_probe", 1);
+  if (debug) {
+    unsigned long long h[4];
+    cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr, "lookup_timing n=%llu grid=%u body_us=%.2f tail_wait_us=%.2f tail_us=%.2f\n",
+                 (unsigned long long)n, grid, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3,
+                 (h[3] - h[2]) * 1e-3);
+  }
   return grid;
 }
 
