@@ -241,8 +241,12 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     const uint64_t i = base + lane;
     const bool mine = lane < uint32_t(P) && i < n;
     pend = mine && my_slot != kNoSlot;
-    if (pend)
-      pend_old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + my_slot), stamp);
+    if (pend) {
+      if (smem_bm & 2)
+        pend_old = 0;  // diagnostic: skip the exchange
+      else
+        pend_old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + my_slot), stamp);
+    }
     if ((d & 3u) == 0) {
       // 128-bit path: the first 32 float4 chunks of every row are loaded for
       // all P positions before any store so P row reads are in flight.
@@ -252,12 +256,13 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
       for (int p = 0; p < P; ++p) {
         if (wk.valid[p] && lane < d4) {
           const float* src = slot[p] != kNoSlot ? c.rows + uint64_t(slot[p]) * d : default_row;
-          v[p] = ld_nc_f4(reinterpret_cast<const float4*>(src) + lane);
+          v[p] = (smem_bm & 4) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                               : ld_nc_f4(reinterpret_cast<const float4*>(src) + lane);
         }
       }
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        if (wk.valid[p] && lane < d4)
+        if (wk.valid[p] && lane < d4 && !(smem_bm & 8))
           st_cs_f4(reinterpret_cast<float4*>(out + (base + p) * d) + lane, v[p]);
       }
       for (uint32_t ch = lane + 32; ch < d4; ch += 32) {
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   __syncthreads();
   if (s_last) {
     if (ls.dbg && threadIdx.x == 0) ls.dbg[2] = gtimer();
-    order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+    order_misses_tail(keys, n, ls, (smem_bm & 1) ? s_bitmap : ls.bitmap, (smem_bm & 1) != 0);
     __syncthreads();
     if (ls.dbg && threadIdx.x == 0) ls.dbg[3] = gtimer();
   }
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   __syncthreads();
   if (s_last) {
     if (ls.dbg && threadIdx.x == 0) ls.dbg[2] = gtimer();
-    order_misses_tail(keys, n, ls, smem_bm ? s_bitmap : ls.bitmap, smem_bm != 0);
+    order_misses_tail(keys, n, ls, (smem_bm & 1) ? s_bitmap : ls.bitmap, (smem_bm & 1) != 0);
     __syncthreads();
     if (ls.dbg && threadIdx.x == 0) ls.dbg[3] = gtimer();
   }
@@ -570,8 +575,11 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
     lsd.dbg = dbg;
   }
+  // bit 0: order in shared memory; bits 1-3 (HPSB_LOOKUP_SKIP, diagnostic
+  // only): skip the recency exchange / the row loads / the row stores
+  static const int skip = std::getenv("HPSB_LOOKUP_SKIP") ? std::atoi(std::getenv("HPSB_LOOKUP_SKIP")) : 0;
   v.fn<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp, lsd,
-                                          smem_bm ? 1 : 0);
+                                          (smem_bm ? 1 : 0) | (skip & 14));
   check_launch("lookup_probe", 1);
   if (debug) {
     unsigned long long h[4];
