@@ -296,19 +296,21 @@ def run_ours(args, rank, world, local_rank):
             cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
                                 flags[s % ring].data_ptr(), default_row.data_ptr(),
                                 mkeys[s % ring].data_ptr(), counts.data_ptr(), sp)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(steps)]
-        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(steps)]
+        # The K steps are captured into one CUDA graph and launched once, so
+        # host-side call overhead cannot starve the GPU between steps; per-step
+        # and per-kernel timestamps are external event records inside it.
+        def mk():
+            return torch.cuda.Event(enable_timing=True, external=True)
+
+        ev = [(mk(), mk()) for _ in range(steps)]
+        kev = [(mk(), mk()) for _ in range(steps)]
         for a, b in kev:  # materialise the cudaEvent_t handles
             a.record(st)
             b.record(st)
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
         l0 = hps.kernel_launch_count()
-        with torch.cuda.stream(st):
+        with torch.cuda.graph(graph, stream=st):
             for s in range(steps):
                 j = s % pool
                 ev[s][0].record(st)
@@ -317,12 +319,20 @@ def run_ours(args, rank, world, local_rank):
                                     flags[s % ring].data_ptr(), default_row.data_ptr(),
                                     mkeys[s % ring].data_ptr(), counts[2 * s:].data_ptr(), sp)
                 ev[s][1].record(st)
-        torch.cuda.synchronize()
-        launches = hps.kernel_launch_count() - l0
+        launches = hps.kernel_launch_count() - l0  # kernel nodes in the timed graph
         cache.set_profile_events(0, 0)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        total_ms = ev[0][0].elapsed_time(ev[-1][1])
+        torch.cuda.synchronize()
+        t0.record(st)
+        graph.replay()
+        t1.record(st)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        total_ms = t0.elapsed_time(t1)
         per = np.array([a.elapsed_time(b) for a, b in ev])
         k1 = np.array([a.elapsed_time(b) for a, b in kev])
         c = counts.cpu().numpy().reshape(-1, 2)[:steps]

@@ -202,10 +202,15 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   LookupScratch ls = lws_;
   ls.miss_keys = miss_keys;
   ls.counts_out = reinterpret_cast<unsigned long long*>(counts);
-  if (prof_start_) HPSB_CUDA(cudaEventRecord(prof_start_, stream_));
-  lws_.blocks_base +=
-      launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, stream_);
-  if (prof_end_) HPSB_CUDA(cudaEventRecord(prof_end_, stream_));
+  // profile events: external records when the stream is being captured into
+  // a CUDA graph, so the timestamps stay readable after graph launches
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (prof_start_ || prof_end_) HPSB_CUDA(cudaStreamIsCapturing(stream_, &cap));
+  const unsigned rec_flags =
+      cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  if (prof_start_) HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, stream_);
+  if (prof_end_) HPSB_CUDA(cudaEventRecordWithFlags(prof_end_, stream_, rec_flags));
   join_to(user);
 }
 

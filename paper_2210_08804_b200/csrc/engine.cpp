@@ -278,7 +278,7 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       } else {
         cache_->join_from(user);
       }
-      ws->ls.blocks_base += launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags,
+      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags,
                                                 d_default_, stamp, ws->ls, st);
       HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts, 16, cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));

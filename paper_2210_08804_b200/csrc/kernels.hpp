@@ -100,8 +100,7 @@ struct LookupScratch {
   uint32_t* list_ctr = nullptr;     // 1 word, left at 0 by the tail
   uint32_t* bitmap = nullptr;       // ceil(n/32) words, left zeroed by the tail
   uint32_t* word_prefix = nullptr;  // ceil(n/32) words
-  unsigned long long* blocks_done = nullptr;  // cumulative block-completion counter
-  unsigned long long blocks_base = 0;         // host: blocks launched before this call
+  unsigned long long* blocks_done = nullptr;  // block-completion counter (reset by the last block)
   unsigned long long* dbg = nullptr;          // diagnostic phase timestamps (HPSB_DEBUG_TIMING)
 };
 // Bytes / carving of a LookupScratch for batches of up to `cap` keys (all
@@ -110,7 +109,7 @@ size_t lookup_scratch_bytes(uint64_t cap);
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
 // One launch per lookup: probe + gather + stamps + miss dedup, and the last
 // block to finish orders the unique misses. Returns the grid size (the
-// caller adds it to ls.blocks_base for the next call).
+// caller may report it).
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
                              const LookupScratch& ls, cudaStream_t st);
