@@ -134,6 +134,16 @@ int hps_cache_lookup_device(hps_cache* cache, const uint64_t* keys, size_t n, fl
  * calls; NULL disables. Used by bench.py to time the dominant kernel. */
 int hps_cache_set_profile_events(hps_cache* cache, void* start_event, void* end_event);
 
+/* CUDA graph capture through this library's runtime (device-mode calls
+ * enqueued on `stream` between begin and end become graph nodes; no host
+ * synchronising calls may be made in between). end_capture instantiates
+ * the graph into *graph_exec; launch replays it on `stream`. A captured
+ * lookup bakes in its recency stamp: launch such a graph once. */
+int hps_stream_begin_capture(void* stream);
+int hps_stream_end_capture(void* stream, void** graph_exec);
+int hps_graph_launch(void* graph_exec, void* stream);
+int hps_graph_destroy(void* graph_exec);
+
 /* replaces SlabCache::replace (slab_cache.cpp:93-107). Rejects a wrong
  * vector size or duplicate keys before any mutation. */
 int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n,

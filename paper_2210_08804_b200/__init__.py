@@ -134,6 +134,10 @@ SIGNATURES = {
     "hps_cache_query": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P, _SZP, C.c_int, _P]),
     "hps_cache_lookup_device": (C.c_int, [_P, _P, C.c_size_t, _P, _P, _P, _P, _P, _P]),
     "hps_cache_set_profile_events": (C.c_int, [_P, _P, _P]),
+    "hps_stream_begin_capture": (C.c_int, [_P]),
+    "hps_stream_end_capture": (C.c_int, [_P, C.POINTER(_P)]),
+    "hps_graph_launch": (C.c_int, [_P, _P]),
+    "hps_graph_destroy": (C.c_int, [_P]),
     "hps_cache_replace": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, C.c_int, _P]),
     "hps_cache_update": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _SZP, C.c_int, _P]),
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
@@ -215,6 +219,34 @@ def xxh64(data: bytes, seed: int = 0) -> int:
 
 def xxh64_key(key: int, seed: int) -> int:
     return int(lib().hps_xxh64_key(key, seed))
+
+
+class StreamGraph:
+    """CUDA graph captured from library calls on `stream` (see
+    hps_stream_begin_capture in include/hps_b200.h)."""
+
+    def __init__(self, stream: int):
+        self.stream = stream
+        self.exec = C.c_void_p()
+
+    def __enter__(self):
+        _check(lib().hps_stream_begin_capture(self.stream))
+        return self
+
+    def __exit__(self, et, ev, tb):
+        rc = lib().hps_stream_end_capture(self.stream, C.byref(self.exec))
+        if et is None:
+            _check(rc)
+
+    def launch(self, stream: int = 0):
+        _check(lib().hps_graph_launch(self.exec, stream or self.stream))
+
+    def __del__(self):
+        try:
+            if self.exec:
+                lib().hps_graph_destroy(self.exec)
+        except Exception:
+            pass
 
 
 def partition_of(key: int, partition_count: int) -> int:

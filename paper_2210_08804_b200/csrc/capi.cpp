@@ -310,6 +310,40 @@ int hps_cache_set_profile_events(hps_cache* cache, void* start_event, void* end_
   });
 }
 
+int hps_stream_begin_capture(void* stream) {
+  return guarded([&] {
+    need(stream != nullptr, "capture needs an explicit stream");
+    HPSB_CUDA(cudaStreamBeginCapture(static_cast<cudaStream_t>(stream),
+                                     cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+int hps_stream_end_capture(void* stream, void** graph_exec) {
+  return guarded([&] {
+    need(stream != nullptr && graph_exec != nullptr, "null argument");
+    cudaGraph_t g = nullptr;
+    HPSB_CUDA(cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g));
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    HPSB_CUDA(e);
+    *graph_exec = ge;
+  });
+}
+
+int hps_graph_launch(void* graph_exec, void* stream) {
+  return guarded([&] {
+    need(graph_exec != nullptr, "null graph");
+    HPSB_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), as_stream(stream)));
+  });
+}
+
+int hps_graph_destroy(void* graph_exec) {
+  return guarded([&] {
+    if (graph_exec) HPSB_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)));
+  });
+}
+
 int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n, const float* vectors,
                       size_t vectors_len, int mem, void* stream) {
   return guarded([&] {

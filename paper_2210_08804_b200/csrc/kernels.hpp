@@ -97,6 +97,7 @@ struct LookupScratch {
   // unique-miss ordering (fused tail of the probe kernel)
   uint32_t* list = nullptr;         // miss-table slots claimed this call (capacity n)
   uint32_t* list_firsts = nullptr;  // their first positions (capacity n)
+  uint64_t* list_keys = nullptr;    // their keys (capacity n)
   uint32_t* list_ctr = nullptr;     // 1 word, left at 0 by the tail
   uint32_t* bitmap = nullptr;       // ceil(n/32) words, left zeroed by the tail
   uint32_t* word_prefix = nullptr;  // ceil(n/32) words

@@ -63,7 +63,8 @@ size_t lookup_scratch_bytes(uint64_t cap) {
   uint64_t tcap = 16;
   while (tcap < 2 * cap) tcap <<= 1;
   const uint64_t words = (cap + 31) / 32;
-  return a256(tcap * 4) + a256(tcap * 4) + a256(cap * 4) * 3 + a256(words * 4) * 2 + a256(64);
+  return a256(tcap * 4) + a256(tcap * 4) + a256(cap * 4) * 3 + a256(cap * 8) +
+         a256(words * 4) * 2 + a256(64);
 }
 
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
@@ -83,6 +84,7 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   ls.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list_firsts = reinterpret_cast<uint32_t*>(take(cap * 4));
+  ls.list_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
   ls.bitmap = reinterpret_cast<uint32_t*>(take(words * 4));
   ls.word_prefix = reinterpret_cast<uint32_t*>(take(words * 4));
   unsigned long long* small = reinterpret_cast<unsigned long long*>(take(64));
@@ -131,13 +133,18 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
     for (uint32_t w = tid; w < words; w += kLookupThreads) bm[w] = 0;
     __syncthreads();
   }
-  // 1. first positions -> bitmap (loads batched for memory-level parallelism)
+  // 1. first positions -> bitmap (loads batched for memory-level parallelism).
+  // With at most one batch per thread (m <= 2048) the entries stay in
+  // registers through phase 3: two dependent global round trips in total.
+  const bool one = m <= uint32_t(kLookupThreads * kTailBatch);
+  uint32_t s[kTailBatch], f[kTailBatch];
+  uint64_t k[kTailBatch];
   for (uint32_t e0 = tid; e0 < m; e0 += kLookupThreads * kTailBatch) {
-    uint32_t s[kTailBatch], f[kTailBatch];
 #pragma unroll
     for (int j = 0; j < kTailBatch; ++j) {
       const uint32_t e = e0 + j * kLookupThreads;
       s[j] = e < m ? __ldcg(ls.list + e) : 0u;
+      k[j] = e < m ? __ldcg(reinterpret_cast<const unsigned long long*>(ls.list_keys) + e) : 0ull;
     }
 #pragma unroll
     for (int j = 0; j < kTailBatch; ++j) {
@@ -148,7 +155,7 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
     for (int j = 0; j < kTailBatch; ++j) {
       const uint32_t e = e0 + j * kLookupThreads;
       if (e < m) {
-        ls.list_firsts[e] = f[j];
+        if (!one) ls.list_firsts[e] = f[j];
         atomicOr(bm + (f[j] >> 5), 1u << (f[j] & 31u));
       }
     }
@@ -167,19 +174,21 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
   }
   __syncthreads();
   // 3. rank = prefix(word) + popc(bits below) -> ordered miss keys, ranks
+  (void)keys;
   for (uint32_t e0 = tid; e0 < m; e0 += kLookupThreads * kTailBatch) {
-    uint32_t s[kTailBatch], f[kTailBatch], r[kTailBatch];
+    uint32_t r[kTailBatch];
+    if (!one) {
 #pragma unroll
-    for (int j = 0; j < kTailBatch; ++j) {
-      const uint32_t e = e0 + j * kLookupThreads;
-      s[j] = e < m ? __ldcg(ls.list + e) : 0u;
-      f[j] = e < m ? ls.list_firsts[e] : 0u;  // written by this thread in phase 1
+      for (int j = 0; j < kTailBatch; ++j) {
+        const uint32_t e = e0 + j * kLookupThreads;
+        s[j] = e < m ? __ldcg(ls.list + e) : 0u;
+        f[j] = e < m ? ls.list_firsts[e] : 0u;  // written by this thread in phase 1
+        k[j] = e < m ? __ldcg(reinterpret_cast<const unsigned long long*>(ls.list_keys) + e)
+                     : 0ull;
+      }
     }
-    uint64_t k[kTailBatch];
 #pragma unroll
     for (int j = 0; j < kTailBatch; ++j) {
-      const uint32_t e = e0 + j * kLookupThreads;
-      k[j] = e < m ? keys[f[j]] : 0ull;
       const uint32_t w = f[j] >> 5;
       const uint32_t word = smem ? bm[w] : __ldcg(bm + w);
       const uint32_t pw = smem ? pre[w] : __ldcg(pre + w);
@@ -276,6 +285,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   const uint32_t d = c.d;
   const uint32_t d4 = d >> 2;
   const bool vec = (d & 3u) == 0;
+  long long ph[5] = {0, 0, 0, 0, 0};  // diagnostic phase cycles (ls.dbg)
   const uint32_t q = lane >> 2;    // probe group (leader) within a pass
   const uint32_t sub = lane & 3u;  // which 8 of the slab's 32 keys this lane checks
   while (t < tiles) {
@@ -285,6 +295,13 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     const uint64_t key = next_key;
     const uint64_t tn = t + stride;
     next_key = (tn < tiles && tn * 32 + lane < n) ? keys[tn * 32 + lane] : 0ull;
+    long long tprev = ls.dbg ? clock64() : 0;
+#define HPSB_PHASE(i)                  \
+  if (ls.dbg) {                        \
+    const long long now_ = clock64();  \
+    ph[i] += now_ - tprev;             \
+    tprev = now_;                      \
+  }
     // ---- group equal keys, hash lane-parallel ----
     const uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
     uint32_t grp = 1u << lane;
@@ -293,6 +310,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     const bool leader = valid && my_leader == lane;
     const uint32_t set = uint32_t(slabset_of(c, key));
     const uint32_t first = first_slab_of(c, key);
+    HPSB_PHASE(0)
     // ---- probe leaders, slab by slab ----
     uint32_t res = kNoSlot;                        // leader's slot
     uint32_t pend = __ballot_sync(0xFFFFFFFFu, leader);
@@ -361,6 +379,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
       }
       pend = __ballot_sync(0xFFFFFFFFu, cont);
     }
+    HPSB_PHASE(1)
     // ---- leaders: recency exchange / miss claim ----
     unsigned long long old = stamp;
     const bool stamp_it = leader && res != kNoSlot;
@@ -374,6 +393,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     }
     const uint32_t my_res = __shfl_sync(0xFFFFFFFFu, res, my_leader);
     const uint32_t my_tsl = __shfl_sync(0xFFFFFFFFu, tslot, my_leader);
+    HPSB_PHASE(2)
     // ---- gather every position's row ----
     if (vec) {
       for (uint32_t j0 = 0; j0 < 32; j0 += kGatherUnroll) {
@@ -413,6 +433,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
         for (uint32_t ch = lane; ch < d; ch += 32) out[(base + j) * d + ch] = src[ch];
       }
     }
+    HPSB_PHASE(3)
     // ---- per-position bookkeeping ----
     if (valid) {
       flags[pos] = my_res == kNoSlot ? 1 : 0;
@@ -424,12 +445,20 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
       uint32_t at = 0;
       if (lane == first_lane) at = atomicAdd(ls.list_ctr, uint32_t(__popc(cm)));
       at = __shfl_sync(0xFFFFFFFFu, at, first_lane);
-      if (claimed) ls.list[at + __popc(cm & ((1u << lane) - 1u))] = tslot;
+      if (claimed) {
+        const uint32_t e = at + __popc(cm & ((1u << lane) - 1u));
+        ls.list[e] = tslot;
+        ls.list_keys[e] = key;
+      }
       um += claimed ? 1u : 0u;
     }
     if (stamp_it) uh += (mode & 2) ? 1u : ((old != stamp) ? 1u : 0u);
+    HPSB_PHASE(4)
+#undef HPSB_PHASE
     t = tn;
   }
+  if (ls.dbg && lane == 0)
+    for (int i = 0; i < 5; ++i) atomicAdd(ls.dbg + 4 + i, (unsigned long long)ph[i]);
   lookup_block_finish(keys, n, ls, uh, um, miss_work, mode, s_counts, &s_last, s_dyn);
 }
 
@@ -482,8 +511,8 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
       std::getenv("HPSB_LOOKUP_SKIP") ? std::atoi(std::getenv("HPSB_LOOKUP_SKIP")) : 0;
   LookupScratch lsd = ls;
   if (debug) {
-    if (!dbg) cudaMalloc(&dbg, 64);
-    const unsigned long long init[4] = {~0ull, 0, 0, 0};
+    if (!dbg) cudaMalloc(&dbg, 128);
+    const unsigned long long init[16] = {~0ull};
     cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
     lsd.dbg = dbg;
   }
@@ -491,12 +520,16 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
                                           (smem_tail ? 1 : 0) | (skip & 14));
   check_launch("lookup_probe", 1);
   if (debug) {
-    unsigned long long h[4];
+    unsigned long long h[16];
     cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    std::fprintf(stderr, "lookup_timing n=%llu grid=%u body_us=%.2f tail_wait_us=%.2f tail_us=%.2f\n",
+    const double tot = double(h[4] + h[5] + h[6] + h[7] + h[8]) + 1e-9;
+    std::fprintf(stderr,
+                 "lookup_timing n=%llu grid=%u body_us=%.2f tail_wait_us=%.2f tail_us=%.2f "
+                 "phases hash=%.2f probe=%.2f exch=%.2f gather=%.2f book=%.2f warp_cycles=%.0f\n",
                  (unsigned long long)n, grid, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3,
-                 (h[3] - h[2]) * 1e-3);
+                 (h[3] - h[2]) * 1e-3, h[4] / tot, h[5] / tot, h[6] / tot, h[7] / tot, h[8] / tot,
+                 tot / double(n / 32));
   }
   return grid;
 }

@@ -52,13 +52,13 @@ def main():
     torch.cuda.synchronize()
     print(f"plain: {a.elapsed_time(b) * 1e3 / K:.2f} us/step (host enqueue {t_host * 1e6 / K:.2f} us/step)")
     # (b) graph without events
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=st):
+    g = hps.StreamGraph(sp)
+    with g:
         for s in range(K):
             step(s)
     torch.cuda.synchronize()
     a.record(st)
-    g.replay()
+    g.launch()
     b.record(st)
     torch.cuda.synchronize()
     print(f"graph: {a.elapsed_time(b) * 1e3 / K:.2f} us/step")
