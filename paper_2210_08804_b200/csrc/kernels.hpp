@@ -102,6 +102,11 @@ struct LookupScratch {
   uint32_t* bitmap = nullptr;       // ceil(n/32) words, left zeroed by the tail
   uint32_t* word_prefix = nullptr;  // ceil(n/32) words
   unsigned long long* blocks_done = nullptr;  // block-completion counter (reset by the last block)
+  // split probe / gather: the probe kernel writes each position's slot
+  // (kNoSlot = miss) and the gather kernel streams the rows
+  uint32_t* pos_slot = nullptr;               // capacity n
+  unsigned long long* gather_done = nullptr;  // gather-kernel completion counter
+  unsigned int* tail_done = nullptr;          // set by the ordering tail, cleared by the gather
   unsigned long long* dbg = nullptr;          // diagnostic phase timestamps (HPSB_DEBUG_TIMING)
 };
 // Bytes / carving of a LookupScratch for batches of up to `cap` keys (all

@@ -63,7 +63,7 @@ size_t lookup_scratch_bytes(uint64_t cap) {
   uint64_t tcap = 16;
   while (tcap < 2 * cap) tcap <<= 1;
   const uint64_t words = (cap + 31) / 32;
-  return a256(tcap * 4) + a256(tcap * 4) + a256(cap * 4) * 3 + a256(cap * 8) +
+  return a256(tcap * 4) + a256(tcap * 4) + a256(cap * 4) * 4 + a256(cap * 8) +
          a256(words * 4) * 2 + a256(64);
 }
 
@@ -85,6 +85,7 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   ls.list = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list_firsts = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  ls.pos_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.bitmap = reinterpret_cast<uint32_t*>(take(words * 4));
   ls.word_prefix = reinterpret_cast<uint32_t*>(take(words * 4));
   unsigned long long* small = reinterpret_cast<unsigned long long*>(take(64));
@@ -92,6 +93,8 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   ls.counts_prev = small + 2;  // [2..3]
   ls.blocks_done = small + 4;  // [4]
   ls.list_ctr = reinterpret_cast<uint32_t*>(small + 5);
+  ls.gather_done = small + 6;  // [6]
+  ls.tail_done = reinterpret_cast<unsigned int*>(small + 7);
   return ls;
 }
 
@@ -235,6 +238,9 @@ __device__ __forceinline__ void lookup_block_finish(const uint64_t* keys, uint64
   }
   if (miss_work) __threadfence();  // publish table / list writes before completion
   __syncthreads();
+  // this block's slots are written: the gather kernel (programmatic
+  // dependent launch) may start once every block got here
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) {
     if (s_counts[0]) atomicAdd(ls.counts + 0, (unsigned long long)s_counts[0]);
     if (s_counts[1]) atomicAdd(ls.counts + 1, (unsigned long long)s_counts[1]);
@@ -257,6 +263,11 @@ __device__ __forceinline__ void lookup_block_finish(const uint64_t* keys, uint64
                       smem);
     __syncthreads();
     if (ls.dbg && threadIdx.x == 0) ls.dbg[3] = gtimer();
+    if (threadIdx.x == 0 && !(flags_mode & 16)) {
+      // release the ordered miss list to the gather kernel's last block
+      __threadfence();
+      atomicExch(ls.tail_done, 1u);
+    }
   }
 }
 
@@ -394,8 +405,11 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     const uint32_t my_res = __shfl_sync(0xFFFFFFFFu, res, my_leader);
     const uint32_t my_tsl = __shfl_sync(0xFFFFFFFFu, tslot, my_leader);
     HPSB_PHASE(2)
-    // ---- gather every position's row ----
-    if (vec) {
+    // ---- gather every position's row (fused mode) or hand the slot to the
+    // gather kernel (split mode, default) ----
+    if (!(mode & 16)) {
+      if (valid) ls.pos_slot[pos] = my_res;
+    } else if (vec) {
       for (uint32_t j0 = 0; j0 < 32; j0 += kGatherUnroll) {
         float4 v[kGatherUnroll];
         uint32_t sj[kGatherUnroll];
@@ -462,6 +476,65 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   lookup_block_finish(keys, n, ls, uh, um, miss_work, mode, s_counts, &s_last, s_dyn);
 }
 
+// Gather kernel (split mode): launched as a programmatic dependent of the
+// probe kernel; one warp streams P positions' rows (hit: cached row, miss:
+// default row) with 128-bit L1-cached loads and evict-first stores. Its last
+// block waits for the probe kernel's ordering tail, so work queued after the
+// gather also sees the ordered miss list.
+template <int P>
+__global__ void __launch_bounds__(256)
+    k_lookup_gather(CacheDev c, uint64_t n, float* __restrict__ out,
+                    const float* __restrict__ default_row, LookupScratch ls, int mode) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t lane = lane_id();
+  const uint64_t base = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * P;
+  const uint32_t d = c.d;
+  if (base < n) {
+    const uint32_t mine = (lane < uint32_t(P) && base + lane < n) ? ls.pos_slot[base + lane] : 0u;
+    uint32_t sj[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) sj[u] = __shfl_sync(0xFFFFFFFFu, mine, u);
+    if ((d & 3u) == 0) {
+      const uint32_t d4 = d >> 2;
+      for (uint32_t ch = lane; ch < d4; ch += 32) {
+        float4 v[P];
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+          if (base + u < n && !(mode & 4)) {
+            const float* src = sj[u] != kNoSlot ? c.rows + uint64_t(sj[u]) * d : default_row;
+            v[u] = ld_row_f4(reinterpret_cast<const float4*>(src) + ch);
+          } else {
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < P; ++u)
+          if (base + u < n && !(mode & 8))
+            st_cs_f4(reinterpret_cast<float4*>(out + (base + u) * d) + ch, v[u]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (base + u >= n) continue;
+        const float* src = sj[u] != kNoSlot ? c.rows + uint64_t(sj[u]) * d : default_row;
+        for (uint32_t ch = lane; ch < d; ch += 32) out[(base + u) * d + ch] = src[ch];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long prev = atomicAdd(ls.gather_done, 1ull);
+    if (prev == gridDim.x - 1) {
+      *ls.gather_done = 0;
+      volatile unsigned int* td = ls.tail_done;
+      while (*td == 0u) {
+      }
+      __threadfence();
+      *ls.tail_done = 0u;
+    }
+  }
+}
+
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
                              const LookupScratch& ls, cudaStream_t st) {
@@ -516,9 +589,25 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
     lsd.dbg = dbg;
   }
-  v.fn<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp, lsd,
-                                          (smem_tail ? 1 : 0) | (skip & 14));
+  const int mode = (smem_tail ? 1 : 0) | (skip & 30);
+  v.fn<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp, lsd, mode);
   check_launch("lookup_probe", 1);
+  if (!(mode & 16)) {
+    constexpr int kGP = 8;
+    const uint64_t warps = (n + kGP - 1) / kGP;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((warps * 32 + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_lookup_gather<kGP>, c, n, out, default_row, lsd, mode);
+    check_launch("lookup_gather", 1);
+  }
   if (debug) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
