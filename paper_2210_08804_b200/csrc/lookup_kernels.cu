@@ -57,6 +57,7 @@ constexpr int kLookupThreads = kLookupWarps * 32;
 constexpr uint64_t kSmemTailMax = 1u << 17;  // positions ordered in shared memory
 constexpr int kTailBatch = 8;
 constexpr int kGatherUnroll = 8;
+constexpr uint32_t kStampSetBits = 11;  // 2048-entry per-block stamped-slot set
 }  // namespace
 
 size_t lookup_scratch_bytes(uint64_t cap) {
@@ -164,6 +165,7 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
     }
   }
   __syncthreads();
+  if (ls.dbg && tid == 0) ls.dbg[9] = gtimer();
   // 2. exclusive popcount prefix per bitmap word
   const uint32_t per = (words + kLookupThreads - 1) / kLookupThreads;
   const uint32_t w0 = min(words, tid * per), w1 = min(words, w0 + per);
@@ -176,6 +178,7 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
     run += __popc(smem ? bm[w] : __ldcg(bm + w));
   }
   __syncthreads();
+  if (ls.dbg && tid == 0) ls.dbg[10] = gtimer();
   // 3. rank = prefix(word) + popc(bits below) -> ordered miss keys, ranks
   (void)keys;
   for (uint32_t e0 = tid; e0 < m; e0 += kLookupThreads * kTailBatch) {
@@ -208,6 +211,7 @@ __device__ __noinline__ void order_misses_tail(const uint64_t* __restrict__ keys
     }
   }
   __syncthreads();
+  if (ls.dbg && tid == 0) ls.dbg[11] = gtimer();
   if (!smem)
     for (uint32_t w = w0; w < w1; ++w) bm[w] = 0;
   if (tid == 0) *ls.list_ctr = 0;
@@ -283,7 +287,10 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   extern __shared__ uint32_t s_dyn[];
   __shared__ unsigned int s_counts[2];
   __shared__ bool s_last;
+  __shared__ uint32_t s_stamped[1u << kStampSetBits];
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+  for (uint32_t i = threadIdx.x; i < (1u << kStampSetBits); i += blockDim.x)
+    s_stamped[i] = kNoSlot;
   __syncthreads();
   const uint32_t lane = lane_id();
   if (ls.dbg && threadIdx.x == 0) atomicMin(ls.dbg + 0, gtimer());
@@ -392,8 +399,25 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     }
     HPSB_PHASE(1)
     // ---- leaders: recency exchange / miss claim ----
+    // The block-level stamped set sends each slot's exchange to L2 once per
+    // block: the hottest key is a leader in every tile, and 2048 exchanges
+    // on one counter would serialise in one L2 slice.
     unsigned long long old = stamp;
-    const bool stamp_it = leader && res != kNoSlot;
+    bool stamp_it = leader && res != kNoSlot;
+    if (stamp_it) {
+      uint32_t h = (res * 0x9E3779B1u) >> (32 - kStampSetBits);
+      bool first_here = true;
+      for (int probe = 0; probe < 16; ++probe) {
+        const uint32_t cur = atomicCAS(&s_stamped[h], kNoSlot, res);
+        if (cur == kNoSlot) break;
+        if (cur == res) {
+          first_here = false;
+          break;
+        }
+        h = (h + 1) & ((1u << kStampSetBits) - 1u);
+      }
+      stamp_it = first_here;
+    }
     if (stamp_it && !(mode & 2))
       old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
     bool claimed = false;
@@ -619,6 +643,9 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
                  (unsigned long long)n, grid, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3,
                  (h[3] - h[2]) * 1e-3, h[4] / tot, h[5] / tot, h[6] / tot, h[7] / tot, h[8] / tot,
                  tot / double(n / 32));
+    std::fprintf(stderr, "  tail phases: firsts=%.2f scan=%.2f ranks=%.2f end=%.2f us\n",
+                 (h[9] - h[2]) * 1e-3, (h[10] - h[9]) * 1e-3, (h[11] - h[10]) * 1e-3,
+                 (h[3] - h[11]) * 1e-3);
   }
   return grid;
 }
