@@ -32,7 +32,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
   uint64_t t = uint64_t(blockIdx.x) * kLookupWarps + (threadIdx.x >> 5);
   uint32_t uh = 0, um = 0;
   bool miss_work = false;
+  const unsigned long long t_start = ls.dbg ? gtimer() : 0ull;
   uint64_t next_key = (t < tiles && t * 32 + lane < n) ? keys[t * 32 + lane] : 0ull;
   const uint32_t d = c.d;
   const uint32_t d4 = d >> 2;
@@ -495,8 +498,14 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
 #undef HPSB_PHASE
     t = tn;
   }
-  if (ls.dbg && lane == 0)
+  if (ls.dbg && lane == 0) {
     for (int i = 0; i < 5; ++i) atomicAdd(ls.dbg + 4 + i, (unsigned long long)ph[i]);
+    // per-warp start / end / miss-work stamps (diagnostic)
+    const uint64_t wid = uint64_t(blockIdx.x) * kLookupWarps + (threadIdx.x >> 5);
+    ls.dbg[16 + 3 * wid + 0] = t_start;
+    ls.dbg[16 + 3 * wid + 1] = gtimer();
+    ls.dbg[16 + 3 * wid + 2] = (miss_work ? 1u : 0u) | (um ? 2u : 0u);
+  }
   lookup_block_finish(keys, n, ls, uh, um, miss_work, mode, s_counts, &s_last, s_dyn);
 }
 
@@ -608,8 +617,8 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
       std::getenv("HPSB_LOOKUP_SKIP") ? std::atoi(std::getenv("HPSB_LOOKUP_SKIP")) : 0;
   LookupScratch lsd = ls;
   if (debug) {
-    if (!dbg) cudaMalloc(&dbg, 128);
-    const unsigned long long init[16] = {~0ull};
+    if (!dbg) cudaMalloc(&dbg, (16 + 3 * 8192) * 8);
+    static unsigned long long init[16 + 3 * 8192] = {~0ull};
     cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
     lsd.dbg = dbg;
   }
@@ -646,6 +655,29 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     std::fprintf(stderr, "  tail phases: firsts=%.2f scan=%.2f ranks=%.2f end=%.2f us\n",
                  (h[9] - h[2]) * 1e-3, (h[10] - h[9]) * 1e-3, (h[11] - h[10]) * 1e-3,
                  (h[3] - h[11]) * 1e-3);
+    const unsigned warps = grid * kLookupWarps;
+    static unsigned long long w[3 * 8192];
+    cudaMemcpy(w, dbg + 16, size_t(warps) * 3 * 8, cudaMemcpyDeviceToHost);
+    std::vector<double> st_off, life, life_miss, life_nomiss;
+    unsigned long long t0 = ~0ull;
+    for (unsigned i = 0; i < warps; ++i) t0 = std::min(t0, w[3 * i]);
+    for (unsigned i = 0; i < warps; ++i) {
+      st_off.push_back((w[3 * i] - t0) * 1e-3);
+      const double l = (w[3 * i + 1] - w[3 * i]) * 1e-3;
+      life.push_back(l);
+      (w[3 * i + 2] & 1 ? life_miss : life_nomiss).push_back(l);
+    }
+    auto pct = [](std::vector<double> v, double p) {
+      if (v.empty()) return 0.0;
+      std::sort(v.begin(), v.end());
+      return v[size_t(p * (v.size() - 1))];
+    };
+    std::fprintf(stderr,
+                 "  warps: start p50=%.2f p99=%.2f max=%.2f | life p10=%.2f p50=%.2f p90=%.2f "
+                 "max=%.2f | life(miss) p50=%.2f (n=%zu) life(no miss) p50=%.2f\n",
+                 pct(st_off, .5), pct(st_off, .99), pct(st_off, 1), pct(life, .1), pct(life, .5),
+                 pct(life, .9), pct(life, 1), pct(life_miss, .5), life_miss.size(),
+                 pct(life_nomiss, .5));
   }
   return grid;
 }
