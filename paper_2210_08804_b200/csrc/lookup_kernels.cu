@@ -335,6 +335,66 @@ __global__ void __launch_bounds__(kLookupThreads, MINB)
     // ---- probe leaders, slab by slab ----
     uint32_t res = kNoSlot;                        // leader's slot
     uint32_t pend = __ballot_sync(0xFFFFFFFFu, leader);
+    if (c.W == 2) {
+      // Two slabs per set (every configured geometry): both probe slabs and
+      // masks are loaded in the same round, so one dependent round trip
+      // resolves a leader (probe order first, first+1; the second slab only
+      // counts if the first is full -- slab_cache.cpp:249-256).
+      const uint32_t slab_a = set * 2 + first;
+      const uint32_t slab_b = set * 2 + (first ^ 1u);
+      const uint32_t np = __popc(pend);
+      const uint32_t my_rank = __popc(pend & ((1u << lane) - 1u));
+      for (uint32_t pass = 0; pass < np; pass += 8) {
+        uint64_t ka[8], kb[8];
+        uint32_t ma = 0, mb = 0;
+        const uint32_t e = pass + q;
+        const bool act = e < np;
+        const uint32_t src = act ? __fns(pend, 0, int(e) + 1) : lane;
+        const uint64_t qkey = __shfl_sync(0xFFFFFFFFu, key, src);
+        const uint32_t sa = __shfl_sync(0xFFFFFFFFu, slab_a, src);
+        const uint32_t sbb = __shfl_sync(0xFFFFFFFFu, slab_b, src);
+        if (act) {
+          ma = c.masks[sa];
+          mb = c.masks[sbb];
+          const ulonglong2* pa =
+              reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(sa) * kSlotsPerSlab) + sub * 4;
+          const ulonglong2* pb =
+              reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(sbb) * kSlotsPerSlab) + sub * 4;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const ulonglong2 va = pa[j];
+            const ulonglong2 vb = pb[j];
+            ka[2 * j] = va.x;
+            ka[2 * j + 1] = va.y;
+            kb[2 * j] = vb.x;
+            kb[2 * j + 1] = vb.y;
+          }
+        }
+        uint32_t ha = 32, hb = 32;
+        if (act) {
+#pragma unroll
+          for (int j = 7; j >= 0; --j) {
+            const uint32_t s = sub * 8 + j;
+            if (((ma >> s) & 1u) && ka[j] == qkey) ha = s;
+            if (((mb >> s) & 1u) && kb[j] == qkey) hb = s;
+          }
+        }
+        ha = min(ha, __shfl_xor_sync(0xFFFFFFFFu, ha, 1));
+        ha = min(ha, __shfl_xor_sync(0xFFFFFFFFu, ha, 2));
+        hb = min(hb, __shfl_xor_sync(0xFFFFFFFFu, hb, 1));
+        hb = min(hb, __shfl_xor_sync(0xFFFFFFFFu, hb, 2));
+        uint32_t found = kNoSlot;
+        if (ha < 32)
+          found = sa * kSlotsPerSlab + ha;
+        else if (act && ma == kFullSlab && hb < 32)
+          found = sbb * kSlotsPerSlab + hb;
+        const uint32_t rank_in_round = my_rank - pass;
+        const uint32_t from = (rank_in_round < 8u) ? rank_in_round * 4 : lane;
+        const uint32_t f = __shfl_sync(0xFFFFFFFFu, found, from);
+        if (((pend >> lane) & 1u) && rank_in_round < 8u) res = f;
+      }
+      pend = 0;
+    }
     for (uint32_t step = 0; step < c.W && pend; ++step) {
       uint32_t sl = first + step;
       sl = (sl >= c.W) ? sl - c.W : sl;
