@@ -628,10 +628,212 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Quad kernel (default): a warp serves 8 positions, 4 lanes per position, so
+// one position's whole chain is short -- key load, both placement hashes, ONE
+// round trip for both probe slabs + masks (each lane compares 8 of the 32
+// keys of each slab; a 4-lane min picks the lowest matching slot), ONE round
+// trip for the row (each lane moves a quarter of it with 128-bit loads and
+// evict-first stores). Hot keys hit the SM's L1 for slabs and rows; a
+// per-block stamped-slot set keeps their recency exchanges off one L2 line.
+constexpr int kQuadPos = 8;       // positions per warp
+constexpr int kQuadSetBits = 7;   // 128-entry per-block stamped set (64 positions)
+constexpr int kQuadRowChunks = 8; // float4 chunks per lane held in flight (d <= 128)
+
+__global__ void __launch_bounds__(kLookupThreads)
+    k_lookup_quad(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                  float* __restrict__ out, uint8_t* __restrict__ flags,
+                  const float* __restrict__ default_row, uint64_t stamp, LookupScratch ls,
+                  int mode) {
+  extern __shared__ uint32_t s_dyn[];
+  __shared__ unsigned int s_counts[2];
+  __shared__ bool s_last;
+  __shared__ uint32_t s_stamped[1u << kQuadSetBits];
+  if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+  for (uint32_t i = threadIdx.x; i < (1u << kQuadSetBits); i += blockDim.x) s_stamped[i] = kNoSlot;
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint32_t q = lane >> 2, sub = lane & 3u;
+  const uint64_t pos = ((uint64_t(blockIdx.x) * kLookupThreads + threadIdx.x) >> 5) * kQuadPos + q;
+  const bool valid = pos < n;
+  uint32_t uh = 0, um = 0;
+  bool miss_work = false;
+  const uint64_t key = valid ? keys[pos] : 0ull;
+  // ---- placement + both probe slabs in one round trip ----
+  const uint32_t set = uint32_t(slabset_of(c, key));
+  const uint32_t first = first_slab_of(c, key);
+  uint32_t res = kNoSlot;
+  if (c.W == 2) {
+    const uint32_t sa = set * 2 + first, sb = set * 2 + (first ^ 1u);
+    uint32_t ma = 0, mb = 0;
+    uint64_t ka[8], kb[8];
+    if (valid) {
+      ma = c.masks[sa];
+      mb = c.masks[sb];
+      const ulonglong2* pa =
+          reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(sa) * kSlotsPerSlab) + sub * 4;
+      const ulonglong2* pb =
+          reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(sb) * kSlotsPerSlab) + sub * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const ulonglong2 va = pa[j];
+        const ulonglong2 vb = pb[j];
+        ka[2 * j] = va.x;
+        ka[2 * j + 1] = va.y;
+        kb[2 * j] = vb.x;
+        kb[2 * j + 1] = vb.y;
+      }
+    }
+    uint32_t ha = 32, hb = 32;
+    if (valid) {
+#pragma unroll
+      for (int j = 7; j >= 0; --j) {
+        const uint32_t s = sub * 8 + j;
+        if (((ma >> s) & 1u) && ka[j] == key) ha = s;
+        if (((mb >> s) & 1u) && kb[j] == key) hb = s;
+      }
+    }
+    ha = min(ha, __shfl_xor_sync(0xFFFFFFFFu, ha, 1));
+    ha = min(ha, __shfl_xor_sync(0xFFFFFFFFu, ha, 2));
+    hb = min(hb, __shfl_xor_sync(0xFFFFFFFFu, hb, 1));
+    hb = min(hb, __shfl_xor_sync(0xFFFFFFFFu, hb, 2));
+    if (ha < 32)
+      res = sa * kSlotsPerSlab + ha;
+    else if (ma == kFullSlab && hb < 32)
+      res = sb * kSlotsPerSlab + hb;
+  } else {
+    // general W: slab by slab in probe order; a group stops at a hit or at
+    // the first slab that is not full
+    bool pending = valid;
+    for (uint32_t step = 0; step < c.W; ++step) {
+      if (!__any_sync(0xFFFFFFFFu, pending)) break;
+      uint32_t sl = first + step;
+      sl = (sl >= c.W) ? sl - c.W : sl;
+      const uint32_t slab = set * c.W + sl;
+      uint32_t m = 0;
+      uint64_t kk[8];
+      if (pending) {
+        m = c.masks[slab];
+        const ulonglong2* p2 =
+            reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(slab) * kSlotsPerSlab) + sub * 4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const ulonglong2 v = p2[j];
+          kk[2 * j] = v.x;
+          kk[2 * j + 1] = v.y;
+        }
+      }
+      uint32_t h = 32;
+      if (pending) {
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+          const uint32_t s = sub * 8 + j;
+          if (((m >> s) & 1u) && kk[j] == key) h = s;
+        }
+      }
+      h = min(h, __shfl_xor_sync(0xFFFFFFFFu, h, 1));
+      h = min(h, __shfl_xor_sync(0xFFFFFFFFu, h, 2));
+      if (pending) {
+        if (h < 32) {
+          res = slab * kSlotsPerSlab + h;
+          pending = false;
+        } else if (m != kFullSlab) {
+          pending = false;
+        }
+      }
+    }
+  }
+  // ---- recency exchange (leader lane of the group), issued before the copy ----
+  unsigned long long old = stamp;
+  bool stamp_it = valid && sub == 0 && res != kNoSlot;
+  if (stamp_it) {
+    uint32_t h = (res * 0x9E3779B1u) >> (32 - kQuadSetBits);
+    for (int probe = 0; probe < 16; ++probe) {
+      const uint32_t cur = atomicCAS(&s_stamped[h], kNoSlot, res);
+      if (cur == kNoSlot) break;
+      if (cur == res) {
+        stamp_it = false;
+        break;
+      }
+      h = (h + 1) & ((1u << kQuadSetBits) - 1u);
+    }
+  }
+  if (stamp_it && !(mode & 2))
+    old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
+  // ---- copy the row: lane `sub` moves float4 chunks sub, sub+4, ... ----
+  if (valid) {
+    const uint32_t d = c.d;
+    const float* src = res != kNoSlot ? c.rows + uint64_t(res) * d : default_row;
+    float* dst = out + pos * d;
+    if ((d & 3u) == 0) {
+      const uint32_t d4 = d >> 2;
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4* o4 = reinterpret_cast<float4*>(dst);
+      for (uint32_t ch0 = 0; ch0 < d4; ch0 += 4 * kQuadRowChunks) {
+        float4 v[kQuadRowChunks];
+#pragma unroll
+        for (int j = 0; j < kQuadRowChunks; ++j) {
+          const uint32_t ch = ch0 + uint32_t(j) * 4 + sub;
+          if (ch < d4 && !(mode & 4)) v[j] = ld_row_f4(s4 + ch);
+        }
+#pragma unroll
+        for (int j = 0; j < kQuadRowChunks; ++j) {
+          const uint32_t ch = ch0 + uint32_t(j) * 4 + sub;
+          if (ch < d4 && !(mode & 8)) st_cs_f4(o4 + ch, (mode & 4) ? make_float4(0, 0, 0, 0) : v[j]);
+        }
+      }
+    } else {
+      for (uint32_t ch = sub; ch < d; ch += 4) dst[ch] = src[ch];
+    }
+  }
+  // ---- misses: leader lane claims the key; bookkeeping ----
+  bool claimed = false;
+  uint32_t tslot = 0;
+  if (valid && sub == 0 && res == kNoSlot) {
+    tslot = miss_insert(ls.miss_table, ls.cap, keys, key, uint32_t(pos), &claimed);
+    ls.miss_slot[pos] = tslot;
+    miss_work = true;
+  }
+  if (valid && sub == 0) flags[pos] = res == kNoSlot ? 1 : 0;
+  const uint32_t cm = __ballot_sync(0xFFFFFFFFu, claimed);
+  if (cm) {
+    const uint32_t first_lane = __ffs(cm) - 1;
+    uint32_t at = 0;
+    if (lane == first_lane) at = atomicAdd(ls.list_ctr, uint32_t(__popc(cm)));
+    at = __shfl_sync(0xFFFFFFFFu, at, first_lane);
+    if (claimed) {
+      const uint32_t e = at + __popc(cm & ((1u << lane) - 1u));
+      ls.list[e] = tslot;
+      ls.list_keys[e] = key;
+    }
+    um = claimed ? 1u : 0u;
+  }
+  if (stamp_it) uh = (mode & 2) ? 1u : ((old != stamp) ? 1u : 0u);
+  lookup_block_finish(keys, n, ls, uh, um, miss_work, mode | 16, s_counts, &s_last, s_dyn);
+}
+
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
                              const LookupScratch& ls, cudaStream_t st) {
   if (n == 0) return 0;
+  static const int quad_off = std::getenv("HPSB_LOOKUP_VARIANT") != nullptr;
+  if (!quad_off) {
+    static std::once_flag qonce;
+    std::call_once(qonce, [] {
+      cudaFuncSetAttribute(k_lookup_quad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kSmemTailMax / 32 * 4 * 2));
+    });
+    const bool smem_tail = n <= kSmemTailMax;
+    const size_t dyn = smem_tail ? ((n + 31) / 32) * 4 * 2 : 0;
+    const uint64_t per_block = uint64_t(kLookupWarps) * kQuadPos;
+    const unsigned grid = unsigned((n + per_block - 1) / per_block);
+    static const int qskip =
+        std::getenv("HPSB_LOOKUP_SKIP") ? std::atoi(std::getenv("HPSB_LOOKUP_SKIP")) : 0;
+    k_lookup_quad<<<grid, kLookupThreads, dyn, st>>>(c, keys, n, out, flags, default_row, stamp,
+                                                     ls, (smem_tail ? 1 : 0) | (qskip & 14));
+    check_launch("lookup_quad", 1);
+    return grid;
+  }
   // Variants: minimum resident blocks per SM (register budget). The default
   // was chosen from B200 measurements (profiles/); HPSB_LOOKUP_VARIANT
   // selects another for experiments.
