@@ -283,6 +283,7 @@ def run_ours(args, rank, world, local_rank):
     outs = [torch.empty(n * d, device=dev) for _ in range(ring)]
     flags = [torch.empty(n, dtype=torch.uint8, device=dev) for _ in range(ring)]
     mkeys = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(ring)]
+    mfirsts = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(ring)]
 
     def device_run(target, steps, warmup, seed):
         batches, p, h_draw = wl.batches(target, pool, seed)
@@ -295,7 +296,8 @@ def run_ours(args, rank, world, local_rank):
             j = s % pool
             cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
                                 flags[s % ring].data_ptr(), default_row.data_ptr(),
-                                mkeys[s % ring].data_ptr(), counts.data_ptr(), sp)
+                                mkeys[s % ring].data_ptr(), mfirsts[s % ring].data_ptr(),
+                                counts.data_ptr(), sp)
         # The K steps are captured into one CUDA graph and launched once, so
         # host-side call overhead cannot starve the GPU between steps; per-step
         # and per-kernel timestamps are external event records inside it.
@@ -315,7 +317,8 @@ def run_ours(args, rank, world, local_rank):
                 cache.set_profile_events(kev[s][0].cuda_event, kev[s][1].cuda_event)
                 cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
                                     flags[s % ring].data_ptr(), default_row.data_ptr(),
-                                    mkeys[s % ring].data_ptr(), counts[2 * s:].data_ptr(), sp)
+                                    mkeys[s % ring].data_ptr(), mfirsts[s % ring].data_ptr(),
+                                    counts[2 * s:].data_ptr(), sp)
         launches = hps.kernel_launch_count() - l0  # kernel nodes in the timed graph
         cache.set_profile_events(0, 0)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -116,18 +116,21 @@ int hps_cache_query(hps_cache* cache, const uint64_t* keys, size_t n, float* out
                     size_t out_len, uint32_t* miss_positions, uint64_t* miss_keys,
                     size_t* n_miss, int mem, void* stream);
 
-/* Lookup-level query, device pointers only: the fused hot path of
+/* Lookup-level query, device pointers only: the hot path of
  * hps_engine_lookup without the tier logic (LookupEngine::lookup's dedup ->
  * query -> expand, lookup_engine.cpp:131-153,194-203). Bumps the recency
  * clock once; out (n * dim) gets every position's row -- the cached row on
  * a hit, default_row (dim floats, device) on a miss; miss_flags[n] = 1 on a
- * miss; miss_keys (capacity n) gets the unique missing keys in
- * first-occurrence order; counts[2] = {unique hits, unique misses} of this
- * call (so h = 1 - counts[1] / (counts[0] + counts[1])). Stream-ordered:
- * returns without synchronising. */
+ * miss; miss_keys / miss_firsts (capacity n each) get the unique missing
+ * keys and their first-occurrence positions, one entry per key in claim
+ * order -- sorting by position gives the reference's miss order;
+ * counts[2] = {unique hits, unique misses} of this call (so
+ * h = 1 - counts[1] / (counts[0] + counts[1]), and counts[1] entries are
+ * valid). Stream-ordered: returns without synchronising. */
 int hps_cache_lookup_device(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
                             uint8_t* miss_flags, const float* default_row,
-                            uint64_t* miss_keys, uint64_t* counts, void* stream);
+                            uint64_t* miss_keys, uint32_t* miss_firsts, uint64_t* counts,
+                            void* stream);
 
 /* Diagnostic: record these cudaEvent_t (as void*) on the cache stream right
  * before / after the probe kernel of subsequent hps_cache_lookup_device

@@ -132,7 +132,7 @@ SIGNATURES = {
     "hps_cache_get_info": (C.c_int, [_P, C.POINTER(_CacheInfo)]),
     "hps_cache_stream": (_P, [_P]),
     "hps_cache_query": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P, _SZP, C.c_int, _P]),
-    "hps_cache_lookup_device": (C.c_int, [_P, _P, C.c_size_t, _P, _P, _P, _P, _P, _P]),
+    "hps_cache_lookup_device": (C.c_int, [_P, _P, C.c_size_t, _P, _P, _P, _P, _P, _P, _P]),
     "hps_cache_set_profile_events": (C.c_int, [_P, _P, _P]),
     "hps_stream_begin_capture": (C.c_int, [_P]),
     "hps_stream_end_capture": (C.c_int, [_P, C.POINTER(_P)]),
@@ -363,13 +363,14 @@ class SlabCache:
         return nm.value
 
     def lookup_device(self, keys_ptr: int, n: int, out_ptr: int, flags_ptr: int,
-                      default_row_ptr: int, miss_keys_ptr: int, counts_ptr: int,
-                      stream: int = 0) -> None:
-        """hps_cache_lookup_device: the fused lookup hot path on device
-        pointers, stream-ordered (no host sync)."""
+                      default_row_ptr: int, miss_keys_ptr: int, miss_firsts_ptr: int,
+                      counts_ptr: int, stream: int = 0) -> None:
+        """hps_cache_lookup_device: the lookup hot path on device pointers,
+        stream-ordered (no host sync). Unique misses come back as (key, first
+        position) in claim order; sort by position for the reference order."""
         _check(lib().hps_cache_lookup_device(self._h, keys_ptr, n, out_ptr, flags_ptr,
-                                             default_row_ptr, miss_keys_ptr, counts_ptr,
-                                             stream or None))
+                                             default_row_ptr, miss_keys_ptr, miss_firsts_ptr,
+                                             counts_ptr, stream or None))
 
     def set_profile_events(self, start_event: int = 0, end_event: int = 0) -> None:
         _check(lib().hps_cache_set_profile_events(self._h, start_event or None,

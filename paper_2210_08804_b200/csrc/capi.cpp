@@ -293,12 +293,13 @@ int hps_cache_query(hps_cache* cache, const uint64_t* keys, size_t n, float* out
 
 int hps_cache_lookup_device(hps_cache* cache, const uint64_t* keys, size_t n, float* out,
                             uint8_t* miss_flags, const float* default_row, uint64_t* miss_keys,
-                            uint64_t* counts, void* stream) {
+                            uint32_t* miss_firsts, uint64_t* counts, void* stream) {
   return guarded([&] {
     need(cache && counts, "null argument");
-    need(n == 0 || (keys && out && miss_flags && default_row && miss_keys), "null argument");
-    cache->impl->lookup_device(keys, n, out, miss_flags, default_row, miss_keys, counts,
-                               as_stream(stream));
+    need(n == 0 || (keys && out && miss_flags && default_row && miss_keys && miss_firsts),
+         "null argument");
+    cache->impl->lookup_device(keys, n, out, miss_flags, default_row, miss_keys, miss_firsts,
+                               counts, as_stream(stream));
   });
 }
 

@@ -176,8 +176,8 @@ size_t DeviceCache::query(const uint64_t* keys, size_t n, float* out, size_t out
 }
 
 void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint8_t* flags,
-                                const float* default_row, uint64_t* miss_keys, uint64_t* counts,
-                                cudaStream_t user) {
+                                const float* default_row, uint64_t* miss_keys,
+                                uint32_t* miss_firsts, uint64_t* counts, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
   const uint64_t stamp = bump_clock();
   DeviceGuard g(device_);
@@ -189,8 +189,8 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   }
   if (n >= (1ull << 32)) throw invalid_argument("lookup batch too large");
   if (n > lcap_) {
-    // (re)carve: miss table >= 2n entries, per-position slots, miss list,
-    // ordering bitmap, counters -- zeroed once, then kept clean by the kernel
+    // (re)carve: miss table >= 2n entries, per-position slots, claim list,
+    // counters -- zeroed once, then kept clean by the kernels
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
     const uint64_t bytes = lookup_scratch_bytes(cap);
@@ -198,9 +198,11 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     HPSB_CUDA(cudaMemsetAsync(b, 0, bytes, stream_));
     lws_ = lookup_scratch_carve(b, cap);
     lcap_ = cap;
+    lparity_ = 0;
   }
   LookupScratch ls = lws_;
-  ls.miss_keys = miss_keys;
+  ls.list_keys = miss_keys;
+  ls.list_firsts = miss_firsts;
   ls.counts_out = reinterpret_cast<unsigned long long*>(counts);
   // profile events: external records when the stream is being captured into
   // a CUDA graph, so the timestamps stay readable after graph launches
@@ -209,7 +211,8 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   const unsigned rec_flags =
       cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (prof_start_) HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
-  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, stream_);
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, lparity_, stream_);
+  lparity_ ^= 1u;
   if (prof_end_) HPSB_CUDA(cudaEventRecordWithFlags(prof_end_, stream_, rec_flags));
   join_to(user);
 }

@@ -46,14 +46,15 @@ class DeviceCache {
   // slab_cache.cpp:109-125
   size_t update(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
                 int mem, cudaStream_t user);
-  // Lookup-level query on device pointers (the engine's fused hot path
-  // without the tier logic): bumps the clock, writes every position's row
-  // (hit: cached row, miss: default_row), miss flags, the unique misses in
-  // first-occurrence order and {unique hits, unique misses} of this call to
+  // Lookup-level query on device pointers (the engine's hot path without
+  // the tier logic): bumps the clock, writes every position's row (hit:
+  // cached row, miss: default_row), miss flags, the unique missing keys with
+  // their first-occurrence positions (claim order; ascending position = the
+  // reference's order) and {unique hits, unique misses} of this call to
   // device memory. Stream-ordered, no host synchronisation.
   void lookup_device(const uint64_t* keys, size_t n, float* out, uint8_t* flags,
-                     const float* default_row, uint64_t* miss_keys, uint64_t* counts,
-                     cudaStream_t user);
+                     const float* default_row, uint64_t* miss_keys, uint32_t* miss_firsts,
+                     uint64_t* counts, cudaStream_t user);
   // Diagnostic: events recorded around the probe kernel of the next
   // lookup_device calls (null = off).
   void set_profile_events(cudaEvent_t start, cudaEvent_t end) {
@@ -110,6 +111,7 @@ class DeviceCache {
   DeviceBuffer lbuf_;
   LookupScratch lws_;
   uint64_t lcap_ = 0;
+  uint32_t lparity_ = 0;
   cudaEvent_t prof_start_ = nullptr, prof_end_ = nullptr;
   unsigned long long* d_small_ = nullptr;  // small device counters
   unsigned long long* h_small_ = nullptr;  // pinned mirror

@@ -121,14 +121,13 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   d_row_of = reinterpret_cast<int32_t*>(take(cap * 4));
   d_staged = reinterpret_cast<float*>(take(cap * uint64_t(d) * 4));
   d_found_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
-  uint64_t* d_miss_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);
-  ls.miss_keys = d_miss_keys;
+  parity = 0;
   prev_counts[0] = prev_counts[1] = 0;
 
-  const uint64_t host_bytes = a256(cap * 8) * 4 + a256(16) + a256(cap * 4) +
+  const uint64_t host_bytes = a256(cap * 8) * 5 + a256(16) + a256(cap * 4) * 3 +
                               a256(cap * uint64_t(d) * 4) * 2 + a256(cap);
   char* h = static_cast<char*>(hbuf.ensure(host_bytes));
   auto htake = [&](uint64_t bytes) {
@@ -145,6 +144,9 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   h_missing = reinterpret_cast<uint64_t*>(htake(cap * 8));
   h_flags = reinterpret_cast<uint8_t*>(htake(cap));
   h_out = reinterpret_cast<float*>(htake(cap * uint64_t(d) * 4));
+  h_claim_keys = reinterpret_cast<uint64_t*>(htake(cap * 8));
+  h_claim_firsts = reinterpret_cast<uint32_t*>(htake(cap * 4));
+  h_row_of_claim = reinterpret_cast<int32_t*>(htake(cap * 4));
   HPSB_CUDA(cudaStreamSynchronize(st));
   capacity = cap;
   dim = d;
@@ -278,8 +280,9 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       } else {
         cache_->join_from(user);
       }
-      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags,
-                                                d_default_, stamp, ws->ls, st);
+      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->ls,
+                          ws->parity, st);
+      ws->parity ^= 1u;
       HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts, 16, cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }
@@ -291,10 +294,20 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
     ws->prev_counts[0] = ws->h_counts[0];
     ws->prev_counts[1] = ws->h_counts[1];
     if (um > 0) {
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_miss_keys, ws->ls.miss_keys, um * 8,
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->ls.list_keys, um * 8,
+                                cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->ls.list_firsts, um * 4,
                                 cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
       HPSB_CUDA(cudaEventSynchronize(ws->done));
+      // the reference's miss order: unique misses by first occurrence
+      // (types.cpp:20-34 + slab_cache.cpp:84-89)
+      ws->order.resize(um);
+      for (uint32_t e = 0; e < um; ++e) ws->order[e] = e;
+      const uint32_t* fp = ws->h_claim_firsts;
+      std::sort(ws->order.begin(), ws->order.end(),
+                [fp](uint32_t a, uint32_t b) { return fp[a] < fp[b]; });
+      for (uint64_t k = 0; k < um; ++k) ws->h_miss_keys[k] = ws->h_claim_keys[ws->order[k]];
     }
   }
   const uint64_t n_unique = uh + um;
@@ -309,7 +322,10 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
     defaults = absent;
     std::lock_guard<std::mutex> lk(cache_->mutex());
     if (nf > 0) {
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of, um * 4, cudaMemcpyHostToDevice, st));
+      // row_of is in miss order; the scatter kernel indexes by claim
+      for (uint64_t k = 0; k < um; ++k) ws->h_row_of_claim[ws->order[k]] = ws->h_row_of[k];
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, um * 4, cudaMemcpyHostToDevice,
+                                st));
       HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
                                 cudaMemcpyHostToDevice, st));
       HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,

@@ -82,6 +82,7 @@ struct Workspace {
   float* d_staged = nullptr;
   uint64_t* d_found_keys = nullptr;
   LookupScratch ls;
+  uint32_t parity = 0;
   unsigned long long prev_counts[2] = {0, 0};
   // pinned host
   PinnedBuffer hbuf;
@@ -94,6 +95,10 @@ struct Workspace {
   uint64_t* h_missing = nullptr;
   uint8_t* h_flags = nullptr;
   float* h_out = nullptr;
+  uint64_t* h_claim_keys = nullptr;    // unique misses in claim order
+  uint32_t* h_claim_firsts = nullptr;  // their first positions
+  int32_t* h_row_of_claim = nullptr;   // staged row per claim (sync branch)
+  std::vector<uint32_t> order;         // claims sorted by first position
   // batch state (for the async task)
   std::vector<uint64_t> missing_keys;
   cudaEvent_t done = nullptr;

@@ -83,42 +83,35 @@ void launch_dedup(const uint64_t* keys, uint64_t n, uint64_t* unique_out, uint32
                   cudaStream_t st);
 
 // ---- lookup (lookup_engine.cpp:130-241) ----
+// Per-call scratch of the lookup kernels. A lookup's unique misses come out
+// as a CLAIM LIST (one entry per missing key, in claim order) with each
+// key's first-occurrence position; sorting the claims by that position gives
+// the reference's order (dedup first-occurrence order, types.cpp:20-34, then
+// ascending miss positions, slab_cache.cpp:84-89).
 struct LookupScratch {
-  uint64_t cap = 0;               // miss table capacity (power of two >= 2 * max_batch)
-  uint32_t* miss_table = nullptr; // 0 = empty, else first position + 1 (cleared by the tail)
-  uint32_t* miss_slot = nullptr;  // per position (valid where missed)
-  uint32_t* rank_of_slot = nullptr;
+  uint64_t cap = 0;                  // miss table capacity (power of two >= 2 * batch)
+  uint32_t* miss_table = nullptr;    // 0 = empty, else first position + 1; cleared per call
+  uint32_t* claim_of_slot = nullptr; // miss-table slot -> claim index
+  uint32_t* miss_slot = nullptr;     // per position (valid where missed)
   unsigned long long* counts = nullptr;  // [0] unique hits, [1] unique misses (cumulative)
-  uint64_t* miss_keys = nullptr;  // unique misses, first-occurrence order
-  // optional per-call deltas written by the ordering tail:
-  // counts_out = counts - counts_prev; counts_prev = counts
-  unsigned long long* counts_prev = nullptr;
-  unsigned long long* counts_out = nullptr;
-  // unique-miss ordering (fused tail of the probe kernel)
-  uint32_t* list = nullptr;         // miss-table slots claimed this call (capacity n)
-  uint32_t* list_firsts = nullptr;  // their first positions (capacity n)
-  uint64_t* list_keys = nullptr;    // their keys (capacity n)
-  uint32_t* list_ctr = nullptr;     // 1 word, left at 0 by the tail
-  uint32_t* bitmap = nullptr;       // ceil(n/32) words, left zeroed by the tail
-  uint32_t* word_prefix = nullptr;  // ceil(n/32) words
-  unsigned long long* blocks_done = nullptr;  // block-completion counter (reset by the last block)
-  // split probe / gather: the probe kernel writes each position's slot
-  // (kNoSlot = miss) and the gather kernel streams the rows
-  uint32_t* pos_slot = nullptr;               // capacity n
-  unsigned long long* gather_done = nullptr;  // gather-kernel completion counter
-  unsigned int* tail_done = nullptr;          // set by the ordering tail, cleared by the gather
-  unsigned long long* dbg = nullptr;          // diagnostic phase timestamps (HPSB_DEBUG_TIMING)
+  unsigned long long* counts_prev = nullptr;  // finalize: per-call deltas
+  unsigned long long* counts_out = nullptr;   // optional per-call counts destination
+  uint32_t* list = nullptr;          // claim -> miss-table slot (capacity n)
+  uint64_t* list_keys = nullptr;     // claim -> key (capacity n)
+  uint32_t* list_firsts = nullptr;   // claim -> first position (written by finalize)
+  uint32_t* list_ctr = nullptr;      // [2]: claim counters, double-buffered by call parity
 };
 // Bytes / carving of a LookupScratch for batches of up to `cap` keys (all
 // regions zero-initialised by the caller once).
 size_t lookup_scratch_bytes(uint64_t cap);
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
-// One launch per lookup: probe + gather + stamps + miss dedup, and the last
-// block to finish orders the unique misses. Returns the grid size (the
-// caller may report it).
+// Two launches per lookup: the lookup kernel (probe, stamps, row gather /
+// default rows, miss claims) and the finalize kernel (first positions of the
+// claims, miss-table cleanup, per-call counts). `parity` alternates per call
+// on the same scratch. Returns the number of kernels launched.
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupScratch& ls, cudaStream_t st);
+                             const LookupScratch& ls, uint32_t parity, cudaStream_t st);
 void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint8_t* flags,
                            const LookupScratch& ls, const int32_t* row_of,
                            const float* staged, float* out, cudaStream_t st);

@@ -29,6 +29,7 @@ def main():
     outs = [torch.empty(n * d, device="cuda") for _ in range(8)]
     fl = [torch.empty(n, dtype=torch.uint8, device="cuda") for _ in range(8)]
     mk = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(8)]
+    mf = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(8)]
     dr = torch.zeros(d, device="cuda")
     K = 200
     counts = torch.zeros(2 * K, dtype=torch.int64, device="cuda")
@@ -36,7 +37,7 @@ def main():
 
     def step(s):
         cache.lookup_device(dk[s % 32].data_ptr(), n, outs[s % 8].data_ptr(), fl[s % 8].data_ptr(),
-                            dr.data_ptr(), mk[s % 8].data_ptr(), counts[2 * s:].data_ptr(), sp)
+                            dr.data_ptr(), mk[s % 8].data_ptr(), mf[s % 8].data_ptr(), counts[2 * s:].data_ptr(), sp)
 
     for s in range(10):
         step(s)
@@ -68,10 +69,11 @@ def main():
     ref_out = torch.empty(n * d, device="cuda")
     rfl = torch.empty(n, dtype=torch.uint8, device="cuda")
     rmk = torch.empty(n, dtype=torch.int64, device="cuda")
+    rmf = torch.empty(n, dtype=torch.int32, device="cuda")
     rc = torch.zeros(2, dtype=torch.int64, device="cuda")
     s = K - 1
     cache.lookup_device(dk[s % 32].data_ptr(), n, ref_out.data_ptr(), rfl.data_ptr(), dr.data_ptr(),
-                        rmk.data_ptr(), rc.data_ptr(), sp)
+                        rmk.data_ptr(), rmf.data_ptr(), rc.data_ptr(), sp)
     torch.cuda.synchronize()
     print("rows equal:", torch.equal(ref_out, outs[s % 8]), "flags equal:", torch.equal(rfl, fl[s % 8]))
 
