@@ -62,11 +62,13 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kPos = 8;           // positions per warp
 constexpr int kSetBits = 7;       // 128-entry per-block stamped-slot set (64 positions)
 constexpr int kRowChunks = 8;     // float4 chunks per lane in flight (a 128-float row)
+constexpr uint32_t kCountLanes = 64;  // distributed (unique hit, unique miss) counter pairs
 }  // namespace
 
 size_t lookup_scratch_bytes(uint64_t cap) {
   const uint64_t tcap = table_cap(cap);
-  return a256(tcap * 4) * 2 + a256(cap * 4) * 3 + a256(cap * 8) + a256(64);
+  return a256(tcap * 4) * 2 + a256(cap * 4) * 3 + a256(cap * 8) + a256(kCountLanes * 16) +
+         a256(64);
 }
 
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
@@ -85,10 +87,10 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   ls.list = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list_firsts = reinterpret_cast<uint32_t*>(take(cap * 4));
   ls.list_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  ls.counts = reinterpret_cast<unsigned long long*>(take(kCountLanes * 16));
   unsigned long long* small = reinterpret_cast<unsigned long long*>(take(64));
-  ls.counts = small;           // [0..1]
-  ls.counts_prev = small + 2;  // [2..3]
-  ls.list_ctr = reinterpret_cast<uint32_t*>(small + 4);  // [2] u32
+  ls.counts_prev = small;  // [0..1] cumulative totals at the previous call
+  ls.list_ctr = reinterpret_cast<uint32_t*>(small + 2);  // [2] u32
   return ls;
 }
 
@@ -139,9 +141,7 @@ __global__ void __launch_bounds__(kThreads)
     k_lookup(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, float* __restrict__ out,
              uint8_t* __restrict__ flags, const float* __restrict__ default_row, uint64_t stamp,
              LookupScratch ls, uint32_t parity) {
-  __shared__ unsigned int s_counts[2];
   __shared__ uint32_t s_stamped[1u << kSetBits];
-  if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
   for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += blockDim.x) s_stamped[i] = kNoSlot;
   // the other parity's claim counter belongs to the next call: reset it
   if (blockIdx.x == 0 && threadIdx.x == 0) ls.list_ctr[parity ^ 1u] = 0;
@@ -269,31 +269,41 @@ __global__ void __launch_bounds__(kThreads)
     uh += __shfl_xor_sync(0xFFFFFFFFu, uh, o);
     um += __shfl_xor_sync(0xFFFFFFFFu, um, o);
   }
+  // fire-and-forget adds into one of kCountLanes counter pairs (no block
+  // barrier at the end, no single hot counter); finalize sums them
   if (lane == 0 && (uh | um)) {
-    atomicAdd(&s_counts[0], uh);
-    atomicAdd(&s_counts[1], um);
+    const uint32_t w = ((blockIdx.x * kWarps) + (threadIdx.x >> 5)) & (kCountLanes - 1);
+    if (uh) atomicAdd(ls.counts + 2 * w, (unsigned long long)uh);
+    if (um) atomicAdd(ls.counts + 2 * w + 1, (unsigned long long)um);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s_counts[0]) atomicAdd(ls.counts + 0, (unsigned long long)s_counts[0]);
-    if (s_counts[1]) atomicAdd(ls.counts + 1, (unsigned long long)s_counts[1]);
-  }
+  // let the finalize kernel (programmatic dependent launch) get scheduled
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Runs after k_lookup (stream order): first position of every claim, miss
 // table left empty for the next call, per-call counts.
 __global__ void __launch_bounds__(256)
     k_finalize(LookupScratch ls, uint32_t parity) {
+  // programmatic dependent launch: wait until every lookup block is done
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t m = ls.list_ctr[parity];
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     const uint32_t s = ls.list[e];
     ls.list_firsts[e] = ls.miss_table[s] - 1u;
     ls.miss_table[s] = 0u;
   }
-  if (ls.counts_out != nullptr && blockIdx.x == 0 && threadIdx.x < 2) {
-    const unsigned long long cum = ls.counts[threadIdx.x];
-    ls.counts_out[threadIdx.x] = cum - ls.counts_prev[threadIdx.x];
-    ls.counts_prev[threadIdx.x] = cum;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    // cumulative totals of the distributed counters -> this call's counts
+    const uint32_t i = threadIdx.x & 1u;
+    unsigned long long v = 0;
+    for (uint32_t w = threadIdx.x >> 1; w < kCountLanes; w += 16) v += ls.counts[2 * w + i];
+#pragma unroll
+    for (int o = 16; o >= 2; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (threadIdx.x < 2) {
+      const unsigned long long prev = ls.counts_prev[i];
+      ls.counts_prev[i] = v;
+      if (ls.counts_out != nullptr) ls.counts_out[i] = v - prev;
+    }
   }
 }
 
@@ -305,9 +315,20 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
   const unsigned grid = unsigned((n + per_block - 1) / per_block);
   k_lookup<<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
   check_launch("lookup", 1);
-  // claims are at most the unique keys; one wave of small blocks covers them
+  // claims are at most the unique keys; one wave of small blocks covers them.
+  // Programmatic dependent launch: scheduled while the lookup drains.
   const unsigned fgrid = unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 4));
-  k_finalize<<<fgrid, 256, 0, st>>>(ls, parity);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(fgrid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_finalize, ls, parity);
   check_launch("lookup_finalize", 1);
   return 2;
 }
