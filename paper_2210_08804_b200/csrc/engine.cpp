@@ -124,8 +124,8 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);
+  ls.counts_out = ls.counts_prev + 4;  // per-call {unique hits, unique misses}
   parity = 0;
-  prev_counts[0] = prev_counts[1] = 0;
 
   const uint64_t host_bytes = a256(cap * 8) * 5 + a256(16) + a256(cap * 4) * 3 +
                               a256(cap * uint64_t(d) * 4) * 2 + a256(cap);
@@ -283,16 +283,14 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->ls,
                           ws->parity, st);
       ws->parity ^= 1u;
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts, 16, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts_out, 16, cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }
   }
   if (n > 0) {
     HPSB_CUDA(cudaEventSynchronize(ws->done));
-    uh = ws->h_counts[0] - ws->prev_counts[0];
-    um = ws->h_counts[1] - ws->prev_counts[1];
-    ws->prev_counts[0] = ws->h_counts[0];
-    ws->prev_counts[1] = ws->h_counts[1];
+    uh = ws->h_counts[0];
+    um = ws->h_counts[1];
     if (um > 0) {
       HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->ls.list_keys, um * 8,
                                 cudaMemcpyDeviceToHost, st));

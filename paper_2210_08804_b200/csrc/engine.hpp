@@ -83,7 +83,6 @@ struct Workspace {
   uint64_t* d_found_keys = nullptr;
   LookupScratch ls;
   uint32_t parity = 0;
-  unsigned long long prev_counts[2] = {0, 0};
   // pinned host
   PinnedBuffer hbuf;
   uint64_t* h_keys = nullptr;
