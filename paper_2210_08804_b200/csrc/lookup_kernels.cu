@@ -59,9 +59,7 @@ inline uint64_t table_cap(uint64_t cap) {
 }
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kPos = 8;           // positions per warp
 constexpr int kSetBits = 7;       // 128-entry per-block stamped-slot set (64 positions)
-constexpr int kRowChunks = 8;     // float4 chunks per lane in flight (a 128-float row)
 constexpr uint32_t kCountLanes = 64;  // distributed (unique hit, unique miss) counter pairs
 }  // namespace
 
@@ -110,45 +108,55 @@ __device__ __forceinline__ void st_cs_f4(float4* p, const float4& v) {
                : "memory");
 }
 
-// Probe one slab for `key` with 4 lanes (this lane checks keys sub*8..+8).
-// Returns the lowest matching slot index in the slab (0..31) or 32.
-__device__ __forceinline__ uint32_t quad_match(const uint64_t (&kk)[8], uint32_t m, uint64_t key,
-                                               uint32_t sub) {
+// Probe one slab for `key` with L lanes per position (this lane checks keys
+// sub*K .. sub*K+K-1, K = 32/L). Returns the lowest matching slot index in
+// the slab (0..31) or 32.
+template <int L>
+__device__ __forceinline__ uint32_t quad_match(const uint64_t (&kk)[32 / L], uint32_t m,
+                                               uint64_t key, uint32_t sub) {
+  constexpr int K = 32 / L;
   uint32_t h = 32;
 #pragma unroll
-  for (int j = 7; j >= 0; --j) {
-    const uint32_t s = sub * 8 + j;
+  for (int j = K - 1; j >= 0; --j) {
+    const uint32_t s = sub * K + j;
     if (((m >> s) & 1u) && kk[j] == key) h = s;
   }
-  h = min(h, __shfl_xor_sync(0xFFFFFFFFu, h, 1));
-  h = min(h, __shfl_xor_sync(0xFFFFFFFFu, h, 2));
+#pragma unroll
+  for (int o = 1; o < L; o <<= 1) h = min(h, __shfl_xor_sync(0xFFFFFFFFu, h, o));
   return h;
 }
 
+template <int L>
 __device__ __forceinline__ void load_slab_part(const CacheDev& c, uint32_t slab, uint32_t sub,
-                                               uint64_t (&kk)[8]) {
+                                               uint64_t (&kk)[32 / L]) {
+  constexpr int K = 32 / L;
   const ulonglong2* p2 =
-      reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(slab) * kSlotsPerSlab) + sub * 4;
+      reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(slab) * kSlotsPerSlab) + sub * (K / 2);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < K / 2; ++j) {
     const ulonglong2 v = p2[j];
     kk[2 * j] = v.x;
     kk[2 * j + 1] = v.y;
   }
 }
 
+// L = lanes per position (4 or 8): a warp serves 32/L positions.
+template <int L>
 __global__ void __launch_bounds__(kThreads)
     k_lookup(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, float* __restrict__ out,
              uint8_t* __restrict__ flags, const float* __restrict__ default_row, uint64_t stamp,
              LookupScratch ls, uint32_t parity) {
+  constexpr int K = 32 / L;   // keys of a slab per lane
+  constexpr int POS = 32 / L; // positions per warp
+  constexpr int RC = 32 / L;  // float4 chunks per lane per 128-float row segment
   __shared__ uint32_t s_stamped[1u << kSetBits];
   for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += blockDim.x) s_stamped[i] = kNoSlot;
   // the other parity's claim counter belongs to the next call: reset it
   if (blockIdx.x == 0 && threadIdx.x == 0) ls.list_ctr[parity ^ 1u] = 0;
   __syncthreads();
   const uint32_t lane = lane_id();
-  const uint32_t q = lane >> 2, sub = lane & 3u;
-  const uint64_t pos = ((uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5) * kPos + q;
+  const uint32_t q = lane / L, sub = lane % L;
+  const uint64_t pos = ((uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5) * POS + q;
   const bool valid = pos < n;
   const uint64_t key = valid ? keys[pos] : 0ull;
   // ---- placement and probe ----
@@ -159,15 +167,15 @@ __global__ void __launch_bounds__(kThreads)
     // both probe slabs and masks in one round trip
     const uint32_t sa = set * 2 + first, sb = set * 2 + (first ^ 1u);
     uint32_t ma = 0, mb = 0;
-    uint64_t ka[8], kb[8];
+    uint64_t ka[K], kb[K];
     if (valid) {
       ma = c.masks[sa];
       mb = c.masks[sb];
-      load_slab_part(c, sa, sub, ka);
-      load_slab_part(c, sb, sub, kb);
+      load_slab_part<L>(c, sa, sub, ka);
+      load_slab_part<L>(c, sb, sub, kb);
     }
-    const uint32_t ha = quad_match(ka, valid ? ma : 0u, key, sub);
-    const uint32_t hb = quad_match(kb, valid ? mb : 0u, key, sub);
+    const uint32_t ha = quad_match<L>(ka, valid ? ma : 0u, key, sub);
+    const uint32_t hb = quad_match<L>(kb, valid ? mb : 0u, key, sub);
     if (ha < 32)
       res = sa * kSlotsPerSlab + ha;
     else if (ma == kFullSlab && hb < 32)
@@ -182,12 +190,12 @@ __global__ void __launch_bounds__(kThreads)
       sl = (sl >= c.W) ? sl - c.W : sl;
       const uint32_t slab = set * c.W + sl;
       uint32_t m = 0;
-      uint64_t kk[8];
+      uint64_t kk[K];
       if (pending) {
         m = c.masks[slab];
-        load_slab_part(c, slab, sub, kk);
+        load_slab_part<L>(c, slab, sub, kk);
       }
-      const uint32_t h = quad_match(kk, pending ? m : 0u, key, sub);
+      const uint32_t h = quad_match<L>(kk, pending ? m : 0u, key, sub);
       if (pending) {
         if (h < 32) {
           res = slab * kSlotsPerSlab + h;
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (stamp_it) old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
-  // ---- row copy: lane `sub` moves float4 chunks sub, sub+4, sub+8, ... ----
+  // ---- row copy: lane `sub` moves float4 chunks sub, sub+L, sub+2L, ... ----
   if (valid) {
     const uint32_t d = c.d;
     const float* src = res != kNoSlot ? c.rows + uint64_t(res) * d : default_row;
@@ -223,21 +231,21 @@ __global__ void __launch_bounds__(kThreads)
       const uint32_t d4 = d >> 2;
       const float4* s4 = reinterpret_cast<const float4*>(src);
       float4* o4 = reinterpret_cast<float4*>(dst);
-      for (uint32_t ch0 = 0; ch0 < d4; ch0 += 4 * kRowChunks) {
-        float4 v[kRowChunks];
+      for (uint32_t ch0 = 0; ch0 < d4; ch0 += L * RC) {
+        float4 v[RC];
 #pragma unroll
-        for (int j = 0; j < kRowChunks; ++j) {
-          const uint32_t ch = ch0 + uint32_t(j) * 4 + sub;
+        for (int j = 0; j < RC; ++j) {
+          const uint32_t ch = ch0 + uint32_t(j) * L + sub;
           if (ch < d4) v[j] = ld_row_f4(s4 + ch);
         }
 #pragma unroll
-        for (int j = 0; j < kRowChunks; ++j) {
-          const uint32_t ch = ch0 + uint32_t(j) * 4 + sub;
+        for (int j = 0; j < RC; ++j) {
+          const uint32_t ch = ch0 + uint32_t(j) * L + sub;
           if (ch < d4) st_cs_f4(o4 + ch, v[j]);
         }
       }
     } else {
-      for (uint32_t ch = sub; ch < d; ch += 4) dst[ch] = src[ch];
+      for (uint32_t ch = sub; ch < d; ch += L) dst[ch] = src[ch];
     }
   }
   // ---- misses: the group's lane 0 claims the key; bookkeeping ----
@@ -311,9 +319,18 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
                              uint8_t* flags, const float* default_row, uint64_t stamp,
                              const LookupScratch& ls, uint32_t parity, cudaStream_t st) {
   if (n == 0) return 0;
-  const uint64_t per_block = uint64_t(kWarps) * kPos;
+  // lanes per position: 8 by default (shorter per-lane state, more warps in
+  // flight); HPSB_LOOKUP_LANES=4 selects the 4-lane variant
+  static const int lanes = (std::getenv("HPSB_LOOKUP_LANES") &&
+                            std::atoi(std::getenv("HPSB_LOOKUP_LANES")) == 4)
+                               ? 4
+                               : 8;
+  const uint64_t per_block = uint64_t(kWarps) * (32 / lanes);
   const unsigned grid = unsigned((n + per_block - 1) / per_block);
-  k_lookup<<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
+  if (lanes == 4)
+    k_lookup<4><<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
+  else
+    k_lookup<8><<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
   check_launch("lookup", 1);
   // claims are at most the unique keys; one wave of small blocks covers them.
   // Programmatic dependent launch: scheduled while the lookup drains.
