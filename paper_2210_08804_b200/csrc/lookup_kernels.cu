@@ -332,6 +332,8 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
   else
     k_lookup<8><<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
   check_launch("lookup", 1);
+  static const bool no_finalize = std::getenv("HPSB_DIAG_NO_FINALIZE") != nullptr;  // diagnostic
+  if (no_finalize) return 1;
   // claims are at most the unique keys; one wave of small blocks covers them.
   // Programmatic dependent launch: scheduled while the lookup drains.
   const unsigned fgrid = unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 4));
