@@ -175,6 +175,11 @@ int hps_cache_check_invariants(hps_cache* cache);
 int hps_cache_export_state(hps_cache* cache, uint64_t* keys, uint64_t* counters,
                            uint32_t* masks, float* rows);
 
+/* Diagnostic (HPSB_TRACE=1 in the environment): per-call phase timeline of
+ * the lookup kernel, 8 u64 per call (see lookup_kernels.cu) for the last
+ * calls in a ring of 4096; copies up to cap values and resets the ring. */
+int hps_cache_debug_trace(hps_cache* cache, uint64_t* out, size_t cap, uint64_t* n_calls);
+
 /* ---- volatile DB (replaces hps::VolatileStore, volatile_store.hpp:45-137) ---- */
 
 int hps_vdb_create(uint32_t lookup_threads, hps_vdb** out);

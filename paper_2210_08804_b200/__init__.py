@@ -143,6 +143,7 @@ SIGNATURES = {
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
     "hps_cache_check_invariants": (C.c_int, [_P]),
     "hps_cache_export_state": (C.c_int, [_P, _P, _P, _P, _P]),
+    "hps_cache_debug_trace": (C.c_int, [_P, _P, C.c_size_t, _U64P]),
     "hps_vdb_create": (C.c_int, [C.c_uint32, C.POINTER(_P)]),
     "hps_vdb_destroy": (C.c_int, [_P]),
     "hps_vdb_register_table": (C.c_int, [_P, C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64]),
@@ -428,6 +429,22 @@ class SlabCache:
         _check(lib().hps_cache_export_state(self._h, _ptr(keys), _ptr(ctr), _ptr(masks),
                                             _ptr(rows)))
         return keys, ctr, masks, rows
+
+    def debug_trace(self) -> np.ndarray:
+        """Per-call lookup phase timeline (HPSB_TRACE=1), absolute globaltimer
+        ns: rows of [first block start, last A done, first release, last
+        release, first copy done, last copy done, finish start, finish end],
+        oldest first; resets the ring."""
+        ring = np.empty(4096 * 8, dtype=np.uint64)
+        n = C.c_uint64(0)
+        _check(lib().hps_cache_debug_trace(self._h, _ptr(ring), ring.size, C.byref(n)))
+        k = min(int(n.value), 4096)
+        r = ring.reshape(-1, 8)
+        idx = [(int(n.value) - k + i) % 4096 for i in range(k)]
+        r = r[idx].copy()
+        for f in (1, 3, 5):
+            r[:, f] = ~r[:, f]
+        return r.astype(np.int64)
 
     # -- accessors (slab_cache.hpp:95-106) ----------------------------------
     def _info(self) -> _CacheInfo:

@@ -318,6 +318,7 @@ __global__ void k_replace_apply(CacheDev c, const uint64_t* __restrict__ keys,
     if (lane == 0) {
       vkeys[slot] = key;
       vctr[slot] = stamp;
+      c.tags[slot] = key_tag(xxh64_key(key, kSlabSeed));
     }
     warp_copy_row(rows + uint64_t(i) * c.d, c.rows + slot * c.d, c.d);
     __threadfence_block();

@@ -7,6 +7,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "device_cache.hpp"
 #include "engine.hpp"
@@ -381,6 +382,15 @@ int hps_cache_export_state(hps_cache* cache, uint64_t* keys, uint64_t* counters,
   return guarded([&] {
     need(cache != nullptr, "null argument");
     cache->impl->export_state(keys, counters, masks, rows);
+  });
+}
+
+int hps_cache_debug_trace(hps_cache* cache, uint64_t* out, size_t cap, uint64_t* n_calls) {
+  return guarded([&] {
+    need(cache != nullptr && n_calls != nullptr, "null argument");
+    std::vector<unsigned long long> ring(hpsb::DeviceCache::kTraceRing * 8);
+    *n_calls = cache->impl->trace(ring.data());
+    if (out != nullptr) std::copy(ring.begin(), ring.begin() + std::min(cap, ring.size()), out);
   });
 }
 

@@ -58,11 +58,15 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
 //   keys     [S][W][32] u64   256 B per slab = two 128 B lines
 //   counters [S][W][32] u64   recency stamps
 //   masks    [S][W]     u32   occupancy bits, grow contiguously from bit 0
+//   tags     [S][W][32] u8    8-bit fingerprint of each stored key (probe
+//                             filter of the lookup kernel; 64 B per W=2 set,
+//                             one 256-bit load per slab)
 //   rows     [S][W][32][d] f32
 struct CacheDev {
   uint64_t* keys;
   uint64_t* counters;
   uint32_t* masks;
+  uint8_t* tags;
   float* rows;
   unsigned long long* occupied;
   uint64_t S;
@@ -91,6 +95,13 @@ __host__ __device__ __forceinline__ uint64_t slabset_of(const CacheDev& c, uint6
 }
 __host__ __device__ __forceinline__ uint32_t first_slab_of(const CacheDev& c, uint64_t key) {
   return uint32_t(fastmod(xxh64_key(key, kSlabSeed), c.W, c.mW));
+}
+
+// Fingerprint of a key: the top byte of its first-slab hash (the slab
+// choice uses h % W, i.e. the low bits for power-of-two W). Maintained by
+// replace next to the key; never part of the reference's state.
+__host__ __device__ __forceinline__ uint8_t key_tag(uint64_t first_slab_hash) {
+  return uint8_t(first_slab_hash >> 56);
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }

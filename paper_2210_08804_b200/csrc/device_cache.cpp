@@ -2,6 +2,7 @@
 #include "device_cache.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <unordered_set>
 #include <vector>
 
@@ -56,11 +57,13 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device
   HPSB_CUDA(cudaMalloc(&dev_.keys, slots * 8));
   HPSB_CUDA(cudaMalloc(&dev_.counters, slots * 8));
   HPSB_CUDA(cudaMalloc(&dev_.masks, slabs * 4));
+  HPSB_CUDA(cudaMalloc(&dev_.tags, slots));
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
   HPSB_CUDA(cudaMemsetAsync(dev_.keys, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.counters, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.masks, 0, slabs * 4, stream_));
+  HPSB_CUDA(cudaMemsetAsync(dev_.tags, 0, slots, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.rows, 0, slots * uint64_t(cfg.dimension) * 4, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.occupied, 0, 8, stream_));
   HPSB_CUDA(cudaMalloc(&d_small_, 64));
@@ -78,12 +81,14 @@ DeviceCache::~DeviceCache() {
   cudaFree(dev_.keys);
   cudaFree(dev_.counters);
   cudaFree(dev_.masks);
+  cudaFree(dev_.tags);
   cudaFree(dev_.rows);
   cudaFree(dev_.occupied);
   cudaFree(d_small_);
   cudaFreeHost(h_small_);
   cudaFree(scan_.tile_ctr);
   cudaFree(scan_.status);
+  cudaFree(trace_);
   cudaEventDestroy(ev_in_);
   cudaEventDestroy(ev_out_);
   cudaStreamDestroy(stream_);
@@ -105,18 +110,21 @@ void DeviceCache::ensure_scan_tiles(uint64_t tiles) {
 
 void DeviceCache::join_from(cudaStream_t user) {
   if (user == nullptr || user == stream_) return;
+  last_op_lookup_ = false;
   HPSB_CUDA(cudaEventRecord(ev_in_, user));
   HPSB_CUDA(cudaStreamWaitEvent(stream_, ev_in_, 0));
 }
 
 void DeviceCache::join_to(cudaStream_t user) {
   if (user == nullptr || user == stream_) return;
+  last_op_lookup_ = false;
   HPSB_CUDA(cudaEventRecord(ev_out_, stream_));
   HPSB_CUDA(cudaStreamWaitEvent(user, ev_out_, 0));
 }
 
 uint64_t DeviceCache::occupied() {
   std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
   DeviceGuard g(device_);
   HPSB_CUDA(cudaMemcpyAsync(h_small_ + 7, dev_.occupied, 8, cudaMemcpyDeviceToHost, stream_));
   HPSB_CUDA(cudaStreamSynchronize(stream_));
@@ -126,6 +134,7 @@ uint64_t DeviceCache::occupied() {
 size_t DeviceCache::query(const uint64_t* keys, size_t n, float* out, size_t out_len,
                           uint32_t* miss_pos, uint64_t* miss_keys, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
   // one tick per call, before anything else (slab_cache.cpp:73-74)
   const uint64_t stamp = bump_clock();
   if (out_len != n * uint64_t(cfg_.dimension))
@@ -183,6 +192,7 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   DeviceGuard g(device_);
   join_from(user);
   if (n == 0) {
+    last_op_lookup_ = false;
     HPSB_CUDA(cudaMemsetAsync(counts, 0, 16, stream_));
     join_to(user);
     return;
@@ -196,30 +206,48 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     const uint64_t bytes = lookup_scratch_bytes(cap);
     void* b = lbuf_.ensure(bytes, stream_);
     HPSB_CUDA(cudaMemsetAsync(b, 0, bytes, stream_));
+    last_op_lookup_ = false;
     lws_ = lookup_scratch_carve(b, cap);
     lcap_ = cap;
     lparity_ = 0;
   }
-  LookupScratch ls = lws_;
-  ls.list_keys = miss_keys;
-  ls.list_firsts = miss_firsts;
-  ls.counts_out = reinterpret_cast<unsigned long long*>(counts);
+  LookupView v = lws_.v[lparity_];
+  static const bool tracing = std::getenv("HPSB_TRACE") != nullptr;
+  if (tracing) {
+    if (trace_ == nullptr) {
+      HPSB_CUDA(cudaMalloc(&trace_, kTraceRing * 64));
+      HPSB_CUDA(cudaMemsetAsync(trace_, 0xFF, kTraceRing * 64, stream_));
+      last_op_lookup_ = false;
+    }
+    v.trace = trace_ + (trace_calls_++ % kTraceRing) * 8;
+  }
+  v.list_keys = miss_keys;
+  v.list_firsts = miss_firsts;
+  v.counts_out = reinterpret_cast<unsigned long long*>(counts);
   // profile events: external records when the stream is being captured into
   // a CUDA graph, so the timestamps stay readable after graph launches
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (prof_start_ || prof_end_) HPSB_CUDA(cudaStreamIsCapturing(stream_, &cap));
   const unsigned rec_flags =
       cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
-  if (prof_start_) HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
-  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, ls, lparity_, stream_);
+  if (prof_start_) {
+    HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
+    last_op_lookup_ = false;
+  }
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, v, last_op_lookup_, stream_);
   lparity_ ^= 1u;
-  if (prof_end_) HPSB_CUDA(cudaEventRecordWithFlags(prof_end_, stream_, rec_flags));
+  last_op_lookup_ = true;
+  if (prof_end_) {
+    HPSB_CUDA(cudaEventRecordWithFlags(prof_end_, stream_, rec_flags));
+    last_op_lookup_ = false;
+  }
   join_to(user);
 }
 
 void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
                           size_t vectors_len, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
   if (vectors_len != n * uint64_t(cfg_.dimension))
     throw invalid_argument("replace vector buffer has wrong size");
   const bool host = mem == kHostMem;
@@ -260,6 +288,7 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
 }
 
 void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const float* d_rows) {
+  last_op_lookup_ = false;
   if (n == 0) return;
   const uint64_t stamp = clock_.load(std::memory_order_relaxed);
   const uint64_t rs_bytes = replace_scratch_bytes(n);
@@ -270,6 +299,7 @@ void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const 
 size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
                            size_t vectors_len, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
   if (vectors_len != n * uint64_t(cfg_.dimension))
     throw invalid_argument("update vector buffer has wrong size");
   if (n == 0) return 0;
@@ -301,6 +331,7 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
 
 size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, size_t cap) {
   std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
   set_end = std::min<uint64_t>(set_end, cfg_.slabset_count);
   if (set_begin >= set_end) return 0;
   DeviceGuard g(device_);
@@ -319,9 +350,23 @@ size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, si
   return n;
 }
 
+uint64_t DeviceCache::trace(unsigned long long* out) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (trace_ == nullptr) return 0;
+  last_op_lookup_ = false;
+  DeviceGuard g(device_);
+  HPSB_CUDA(cudaMemcpyAsync(out, trace_, kTraceRing * 64, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaMemsetAsync(trace_, 0xFF, kTraceRing * 64, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  const uint64_t n = trace_calls_;
+  trace_calls_ = 0;
+  return n;
+}
+
 void DeviceCache::export_state(uint64_t* keys, uint64_t* counters, uint32_t* masks,
                                float* rows) {
   std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
   DeviceGuard g(device_);
   const uint64_t slabs = cfg_.slabset_count * cfg_.slabs_per_set;
   const uint64_t slots = slabs * 32ull;
@@ -342,6 +387,14 @@ void DeviceCache::check_invariants() {
   std::vector<uint64_t> keys(slots), ctr(slots);
   std::vector<uint32_t> masks(S * W);
   export_state(keys.data(), ctr.data(), masks.data(), nullptr);
+  std::vector<uint8_t> tags(slots);
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    last_op_lookup_ = false;
+    DeviceGuard g(device_);
+    HPSB_CUDA(cudaMemcpyAsync(tags.data(), dev_.tags, slots, cudaMemcpyDeviceToHost, stream_));
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+  }
   const uint64_t clock_now = recency_clock();
   const uint64_t occ = occupied();
   std::unordered_set<uint64_t> seen;
@@ -362,6 +415,9 @@ void DeviceCache::check_invariants() {
           throw logic_error("slab cache key stored outside its slabset");
         if (!seen.insert(key).second) throw logic_error("slab cache holds a key in two slots");
         if (ctr[slot] > clock_now) throw logic_error("slab cache slot counter exceeds the clock");
+        // B200 layout: the lookup kernel's probe filter must match the key
+        if (tags[slot] != key_tag(hpsb::xxh64_key(key, kSlabSeed)))
+          throw logic_error("slab cache key fingerprint is out of sync");
       }
     }
   }

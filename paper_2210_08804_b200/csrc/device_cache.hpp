@@ -80,6 +80,9 @@ class DeviceCache {
 
   // ---- engine-facing primitives (caller holds mutex()) ----
   std::mutex& mutex() { return mu_; }
+  // Callers that enqueue their own work on stream() (the engine) call this
+  // under mutex() so the next lookup does not chain onto a stale lookup.
+  void note_stream_op() { last_op_lookup_ = false; }
   uint64_t bump_clock() { return clock_.fetch_add(1, std::memory_order_relaxed) + 1; }
   // Device keys / rows, distinct keys guaranteed by the caller; stamp = the
   // current clock. Enqueued on stream(); scratch is the cache's own.
@@ -112,6 +115,20 @@ class DeviceCache {
   LookupScratch lws_;
   uint64_t lcap_ = 0;
   uint32_t lparity_ = 0;
+  // true while the last operation enqueued on stream_ is a lookup kernel
+  // (the next lookup may then launch as its programmatic dependent)
+  bool last_op_lookup_ = false;
+  // diagnostic lookup timeline ring (HPSB_TRACE=1): kTraceRing calls x 8
+  unsigned long long* trace_ = nullptr;
+  uint64_t trace_calls_ = 0;
+
+ public:
+  static constexpr uint64_t kTraceRing = 4096;
+  // Copies the ring (kTraceRing x 8 u64, call k at row k % kTraceRing) and
+  // returns the number of traced calls; 0 when tracing is off.
+  uint64_t trace(unsigned long long* out);
+
+ private:
   cudaEvent_t prof_start_ = nullptr, prof_end_ = nullptr;
   unsigned long long* d_small_ = nullptr;  // small device counters
   unsigned long long* h_small_ = nullptr;  // pinned mirror

@@ -124,7 +124,6 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);
-  ls.counts_out = ls.counts_prev + 4;  // per-call {unique hits, unique misses}
   parity = 0;
 
   const uint64_t host_bytes = a256(cap * 8) * 5 + a256(16) + a256(cap * 4) * 3 +
@@ -280,10 +279,12 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       } else {
         cache_->join_from(user);
       }
-      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->ls,
-                          ws->parity, st);
+      ws->lv = ws->ls.v[ws->parity];
       ws->parity ^= 1u;
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->ls.counts_out, 16, cudaMemcpyDeviceToHost, st));
+      cache_->note_stream_op();  // the engine's own copies follow on the stream
+      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->lv,
+                          /*after_lookup=*/false, st);
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->lv.counts_out, 16, cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }
   }
@@ -292,9 +293,9 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
     uh = ws->h_counts[0];
     um = ws->h_counts[1];
     if (um > 0) {
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->ls.list_keys, um * 8,
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, um * 8,
                                 cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->ls.list_firsts, um * 4,
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, um * 4,
                                 cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
       HPSB_CUDA(cudaEventSynchronize(ws->done));
@@ -328,8 +329,8 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
                                 cudaMemcpyHostToDevice, st));
       HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
                                 cudaMemcpyHostToDevice, st));
-      launch_lookup_scatter(n, d, d_flags, d_flags, ws->ls, ws->d_row_of, ws->d_staged, d_out,
-                            st);
+      cache_->note_stream_op();
+      launch_lookup_scatter(n, d, d_flags, ws->lv, ws->d_row_of, ws->d_staged, d_out, st);
       cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
     }
     HPSB_CUDA(cudaEventRecord(ws->done, st));

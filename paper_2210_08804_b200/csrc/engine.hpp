@@ -82,6 +82,7 @@ struct Workspace {
   float* d_staged = nullptr;
   uint64_t* d_found_keys = nullptr;
   LookupScratch ls;
+  LookupView lv;  // the view of the last lookup
   uint32_t parity = 0;
   // pinned host
   PinnedBuffer hbuf;

@@ -83,37 +83,47 @@ void launch_dedup(const uint64_t* keys, uint64_t n, uint64_t* unique_out, uint32
                   cudaStream_t st);
 
 // ---- lookup (lookup_engine.cpp:130-241) ----
-// Per-call scratch of the lookup kernels. A lookup's unique misses come out
-// as a CLAIM LIST (one entry per missing key, in claim order) with each
-// key's first-occurrence position; sorting the claims by that position gives
-// the reference's order (dedup first-occurrence order, types.cpp:20-34, then
-// ascending miss positions, slab_cache.cpp:84-89).
-struct LookupScratch {
-  uint64_t cap = 0;                  // miss table capacity (power of two >= 2 * batch)
-  uint32_t* miss_table = nullptr;    // 0 = empty, else first position + 1; cleared per call
-  uint32_t* claim_of_slot = nullptr; // miss-table slot -> claim index
-  uint32_t* miss_slot = nullptr;     // per position (valid where missed)
-  unsigned long long* counts = nullptr;  // [0] unique hits, [1] unique misses (cumulative)
-  unsigned long long* counts_prev = nullptr;  // finalize: per-call deltas
-  unsigned long long* counts_out = nullptr;   // optional per-call counts destination
-  uint32_t* list = nullptr;          // claim -> miss-table slot (capacity n)
-  uint64_t* list_keys = nullptr;     // claim -> key (capacity n)
-  uint32_t* list_firsts = nullptr;   // claim -> first position (written by finalize)
-  uint32_t* list_ctr = nullptr;      // [2]: claim counters, double-buffered by call parity
+// Scratch of ONE lookup call. A lookup's unique misses come out as a CLAIM
+// LIST (one entry per missing key, in claim order) with each key's
+// first-occurrence position; sorting the claims by that position gives the
+// reference's order (dedup first-occurrence order, types.cpp:20-34, then
+// ascending miss positions, slab_cache.cpp:84-89). Every field is back to
+// its initial state (zero) when the call completes.
+struct LookupView {
+  uint64_t cap = 0;                       // miss table capacity (power of two >= 2 * batch)
+  uint32_t* miss_table = nullptr;         // 0 = empty, else first position + 1
+  uint32_t* claim_of_slot = nullptr;      // miss-table slot -> claim index
+  uint32_t* miss_slot = nullptr;          // per position (valid where missed)
+  uint32_t* list = nullptr;               // claim -> miss-table slot (capacity batch)
+  uint64_t* list_keys = nullptr;          // claim -> key (per-call destination)
+  uint32_t* list_firsts = nullptr;        // claim -> first position (per-call destination)
+  unsigned long long* counts = nullptr;   // distributed (unique hit, unique miss) pairs
+  unsigned long long* counts_out = nullptr;  // [2] per-call destination
+  uint32_t* list_ctr = nullptr;           // claims so far
+  uint32_t* done = nullptr;               // [2] block tickets (claims done, counts done)
+  // diagnostic phase timeline (HPSB_TRACE): 8 u64 per call, filled with
+  // 0xFF before the call; fields hold min(t) or min(~t) (= max t) over blocks
+  unsigned long long* trace = nullptr;
 };
-// Bytes / carving of a LookupScratch for batches of up to `cap` keys (all
-// regions zero-initialised by the caller once).
+// Two views; consecutive calls on one stream alternate between them, so a
+// call can start while the previous one finishes (programmatic dependent
+// launch).
+struct LookupScratch {
+  LookupView v[2];
+};
+// Bytes / carving of a LookupScratch for batches of up to `cap` keys (the
+// caller zero-fills the block once).
 size_t lookup_scratch_bytes(uint64_t cap);
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
-// Two launches per lookup: the lookup kernel (probe, stamps, row gather /
-// default rows, miss claims) and the finalize kernel (first positions of the
-// claims, miss-table cleanup, per-call counts). `parity` alternates per call
-// on the same scratch. Returns the number of kernels launched.
+// One launch per lookup (probe, claims, stamps, row gather / default rows,
+// and the call's completion by its last block). after_lookup: the previous
+// operation on `st` was a lookup kernel on the OTHER view -> launched as its
+// programmatic dependent. Returns the number of kernels launched.
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupScratch& ls, uint32_t parity, cudaStream_t st);
-void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint8_t* flags,
-                           const LookupScratch& ls, const int32_t* row_of,
-                           const float* staged, float* out, cudaStream_t st);
+                             const LookupView& v, bool after_lookup, cudaStream_t st);
+void launch_lookup_scatter(uint64_t n, uint32_t d, uint8_t* flags, const LookupView& v,
+                           const int32_t* row_of_claim, const float* staged, float* out,
+                           cudaStream_t st);
 
 }  // namespace hpsb

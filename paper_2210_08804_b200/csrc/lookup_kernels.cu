@@ -1,41 +1,50 @@
 // lookup_kernels.cu -- the lookup hot path (sm_100a).
 //
-// Restates LookupEngine::lookup (lookup_engine.cpp:130-241) for a batch of
-// |Q| query positions:
+// Restates LookupEngine::lookup's device half (lookup_engine.cpp:130-241:
+// dedup -> query -> unique-key counts -> expansion, with the default row for
+// missing positions, :185-203) for a batch of |Q| query positions, in ONE
+// kernel launch per call:
 //
-//   k_lookup    a warp serves 8 positions, 4 lanes per position, so each
-//               position's dependent chain is short: key load, both
-//               placement hashes (XXH64 + Barrett modulo), ONE round trip
-//               for both probe slabs and masks (each lane compares 8 of a
-//               slab's 32 keys loaded as 128-bit vectors; a 4-lane min picks
-//               the lowest matching slot -- the ballot/ffs rule of
-//               slab_cache.cpp:240-245, and the second slab only counts when
-//               the first is full, :249-256), ONE round trip for the row
-//               (each lane moves a quarter of it with 128-bit L1-cached
-//               loads and evict-first stores) straight into the position's
-//               output row: the expansion of lookup_engine.cpp:194-203 is
-//               fused, and missing positions get the default row (the async
-//               branch's answer, :185-192).
-//               Recency: the exchange that first moves a slot to this call's
-//               stamp counts one UNIQUE hit, so |Q*| needs no dedup of hits;
-//               a per-block set of stamped slots keeps the hottest keys'
-//               exchanges (power-law batches repeat their top key in ~19% of
-//               positions) off a single L2 line.
-//               Misses: the group leader inserts the key into a per-call
-//               miss table keeping the minimum position; the position that
-//               claims an empty entry appends a claim (slot, key).
-//   k_finalize  per claim: first position = table entry, entry cleared for
-//               the next call; per-call counts. Sorting claims by first
-//               position gives the reference's miss order -- the engine does
-//               it on the host, where the tiers are.
-//   k_scatter   (sync branch only) copies the rows fetched from the tiers
-//               into every position of their key and clears the default
-//               flag (lookup_engine.cpp:165-181).
+//   k_lookup_tag  (default) lane i of a warp owns position base+i:
+//       A  key (coalesced), both placement hashes (XXH64 + Barrett modulo),
+//          the set's 8-bit fingerprints and occupancy masks (W = 2: 64 B in
+//          two 256-bit loads + one 8 B load, one round trip), candidate
+//          keys verified in slot order (the first equal key is the
+//          reference's lowest-matching-slot hit, slab_cache.cpp:240-245; the
+//          second slab only counts when the first is full, :249-256);
+//          missing keys claimed in a per-call miss table (minimum position
+//          kept), one attempt per warp-distinct key; miss flags
+//       B  griddepcontrol.wait: when launched as a programmatic dependent of
+//          the previous lookup on the stream, everything above overlapped
+//          that lookup's row traffic; from here on the previous call is
+//          complete (its stamps landed, its last block finished)
+//       C  recency exchange (one per distinct slot per block; the exchange
+//          that moves a slot to this call's stamp counts one UNIQUE hit, so
+//          |Q*| needs no dedup of hits), row copy of the warp's 32 rows as
+//          one contiguous output block with 256-bit L1-allocating loads and
+//          evict-first stores, per-warp counts
+//       D  the last block to finish completes the call: first position of
+//          every claim (sorting claims by it gives the reference's miss
+//          order -- dedup first-occurrence, types.cpp:20-34, then ascending
+//          miss positions, slab_cache.cpp:84-89), miss table cleared,
+//          per-call counts, per-call state reset for the call after next
+//   k_lookup<L>   the warp-cooperative variant (L lanes per position probe a
+//          slab's 32 keys with 128-bit loads and a min/ballot rule), kept
+//          for A/B measurement (HPSB_LOOKUP_KERNEL=warp4|warp8)
+//   k_lookup_scatter (sync branch only) copies the rows fetched from the
+//          tiers into every position of their key and clears the default
+//          flag (lookup_engine.cpp:165-181).
+//
+// Consecutive lookups on one stream alternate between the two halves
+// (parities) of a LookupScratch, so call i+1's phase A may run while call i
+// is still copying rows: nothing in phase A reads state that call i writes.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -57,17 +66,23 @@ inline uint64_t table_cap(uint64_t cap) {
   while (t < 2 * cap) t <<= 1;
   return t;
 }
-constexpr int kWarps = 8;
+constexpr int kWarps = 8;  // warp variant: 256-thread blocks
 constexpr int kThreads = kWarps * 32;
-constexpr int kSetBits = 7;       // 128-entry per-block stamped-slot set (64 positions)
+constexpr int kSetBits = 7;           // warp variant: 128-entry per-block stamped-slot set
 constexpr uint32_t kCountLanes = 64;  // distributed (unique hit, unique miss) counter pairs
-}  // namespace
 
-size_t lookup_scratch_bytes(uint64_t cap) {
+// Diagnostic skip bits (HPSB_DIAG_SKIP, measurement only; results are wrong
+// with any bit set): 1 = recency exchange, 2 = miss claims, 4 = row copy.
+constexpr uint32_t kSkipStamp = 1, kSkipMiss = 2, kSkipCopy = 4;
+
+uint64_t view_bytes(uint64_t cap) {
   const uint64_t tcap = table_cap(cap);
   return a256(tcap * 4) * 2 + a256(cap * 4) * 3 + a256(cap * 8) + a256(kCountLanes * 16) +
          a256(64);
 }
+}  // namespace
+
+size_t lookup_scratch_bytes(uint64_t cap) { return 2 * view_bytes(cap); }
 
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   LookupScratch ls;
@@ -78,20 +93,25 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
     p += a256(b);
     return r;
   };
-  ls.cap = tcap;
-  ls.miss_table = reinterpret_cast<uint32_t*>(take(tcap * 4));
-  ls.claim_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
-  ls.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
-  ls.list = reinterpret_cast<uint32_t*>(take(cap * 4));
-  ls.list_firsts = reinterpret_cast<uint32_t*>(take(cap * 4));
-  ls.list_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
-  ls.counts = reinterpret_cast<unsigned long long*>(take(kCountLanes * 16));
-  unsigned long long* small = reinterpret_cast<unsigned long long*>(take(64));
-  ls.counts_prev = small;  // [0..1] cumulative totals at the previous call
-  ls.list_ctr = reinterpret_cast<uint32_t*>(small + 2);  // [2] u32
+  for (int k = 0; k < 2; ++k) {
+    LookupView& v = ls.v[k];
+    v.cap = tcap;
+    v.miss_table = reinterpret_cast<uint32_t*>(take(tcap * 4));
+    v.claim_of_slot = reinterpret_cast<uint32_t*>(take(tcap * 4));
+    v.miss_slot = reinterpret_cast<uint32_t*>(take(cap * 4));
+    v.list = reinterpret_cast<uint32_t*>(take(cap * 4));
+    v.list_firsts = reinterpret_cast<uint32_t*>(take(cap * 4));
+    v.list_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+    v.counts = reinterpret_cast<unsigned long long*>(take(kCountLanes * 16));
+    unsigned long long* small = reinterpret_cast<unsigned long long*>(take(64));
+    v.counts_out = small;                                 // [0..1] default destination
+    v.list_ctr = reinterpret_cast<uint32_t*>(small + 2);  // claim counter
+    v.done = reinterpret_cast<uint32_t*>(small + 3);      // [2] block tickets
+  }
   return ls;
 }
 
+// ------------------------------------------------------------ accessors --
 // Row loads: non-coherent path with L1 allocation (the table does not change
 // during a lookup; repeated hot rows are served from the SM's L1).
 __device__ __forceinline__ float4 ld_row_f4(const float4* p) {
@@ -107,7 +127,174 @@ __device__ __forceinline__ void st_cs_f4(float4* p, const float4& v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
+__device__ __forceinline__ void ld256_nc(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st256_cs(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Trace fields: 0 first block start, 1 last block done with A, 2 first
+// block released by the wait, 3 last block released, 4 first block done
+// copying, 5 last block done copying, 6 claims finish start, 7 claims
+// finish end.
+__device__ __forceinline__ void trace_min(const LookupView& v, int f, bool as_max) {
+  if (v.trace != nullptr && threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    atomicMin(v.trace + f, as_max ? ~t : t);
+  }
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
+// ------------------------------------------------------- call completion --
+// A call completes in two parts, each run by the last block through a
+// ticket (__threadfence + atomic ticket, so all earlier blocks' writes are
+// visible):
+//   finish_claims  once every block has made its claims (before the row
+//                  copies): first position of each claim, miss table cleared;
+//                  it overlaps the other blocks' copies
+//   finish_counts  once every block has added its counts (after the copies):
+//                  per-call counts, counters zeroed, tickets and claim
+//                  counter reset for the next call on this view
+// finish_claims is one block's work, written for memory-level parallelism:
+// each thread issues all its loads of a round before using any.
+__device__ void finish_claims(const LookupView& v) {
+  constexpr int kClaimsPerThread = 8;
+  const uint32_t m = __ldcg(v.list_ctr);
+  for (uint32_t e0 = 0; e0 < m; e0 += kClaimsPerThread * blockDim.x) {
+    uint32_t s[kClaimsPerThread], f[kClaimsPerThread];
+#pragma unroll
+    for (int k = 0; k < kClaimsPerThread; ++k) {
+      const uint32_t e = e0 + k * blockDim.x + threadIdx.x;
+      s[k] = e < m ? __ldcg(v.list + e) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kClaimsPerThread; ++k) {
+      const uint32_t e = e0 + k * blockDim.x + threadIdx.x;
+      f[k] = e < m ? __ldcg(v.miss_table + s[k]) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kClaimsPerThread; ++k) {
+      const uint32_t e = e0 + k * blockDim.x + threadIdx.x;
+      if (e < m) {
+        v.list_firsts[e] = f[k] - 1u;
+        v.miss_table[s[k]] = 0u;  // the table is all-zero between calls
+      }
+    }
+  }
+}
+
+__device__ void finish_counts(const LookupView& v) {
+  if (threadIdx.x < 32) {
+    // 128 values, 4 per lane, loaded together
+    const uint32_t i = threadIdx.x & 1u;
+    unsigned long long x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __ldcg(v.counts + 2 * ((threadIdx.x >> 1) + 16 * k) + i);
+    unsigned long long s = x[0] + x[1] + x[2] + x[3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v.counts[2 * ((threadIdx.x >> 1) + 16 * k) + i] = 0ull;
+#pragma unroll
+    for (int o = 16; o >= 2; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (threadIdx.x < 2) v.counts_out[i] = s;
+    if (threadIdx.x == 0) {
+      *v.list_ctr = 0u;
+      v.done[0] = 0u;
+      v.done[1] = 0u;
+    }
+  }
+}
+
+// Ticket `t` (0 = claims, 1 = counts): true in every thread of the block
+// that got there last.
+__device__ __forceinline__ bool last_block(const LookupView& v, int t) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(v.done + t, 1u) == gridDim.x - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+// Adds a warp's (unique hit, unique miss) totals into one of kCountLanes
+// counter pairs (no single hot counter).
+__device__ __forceinline__ void warp_add_counts(const LookupView& v, uint32_t uh, uint32_t um,
+                                                uint32_t warp_global) {
+  uh = __reduce_add_sync(0xFFFFFFFFu, uh);
+  um = __reduce_add_sync(0xFFFFFFFFu, um);
+  if (lane_id() == 0 && (uh | um)) {
+    const uint32_t w = warp_global & (kCountLanes - 1);
+    if (uh) atomicAdd(v.counts + 2 * w, (unsigned long long)uh);
+    if (um) atomicAdd(v.counts + 2 * w + 1, (unsigned long long)um);
+  }
+}
+
+// Claims the missing keys of a warp (one lane per position; `miss` lanes):
+// one miss-table attempt per warp-distinct key by its lowest position, the
+// claim appended to the call's list; miss_slot recorded for the scatter
+// kernel. Returns this lane's unique-miss contribution (0/1).
+__device__ __forceinline__ uint32_t warp_claim_misses(const LookupView& v,
+                                                      const uint64_t* __restrict__ keys,
+                                                      uint64_t pos, uint64_t key, bool miss) {
+  const uint32_t lane = lane_id();
+  const uint32_t miss_lanes = __ballot_sync(0xFFFFFFFFu, miss);
+  if (miss_lanes == 0) return 0;
+  uint32_t key_leader = lane;
+  bool claimed = false;
+  uint32_t tslot = 0;
+  if (miss) {
+    key_leader = __ffs(__match_any_sync(miss_lanes, key)) - 1;
+    if (key_leader == lane) tslot = miss_insert(v.miss_table, v.cap, keys, key, uint32_t(pos), &claimed);
+  }
+  // lanes of the same key share the table slot (the scatter kernel reads it)
+  tslot = __shfl_sync(0xFFFFFFFFu, tslot, key_leader);
+  if (miss) v.miss_slot[pos] = tslot;
+  const uint32_t cm = __ballot_sync(0xFFFFFFFFu, claimed);
+  if (cm) {
+    const uint32_t first_lane = __ffs(cm) - 1;
+    uint32_t at = 0;
+    if (lane == first_lane) at = atomicAdd(v.list_ctr, uint32_t(__popc(cm)));
+    at = __shfl_sync(0xFFFFFFFFu, at, first_lane);
+    if (claimed) {
+      const uint32_t e = at + __popc(cm & ((1u << lane) - 1u));
+      v.list[e] = tslot;
+      v.list_keys[e] = key;
+      v.claim_of_slot[tslot] = e;
+    }
+  }
+  return claimed ? 1u : 0u;
+}
+
+// Inserts `slot` into a block-shared open-addressing set; false when the
+// block already holds it (another warp of the block exchanged it).
+__device__ __forceinline__ bool block_set_insert(uint32_t* set, uint32_t size_pow2, uint32_t slot) {
+  uint32_t h = (slot * 0x9E3779B1u) >> 7;
+  for (int probe = 0; probe < 32; ++probe) {
+    h &= size_pow2 - 1;
+    const uint32_t cur = atomicCAS(&set[h], kNoSlot, slot);
+    if (cur == kNoSlot) return true;
+    if (cur == slot) return false;
+    ++h;
+  }
+  return true;  // set crowded: fall back to the global exchange
+}
+
+// ============================================== warp-cooperative variant --
 // Probe one slab for `key` with L lanes per position (this lane checks keys
 // sub*K .. sub*K+K-1, K = 32/L). Returns the lowest matching slot index in
 // the slab (0..31) or 32.
@@ -134,9 +321,9 @@ __device__ __forceinline__ void load_slab_part(const CacheDev& c, uint32_t slab,
       reinterpret_cast<const ulonglong2*>(c.keys + uint64_t(slab) * kSlotsPerSlab) + sub * (K / 2);
 #pragma unroll
   for (int j = 0; j < K / 2; ++j) {
-    const ulonglong2 v = p2[j];
-    kk[2 * j] = v.x;
-    kk[2 * j + 1] = v.y;
+    const ulonglong2 x = p2[j];
+    kk[2 * j] = x.x;
+    kk[2 * j + 1] = x.y;
   }
 }
 
@@ -145,21 +332,18 @@ template <int L>
 __global__ void __launch_bounds__(kThreads)
     k_lookup(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, float* __restrict__ out,
              uint8_t* __restrict__ flags, const float* __restrict__ default_row, uint64_t stamp,
-             LookupScratch ls, uint32_t parity) {
-  constexpr int K = 32 / L;   // keys of a slab per lane
-  constexpr int POS = 32 / L; // positions per warp
-  constexpr int RC = 32 / L;  // float4 chunks per lane per 128-float row segment
+             LookupView v) {
+  constexpr int K = 32 / L;    // keys of a slab per lane
+  constexpr int POS = 32 / L;  // positions per warp
+  constexpr int RC = 32 / L;   // float4 chunks per lane per 128-float row segment
   __shared__ uint32_t s_stamped[1u << kSetBits];
-  for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += blockDim.x) s_stamped[i] = kNoSlot;
-  // the other parity's claim counter belongs to the next call: reset it
-  if (blockIdx.x == 0 && threadIdx.x == 0) ls.list_ctr[parity ^ 1u] = 0;
+  for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += kThreads) s_stamped[i] = kNoSlot;
   __syncthreads();
   const uint32_t lane = lane_id();
   const uint32_t q = lane / L, sub = lane % L;
   const uint64_t pos = ((uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5) * POS + q;
   const bool valid = pos < n;
   const uint64_t key = valid ? keys[pos] : 0ull;
-  // ---- placement and probe ----
   const uint32_t set = uint32_t(slabset_of(c, key));
   const uint32_t first = first_slab_of(c, key);
   uint32_t res = kNoSlot;
@@ -206,160 +390,351 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
-  // ---- recency exchange by the group's lane 0, issued before the copy ----
+  // misses: the group's lane 0 claims the key
+  bool claimed = false;
+  uint32_t tslot = 0;
+  if (valid && sub == 0 && res == kNoSlot) {
+    tslot = miss_insert(v.miss_table, v.cap, keys, key, uint32_t(pos), &claimed);
+    v.miss_slot[pos] = tslot;
+  }
+  if (valid && sub == 0) flags[pos] = res == kNoSlot ? 1 : 0;
+  pdl_wait();
+  pdl_trigger();
+  // recency exchange by the group's lane 0, issued before the copy
   unsigned long long old = stamp;
   bool stamp_it = valid && sub == 0 && res != kNoSlot;
-  if (stamp_it) {
-    uint32_t h = (res * 0x9E3779B1u) >> (32 - kSetBits);
-    for (int probe = 0; probe < 16; ++probe) {
-      const uint32_t cur = atomicCAS(&s_stamped[h], kNoSlot, res);
-      if (cur == kNoSlot) break;
-      if (cur == res) {
-        stamp_it = false;  // this block already exchanged this slot
-        break;
-      }
-      h = (h + 1) & ((1u << kSetBits) - 1u);
-    }
-  }
+  if (stamp_it) stamp_it = block_set_insert(s_stamped, 1u << kSetBits, res);
   if (stamp_it) old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
-  // ---- row copy: lane `sub` moves float4 chunks sub, sub+L, sub+2L, ... ----
-  if (valid) {
+  // row copy (after the call's bookkeeping): lane `sub` moves float4
+  // chunks sub, sub+L, sub+2L, ...
+  auto copy_row = [&] {
     const uint32_t d = c.d;
     const float* src = res != kNoSlot ? c.rows + uint64_t(res) * d : default_row;
     float* dst = out + pos * d;
-    if ((d & 3u) == 0) {
+    if ((d & 3u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 &&
+        (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
       const uint32_t d4 = d >> 2;
       const float4* s4 = reinterpret_cast<const float4*>(src);
       float4* o4 = reinterpret_cast<float4*>(dst);
       for (uint32_t ch0 = 0; ch0 < d4; ch0 += L * RC) {
-        float4 v[RC];
+        float4 x[RC];
 #pragma unroll
         for (int j = 0; j < RC; ++j) {
           const uint32_t ch = ch0 + uint32_t(j) * L + sub;
-          if (ch < d4) v[j] = ld_row_f4(s4 + ch);
+          if (ch < d4) x[j] = ld_row_f4(s4 + ch);
         }
 #pragma unroll
         for (int j = 0; j < RC; ++j) {
           const uint32_t ch = ch0 + uint32_t(j) * L + sub;
-          if (ch < d4) st_cs_f4(o4 + ch, v[j]);
+          if (ch < d4) st_cs_f4(o4 + ch, x[j]);
         }
       }
     } else {
       for (uint32_t ch = sub; ch < d; ch += L) dst[ch] = src[ch];
     }
-  }
-  // ---- misses: the group's lane 0 claims the key; bookkeeping ----
-  bool claimed = false;
-  uint32_t tslot = 0;
-  if (valid && sub == 0 && res == kNoSlot) {
-    tslot = miss_insert(ls.miss_table, ls.cap, keys, key, uint32_t(pos), &claimed);
-    ls.miss_slot[pos] = tslot;
-  }
-  if (valid && sub == 0) flags[pos] = res == kNoSlot ? 1 : 0;
+  };
+  // claims and counts
   const uint32_t cm = __ballot_sync(0xFFFFFFFFu, claimed);
-  uint32_t uh = 0, um = 0;
   if (cm) {
     const uint32_t first_lane = __ffs(cm) - 1;
     uint32_t at = 0;
-    if (lane == first_lane) at = atomicAdd(ls.list_ctr + parity, uint32_t(__popc(cm)));
+    if (lane == first_lane) at = atomicAdd(v.list_ctr, uint32_t(__popc(cm)));
     at = __shfl_sync(0xFFFFFFFFu, at, first_lane);
     if (claimed) {
       const uint32_t e = at + __popc(cm & ((1u << lane) - 1u));
-      ls.list[e] = tslot;
-      ls.list_keys[e] = key;
-      ls.claim_of_slot[tslot] = e;
-    }
-    um = claimed ? 1u : 0u;
-  }
-  if (stamp_it) uh = (old != stamp) ? 1u : 0u;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uh += __shfl_xor_sync(0xFFFFFFFFu, uh, o);
-    um += __shfl_xor_sync(0xFFFFFFFFu, um, o);
-  }
-  // fire-and-forget adds into one of kCountLanes counter pairs (no block
-  // barrier at the end, no single hot counter); finalize sums them
-  if (lane == 0 && (uh | um)) {
-    const uint32_t w = ((blockIdx.x * kWarps) + (threadIdx.x >> 5)) & (kCountLanes - 1);
-    if (uh) atomicAdd(ls.counts + 2 * w, (unsigned long long)uh);
-    if (um) atomicAdd(ls.counts + 2 * w + 1, (unsigned long long)um);
-  }
-  // let the finalize kernel (programmatic dependent launch) get scheduled
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-// Runs after k_lookup (stream order): first position of every claim, miss
-// table left empty for the next call, per-call counts.
-__global__ void __launch_bounds__(256)
-    k_finalize(LookupScratch ls, uint32_t parity) {
-  // programmatic dependent launch: wait until every lookup block is done
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t m = ls.list_ctr[parity];
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-    const uint32_t s = ls.list[e];
-    ls.list_firsts[e] = ls.miss_table[s] - 1u;
-    ls.miss_table[s] = 0u;
-  }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    // cumulative totals of the distributed counters -> this call's counts
-    const uint32_t i = threadIdx.x & 1u;
-    unsigned long long v = 0;
-    for (uint32_t w = threadIdx.x >> 1; w < kCountLanes; w += 16) v += ls.counts[2 * w + i];
-#pragma unroll
-    for (int o = 16; o >= 2; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    if (threadIdx.x < 2) {
-      const unsigned long long prev = ls.counts_prev[i];
-      ls.counts_prev[i] = v;
-      if (ls.counts_out != nullptr) ls.counts_out[i] = v - prev;
+      v.list[e] = tslot;
+      v.list_keys[e] = key;
+      v.claim_of_slot[tslot] = e;
     }
   }
+  if (last_block(v, 0)) finish_claims(v);
+  if (valid) copy_row();
+  warp_add_counts(v, (stamp_it && old != stamp) ? 1u : 0u, claimed ? 1u : 0u,
+                  blockIdx.x * kWarps + (threadIdx.x >> 5));
+  if (last_block(v, 1)) finish_counts(v);
 }
 
+// ====================================================== lane-per-position --
+// Bit j set when byte j of the 32-byte fingerprint block may equal `tag`
+// (zero-byte test on w ^ tag; it can over-report -- verified against the
+// key -- but never misses an equal byte).
+__device__ __forceinline__ uint32_t tag_candidates(const uint32_t (&w)[8], uint32_t tag4) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t x = w[i] ^ tag4;
+    const uint32_t z = (x - 0x01010101u) & ~x & 0x80808080u;
+    m |= ((z * 0x00204081u) >> 28) << (4 * i);
+  }
+  return m;
+}
+
+// Placement + fingerprint probe of one position. Returns the global slot of
+// `key` or kNoSlot.
+__device__ __forceinline__ uint32_t lane_probe(const CacheDev& c, uint64_t key, bool valid) {
+  const uint64_t h2 = xxh64_key(key, kSlabSeed);
+  const uint32_t set = uint32_t(slabset_of(c, key));
+  const uint32_t first = c.W == 2 ? uint32_t(h2 & 1u) : uint32_t(fastmod(h2, c.W, c.mW));
+  const uint32_t tag4 = uint32_t(key_tag(h2)) * 0x01010101u;
+  if (!valid) return kNoSlot;
+  const unsigned long long* ck = reinterpret_cast<const unsigned long long*>(c.keys);
+  if (c.W == 2) {
+    // both slabs' fingerprints and masks in one round trip
+    uint32_t t0[8], t1[8];
+    const uint8_t* tp = c.tags + uint64_t(set) * 64;
+    ld256_nc(tp, t0);
+    ld256_nc(tp + 32, t1);
+    const uint2 mm = __ldg(reinterpret_cast<const uint2*>(c.masks) + set);
+    const uint32_t c0 = tag_candidates(t0, tag4) & mm.x;
+    const uint32_t c1 = tag_candidates(t1, tag4) & mm.y;
+    // probe order: slab `first`, then the other one only if `first` is full
+    const uint32_t ma = first ? mm.y : mm.x;
+    const uint32_t ca = first ? c1 : c0;
+    const uint32_t cb = (ma == kFullSlab) ? (first ? c0 : c1) : 0u;
+    const uint32_t sa = (set * 2 + first) * kSlotsPerSlab;
+    const uint32_t sb = (set * 2 + (first ^ 1u)) * kSlotsPerSlab;
+    uint64_t cand = uint64_t(ca) | (uint64_t(cb) << 32);
+    while (cand) {
+      // two candidates per round trip
+      const uint32_t b1 = __ffsll(cand) - 1;
+      cand &= cand - 1;
+      const uint32_t s1 = b1 < 32 ? sa + b1 : sb + (b1 - 32);
+      uint32_t s2 = kNoSlot;
+      if (cand) {
+        const uint32_t b2 = __ffsll(cand) - 1;
+        cand &= cand - 1;
+        s2 = b2 < 32 ? sa + b2 : sb + (b2 - 32);
+      }
+      const uint64_t k1 = __ldg(ck + s1);
+      const uint64_t k2 = s2 != kNoSlot ? __ldg(ck + s2) : ~key;
+      if (k1 == key) return s1;
+      if (k2 == key) return s2;
+    }
+    return kNoSlot;
+  }
+  // general W: slab by slab in probe order, stop at a hit or at the first
+  // slab that is not full
+  for (uint32_t step = 0; step < c.W; ++step) {
+    uint32_t sl = first + step;
+    sl = (sl >= c.W) ? sl - c.W : sl;
+    const uint32_t slab = set * c.W + sl;
+    uint32_t t[8];
+    ld256_nc(c.tags + uint64_t(slab) * 32, t);
+    const uint32_t m = __ldg(c.masks + slab);
+    uint32_t cand = tag_candidates(t, tag4) & m;
+    while (cand) {
+      const uint32_t b = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint32_t s = slab * kSlotsPerSlab + b;
+      if (__ldg(ck + s) == key) return s;
+    }
+    if (m != kFullSlab) break;
+  }
+  return kNoSlot;
+}
+
+// Copy of a warp's rows (lane i's row = slot `res` of lane i, or the
+// default row) into the warp's contiguous output block: `CH` floats per
+// access (8 = 256-bit, 4 = 128-bit, 1 = scalar), U accesses in flight.
+template <int CH>
+struct Chunk;
+template <>
+struct Chunk<8> {
+  uint32_t x[8];
+  __device__ __forceinline__ void load(const float* p) { ld256_nc(p, x); }
+  __device__ __forceinline__ void store(float* p) const { st256_cs(p, x); }
+};
+template <>
+struct Chunk<4> {
+  float4 x;
+  __device__ __forceinline__ void load(const float* p) {
+    x = ld_row_f4(reinterpret_cast<const float4*>(p));
+  }
+  __device__ __forceinline__ void store(float* p) const {
+    st_cs_f4(reinterpret_cast<float4*>(p), x);
+  }
+};
+template <>
+struct Chunk<1> {
+  float x;
+  __device__ __forceinline__ void load(const float* p) { x = __ldg(p); }
+  __device__ __forceinline__ void store(float* p) const { __stcs(p, x); }
+};
+
+template <int CH, int U>
+__device__ __forceinline__ void warp_copy_rows(const CacheDev& c, uint32_t res, uint32_t nrows,
+                                               const float* __restrict__ default_row,
+                                               float* __restrict__ obase) {
+  const uint32_t lane = lane_id();
+  const uint32_t d = c.d;
+  const uint32_t cpr = d / CH;  // chunks per row
+  const bool pow2 = (cpr & (cpr - 1)) == 0;
+  const uint32_t sh = __ffs(cpr) - 1;
+  const uint32_t total = nrows * cpr;
+  for (uint32_t c0 = 0; c0 < total; c0 += 32 * U) {
+    Chunk<CH> x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
+      uint32_t row = pow2 ? (ch >> sh) : (ch / cpr);
+      row = min(row, 31u);
+      const uint32_t slot = __shfl_sync(0xFFFFFFFFu, res, row);
+      if (ch < total) {
+        const uint32_t j = ch - row * cpr;
+        const float* src = slot != kNoSlot ? c.rows + uint64_t(slot) * d : default_row;
+        x[u].load(src + j * CH);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
+      if (ch < total) x[u].store(obase + uint64_t(ch) * CH);
+    }
+  }
+}
+
+// WARPS = warps per block; the block keeps a shared set of the slots it has
+// stamped, so a hot slot sees one global exchange per block (a power-law
+// batch repeats its top key in ~19% of positions). The register budget is
+// capped so the next lookup's blocks can be resident during this one's
+// copies (2 x 1024 threads per SM).
+template <int CH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
+    k_lookup_tag(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                 float* __restrict__ out, uint8_t* __restrict__ flags,
+                 const float* __restrict__ default_row, uint64_t stamp, LookupView v,
+                 uint32_t skip) {
+  constexpr int kThreadsB = WARPS * 32;
+  constexpr uint32_t kSetSize = 2 * kThreadsB;  // power of two for WARPS in {2, 4, 8, 16}
+  __shared__ uint32_t s_stamped[kSetSize];
+  for (uint32_t i = threadIdx.x; i < kSetSize; i += kThreadsB) s_stamped[i] = kNoSlot;
+  __syncthreads();
+  trace_min(v, 0, false);
+  const uint32_t lane = lane_id();
+  const uint64_t base = (uint64_t(blockIdx.x) * kThreadsB + threadIdx.x) & ~31ull;
+  const uint64_t pos = base + lane;
+  const bool valid = pos < n;
+  // ---- A: probe, claims, flags (independent of the previous call) ----
+  const uint64_t key = valid ? keys[pos] : 0ull;
+  const uint32_t res = lane_probe(c, key, valid);
+  const bool miss = valid && res == kNoSlot && !(skip & kSkipMiss);
+  const uint32_t um = warp_claim_misses(v, keys, pos, key, miss);
+  if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
+  // ---- B: the previous lookup on the stream is complete from here on ----
+  if (v.trace) {
+    __syncthreads();
+    trace_min(v, 1, true);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (v.trace) {
+    trace_min(v, 2, false);
+    trace_min(v, 3, true);
+  }
+  // ---- the last block to have made its claims completes the claim list
+  // (overlapping the other blocks' copies) ----
+  if (last_block(v, 0)) {
+    trace_min(v, 6, false);
+    finish_claims(v);
+    trace_min(v, 7, false);
+  }
+  // ---- C: recency exchange, row copy, counts ----
+  const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
+  bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
+  if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
+  unsigned long long old = stamp;
+  if (stamp_it) old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
+  const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
+  if (!(skip & kSkipCopy))
+    warp_copy_rows<CH, CH == 8 ? 4 : 8>(c, res, nrows, default_row, out + base * c.d);
+  warp_add_counts(v, (stamp_it && old != stamp) ? 1u : 0u, um,
+                  blockIdx.x * WARPS + (threadIdx.x >> 5));
+  if (v.trace) {
+    __syncthreads();
+    trace_min(v, 4, false);
+    trace_min(v, 5, true);
+  }
+  if (last_block(v, 1)) finish_counts(v);
+}
+
+// --------------------------------------------------------------- launch --
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupScratch& ls, uint32_t parity, cudaStream_t st) {
+                             const LookupView& v, bool after_lookup, cudaStream_t st) {
   if (n == 0) return 0;
-  // lanes per position: 8 by default (shorter per-lane state, more warps in
-  // flight); HPSB_LOOKUP_LANES=4 selects the 4-lane variant
-  static const int lanes = (std::getenv("HPSB_LOOKUP_LANES") &&
-                            std::atoi(std::getenv("HPSB_LOOKUP_LANES")) == 4)
-                               ? 4
-                               : 8;
-  const uint64_t per_block = uint64_t(kWarps) * (32 / lanes);
-  const unsigned grid = unsigned((n + per_block - 1) / per_block);
-  if (lanes == 4)
-    k_lookup<4><<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
-  else
-    k_lookup<8><<<grid, kThreads, 0, st>>>(c, keys, n, out, flags, default_row, stamp, ls, parity);
-  check_launch("lookup", 1);
-  static const bool no_finalize = std::getenv("HPSB_DIAG_NO_FINALIZE") != nullptr;  // diagnostic
-  if (no_finalize) return 1;
-  // claims are at most the unique keys; one wave of small blocks covers them.
-  // Programmatic dependent launch: scheduled while the lookup drains.
-  const unsigned fgrid = unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 4));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(fgrid);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
+  // Kernel choice (HPSB_LOOKUP_KERNEL): lane-per-position fingerprint probe
+  // by default; "warp4" / "warp8" = the warp-cooperative ballot probe (4 or
+  // 8 lanes per position) for A/B measurement.
+  static const int variant = [] {
+    const char* e = std::getenv("HPSB_LOOKUP_KERNEL");
+    if (e && std::string(e) == "warp4") return 4;
+    if (e && std::string(e) == "warp8") return 8;
+    return 0;
+  }();
+  static const uint32_t skip = [] {
+    const char* e = std::getenv("HPSB_DIAG_SKIP");
+    return e ? uint32_t(std::atoi(e)) : 0u;
+  }();
+  static const int warps = [] {
+    const char* e = std::getenv("HPSB_LOOKUP_WARPS");
+    const int w = e ? std::atoi(e) : 8;
+    return (w == 2 || w == 4 || w == 16) ? w : 8;
+  }();
+  // Programmatic dependent launch behind a preceding lookup kernel on this
+  // stream (HPSB_NO_PDL=1 disables): its phase A overlaps that lookup's tail.
+  static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_finalize, ls, parity);
-  check_launch("lookup_finalize", 1);
-  return 2;
+  cfg.numAttrs = (after_lookup && !no_pdl) ? 1 : 0;
+  if (variant == 0) {
+    auto aligned = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; };
+    const int ch = (c.d % 8 == 0 && aligned(out, 32) && aligned(default_row, 32))   ? 8
+                   : (c.d % 4 == 0 && aligned(out, 16) && aligned(default_row, 16)) ? 4
+                                                                                     : 1;
+    auto go = [&](auto chc, auto wc) {
+      constexpr int CH = decltype(chc)::value, WARPS = decltype(wc)::value;
+      cfg.gridDim = dim3(unsigned((n + WARPS * 32 - 1) / (WARPS * 32)));
+      cfg.blockDim = dim3(WARPS * 32);
+      cudaLaunchKernelEx(&cfg, k_lookup_tag<CH, WARPS>, c, keys, n, out, flags, default_row,
+                         stamp, v, skip);
+    };
+    auto by_warps = [&](auto chc) {
+      switch (warps) {
+        case 2: go(chc, std::integral_constant<int, 2>{}); break;
+        case 4: go(chc, std::integral_constant<int, 4>{}); break;
+        case 16: go(chc, std::integral_constant<int, 16>{}); break;
+        default: go(chc, std::integral_constant<int, 8>{}); break;
+      }
+    };
+    if (ch == 8) by_warps(std::integral_constant<int, 8>{});
+    else if (ch == 4) by_warps(std::integral_constant<int, 4>{});
+    else by_warps(std::integral_constant<int, 1>{});
+  } else {
+    const uint64_t per_block = uint64_t(kWarps) * (32 / variant);
+    cfg.gridDim = dim3(unsigned((n + per_block - 1) / per_block));
+    cfg.blockDim = dim3(kThreads);
+    if (variant == 4)
+      cudaLaunchKernelEx(&cfg, k_lookup<4>, c, keys, n, out, flags, default_row, stamp, v);
+    else
+      cudaLaunchKernelEx(&cfg, k_lookup<8>, c, keys, n, out, flags, default_row, stamp, v);
+  }
+  check_launch("lookup", 1);
+  return 1;
 }
 
+// ---------------------------------------------------- sync-branch scatter --
 __global__ void __launch_bounds__(256)
-    k_lookup_scatter(uint64_t n, uint32_t d, uint8_t* __restrict__ flags, LookupScratch ls,
+    k_lookup_scatter(uint64_t n, uint32_t d, uint8_t* __restrict__ flags, LookupView v,
                      const int32_t* __restrict__ row_of_claim, const float* __restrict__ staged,
                      float* __restrict__ out) {
   const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   if (flags[i] == 0) return;
-  const uint32_t e = ls.claim_of_slot[ls.miss_slot[i]];
+  const uint32_t e = v.claim_of_slot[v.miss_slot[i]];
   const int32_t r = row_of_claim[e];
   if (r < 0) return;  // absent from every tier: keep default + flag
   warp_copy_row(staged + uint64_t(r) * d, out + i * d, d);
@@ -367,14 +742,13 @@ __global__ void __launch_bounds__(256)
   if (lane_id() == 0) flags[i] = 0;
 }
 
-void launch_lookup_scatter(uint64_t n, uint32_t d, const uint8_t* flags_in, uint8_t* flags,
-                           const LookupScratch& ls, const int32_t* row_of_claim,
-                           const float* staged, float* out, cudaStream_t st) {
-  (void)flags_in;
+void launch_lookup_scatter(uint64_t n, uint32_t d, uint8_t* flags, const LookupView& v,
+                           const int32_t* row_of_claim, const float* staged, float* out,
+                           cudaStream_t st) {
   if (n == 0) return;
   const uint64_t threads = n * 32;
-  k_lookup_scatter<<<unsigned((threads + 255) / 256), 256, 0, st>>>(n, d, flags, ls,
-                                                                    row_of_claim, staged, out);
+  k_lookup_scatter<<<unsigned((threads + 255) / 256), 256, 0, st>>>(n, d, flags, v, row_of_claim,
+                                                                    staged, out);
   check_launch("lookup_scatter", 1);
 }
 

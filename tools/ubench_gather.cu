@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <random>
@@ -83,12 +84,30 @@ int main() {
       k_write<<<148 * 4, 256>>>(reinterpret_cast<float4*>(out) + (it % 8) * n4, n4);
     });
   }
-  for (uint64_t span : {uint64_t(32768), uint64_t(262144), slots}) {
+  // power-law (alpha 1.2) slots over the whole table: the lookup's real mix
+  std::vector<double> cdf(slots);
+  {
+    double acc = 0;
+    for (uint64_t r = 0; r < slots; ++r) cdf[r] = (acc += std::pow(double(r + 1), -1.2));
+    for (auto& x : cdf) x /= acc;
+  }
+  std::vector<uint32_t> perm(slots);
+  for (uint64_t i = 0; i < slots; ++i) perm[i] = uint32_t(i);
+  std::shuffle(perm.begin(), perm.end(), g);
+  for (uint64_t span : {uint64_t(0), uint64_t(32768), uint64_t(262144), slots}) {
     std::vector<uint32_t> h(uint64_t(n) * K);
-    for (auto& x : h) x = uint32_t(g() % span);
+    std::uniform_real_distribution<double> U(0, 1);
+    for (auto& x : h) {
+      if (span == 0) {
+        const uint64_t r = std::lower_bound(cdf.begin(), cdf.end(), U(g)) - cdf.begin();
+        x = perm[std::min<uint64_t>(r, slots - 1)];
+      } else {
+        x = uint32_t(g() % span);
+      }
+    }
     cudaMemcpy(slot, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
     char buf[128];
-    snprintf(buf, sizeof buf, "gather P=4 span %.0f MB", span * 512.0 / 1e6);
+    snprintf(buf, sizeof buf, "gather P=4 span %.0f MB (0=powerlaw)", span * 512.0 / 1e6);
     run(buf, [&](int it) {
       k_gather<4><<<n / 4 / 8, 256>>>(rows, slot + uint64_t(it) * n, n, out + uint64_t(it % 8) * n * D);
     });
