@@ -236,7 +236,7 @@ def ncu_traffic():
     f = ROOT / "profiles" / "ncu_traffic.json"
     if f.exists():
         try:
-            return json.loads(f.read_text()).get("lookup_probe_dram_bytes_per_launch")
+            return json.loads(f.read_text()).get("lookup_dram_bytes_per_launch")
         except Exception:
             return None
     return None
@@ -353,6 +353,9 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         bytes_per = float(np.mean([ab[s % pool][0] for s in range(steps)]))
+        # consecutive lookups overlap (programmatic dependent launch): the
+        # kernel's average duration over the timed region is total / steps;
+        # the event-bracketed per-call times above are single-call latencies
         return dict(total_ms=total_ms, p50_us=float(np.median(per) * 1e3),
                     p99_us=float(np.percentile(per, 99) * 1e3), k1_us=float(k1.mean() * 1e3),
                     h=h_meas, h_draw=h_draw, p=p, bytes_per_batch=bytes_per,
@@ -368,13 +371,13 @@ def run_ours(args, rank, world, local_rank):
             sweep[f"{h:.2f}"] = {
                 "keys_per_s": world * max(args.steps // 4, 4) * n / (r["total_ms"] / 1e3),
                 "p50_batch_us": r["p50_us"], "measured_unique_hit_rate": r["h"],
-                "probe_kernel_us": r["k1_us"],
-                "probe_kernel_gbs": r["bytes_per_batch"] / (r["k1_us"] * 1e-6) / 1e9}
+                "kernel_us": r["total_ms"] * 1e3 / max(args.steps // 4, 4),
+                "kernel_gbs": r["bytes_per_batch"] / (r["total_ms"] * 1e-3 / max(args.steps // 4, 4)) / 1e9}
     sweep[f"{args.hit:.2f}"] = {
         "keys_per_s": world * args.steps * n / (main["total_ms"] / 1e3),
         "p50_batch_us": main["p50_us"], "measured_unique_hit_rate": main["h"],
-        "probe_kernel_us": main["k1_us"],
-        "probe_kernel_gbs": main["bytes_per_batch"] / (main["k1_us"] * 1e-6) / 1e9}
+        "kernel_us": main["total_ms"] * 1e3 / args.steps,
+        "kernel_gbs": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9}
 
     e2e = None
     if not args.no_e2e:
@@ -383,7 +386,8 @@ def run_ours(args, rank, world, local_rank):
 
     value = world * args.steps * n / (main["total_ms"] / 1e3)
     peak, peak_kind = hbm_peak()
-    achieved = main["bytes_per_batch"] / (main["k1_us"] * 1e-6) / 1e9
+    kernel_us = main["total_ms"] * 1e3 / args.steps  # one lookup kernel per step
+    achieved = main["bytes_per_batch"] / (kernel_us * 1e-6) / 1e9
     result = None
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args, wl)
@@ -406,11 +410,12 @@ def run_ours(args, rank, world, local_rank):
             "unique_keys_per_batch": main["unique_per_batch"],
             "slabs_probed_per_unique_key": main["probes_per_unique"],
             "hit_rate_sweep": sweep,
-            "roofline": {"bound": "hbm", "kernel": "k_lookup_probe", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "k_lookup_tag", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
                          "algorithmic_bytes_per_launch": main["bytes_per_batch"],
-                         "kernel_us": main["k1_us"],
+                         "kernel_us": kernel_us,
+                         "single_call_latency_us": main["k1_us"],
                          "frac_of_8tbs_spec": achieved / 8000.0},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": main["launches"],

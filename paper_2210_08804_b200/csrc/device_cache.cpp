@@ -60,6 +60,7 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device
   HPSB_CUDA(cudaMalloc(&dev_.tags, slots));
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
+  lookup_marks_locked();  // allocated up front: lookups may be graph-captured
   HPSB_CUDA(cudaMemsetAsync(dev_.keys, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.counters, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.masks, 0, slabs * 4, stream_));
@@ -89,6 +90,7 @@ DeviceCache::~DeviceCache() {
   cudaFree(scan_.tile_ctr);
   cudaFree(scan_.status);
   cudaFree(trace_);
+  cudaFree(marks_);
   cudaEventDestroy(ev_in_);
   cudaEventDestroy(ev_out_);
   cudaStreamDestroy(stream_);
@@ -209,9 +211,13 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     last_op_lookup_ = false;
     lws_ = lookup_scratch_carve(b, cap);
     lcap_ = cap;
-    lparity_ = 0;
   }
-  LookupView v = lws_.v[lparity_];
+  // programmatic dependent of the previous lookup when nothing else was
+  // enqueued in between (the kernel orders itself against it)
+  static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
+  const bool chain = last_op_lookup_ && !no_pdl;
+  LookupView v = lookup_next_view(lws_, chain);
+  v.marks = lookup_marks_locked() + uint64_t(lws_.last) * capacity_slots();
   static const bool tracing = std::getenv("HPSB_TRACE") != nullptr;
   if (tracing) {
     if (trace_ == nullptr) {
@@ -234,8 +240,7 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
     last_op_lookup_ = false;
   }
-  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, v, last_op_lookup_, stream_);
-  lparity_ ^= 1u;
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, v, chain, stream_);
   last_op_lookup_ = true;
   if (prof_end_) {
     HPSB_CUDA(cudaEventRecordWithFlags(prof_end_, stream_, rec_flags));
@@ -348,6 +353,16 @@ size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, si
     HPSB_CUDA(cudaStreamSynchronize(stream_));
   }
   return n;
+}
+
+unsigned long long* DeviceCache::lookup_marks_locked() {
+  if (marks_ == nullptr) {
+    const uint64_t bytes = uint64_t(kLookupViews) * capacity_slots() * 8;
+    HPSB_CUDA(cudaMalloc(&marks_, bytes));
+    HPSB_CUDA(cudaMemsetAsync(marks_, 0, bytes, stream_));
+    last_op_lookup_ = false;
+  }
+  return marks_;
 }
 
 uint64_t DeviceCache::trace(unsigned long long* out) {

@@ -83,6 +83,10 @@ class DeviceCache {
   // Callers that enqueue their own work on stream() (the engine) call this
   // under mutex() so the next lookup does not chain onto a stale lookup.
   void note_stream_op() { last_op_lookup_ = false; }
+  // Mark arrays of the lookup kernels (call under mutex()); array i at
+  // + i * capacity_slots().
+  unsigned long long* lookup_marks_locked();
+  uint64_t capacity_slots() const { return cfg_.slabset_count * cfg_.slabs_per_set * 32ull; }
   uint64_t bump_clock() { return clock_.fetch_add(1, std::memory_order_relaxed) + 1; }
   // Device keys / rows, distinct keys guaranteed by the caller; stamp = the
   // current clock. Enqueued on stream(); scratch is the cache's own.
@@ -114,10 +118,12 @@ class DeviceCache {
   DeviceBuffer lbuf_;
   LookupScratch lws_;
   uint64_t lcap_ = 0;
-  uint32_t lparity_ = 0;
   // true while the last operation enqueued on stream_ is a lookup kernel
   // (the next lookup may then launch as its programmatic dependent)
   bool last_op_lookup_ = false;
+  // unique-hit marks of the lookup kernels: kLookupViews arrays of one u64
+  // per slot (lazily allocated; see LookupView::marks)
+  unsigned long long* marks_ = nullptr;
   // diagnostic lookup timeline ring (HPSB_TRACE=1): kTraceRing calls x 8
   unsigned long long* trace_ = nullptr;
   uint64_t trace_calls_ = 0;

@@ -124,7 +124,6 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);
-  parity = 0;
 
   const uint64_t host_bytes = a256(cap * 8) * 5 + a256(16) + a256(cap * 4) * 3 +
                               a256(cap * uint64_t(d) * 4) * 2 + a256(cap);
@@ -279,8 +278,8 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       } else {
         cache_->join_from(user);
       }
-      ws->lv = ws->ls.v[ws->parity];
-      ws->parity ^= 1u;
+      ws->lv = lookup_next_view(ws->ls, /*chain=*/false);
+      ws->lv.marks = cache_->lookup_marks_locked();
       cache_->note_stream_op();  // the engine's own copies follow on the stream
       launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->lv,
                           /*after_lookup=*/false, st);

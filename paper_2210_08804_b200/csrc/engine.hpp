@@ -83,7 +83,6 @@ struct Workspace {
   uint64_t* d_found_keys = nullptr;
   LookupScratch ls;
   LookupView lv;  // the view of the last lookup
-  uint32_t parity = 0;
   // pinned host
   PinnedBuffer hbuf;
   uint64_t* h_keys = nullptr;

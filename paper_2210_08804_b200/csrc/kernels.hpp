@@ -104,15 +104,33 @@ struct LookupView {
   // diagnostic phase timeline (HPSB_TRACE): 8 u64 per call, filled with
   // 0xFF before the call; fields hold min(t) or min(~t) (= max t) over blocks
   unsigned long long* trace = nullptr;
+  // ---- ordering between overlapping calls ----
+  unsigned long long* completed = nullptr;  // uses of this view completed so far
+  unsigned long long gen = 0;               // this call's use number of the view
+  // the previous call on the stream (its completion precedes this call's)
+  const unsigned long long* prev_completed = nullptr;
+  unsigned long long prev_target = 0;
+  // per-slot stamp of the last call that counted the slot as a unique hit
+  // (one array per concurrently running call, see DeviceCache::lookup_marks)
+  unsigned long long* marks = nullptr;
 };
-// Two views; consecutive calls on one stream alternate between them, so a
-// call can start while the previous one finishes (programmatic dependent
-// launch).
+// A ring of views: consecutive lookups on one stream take consecutive views,
+// so up to kLookupViews calls can be in flight (programmatic dependent
+// launch); a call waits on the device until the previous use of its view
+// has completed.
+constexpr int kLookupViews = 4;
 struct LookupScratch {
-  LookupView v[2];
+  LookupView v[kLookupViews];
+  uint64_t uses[kLookupViews] = {};  // host: uses handed out per view
+  int next = 0;
+  int last = -1;
 };
+// The view of the next call (host bookkeeping; marks not set). chain: the
+// call is launched as a programmatic dependent of the previous call taken
+// from this scratch, whose completion it then waits for before completing.
+LookupView lookup_next_view(LookupScratch& ls, bool chain);
 // Bytes / carving of a LookupScratch for batches of up to `cap` keys (the
-// caller zero-fills the block once).
+// caller zero-fills the block once; carving resets the host bookkeeping).
 size_t lookup_scratch_bytes(uint64_t cap);
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
 // One launch per lookup (probe, claims, stamps, row gather / default rows,

@@ -82,7 +82,20 @@ uint64_t view_bytes(uint64_t cap) {
 }
 }  // namespace
 
-size_t lookup_scratch_bytes(uint64_t cap) { return 2 * view_bytes(cap); }
+size_t lookup_scratch_bytes(uint64_t cap) { return kLookupViews * view_bytes(cap); }
+
+LookupView lookup_next_view(LookupScratch& ls, bool chain) {
+  const int i = ls.next;
+  LookupView v = ls.v[i];
+  v.gen = ls.uses[i]++;
+  if (chain && ls.last >= 0) {
+    v.prev_completed = ls.v[ls.last].completed;
+    v.prev_target = ls.uses[ls.last];  // that call's gen + 1
+  }
+  ls.last = i;
+  ls.next = (i + 1) % kLookupViews;
+  return v;
+}
 
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
   LookupScratch ls;
@@ -93,7 +106,7 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
     p += a256(b);
     return r;
   };
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kLookupViews; ++k) {
     LookupView& v = ls.v[k];
     v.cap = tcap;
     v.miss_table = reinterpret_cast<uint32_t*>(take(tcap * 4));
@@ -107,6 +120,7 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
     v.counts_out = small;                                 // [0..1] default destination
     v.list_ctr = reinterpret_cast<uint32_t*>(small + 2);  // claim counter
     v.done = reinterpret_cast<uint32_t*>(small + 3);      // [2] block tickets
+    v.completed = small + 4;
   }
   return ls;
 }
@@ -153,7 +167,26 @@ __device__ __forceinline__ void trace_min(const LookupView& v, int f, bool as_ma
     atomicMin(v.trace + f, as_max ? ~t : t);
   }
 }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Spins (one thread) until *p >= target. Calls on one stream only ever wait
+// on calls launched before them, whose blocks have all started, so this
+// cannot deadlock -- unless captured graphs are replayed out of capture
+// order; a wait longer than 2 s traps (the launch fails) instead of hanging.
+__device__ __forceinline__ void spin_ge(const unsigned long long* p, unsigned long long target) {
+  if (ld_acquire(p) >= target) return;
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire(p) < target) {
+    __nanosleep(200);
+    if (global_ns() - t0 > 2000000000ull) __trap();
+  }
+}
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -213,6 +246,11 @@ __device__ void finish_counts(const LookupView& v) {
       *v.list_ctr = 0u;
       v.done[0] = 0u;
       v.done[1] = 0u;
+      // completion order = launch order: this call completes after the
+      // previous one, so stream work after it sees every earlier lookup done
+      if (v.prev_completed != nullptr) spin_ge(v.prev_completed, v.prev_target);
+      __threadfence();
+      st_release(v.completed, v.gen + 1);  // the view is free for its next use
     }
   }
 }
@@ -280,6 +318,16 @@ __device__ __forceinline__ uint32_t warp_claim_misses(const LookupView& v,
   return claimed ? 1u : 0u;
 }
 
+// Recency exchange of a hit slot: the call's stamp becomes the slot's
+// counter (max: calls may overlap, a later call's stamp wins), and the
+// exchange on the call's mark array tells whether this is the call's first
+// hit of the slot (one unique hit).
+__device__ __forceinline__ uint32_t stamp_slot(const CacheDev& c, const LookupView& v,
+                                               uint32_t slot, unsigned long long stamp) {
+  atomicMax(reinterpret_cast<unsigned long long*>(c.counters + slot), stamp);
+  return atomicExch(v.marks + slot, stamp) != stamp ? 1u : 0u;
+}
+
 // Inserts `slot` into a block-shared open-addressing set; false when the
 // block already holds it (another warp of the block exchanged it).
 __device__ __forceinline__ bool block_set_insert(uint32_t* set, uint32_t size_pow2, uint32_t slot) {
@@ -338,6 +386,7 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int RC = 32 / L;   // float4 chunks per lane per 128-float row segment
   __shared__ uint32_t s_stamped[1u << kSetBits];
   for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += kThreads) s_stamped[i] = kNoSlot;
+  if (threadIdx.x == 0) spin_ge(v.completed, v.gen);
   __syncthreads();
   const uint32_t lane = lane_id();
   const uint32_t q = lane / L, sub = lane % L;
@@ -398,13 +447,11 @@ __global__ void __launch_bounds__(kThreads)
     v.miss_slot[pos] = tslot;
   }
   if (valid && sub == 0) flags[pos] = res == kNoSlot ? 1 : 0;
-  pdl_wait();
   pdl_trigger();
   // recency exchange by the group's lane 0, issued before the copy
-  unsigned long long old = stamp;
   bool stamp_it = valid && sub == 0 && res != kNoSlot;
   if (stamp_it) stamp_it = block_set_insert(s_stamped, 1u << kSetBits, res);
-  if (stamp_it) old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
+  const uint32_t uh = stamp_it ? stamp_slot(c, v, res, stamp) : 0u;
   // row copy (after the call's bookkeeping): lane `sub` moves float4
   // chunks sub, sub+L, sub+2L, ...
   auto copy_row = [&] {
@@ -449,8 +496,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (last_block(v, 0)) finish_claims(v);
   if (valid) copy_row();
-  warp_add_counts(v, (stamp_it && old != stamp) ? 1u : 0u, claimed ? 1u : 0u,
-                  blockIdx.x * kWarps + (threadIdx.x >> 5));
+  warp_add_counts(v, uh, claimed ? 1u : 0u, blockIdx.x * kWarps + (threadIdx.x >> 5));
   if (last_block(v, 1)) finish_counts(v);
 }
 
@@ -608,6 +654,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   constexpr uint32_t kSetSize = 2 * kThreadsB;  // power of two for WARPS in {2, 4, 8, 16}
   __shared__ uint32_t s_stamped[kSetSize];
   for (uint32_t i = threadIdx.x; i < kSetSize; i += kThreadsB) s_stamped[i] = kNoSlot;
+  // the view's previous use must have completed (normally long ago)
+  if (threadIdx.x == 0) spin_ge(v.completed, v.gen);
   __syncthreads();
   trace_min(v, 0, false);
   const uint32_t lane = lane_id();
@@ -620,12 +668,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   const bool miss = valid && res == kNoSlot && !(skip & kSkipMiss);
   const uint32_t um = warp_claim_misses(v, keys, pos, key, miss);
   if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
-  // ---- B: the previous lookup on the stream is complete from here on ----
+  // ---- B: the next lookup on the stream may start (programmatic
+  // dependent launch); nothing below depends on the previous one ----
   if (v.trace) {
     __syncthreads();
     trace_min(v, 1, true);
   }
-  pdl_wait();
   pdl_trigger();
   if (v.trace) {
     trace_min(v, 2, false);
@@ -642,13 +690,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
   bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
   if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
-  unsigned long long old = stamp;
-  if (stamp_it) old = atomicExch(reinterpret_cast<unsigned long long*>(c.counters + res), stamp);
+  const uint32_t uh = stamp_it ? stamp_slot(c, v, res, stamp) : 0u;
   const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
   if (!(skip & kSkipCopy))
     warp_copy_rows<CH, CH == 8 ? 4 : 8>(c, res, nrows, default_row, out + base * c.d);
-  warp_add_counts(v, (stamp_it && old != stamp) ? 1u : 0u, um,
-                  blockIdx.x * WARPS + (threadIdx.x >> 5));
+  warp_add_counts(v, uh, um, blockIdx.x * WARPS + (threadIdx.x >> 5));
   if (v.trace) {
     __syncthreads();
     trace_min(v, 4, false);
