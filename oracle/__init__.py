@@ -28,6 +28,8 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libhps_ref.so"
+# the reference's tests/unit/test_slab_cache.cpp built against include/hps/slab_cache.hpp
+REF_CACHE_TEST = HERE / "_ref" / "test_slab_cache_b200"
 REF_SRC = Path("/root/reference/proj")
 
 _P = C.c_void_p

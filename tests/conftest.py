@@ -22,6 +22,7 @@ def _built():
         _build.build()
     import oracle
 
-    if not oracle.ORACLE_SO.exists() or (oracle.REF_SRC.exists() and not oracle.REF_SO.exists()):
+    if not oracle.ORACLE_SO.exists() or (oracle.REF_SRC.exists() and not (
+            oracle.REF_SO.exists() and oracle.REF_CACHE_TEST.exists())):
         oracle.build()
     yield

@@ -1,0 +1,55 @@
+"""The drop-in C++ surface: include/hps/slab_cache.hpp re-exposes the
+reference's hps::SlabCache (slab_cache.hpp:23-178) over the C ABI, and the
+reference's OWN unit test, tests/unit/test_slab_cache.cpp, compiled unchanged
+against it (oracle/Makefile target _ref/test_slab_cache_b200; doctest is the
+local stand-in oracle/doctest_stub), must pass on the GPU."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+import oracle
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_dropin_header_compiles_standalone(tmp_path):
+    """Without the reference's headers on the path the shim supplies its own
+    vocabulary (EmbeddingKey, TierFault) and still compiles."""
+    src = tmp_path / "use.cpp"
+    src.write_text(
+        '#include "hps/slab_cache.hpp"\n'
+        "int main() {\n"
+        "  hps::SlabCacheConfig c{.slabset_count = 4, .slabs_per_set = 2, .dimension = 8};\n"
+        "  static_assert(sizeof(hps::CacheMiss) == 16);\n"
+        "  return int(hps::SlabCache::slabset_of(42, c.slabset_count) >= 4);\n"
+        "}\n")
+    exe = tmp_path / "use"
+    r = subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT / 'include'}", str(src),
+                        f"-L{ROOT / 'paper_2210_08804_b200'}", "-lhps_b200",
+                        f"-Wl,-rpath,{ROOT / 'paper_2210_08804_b200'}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    # placement hash runs on the host: no GPU needed
+    assert subprocess.run([str(exe)]).returncode == 0
+
+
+def test_reference_unit_test_binary_is_built_against_the_library():
+    if not oracle.REF_CACHE_TEST.exists():
+        pytest.skip("reference sources absent and no prebuilt binary")
+    r = subprocess.run(["ldd", str(oracle.REF_CACHE_TEST)], capture_output=True, text=True)
+    assert "libhps_b200.so" in r.stdout
+    # the reference's own cache implementation is NOT linked in
+    nm = subprocess.run(["nm", "-C", str(oracle.REF_CACHE_TEST)], capture_output=True,
+                        text=True).stdout
+    assert "hps::SlabCache::apply_query" not in nm and "hps::SlabCache::run_grouped" not in nm
+
+
+@pytest.mark.gpu
+def test_reference_slab_cache_unit_test_passes_on_b200():
+    if not oracle.REF_CACHE_TEST.exists():
+        pytest.skip("binary not built")
+    r = subprocess.run([str(oracle.REF_CACHE_TEST)], capture_output=True, text=True, timeout=600)
+    tail = "\n".join(r.stderr.splitlines()[-40:])
+    assert r.returncode == 0, tail
+    assert "0 failed" in r.stderr, tail
