@@ -1,0 +1,233 @@
+// include/hps/lookup_engine.hpp -- drop-in replacement for the reference's
+// core/include/hps/lookup_engine.hpp (hps::LookupEngine, tier_fetch,
+// lookup_engine.hpp:29-196), backed by the B200 lookup engine of
+// libhps_b200.so (hps_engine_* in include/hps_b200.h).
+//
+// The dedup -> cache query -> hit-rate switch -> expansion runs on the GPU
+// (one kernel per lookup, lookup_kernels.cu); the misses are fetched from
+// the caller's own storage tiers -- the reference's VolatileStore and
+// PersistentStore, which a reference build keeps -- through the engine's
+// cold-tier callback, in the reference's tier order (tier_fetch below,
+// lookup_engine.cpp:50-89), and admitted with the GPU replace.
+//
+// Use: this repo's include/ ahead of core/include, link libhps_b200.so and
+// the reference's tier sources (types.cpp, volatile_store.cpp,
+// persistent_store.cpp) instead of slab_cache.cpp / lookup_engine.cpp. The
+// reference's tests/unit/test_lookup_engine.cpp compiles unchanged against
+// it (oracle/Makefile target _ref/test_lookup_engine_b200).
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hps/persistent_store.hpp"
+#include "hps/slab_cache.hpp"
+#include "hps/types.hpp"
+#include "hps/volatile_store.hpp"
+#include "hps_b200.h"
+
+namespace hps {
+
+// lookup_engine.hpp:29-37
+struct EngineConfig {
+  double hit_rate_threshold = 0.8;
+  std::vector<float> default_vector;
+  std::size_t workspace_pool_size = 16;
+  std::uint32_t async_worker_count = 2;
+  bool volatile_tier_enabled = true;
+};
+
+// lookup_engine.hpp:115-119
+struct TierCounters {
+  std::uint64_t vdb_hits = 0;
+  std::uint64_t pdb_hits = 0;
+  std::uint64_t missing = 0;
+};
+
+// lookup_engine.cpp:50-89: volatile tier first, persistent for the rest,
+// persistent hits promoted to the volatile tier asynchronously; found rows
+// in (volatile-found, persistent-found) order.
+inline FetchResult tier_fetch(const TableId& table, std::span<const EmbeddingKey> keys,
+                              VolatileStore* vdb, PersistentStore& pdb,
+                              TierCounters* counters = nullptr) {
+  FetchResult out;
+  if (keys.empty()) return out;
+  const bool use_vdb = vdb != nullptr && vdb->has_table(table.name);
+  std::vector<EmbeddingKey> remaining;
+  if (use_vdb) {
+    FetchResult v = vdb->lookup(table.name, keys);
+    if (counters) counters->vdb_hits += v.found_keys.size();
+    out.found_keys = std::move(v.found_keys);
+    out.found_vectors = std::move(v.found_vectors);
+    remaining = std::move(v.missing_keys);
+  } else {
+    remaining.assign(keys.begin(), keys.end());
+  }
+  if (!remaining.empty()) {
+    FetchResult p = pdb.get(table.name, remaining);
+    if (counters) {
+      counters->pdb_hits += p.found_keys.size();
+      counters->missing += p.missing_keys.size();
+    }
+    if (use_vdb && !p.found_keys.empty())
+      vdb->insert_async(table.name, p.found_keys, p.found_vectors);
+    out.found_keys.insert(out.found_keys.end(), p.found_keys.begin(), p.found_keys.end());
+    out.found_vectors.insert(out.found_vectors.end(), p.found_vectors.begin(),
+                             p.found_vectors.end());
+    out.missing_keys = std::move(p.missing_keys);
+  }
+  return out;
+}
+
+// lookup_engine.hpp:129-142
+struct EngineStatsSnapshot {
+  std::uint64_t queries = 0;
+  std::uint64_t queried_keys = 0;
+  std::uint64_t unique_keys = 0;
+  std::uint64_t cache_hits = 0;
+  std::uint64_t cache_misses = 0;
+  std::uint64_t sync_batches = 0;
+  std::uint64_t async_batches = 0;
+  std::uint64_t defaults_returned = 0;
+  std::uint64_t vdb_hits = 0;
+  std::uint64_t pdb_hits = 0;
+  std::uint64_t tier_missing = 0;
+  std::uint64_t async_faults = 0;
+};
+
+// lookup_engine.hpp:145-150
+struct LookupOutcome {
+  bool sync_branch = false;
+  double unique_hit_rate = 0.0;
+  std::size_t unique_count = 0;
+  std::size_t defaults_returned = 0;
+};
+
+// The engine's bounded workspace pool (lookup_engine.hpp:49-71): each
+// workspace is a device + pinned staging set; acquiring one is the admission
+// ticket, a background fill holds it until the fetched rows are admitted.
+class WorkspacePool {
+ public:
+  std::size_t size() const { return info(0); }
+  std::size_t outstanding() const { return info(1); }
+  std::size_t peak_outstanding() const { return info(2); }
+
+ private:
+  friend class LookupEngine;
+  std::size_t info(int which) const {
+    std::uint64_t v[3] = {0, 0, 0};
+    b200_detail::check(hps_engine_pool_info(engine_, &v[0], &v[1], &v[2]));
+    return v[which];
+  }
+  hps_engine* engine_ = nullptr;
+};
+
+class LookupEngine {
+ public:
+  // lookup_engine.cpp:91-117 (same validation, std::invalid_argument)
+  LookupEngine(const TableId& table, SlabCache& cache, VolatileStore* vdb, PersistentStore& pdb,
+               EngineConfig config)
+      : table_(table), cache_(cache), vdb_(vdb), pdb_(pdb), config_(std::move(config)) {
+    if (config_.workspace_pool_size == 0)
+      throw std::invalid_argument("workspace pool size must be positive");
+    validate_table_id(table_);
+    hps_engine_config c{};
+    c.hit_rate_threshold = config_.hit_rate_threshold;
+    c.default_vector = config_.default_vector.empty() ? nullptr : config_.default_vector.data();
+    c.default_vector_len = uint32_t(config_.default_vector.size());
+    c.workspace_pool_size = uint32_t(config_.workspace_pool_size);
+    c.async_worker_count = config_.async_worker_count;
+    c.volatile_tier_enabled = 0;  // the tiers are reached through cold_fetch
+    c.max_batch = 0;
+    b200_detail::check(hps_engine_create(table_.name.c_str(), table_.dimension, cache_.handle(),
+                                         nullptr, &LookupEngine::cold_fetch, this, &c, &h_));
+    pool_.engine_ = h_;
+  }
+  ~LookupEngine() { hps_engine_destroy(h_); }
+
+  LookupEngine(const LookupEngine&) = delete;
+  LookupEngine& operator=(const LookupEngine&) = delete;
+
+  // lookup_engine.cpp:130-241
+  LookupResult lookup(std::span<const EmbeddingKey> keys, LookupOutcome* outcome = nullptr) {
+    LookupResult r;
+    r.dimension = table_.dimension;
+    r.vectors.resize(keys.size() * table_.dimension);
+    r.miss_flags.resize(keys.size());
+    hps_lookup_outcome o{};
+    b200_detail::check(hps_engine_lookup(h_, keys.data(), keys.size(), r.vectors.data(),
+                                         r.vectors.size(), r.miss_flags.data(), &o, HPS_MEM_HOST,
+                                         nullptr));
+    if (outcome) {
+      outcome->sync_branch = o.sync_branch != 0;
+      outcome->unique_hit_rate = o.unique_hit_rate;
+      outcome->unique_count = o.unique_count;
+      outcome->defaults_returned = o.defaults_returned;
+    }
+    return r;
+  }
+
+  void drain_async() { b200_detail::check(hps_engine_drain_async(h_)); }
+
+  EngineStatsSnapshot stats() const {
+    hps_engine_stats s{};
+    b200_detail::check(hps_engine_get_stats(h_, &s));
+    EngineStatsSnapshot o;
+    o.queries = s.queries;
+    o.queried_keys = s.queried_keys;
+    o.unique_keys = s.unique_keys;
+    o.cache_hits = s.cache_hits;
+    o.cache_misses = s.cache_misses;
+    o.sync_batches = s.sync_batches;
+    o.async_batches = s.async_batches;
+    o.defaults_returned = s.defaults_returned;
+    o.async_faults = s.async_faults;
+    // tier split as seen by tier_fetch (sync and background fetches alike)
+    o.vdb_hits = vdb_hits_.load();
+    o.pdb_hits = pdb_hits_.load();
+    o.tier_missing = missing_.load();
+    return o;
+  }
+  const TableId& table() const { return table_; }
+  WorkspacePool& workspace_pool() { return pool_; }
+
+ private:
+  // hps_cold_fetch_fn: the reference tiers behind the GPU engine
+  static int cold_fetch(void* ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
+                        float* found_vectors, size_t* n_found, uint64_t* missing_keys,
+                        size_t* n_missing) {
+    auto* self = static_cast<LookupEngine*>(ctx);
+    try {
+      TierCounters tc;
+      FetchResult f = tier_fetch(self->table_, std::span<const EmbeddingKey>(keys, n),
+                                 self->config_.volatile_tier_enabled ? self->vdb_ : nullptr,
+                                 self->pdb_, &tc);
+      self->vdb_hits_ += tc.vdb_hits;
+      self->pdb_hits_ += tc.pdb_hits;
+      self->missing_ += tc.missing;
+      std::copy(f.found_keys.begin(), f.found_keys.end(), found_keys);
+      std::copy(f.found_vectors.begin(), f.found_vectors.end(), found_vectors);
+      std::copy(f.missing_keys.begin(), f.missing_keys.end(), missing_keys);
+      *n_found = f.found_keys.size();
+      *n_missing = f.missing_keys.size();
+      return 0;
+    } catch (...) {
+      return 1;  // surfaces as TierFault (sync) or an async fault
+    }
+  }
+
+  TableId table_;
+  SlabCache& cache_;
+  VolatileStore* vdb_;
+  PersistentStore& pdb_;
+  EngineConfig config_;
+  hps_engine* h_ = nullptr;
+  WorkspacePool pool_;
+  std::atomic<std::uint64_t> vdb_hits_{0}, pdb_hits_{0}, missing_{0};
+};
+
+}  // namespace hps

@@ -30,6 +30,8 @@ ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libhps_ref.so"
 # the reference's tests/unit/test_slab_cache.cpp built against include/hps/slab_cache.hpp
 REF_CACHE_TEST = HERE / "_ref" / "test_slab_cache_b200"
+# tests/unit/test_lookup_engine.cpp built against include/hps/lookup_engine.hpp
+REF_ENGINE_TEST = HERE / "_ref" / "test_lookup_engine_b200"
 REF_SRC = Path("/root/reference/proj")
 
 _P = C.c_void_p

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <unordered_map>
 
 namespace hpsb {
 
@@ -71,14 +72,16 @@ void tier_fetch_staged(VolatileStore* vdb, const std::string& table, uint32_t di
   }
   std::copy(cf_keys.begin(), cf_keys.begin() + cf, found_keys + nf);
   std::copy(cf_rows.begin(), cf_rows.begin() + cf * dim, rows + nf * dim);
-  // cold hits are a subsequence of `remaining` (input order): two pointers
-  size_t j = 0;
-  for (size_t i = 0; i < n && j < cf; ++i) {
+  // cold hits in the cold tier's own order (a tier that reads through
+  // further levels, like the reference's tier_fetch, need not keep input
+  // order): map them back by key (keys are unique)
+  std::unordered_map<uint64_t, int32_t> cold_row;
+  cold_row.reserve(cf * 2);
+  for (size_t j = 0; j < cf; ++j) cold_row.emplace(cf_keys[j], int32_t(nf + j));
+  for (size_t i = 0; i < n; ++i) {
     if (row_of[i] >= 0) continue;
-    if (keys[i] == cf_keys[j]) {
-      row_of[i] = int32_t(nf + j);
-      ++j;
-    }
+    auto it = cold_row.find(keys[i]);
+    if (it != cold_row.end()) row_of[i] = it->second;
   }
   std::copy(cm_keys.begin(), cm_keys.begin() + cm, missing_keys);
   *n_found = nf + cf;

@@ -23,6 +23,7 @@ def _built():
     import oracle
 
     if not oracle.ORACLE_SO.exists() or (oracle.REF_SRC.exists() and not (
-            oracle.REF_SO.exists() and oracle.REF_CACHE_TEST.exists())):
+            oracle.REF_SO.exists() and oracle.REF_CACHE_TEST.exists()
+            and oracle.REF_ENGINE_TEST.exists())):
         oracle.build()
     yield

@@ -1,8 +1,10 @@
-"""The drop-in C++ surface: include/hps/slab_cache.hpp re-exposes the
-reference's hps::SlabCache (slab_cache.hpp:23-178) over the C ABI, and the
-reference's OWN unit test, tests/unit/test_slab_cache.cpp, compiled unchanged
-against it (oracle/Makefile target _ref/test_slab_cache_b200; doctest is the
-local stand-in oracle/doctest_stub), must pass on the GPU."""
+"""The drop-in C++ surface: include/hps/slab_cache.hpp and
+include/hps/lookup_engine.hpp re-expose the reference's hps::SlabCache
+(slab_cache.hpp:23-178) and hps::LookupEngine / tier_fetch
+(lookup_engine.hpp:29-196) over the C ABI, and the reference's OWN unit
+tests, tests/unit/test_slab_cache.cpp and test_lookup_engine.cpp, compiled
+unchanged against them (oracle/Makefile targets _ref/test_*_b200; doctest is
+the local stand-in oracle/doctest_stub), must pass on the GPU."""
 import subprocess
 from pathlib import Path
 
@@ -34,22 +36,28 @@ def test_dropin_header_compiles_standalone(tmp_path):
     assert subprocess.run([str(exe)]).returncode == 0
 
 
-def test_reference_unit_test_binary_is_built_against_the_library():
-    if not oracle.REF_CACHE_TEST.exists():
+BINARIES = [oracle.REF_CACHE_TEST, oracle.REF_ENGINE_TEST]
+
+
+@pytest.mark.parametrize("exe", BINARIES, ids=lambda p: p.name)
+def test_reference_unit_test_binary_is_built_against_the_library(exe):
+    if not exe.exists():
         pytest.skip("reference sources absent and no prebuilt binary")
-    r = subprocess.run(["ldd", str(oracle.REF_CACHE_TEST)], capture_output=True, text=True)
+    r = subprocess.run(["ldd", str(exe)], capture_output=True, text=True)
     assert "libhps_b200.so" in r.stdout
-    # the reference's own cache implementation is NOT linked in
-    nm = subprocess.run(["nm", "-C", str(oracle.REF_CACHE_TEST)], capture_output=True,
-                        text=True).stdout
-    assert "hps::SlabCache::apply_query" not in nm and "hps::SlabCache::run_grouped" not in nm
+    # the reference's own cache / engine implementation is NOT linked in
+    nm = subprocess.run(["nm", "-C", str(exe)], capture_output=True, text=True).stdout
+    for sym in ("hps::SlabCache::apply_query", "hps::SlabCache::run_grouped",
+                "hps::LookupEngine::async_loop"):
+        assert sym not in nm
 
 
 @pytest.mark.gpu
-def test_reference_slab_cache_unit_test_passes_on_b200():
-    if not oracle.REF_CACHE_TEST.exists():
+@pytest.mark.parametrize("exe", BINARIES, ids=lambda p: p.name)
+def test_reference_unit_test_passes_on_b200(exe):
+    if not exe.exists():
         pytest.skip("binary not built")
-    r = subprocess.run([str(oracle.REF_CACHE_TEST)], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     tail = "\n".join(r.stderr.splitlines()[-40:])
     assert r.returncode == 0, tail
     assert "0 failed" in r.stderr, tail
