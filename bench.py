@@ -379,6 +379,9 @@ def run_ours(args, rank, world, local_rank):
         "kernel_us": main["total_ms"] * 1e3 / args.steps,
         "kernel_gbs": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9}
 
+    online = None
+    if not args.no_online:
+        online = run_online(args, hps, torch, cache, wl, dev, st, dkeys_for_online(wl, dev, torch))
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, hps, torch, cache, wl, dev, rank, dist)
@@ -417,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
                          "kernel_us": kernel_us,
                          "single_call_latency_us": main["k1_us"],
                          "frac_of_8tbs_spec": achieved / 8000.0},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "online": online,
             "gpu_launches": main["launches"],
         }
         print(json.dumps(result))
@@ -425,6 +428,89 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def dkeys_for_online(wl, dev, torch):
+    batches, _, _ = wl.batches(0.9, 8, seed=5000)
+    return [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
+
+
+def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
+    """Online-training legs (BASELINE.json configs[3], SURVEY §8d cfg 4):
+    * refresh-style Update of EVERY resident row (1.02 GB of rows at cfg 2):
+      GB of cache rows rewritten per second -- the paper's Table 3 metric
+      (A100: 194.2 GB/s at 1 GB, PAPER.md:529);
+    * Dump of the whole resident key set (device kernel + 16 MB D2H);
+    * cfg 4: every lookup batch followed by a stream-ordered Update of 1 %% of
+      the resident rows (20K rows), keys/s of the interleaved stream."""
+    d, n = wl.dim, wl.batch
+    sp = st.cuda_stream
+    resident = cache.dump_all()
+    R = len(resident)
+    rk = torch.from_numpy(resident.view(np.int64)).to(dev)
+    rows = torch.empty(R * d, device=dev).uniform_(-1, 1)
+    written = torch.zeros(1, dtype=torch.int64, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    reps = 5
+    for _ in range(2):
+        cache.update_device_async(rk.data_ptr(), R, rows.data_ptr(), written.data_ptr(), sp)
+    torch.cuda.synchronize()
+    ev[0].record(st)
+    for _ in range(reps):
+        cache.update_device_async(rk.data_ptr(), R, rows.data_ptr(), written.data_ptr(), sp)
+    ev[1].record(st)
+    torch.cuda.synchronize()
+    upd_ms = ev[0].elapsed_time(ev[1]) / reps
+    assert int(written.item()) == R
+    row_bytes = R * d * 4
+    t0 = time.perf_counter()
+    for _ in range(3):
+        cache.dump_all()
+    dump_ms = (time.perf_counter() - t0) * 1e3 / 3
+    # cfg 4: lookup + 1 % update per batch
+    u = max(1, R // 100)
+    rng = np.random.default_rng(77)
+    upd_sets = []
+    for j in range(8):
+        idx = rng.choice(R, u, replace=False)
+        upd_sets.append((torch.from_numpy(resident[idx].view(np.int64)).to(dev),
+                         torch.empty(u * d, device=dev).uniform_(-1, 1)))
+    out = [torch.empty(n * d, device=dev) for _ in range(4)]
+    fl = torch.empty(n, dtype=torch.uint8, device=dev)
+    mk = torch.empty(n, dtype=torch.int64, device=dev)
+    mf = torch.empty(n, dtype=torch.int32, device=dev)
+    steps = max(args.steps // 4, 8)
+    cnt = torch.zeros(2 * steps, dtype=torch.int64, device=dev)
+    dr = torch.zeros(d, device=dev)
+
+    def step(s):
+        cache.lookup_device(dkeys[s % 8].data_ptr(), n, out[s % 4].data_ptr(), fl.data_ptr(),
+                            dr.data_ptr(), mk.data_ptr(), mf.data_ptr(), cnt[2 * s:].data_ptr(), sp)
+        k, r = upd_sets[s % 8]
+        cache.update_device_async(k.data_ptr(), u, r.data_ptr(), written.data_ptr(), sp)
+
+    for s in range(4):
+        step(s)
+    torch.cuda.synchronize()
+    g = hps.StreamGraph(sp)
+    with g:
+        for s in range(steps):
+            step(s)
+    torch.cuda.synchronize()
+    ev[0].record(st)
+    g.launch()
+    ev[1].record(st)
+    torch.cuda.synchronize()
+    mixed_ms = ev[0].elapsed_time(ev[1]) / steps
+    return {"update_all_resident": {"rows": R, "row_bytes": row_bytes, "ms": upd_ms,
+                                    "gb_per_s": row_bytes / (upd_ms * 1e-3) / 1e9,
+                                    "paper_a100_gb_per_s_1gb": 194.20,
+                                    "vs_paper_a100": row_bytes / (upd_ms * 1e-3) / 1e9 / 194.20},
+            "dump_all": {"keys": R, "ms": dump_ms, "api": "SlabCache::dump_all (device kernel + D2H)",
+                         "paper_a100_ms_1gb": 0.064},
+            "cfg4_lookup_plus_update_1pct": {"keys_per_s": n / (mixed_ms * 1e-3),
+                                             "updated_rows_per_batch": u,
+                                             "ms_per_batch": mixed_ms}}
 
 
 def run_e2e(args, hps, torch, cache, wl, dev, rank, dist):
@@ -587,6 +673,7 @@ def main():
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-online", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -159,6 +159,13 @@ int hps_cache_update(hps_cache* cache, const uint64_t* keys, size_t n,
                      const float* vectors, size_t vectors_len, size_t* written,
                      int mem, void* stream);
 
+/* Stream-ordered SlabCache::update on device pointers (the online-training
+ * path: no host synchronisation). *written (device u64, may be NULL) gets the
+ * number of positions whose key was resident once `stream` reaches the call. */
+int hps_cache_update_device(hps_cache* cache, const uint64_t* keys, size_t n,
+                            const float* vectors, size_t vectors_len, uint64_t* written,
+                            void* stream);
+
 /* replaces DumpCursor::next (slab_cache.cpp:367-394) over the slabset range
  * [set_begin, set_end): resident keys in set, slab, slot order into the host
  * buffer out (capacity cap). *n_out = number of resident keys in the range

@@ -144,6 +144,7 @@ SIGNATURES = {
     "hps_cache_check_invariants": (C.c_int, [_P]),
     "hps_cache_export_state": (C.c_int, [_P, _P, _P, _P, _P]),
     "hps_cache_debug_trace": (C.c_int, [_P, _P, C.c_size_t, _U64P]),
+    "hps_cache_update_device": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P]),
     "hps_vdb_create": (C.c_int, [C.c_uint32, C.POINTER(_P)]),
     "hps_vdb_destroy": (C.c_int, [_P]),
     "hps_vdb_register_table": (C.c_int, [_P, C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64]),
@@ -400,6 +401,13 @@ class SlabCache:
         _check(lib().hps_cache_update(self._h, keys_ptr, n, rows_ptr, n * self._dim, C.byref(w),
                                       HPS_MEM_DEVICE, stream or None))
         return w.value
+
+    def update_device_async(self, keys_ptr: int, n: int, rows_ptr: int, written_ptr: int = 0,
+                            stream: int = 0) -> None:
+        """hps_cache_update_device: stream-ordered update on device pointers;
+        the written count lands in device memory at written_ptr (optional)."""
+        _check(lib().hps_cache_update_device(self._h, keys_ptr, n, rows_ptr, n * self._dim,
+                                             written_ptr or None, stream or None))
 
     def dump(self, batch_size: int) -> "DumpCursor":
         if batch_size == 0:

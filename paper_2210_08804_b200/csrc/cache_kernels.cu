@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "kernels.hpp"
 #include "probe.cuh"
+#include "tag_probe.cuh"
 
 namespace hpsb {
 
@@ -348,92 +349,92 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
 }
 
 // ----------------------------------------------------------------- update --
-// Overwrite resident rows; the last occurrence of a key in input order
-// wins (the reference applies a set's keys in input order,
-// slab_cache.cpp:137-142, 328-358). Phase A probes and records
-// max(position) per hit slot; phase B lets only that position write.
-size_t update_scratch_bytes(uint64_t n) {
-  const uint64_t cap = pow2_at_least(2 * n);
-  return align_up(cap * 8, 256) + align_up(cap * 4, 256) + align_up(n * 4, 256) + 256;
+// Overwrite resident rows; the last occurrence of a key in input order wins
+// (the reference applies a set's keys in input order, slab_cache.cpp:137-142,
+// 328-358), counters untouched, nothing admitted.
+//   k_update_probe  lane per position: fingerprint probe (tag_probe.cuh);
+//                   slot recorded; max(position + 1) per hit slot into the
+//                   cache's `winner` array (fire-and-forget); hits counted
+//   k_update_write  lane per position, warp per 32: the winning position of
+//                   each slot copies its row (256-bit loads from the
+//                   contiguous input block, write-back stores into the table)
+//                   and clears the winner entry (the array is all-zero
+//                   between calls)
+__global__ void __launch_bounds__(256)
+    k_update_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                   uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner,
+                   unsigned long long* written) {
+  const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool valid = pos < n;
+  const uint64_t key = valid ? keys[pos] : 0ull;
+  const uint32_t res = lane_probe(c, key, valid);
+  if (valid) slot_of[pos] = res;
+  if (res != kNoSlot) atomicMax(winner + res, uint32_t(pos + 1));
+  const uint32_t hits = __reduce_add_sync(0xFFFFFFFFu, res != kNoSlot ? 1u : 0u);
+  if (lane_id() == 0 && hits) atomicAdd(written, (unsigned long long)hits);
 }
 
-UpdateScratch update_scratch_carve(void* base, uint64_t n) {
-  UpdateScratch u;
-  u.cap = pow2_at_least(2 * n);
-  char* p = static_cast<char*>(base);
-  u.ut_key = reinterpret_cast<uint64_t*>(p);
-  p += align_up(u.cap * 8, 256);
-  u.ut_pos = reinterpret_cast<uint32_t*>(p);
-  p += align_up(u.cap * 4, 256);
-  u.found_tab = reinterpret_cast<uint32_t*>(p);
-  p += align_up(n * 4, 256);
-  u.written = reinterpret_cast<unsigned long long*>(p);
-  return u;
-}
-
-template <int P>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_update_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, UpdateScratch us) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * kWarpsPerBlock) + (threadIdx.x >> 5);
-  const uint64_t base = warp * P;
-  if (base >= n) return;
-  WarpKeys<P> wk;
-  warp_load_keys<P>(c, keys, base, n, wk);
-  uint32_t slot[P];
-  warp_probe<P>(c, wk, slot);
+template <int CH>
+__global__ void __launch_bounds__(256)
+    k_update_write(CacheDev c, const float* __restrict__ rows, uint64_t n,
+                   const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner) {
+  constexpr int U = CH == 8 ? 4 : 8;
   const uint32_t lane = lane_id();
-  if (lane >= uint32_t(P)) return;
-  // lane p handles position base + p
-  uint32_t my_slot = kNoSlot;
+  const uint64_t base = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull;
+  const uint64_t pos = base + lane;
+  uint32_t slot = kNoSlot;
+  if (pos < n) {
+    slot = slot_of[pos];
+    if (slot != kNoSlot && __ldcg(winner + slot) != uint32_t(pos + 1)) slot = kNoSlot;  // a later duplicate wins
+  }
+  const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
+  const uint32_t d = c.d;
+  const uint32_t cpr = d / CH;
+  const bool pow2 = (cpr & (cpr - 1)) == 0;
+  const uint32_t sh = __ffs(cpr) - 1;
+  const uint32_t total = nrows * cpr;
+  const float* src = rows + base * d;
+  for (uint32_t c0 = 0; c0 < total; c0 += 32 * U) {
+    Chunk<CH> x[U];
+    uint32_t dst_slot[U];
 #pragma unroll
-  for (int p = 0; p < P; ++p)
-    if (uint32_t(p) == lane) my_slot = slot[p];
-  const uint64_t i = base + lane;
-  if (i >= n) return;
-  if (my_slot == kNoSlot) {
-    us.found_tab[i] = 0xFFFFFFFFu;
-    return;
+    for (int u = 0; u < U; ++u) {
+      const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
+      uint32_t row = pow2 ? (ch >> sh) : (ch / cpr);
+      row = min(row, 31u);
+      dst_slot[u] = __shfl_sync(0xFFFFFFFFu, slot, row);
+      if (ch < total && dst_slot[u] != kNoSlot) x[u].load(src + uint64_t(ch) * CH);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
+      if (ch < total && dst_slot[u] != kNoSlot) {
+        const uint32_t row = pow2 ? (ch >> sh) : (ch / cpr);
+        x[u].store_wb(c.rows + uint64_t(dst_slot[u]) * d + (ch - row * cpr) * CH);
+      }
+    }
   }
-  atomicAdd(us.written, 1ull);
-  const uint64_t g = uint64_t(my_slot);
-  uint64_t t = fmix64(g) & (us.cap - 1);
-  while (true) {
-    const unsigned long long old =
-        atomicCAS(reinterpret_cast<unsigned long long*>(us.ut_key + t), ~0ull, g);
-    if (old == ~0ull || old == g) break;
-    t = (t + 1) & (us.cap - 1);
-  }
-  atomicMax(us.ut_pos + t, uint32_t(i + 1));
-  us.found_tab[i] = uint32_t(t);
-}
-
-__global__ void k_update_write(CacheDev c, const float* __restrict__ rows, uint64_t n,
-                               UpdateScratch us) {
-  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const uint32_t t = us.found_tab[i];
-  if (t == 0xFFFFFFFFu) return;
-  if (us.ut_pos[t] != uint32_t(i + 1)) return;  // a later duplicate wins
-  const uint64_t g = us.ut_key[t];
-  warp_copy_row(rows + i * c.d, c.rows + g * c.d, c.d);
+  if (slot != kNoSlot) winner[slot] = 0u;
 }
 
 void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
-                   int keys_per_warp, const UpdateScratch& us, cudaStream_t st) {
-  cudaMemsetAsync(us.written, 0, 8, st);
-  if (n == 0) return;
-  cudaMemsetAsync(us.ut_key, 0xFF, us.cap * 8, st);
-  cudaMemsetAsync(us.ut_pos, 0, us.cap * 4, st);
-  const int P = keys_per_warp >= 8 ? 8 : (keys_per_warp >= 4 ? 4 : 1);
-  const uint64_t warps = (n + P - 1) / P;
-  const unsigned grid = unsigned((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  switch (P) {
-    case 8: k_update_probe<8><<<grid, kWarpsPerBlock * 32, 0, st>>>(c, keys, n, us); break;
-    case 4: k_update_probe<4><<<grid, kWarpsPerBlock * 32, 0, st>>>(c, keys, n, us); break;
-    default: k_update_probe<1><<<grid, kWarpsPerBlock * 32, 0, st>>>(c, keys, n, us); break;
+                   uint32_t* slot_of, uint32_t* winner, unsigned long long* written,
+                   cudaStream_t st) {
+  cudaMemsetAsync(written, 0, 8, st);
+  if (n == 0) {
+    check_launch("update", 0);
+    return;
   }
-  const uint64_t threads = n * 32;
-  k_update_write<<<unsigned((threads + 255) / 256), 256, 0, st>>>(c, rows, n, us);
+  const unsigned grid = unsigned((n + 255) / 256);
+  k_update_probe<<<grid, 256, 0, st>>>(c, keys, n, slot_of, winner, written);
+  const bool a32 = (reinterpret_cast<uintptr_t>(rows) % 32) == 0;
+  const bool a16 = (reinterpret_cast<uintptr_t>(rows) % 16) == 0;
+  if (c.d % 8 == 0 && a32)
+    k_update_write<8><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner);
+  else if (c.d % 4 == 0 && a16)
+    k_update_write<4><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner);
+  else
+    k_update_write<1><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner);
   check_launch("update", 2);
 }
 

@@ -362,6 +362,17 @@ int hps_cache_update(hps_cache* cache, const uint64_t* keys, size_t n, const flo
   });
 }
 
+int hps_cache_update_device(hps_cache* cache, const uint64_t* keys, size_t n,
+                            const float* vectors, size_t vectors_len, uint64_t* written,
+                            void* stream) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    need(vectors_len == n * uint64_t(cache->impl->dimension()),
+         "update vector buffer has wrong size");
+    cache->impl->update_device(keys, n, vectors, written, as_stream(stream));
+  });
+}
+
 int hps_cache_dump(hps_cache* cache, uint64_t set_begin, uint64_t set_end, uint64_t* out,
                    size_t cap, size_t* n_out) {
   return guarded([&] {

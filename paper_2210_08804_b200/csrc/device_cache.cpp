@@ -61,6 +61,8 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
   lookup_marks_locked();  // allocated up front: lookups may be graph-captured
+  HPSB_CUDA(cudaMalloc(&winner_, slots * 4));  // update: last position per slot
+  HPSB_CUDA(cudaMemsetAsync(winner_, 0, slots * 4, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.keys, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.counters, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.masks, 0, slabs * 4, stream_));
@@ -91,6 +93,7 @@ DeviceCache::~DeviceCache() {
   cudaFree(scan_.status);
   cudaFree(trace_);
   cudaFree(marks_);
+  cudaFree(winner_);
   cudaEventDestroy(ev_in_);
   cudaEventDestroy(ev_out_);
   cudaStreamDestroy(stream_);
@@ -308,13 +311,13 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
   if (vectors_len != n * uint64_t(cfg_.dimension))
     throw invalid_argument("update vector buffer has wrong size");
   if (n == 0) return 0;
+  if (n >= (1ull << 32) - 1) throw invalid_argument("update batch too large");
   DeviceGuard g(device_);
   const uint64_t d = cfg_.dimension;
   const bool host = mem == kHostMem;
-  const uint64_t us_bytes = update_scratch_bytes(n);
-  const uint64_t bytes = align256(us_bytes) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
+  const uint64_t bytes = align256(n * 4) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
   Carver cv{static_cast<char*>(scratch(bytes))};
-  UpdateScratch us = update_scratch_carve(cv.take<char>(us_bytes), n);
+  uint32_t* slot_of = cv.take<uint32_t>(n);
   const uint64_t* d_keys = keys;
   const float* d_rows = vectors;
   if (host) {
@@ -327,11 +330,33 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
   } else {
     join_from(user);
   }
-  launch_update(dev_, d_keys, n, d_rows, keys_per_warp_, us, stream_);
-  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 2, us.written, 8, cudaMemcpyDeviceToHost, stream_));
+  launch_update(dev_, d_keys, n, d_rows, slot_of, winner_, d_small_ + 2, stream_);
+  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 2, d_small_ + 2, 8, cudaMemcpyDeviceToHost, stream_));
   HPSB_CUDA(cudaStreamSynchronize(stream_));
   if (!host) join_to(user);
   return h_small_[2];
+}
+
+void DeviceCache::update_device(const uint64_t* keys, size_t n, const float* vectors,
+                                uint64_t* written, cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
+  if (n >= (1ull << 32) - 1) throw invalid_argument("update batch too large");
+  DeviceGuard g(device_);
+  join_from(user);
+  if (n > ucap_) {
+    uint64_t cap = 1024;
+    while (cap < n) cap <<= 1;
+    ubuf_.ensure(align256(cap * 4) + 256, stream_);
+    ucap_ = cap;
+  }
+  uint32_t* slot_of = static_cast<uint32_t*>(ubuf_.get());
+  unsigned long long* w = written != nullptr
+                              ? reinterpret_cast<unsigned long long*>(written)
+                              : reinterpret_cast<unsigned long long*>(
+                                    static_cast<char*>(ubuf_.get()) + align256(ucap_ * 4));
+  launch_update(dev_, keys, n, vectors, slot_of, winner_, w, stream_);
+  join_to(user);
 }
 
 size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, size_t cap) {

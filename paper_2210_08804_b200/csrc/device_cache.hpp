@@ -46,6 +46,10 @@ class DeviceCache {
   // slab_cache.cpp:109-125
   size_t update(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
                 int mem, cudaStream_t user);
+  // Stream-ordered update on device pointers (online training path): no
+  // host sync; *written (device u64, may be null) gets the count.
+  void update_device(const uint64_t* keys, size_t n, const float* vectors, uint64_t* written,
+                     cudaStream_t user);
   // Lookup-level query on device pointers (the engine's hot path without
   // the tier logic): bumps the clock, writes every position's row (hit:
   // cached row, miss: default_row), miss flags, the unique missing keys with
@@ -124,6 +128,10 @@ class DeviceCache {
   // unique-hit marks of the lookup kernels: kLookupViews arrays of one u64
   // per slot (lazily allocated; see LookupView::marks)
   unsigned long long* marks_ = nullptr;
+  // update: per-slot winning position + 1 (all-zero between calls)
+  uint32_t* winner_ = nullptr;
+  DeviceBuffer ubuf_;  // update_device scratch
+  uint64_t ucap_ = 0;
   // diagnostic lookup timeline ring (HPSB_TRACE=1): kTraceRing calls x 8
   unsigned long long* trace_ = nullptr;
   uint64_t trace_calls_ = 0;

@@ -55,17 +55,12 @@ ReplaceScratch replace_scratch_carve(void* base, uint64_t n);
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st);
 
-struct UpdateScratch {
-  uint64_t cap = 0;
-  uint64_t* ut_key = nullptr;    // cap, EMPTY = ~0
-  uint32_t* ut_pos = nullptr;    // cap, max(position + 1)
-  uint32_t* found_tab = nullptr; // n
-  unsigned long long* written = nullptr;
-};
-size_t update_scratch_bytes(uint64_t n);
-UpdateScratch update_scratch_carve(void* base, uint64_t n);
+// Update (slab_cache.cpp:109-125): slot_of = n u32 of scratch; winner = the
+// cache's per-slot u32 array (all-zero between calls); *written = number of
+// positions whose key is resident (device memory).
 void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
-                   int keys_per_warp, const UpdateScratch& us, cudaStream_t st);
+                   uint32_t* slot_of, uint32_t* winner, unsigned long long* written,
+                   cudaStream_t st);
 
 void launch_dump(const CacheDev& c, uint64_t set_begin, uint64_t set_end, uint64_t* out,
                  unsigned long long* n_out, ScanState& scan, cudaStream_t st);

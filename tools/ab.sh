@@ -5,7 +5,7 @@ tag=$1; shift
 out=gpurun_out/$tag; mkdir -p $out
 i=0
 for cfg in "$@"; do
-  env $cfg timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-sweep --steps 1000 > $out/ab_$i.json 2>> $out/ab.err
+  env $cfg timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-sweep --no-online --steps 1000 > $out/ab_$i.json 2>> $out/ab.err
   python - "$cfg" $out/ab_$i.json <<'PY' >> $out/ab.txt
 import json, sys
 d = json.loads(open(sys.argv[2]).read().splitlines()[0])

@@ -13,7 +13,7 @@ for v in ${AB_VARIANTS:-}; do
   HPSB_LOOKUP_KERNEL=$v timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-sweep > $out/bench_$v.json 2>> $out/bench.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
-  python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > $out/ncu_launch.log 2>&1
+  python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline --no-online > $out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lookup_tag -s 40 -c 2 \
-  -o $out/prof python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > $out/ncu_full.log 2>&1
+  -o $out/prof python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline --no-online > $out/ncu_full.log 2>&1
 ls -la $out
