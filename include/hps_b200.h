@@ -291,6 +291,27 @@ int hps_engine_get_stats(hps_engine* engine, hps_engine_stats* out);
 int hps_engine_pool_info(hps_engine* engine, uint64_t* size, uint64_t* outstanding,
                          uint64_t* peak_outstanding);
 
+/* ---- key-hash-sharded mode (tables larger than one GPU's HBM; SURVEY
+ *      §8e -- no reference counterpart: the reference is single-process and
+ *      the paper deploys one replica per GPU). Rank r of G owns
+ *      the keys with hps_shard_of(key, G) == r; a lookup routes keys to their
+ *      owners (NCCL all-to-all in paper_2210_08804_b200/sharded.py), each
+ *      owner runs hps_cache_lookup_device on its shard, and the rows come
+ *      back the same way. All pointers are device memory on `device`. ---- */
+uint32_t hps_shard_of(uint64_t key, uint32_t world);
+/* counts[world] (u64) = keys per owner */
+int hps_shard_count(int device, const uint64_t* keys, size_t n, uint32_t world, uint64_t* counts,
+                    void* stream);
+/* cursor[world] = each owner's segment start in send_keys / send_pos (advanced
+ * by the call); send_pos[j] = the original position of send_keys[j] */
+int hps_shard_scatter(int device, const uint64_t* keys, size_t n, uint32_t world, uint64_t* cursor,
+                      uint64_t* send_keys, uint32_t* send_pos, void* stream);
+/* out[send_pos[j]] = rows[j] (dim floats), flags_out[send_pos[j]] = flags_in[j]
+ * (flags may be NULL) */
+int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_pos,
+                      const float* rows, const uint8_t* flags_in, float* out, uint8_t* flags_out,
+                      void* stream);
+
 /* ---- workload (harness input; replaces PowerLawSampler::sample,
  *      workload.cpp:24-70, bit-exact) ---- */
 int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,

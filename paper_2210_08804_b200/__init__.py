@@ -145,6 +145,10 @@ SIGNATURES = {
     "hps_cache_export_state": (C.c_int, [_P, _P, _P, _P, _P]),
     "hps_cache_debug_trace": (C.c_int, [_P, _P, C.c_size_t, _U64P]),
     "hps_cache_update_device": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P]),
+    "hps_shard_of": (C.c_uint32, [C.c_uint64, C.c_uint32]),
+    "hps_shard_count": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P]),
+    "hps_shard_scatter": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P, _P, _P]),
+    "hps_shard_unroute": (C.c_int, [C.c_int, C.c_size_t, C.c_uint32, _P, _P, _P, _P, _P, _P]),
     "hps_vdb_create": (C.c_int, [C.c_uint32, C.POINTER(_P)]),
     "hps_vdb_destroy": (C.c_int, [_P]),
     "hps_vdb_register_table": (C.c_int, [_P, C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64]),

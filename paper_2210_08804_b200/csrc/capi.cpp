@@ -405,6 +405,46 @@ int hps_cache_debug_trace(hps_cache* cache, uint64_t* out, size_t cap, uint64_t*
   });
 }
 
+// ---------------------------------------------------------------- sharded --
+uint32_t hps_shard_of(uint64_t key, uint32_t world) {
+  return world == 0 ? 0u : hpsb::shard_of(key, world);
+}
+
+int hps_shard_count(int device, const uint64_t* keys, size_t n, uint32_t world, uint64_t* counts,
+                    void* stream) {
+  return guarded([&] {
+    need(counts != nullptr && (n == 0 || keys != nullptr), "null argument");
+    need(world >= 1 && world <= 64, "world size must be within [1, 64]");
+    hpsb::DeviceGuard g(device);
+    hpsb::launch_shard_count(keys, n, world, reinterpret_cast<unsigned long long*>(counts),
+                             as_stream(stream));
+  });
+}
+
+int hps_shard_scatter(int device, const uint64_t* keys, size_t n, uint32_t world, uint64_t* cursor,
+                      uint64_t* send_keys, uint32_t* send_pos, void* stream) {
+  return guarded([&] {
+    need(cursor != nullptr && (n == 0 || (keys && send_keys && send_pos)), "null argument");
+    need(world >= 1 && world <= 64, "world size must be within [1, 64]");
+    need(n < (1ull << 32), "batch too large");
+    hpsb::DeviceGuard g(device);
+    hpsb::launch_shard_scatter(keys, n, world, reinterpret_cast<unsigned long long*>(cursor),
+                               send_keys, send_pos, as_stream(stream));
+  });
+}
+
+int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_pos,
+                      const float* rows, const uint8_t* flags_in, float* out, uint8_t* flags_out,
+                      void* stream) {
+  return guarded([&] {
+    need(m == 0 || (send_pos && rows && out), "null argument");
+    need(dim > 0, "dimension must be positive");
+    need((flags_in == nullptr) == (flags_out == nullptr), "flags in / out must both be given");
+    hpsb::DeviceGuard g(device);
+    hpsb::launch_shard_unroute(m, dim, send_pos, rows, flags_in, out, flags_out, as_stream(stream));
+  });
+}
+
 // -------------------------------------------------------------------- vdb --
 int hps_vdb_create(uint32_t lookup_threads, hps_vdb** out) {
   return guarded([&] {

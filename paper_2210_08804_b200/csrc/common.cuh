@@ -17,6 +17,7 @@ constexpr uint32_t kSlotsPerSlab = 32;  // slab_cache.hpp:25
 constexpr uint64_t kSlabsetSeed = 0x5EED5E7ull;  // xxhash64.hpp:127
 constexpr uint64_t kSlabSeed = 0x51ABull;        // xxhash64.hpp:128
 constexpr uint64_t kPartitionSeed = 0ull;        // xxhash64.hpp:129
+constexpr uint64_t kShardSeed = 0x5A4D5EEDull;   // sharded mode owner hash (ours)
 constexpr uint32_t kFullSlab = 0xFFFFFFFFu;
 
 constexpr uint64_t kP1 = 0x9E3779B185EBCA87ull;

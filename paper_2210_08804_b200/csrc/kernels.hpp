@@ -139,4 +139,15 @@ void launch_lookup_scatter(uint64_t n, uint32_t d, uint8_t* flags, const LookupV
                            const int32_t* row_of_claim, const float* staged, float* out,
                            cudaStream_t st);
 
+// ---- key-hash-sharded mode (shard_kernels.cu) ----
+uint32_t shard_of(uint64_t key, uint32_t world);
+void launch_shard_count(const uint64_t* keys, uint64_t n, uint32_t world,
+                        unsigned long long* counts, cudaStream_t st);
+void launch_shard_scatter(const uint64_t* keys, uint64_t n, uint32_t world,
+                          unsigned long long* cursor, uint64_t* send_keys, uint32_t* send_pos,
+                          cudaStream_t st);
+void launch_shard_unroute(uint64_t m, uint32_t d, const uint32_t* send_pos, const float* rows,
+                          const uint8_t* flags_in, float* out, uint8_t* flags_out,
+                          cudaStream_t st);
+
 }  // namespace hpsb

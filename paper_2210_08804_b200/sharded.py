@@ -1,0 +1,148 @@
+"""Key-hash-sharded lookup over torch.distributed.
+
+For tables larger than one GPU's HBM: rank r of G holds the shard of keys
+with ``shard_of(key, G) == r`` (``hps_shard_of``; its own seed, not the
+slabset seed) in its own :class:`SlabCache`. A lookup is collective -- every
+rank calls it with its own batch:
+
+1. route: per-owner counts and the keys scattered into per-owner segments
+   (CUDA kernels ``hps_shard_count`` / ``hps_shard_scatter``; original
+   positions ride along);
+2. exchange: the counts, then the keys (all-to-all; NCCL over NVLink on the
+   GPU box, gloo in the CPU tests);
+3. each owner runs ONE lookup of everything it received
+   (``hps_cache_lookup_device``: probe, recency, rows, default rows for
+   misses, its unique misses -- the owner fills its own shard);
+4. exchange back: rows and miss flags (reverse all-to-all);
+5. unroute: rows to the requester's original positions
+   (``hps_shard_unroute``).
+
+The only collectives are these exchanges; the replica mode (one full cache
+per GPU, ``bench.py --gpus N``) has none. There is no reference counterpart:
+the reference is single-process and the paper deploys replicas
+(PAPER.md:809).
+
+The device ops and the local lookup are injectable (``ops``,
+``local_lookup``) so the orchestration runs under gloo on CPU in the tests.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import HPS_MEM_DEVICE, _check, lib  # noqa: F401  (re-exported helpers)
+
+
+def shard_of(keys, world: int) -> np.ndarray:
+    """Owner rank of each key (host; same function as the device kernels)."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    f = lib().hps_shard_of
+    return np.fromiter((f(int(x), world) for x in k), dtype=np.int64, count=len(k))
+
+
+class ShardOps:
+    """Routing kernels of one rank (device pointers, torch CUDA tensors)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+
+    def _stream(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def count(self, keys, world: int):
+        import torch
+
+        counts = torch.empty(world, dtype=torch.int64, device=keys.device)
+        _check(lib().hps_shard_count(self.device, keys.data_ptr(), keys.numel(), world,
+                                     counts.data_ptr(), self._stream()))
+        return counts
+
+    def scatter(self, keys, world: int, offsets):
+        import torch
+
+        send_keys = torch.empty_like(keys)
+        send_pos = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
+        cursor = offsets.clone()
+        _check(lib().hps_shard_scatter(self.device, keys.data_ptr(), keys.numel(), world,
+                                       cursor.data_ptr(), send_keys.data_ptr(),
+                                       send_pos.data_ptr(), self._stream()))
+        return send_keys, send_pos
+
+    def unroute(self, send_pos, rows, flags_in, out, flags_out, dim: int):
+        _check(lib().hps_shard_unroute(self.device, send_pos.numel(), dim, send_pos.data_ptr(),
+                                       rows.data_ptr(), flags_in.data_ptr(), out.data_ptr(),
+                                       flags_out.data_ptr(), self._stream()))
+
+
+def cache_local_lookup(cache, device: int = 0) -> Callable:
+    """The owner-side lookup on a local shard: one hps_cache_lookup_device on
+    the received keys. Returns (rows, flags, miss_keys, miss_firsts, counts)."""
+
+    def run(keys, default_row):
+        import torch
+
+        n = keys.numel()
+        d = cache.dimension()
+        rows = torch.empty(max(n, 1) * d, device=keys.device)
+        flags = torch.empty(max(n, 1), dtype=torch.uint8, device=keys.device)
+        mk = torch.empty(max(n, 1), dtype=torch.int64, device=keys.device)
+        mf = torch.empty(max(n, 1), dtype=torch.int32, device=keys.device)
+        cnt = torch.zeros(2, dtype=torch.int64, device=keys.device)
+        st = torch.cuda.current_stream(device).cuda_stream
+        cache.lookup_device(keys.data_ptr(), n, rows.data_ptr(), flags.data_ptr(),
+                            default_row.data_ptr(), mk.data_ptr(), mf.data_ptr(), cnt.data_ptr(),
+                            st)
+        return rows[: n * d], flags[:n], mk, mf, cnt
+
+    return run
+
+
+class ShardedLookup:
+    """Collective lookup over a key-hash-sharded cache (see module doc)."""
+
+    def __init__(self, dim: int, local_lookup: Callable, group=None, ops=None, device: int = 0):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.dim = dim
+        self.local_lookup = local_lookup
+        self.ops = ops if ops is not None else ShardOps(device)
+
+    def lookup(self, keys, default_row):
+        """keys: int64 tensor of this rank's batch. Returns (rows [n*dim],
+        miss flags [n], owner_side) where owner_side = (miss_keys,
+        miss_firsts, counts) of THIS rank's shard lookup (its unique misses,
+        to be fetched from the tiers and replaced by this rank)."""
+        import torch
+
+        dist, G, d = self.dist, self.world, self.dim
+        n = keys.numel()
+        counts = self.ops.count(keys, G)
+        offsets = torch.zeros_like(counts)
+        if G > 1:
+            offsets[1:] = torch.cumsum(counts, 0)[:-1]
+        send_keys, send_pos = self.ops.scatter(keys, G, offsets)
+        send_splits = counts.cpu().tolist()
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        recv_splits = recv_counts.cpu().tolist()
+        recv_keys = torch.empty(sum(recv_splits), dtype=keys.dtype, device=keys.device)
+        dist.all_to_all_single(recv_keys, send_keys, recv_splits, send_splits, group=self.group)
+        rows, flags, mk, mf, cnt = self.local_lookup(recv_keys, default_row)
+        back_rows = torch.empty(n * d, dtype=rows.dtype, device=keys.device)
+        dist.all_to_all_single(back_rows.view(-1, d) if n else back_rows,
+                               rows.view(-1, d) if rows.numel() else rows,
+                               send_splits, recv_splits, group=self.group)
+        back_flags = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        dist.all_to_all_single(back_flags, flags.contiguous(), send_splits, recv_splits,
+                               group=self.group)
+        out = torch.empty(n * d, dtype=rows.dtype, device=keys.device)
+        flags_out = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        self.ops.unroute(send_pos, back_rows, back_flags, out, flags_out, d)
+        return out, flags_out, (mk, mf, cnt)

@@ -1,0 +1,200 @@
+"""Key-hash-sharded mode and the multi-rank path.
+
+* CPU, gloo, world size 2 (and 3): the collective orchestration of
+  paper_2210_08804_b200/sharded.py with CPU stand-ins for the routing kernels
+  and an oracle-backed shard lookup per rank -- every rank's rows and miss
+  flags must equal what the owner shards hold, whatever the routing order.
+* GPU: the routing kernels (count / scatter / unroute) against numpy, and a
+  world-size-1 NCCL run of the whole path against the oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2210_08804_b200 as hps
+from paper_2210_08804_b200 import sharded
+
+D = 8
+KEYSPACE = 4000
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def key_rows(keys):
+    k = np.asarray(keys, dtype=np.float64)
+    return (k[:, None] * 0.5 + np.arange(D)[None, :]).astype(np.float32).reshape(-1)
+
+
+class CpuOps:
+    """CPU stand-ins for ShardOps (same contract; owners from the product's
+    host hash hps_shard_of)."""
+
+    def count(self, keys, world):
+        own = sharded.shard_of(keys.numpy().view(np.uint64), world)
+        return torch.from_numpy(np.bincount(own, minlength=world).astype(np.int64))
+
+    def scatter(self, keys, world, offsets):
+        k = keys.numpy().view(np.uint64)
+        own = sharded.shard_of(k, world)
+        # deliberately NOT input order inside a segment: the carried
+        # positions must undo any order
+        order = np.lexsort((-np.arange(len(k)), own))
+        return (torch.from_numpy(k[order].view(np.int64).copy()),
+                torch.from_numpy(order.astype(np.int32)))
+
+    def unroute(self, send_pos, rows, flags_in, out, flags_out, dim):
+        p = send_pos.numpy().astype(np.int64)
+        out.view(-1, dim)[torch.from_numpy(p)] = rows.view(-1, dim)
+        flags_out[torch.from_numpy(p)] = flags_in
+
+
+def oracle_shard_lookup(shard: "oracle.OracleCache", default):
+    def run(keys, default_row):
+        k = keys.numpy().view(np.uint64)
+        uniq, inv = oracle.dedup(k)
+        ws = np.zeros(len(uniq) * D, np.float32)
+        hit = shard.query(uniq, ws)
+        ws = ws.reshape(-1, D)
+        ws[hit == 0] = default
+        rows = torch.from_numpy(ws[inv].reshape(-1).copy())
+        flags = torch.from_numpy((1 - hit)[inv].astype(np.uint8))
+        miss = uniq[hit == 0]
+        cnt = torch.tensor([int(hit.sum()), len(miss)], dtype=torch.int64)
+        return rows, flags, torch.from_numpy(miss.view(np.int64).copy()), None, cnt
+    return run
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(7)
+        table = rng.choice(KEYSPACE, 1500, replace=False).astype(np.uint64)
+        own = sharded.shard_of(table, world)
+        mine = table[own == rank]
+        shard = oracle.OracleCache(64, 2, D)
+        shard.replace(mine, key_rows(mine))
+        default = np.full(D, -1.0, np.float32)
+        sl = sharded.ShardedLookup(D, oracle_shard_lookup(shard, default), ops=CpuOps())
+        resident = set(int(k) for k in table)  # every key lives on exactly one owner
+        ok = True
+        for b in range(3):
+            brng = np.random.default_rng(100 * rank + b)
+            batch = brng.integers(0, KEYSPACE, 700 + 97 * rank, dtype=np.uint64)
+            batch[:5] = batch[5:10]  # duplicates within the batch
+            out, flags, (mk, _, cnt) = sl.lookup(torch.from_numpy(batch.view(np.int64)),
+                                                 torch.from_numpy(default))
+            # each owner's shard must hold the keys it owns (capacity is
+            # 4096 slots, no eviction at 1500 keys)
+            in_cache = np.array([int(k) in resident for k in batch])
+            want = key_rows(batch).reshape(-1, D)
+            want[~in_cache] = default
+            ok &= out.numpy().reshape(-1, D).tobytes() == want.tobytes()
+            ok &= (flags.numpy() == (~in_cache).astype(np.uint8)).all()
+            # owner-side unique misses are keys this rank owns
+            ok &= bool((sharded.shard_of(mk.numpy().view(np.uint64), world) == rank).all())
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_lookup_orchestration_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get() for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res
+
+
+def test_shard_hash_is_balanced_and_independent_of_placement():
+    """Owners spread evenly, and the owner hash is not the slabset hash: a
+    shard's keys still fill all of its slabsets."""
+    keys = np.arange(200000, dtype=np.uint64) * 2654435761 % (1 << 40)
+    for world in (2, 4, 8):
+        own = sharded.shard_of(keys, world)
+        frac = np.bincount(own, minlength=world) / len(keys)
+        assert np.all(np.abs(frac - 1 / world) < 0.01)
+    own = sharded.shard_of(keys, 8)
+    sets = np.array([oracle.slabset_of(int(k), 64) for k in keys[own == 3][:20000]])
+    assert len(np.unique(sets)) == 64
+
+
+@pytest.mark.gpu
+def test_routing_kernels_match_numpy():
+    ops = sharded.ShardOps(0)
+    rng = np.random.default_rng(3)
+    for n, world in [(1, 4), (1000, 2), (65536, 8), (4097, 5)]:
+        k = rng.integers(0, 2**63, n, dtype=np.uint64)
+        kt = torch.from_numpy(k.view(np.int64)).cuda()
+        counts = ops.count(kt, world)
+        own = sharded.shard_of(k, world)
+        assert (counts.cpu().numpy() == np.bincount(own, minlength=world)).all()
+        offsets = torch.zeros_like(counts)
+        offsets[1:] = torch.cumsum(counts, 0)[:-1]
+        sk, sp = ops.scatter(kt, world, offsets)
+        sk, sp = sk.cpu().numpy().view(np.uint64), sp.cpu().numpy()
+        assert (sk == k[sp]).all() and (np.sort(sp) == np.arange(n)).all()
+        off = offsets.cpu().numpy()
+        for o in range(world):
+            seg = sk[off[o]: off[o] + counts[o].item()]
+            assert (sharded.shard_of(seg, world) == o).all()
+        rows = torch.from_numpy(key_rows(sk)).cuda()
+        fl_in = torch.from_numpy((sk % 2).astype(np.uint8)).cuda()
+        out = torch.empty(n * D, device="cuda")
+        fl = torch.empty(n, dtype=torch.uint8, device="cuda")
+        ops.unroute(torch.from_numpy(sp).cuda(), rows, fl_in, out, fl, D)
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == key_rows(k).tobytes()
+        assert (fl.cpu().numpy() == (k % 2)).all()
+
+
+@pytest.mark.gpu
+def test_sharded_lookup_world_one_nccl_matches_oracle():
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        S, W = 64, 2
+        cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=W, dimension=D))
+        o = oracle.OracleCache(S, W, D)
+        rng = np.random.default_rng(5)
+        keys = rng.choice(KEYSPACE, 1500, replace=False).astype(np.uint64)
+        cache.replace(keys, key_rows(keys))
+        o.replace(keys, key_rows(keys))
+        default = np.full(D, 3.0, np.float32)
+        sl = sharded.ShardedLookup(D, sharded.cache_local_lookup(cache))
+        for b in range(3):
+            q = rng.integers(0, KEYSPACE, 3000, dtype=np.uint64)
+            out, fl, (mk, mf, cnt) = sl.lookup(torch.from_numpy(q.view(np.int64)).cuda(),
+                                               torch.from_numpy(default).cuda())
+            torch.cuda.synchronize()
+            uniq, inv = oracle.dedup(q)
+            ws = np.zeros(len(uniq) * D, np.float32)
+            hit = o.query(uniq, ws)
+            ws = ws.reshape(-1, D)
+            ws[hit == 0] = default
+            assert out.cpu().numpy().tobytes() == ws[inv].reshape(-1).tobytes()
+            assert (fl.cpu().numpy() == (1 - hit)[inv]).all()
+            um = int((hit == 0).sum())
+            assert cnt.cpu().tolist() == [len(uniq) - um, um]
+    finally:
+        dist.destroy_process_group()
