@@ -261,6 +261,10 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
   ws->ensure(std::max<size_t>(n, 1), d, st);
 
   uint64_t uh = 0, um = 0;
+  uint64_t spec_claims = 0;
+  const bool spec_rows = host && last_async_.load(std::memory_order_relaxed);
+  const bool out_pinned = host && n > 0 && is_pinned(out);
+  const bool flags_pinned = host && n > 0 && is_pinned(flags);
   const uint64_t* d_keys = keys;
   float* d_out = out;
   uint8_t* d_flags = flags;
@@ -287,6 +291,20 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
       launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->lv,
                           /*after_lookup=*/false, st);
       HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->lv.counts_out, 16, cudaMemcpyDeviceToHost, st));
+      // One host round trip on the common path: the first claims and -- when
+      // the previous call took the async branch, whose rows are final as the
+      // kernel leaves them -- the rows and flags come back with the counts.
+      spec_claims = std::min<uint64_t>(n, kSpeculativeClaims);
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, spec_claims * 8,
+                                cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, spec_claims * 4,
+                                cudaMemcpyDeviceToHost, st));
+      if (host && spec_rows) {
+        HPSB_CUDA(cudaMemcpyAsync(out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
+                                  cudaMemcpyDeviceToHost, st));
+        HPSB_CUDA(cudaMemcpyAsync(flags_pinned ? flags : ws->h_flags, d_flags, n,
+                                  cudaMemcpyDeviceToHost, st));
+      }
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }
   }
@@ -294,13 +312,16 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
     HPSB_CUDA(cudaEventSynchronize(ws->done));
     uh = ws->h_counts[0];
     um = ws->h_counts[1];
-    if (um > 0) {
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, um * 8,
-                                cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, um * 4,
+    if (um > spec_claims) {
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys + spec_claims, ws->lv.list_keys + spec_claims,
+                                (um - spec_claims) * 8, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts + spec_claims,
+                                ws->lv.list_firsts + spec_claims, (um - spec_claims) * 4,
                                 cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
       HPSB_CUDA(cudaEventSynchronize(ws->done));
+    }
+    if (um > 0) {
       // the reference's miss order: unique misses by first occurrence
       // (types.cpp:20-34 + slab_cache.cpp:84-89)
       ws->order.resize(um);
@@ -341,17 +362,20 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
     defaults = um;
   }
 
+  last_async_.store(!sync_branch, std::memory_order_relaxed);
   if (n > 0) {
     if (host) {
-      const bool po = is_pinned(out), pf = is_pinned(flags);
-      HPSB_CUDA(cudaMemcpyAsync(po ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
-                                cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaMemcpyAsync(pf ? flags : ws->h_flags, d_flags, n, cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaEventRecord(ws->done, st));
-      HPSB_CUDA(cudaEventSynchronize(ws->done));
+      if (sync_branch || !spec_rows) {
+        HPSB_CUDA(cudaMemcpyAsync(out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
+                                  cudaMemcpyDeviceToHost, st));
+        HPSB_CUDA(cudaMemcpyAsync(flags_pinned ? flags : ws->h_flags, d_flags, n,
+                                  cudaMemcpyDeviceToHost, st));
+        HPSB_CUDA(cudaEventRecord(ws->done, st));
+        HPSB_CUDA(cudaEventSynchronize(ws->done));
+      }
       ws->pending = false;
-      if (!po) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
-      if (!pf) std::memcpy(flags, ws->h_flags, n);
+      if (!out_pinned) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
+      if (!flags_pinned) std::memcpy(flags, ws->h_flags, n);
     } else {
       cache_->join_to(user);
     }

@@ -138,6 +138,13 @@ class LookupEngine {
   WorkspacePool& pool() { return pool_; }
 
  private:
+  // claims copied back speculatively with the counts (one round trip when a
+  // call has at most this many unique misses)
+  static constexpr uint64_t kSpeculativeClaims = 4096;
+  // the previous lookup took the async branch: speculate that this one will
+  // too and bring its rows back with the counts
+  std::atomic<bool> last_async_{false};
+
   struct AsyncTask {
     Workspace* ws;
   };

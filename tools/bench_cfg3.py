@@ -1,0 +1,150 @@
+#!/usr/bin/env python
+"""cfg 3 (BASELINE.json configs[2]): Criteo-shaped 26 sparse tables, ~100M
+keys in total, dim 128, batch sizes 1 .. 131072; Query + host VDB miss fetch;
+END-TO-END lookup latency through the reference-facing engine call
+(hps_engine_lookup = LookupEngine::lookup, pinned host keys / rows / flags,
+H2D + D2H inside every timed call).
+
+  python tools/bench_cfg3.py [--keys-per-table 3850000] [--tables 26] > out.json
+
+Each table: power-law (alpha 1.2) key stream over its own keyspace, a GPU
+cache of --cache-frac of the table (the paper's Criteo runs use 0.5), the
+whole table in the host volatile DB (the miss path), threshold 0.8. Rows are
+synthetic (a hash of key and column). Per batch size: p50 / p99 latency of
+one table lookup (one table at a time), and of a 26-table sample batch with
+the tables looked up concurrently from a thread pool (one engine per table),
+plus samples/s. Warm-up fills the caches to steady state first.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    import bench
+    import paper_2210_08804_b200 as hps
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tables", type=int, default=26)
+    ap.add_argument("--keys-per-table", type=int, default=3_850_000)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--cache-frac", type=float, default=0.5)
+    ap.add_argument("--batches", default="1,16,256,1024,4096,16384,65536,131072")
+    ap.add_argument("--calls", type=int, default=60)
+    a = ap.parse_args()
+    d, T, K = a.dim, a.tables, a.keys_per_table
+    sizes = [int(x) for x in a.batches.split(",")]
+    t_setup = time.perf_counter()
+    vdb = hps.VolatileStore(os.cpu_count() or 8)
+    caches, engines, samplers = [], [], []
+    S = int(-(-int(K * a.cache_frac) // 64))
+    for t in range(T):
+        name = f"t{t:02d}"
+        table = hps.TableId(name, d)
+        vdb.register_table(table, hps.VolatileTableConfig(partition_count=16,
+                                                          overflow_margin=1 << 40))
+        base = np.uint64(t) << np.uint64(40)  # disjoint keyspaces
+        for i in range(0, K, 1 << 20):
+            k = base + np.arange(i, min(K, i + (1 << 20)), dtype=np.uint64)
+            vdb.insert(name, k, bench.table_rows(k, d))
+        c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d,
+                                              worker_pool_size=8, tasks_per_worker=8), device=0)
+        e = hps.LookupEngine(table, c, vdb, None,
+                             hps.EngineConfig(hit_rate_threshold=0.8, workspace_pool_size=4,
+                                              async_worker_count=2, max_batch=max(sizes)))
+        caches.append(c)
+        engines.append(e)
+        rng = np.random.default_rng(1000 + t)
+        perm = rng.permutation(K).astype(np.uint64) + base
+        w = np.arange(1, K + 1, dtype=np.float64) ** -1.2
+        cdf = np.cumsum(w)
+        cdf /= cdf[-1]
+        samplers.append((perm, cdf, rng))
+    setup_s = time.perf_counter() - t_setup
+
+    def draw(t, n):
+        perm, cdf, rng = samplers[t]
+        return np.ascontiguousarray(perm[np.minimum(np.searchsorted(cdf, rng.random(n)), K - 1)])
+
+    maxb = max(sizes)
+    pk = [torch.empty(maxb, dtype=torch.int64).pin_memory() for _ in range(T)]
+    po = [torch.empty(maxb * d).pin_memory() for _ in range(T)]
+    pf = [torch.empty(maxb, dtype=torch.uint8).pin_memory() for _ in range(T)]
+
+    def call(t, n, keys):
+        pk[t][:n].copy_(torch.from_numpy(keys.view(np.int64)))
+        t0 = time.perf_counter()
+        o = engines[t].lookup_ptrs(pk[t].data_ptr(), n, po[t].data_ptr(), pf[t].data_ptr(),
+                                   hps.HPS_MEM_HOST)
+        return time.perf_counter() - t0, o.unique_hit_rate
+
+    # warm-up to steady state: every table sees ~2x its cache capacity of draws
+    for t in range(T):
+        for _ in range(max(2, (4 * S * 64) // 65536)):
+            call(t, 65536, draw(t, 65536))
+        engines[t].drain_async()
+    result = {"config": {"workload": "cfg3: Criteo-shaped tables, power-law alpha 1.2, host VDB "
+                                     "holds every table, threshold 0.8",
+                         "tables": T, "keys_per_table": K, "total_keys": T * K, "dim": d,
+                         "cache_frac": a.cache_frac, "slabsets_per_table": S,
+                         "vdb_bytes": T * K * (d * 4 + 8)},
+              "setup_s": setup_s, "per_batch": []}
+    pool = ThreadPoolExecutor(max_workers=min(T, os.cpu_count() or 8))
+    for n in sizes:
+        calls = max(8, min(a.calls, (64 * 65536) // max(n, 1)))
+        batches = [[draw(t, n) for t in range(T)] for _ in range(max(2, calls // T + 1))]
+        for t in range(T):  # size the workspaces for this batch size (untimed)
+            for _ in range(2):
+                call(t, n, draw(t, n))
+            engines[t].drain_async()
+        lat, hits = [], []
+        for i in range(calls):  # one table at a time
+            t = i % T
+            dt, h = call(t, n, batches[i // T % len(batches)][t])
+            lat.append(dt)
+            hits.append(h)
+        sample_lat = []
+        reps = max(3, min(20, calls // 4))
+        for r in range(reps):  # a 26-table sample batch, tables concurrently
+            bs = batches[r % len(batches)]
+            t0 = time.perf_counter()
+            list(pool.map(lambda t: call(t, n, bs[t]), range(T)))
+            sample_lat.append(time.perf_counter() - t0)
+        for e in engines:
+            e.drain_async()
+        lat = np.array(lat) * 1e6
+        sl = np.array(sample_lat) * 1e6
+        result["per_batch"].append({
+            "batch": n, "table_lookup_p50_us": float(np.median(lat)),
+            "table_lookup_p99_us": float(np.percentile(lat, 99)),
+            "table_lookup_keys_per_s": n / (np.median(lat) * 1e-6),
+            "sample_batch_26_tables_p50_us": float(np.median(sl)),
+            "samples_per_s": n / (np.median(sl) * 1e-6),
+            "mean_unique_hit_rate": float(np.mean(hits))})
+        print(json.dumps(result["per_batch"][-1]), file=sys.stderr)
+    stats = [e.stats() for e in engines]
+    result["engine_totals"] = {
+        "sync_batches": int(sum(s.sync_batches for s in stats)),
+        "async_batches": int(sum(s.async_batches for s in stats)),
+        "vdb_hits": int(sum(s.vdb_hits for s in stats)),
+        "defaults_returned": int(sum(s.defaults_returned for s in stats))}
+    print(json.dumps(result))
+    for e in engines:
+        e.close()
+
+
+if __name__ == "__main__":
+    main()
