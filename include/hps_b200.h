@@ -283,6 +283,15 @@ int hps_engine_lookup(hps_engine* engine, const uint64_t* keys, size_t n, float*
                       size_t out_len, uint8_t* miss_flags, hps_lookup_outcome* outcome,
                       int mem, void* stream);
 
+/* Several tables in one call (the reference's caller -- e.g. Node::lookup
+ * per table, server.cpp:198-202 -- loops over tables): engines[t] looks up
+ * keys[t][0..n[t]) into out[t] / miss_flags[t] with exactly the semantics of
+ * hps_engine_lookup; all tables' device work is enqueued before the first
+ * host wait, so the lookups overlap on the GPU. outcomes may be NULL. */
+int hps_engine_lookup_multi(hps_engine* const* engines, size_t count,
+                            const uint64_t* const* keys, const size_t* n, float* const* out,
+                            uint8_t* const* miss_flags, hps_lookup_outcome* outcomes, int mem);
+
 /* replaces drain_async (lookup_engine.cpp:286-289) */
 int hps_engine_drain_async(hps_engine* engine);
 /* replaces stats (lookup_engine.cpp:291-294) */

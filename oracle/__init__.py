@@ -32,6 +32,8 @@ REF_SO = HERE / "_ref" / "libhps_ref.so"
 REF_CACHE_TEST = HERE / "_ref" / "test_slab_cache_b200"
 # tests/unit/test_lookup_engine.cpp built against include/hps/lookup_engine.hpp
 REF_ENGINE_TEST = HERE / "_ref" / "test_lookup_engine_b200"
+# tests/unit/test_refresh_engine.cpp + the reference's refresh_engine.cpp over the B200 cache
+REF_REFRESH_TEST = HERE / "_ref" / "test_refresh_engine_b200"
 REF_SRC = Path("/root/reference/proj")
 
 _P = C.c_void_p

@@ -146,6 +146,7 @@ SIGNATURES = {
     "hps_cache_debug_trace": (C.c_int, [_P, _P, C.c_size_t, _U64P]),
     "hps_cache_update_device": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P]),
     "hps_shard_of": (C.c_uint32, [C.c_uint64, C.c_uint32]),
+    "hps_engine_lookup_multi": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, _P, C.c_int]),
     "hps_shard_count": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P]),
     "hps_shard_scatter": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P, _P, _P]),
     "hps_shard_unroute": (C.c_int, [C.c_int, C.c_size_t, C.c_uint32, _P, _P, _P, _P, _P, _P]),
@@ -829,6 +830,19 @@ class LookupEngine:
                                        flags_ptr, C.byref(o), mem, stream or None))
         return LookupOutcome(bool(o.sync_branch), float(o.unique_hit_rate), int(o.unique_count),
                              int(o.defaults_returned))
+
+    @staticmethod
+    def lookup_multi_ptrs(engines, keys_ptrs, ns, out_ptrs, flags_ptrs, mem: int):
+        """hps_engine_lookup_multi over pointers (one entry per engine/table);
+        returns the per-table LookupOutcome list."""
+        t = len(engines)
+        PA = C.c_void_p * t
+        outs = (_Outcome * t)()
+        _check(lib().hps_engine_lookup_multi(
+            PA(*[e._h for e in engines]), t, PA(*keys_ptrs), (C.c_size_t * t)(*ns),
+            PA(*out_ptrs), PA(*flags_ptrs), outs, mem))
+        return [LookupOutcome(bool(o.sync_branch), float(o.unique_hit_rate), int(o.unique_count),
+                              int(o.defaults_returned)) for o in outs]
 
     def drain_async(self) -> None:
         _check(lib().hps_engine_drain_async(self._h))

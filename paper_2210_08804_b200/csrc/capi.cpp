@@ -582,6 +582,28 @@ int hps_engine_lookup(hps_engine* engine, const uint64_t* keys, size_t n, float*
     }
   });
 }
+int hps_engine_lookup_multi(hps_engine* const* engines, size_t count,
+                            const uint64_t* const* keys, const size_t* n, float* const* out,
+                            uint8_t* const* miss_flags, hps_lookup_outcome* outcomes, int mem) {
+  return guarded([&] {
+    need(count == 0 || (engines && keys && n && out && miss_flags), "null argument");
+    std::vector<hpsb::LookupEngine*> impls(count);
+    for (size_t t = 0; t < count; ++t) {
+      need(engines[t] != nullptr, "null engine");
+      impls[t] = engines[t]->impl.get();
+    }
+    std::vector<hpsb::LookupOutcome> o(count);
+    hpsb::LookupEngine::lookup_multi(impls.data(), count, keys, n, out, miss_flags, o.data(), mem);
+    if (outcomes) {
+      for (size_t t = 0; t < count; ++t) {
+        outcomes[t].sync_branch = o[t].sync_branch ? 1 : 0;
+        outcomes[t].unique_hit_rate = o[t].unique_hit_rate;
+        outcomes[t].unique_count = o[t].unique_count;
+        outcomes[t].defaults_returned = o[t].defaults_returned;
+      }
+    }
+  });
+}
 int hps_engine_drain_async(hps_engine* engine) {
   return guarded([&] { engine->impl->drain_async(); });
 }

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <exception>
 #include <unordered_map>
 
 namespace hpsb {
@@ -242,33 +243,70 @@ size_t LookupEngine::fetch_and_upload(Workspace& ws, const uint64_t* miss_keys, 
 
 void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out_len,
                           uint8_t* flags, LookupOutcome* outcome, int mem, cudaStream_t user) {
+  LookupCall call = begin(keys, n, out, out_len, flags, mem, user);
+  finish(call, outcome);
+}
+
+void LookupEngine::lookup_multi(LookupEngine* const* engines, size_t count,
+                                const uint64_t* const* keys, const size_t* n, float* const* out,
+                                uint8_t* const* flags, LookupOutcome* outcomes, int mem) {
+  // every table's keys, kernel and first copies are in flight before any
+  // host waits: the tables' lookups overlap on the device
+  std::vector<LookupCall> calls;
+  calls.reserve(count);
+  try {
+    for (size_t t = 0; t < count; ++t)
+      calls.push_back(engines[t]->begin(keys[t], n[t], out[t], n[t] * engines[t]->dim_, flags[t],
+                                        mem, nullptr));
+  } catch (...) {
+    for (auto& c : calls) c.engine->abandon(c);
+    throw;
+  }
+  std::exception_ptr first_error;
+  for (size_t t = 0; t < count; ++t) {
+    try {
+      calls[t].engine->finish(calls[t], outcomes ? outcomes + t : nullptr);
+    } catch (...) {
+      if (!first_error) first_error = std::current_exception();
+    }
+  }
+  if (first_error) std::rethrow_exception(first_error);
+}
+
+void LookupEngine::abandon(LookupCall& c) {
+  if (c.ws == nullptr) return;
+  if (c.n > 0) cudaEventSynchronize(c.ws->done);
+  pool_.release(c.ws);
+  c.ws = nullptr;
+}
+
+LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, float* out,
+                                             size_t out_len, uint8_t* flags, int mem,
+                                             cudaStream_t user) {
   if (out_len != n * uint64_t(dim_)) throw invalid_argument("lookup output buffer has wrong size");
-  const bool host = mem == kHostMem;
+  LookupCall c;
+  c.engine = this;
+  c.n = n;
+  c.out = out;
+  c.flags = flags;
+  c.mem = mem;
+  c.user = user;
+  c.host = mem == kHostMem;
+  const bool host = c.host;
   const uint32_t d = dim_;
   Workspace* ws = pool_.acquire();
-  bool handed_off = false;
-  struct LeaseGuard {
-    WorkspacePool& pool;
-    Workspace* ws;
-    bool* handed;
-    ~LeaseGuard() {
-      if (!*handed) pool.release(ws);
-    }
-  } guard{pool_, ws, &handed_off};
-  ws->wait_idle();
-  DeviceGuard g(cache_->device());
-  cudaStream_t st = cache_->stream();
-  ws->ensure(std::max<size_t>(n, 1), d, st);
-
-  uint64_t uh = 0, um = 0;
-  uint64_t spec_claims = 0;
-  const bool spec_rows = host && last_async_.load(std::memory_order_relaxed);
-  const bool out_pinned = host && n > 0 && is_pinned(out);
-  const bool flags_pinned = host && n > 0 && is_pinned(flags);
-  const uint64_t* d_keys = keys;
-  float* d_out = out;
-  uint8_t* d_flags = flags;
-  {
+  c.ws = ws;
+  try {
+    ws->wait_idle();
+    DeviceGuard g(cache_->device());
+    cudaStream_t st = cache_->stream();
+    ws->ensure(std::max<size_t>(n, 1), d, st);
+    c.spec_rows = host && last_async_.load(std::memory_order_relaxed);
+    c.out_pinned = host && n > 0 && is_pinned(out);
+    c.flags_pinned = host && n > 0 && is_pinned(flags);
+    c.d_keys = keys;
+    c.d_out = out;
+    c.d_flags = flags;
     std::lock_guard<std::mutex> lk(cache_->mutex());
     const uint64_t stamp = cache_->bump_clock();  // query ticks even when empty
     if (n > 0) {
@@ -279,44 +317,73 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
           std::memcpy(ws->h_keys, keys, n * 8);
           HPSB_CUDA(cudaMemcpyAsync(ws->d_keys, ws->h_keys, n * 8, cudaMemcpyHostToDevice, st));
         }
-        d_keys = ws->d_keys;
-        d_out = ws->d_out;
-        d_flags = ws->d_flags;
+        c.d_keys = ws->d_keys;
+        c.d_out = ws->d_out;
+        c.d_flags = ws->d_flags;
       } else {
         cache_->join_from(user);
       }
       ws->lv = lookup_next_view(ws->ls, /*chain=*/false);
       ws->lv.marks = cache_->lookup_marks_locked();
       cache_->note_stream_op();  // the engine's own copies follow on the stream
-      launch_lookup_probe(cache_->dev(), d_keys, n, d_out, d_flags, d_default_, stamp, ws->lv,
-                          /*after_lookup=*/false, st);
+      launch_lookup_probe(cache_->dev(), c.d_keys, n, c.d_out, c.d_flags, d_default_, stamp,
+                          ws->lv, /*after_lookup=*/false, st);
       HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->lv.counts_out, 16, cudaMemcpyDeviceToHost, st));
       // One host round trip on the common path: the first claims and -- when
       // the previous call took the async branch, whose rows are final as the
       // kernel leaves them -- the rows and flags come back with the counts.
-      spec_claims = std::min<uint64_t>(n, kSpeculativeClaims);
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, spec_claims * 8,
+      c.spec_claims = std::min<uint64_t>(n, kSpeculativeClaims);
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, c.spec_claims * 8,
                                 cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, spec_claims * 4,
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, c.spec_claims * 4,
                                 cudaMemcpyDeviceToHost, st));
-      if (host && spec_rows) {
-        HPSB_CUDA(cudaMemcpyAsync(out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
+      if (host && c.spec_rows) {
+        HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, c.d_out, n * uint64_t(d) * 4,
                                   cudaMemcpyDeviceToHost, st));
-        HPSB_CUDA(cudaMemcpyAsync(flags_pinned ? flags : ws->h_flags, d_flags, n,
+        HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, c.d_flags, n,
                                   cudaMemcpyDeviceToHost, st));
       }
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }
+  } catch (...) {
+    pool_.release(ws);
+    throw;
   }
+  return c;
+}
+
+void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
+  Workspace* ws = c.ws;
+  bool handed_off = false;
+  struct LeaseGuard {
+    WorkspacePool& pool;
+    LookupCall& c;
+    bool* handed;
+    ~LeaseGuard() {
+      if (!*handed && c.ws) pool.release(c.ws);
+      c.ws = nullptr;
+    }
+  } guard{pool_, c, &handed_off};
+  const size_t n = c.n;
+  const bool host = c.host;
+  const uint32_t d = dim_;
+  float* out = c.out;
+  uint8_t* flags = c.flags;
+  float* d_out = c.d_out;
+  uint8_t* d_flags = c.d_flags;
+  DeviceGuard g(cache_->device());
+  cudaStream_t st = cache_->stream();
+  uint64_t uh = 0, um = 0;
   if (n > 0) {
     HPSB_CUDA(cudaEventSynchronize(ws->done));
     uh = ws->h_counts[0];
     um = ws->h_counts[1];
-    if (um > spec_claims) {
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys + spec_claims, ws->lv.list_keys + spec_claims,
-                                (um - spec_claims) * 8, cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts + spec_claims,
-                                ws->lv.list_firsts + spec_claims, (um - spec_claims) * 4,
+    if (um > c.spec_claims) {
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys + c.spec_claims,
+                                ws->lv.list_keys + c.spec_claims, (um - c.spec_claims) * 8,
+                                cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts + c.spec_claims,
+                                ws->lv.list_firsts + c.spec_claims, (um - c.spec_claims) * 4,
                                 cudaMemcpyDeviceToHost, st));
       HPSB_CUDA(cudaEventRecord(ws->done, st));
       HPSB_CUDA(cudaEventSynchronize(ws->done));
@@ -365,19 +432,19 @@ void LookupEngine::lookup(const uint64_t* keys, size_t n, float* out, size_t out
   last_async_.store(!sync_branch, std::memory_order_relaxed);
   if (n > 0) {
     if (host) {
-      if (sync_branch || !spec_rows) {
-        HPSB_CUDA(cudaMemcpyAsync(out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
+      if (sync_branch || !c.spec_rows) {
+        HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
                                   cudaMemcpyDeviceToHost, st));
-        HPSB_CUDA(cudaMemcpyAsync(flags_pinned ? flags : ws->h_flags, d_flags, n,
+        HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
                                   cudaMemcpyDeviceToHost, st));
         HPSB_CUDA(cudaEventRecord(ws->done, st));
         HPSB_CUDA(cudaEventSynchronize(ws->done));
       }
       ws->pending = false;
-      if (!out_pinned) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
-      if (!flags_pinned) std::memcpy(flags, ws->h_flags, n);
+      if (!c.out_pinned) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
+      if (!c.flags_pinned) std::memcpy(flags, ws->h_flags, n);
     } else {
-      cache_->join_to(user);
+      cache_->join_to(c.user);
     }
   }
 

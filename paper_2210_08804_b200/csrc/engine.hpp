@@ -133,6 +133,12 @@ class LookupEngine {
 
   void lookup(const uint64_t* keys, size_t n, float* out, size_t out_len, uint8_t* flags,
               LookupOutcome* outcome, int mem, cudaStream_t user);
+  // Several tables at once (one engine each; the reference's caller loops
+  // over tables): every table's device work is enqueued before any host
+  // wait, so the lookups overlap on the GPU. Same per-table semantics.
+  static void lookup_multi(LookupEngine* const* engines, size_t count,
+                           const uint64_t* const* keys, const size_t* n, float* const* out,
+                           uint8_t* const* flags, LookupOutcome* outcomes, int mem);
   void drain_async();
   EngineStats stats() const;
   WorkspacePool& pool() { return pool_; }
@@ -141,6 +147,25 @@ class LookupEngine {
   // claims copied back speculatively with the counts (one round trip when a
   // call has at most this many unique misses)
   static constexpr uint64_t kSpeculativeClaims = 4096;
+  // one lookup split at its first host wait (begin enqueues, finish waits)
+  struct LookupCall {
+    LookupEngine* engine = nullptr;
+    Workspace* ws = nullptr;
+    size_t n = 0;
+    float* out = nullptr;
+    uint8_t* flags = nullptr;
+    int mem = 0;
+    cudaStream_t user = nullptr;
+    bool host = true, spec_rows = false, out_pinned = false, flags_pinned = false;
+    uint64_t spec_claims = 0;
+    const uint64_t* d_keys = nullptr;
+    float* d_out = nullptr;
+    uint8_t* d_flags = nullptr;
+  };
+  LookupCall begin(const uint64_t* keys, size_t n, float* out, size_t out_len, uint8_t* flags,
+                   int mem, cudaStream_t user);
+  void finish(LookupCall& c, LookupOutcome* outcome);
+  void abandon(LookupCall& c);
   // the previous lookup took the async branch: speculate that this one will
   // too and bring its rows back with the counts
   std::atomic<bool> last_async_{false};

@@ -2,8 +2,9 @@
 include/hps/lookup_engine.hpp re-expose the reference's hps::SlabCache
 (slab_cache.hpp:23-178) and hps::LookupEngine / tier_fetch
 (lookup_engine.hpp:29-196) over the C ABI, and the reference's OWN unit
-tests, tests/unit/test_slab_cache.cpp and test_lookup_engine.cpp, compiled
-unchanged against them (oracle/Makefile targets _ref/test_*_b200; doctest is
+tests, tests/unit/test_slab_cache.cpp and test_lookup_engine.cpp -- and the
+reference's refresh loop (refresh_engine.cpp, a caller of the cache) with
+test_refresh_engine.cpp -- compiled unchanged against them (oracle/Makefile targets _ref/test_*_b200; doctest is
 the local stand-in oracle/doctest_stub), must pass on the GPU."""
 import subprocess
 from pathlib import Path
@@ -36,7 +37,7 @@ def test_dropin_header_compiles_standalone(tmp_path):
     assert subprocess.run([str(exe)]).returncode == 0
 
 
-BINARIES = [oracle.REF_CACHE_TEST, oracle.REF_ENGINE_TEST]
+BINARIES = [oracle.REF_CACHE_TEST, oracle.REF_ENGINE_TEST, oracle.REF_REFRESH_TEST]
 
 
 @pytest.mark.parametrize("exe", BINARIES, ids=lambda p: p.name)

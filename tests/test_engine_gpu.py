@@ -280,3 +280,54 @@ def test_device_and_pinned_pointer_lookups_match_host_lookup():
         ep.drain_async()
         assert op.numpy().tobytes() == r.vectors.tobytes()
         assert (fp.numpy() == r.miss_flags).all()
+
+
+def test_multi_table_lookup_equals_per_table_lookups():
+    """hps_engine_lookup_multi (all tables' device work in flight before the
+    first host wait) must give every table exactly what a per-table
+    hps_engine_lookup gives: rows, flags, outcomes, cache state, stats --
+    over sync and async branches, with the tables' VDBs and cold tiers."""
+    import torch
+
+    d, T_, n = 16, 5, 3000
+
+    def build():
+        vdb = hps.VolatileStore(4)
+        engines, caches = [], []
+        for t in range(T_):
+            table = T(f"m{t}", d)
+            vdb.register_table(table)
+            keys = np.arange(t * 100000, t * 100000 + 20000, dtype=np.uint64)
+            vdb.insert(table.name, keys, row_values(keys, d, t))
+            c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=64, slabs_per_set=2, dimension=d))
+            caches.append(c)
+            engines.append(hps.LookupEngine(table, c, vdb, None,
+                                            hps.EngineConfig(hit_rate_threshold=0.6,
+                                                             default_vector=[float(t)] * d)))
+        return vdb, caches, engines
+
+    va, ca, ea = build()
+    vb, cb, eb = build()
+    rng = np.random.default_rng(9)
+    for r in range(6):
+        batches = [hps.powerlaw_sample(1.1, 26000, t, 50 * r + t, n) + np.uint64(t * 100000)
+                   for t in range(T_)]
+        pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
+        po = [torch.empty(n * d).pin_memory() for _ in range(T_)]
+        pf = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(T_)]
+        outs = hps.LookupEngine.lookup_multi_ptrs(ea, [p.data_ptr() for p in pk], [n] * T_,
+                                                  [p.data_ptr() for p in po],
+                                                  [p.data_ptr() for p in pf], hps.HPS_MEM_HOST)
+        for t in range(T_):
+            o = hps.LookupOutcome()
+            want = eb[t].lookup(batches[t], o)
+            assert po[t].numpy().tobytes() == want.vectors.tobytes(), (r, t)
+            assert (pf[t].numpy() == want.miss_flags).all(), (r, t)
+            assert outs[t] == o, (r, t)
+        for e in ea + eb:
+            e.drain_async()
+    for t in range(T_):
+        assert ca[t].dump_all().tolist() == cb[t].dump_all().tolist()
+        assert ea[t].stats() == eb[t].stats()
+    for e in ea + eb:
+        e.close()

@@ -11,9 +11,9 @@ Each table: power-law (alpha 1.2) key stream over its own keyspace, a GPU
 cache of --cache-frac of the table (the paper's Criteo runs use 0.5), the
 whole table in the host volatile DB (the miss path), threshold 0.8. Rows are
 synthetic (a hash of key and column). Per batch size: p50 / p99 latency of
-one table lookup (one table at a time), and of a 26-table sample batch with
-the tables looked up concurrently from a thread pool (one engine per table),
-plus samples/s. Warm-up fills the caches to steady state first.
+one table lookup (one table at a time), and of a 26-table sample batch --
+tables looked up concurrently from a thread pool (one engine per table), and
+all 26 through one hps_engine_lookup_multi call -- plus samples/s. Warm-up fills the caches to steady state first.
 """
 from __future__ import annotations
 
@@ -116,23 +116,35 @@ def main():
             dt, h = call(t, n, batches[i // T % len(batches)][t])
             lat.append(dt)
             hits.append(h)
-        sample_lat = []
+        sample_lat, multi_lat = [], []
         reps = max(3, min(20, calls // 4))
         for r in range(reps):  # a 26-table sample batch, tables concurrently
             bs = batches[r % len(batches)]
             t0 = time.perf_counter()
             list(pool.map(lambda t: call(t, n, bs[t]), range(T)))
             sample_lat.append(time.perf_counter() - t0)
+        for r in range(reps):  # the same through one hps_engine_lookup_multi call
+            bs = batches[r % len(batches)]
+            for t in range(T):
+                pk[t][:n].copy_(torch.from_numpy(bs[t].view(np.int64)))
+            t0 = time.perf_counter()
+            hps.LookupEngine.lookup_multi_ptrs(engines, [p.data_ptr() for p in pk], [n] * T,
+                                               [p.data_ptr() for p in po],
+                                               [p.data_ptr() for p in pf], hps.HPS_MEM_HOST)
+            multi_lat.append(time.perf_counter() - t0)
         for e in engines:
             e.drain_async()
         lat = np.array(lat) * 1e6
         sl = np.array(sample_lat) * 1e6
+        ml = np.array(multi_lat) * 1e6
         result["per_batch"].append({
             "batch": n, "table_lookup_p50_us": float(np.median(lat)),
             "table_lookup_p99_us": float(np.percentile(lat, 99)),
             "table_lookup_keys_per_s": n / (np.median(lat) * 1e-6),
             "sample_batch_26_tables_p50_us": float(np.median(sl)),
             "samples_per_s": n / (np.median(sl) * 1e-6),
+            "sample_batch_26_tables_lookup_multi_p50_us": float(np.median(ml)),
+            "samples_per_s_lookup_multi": n / (np.median(ml) * 1e-6),
             "mean_unique_hit_rate": float(np.mean(hits))})
         print(json.dumps(result["per_batch"][-1]), file=sys.stderr)
     stats = [e.stats() for e in engines]
