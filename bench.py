@@ -242,6 +242,19 @@ def ncu_traffic():
     return None
 
 
+def max_over_ranks(x: float, dist, dev) -> float:
+    """Max of a per-rank time over all ranks (the slowest rank defines the
+    job's time); identity when not distributed."""
+    if not dist:
+        return x
+    import torch
+
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ------------------------------------------------------------ our arm -----
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -249,12 +262,20 @@ def run_ours(args, rank, world, local_rank):
     import paper_2210_08804_b200 as hps
 
     dist = None
+    # HPSB_BENCH_DEVICE pins every rank to one GPU and HPSB_BENCH_BACKEND picks
+    # the process-group backend: together they let the N > 1 path run (gloo)
+    # on a one-GPU box for testing; the driver's runs use one GPU per rank +
+    # NCCL. Only the barrier and the max-over-ranks reduction are collective.
+    dev = int(os.environ.get("HPSB_BENCH_DEVICE", local_rank))
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    torch.cuda.set_device(local_rank)
-    dev = local_rank
+        backend = os.environ.get("HPSB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    torch.cuda.set_device(dev)
     wl = Workload(keyspace=args.keyspace, dim=args.dim, cache_frac=args.cache_frac,
                   batch=args.batch)
     d, n = wl.dim, wl.batch
@@ -348,10 +369,7 @@ def run_ours(args, rank, world, local_rank):
         k1 = np.array([a.elapsed_time(b) for a, b in kev])
         per = k1
         h_meas = float(np.mean(1.0 - c[:, 1] / np.maximum(c.sum(axis=1), 1)))
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms, dist, dev)
         bytes_per = float(np.mean([ab[s % pool][0] for s in range(steps)]))
         # consecutive lookups overlap (programmatic dependent launch): the
         # kernel's average duration over the timed region is total / steps;
@@ -372,12 +390,18 @@ def run_ours(args, rank, world, local_rank):
                 "keys_per_s": world * max(args.steps // 4, 4) * n / (r["total_ms"] / 1e3),
                 "p50_batch_us": r["p50_us"], "measured_unique_hit_rate": r["h"],
                 "kernel_us": r["total_ms"] * 1e3 / max(args.steps // 4, 4),
-                "kernel_gbs": r["bytes_per_batch"] / (r["total_ms"] * 1e-3 / max(args.steps // 4, 4)) / 1e9}
+                "kernel_gbs": r["bytes_per_batch"] / (r["total_ms"] * 1e-3 / max(args.steps // 4, 4)) / 1e9,
+                "roofline_frac": r["bytes_per_batch"] / (r["total_ms"] * 1e-3 / max(args.steps // 4, 4))
+                / 1e9 / hbm_peak()[0],
+                "algorithmic_bytes_per_batch": r["bytes_per_batch"]}
     sweep[f"{args.hit:.2f}"] = {
         "keys_per_s": world * args.steps * n / (main["total_ms"] / 1e3),
         "p50_batch_us": main["p50_us"], "measured_unique_hit_rate": main["h"],
         "kernel_us": main["total_ms"] * 1e3 / args.steps,
-        "kernel_gbs": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9}
+        "kernel_gbs": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9,
+        "roofline_frac": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9
+        / hbm_peak()[0],
+        "algorithmic_bytes_per_batch": main["bytes_per_batch"]}
 
     online = None
     if not args.no_online:
@@ -550,10 +574,7 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist):
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     launches = hps.kernel_launch_count() - l0
-    if dist:
-        t = torch.tensor([el], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
+    el = max_over_ranks(el, dist, dev)
     world = dist.get_world_size() if dist else 1
     st = eng.stats()
     eng.close()
