@@ -173,6 +173,13 @@ int hps_cache_update_device(hps_cache* cache, const uint64_t* keys, size_t n,
 int hps_cache_dump(hps_cache* cache, uint64_t set_begin, uint64_t set_end,
                    uint64_t* out, size_t cap, size_t* n_out);
 
+/* Stream-ordered DumpCursor pass into DEVICE memory (the GPU refresh path):
+ * resident keys of slabsets [set_begin, set_end) in set, slab, slot order
+ * into `out` (capacity (set_end - set_begin) * slabs_per_set * 32 keys) and
+ * their count into *n_out (device u64). */
+int hps_cache_dump_device(hps_cache* cache, uint64_t set_begin, uint64_t set_end, uint64_t* out,
+                          uint64_t* n_out, void* stream);
+
 /* replaces SlabCache::check_invariants (slab_cache.cpp:407-442); returns
  * HPS_LOGIC_ERROR with the reference's message on violation. */
 int hps_cache_check_invariants(hps_cache* cache);

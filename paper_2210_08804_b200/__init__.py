@@ -147,6 +147,7 @@ SIGNATURES = {
     "hps_cache_update_device": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P, _P]),
     "hps_shard_of": (C.c_uint32, [C.c_uint64, C.c_uint32]),
     "hps_engine_lookup_multi": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, _P, C.c_int]),
+    "hps_cache_dump_device": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, _P, _P]),
     "hps_shard_count": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P]),
     "hps_shard_scatter": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P, _P, _P]),
     "hps_shard_unroute": (C.c_int, [C.c_int, C.c_size_t, C.c_uint32, _P, _P, _P, _P, _P, _P]),
@@ -413,6 +414,12 @@ class SlabCache:
         the written count lands in device memory at written_ptr (optional)."""
         _check(lib().hps_cache_update_device(self._h, keys_ptr, n, rows_ptr, n * self._dim,
                                              written_ptr or None, stream or None))
+
+    def dump_device_async(self, set_begin: int, set_end: int, out_ptr: int, n_out_ptr: int,
+                          stream: int = 0) -> None:
+        """hps_cache_dump_device: stream-ordered dump into device memory."""
+        _check(lib().hps_cache_dump_device(self._h, set_begin, set_end, out_ptr, n_out_ptr,
+                                           stream or None))
 
     def dump(self, batch_size: int) -> "DumpCursor":
         if batch_size == 0:

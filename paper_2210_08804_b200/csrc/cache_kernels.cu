@@ -440,28 +440,41 @@ void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const fl
 
 // ------------------------------------------------------------------- dump --
 // Resident keys of slabs [set_begin*W, set_end*W) in slab order, slot order
-// inside a slab (slab_cache.cpp:380-392). One item = one slab.
-// Count-weighted variant of select_tile: each item contributes popc(mask).
+// inside a slab (slab_cache.cpp:380-392). A tile = kScanTile slabs: (1) each
+// thread reads kScanItems masks, a block scan of their popcounts plus a
+// decoupled look-back give every slab its output offset; (2) the warps copy
+// the keys slab by slab -- occupancy grows contiguously from bit 0, so lane j
+// of an occupied slab writes out[offset + j]: coalesced 256 B loads and
+// contiguous stores, four slabs in flight per warp.
 __global__ void __launch_bounds__(kScanBlock)
     k_dump_keys(CacheDev c, uint64_t slab_begin, uint64_t n_slabs, uint64_t* __restrict__ out,
                 unsigned long long* n_out, ScanState scan) {
   __shared__ uint32_t s_warp[kScanBlock / 32];
   __shared__ uint64_t s_tile;
   __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_off[kScanTile];
+  __shared__ uint32_t s_cnt[kScanTile];
   if (threadIdx.x == 0) s_tile = atomicAdd(scan.tile_ctr, 1ull) - scan.tile_base;
   __syncthreads();
   const uint64_t tile = s_tile;
-  const uint64_t first = tile * kScanTile + uint64_t(threadIdx.x) * kScanItems;
+  const uint64_t first = tile * kScanTile;
   uint32_t m[kScanItems];
   uint32_t cnt = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t s = first + k;
-    m[k] = (s < n_slabs) ? c.masks[slab_begin + s] : 0u;
+    const uint64_t sl = first + uint64_t(threadIdx.x) * kScanItems + k;
+    m[k] = (sl < n_slabs) ? c.masks[slab_begin + sl] : 0u;
     cnt += __popc(m[k]);
   }
   uint32_t block_total;
-  const uint32_t excl = block_exclusive_scan<kScanBlock>(cnt, s_warp, &block_total);
+  uint32_t excl = block_exclusive_scan<kScanBlock>(cnt, s_warp, &block_total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint32_t i = threadIdx.x * kScanItems + k;
+    s_off[i] = excl;
+    s_cnt[i] = __popc(m[k]);
+    excl += __popc(m[k]);
+  }
   if (threadIdx.x < 32) {
     const uint64_t pre = lb_exclusive_prefix(scan.status, uint32_t(tile), scan.epoch, block_total);
     if (threadIdx.x == 0) {
@@ -471,15 +484,21 @@ __global__ void __launch_bounds__(kScanBlock)
     }
   }
   __syncthreads();
-  uint64_t r = s_prefix + excl;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr uint32_t kWarpsB = kScanBlock / 32;
+  const uint64_t prefix = s_prefix;
+  const uint64_t* kbase = c.keys + (slab_begin + first) * kSlotsPerSlab;
+  for (uint32_t i0 = warp; i0 < kScanTile; i0 += 4 * kWarpsB) {
+    uint64_t k[4];
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    uint32_t mm = m[k];
-    const uint64_t slab = slab_begin + first + k;
-    while (mm) {
-      const uint32_t j = __ffs(mm) - 1;
-      mm &= mm - 1;
-      out[r++] = c.keys[slab * kSlotsPerSlab + j];
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * kWarpsB;
+      k[u] = (i < kScanTile && lane < s_cnt[i]) ? kbase[uint64_t(i) * kSlotsPerSlab + lane] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * kWarpsB;
+      if (i < kScanTile && lane < s_cnt[i]) out[prefix + s_off[i] + lane] = k[u];
     }
   }
 }

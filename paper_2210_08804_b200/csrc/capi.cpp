@@ -373,6 +373,14 @@ int hps_cache_update_device(hps_cache* cache, const uint64_t* keys, size_t n,
   });
 }
 
+int hps_cache_dump_device(hps_cache* cache, uint64_t set_begin, uint64_t set_end, uint64_t* out,
+                          uint64_t* n_out, void* stream) {
+  return guarded([&] {
+    need(cache && out && n_out, "null argument");
+    cache->impl->dump_device(set_begin, set_end, out, n_out, as_stream(stream));
+  });
+}
+
 int hps_cache_dump(hps_cache* cache, uint64_t set_begin, uint64_t set_end, uint64_t* out,
                    size_t cap, size_t* n_out) {
   return guarded([&] {

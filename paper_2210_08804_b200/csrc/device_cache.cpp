@@ -403,6 +403,23 @@ uint64_t DeviceCache::trace(unsigned long long* out) {
   return n;
 }
 
+void DeviceCache::dump_device(uint64_t set_begin, uint64_t set_end, uint64_t* out,
+                              uint64_t* n_out, cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  last_op_lookup_ = false;
+  set_end = std::min<uint64_t>(set_end, cfg_.slabset_count);
+  DeviceGuard g(device_);
+  join_from(user);
+  if (set_begin >= set_end) {
+    HPSB_CUDA(cudaMemsetAsync(n_out, 0, 8, stream_));
+  } else {
+    ensure_scan_tiles(((set_end - set_begin) * cfg_.slabs_per_set + kScanTile - 1) / kScanTile);
+    launch_dump(dev_, set_begin, set_end, out, reinterpret_cast<unsigned long long*>(n_out),
+                scan_, stream_);
+  }
+  join_to(user);
+}
+
 void DeviceCache::export_state(uint64_t* keys, uint64_t* counters, uint32_t* masks,
                                float* rows) {
   std::lock_guard<std::mutex> lk(mu_);

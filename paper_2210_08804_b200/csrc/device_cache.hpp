@@ -50,6 +50,11 @@ class DeviceCache {
   // host sync; *written (device u64, may be null) gets the count.
   void update_device(const uint64_t* keys, size_t n, const float* vectors, uint64_t* written,
                      cudaStream_t user);
+  // Stream-ordered dump into device memory (refresh on the GPU): resident
+  // keys of sets [set_begin, set_end) in set / slab / slot order into `out`
+  // (capacity (set_end - set_begin) * W * 32), the count into *n_out.
+  void dump_device(uint64_t set_begin, uint64_t set_end, uint64_t* out, uint64_t* n_out,
+                   cudaStream_t user);
   // Lookup-level query on device pointers (the engine's hot path without
   // the tier logic): bumps the clock, writes every position's row (hit:
   // cached row, miss: default_row), miss flags, the unique missing keys with
