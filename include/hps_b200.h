@@ -247,6 +247,17 @@ int hps_tier_fetch(hps_vdb* vdb, const char* table, uint32_t dimension,
                    size_t* n_found, uint64_t* missing_keys, size_t* n_missing,
                    uint64_t* counters);
 
+/* replaces hps::refresh_cache (refresh_engine.cpp:5-22): every resident key,
+ * in dump order and batches of dump_batch, re-fetched from the tiers (VDB
+ * first, then the cold tier) and written back with the non-admitting update;
+ * *refreshed = rows rewritten, unresolved (capacity unresolved_cap, may be
+ * NULL) = resident keys absent from every tier, *n_unresolved their count.
+ * The host tier fetch of one batch overlaps the device update of the last. */
+int hps_refresh_cache(hps_cache* cache, hps_vdb* vdb, const char* table,
+                      hps_cold_fetch_fn cold, void* cold_ctx, size_t dump_batch,
+                      uint64_t* refreshed, uint64_t* unresolved, size_t unresolved_cap,
+                      size_t* n_unresolved);
+
 /* ---- lookup engine (replaces hps::LookupEngine, lookup_engine.hpp:152-196) ---- */
 
 /* Mirrors EngineConfig (lookup_engine.hpp:29-37). */

@@ -148,6 +148,8 @@ SIGNATURES = {
     "hps_shard_of": (C.c_uint32, [C.c_uint64, C.c_uint32]),
     "hps_engine_lookup_multi": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, _P, C.c_int]),
     "hps_cache_dump_device": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, _P, _P]),
+    "hps_refresh_cache": (C.c_int, [_P, _P, C.c_char_p, _P, _P, C.c_size_t, _U64P, _P,
+                                    C.c_size_t, _SZP]),
     "hps_shard_count": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P]),
     "hps_shard_scatter": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P, _P, _P]),
     "hps_shard_unroute": (C.c_int, [C.c_int, C.c_size_t, C.c_uint32, _P, _P, _P, _P, _P, _P]),
@@ -729,6 +731,30 @@ def tier_fetch(table: TableId, keys, vdb: Optional[VolatileStore], pdb=None,
         counters["pdb_hits"] = counters.get("pdb_hits", 0) + int(cnt[1])
         counters["missing"] = counters.get("missing", 0) + int(cnt[2])
     return FetchResult(fk[: nf.value].copy(), fv[: nf.value * d].copy(), mk[: nm.value].copy())
+
+
+@dataclass
+class RefreshOutcome:
+    """refresh_engine.hpp:30-33"""
+    refreshed: int = 0
+    unresolved: np.ndarray = field(default_factory=lambda: np.empty(0, np.uint64))
+
+
+def refresh_cache(cache: "SlabCache", table: TableId, vdb: Optional[VolatileStore], pdb=None,
+                  dump_batch_size: int = 65536) -> RefreshOutcome:
+    """refresh_engine.cpp:5-22 on the B200 cache (hps_refresh_cache): dump,
+    tier fetch (VDB, then pdb), non-admitting update; the host fetch of one
+    batch overlaps the device update of the previous one."""
+    cold = ColdTier(pdb, table.dimension) if pdb is not None else None
+    cap = cache.capacity()
+    un = np.empty(max(cap, 1), dtype=np.uint64)
+    refreshed = C.c_uint64(0)
+    nu = C.c_size_t(0)
+    _check(lib().hps_refresh_cache(cache.handle, vdb.handle if vdb else None,
+                                   table.name.encode(), cold.fn if cold else _NULL_COLD, None,
+                                   dump_batch_size, C.byref(refreshed), _ptr(un), cap,
+                                   C.byref(nu)))
+    return RefreshOutcome(int(refreshed.value), un[: nu.value].copy())
 
 
 # ----------------------------------------------------------------- engine --

@@ -550,6 +550,22 @@ int hps_tier_fetch(hps_vdb* vdb, const char* table, uint32_t dimension, hps_cold
   });
 }
 
+int hps_refresh_cache(hps_cache* cache, hps_vdb* vdb, const char* table,
+                      hps_cold_fetch_fn cold, void* cold_ctx, size_t dump_batch,
+                      uint64_t* refreshed, uint64_t* unresolved, size_t unresolved_cap,
+                      size_t* n_unresolved) {
+  return guarded([&] {
+    need(cache && table && refreshed && n_unresolved, "null argument");
+    auto r = hpsb::refresh_cache(*cache->impl, vdb ? vdb->impl.get() : nullptr, table, cold,
+                                 cold_ctx, dump_batch);
+    *refreshed = r.refreshed;
+    *n_unresolved = r.unresolved.size();
+    if (unresolved)
+      std::copy(r.unresolved.begin(),
+                r.unresolved.begin() + std::min(unresolved_cap, r.unresolved.size()), unresolved);
+  });
+}
+
 // ----------------------------------------------------------------- engine --
 int hps_engine_create(const char* table, uint32_t dimension, hps_cache* cache, hps_vdb* vdb,
                       hps_cold_fetch_fn cold, void* cold_ctx, const hps_engine_config* config,

@@ -89,6 +89,82 @@ void tier_fetch_staged(VolatileStore* vdb, const std::string& table, uint32_t di
   *n_missing = cm;
 }
 
+// ---------------------------------------------------------------- refresh --
+// refresh_engine.cpp:5-22 (refresh_cache): the resident keys in dump order,
+// batch by batch fetched from the tiers and written back with the
+// non-admitting update. B200 pipeline: the host tier fetch of batch i+1
+// (found rows land straight in pinned staging) overlaps the H2D copy and the
+// device update of batch i (two staging buffers, stream-ordered on the
+// cache's stream); the written counts stay on the device until the end.
+RefreshResult refresh_cache(DeviceCache& cache, VolatileStore* vdb, const std::string& table,
+                            ColdFetchFn cold, void* cold_ctx, size_t dump_batch) {
+  if (dump_batch == 0) throw invalid_argument("dump batch size must be positive");
+  RefreshResult r;
+  const uint32_t d = cache.dimension();
+  const uint64_t S = cache.slabset_count();
+  std::vector<uint64_t> keys(S * cache.slabs_per_set() * 32ull);
+  keys.resize(cache.dump(0, S, keys.data(), keys.size()));
+  if (keys.empty()) return r;
+  DeviceGuard g(cache.device());
+  cudaStream_t st = cache.stream();
+  const uint64_t nb = (keys.size() + dump_batch - 1) / dump_batch;
+  struct Stage {
+    PinnedBuffer h;
+    DeviceBuffer dv;
+    cudaEvent_t done = nullptr;
+    uint64_t* h_keys = nullptr;
+    float* h_rows = nullptr;
+    uint64_t* d_keys = nullptr;
+    float* d_rows = nullptr;
+  } stage[2];
+  std::vector<uint64_t> missing(dump_batch);
+  std::vector<int32_t> row_of(dump_batch);
+  DeviceBuffer written_buf;
+  uint64_t* written = static_cast<uint64_t*>(written_buf.ensure(nb * 8, st));
+  HPSB_CUDA(cudaMemsetAsync(written, 0, nb * 8, st));
+  for (auto& sg : stage) {
+    HPSB_CUDA(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
+    char* hp = static_cast<char*>(sg.h.ensure(dump_batch * (8 + uint64_t(d) * 4)));
+    sg.h_keys = reinterpret_cast<uint64_t*>(hp);
+    sg.h_rows = reinterpret_cast<float*>(hp + dump_batch * 8);
+    char* dp = static_cast<char*>(sg.dv.ensure(dump_batch * (8 + uint64_t(d) * 4) + 256, st));
+    sg.d_keys = reinterpret_cast<uint64_t*>(dp);
+    sg.d_rows = reinterpret_cast<float*>(dp + (dump_batch * 8 + 255) / 256 * 256);
+  }
+  std::exception_ptr err;
+  try {
+    for (uint64_t b = 0; b < nb; ++b) {
+      Stage& sg = stage[b & 1];
+      HPSB_CUDA(cudaEventSynchronize(sg.done));  // staging b is free again
+      const uint64_t k0 = b * dump_batch;
+      const uint64_t m = std::min<uint64_t>(dump_batch, keys.size() - k0);
+      size_t nf = 0, nm = 0;
+      TierCounters tc;
+      tier_fetch_staged(vdb, table, d, cold, cold_ctx, keys.data() + k0, m, sg.h_keys, sg.h_rows,
+                        row_of.data(), &nf, missing.data(), &nm, &tc);
+      r.unresolved.insert(r.unresolved.end(), missing.begin(), missing.begin() + nm);
+      if (nf > 0) {
+        HPSB_CUDA(cudaMemcpyAsync(sg.d_keys, sg.h_keys, nf * 8, cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(sg.d_rows, sg.h_rows, nf * uint64_t(d) * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaEventRecord(sg.done, st));
+        cache.update_device(sg.d_keys, nf, sg.d_rows, written + b, st);
+      }
+    }
+  } catch (...) {
+    // a tier fault aborts the pass; batches already applied stay applied
+    // (refresh_engine.hpp:35-39)
+    err = std::current_exception();
+  }
+  std::vector<uint64_t> w(nb);
+  HPSB_CUDA(cudaMemcpyAsync(w.data(), written, nb * 8, cudaMemcpyDeviceToHost, st));
+  HPSB_CUDA(cudaStreamSynchronize(st));
+  for (auto& sg : stage) cudaEventDestroy(sg.done);
+  for (uint64_t x : w) r.refreshed += x;
+  if (err) std::rethrow_exception(err);
+  return r;
+}
+
 // -------------------------------------------------------------- workspace --
 Workspace::~Workspace() {
   if (done) {

@@ -46,6 +46,15 @@ void tier_fetch_staged(VolatileStore* vdb, const std::string& table, uint32_t di
                        uint64_t* found_keys, float* rows, int32_t* row_of, size_t* n_found,
                        uint64_t* missing_keys, size_t* n_missing, TierCounters* counters);
 
+// refresh_engine.cpp:5-22 (refresh_cache) on the B200 cache: dump, tier
+// fetch, non-admitting update, pipelined over two staging buffers.
+struct RefreshResult {
+  uint64_t refreshed = 0;            // cache rows actually rewritten
+  std::vector<uint64_t> unresolved;  // resident but absent from every tier (dump order)
+};
+RefreshResult refresh_cache(DeviceCache& cache, VolatileStore* vdb, const std::string& table,
+                            ColdFetchFn cold, void* cold_ctx, size_t dump_batch);
+
 struct EngineConfig {
   double hit_rate_threshold = 0.8;
   std::vector<float> default_vector;

@@ -331,3 +331,75 @@ def test_multi_table_lookup_equals_per_table_lookups():
         assert ea[t].stats() == eb[t].stats()
     for e in ea + eb:
         e.close()
+
+
+@pytest.mark.parametrize("dump_batch", [1, 97, 4096])
+def test_native_refresh_matches_reference_semantics(dump_batch):
+    """hps_refresh_cache = refresh_cache (refresh_engine.cpp:5-22): every
+    resident key in dump order, VDB value first, then the cold tier; found
+    rows written back with update (nothing admitted, recency untouched),
+    keys absent from both reported unresolved in dump order."""
+    d = 8
+    cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=32, slabs_per_set=2, dimension=d))
+    o = oracle.OracleCache(32, 2, d)
+    rng = np.random.default_rng(dump_batch)
+    keys = rng.choice(100000, 1500, replace=False).astype(np.uint64)
+    cache.replace(keys, row_values(keys, d, 0))
+    o.replace(keys, row_values(keys, d, 0))
+    resident = cache.dump_all()
+    assert (resident == o.dump()).all()
+    table = T("r", d)
+    vdb = hps.VolatileStore(2)
+    vdb.register_table(table)
+    in_vdb = resident[rng.random(len(resident)) < 0.5]
+    vdb.insert("r", in_vdb, row_values(in_vdb, d, 1))
+    rest = np.setdiff1d(resident, in_vdb)
+    in_cold = rest[rng.random(len(rest)) < 0.6]
+    pdb = hps.DictStore(d)
+    pdb.put(in_cold, row_values(in_cold, d, 2))
+    clock = cache.recency_clock()
+    out = hps.refresh_cache(cache, table, vdb, pdb, dump_batch_size=dump_batch)
+    found = np.concatenate([in_vdb, in_cold])
+    want_un = resident[~np.isin(resident, found)]
+    assert out.refreshed == len(found)
+    assert out.unresolved.tolist() == want_un.tolist()
+    vset = set(in_vdb.tolist())
+    for b in range(0, len(resident), dump_batch):
+        bk = resident[b:b + dump_batch]
+        fv = [k for k in bk if int(k) in vset]
+        fc = [k for k in bk if int(k) not in vset and k in set(in_cold.tolist())]
+        if fv:
+            o.update(np.array(fv, np.uint64), row_values(np.array(fv, np.uint64), d, 1))
+        if fc:
+            o.update(np.array(fc, np.uint64), row_values(np.array(fc, np.uint64), d, 2))
+    gk, gc, gm, gr = cache.export_state()
+    ok, oc, om, orow = o.state()
+    occ = (np.repeat(gm, 32).reshape(-1, 32) >> np.arange(32, dtype=np.uint32) & 1).reshape(-1) == 1
+    assert (gm == om).all() and (gk[occ] == ok[occ]).all() and (gc[occ] == oc[occ]).all()
+    assert gr.reshape(-1, d)[occ].tobytes() == orow.reshape(-1, d)[occ].tobytes()
+    assert cache.recency_clock() == clock and cache.occupied() == len(resident)
+
+
+def test_native_refresh_tier_fault_keeps_finished_batches():
+    d = 4
+    cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=16, slabs_per_set=2, dimension=d))
+    keys = np.arange(600, dtype=np.uint64)
+    cache.replace(keys, row_values(keys, d, 0))
+    resident = cache.dump_all()
+
+    class Flaky:
+        calls = 0
+
+        def get(self, ks):
+            Flaky.calls += 1
+            if Flaky.calls > 2:
+                raise IOError("segment unreadable")
+            return hps.FetchResult(ks, row_values(ks, d, 5), np.empty(0, np.uint64))
+
+    with pytest.raises(hps.TierFault):
+        hps.refresh_cache(cache, T("f", d), None, Flaky(), dump_batch_size=100)
+    got = np.zeros(len(resident) * d, np.float32)
+    cache.query(resident, got)
+    got = got.reshape(-1, d)
+    assert got[:200].tobytes() == row_values(resident[:200], d, 5).tobytes()
+    assert got[200:].tobytes() == row_values(resident[200:], d, 0).tobytes()
