@@ -9,6 +9,7 @@
 #include "volatile_store.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <atomic>
 #include <cmath>
 
@@ -242,55 +243,68 @@ void VolatileStore::lookup(const std::string& name, const uint64_t* keys, size_t
   Table& t = table_ref(name);
   const uint64_t stamp = t.clock.fetch_add(1, std::memory_order_relaxed) + 1;
   const uint32_t dim = t.dim;
-  struct Chunk {
-    std::vector<uint64_t> fk, mk;
-    std::vector<float> rows;
-    std::vector<int32_t> local;  // per input in chunk: local found index or -1
-  };
+  // Every partition's shared lock for the whole call (one acquisition per
+  // partition instead of per key): entry positions found in pass 1 stay
+  // valid for the copies of pass 2. Writers (insert / evict) wait.
+  std::vector<std::shared_lock<std::shared_mutex>> held;
+  held.reserve(t.parts.size());
+  for (auto& p : t.parts) held.emplace_back(p->mu);
   const size_t min_chunk = 512;
-  const size_t nchunks = std::max<size_t>(1, std::min<size_t>(pool_.size(), (n + min_chunk - 1) / min_chunk));
-  std::vector<Chunk> chunks(nchunks);
+  const size_t nchunks =
+      std::max<size_t>(1, std::min<size_t>(pool_.size(), (n + min_chunk - 1) / min_chunk));
   const size_t per = (n + nchunks - 1) / nchunks;
+  std::vector<const float*> src(n);  // row of each found key, else null
+  std::vector<size_t> nf(nchunks, 0);
+  // pass 1: index probes, software-prefetched a few keys ahead
   pool_.parallel_for(nchunks, 1, [&](size_t cb, size_t ce) {
+    constexpr size_t kAhead = 8;
     for (size_t c = cb; c < ce; ++c) {
-      Chunk& ch = chunks[c];
       const size_t b = c * per, e = std::min(n, b + per);
-      if (b >= e) continue;
-      ch.local.resize(e - b);
+      size_t found = 0;
       for (size_t i = b; i < e; ++i) {
+        if (i + kAhead < e) {
+          const uint64_t kp = keys[i + kAhead];
+          const Partition& pp = *t.parts[partition_of(kp, t.partition_count)];
+          if (!pp.index.empty())
+            __builtin_prefetch(&pp.index[idx_hash(kp) & (pp.index.size() - 1)]);
+        }
         const uint64_t k = keys[i];
         Partition& p = *t.parts[partition_of(k, t.partition_count)];
-        std::shared_lock<std::shared_mutex> lk(p.mu);
         const int64_t ent = p.find(k);
         if (ent < 0) {
-          ch.mk.push_back(k);
-          ch.local[i - b] = -1;
+          src[i] = nullptr;
         } else {
-          ch.local[i - b] = int32_t(ch.fk.size());
-          ch.fk.push_back(k);
-          const float* src = p.rows.data() + size_t(ent) * dim;
-          ch.rows.insert(ch.rows.end(), src, src + dim);
+          src[i] = p.rows.data() + size_t(ent) * dim;
+          __builtin_prefetch(src[i]);
           atomic_max(p.last_access[size_t(ent)], stamp);
+          ++found;
         }
       }
+      nf[c] = found;
     }
   });
-  // stitch chunks in input order
   std::vector<size_t> foff(nchunks + 1, 0), moff(nchunks + 1, 0);
   for (size_t c = 0; c < nchunks; ++c) {
-    foff[c + 1] = foff[c] + chunks[c].fk.size();
-    moff[c + 1] = moff[c] + chunks[c].mk.size();
+    const size_t len = std::min(n, (c + 1) * per) - std::min(n, c * per);
+    foff[c + 1] = foff[c] + nf[c];
+    moff[c + 1] = moff[c] + (len - nf[c]);
   }
+  // pass 2: rows copied once, straight to their final (input-order) place
   pool_.parallel_for(nchunks, 1, [&](size_t cb, size_t ce) {
     for (size_t c = cb; c < ce; ++c) {
-      const Chunk& ch = chunks[c];
-      std::copy(ch.fk.begin(), ch.fk.end(), found_keys + foff[c]);
-      std::copy(ch.mk.begin(), ch.mk.end(), missing_keys + moff[c]);
-      if (!ch.rows.empty()) std::copy(ch.rows.begin(), ch.rows.end(), found_rows + foff[c] * dim);
-      if (found_idx) {
-        const size_t b = c * per;
-        for (size_t j = 0; j < ch.local.size(); ++j)
-          found_idx[b + j] = ch.local[j] < 0 ? -1 : int32_t(foff[c] + size_t(ch.local[j]));
+      const size_t b = c * per, e = std::min(n, b + per);
+      size_t f = foff[c], m = moff[c];
+      for (size_t i = b; i < e; ++i) {
+        if (src[i] != nullptr) {
+          if (i + 4 < e && src[i + 4] != nullptr) __builtin_prefetch(src[i + 4] + 16);
+          found_keys[f] = keys[i];
+          std::memcpy(found_rows + f * dim, src[i], size_t(dim) * 4);
+          if (found_idx) found_idx[i] = int32_t(f);
+          ++f;
+        } else {
+          missing_keys[m++] = keys[i];
+          if (found_idx) found_idx[i] = -1;
+        }
       }
     }
   });
