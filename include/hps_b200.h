@@ -49,6 +49,7 @@ extern "C" {
 typedef struct hps_cache hps_cache;
 typedef struct hps_vdb hps_vdb;
 typedef struct hps_engine hps_engine;
+typedef struct hps_multi hps_multi;
 
 /* ---- vocabulary ------------------------------------------------------- */
 
@@ -100,6 +101,12 @@ typedef struct {
 
 /* replaces SlabCache::SlabCache (slab_cache.cpp:17-41) */
 int hps_cache_create(const hps_cache_config* config, int device, hps_cache** out);
+/* A cache in the same CACHE GROUP as `share_with`: same device, one CUDA
+ * stream for all members (the tables of one model), so a multi-table lookup
+ * (hps_multi_*) can run every member in one launch. Otherwise identical to
+ * hps_cache_create. */
+int hps_cache_create_shared(const hps_cache_config* config, int device, hps_cache* share_with,
+                            hps_cache** out);
 /* replaces SlabCache::~SlabCache (slab_cache.cpp:43-52) */
 int hps_cache_destroy(hps_cache* cache);
 int hps_cache_get_info(hps_cache* cache, hps_cache_info* out);
@@ -309,6 +316,17 @@ int hps_engine_lookup(hps_engine* engine, const uint64_t* keys, size_t n, float*
 int hps_engine_lookup_multi(hps_engine* const* engines, size_t count,
                             const uint64_t* const* keys, const size_t* n, float* const* out,
                             uint8_t* const* miss_flags, hps_lookup_outcome* outcomes, int mem);
+
+/* Multi-table lookup over engines whose caches form one cache group
+ * (hps_cache_create_shared), one engine per table, batches of up to
+ * max_batch keys per table: ONE H2D, ONE kernel launch for every table, one
+ * D2H of all results, one host wait -- then each table's hit-rate switch and
+ * miss path exactly as hps_engine_lookup (host buffers). */
+int hps_multi_create(hps_engine* const* engines, size_t count, size_t max_batch,
+                     hps_multi** out);
+int hps_multi_destroy(hps_multi* multi);
+int hps_multi_lookup(hps_multi* multi, const uint64_t* const* keys, const size_t* n,
+                     float* const* out, uint8_t* const* miss_flags, hps_lookup_outcome* outcomes);
 
 /* replaces drain_async (lookup_engine.cpp:286-289) */
 int hps_engine_drain_async(hps_engine* engine);

@@ -148,6 +148,10 @@ SIGNATURES = {
     "hps_shard_of": (C.c_uint32, [C.c_uint64, C.c_uint32]),
     "hps_engine_lookup_multi": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, _P, C.c_int]),
     "hps_cache_dump_device": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, _P, _P]),
+    "hps_cache_create_shared": (C.c_int, [_P, C.c_int, _P, C.POINTER(_P)]),
+    "hps_multi_create": (C.c_int, [_P, C.c_size_t, C.c_size_t, C.POINTER(_P)]),
+    "hps_multi_destroy": (C.c_int, [_P]),
+    "hps_multi_lookup": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "hps_refresh_cache": (C.c_int, [_P, _P, C.c_char_p, _P, _P, C.c_size_t, _U64P, _P,
                                     C.c_size_t, _SZP]),
     "hps_shard_count": (C.c_int, [C.c_int, _P, C.c_size_t, C.c_uint32, _P, _P]),
@@ -311,11 +315,19 @@ class CacheMiss(NamedTuple):
 class SlabCache:
     """HBM-resident set-associative embedding cache (slab_cache.hpp:41-116)."""
 
-    def __init__(self, config: SlabCacheConfig, device: int = 0):
+    def __init__(self, config: SlabCacheConfig, device: int = 0,
+                 share_stream_with: Optional["SlabCache"] = None):
+        """share_stream_with: join that cache's CACHE GROUP (one stream; the
+        tables of one model) so a MultiLookup can run them in one launch."""
         self._h = C.c_void_p()
         cfg = _CacheConfig(config.slabset_count, config.slabs_per_set, config.dimension,
                            config.worker_pool_size, config.tasks_per_worker)
-        _check(lib().hps_cache_create(C.byref(cfg), device, C.byref(self._h)))
+        if share_stream_with is None:
+            _check(lib().hps_cache_create(C.byref(cfg), device, C.byref(self._h)))
+        else:
+            _check(lib().hps_cache_create_shared(C.byref(cfg), device, share_stream_with.handle,
+                                                 C.byref(self._h)))
+            self._group_anchor = share_stream_with
         self._dim = int(config.dimension)
         self.device = device
 
@@ -889,6 +901,47 @@ class LookupEngine:
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
         _check(lib().hps_engine_pool_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
         return PoolInfo(a.value, b.value, c.value)
+
+
+class MultiLookup:
+    """hps_multi_*: one lookup of several tables (engines whose caches form one
+    cache group) with one H2D, one kernel launch, one D2H and one host wait;
+    per-table semantics of LookupEngine.lookup."""
+
+    def __init__(self, engines: Sequence["LookupEngine"], max_batch: int):
+        self.engines = list(engines)
+        self._h = C.c_void_p()
+        t = len(self.engines)
+        _check(lib().hps_multi_create((C.c_void_p * t)(*[e._h for e in self.engines]), t,
+                                      max_batch, C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hps_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def lookup_ptrs(self, keys_ptrs, ns, out_ptrs, flags_ptrs) -> List[LookupOutcome]:
+        t = len(self.engines)
+        PA = C.c_void_p * t
+        outs = (_Outcome * t)()
+        _check(lib().hps_multi_lookup(self._h, PA(*keys_ptrs), (C.c_size_t * t)(*ns),
+                                      PA(*out_ptrs), PA(*flags_ptrs), outs))
+        return [LookupOutcome(bool(o.sync_branch), float(o.unique_hit_rate), int(o.unique_count),
+                              int(o.defaults_returned)) for o in outs]
+
+    def lookup(self, keys_per_table) -> List["LookupResult"]:
+        ks = [_u64(k) for k in keys_per_table]
+        res = [LookupResult(e.table.dimension, np.zeros(len(k) * e.table.dimension, np.float32),
+                            np.zeros(len(k), np.uint8)) for e, k in zip(self.engines, ks)]
+        self.lookup_ptrs([k.ctypes.data for k in ks], [len(k) for k in ks],
+                         [r.vectors.ctypes.data for r in res], [r.miss_flags.ctypes.data for r in res])
+        return res
 
 
 def powerlaw_sample(alpha: float, keyspace: int, permute_seed: int, draw_seed: int,

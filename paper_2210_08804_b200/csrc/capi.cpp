@@ -22,6 +22,9 @@ struct hps_vdb {
 struct hps_engine {
   std::unique_ptr<hpsb::LookupEngine> impl;
 };
+struct hps_multi {
+  std::unique_ptr<hpsb::MultiLookup> impl;
+};
 
 namespace hpsb {
 void powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed, uint64_t draw_seed,
@@ -257,6 +260,22 @@ int hps_cache_create(const hps_cache_config* config, int device, hps_cache** out
     c.tasks_per_worker = config->tasks_per_worker;
     auto h = std::make_unique<hps_cache>();
     h->impl = std::make_unique<hpsb::DeviceCache>(c, device);
+    *out = h.release();
+  });
+}
+
+int hps_cache_create_shared(const hps_cache_config* config, int device, hps_cache* share_with,
+                            hps_cache** out) {
+  return guarded([&] {
+    need(config != nullptr && out != nullptr && share_with != nullptr, "null argument");
+    hpsb::CacheConfig c;
+    c.slabset_count = config->slabset_count;
+    c.slabs_per_set = config->slabs_per_set;
+    c.dimension = config->dimension;
+    c.worker_pool_size = config->worker_pool_size;
+    c.tasks_per_worker = config->tasks_per_worker;
+    auto h = std::make_unique<hps_cache>();
+    h->impl = std::make_unique<hpsb::DeviceCache>(c, device, share_with->impl.get());
     *out = h.release();
   });
 }
@@ -628,6 +647,44 @@ int hps_engine_lookup_multi(hps_engine* const* engines, size_t count,
     }
   });
 }
+int hps_multi_create(hps_engine* const* engines, size_t count, size_t max_batch,
+                     hps_multi** out) {
+  return guarded([&] {
+    need(out != nullptr && (count == 0 || engines != nullptr), "null argument");
+    std::vector<hpsb::LookupEngine*> v(count);
+    for (size_t t = 0; t < count; ++t) {
+      need(engines[t] != nullptr, "null engine");
+      v[t] = engines[t]->impl.get();
+    }
+    auto h = std::make_unique<hps_multi>();
+    h->impl = std::make_unique<hpsb::MultiLookup>(std::move(v), max_batch);
+    *out = h.release();
+  });
+}
+
+int hps_multi_destroy(hps_multi* multi) {
+  return guarded([&] { delete multi; });
+}
+
+int hps_multi_lookup(hps_multi* multi, const uint64_t* const* keys, const size_t* n,
+                     float* const* out, uint8_t* const* miss_flags,
+                     hps_lookup_outcome* outcomes) {
+  return guarded([&] {
+    need(multi && keys && n && out && miss_flags, "null argument");
+    const size_t T = multi->impl ? multi->impl->tables() : 0;
+    std::vector<hpsb::LookupOutcome> o(T);
+    multi->impl->lookup(keys, n, out, miss_flags, o.data());
+    if (outcomes) {
+      for (size_t t = 0; t < T; ++t) {
+        outcomes[t].sync_branch = o[t].sync_branch ? 1 : 0;
+        outcomes[t].unique_hit_rate = o[t].unique_hit_rate;
+        outcomes[t].unique_count = o[t].unique_count;
+        outcomes[t].defaults_returned = o[t].defaults_returned;
+      }
+    }
+  });
+}
+
 int hps_engine_drain_async(hps_engine* engine) {
   return guarded([&] { engine->impl->drain_async(); });
 }

@@ -32,7 +32,8 @@ int keys_per_warp_for(uint32_t tasks_per_worker) {
 }
 }  // namespace
 
-DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device_(device) {
+DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* share_stream_with)
+    : cfg_(cfg), device_(device) {
   // same validation, same messages as slab_cache.cpp:18-29
   if (cfg.slabset_count == 0) throw invalid_argument("slabset_count must be positive");
   if (cfg.slabs_per_set == 0) throw invalid_argument("slabs_per_set must be positive");
@@ -44,7 +45,17 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device) : cfg_(cfg), device
     throw invalid_argument("cache capacity must stay below 2^32 slots per replica");
   keys_per_warp_ = keys_per_warp_for(std::max<uint32_t>(1, cfg.tasks_per_worker));
   DeviceGuard g(device_);
-  HPSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  if (share_stream_with != nullptr) {
+    // a cache group: several tables' caches ordered on one stream (the
+    // multi-table lookup runs them in one launch)
+    if (share_stream_with->device_ != device)
+      throw invalid_argument("caches sharing a stream must be on the same device");
+    stream_holder_ = share_stream_with->stream_holder_;
+  } else {
+    stream_holder_ = std::make_shared<StreamHolder>();
+    HPSB_CUDA(cudaStreamCreateWithFlags(&stream_holder_->s, cudaStreamNonBlocking));
+  }
+  stream_ = stream_holder_->s;
   HPSB_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
   HPSB_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
   const uint64_t slabs = cfg.slabset_count * cfg.slabs_per_set;
@@ -96,7 +107,7 @@ DeviceCache::~DeviceCache() {
   cudaFree(winner_);
   cudaEventDestroy(ev_in_);
   cudaEventDestroy(ev_out_);
-  cudaStreamDestroy(stream_);
+  stream_holder_.reset();  // the last cache of a group destroys the stream
 }
 
 void DeviceCache::ensure_scan_tiles(uint64_t tiles) {
@@ -218,7 +229,8 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   // programmatic dependent of the previous lookup when nothing else was
   // enqueued in between (the kernel orders itself against it)
   static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
-  const bool chain = last_op_lookup_ && !no_pdl;
+  // (never inside a cache group: other caches' work shares the stream)
+  const bool chain = last_op_lookup_ && !no_pdl && stream_holder_.use_count() == 1;
   LookupView v = lookup_next_view(lws_, chain);
   v.marks = lookup_marks_locked() + uint64_t(lws_.last) * capacity_slots();
   static const bool tracing = std::getenv("HPSB_TRACE") != nullptr;

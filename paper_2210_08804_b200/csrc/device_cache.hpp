@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -30,9 +31,18 @@ struct CacheConfig {
 
 enum MemKind : int { kHostMem = 0, kDeviceMem = 1 };
 
+struct StreamHolder {
+  cudaStream_t s = nullptr;
+  ~StreamHolder() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
 class DeviceCache {
  public:
-  DeviceCache(const CacheConfig& cfg, int device);
+  // share_stream_with: join another cache's stream (a cache group on one
+  // device, e.g. the tables of one model); null = a stream of its own.
+  DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* share_stream_with = nullptr);
   ~DeviceCache();
   DeviceCache(const DeviceCache&) = delete;
   DeviceCache& operator=(const DeviceCache&) = delete;
@@ -130,6 +140,7 @@ class DeviceCache {
   // true while the last operation enqueued on stream_ is a lookup kernel
   // (the next lookup may then launch as its programmatic dependent)
   bool last_op_lookup_ = false;
+  std::shared_ptr<StreamHolder> stream_holder_;
   // unique-hit marks of the lookup kernels: kLookupViews arrays of one u64
   // per slot (lazily allocated; see LookupView::marks)
   unsigned long long* marks_ = nullptr;

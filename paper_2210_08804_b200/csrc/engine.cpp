@@ -559,6 +559,260 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   }
 }
 
+void LookupEngine::finish_group(const GroupResult& r, LookupOutcome* outcome) {
+  const uint32_t d = dim_;
+  const uint64_t n_unique = r.uh + r.um;
+  // lookup_engine.cpp:148-153
+  const double h = n_unique == 0 ? 1.0 : 1.0 - double(r.um) / double(n_unique);
+  const bool sync_branch = h < cfg_.hit_rate_threshold;
+  TierCounters counters;
+  uint64_t defaults = 0;
+  DeviceGuard g(cache_->device());
+  cudaStream_t st = cache_->stream();
+  if (sync_branch) {
+    Workspace* ws = pool_.acquire();
+    struct Release {
+      WorkspacePool& p;
+      Workspace* w;
+      ~Release() { p.release(w); }
+    } rel{pool_, ws};
+    ws->wait_idle();
+    ws->ensure(std::max<uint64_t>(r.um, 1), d, st);
+    size_t nf = 0;
+    defaults = fetch_and_upload(*ws, r.miss_keys, r.um, &counters, &nf);
+    if (nf > 0) {
+      std::lock_guard<std::mutex> lk(cache_->mutex());
+      for (uint64_t k = 0; k < r.um; ++k) ws->h_row_of_claim[r.order[k]] = ws->h_row_of[k];
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, r.um * 4,
+                                cudaMemcpyHostToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                cudaMemcpyHostToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                cudaMemcpyHostToDevice, st));
+      cache_->note_stream_op();
+      launch_lookup_scatter(r.n, d, r.d_flags, r.v, ws->d_row_of, ws->d_staged, r.d_out, st);
+      cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+      HPSB_CUDA(cudaMemcpyAsync(r.out, r.d_out, r.n * uint64_t(d) * 4, cudaMemcpyDeviceToHost,
+                                st));
+      HPSB_CUDA(cudaMemcpyAsync(r.flags, r.d_flags, r.n, cudaMemcpyDeviceToHost, st));
+    }
+    HPSB_CUDA(cudaEventRecord(ws->done, st));
+    HPSB_CUDA(cudaEventSynchronize(ws->done));
+  } else {
+    defaults = r.um;
+  }
+  last_async_.store(!sync_branch, std::memory_order_relaxed);
+  if (outcome) {
+    outcome->sync_branch = sync_branch;
+    outcome->unique_hit_rate = h;
+    outcome->unique_count = n_unique;
+    outcome->defaults_returned = defaults;
+  }
+  {
+    std::lock_guard<std::mutex> lk(stats_mu_);
+    stats_.queries += 1;
+    stats_.queried_keys += r.n;
+    stats_.unique_keys += n_unique;
+    stats_.cache_hits += r.uh;
+    stats_.cache_misses += r.um;
+    stats_.defaults_returned += defaults;
+    if (sync_branch) {
+      stats_.sync_batches += 1;
+      stats_.vdb_hits += counters.vdb_hits;
+      stats_.pdb_hits += counters.cold_hits;
+      stats_.tier_missing += counters.missing;
+    } else {
+      stats_.async_batches += 1;
+    }
+  }
+  if (!sync_branch && r.um > 0) {
+    Workspace* ws = pool_.acquire();
+    try {
+      ws->wait_idle();
+      ws->ensure(r.um, d, st);
+      ws->missing_keys.assign(r.miss_keys, r.miss_keys + r.um);
+    } catch (...) {
+      pool_.release(ws);
+      throw;
+    }
+    {
+      std::lock_guard<std::mutex> lk(q_mu_);
+      queue_.push_back(AsyncTask{ws});
+    }
+    q_cv_.notify_one();
+  }
+}
+
+// ------------------------------------------------------------ multi-table --
+namespace {
+inline uint64_t a256m(uint64_t v) { return (v + 255) / 256 * 256; }
+}  // namespace
+
+MultiLookup::MultiLookup(std::vector<LookupEngine*> engines, uint64_t max_batch)
+    : eng_(std::move(engines)), maxb_(std::max<uint64_t>(max_batch, 1)) {
+  if (eng_.empty()) throw invalid_argument("multi-table lookup needs at least one engine");
+  const DeviceCache* c0 = eng_[0]->cache();
+  bool all8 = true, all4 = true;
+  for (auto* e : eng_) {
+    if (e == nullptr) throw invalid_argument("null engine");
+    if (e->cache()->stream() != c0->stream() || e->cache()->device() != c0->device())
+      throw invalid_argument("multi-table lookup needs the tables' caches in one cache group");
+    all8 &= e->dim() % 8 == 0;
+    all4 &= e->dim() % 4 == 0;
+  }
+  for (size_t i = 0; i < eng_.size(); ++i)
+    for (size_t j = i + 1; j < eng_.size(); ++j)
+      if (eng_[i]->cache() == eng_[j]->cache())
+        throw invalid_argument("multi-table lookup needs one cache per table");
+  ch_ = all8 ? 8 : (all4 ? 4 : 1);
+  const uint64_t T = eng_.size();
+  DeviceGuard g(c0->device());
+  cudaStream_t st = c0->stream();
+  uint64_t rows = 0;
+  for (auto* e : eng_) rows += maxb_ * e->dim();
+  // device: [desc][keys][counts][flags][claim keys][claim firsts][rows]
+  uint64_t o = 0;
+  d_desc_ = o;
+  o += a256m(T * sizeof(TableLookup));
+  d_keys_ = o;
+  o += a256m(T * maxb_ * 8);
+  d_counts_ = o;
+  o += a256m(T * 16);
+  d_flags_ = o;
+  o += a256m(T * maxb_ + 32 * T);
+  d_ckeys_ = o;
+  o += a256m(T * maxb_ * 8);
+  d_cfirsts_ = o;
+  o += a256m(T * maxb_ * 4);
+  d_rows_ = o;
+  o += a256m(rows * 4 + 32 * T);
+  dev_.ensure(o, st);
+  host_.ensure(o);
+  h_rows_ = d_rows_;
+  const uint64_t sbytes = lookup_scratch_bytes(maxb_);
+  char* sp = static_cast<char*>(scratch_dev_.ensure(a256m(sbytes) * T, st));
+  HPSB_CUDA(cudaMemsetAsync(sp, 0, a256m(sbytes) * T, st));
+  for (uint64_t t = 0; t < T; ++t) ls_.push_back(lookup_scratch_carve(sp + t * a256m(sbytes), maxb_));
+  HPSB_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
+  HPSB_CUDA(cudaStreamSynchronize(st));
+}
+
+MultiLookup::~MultiLookup() {
+  if (done_) {
+    cudaEventSynchronize(done_);
+    cudaEventDestroy(done_);
+  }
+}
+
+void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* const* out,
+                         uint8_t* const* flags, LookupOutcome* outcomes) {
+  std::lock_guard<std::mutex> lk(mu_);
+  const uint64_t T = eng_.size();
+  for (uint64_t t = 0; t < T; ++t)
+    if (n[t] > maxb_) throw invalid_argument("multi-table batch exceeds the group's max batch");
+  DeviceCache* c0 = eng_[0]->cache();
+  DeviceGuard g(c0->device());
+  cudaStream_t st = c0->stream();
+  char* hb = static_cast<char*>(host_.get());
+  char* db = static_cast<char*>(dev_.get());
+  auto* desc = reinterpret_cast<TableLookup*>(hb + d_desc_);
+  auto* hkeys = reinterpret_cast<uint64_t*>(hb + d_keys_);
+  // packed per-call offsets: keys / flags / claims by position, rows by float
+  std::vector<uint64_t> koff(T + 1, 0), roff(T + 1, 0);
+  for (uint64_t t = 0; t < T; ++t) {
+    koff[t + 1] = koff[t] + n[t];
+    roff[t + 1] = roff[t] + n[t] * eng_[t]->dim() + 7;  // keep 32 B alignment
+    roff[t + 1] &= ~7ull;
+  }
+  uint32_t blocks = 0;
+  std::vector<LookupView> views(T);
+  for (uint64_t t = 0; t < T; ++t) {
+    DeviceCache* c = eng_[t]->cache();
+    std::memcpy(hkeys + koff[t], keys[t], n[t] * 8);
+    std::lock_guard<std::mutex> clk(c->mutex());
+    const uint64_t stamp = c->bump_clock();  // query ticks even when empty
+    c->note_stream_op();
+    LookupView v = lookup_next_view(ls_[t], false);
+    v.marks = c->lookup_marks_locked();
+    v.list_keys = reinterpret_cast<uint64_t*>(db + d_ckeys_) + koff[t];
+    v.list_firsts = reinterpret_cast<uint32_t*>(db + d_cfirsts_) + koff[t];
+    v.counts_out = reinterpret_cast<unsigned long long*>(db + d_counts_) + 2 * t;
+    views[t] = v;
+    TableLookup& tl = desc[t];
+    tl.c = c->dev();
+    tl.keys = reinterpret_cast<const uint64_t*>(db + d_keys_) + koff[t];
+    tl.n = n[t];
+    tl.out = reinterpret_cast<float*>(db + d_rows_) + roff[t];
+    tl.flags = reinterpret_cast<uint8_t*>(db + d_flags_) + koff[t];
+    tl.default_row = eng_[t]->default_row();
+    tl.stamp = stamp;
+    tl.v = v;
+    tl.block_begin = blocks;
+    tl.nblocks = uint32_t((n[t] + kMultiBlockPositions - 1) / kMultiBlockPositions);
+    blocks += tl.nblocks;
+  }
+  // one H2D (descriptors + packed keys), one launch
+  HPSB_CUDA(cudaMemcpyAsync(db + d_desc_, hb + d_desc_, (d_keys_ - d_desc_) + koff[T] * 8,
+                            cudaMemcpyHostToDevice, st));
+  launch_lookup_multi(reinterpret_cast<const TableLookup*>(db + d_desc_), uint32_t(T), blocks,
+                      ch_, st);
+  // one D2H each: counts, flags, claims (whole packed regions), rows
+  auto d2h = [&](uint64_t off, uint64_t bytes) {
+    if (bytes) HPSB_CUDA(cudaMemcpyAsync(hb + off, db + off, bytes, cudaMemcpyDeviceToHost, st));
+  };
+  d2h(d_counts_, T * 16);
+  d2h(d_flags_, koff[T]);
+  d2h(d_ckeys_, koff[T] * 8);
+  d2h(d_cfirsts_, koff[T] * 4);
+  // rows: small batches in one packed copy (+ host scatter); large ones
+  // straight into each table's output (no extra host copy of big rows)
+  const bool packed_rows = roff[T] * 4 <= kPackedRowBytes;
+  if (packed_rows) {
+    d2h(d_rows_, roff[T] * 4);
+  } else {
+    for (uint64_t t = 0; t < T; ++t)
+      if (n[t])
+        HPSB_CUDA(cudaMemcpyAsync(out[t], db + d_rows_ + roff[t] * 4,
+                                  n[t] * uint64_t(eng_[t]->dim()) * 4, cudaMemcpyDeviceToHost, st));
+  }
+  HPSB_CUDA(cudaEventRecord(done_, st));
+  HPSB_CUDA(cudaEventSynchronize(done_));
+  const auto* hcounts = reinterpret_cast<const unsigned long long*>(hb + d_counts_);
+  const auto* hflags = reinterpret_cast<const uint8_t*>(hb + d_flags_);
+  const auto* hck = reinterpret_cast<const uint64_t*>(hb + d_ckeys_);
+  const auto* hcf = reinterpret_cast<const uint32_t*>(hb + d_cfirsts_);
+  const auto* hrows = reinterpret_cast<const float*>(hb + d_rows_);
+  std::exception_ptr first_error;
+  for (uint64_t t = 0; t < T; ++t) {
+    try {
+      const uint32_t d = eng_[t]->dim();
+      if (packed_rows) std::memcpy(out[t], hrows + roff[t], n[t] * uint64_t(d) * 4);
+      std::memcpy(flags[t], hflags + koff[t], n[t]);
+      LookupEngine::GroupResult r;
+      r.n = n[t];
+      r.uh = n[t] ? hcounts[2 * t] : 0;
+      r.um = n[t] ? hcounts[2 * t + 1] : 0;
+      order_.resize(r.um);
+      miss_.resize(r.um);
+      for (uint32_t e = 0; e < r.um; ++e) order_[e] = e;
+      const uint32_t* fp = hcf + koff[t];
+      std::sort(order_.begin(), order_.end(), [fp](uint32_t a, uint32_t b) { return fp[a] < fp[b]; });
+      for (uint64_t k = 0; k < r.um; ++k) miss_[k] = hck[koff[t] + order_[k]];
+      r.miss_keys = miss_.data();
+      r.order = order_.data();
+      r.v = views[t];
+      r.d_out = reinterpret_cast<float*>(db + d_rows_) + roff[t];
+      r.d_flags = reinterpret_cast<uint8_t*>(db + d_flags_) + koff[t];
+      r.out = out[t];
+      r.flags = flags[t];
+      eng_[t]->finish_group(r, outcomes ? outcomes + t : nullptr);
+    } catch (...) {
+      if (!first_error) first_error = std::current_exception();
+    }
+  }
+  if (first_error) std::rethrow_exception(first_error);
+}
+
 void LookupEngine::async_loop() {
   for (;;) {
     AsyncTask task;

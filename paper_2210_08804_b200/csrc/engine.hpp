@@ -151,6 +151,28 @@ class LookupEngine {
   void drain_async();
   EngineStats stats() const;
   WorkspacePool& pool() { return pool_; }
+  DeviceCache* cache() const { return cache_; }
+  uint32_t dim() const { return dim_; }
+  const float* default_row() const { return d_default_; }
+
+  // One table of a MultiLookup: its device part ran in the group launch and
+  // the counts, the claims (sorted to the reference's miss order) and the
+  // rows are already on the host (`out`/`flags`, user memory). Applies the
+  // hit-rate switch, the miss path (sync: fetch, scatter into the table's
+  // device rows d_out with view `v`, replace, rows copied back; async: the
+  // background fill) and the stats -- exactly LookupEngine::finish's rules.
+  struct GroupResult {
+    size_t n = 0;
+    uint64_t uh = 0, um = 0;
+    const uint64_t* miss_keys = nullptr;  // um keys, reference order
+    const uint32_t* order = nullptr;      // claim index of each miss (sync scatter)
+    LookupView v;
+    float* d_out = nullptr;
+    uint8_t* d_flags = nullptr;
+    float* out = nullptr;
+    uint8_t* flags = nullptr;
+  };
+  void finish_group(const GroupResult& r, LookupOutcome* outcome);
 
  private:
   // claims copied back speculatively with the counts (one round trip when a
@@ -207,6 +229,42 @@ class LookupEngine {
   size_t active_ = 0;
   bool stopping_ = false;
   std::vector<std::thread> workers_;
+};
+
+// Several tables whose caches form one cache group (one stream): a lookup
+// of all of them is ONE H2D (descriptors + packed keys), ONE kernel
+// (k_lookup_tag_multi), one D2H of every table's counts / flags / first
+// claims, one D2H of the rows, and one host wait -- then each table's
+// hit-rate switch and miss path (LookupEngine::finish_group). The small-batch
+// latency of a many-table model is then one round trip, not one per table.
+class MultiLookup {
+ public:
+  MultiLookup(std::vector<LookupEngine*> engines, uint64_t max_batch);
+  ~MultiLookup();
+  MultiLookup(const MultiLookup&) = delete;
+  MultiLookup& operator=(const MultiLookup&) = delete;
+  void lookup(const uint64_t* const* keys, const size_t* n, float* const* out,
+              uint8_t* const* flags, LookupOutcome* outcomes);
+  size_t tables() const { return eng_.size(); }
+
+ private:
+  static constexpr uint64_t kPackedRowBytes = 1 << 20;
+  std::vector<LookupEngine*> eng_;
+  uint64_t maxb_;
+  int ch_ = 1;
+  std::mutex mu_;
+  std::vector<LookupScratch> ls_;  // per table, its own views
+  DeviceBuffer scratch_dev_;
+  DeviceBuffer dev_;
+  PinnedBuffer host_;
+  cudaEvent_t done_ = nullptr;
+  // layout (offsets in the device / host blocks)
+  uint64_t d_desc_ = 0, d_keys_ = 0, d_counts_ = 0, d_flags_ = 0, d_ckeys_ = 0, d_cfirsts_ = 0,
+           d_rows_ = 0;
+  std::vector<uint64_t> row_off_;  // per table, in floats from d_rows_
+  uint64_t h_rows_ = 0;
+  std::vector<uint32_t> order_;
+  std::vector<uint64_t> miss_;
 };
 
 }  // namespace hpsb

@@ -135,6 +135,24 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
                              const LookupView& v, bool after_lookup, cudaStream_t st);
+// One table of a multi-table lookup launch (device-resident descriptor).
+struct TableLookup {
+  CacheDev c;
+  const uint64_t* keys;
+  uint64_t n;
+  float* out;
+  uint8_t* flags;
+  const float* default_row;
+  uint64_t stamp;
+  LookupView v;
+  uint32_t block_begin;  // first block of this table in the launch
+  uint32_t nblocks;      // ceil(n / 256)
+};
+constexpr uint32_t kMultiBlockPositions = 256;  // positions per block of the multi kernel
+// One launch for `count` tables (descriptors in device memory, block ranges
+// consecutive); ch = row chunk width valid for every table (8, 4 or 1).
+void launch_lookup_multi(const TableLookup* d_tables, uint32_t count, uint32_t total_blocks,
+                         int ch, cudaStream_t st);
 void launch_lookup_scatter(uint64_t n, uint32_t d, uint8_t* flags, const LookupView& v,
                            const int32_t* row_of_claim, const float* staged, float* out,
                            cudaStream_t st);

@@ -232,12 +232,12 @@ __device__ void finish_counts(const LookupView& v) {
 
 // Ticket `t` (0 = claims, 1 = counts): true in every thread of the block
 // that got there last.
-__device__ __forceinline__ bool last_block(const LookupView& v, int t) {
+__device__ __forceinline__ bool last_block(const LookupView& v, int t, uint32_t nblocks) {
   __shared__ uint32_t s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(v.done + t, 1u) == gridDim.x - 1 ? 1u : 0u;
+    s_last = atomicAdd(v.done + t, 1u) == nblocks - 1 ? 1u : 0u;
   }
   __syncthreads();
   if (s_last) __threadfence();
@@ -469,10 +469,10 @@ __global__ void __launch_bounds__(kThreads)
       v.claim_of_slot[tslot] = e;
     }
   }
-  if (last_block(v, 0)) finish_claims(v);
+  if (last_block(v, 0, gridDim.x)) finish_claims(v);
   if (valid) copy_row();
   warp_add_counts(v, uh, claimed ? 1u : 0u, blockIdx.x * kWarps + (threadIdx.x >> 5));
-  if (last_block(v, 1)) finish_counts(v);
+  if (last_block(v, 1, gridDim.x)) finish_counts(v);
 }
 
 // ====================================================== lane-per-position --
@@ -516,12 +516,16 @@ __device__ __forceinline__ void warp_copy_rows(const CacheDev& c, uint32_t res, 
 // batch repeats its top key in ~19% of positions). The register budget is
 // capped so the next lookup's blocks can be resident during this one's
 // copies (2 x 1024 threads per SM).
+// The body of one table's lookup for block `blk` of its `nblocks` blocks
+// (the single-table kernel passes blockIdx / gridDim; the multi-table
+// kernel the block's rank within its table).
 template <int CH, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
-    k_lookup_tag(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
-                 float* __restrict__ out, uint8_t* __restrict__ flags,
-                 const float* __restrict__ default_row, uint64_t stamp, LookupView v,
-                 uint32_t skip) {
+__device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* __restrict__ keys,
+                                            uint64_t n, float* __restrict__ out,
+                                            uint8_t* __restrict__ flags,
+                                            const float* __restrict__ default_row,
+                                            uint64_t stamp, const LookupView& v, uint32_t skip,
+                                            uint32_t blk, uint32_t nblocks) {
   constexpr int kThreadsB = WARPS * 32;
   constexpr uint32_t kSetSize = 2 * kThreadsB;  // power of two for WARPS in {2, 4, 8, 16}
   __shared__ uint32_t s_stamped[kSetSize];
@@ -531,7 +535,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   __syncthreads();
   trace_min(v, 0, false);
   const uint32_t lane = lane_id();
-  const uint64_t base = (uint64_t(blockIdx.x) * kThreadsB + threadIdx.x) & ~31ull;
+  const uint64_t base = (uint64_t(blk) * kThreadsB + threadIdx.x) & ~31ull;
   const uint64_t pos = base + lane;
   const bool valid = pos < n;
   // ---- A: probe, claims, flags (independent of the previous call) ----
@@ -553,7 +557,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   }
   // ---- the last block to have made its claims completes the claim list
   // (overlapping the other blocks' copies) ----
-  if (last_block(v, 0)) {
+  if (last_block(v, 0, nblocks)) {
     trace_min(v, 6, false);
     finish_claims(v);
     trace_min(v, 7, false);
@@ -566,13 +570,54 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
   if (!(skip & kSkipCopy))
     warp_copy_rows<CH, CH == 8 ? 4 : 8>(c, res, nrows, default_row, out + base * c.d);
-  warp_add_counts(v, uh, um, blockIdx.x * WARPS + (threadIdx.x >> 5));
+  warp_add_counts(v, uh, um, blk * WARPS + (threadIdx.x >> 5));
   if (v.trace) {
     __syncthreads();
     trace_min(v, 4, false);
     trace_min(v, 5, true);
   }
-  if (last_block(v, 1)) finish_counts(v);
+  if (last_block(v, 1, nblocks)) finish_counts(v);
+}
+
+template <int CH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
+    k_lookup_tag(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                 float* __restrict__ out, uint8_t* __restrict__ flags,
+                 const float* __restrict__ default_row, uint64_t stamp, LookupView v,
+                 uint32_t skip) {
+  lookup_body<CH, WARPS>(c, keys, n, out, flags, default_row, stamp, v, skip, blockIdx.x,
+                         gridDim.x);
+}
+
+// Several tables (caches) in ONE launch: block b belongs to the table whose
+// [block_begin, block_begin + nblocks) range holds b; each table runs the
+// single-table body on its own blocks, views and tickets.
+template <int CH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
+    k_lookup_tag_multi(const TableLookup* __restrict__ tables, uint32_t count) {
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    while (t + 1 < count && tables[t + 1].block_begin <= blockIdx.x) ++t;
+    s_t = t;
+  }
+  __syncthreads();
+  const TableLookup& tl = tables[s_t];
+  lookup_body<CH, WARPS>(tl.c, tl.keys, tl.n, tl.out, tl.flags, tl.default_row, tl.stamp, tl.v, 0u,
+                         blockIdx.x - tl.block_begin, tl.nblocks);
+}
+
+void launch_lookup_multi(const TableLookup* d_tables, uint32_t count, uint32_t total_blocks,
+                         int ch, cudaStream_t st) {
+  if (total_blocks == 0) return;
+  constexpr int W = 8;
+  if (ch == 8)
+    k_lookup_tag_multi<8, W><<<total_blocks, W * 32, 0, st>>>(d_tables, count);
+  else if (ch == 4)
+    k_lookup_tag_multi<4, W><<<total_blocks, W * 32, 0, st>>>(d_tables, count);
+  else
+    k_lookup_tag_multi<1, W><<<total_blocks, W * 32, 0, st>>>(d_tables, count);
+  check_launch("lookup_multi", 1);
 }
 
 // --------------------------------------------------------------- launch --

@@ -403,3 +403,55 @@ def test_native_refresh_tier_fault_keeps_finished_batches():
     got = got.reshape(-1, d)
     assert got[:200].tobytes() == row_values(resident[:200], d, 5).tobytes()
     assert got[200:].tobytes() == row_values(resident[200:], d, 0).tobytes()
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16, 16), (8, 12, 16, 20, 4), (3, 5)])
+def test_group_multi_lookup_one_launch_equals_per_table_lookups(dims):
+    """MultiLookup (cache group, ONE kernel launch for all tables) must give
+    every table exactly what a per-table hps_engine_lookup gives on an
+    identical twin: rows, flags, outcomes, cache contents, stats -- with
+    different dims per table, ragged and empty per-table batches, and both
+    the sync and the async branch."""
+    T_ = len(dims)
+
+    def build(grouped):
+        vdb = hps.VolatileStore(4)
+        caches, engines = [], []
+        for t, d in enumerate(dims):
+            table = T(f"g{t}", d)
+            vdb.register_table(table)
+            keys = np.arange(t * 100000, t * 100000 + 9000, dtype=np.uint64)
+            vdb.insert(table.name, keys, row_values(keys, d, t))
+            cfg = hps.SlabCacheConfig(slabset_count=32, slabs_per_set=2, dimension=d)
+            c = hps.SlabCache(cfg, share_stream_with=caches[0] if (grouped and caches) else None)
+            caches.append(c)
+            engines.append(hps.LookupEngine(table, c, vdb, None,
+                                            hps.EngineConfig(hit_rate_threshold=0.55,
+                                                             default_vector=[1.5 + t] * d)))
+        return vdb, caches, engines
+
+    va, ca, ea = build(True)
+    vb, cb, eb = build(False)
+    m = hps.MultiLookup(ea, max_batch=4096)
+    for r in range(6):
+        ns = [(700 + 311 * t + 97 * r) % 4097 for t in range(T_)]
+        if r == 2:
+            ns[0] = 0
+        batches = [hps.powerlaw_sample(1.1, 11000, t, 70 * r + t, ns[t]) + np.uint64(t * 100000)
+                   for t in range(T_)]
+        got = m.lookup(batches)
+        for t in range(T_):
+            o = hps.LookupOutcome()
+            want = eb[t].lookup(batches[t], o)
+            assert got[t].vectors.tobytes() == want.vectors.tobytes(), (r, t)
+            assert (got[t].miss_flags == want.miss_flags).all(), (r, t)
+        for e in ea + eb:
+            e.drain_async()
+    for t in range(T_):
+        assert ca[t].dump_all().tolist() == cb[t].dump_all().tolist()
+        sa, sb = ea[t].stats(), eb[t].stats()
+        assert sa == sb, (t, sa, sb)
+        ca[t].check_invariants()
+    m.close()
+    for e in ea + eb:
+        e.close()

@@ -13,7 +13,8 @@ whole table in the host volatile DB (the miss path), threshold 0.8. Rows are
 synthetic (a hash of key and column). Per batch size: p50 / p99 latency of
 one table lookup (one table at a time), and of a 26-table sample batch --
 tables looked up concurrently from a thread pool (one engine per table), and
-all 26 through one hps_engine_lookup_multi call -- plus samples/s. Warm-up fills the caches to steady state first.
+all 26 through one hps_engine_lookup_multi call, and all 26 through the
+cache group's one-launch MultiLookup (hps_multi_lookup) -- plus samples/s. Warm-up fills the caches to steady state first.
 """
 from __future__ import annotations
 
@@ -60,8 +61,10 @@ def main():
         for i in range(0, K, 1 << 20):
             k = base + np.arange(i, min(K, i + (1 << 20)), dtype=np.uint64)
             vdb.insert(name, k, bench.table_rows(k, d))
+        # one cache group (one stream) for the model's tables
         c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d,
-                                              worker_pool_size=8, tasks_per_worker=8), device=0)
+                                              worker_pool_size=8, tasks_per_worker=8), device=0,
+                          share_stream_with=caches[0] if caches else None)
         e = hps.LookupEngine(table, c, vdb, None,
                              hps.EngineConfig(hit_rate_threshold=0.8, workspace_pool_size=4,
                                               async_worker_count=2, max_batch=max(sizes)))
@@ -80,6 +83,7 @@ def main():
         return np.ascontiguousarray(perm[np.minimum(np.searchsorted(cdf, rng.random(n)), K - 1)])
 
     maxb = max(sizes)
+    group = hps.MultiLookup(engines, max_batch=maxb)
     pk = [torch.empty(maxb, dtype=torch.int64).pin_memory() for _ in range(T)]
     po = [torch.empty(maxb * d).pin_memory() for _ in range(T)]
     pf = [torch.empty(maxb, dtype=torch.uint8).pin_memory() for _ in range(T)]
@@ -132,11 +136,23 @@ def main():
                                                [p.data_ptr() for p in po],
                                                [p.data_ptr() for p in pf], hps.HPS_MEM_HOST)
             multi_lat.append(time.perf_counter() - t0)
+        group_lat = []
+        for e in engines:
+            e.drain_async()
+        for r in range(max(reps, 10)):  # the cache group: one launch for all tables
+            bs = batches[r % len(batches)]
+            for t in range(T):
+                pk[t][:n].copy_(torch.from_numpy(bs[t].view(np.int64)))
+            t0 = time.perf_counter()
+            group.lookup_ptrs([p.data_ptr() for p in pk], [n] * T, [p.data_ptr() for p in po],
+                              [p.data_ptr() for p in pf])
+            group_lat.append(time.perf_counter() - t0)
         for e in engines:
             e.drain_async()
         lat = np.array(lat) * 1e6
         sl = np.array(sample_lat) * 1e6
         ml = np.array(multi_lat) * 1e6
+        gl = np.array(group_lat) * 1e6
         result["per_batch"].append({
             "batch": n, "table_lookup_p50_us": float(np.median(lat)),
             "table_lookup_p99_us": float(np.percentile(lat, 99)),
@@ -145,6 +161,9 @@ def main():
             "samples_per_s": n / (np.median(sl) * 1e-6),
             "sample_batch_26_tables_lookup_multi_p50_us": float(np.median(ml)),
             "samples_per_s_lookup_multi": n / (np.median(ml) * 1e-6),
+            "sample_batch_26_tables_group_one_launch_p50_us": float(np.median(gl)),
+            "sample_batch_26_tables_group_one_launch_p99_us": float(np.percentile(gl, 99)),
+            "samples_per_s_group": n / (np.median(gl) * 1e-6),
             "mean_unique_hit_rate": float(np.mean(hits))})
         print(json.dumps(result["per_batch"][-1]), file=sys.stderr)
     stats = [e.stats() for e in engines]
@@ -154,6 +173,7 @@ def main():
         "vdb_hits": int(sum(s.vdb_hits for s in stats)),
         "defaults_returned": int(sum(s.defaults_returned for s in stats))}
     print(json.dumps(result))
+    group.close()
     for e in engines:
         e.close()
 
