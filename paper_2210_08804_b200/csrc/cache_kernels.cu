@@ -363,23 +363,44 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
 __global__ void __launch_bounds__(256)
     k_update_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                    uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner,
-                   unsigned long long* written) {
+                   uint32_t* __restrict__ block_hits, uint32_t wait_at_end) {
   const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool valid = pos < n;
   const uint64_t key = valid ? keys[pos] : 0ull;
   const uint32_t res = lane_probe(c, key, valid);
   if (valid) slot_of[pos] = res;
   if (res != kNoSlot) atomicMax(winner + res, uint32_t(pos + 1));
+  // per-block hit count (no zeroed counter needed: every block writes its own)
+  __shared__ uint32_t s_hits;
+  if (threadIdx.x == 0) s_hits = 0;
+  __syncthreads();
   const uint32_t hits = __reduce_add_sync(0xFFFFFFFFu, res != kNoSlot ? 1u : 0u);
-  if (lane_id() == 0 && hits) atomicAdd(written, (unsigned long long)hits);
+  if (lane_id() == 0 && hits) atomicAdd(&s_hits, hits);
+  __syncthreads();
+  if (threadIdx.x == 0) block_hits[blockIdx.x] = s_hits;
+  // Launched as the programmatic dependent of a lookup (it only reads the
+  // probe structures, which lookups do not change): complete only after that
+  // lookup, so the row writes that follow never race its row reads.
+  if (wait_at_end) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 template <int CH>
 __global__ void __launch_bounds__(256)
     k_update_write(CacheDev c, const float* __restrict__ rows, uint64_t n,
-                   const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner) {
+                   const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner,
+                   const uint32_t* __restrict__ block_hits, uint32_t nblocks,
+                   unsigned long long* __restrict__ written) {
+  // the next lookup may launch now (it waits for this grid before its copies)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int U = CH == 8 ? 4 : 8;
   const uint32_t lane = lane_id();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    unsigned long long h = 0;
+    for (uint32_t b = threadIdx.x; b < nblocks; b += 32) h += block_hits[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+    if (threadIdx.x == 0) *written = h;
+  }
   const uint64_t base = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull;
   const uint64_t pos = base + lane;
   uint32_t slot = kNoSlot;
@@ -417,24 +438,39 @@ __global__ void __launch_bounds__(256)
   if (slot != kNoSlot) winner[slot] = 0u;
 }
 
+size_t update_scratch_bytes(uint64_t n) { return (n * 4 + 255) / 256 * 256 + ((n + 255) / 256) * 4; }
+
 void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
-                   uint32_t* slot_of, uint32_t* winner, unsigned long long* written,
-                   cudaStream_t st) {
-  cudaMemsetAsync(written, 0, 8, st);
+                   void* scratch, uint32_t* winner, unsigned long long* written,
+                   bool after_lookup, cudaStream_t st) {
   if (n == 0) {
+    cudaMemsetAsync(written, 0, 8, st);
     check_launch("update", 0);
     return;
   }
+  uint32_t* slot_of = static_cast<uint32_t*>(scratch);
+  uint32_t* block_hits = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) +
+                                                     (n * 4 + 255) / 256 * 256);
   const unsigned grid = unsigned((n + 255) / 256);
-  k_update_probe<<<grid, 256, 0, st>>>(c, keys, n, slot_of, winner, written);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = after_lookup ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_update_probe, c, keys, n, slot_of, winner, block_hits,
+                     uint32_t(after_lookup ? 1 : 0));
   const bool a32 = (reinterpret_cast<uintptr_t>(rows) % 32) == 0;
   const bool a16 = (reinterpret_cast<uintptr_t>(rows) % 16) == 0;
   if (c.d % 8 == 0 && a32)
-    k_update_write<8><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner);
+    k_update_write<8><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
   else if (c.d % 4 == 0 && a16)
-    k_update_write<4><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner);
+    k_update_write<4><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
   else
-    k_update_write<1><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner);
+    k_update_write<1><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
   check_launch("update", 2);
 }
 

@@ -126,21 +126,21 @@ void DeviceCache::ensure_scan_tiles(uint64_t tiles) {
 
 void DeviceCache::join_from(cudaStream_t user) {
   if (user == nullptr || user == stream_) return;
-  last_op_lookup_ = false;
+  mark_other_op();
   HPSB_CUDA(cudaEventRecord(ev_in_, user));
   HPSB_CUDA(cudaStreamWaitEvent(stream_, ev_in_, 0));
 }
 
 void DeviceCache::join_to(cudaStream_t user) {
   if (user == nullptr || user == stream_) return;
-  last_op_lookup_ = false;
+  mark_other_op();
   HPSB_CUDA(cudaEventRecord(ev_out_, stream_));
   HPSB_CUDA(cudaStreamWaitEvent(user, ev_out_, 0));
 }
 
 uint64_t DeviceCache::occupied() {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   DeviceGuard g(device_);
   HPSB_CUDA(cudaMemcpyAsync(h_small_ + 7, dev_.occupied, 8, cudaMemcpyDeviceToHost, stream_));
   HPSB_CUDA(cudaStreamSynchronize(stream_));
@@ -150,7 +150,7 @@ uint64_t DeviceCache::occupied() {
 size_t DeviceCache::query(const uint64_t* keys, size_t n, float* out, size_t out_len,
                           uint32_t* miss_pos, uint64_t* miss_keys, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   // one tick per call, before anything else (slab_cache.cpp:73-74)
   const uint64_t stamp = bump_clock();
   if (out_len != n * uint64_t(cfg_.dimension))
@@ -208,7 +208,7 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   DeviceGuard g(device_);
   join_from(user);
   if (n == 0) {
-    last_op_lookup_ = false;
+    mark_other_op();
     HPSB_CUDA(cudaMemsetAsync(counts, 0, 16, stream_));
     join_to(user);
     return;
@@ -222,7 +222,7 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     const uint64_t bytes = lookup_scratch_bytes(cap);
     void* b = lbuf_.ensure(bytes, stream_);
     HPSB_CUDA(cudaMemsetAsync(b, 0, bytes, stream_));
-    last_op_lookup_ = false;
+    mark_other_op();
     lws_ = lookup_scratch_carve(b, cap);
     lcap_ = cap;
   }
@@ -230,7 +230,9 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   // enqueued in between (the kernel orders itself against it)
   static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
   // (never inside a cache group: other caches' work shares the stream)
-  const bool chain = last_op_lookup_ && !no_pdl && stream_holder_.use_count() == 1;
+  const bool after_update = last_op_update_;
+  const bool chain = (last_op_lookup_ || last_op_update_) && !no_pdl &&
+                     stream_holder_.use_count() == 1;
   LookupView v = lookup_next_view(lws_, chain);
   v.marks = lookup_marks_locked() + uint64_t(lws_.last) * capacity_slots();
   static const bool tracing = std::getenv("HPSB_TRACE") != nullptr;
@@ -238,7 +240,7 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     if (trace_ == nullptr) {
       HPSB_CUDA(cudaMalloc(&trace_, kTraceRing * 64));
       HPSB_CUDA(cudaMemsetAsync(trace_, 0xFF, kTraceRing * 64, stream_));
-      last_op_lookup_ = false;
+      mark_other_op();
     }
     v.trace = trace_ + (trace_calls_++ % kTraceRing) * 8;
   }
@@ -253,13 +255,15 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
       cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (prof_start_) {
     HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
-    last_op_lookup_ = false;
+    mark_other_op();
   }
-  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, v, chain, stream_);
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, v, chain, stream_,
+                      /*wait_before_copy=*/after_update);
+  mark_other_op();
   last_op_lookup_ = true;
   if (prof_end_) {
     HPSB_CUDA(cudaEventRecordWithFlags(prof_end_, stream_, rec_flags));
-    last_op_lookup_ = false;
+    mark_other_op();
   }
   join_to(user);
 }
@@ -267,7 +271,7 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
 void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
                           size_t vectors_len, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   if (vectors_len != n * uint64_t(cfg_.dimension))
     throw invalid_argument("replace vector buffer has wrong size");
   const bool host = mem == kHostMem;
@@ -308,7 +312,7 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
 }
 
 void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const float* d_rows) {
-  last_op_lookup_ = false;
+  mark_other_op();
   if (n == 0) return;
   const uint64_t stamp = clock_.load(std::memory_order_relaxed);
   const uint64_t rs_bytes = replace_scratch_bytes(n);
@@ -319,7 +323,7 @@ void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const 
 size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
                            size_t vectors_len, int mem, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   if (vectors_len != n * uint64_t(cfg_.dimension))
     throw invalid_argument("update vector buffer has wrong size");
   if (n == 0) return 0;
@@ -327,9 +331,10 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
   DeviceGuard g(device_);
   const uint64_t d = cfg_.dimension;
   const bool host = mem == kHostMem;
-  const uint64_t bytes = align256(n * 4) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
+  const uint64_t ub = update_scratch_bytes(n);
+  const uint64_t bytes = align256(ub) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
   Carver cv{static_cast<char*>(scratch(bytes))};
-  uint32_t* slot_of = cv.take<uint32_t>(n);
+  void* scratch_u = cv.take<char>(ub);
   const uint64_t* d_keys = keys;
   const float* d_rows = vectors;
   if (host) {
@@ -342,7 +347,8 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
   } else {
     join_from(user);
   }
-  launch_update(dev_, d_keys, n, d_rows, slot_of, winner_, d_small_ + 2, stream_);
+  launch_update(dev_, d_keys, n, d_rows, scratch_u, winner_, d_small_ + 2, /*after_lookup=*/false,
+                stream_);
   HPSB_CUDA(cudaMemcpyAsync(h_small_ + 2, d_small_ + 2, 8, cudaMemcpyDeviceToHost, stream_));
   HPSB_CUDA(cudaStreamSynchronize(stream_));
   if (!host) join_to(user);
@@ -352,28 +358,36 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
 void DeviceCache::update_device(const uint64_t* keys, size_t n, const float* vectors,
                                 uint64_t* written, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
+  // right behind a lookup kernel: the probe overlaps that lookup (and
+  // completes after it); the next lookup may overlap this update the same way
+  const bool after_lookup = last_op_lookup_ && !no_pdl && stream_holder_.use_count() == 1 &&
+                            (user == nullptr || user == stream_);
+  mark_other_op();
   if (n >= (1ull << 32) - 1) throw invalid_argument("update batch too large");
   DeviceGuard g(device_);
   join_from(user);
+  bool chain = after_lookup;
   if (n > ucap_) {
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
-    ubuf_.ensure(align256(cap * 4) + 256, stream_);
+    ubuf_.ensure(align256(update_scratch_bytes(cap)) + 256, stream_);
     ucap_ = cap;
+    chain = false;  // (re)allocation enqueued work in between
   }
-  uint32_t* slot_of = static_cast<uint32_t*>(ubuf_.get());
   unsigned long long* w = written != nullptr
                               ? reinterpret_cast<unsigned long long*>(written)
                               : reinterpret_cast<unsigned long long*>(
-                                    static_cast<char*>(ubuf_.get()) + align256(ucap_ * 4));
-  launch_update(dev_, keys, n, vectors, slot_of, winner_, w, stream_);
+                                    static_cast<char*>(ubuf_.get()) +
+                                    align256(update_scratch_bytes(ucap_)));
+  launch_update(dev_, keys, n, vectors, ubuf_.get(), winner_, w, chain, stream_);
+  last_op_update_ = n > 0 && (user == nullptr || user == stream_);
   join_to(user);
 }
 
 size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, size_t cap) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   set_end = std::min<uint64_t>(set_end, cfg_.slabset_count);
   if (set_begin >= set_end) return 0;
   DeviceGuard g(device_);
@@ -397,7 +411,7 @@ unsigned long long* DeviceCache::lookup_marks_locked() {
     const uint64_t bytes = uint64_t(kLookupViews) * capacity_slots() * 8;
     HPSB_CUDA(cudaMalloc(&marks_, bytes));
     HPSB_CUDA(cudaMemsetAsync(marks_, 0, bytes, stream_));
-    last_op_lookup_ = false;
+    mark_other_op();
   }
   return marks_;
 }
@@ -405,7 +419,7 @@ unsigned long long* DeviceCache::lookup_marks_locked() {
 uint64_t DeviceCache::trace(unsigned long long* out) {
   std::lock_guard<std::mutex> lk(mu_);
   if (trace_ == nullptr) return 0;
-  last_op_lookup_ = false;
+  mark_other_op();
   DeviceGuard g(device_);
   HPSB_CUDA(cudaMemcpyAsync(out, trace_, kTraceRing * 64, cudaMemcpyDeviceToHost, stream_));
   HPSB_CUDA(cudaMemsetAsync(trace_, 0xFF, kTraceRing * 64, stream_));
@@ -418,7 +432,7 @@ uint64_t DeviceCache::trace(unsigned long long* out) {
 void DeviceCache::dump_device(uint64_t set_begin, uint64_t set_end, uint64_t* out,
                               uint64_t* n_out, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   set_end = std::min<uint64_t>(set_end, cfg_.slabset_count);
   DeviceGuard g(device_);
   join_from(user);
@@ -435,7 +449,7 @@ void DeviceCache::dump_device(uint64_t set_begin, uint64_t set_end, uint64_t* ou
 void DeviceCache::export_state(uint64_t* keys, uint64_t* counters, uint32_t* masks,
                                float* rows) {
   std::lock_guard<std::mutex> lk(mu_);
-  last_op_lookup_ = false;
+  mark_other_op();
   DeviceGuard g(device_);
   const uint64_t slabs = cfg_.slabset_count * cfg_.slabs_per_set;
   const uint64_t slots = slabs * 32ull;
@@ -459,7 +473,7 @@ void DeviceCache::check_invariants() {
   std::vector<uint8_t> tags(slots);
   {
     std::lock_guard<std::mutex> lk(mu_);
-    last_op_lookup_ = false;
+    mark_other_op();
     DeviceGuard g(device_);
     HPSB_CUDA(cudaMemcpyAsync(tags.data(), dev_.tags, slots, cudaMemcpyDeviceToHost, stream_));
     HPSB_CUDA(cudaStreamSynchronize(stream_));

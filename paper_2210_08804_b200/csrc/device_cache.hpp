@@ -101,7 +101,7 @@ class DeviceCache {
   std::mutex& mutex() { return mu_; }
   // Callers that enqueue their own work on stream() (the engine) call this
   // under mutex() so the next lookup does not chain onto a stale lookup.
-  void note_stream_op() { last_op_lookup_ = false; }
+  void note_stream_op() { mark_other_op(); }
   // Mark arrays of the lookup kernels (call under mutex()); array i at
   // + i * capacity_slots().
   unsigned long long* lookup_marks_locked();
@@ -140,6 +140,13 @@ class DeviceCache {
   // true while the last operation enqueued on stream_ is a lookup kernel
   // (the next lookup may then launch as its programmatic dependent)
   bool last_op_lookup_ = false;
+  // true while the last operation enqueued is an update's write kernel (the
+  // next lookup may chain behind it, waiting before its row copies)
+  bool last_op_update_ = false;
+  void mark_other_op() {
+    last_op_lookup_ = false;
+    last_op_update_ = false;
+  }
   std::shared_ptr<StreamHolder> stream_holder_;
   // unique-hit marks of the lookup kernels: kLookupViews arrays of one u64
   // per slot (lazily allocated; see LookupView::marks)

@@ -55,12 +55,16 @@ ReplaceScratch replace_scratch_carve(void* base, uint64_t n);
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st);
 
-// Update (slab_cache.cpp:109-125): slot_of = n u32 of scratch; winner = the
+// Update (slab_cache.cpp:109-125): scratch = update_scratch_bytes(n) of
+// device memory (per-position slots + per-block hit counts); winner = the
 // cache's per-slot u32 array (all-zero between calls); *written = number of
-// positions whose key is resident (device memory).
+// positions whose key is resident (device memory, no pre-zeroing needed).
+// after_lookup: the previous operation on `st` is a lookup kernel -> the
+// probe launches as its programmatic dependent (and completes after it).
+size_t update_scratch_bytes(uint64_t n);
 void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
-                   uint32_t* slot_of, uint32_t* winner, unsigned long long* written,
-                   cudaStream_t st);
+                   void* scratch, uint32_t* winner, unsigned long long* written,
+                   bool after_lookup, cudaStream_t st);
 
 void launch_dump(const CacheDev& c, uint64_t set_begin, uint64_t set_end, uint64_t* out,
                  unsigned long long* n_out, ScanState& scan, cudaStream_t st);
@@ -130,11 +134,14 @@ size_t lookup_scratch_bytes(uint64_t cap);
 LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
 // One launch per lookup (probe, claims, stamps, row gather / default rows,
 // and the call's completion by its last block). after_lookup: the previous
-// operation on `st` was a lookup kernel on the OTHER view -> launched as its
-// programmatic dependent. Returns the number of kernels launched.
+// operation on `st` was a lookup or update kernel -> launched as its
+// programmatic dependent; wait_before_copy (after an update): the rows are
+// read only once that update's grid has completed. Returns the number of
+// kernels launched.
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupView& v, bool after_lookup, cudaStream_t st);
+                             const LookupView& v, bool after_lookup, cudaStream_t st,
+                             bool wait_before_copy = false);
 // One table of a multi-table lookup launch (device-resident descriptor).
 struct TableLookup {
   CacheDev c;

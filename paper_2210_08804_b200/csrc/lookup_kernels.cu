@@ -75,6 +75,8 @@ constexpr uint32_t kCountLanes = 64;  // distributed (unique hit, unique miss) c
 // Diagnostic skip bits (HPSB_DIAG_SKIP, measurement only; results are wrong
 // with any bit set): 1 = recency exchange, 2 = miss claims, 4 = row copy.
 constexpr uint32_t kSkipStamp = 1, kSkipMiss = 2, kSkipCopy = 4;
+// not a diagnostic: set by the launcher when the lookup follows an update
+constexpr uint32_t kWaitBeforeCopy = 1u << 8;
 
 uint64_t view_bytes(uint64_t cap) {
   const uint64_t tcap = table_cap(cap);
@@ -162,6 +164,7 @@ __device__ __forceinline__ void spin_ge(const unsigned long long* p, unsigned lo
     if (global_ns() - t0 > 2000000000ull) __trap();
   }
 }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -567,6 +570,9 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
   if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
   const uint32_t uh = stamp_it ? stamp_slot(c, v, res, stamp) : 0u;
+  // behind an update (programmatic dependent launch): its row writes must be
+  // complete before the rows are read
+  if (skip & kWaitBeforeCopy) pdl_wait();
   const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
   if (!(skip & kSkipCopy))
     warp_copy_rows<CH, CH == 8 ? 4 : 8>(c, res, nrows, default_row, out + base * c.d);
@@ -623,7 +629,8 @@ void launch_lookup_multi(const TableLookup* d_tables, uint32_t count, uint32_t t
 // --------------------------------------------------------------- launch --
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
-                             const LookupView& v, bool after_lookup, cudaStream_t st) {
+                             const LookupView& v, bool after_lookup, cudaStream_t st,
+                             bool wait_before_copy) {
   if (n == 0) return 0;
   // Kernel choice (HPSB_LOOKUP_KERNEL): lane-per-position fingerprint probe
   // by default; "warp4" / "warp8" = the warp-cooperative ballot probe (4 or
@@ -634,10 +641,11 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     if (e && std::string(e) == "warp8") return 8;
     return 0;
   }();
-  static const uint32_t skip = [] {
+  static const uint32_t diag_skip = [] {
     const char* e = std::getenv("HPSB_DIAG_SKIP");
-    return e ? uint32_t(std::atoi(e)) : 0u;
+    return e ? uint32_t(std::atoi(e)) & 7u : 0u;
   }();
+  const uint32_t skip = diag_skip | ((wait_before_copy && after_lookup) ? kWaitBeforeCopy : 0u);
   static const int warps = [] {
     const char* e = std::getenv("HPSB_LOOKUP_WARPS");
     const int w = e ? std::atoi(e) : 8;
@@ -652,7 +660,9 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
   cudaLaunchConfig_t cfg = {};
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = (after_lookup && !no_pdl) ? 1 : 0;
+  // (the warp-cooperative variant has no grid wait before its copies: it
+  // never chains behind an update)
+  cfg.numAttrs = (after_lookup && !no_pdl && !(variant != 0 && wait_before_copy)) ? 1 : 0;
   if (variant == 0) {
     auto aligned = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; };
     const int ch = (c.d % 8 == 0 && aligned(out, 32) && aligned(default_row, 32))   ? 8
