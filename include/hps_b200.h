@@ -357,6 +357,18 @@ int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_p
                       const float* rows, const uint8_t* flags_in, float* out, uint8_t* flags_out,
                       void* stream);
 
+/* ---- wire LOOKUP response frame (replaces encode_response_frame for
+ *      Opcode::Lookup, wire.cpp:174-188; layout wire.hpp:18-21, byte-exact:
+ *      [u32 body_len][u8 0][u32 count][u32 dim][count*dim f32][ceil(count/8)
+ *      miss bitmap, bit i%8 of byte i/8]). rows / miss_flags are the lookup's
+ *      output (HPS_MEM_HOST or, with HPS_MEM_DEVICE, device pointers on
+ *      `device`: the bitmap is packed on the GPU and rows + bitmap are copied
+ *      straight into `frame`, which should be pinned). frame = NULL queries
+ *      the size. Synchronous: the frame is complete on return. ---- */
+int hps_wire_lookup_frame(int device, const float* rows, const uint8_t* miss_flags,
+                          uint32_t count, uint32_t dim, int mem, uint8_t* frame, size_t cap,
+                          size_t* frame_len, void* stream);
+
 /* ---- workload (harness input; replaces PowerLawSampler::sample,
  *      workload.cpp:24-70, bit-exact) ---- */
 int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,

@@ -103,6 +103,8 @@ def rlib() -> C.CDLL:
             raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference sources)")
         l = C.CDLL(str(REF_SO))
         l.ref_last_error.restype = C.c_char_p
+        l.ref_wire_lookup_frame.restype = _SZ
+        l.ref_wire_lookup_frame.argtypes = [_P, _P, C.c_uint32, C.c_uint32, _P, _SZ]
         l.ref_xxh64.restype = C.c_uint64
         l.ref_xxh64.argtypes = [_P, _SZ, C.c_uint64]
         l.ref_xxh64_key.restype = C.c_uint64
@@ -531,6 +533,15 @@ def ref_powerlaw_sample(alpha, keyspace, permute_seed, draw_seed, count) -> np.n
 def ref_xxh64(data: bytes, seed: int = 0) -> int:
     b = C.create_string_buffer(bytes(data), len(data))
     return int(rlib().ref_xxh64(b, len(data), seed))
+
+
+def ref_wire_lookup_frame(rows, flags, dim: int) -> bytes:
+    r = _f32(rows)
+    f = np.ascontiguousarray(flags, dtype=np.uint8)
+    cap = 13 + r.size * 4 + (len(f) + 7) // 8
+    out = np.empty(max(cap, 1), dtype=np.uint8)
+    n = rlib().ref_wire_lookup_frame(_p(r), _p(f), len(f), dim, _p(out), out.size)
+    return out[:n].tobytes()
 
 
 def ref_dedup(keys):

@@ -15,6 +15,7 @@
 //   hps::PowerLawSampler      core/src/workload.cpp:24-70
 //   hps::VolatileStore        core/include/hps/volatile_store.hpp:45-137
 //   hps::LookupEngine         core/include/hps/lookup_engine.hpp:152-196
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <filesystem>
@@ -28,6 +29,7 @@
 #include "hps/persistent_store.hpp"
 #include "hps/slab_cache.hpp"
 #include "hps/types.hpp"
+#include "hps/wire.hpp"
 #include "hps/volatile_store.hpp"
 #include "hps/workload.hpp"
 #include "hps/xxhash64.hpp"
@@ -279,5 +281,23 @@ void ref_engine_stats(void* e, uint64_t* s) {
 void* ref_engine_cache(void* e) { return static_cast<RefEngine*>(e)->cache.get(); }
 
 unsigned ref_hw_threads() { return std::thread::hardware_concurrency(); }
+
+// hps::encode_response_frame(Opcode::Lookup, ...) (wire.cpp:174-188) with the
+// miss bitmap built as handle_frame does (server.cpp:284-294); returns the
+// frame length (copies min(len, cap) bytes).
+size_t ref_wire_lookup_frame(const float* rows, const uint8_t* flags, uint32_t count, uint32_t dim,
+                             uint8_t* out, size_t cap) {
+  hps::WireResponse resp;
+  resp.status = hps::Status::Ok;
+  resp.count = count;
+  resp.dim = dim;
+  resp.vectors.assign(rows, rows + size_t(count) * dim);
+  resp.miss_bitmap.assign((size_t(count) + 7) / 8, 0);
+  for (uint32_t i = 0; i < count; ++i)
+    if (flags[i]) hps::set_miss_bit(resp.miss_bitmap, i);
+  const auto f = hps::encode_response_frame(hps::Opcode::Lookup, resp);
+  std::memcpy(out, f.data(), std::min(cap, f.size()));
+  return f.size();
+}
 
 }  // extern "C"

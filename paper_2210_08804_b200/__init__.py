@@ -149,6 +149,8 @@ SIGNATURES = {
     "hps_engine_lookup_multi": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, _P, C.c_int]),
     "hps_cache_dump_device": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, _P, _P]),
     "hps_cache_create_shared": (C.c_int, [_P, C.c_int, _P, C.POINTER(_P)]),
+    "hps_wire_lookup_frame": (C.c_int, [C.c_int, _P, _P, C.c_uint32, C.c_uint32, C.c_int, _P,
+                                        C.c_size_t, _SZP, _P]),
     "hps_multi_create": (C.c_int, [_P, C.c_size_t, C.c_size_t, C.POINTER(_P)]),
     "hps_multi_destroy": (C.c_int, [_P]),
     "hps_multi_lookup": (C.c_int, [_P, _P, _P, _P, _P, _P]),
@@ -942,6 +944,31 @@ class MultiLookup:
         self.lookup_ptrs([k.ctypes.data for k in ks], [len(k) for k in ks],
                          [r.vectors.ctypes.data for r in res], [r.miss_flags.ctypes.data for r in res])
         return res
+
+
+def wire_lookup_frame(rows, miss_flags, dim: int) -> bytes:
+    """hps_wire_lookup_frame on host arrays: the reference's LOOKUP response
+    frame (wire.cpp:174-188), byte-exact."""
+    r = _f32(rows)
+    f = np.ascontiguousarray(miss_flags, dtype=np.uint8)
+    count = len(f)
+    n = C.c_size_t(0)
+    _check(lib().hps_wire_lookup_frame(0, None, None, count, dim, HPS_MEM_HOST, None, 0,
+                                       C.byref(n), None))
+    buf = np.empty(n.value, dtype=np.uint8)
+    _check(lib().hps_wire_lookup_frame(0, _ptr(r), _ptr(f), count, dim, HPS_MEM_HOST, _ptr(buf),
+                                       buf.size, C.byref(n), None))
+    return buf.tobytes()
+
+
+def wire_lookup_frame_device(rows_ptr: int, flags_ptr: int, count: int, dim: int, frame_ptr: int,
+                             cap: int, device: int = 0, stream: int = 0) -> int:
+    """Device-mode frame (rows / flags in HBM, frame ideally pinned); returns
+    the frame length."""
+    n = C.c_size_t(0)
+    _check(lib().hps_wire_lookup_frame(device, rows_ptr, flags_ptr, count, dim, HPS_MEM_DEVICE,
+                                       frame_ptr, cap, C.byref(n), stream or None))
+    return n.value
 
 
 def powerlaw_sample(alpha: float, keyspace: int, permute_seed: int, draw_seed: int,

@@ -472,6 +472,38 @@ int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_p
   });
 }
 
+// ------------------------------------------------------------------- wire --
+int hps_wire_lookup_frame(int device, const float* rows, const uint8_t* miss_flags,
+                          uint32_t count, uint32_t dim, int mem, uint8_t* frame, size_t cap,
+                          size_t* frame_len, void* stream) {
+  return guarded([&] {
+    need(frame_len != nullptr, "null argument");
+    need(dim > 0, "dimension must be positive");
+    const size_t bytes = hpsb::wire_lookup_frame_bytes(count, dim);
+    need(bytes - 4 <= 0xFFFFFFFFull, "frame too large");
+    *frame_len = bytes;
+    if (frame == nullptr) return;  // size query
+    need(cap >= bytes, "frame buffer too small");
+    need(count == 0 || (rows && miss_flags), "null argument");
+    if (mem == HPS_MEM_HOST) {
+      hpsb::wire_encode_lookup_host(rows, miss_flags, count, dim, frame);
+      return;
+    }
+    hpsb::DeviceGuard g(device);
+    cudaStream_t st = as_stream(stream);
+    uint8_t* bm = nullptr;
+    if (count) HPSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bm), (count + 7) / 8 + 4, st));
+    try {
+      hpsb::wire_encode_lookup_device(rows, miss_flags, count, dim, bm, frame, st);
+    } catch (...) {
+      if (bm) cudaFreeAsync(bm, st);
+      throw;
+    }
+    if (bm) HPSB_CUDA(cudaFreeAsync(bm, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 // -------------------------------------------------------------------- vdb --
 int hps_vdb_create(uint32_t lookup_threads, hps_vdb** out) {
   return guarded([&] {

@@ -175,4 +175,12 @@ void launch_shard_unroute(uint64_t m, uint32_t d, const uint32_t* send_pos, cons
                           const uint8_t* flags_in, float* out, uint8_t* flags_out,
                           cudaStream_t st);
 
+// ---- wire LOOKUP response frames (wire.cu; wire.hpp:18-21) ----
+size_t wire_lookup_frame_bytes(uint64_t count, uint32_t dim);
+void wire_encode_lookup_host(const float* rows, const uint8_t* flags, uint32_t count, uint32_t dim,
+                             uint8_t* frame);
+void wire_encode_lookup_device(const float* d_rows, const uint8_t* d_flags, uint32_t count,
+                               uint32_t dim, uint8_t* d_bitmap_scratch, uint8_t* frame,
+                               cudaStream_t st);
+
 }  // namespace hpsb
