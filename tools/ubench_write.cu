@@ -8,11 +8,12 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 #include <vector>
 
 constexpr int D = 128;
-constexpr int N = 65536;
+static int N = 65536;  // rows per launch (argv[1] multiplies it)
 
 __device__ __forceinline__ void st256(void* p, uint32_t v, bool cs) {
   if (cs)
@@ -101,13 +102,14 @@ __global__ void __launch_bounds__(256) k_gather8(const float* __restrict__ rows,
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) N *= atoi(argv[1]);
   const uint64_t slots = 2000000, bytes = uint64_t(N) * D * 4;
   float *rows, *out;
   uint32_t* slot;
   const int K = 40;
   cudaMalloc(&rows, slots * D * 4);
-  cudaMalloc(&out, bytes * 8);
+  cudaMalloc(&out, bytes * (N > 65536 ? 2 : 8));
   cudaMalloc(&slot, uint64_t(N) * 4 * K);
   cudaMemset(rows, 0, slots * D * 4);
   cudaEvent_t a, b;
@@ -125,7 +127,7 @@ int main() {
     const double us = ms * 1000 / K;
     printf("%-46s %7.2f us  %6.0f GB/s\n", name, us, moved / (us * 1e3));
   };
-  auto ob = [&](int it) { return reinterpret_cast<uint8_t*>(out) + (it % 8) * bytes; };
+  auto ob = [&](int it) { return reinterpret_cast<uint8_t*>(out) + (it % (N > 65536 ? 2 : 8)) * bytes; };
   for (int g : {148 * 4, 148 * 8, 148 * 16}) {
     char nm[96];
     snprintf(nm, sizeof nm, "write float4 grid %d", g);
