@@ -42,7 +42,10 @@ from typing import List, NamedTuple, Optional, Sequence
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libhps_b200.so"
+# HPSB_LIB_VARIANT=<name> loads libhps_b200.<name>.so built next to it (same-box
+# A/B of two builds, tools/ab.sh); the default is the in-tree build.
+LIB_PATH = _PKG / (f"libhps_b200.{os.environ['HPSB_LIB_VARIANT']}.so"
+                   if os.environ.get("HPSB_LIB_VARIANT") else "libhps_b200.so")
 
 kSlotsPerSlab = 32
 kSlabsetSeed = 0x5EED5E7
@@ -468,8 +471,8 @@ class SlabCache:
 
     def debug_trace(self) -> np.ndarray:
         """Per-call lookup phase timeline (HPSB_TRACE=1), absolute globaltimer
-        ns: rows of [first block start, last A done, first release, last
-        release, first copy done, last copy done, finish start, finish end],
+        ns: rows of [first block start, last A done, last block start, first
+        A done, first copy done, last copy done, finish start, finish end],
         oldest first; resets the ring."""
         ring = np.empty(4096 * 8, dtype=np.uint64)
         n = C.c_uint64(0)
@@ -478,7 +481,7 @@ class SlabCache:
         r = ring.reshape(-1, 8)
         idx = [(int(n.value) - k + i) % 4096 for i in range(k)]
         r = r[idx].copy()
-        for f in (1, 3, 5):
+        for f in (1, 2, 5):
             r[:, f] = ~r[:, f]
         return r.astype(np.int64)
 

@@ -33,30 +33,35 @@ def _newest_header() -> float:
     return max(h.stat().st_mtime for h in hs)
 
 
-def build(verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(verbose: bool = False, variant: str | None = None, defines: tuple = ()) -> Path:
+    """Builds libhps_b200.so; with `variant`, libhps_b200.<variant>.so from the
+    same sources plus `-D` `defines` (compile-time A/B builds, loaded with
+    HPSB_LIB_VARIANT=<variant>; tools/build_variant.py)."""
+    bdir = BUILD / variant if variant else BUILD
+    lib = PKG / f"libhps_b200.{variant}.so" if variant else LIB
+    bdir.mkdir(parents=True, exist_ok=True)
     hdr = _newest_header()
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = BUILD / (src + ".o")
+        o = bdir / (src + ".o")
         objs.append(o)
         if o.exists() and o.stat().st_mtime >= max(s.stat().st_mtime, hdr):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS]
+        cmd = [NVCC, *ARCH, *FLAGS, *(f"-D{d}" for d in defines)]
         if src.endswith(".cpp"):
             cmd += ["-x", "cu"]
         cmd += ["-c", str(s), "-o", str(o)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-    if not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+    if not lib.exists() or lib.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart_static",
                "-lpthread", "-ldl", "-lrt"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -71,7 +71,7 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
   HPSB_CUDA(cudaMalloc(&dev_.tags, slots));
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
-  lookup_marks_locked();  // allocated up front: lookups may be graph-captured
+  lookup_marks_locked(0);  // allocated up front: lookups may be graph-captured
   HPSB_CUDA(cudaMalloc(&winner_, slots * 4));  // update: last position per slot
   HPSB_CUDA(cudaMemsetAsync(winner_, 0, slots * 4, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.keys, 0, slots * 8, stream_));
@@ -230,11 +230,12 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   // enqueued in between (the kernel orders itself against it)
   static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
   // (never inside a cache group: other caches' work shares the stream)
+  uint32_t* marks = lookup_marks_locked(stamp);  // (may enqueue a reset first)
   const bool after_update = last_op_update_;
   const bool chain = (last_op_lookup_ || last_op_update_) && !no_pdl &&
                      stream_holder_.use_count() == 1;
   LookupView v = lookup_next_view(lws_, chain);
-  v.marks = lookup_marks_locked() + uint64_t(lws_.last) * capacity_slots();
+  v.marks = marks + uint64_t(lws_.last) * capacity_slots();
   static const bool tracing = std::getenv("HPSB_TRACE") != nullptr;
   if (tracing) {
     if (trace_ == nullptr) {
@@ -406,12 +407,19 @@ size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, si
   return n;
 }
 
-unsigned long long* DeviceCache::lookup_marks_locked() {
+uint32_t* DeviceCache::lookup_marks_locked(uint64_t stamp) {
+  const uint64_t bytes = uint64_t(kLookupViews) * capacity_slots() * 4;
   if (marks_ == nullptr) {
-    const uint64_t bytes = uint64_t(kLookupViews) * capacity_slots() * 8;
     HPSB_CUDA(cudaMalloc(&marks_, bytes));
     HPSB_CUDA(cudaMemsetAsync(marks_, 0, bytes, stream_));
     mark_other_op();
+    marks_epoch_ = stamp >> 32;
+  } else if ((stamp >> 32) != marks_epoch_) {
+    // every 2^32 stamps: a mark from the previous epoch could equal this
+    // call's low bits (stream-ordered after every earlier lookup)
+    HPSB_CUDA(cudaMemsetAsync(marks_, 0, bytes, stream_));
+    mark_other_op();
+    marks_epoch_ = stamp >> 32;
   }
   return marks_;
 }

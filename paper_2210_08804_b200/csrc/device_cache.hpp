@@ -102,11 +102,17 @@ class DeviceCache {
   // Callers that enqueue their own work on stream() (the engine) call this
   // under mutex() so the next lookup does not chain onto a stale lookup.
   void note_stream_op() { mark_other_op(); }
-  // Mark arrays of the lookup kernels (call under mutex()); array i at
-  // + i * capacity_slots().
-  unsigned long long* lookup_marks_locked();
+  // Mark arrays of the lookup kernels (call under mutex()) for a call with
+  // `stamp`; array i at + i * capacity_slots(). Marks hold the low 32 bits of
+  // stamps; they are reset when the high 32 bits change.
+  uint32_t* lookup_marks_locked(uint64_t stamp);
   uint64_t capacity_slots() const { return cfg_.slabset_count * cfg_.slabs_per_set * 32ull; }
-  uint64_t bump_clock() { return clock_.fetch_add(1, std::memory_order_relaxed) + 1; }
+  // Stamps never have zero low 32 bits (the reset value of the marks).
+  uint64_t bump_clock() {
+    uint64_t s = clock_.fetch_add(1, std::memory_order_relaxed) + 1;
+    if (uint32_t(s) == 0) s = clock_.fetch_add(1, std::memory_order_relaxed) + 1;
+    return s;
+  }
   // Device keys / rows, distinct keys guaranteed by the caller; stamp = the
   // current clock. Enqueued on stream(); scratch is the cache's own.
   void replace_device_locked(const uint64_t* d_keys, size_t n, const float* d_rows);
@@ -148,9 +154,10 @@ class DeviceCache {
     last_op_update_ = false;
   }
   std::shared_ptr<StreamHolder> stream_holder_;
-  // unique-hit marks of the lookup kernels: kLookupViews arrays of one u64
-  // per slot (lazily allocated; see LookupView::marks)
-  unsigned long long* marks_ = nullptr;
+  // unique-hit marks of the lookup kernels: kLookupViews arrays of one u32
+  // per slot (see LookupView::marks), valid for stamps of epoch marks_epoch_
+  uint32_t* marks_ = nullptr;
+  uint64_t marks_epoch_ = 0;
   // update: per-slot winning position + 1 (all-zero between calls)
   uint32_t* winner_ = nullptr;
   DeviceBuffer ubuf_;  // update_device scratch

@@ -400,7 +400,7 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
         cache_->join_from(user);
       }
       ws->lv = lookup_next_view(ws->ls, /*chain=*/false);
-      ws->lv.marks = cache_->lookup_marks_locked();
+      ws->lv.marks = cache_->lookup_marks_locked(stamp);
       cache_->note_stream_op();  // the engine's own copies follow on the stream
       launch_lookup_probe(cache_->dev(), c.d_keys, n, c.d_out, c.d_flags, d_default_, stamp,
                           ws->lv, /*after_lookup=*/false, st);
@@ -733,7 +733,7 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
     const uint64_t stamp = c->bump_clock();  // query ticks even when empty
     c->note_stream_op();
     LookupView v = lookup_next_view(ls_[t], false);
-    v.marks = c->lookup_marks_locked();
+    v.marks = c->lookup_marks_locked(stamp);
     v.list_keys = reinterpret_cast<uint64_t*>(db + d_ckeys_) + koff[t];
     v.list_firsts = reinterpret_cast<uint32_t*>(db + d_cfirsts_) + koff[t];
     v.counts_out = reinterpret_cast<unsigned long long*>(db + d_counts_) + 2 * t;

@@ -109,15 +109,19 @@ struct LookupView {
   // the previous call on the stream (its completion precedes this call's)
   const unsigned long long* prev_completed = nullptr;
   unsigned long long prev_target = 0;
-  // per-slot stamp of the last call that counted the slot as a unique hit
-  // (one array per concurrently running call, see DeviceCache::lookup_marks)
-  unsigned long long* marks = nullptr;
+  // per-slot low 32 bits of the stamp of the last call that counted the slot
+  // as a unique hit (one array per concurrently running call, see
+  // DeviceCache::lookup_marks_locked)
+  uint32_t* marks = nullptr;
 };
 // A ring of views: consecutive lookups on one stream take consecutive views,
 // so up to kLookupViews calls can be in flight (programmatic dependent
 // launch); a call waits on the device until the previous use of its view
 // has completed.
-constexpr int kLookupViews = 4;
+#ifndef HPSB_LOOKUP_VIEWS
+#define HPSB_LOOKUP_VIEWS 8
+#endif
+constexpr int kLookupViews = HPSB_LOOKUP_VIEWS;
 struct LookupScratch {
   LookupView v[kLookupViews];
   uint64_t uses[kLookupViews] = {};  // host: uses handed out per view

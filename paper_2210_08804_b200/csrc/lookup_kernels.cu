@@ -134,8 +134,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Trace fields: 0 first block start, 1 last block done with A, 2 first
-// block released by the wait, 3 last block released, 4 first block done
+// Trace fields: 0 first block start, 1 last block done with A, 2 last
+// block start, 3 first block done with A, 4 first block done
 // copying, 5 last block done copying, 6 claims finish start, 7 claims
 // finish end.
 __device__ __forceinline__ void trace_min(const LookupView& v, int f, bool as_max) {
@@ -152,6 +152,21 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Block ticket arrival: a release (this block's writes -- ordered before it
+// by the preceding barrier -- are visible to whoever sees the count) without
+// the acquire half, which on sm_100 invalidates the SM's whole L1 (CCTL.IVALL)
+// and with it the hot rows every resident block is reading.
+__device__ __forceinline__ uint32_t atom_add_release(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // Spins (one thread) until *p >= target. Calls on one stream only ever wait
 // on calls launched before them, whose blocks have all started, so this
 // cannot deadlock -- unless captured graphs are replayed out of capture
@@ -164,6 +179,19 @@ __device__ __forceinline__ void spin_ge(const unsigned long long* p, unsigned lo
     if (global_ns() - t0 > 2000000000ull) __trap();
   }
 }
+// The same wait at every block start of a lookup, with relaxed loads: a
+// view's scratch is only ever accessed through L2 (atomics, .cg loads,
+// stores), which already holds the previous use's writes when its release
+// is observed, so the L1-invalidating acquire is not needed here.
+__device__ __forceinline__ void spin_ge_relaxed(const unsigned long long* p,
+                                                unsigned long long target) {
+  if (ld_relaxed(p) >= target) return;
+  const unsigned long long t0 = global_ns();
+  while (ld_relaxed(p) < target) {
+    __nanosleep(200);
+    if (global_ns() - t0 > 2000000000ull) __trap();
+  }
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -171,8 +199,8 @@ __device__ __forceinline__ void pdl_trigger() {
 
 // ------------------------------------------------------- call completion --
 // A call completes in two parts, each run by the last block through a
-// ticket (__threadfence + atomic ticket, so all earlier blocks' writes are
-// visible):
+// ticket (a release atomic per block, an acquire fence in the last one, so
+// all earlier blocks' writes are visible):
 //   finish_claims  once every block has made its claims (before the row
 //                  copies): first position of each claim, miss table cleared;
 //                  it overlaps the other blocks' copies
@@ -239,11 +267,10 @@ __device__ __forceinline__ bool last_block(const LookupView& v, int t, uint32_t 
   __shared__ uint32_t s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(v.done + t, 1u) == nblocks - 1 ? 1u : 0u;
+    s_last = atom_add_release(v.done + t, 1u) == nblocks - 1 ? 1u : 0u;
+    if (s_last) fence_acq_rel();  // acquire: every block's writes (one block per call)
   }
   __syncthreads();
-  if (s_last) __threadfence();
   return s_last != 0;
 }
 
@@ -303,7 +330,8 @@ __device__ __forceinline__ uint32_t warp_claim_misses(const LookupView& v,
 __device__ __forceinline__ uint32_t stamp_slot(const CacheDev& c, const LookupView& v,
                                                uint32_t slot, unsigned long long stamp) {
   atomicMax(reinterpret_cast<unsigned long long*>(c.counters + slot), stamp);
-  return atomicExch(v.marks + slot, stamp) != stamp ? 1u : 0u;
+  const uint32_t s32 = uint32_t(stamp);  // never 0 (DeviceCache::bump_clock)
+  return atomicExch(v.marks + slot, s32) != s32 ? 1u : 0u;
 }
 
 // Inserts `slot` into a block-shared open-addressing set; false when the
@@ -364,7 +392,7 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int RC = 32 / L;   // float4 chunks per lane per 128-float row segment
   __shared__ uint32_t s_stamped[1u << kSetBits];
   for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += kThreads) s_stamped[i] = kNoSlot;
-  if (threadIdx.x == 0) spin_ge(v.completed, v.gen);
+  if (threadIdx.x == 0) spin_ge_relaxed(v.completed, v.gen);
   __syncthreads();
   const uint32_t lane = lane_id();
   const uint32_t q = lane / L, sub = lane % L;
@@ -479,6 +507,18 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ====================================================== lane-per-position --
+// Compile-time A/B knobs (tools/build_variant.py): 256-bit chunks in flight
+// per lane in the row copy, and the minimum resident blocks per SM (the
+// register cap); defaults = the measured best.
+#ifndef HPSB_COPY_U
+#define HPSB_COPY_U 2
+#endif
+#ifndef HPSB_EARLY_TRIGGER
+#define HPSB_EARLY_TRIGGER 0
+#endif
+#ifndef HPSB_MINB_THREADS
+#define HPSB_MINB_THREADS 1536
+#endif
 // Copy of a warp's rows (lane i's row = slot `res` of lane i, or the
 // default row) into the warp's contiguous output block: `CH` floats per
 // access (8 = 256-bit, 4 = 128-bit, 1 = scalar), U accesses in flight.
@@ -534,9 +574,13 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   __shared__ uint32_t s_stamped[kSetSize];
   for (uint32_t i = threadIdx.x; i < kSetSize; i += kThreadsB) s_stamped[i] = kNoSlot;
   // the view's previous use must have completed (normally long ago)
-  if (threadIdx.x == 0) spin_ge(v.completed, v.gen);
+  if (threadIdx.x == 0) spin_ge_relaxed(v.completed, v.gen);
   __syncthreads();
   trace_min(v, 0, false);
+  trace_min(v, 2, true);
+#if HPSB_EARLY_TRIGGER
+  pdl_trigger();
+#endif
   const uint32_t lane = lane_id();
   const uint64_t base = (uint64_t(blk) * kThreadsB + threadIdx.x) & ~31ull;
   const uint64_t pos = base + lane;
@@ -552,12 +596,11 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   if (v.trace) {
     __syncthreads();
     trace_min(v, 1, true);
+    trace_min(v, 3, false);
   }
+#if !HPSB_EARLY_TRIGGER
   pdl_trigger();
-  if (v.trace) {
-    trace_min(v, 2, false);
-    trace_min(v, 3, true);
-  }
+#endif
   // ---- the last block to have made its claims completes the claim list
   // (overlapping the other blocks' copies) ----
   if (last_block(v, 0, nblocks)) {
@@ -575,7 +618,8 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   if (skip & kWaitBeforeCopy) pdl_wait();
   const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
   if (!(skip & kSkipCopy))
-    warp_copy_rows<CH, CH == 8 ? 4 : 8>(c, res, nrows, default_row, out + base * c.d);
+    warp_copy_rows<CH, CH == 8 ? HPSB_COPY_U : 2 * HPSB_COPY_U>(c, res, nrows, default_row,
+                                                              out + base * c.d);
   warp_add_counts(v, uh, um, blk * WARPS + (threadIdx.x >> 5));
   if (v.trace) {
     __syncthreads();
@@ -586,7 +630,7 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
 }
 
 template <int CH, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
+__global__ void __launch_bounds__(WARPS * 32, HPSB_MINB_THREADS / (WARPS * 32))
     k_lookup_tag(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                  float* __restrict__ out, uint8_t* __restrict__ flags,
                  const float* __restrict__ default_row, uint64_t stamp, LookupView v,

@@ -60,7 +60,7 @@ def main():
     torch.cuda.synchronize()
     t = cache.debug_trace()[-a.steps:]
     rel = (t[:, 1:] - t[:, :1]) / 1e3
-    names = ["last A done", "first release", "last release", "first copy done",
+    names = ["last A done", "last block start", "first A done", "first copy done",
              "last copy done", "finish start", "finish end"]
     print(f"{len(t)} calls; per-call timeline (us from the call's first block start), median [p10, p90]:")
     for j, nm in enumerate(names):
@@ -70,7 +70,8 @@ def main():
     end_to_start = (t[1:, 0] - t[:-1, 7]) / 1e3
     print(f"  start-to-start gap      {np.median(gap):7.2f}  [{np.percentile(gap, 10):6.2f}, {np.percentile(gap, 90):6.2f}]")
     print(f"  next start - finish end {np.median(end_to_start):7.2f}")
-    print(f"  prev finish end -> first release {np.median((t[1:, 2] - t[:-1, 7]) / 1e3):7.2f}")
+    print(f"  next start - last A done {np.median((t[1:, 0] - t[:-1, 1]) / 1e3):7.2f}")
+    print(f"  next start - last copy done {np.median((t[1:, 0] - t[:-1, 5]) / 1e3):7.2f}")
 
 
 if __name__ == "__main__":
