@@ -326,12 +326,18 @@ __device__ __forceinline__ uint32_t warp_claim_misses(const LookupView& v,
 // Recency exchange of a hit slot: the call's stamp becomes the slot's
 // counter (max: calls may overlap, a later call's stamp wins), and the
 // exchange on the call's mark array tells whether this is the call's first
-// hit of the slot (one unique hit).
+// hit of the slot (one unique hit). Both are read first and only written
+// when not already done: a power-law batch's hot slot is hit by every block
+// of the call, and same-line read-modify-writes serialise in its L2 slice
+// (reading first: 10.27 vs 11.25 us per cfg-2 batch).
 __device__ __forceinline__ uint32_t stamp_slot(const CacheDev& c, const LookupView& v,
                                                uint32_t slot, unsigned long long stamp) {
-  atomicMax(reinterpret_cast<unsigned long long*>(c.counters + slot), stamp);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c.counters) + slot;
   const uint32_t s32 = uint32_t(stamp);  // never 0 (DeviceCache::bump_clock)
-  return atomicExch(v.marks + slot, s32) != s32 ? 1u : 0u;
+  const unsigned long long cur_ctr = __ldcg(ctr);
+  const uint32_t cur_mark = __ldcg(v.marks + slot);
+  if (cur_ctr < stamp) atomicMax(ctr, stamp);
+  return (cur_mark != s32 && atomicExch(v.marks + slot, s32) != s32) ? 1u : 0u;
 }
 
 // Inserts `slot` into a block-shared open-addressing set; false when the

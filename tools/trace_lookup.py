@@ -15,7 +15,10 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-os.environ.setdefault("HPSB_TRACE", "1")
+if "--no-trace" in sys.argv:  # just run the graph once (e.g. under ncu --graph-profiling graph)
+    os.environ.pop("HPSB_TRACE", None)
+else:
+    os.environ.setdefault("HPSB_TRACE", "1")
 
 
 def main():
@@ -27,6 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--hit", type=float, default=0.9)
+    ap.add_argument("--no-trace", action="store_true")
     a = ap.parse_args()
     wl = bench.Workload()
     d, n = wl.dim, wl.batch
@@ -58,6 +62,8 @@ def main():
                                 cnt[2 * s:].data_ptr(), sp)
     g.launch()
     torch.cuda.synchronize()
+    if a.no_trace:
+        return
     t = cache.debug_trace()[-a.steps:]
     rel = (t[:, 1:] - t[:, :1]) / 1e3
     names = ["last A done", "last block start", "first A done", "first copy done",
