@@ -201,9 +201,9 @@ __device__ __forceinline__ void pdl_trigger() {
 // A call completes in two parts, each run by the last block through a
 // ticket (a release atomic per block, an acquire fence in the last one, so
 // all earlier blocks' writes are visible):
-//   finish_claims  once every block has made its claims (before the row
-//                  copies): first position of each claim, miss table cleared;
-//                  it overlaps the other blocks' copies
+//   finish_claims  once every block has made its claims (ticket taken before
+//                  the row copies, run after the block's own copies): first
+//                  position of each claim, miss table cleared
 //   finish_counts  once every block has added its counts (after the copies):
 //                  per-call counts, counters zeroed, tickets and claim
 //                  counter reset for the next call on this view
@@ -607,12 +607,20 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
 #if !HPSB_EARLY_TRIGGER
   pdl_trigger();
 #endif
-  // ---- the last block to have made its claims completes the claim list
-  // (overlapping the other blocks' copies) ----
-  if (last_block(v, 0, nblocks)) {
-    trace_min(v, 6, false);
-    finish_claims(v);
-    trace_min(v, 7, false);
+  // ---- claims ticket without stalling the block: warps 1.. arrive at a
+  // named barrier and go on; warp 0 waits for them and takes the ticket; the
+  // block that was last completes the claim list after its copies (a
+  // block-wide barrier + ticket here: 10.33 vs 10.01 us per cfg-2 batch) ----
+  __shared__ uint32_t s_last_claims;
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreadsB) : "memory");
+    if (threadIdx.x == 0) {
+      const bool last = atom_add_release(v.done, 1u) == nblocks - 1;
+      if (last) fence_acq_rel();
+      s_last_claims = last ? 1u : 0u;
+    }
+  } else {
+    asm volatile("bar.arrive 1, %0;" ::"r"(kThreadsB) : "memory");
   }
   // ---- C: recency exchange, row copy, counts ----
   const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
@@ -631,6 +639,12 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
     __syncthreads();
     trace_min(v, 4, false);
     trace_min(v, 5, true);
+  }
+  __syncthreads();
+  if (s_last_claims) {
+    trace_min(v, 6, false);
+    finish_claims(v);
+    trace_min(v, 7, false);
   }
   if (last_block(v, 1, nblocks)) finish_counts(v);
 }
