@@ -519,9 +519,6 @@ __global__ void __launch_bounds__(kThreads)
 #ifndef HPSB_COPY_U
 #define HPSB_COPY_U 2
 #endif
-#ifndef HPSB_EARLY_TRIGGER
-#define HPSB_EARLY_TRIGGER 0
-#endif
 #ifndef HPSB_MINB_THREADS
 #define HPSB_MINB_THREADS 1536
 #endif
@@ -584,9 +581,12 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   __syncthreads();
   trace_min(v, 0, false);
   trace_min(v, 2, true);
-#if HPSB_EARLY_TRIGGER
+  // The next lookup on the stream may start now (programmatic dependent
+  // launch): nothing in this call depends on the previous one past the
+  // view wait above, so as many calls overlap as views and SM slots allow
+  // (trigger here vs after the probe and claims: 9.4 vs 10.0 us per cfg-2
+  // batch).
   pdl_trigger();
-#endif
   const uint32_t lane = lane_id();
   const uint64_t base = (uint64_t(blk) * kThreadsB + threadIdx.x) & ~31ull;
   const uint64_t pos = base + lane;
@@ -597,16 +597,11 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   const bool miss = valid && res == kNoSlot && !(skip & kSkipMiss);
   const uint32_t um = warp_claim_misses(v, keys, pos, key, miss);
   if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
-  // ---- B: the next lookup on the stream may start (programmatic
-  // dependent launch); nothing below depends on the previous one ----
   if (v.trace) {
     __syncthreads();
     trace_min(v, 1, true);
     trace_min(v, 3, false);
   }
-#if !HPSB_EARLY_TRIGGER
-  pdl_trigger();
-#endif
   // ---- claims ticket without stalling the block: warps 1.. arrive at a
   // named barrier and go on; warp 0 waits for them and takes the ticket; the
   // block that was last completes the claim list after its copies (a
