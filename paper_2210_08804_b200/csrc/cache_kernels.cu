@@ -355,11 +355,16 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
 //   k_update_probe  lane per position: fingerprint probe (tag_probe.cuh);
 //                   slot recorded; max(position + 1) per hit slot into the
 //                   cache's `winner` array (fire-and-forget); hits counted
-//   k_update_write  lane per position, warp per 32: the winning position of
-//                   each slot copies its row (256-bit loads from the
-//                   contiguous input block, write-back stores into the table)
-//                   and clears the winner entry (the array is all-zero
-//                   between calls)
+//   k_update_write  warp per 8 positions: the winning position of each
+//                   slot copies its row (256-bit loads from the contiguous
+//                   input block, write-back stores into the table; a d = 128
+//                   warp moves its 4 KB in ONE round trip, every row of the
+//                   call in flight at once) and clears the winner entry (the
+//                   array is all-zero between calls)
+// Consecutive updates alternate between two winner arrays and two scratch
+// halves (DeviceCache): the next update's probe may run while this write is
+// still in flight (it launches behind the next lookup, which launches when
+// this write starts).
 __global__ void __launch_bounds__(256)
     k_update_probe(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                    uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner,
@@ -384,31 +389,34 @@ __global__ void __launch_bounds__(256)
   if (wait_at_end) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+constexpr uint32_t kUpdateRowsPerWarp = 8;
+
 template <int CH>
 __global__ void __launch_bounds__(256)
     k_update_write(CacheDev c, const float* __restrict__ rows, uint64_t n,
                    const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ winner,
-                   const uint32_t* __restrict__ block_hits, uint32_t nblocks,
+                   const uint32_t* __restrict__ block_hits, uint32_t probe_blocks,
                    unsigned long long* __restrict__ written) {
   // the next lookup may launch now (it waits for this grid before its copies)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr uint32_t R = kUpdateRowsPerWarp;
   constexpr int U = CH == 8 ? 4 : 8;
   const uint32_t lane = lane_id();
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     unsigned long long h = 0;
-    for (uint32_t b = threadIdx.x; b < nblocks; b += 32) h += block_hits[b];
+    for (uint32_t b = threadIdx.x; b < probe_blocks; b += 32) h += block_hits[b];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
     if (threadIdx.x == 0) *written = h;
   }
-  const uint64_t base = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull;
+  const uint64_t base = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * R;
   const uint64_t pos = base + lane;
   uint32_t slot = kNoSlot;
-  if (pos < n) {
+  if (lane < R && pos < n) {
     slot = slot_of[pos];
     if (slot != kNoSlot && __ldcg(winner + slot) != uint32_t(pos + 1)) slot = kNoSlot;  // a later duplicate wins
   }
-  const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
+  const uint32_t nrows = n > base + R ? R : uint32_t(n > base ? n - base : 0);
   const uint32_t d = c.d;
   const uint32_t cpr = d / CH;
   const bool pow2 = (cpr & (cpr - 1)) == 0;
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < U; ++u) {
       const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
       uint32_t row = pow2 ? (ch >> sh) : (ch / cpr);
-      row = min(row, 31u);
+      row = min(row, R - 1);
       dst_slot[u] = __shfl_sync(0xFFFFFFFFu, slot, row);
       if (ch < total && dst_slot[u] != kNoSlot) x[u].load(src + uint64_t(ch) * CH);
     }
@@ -465,12 +473,13 @@ void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const fl
                      uint32_t(after_lookup ? 1 : 0));
   const bool a32 = (reinterpret_cast<uintptr_t>(rows) % 32) == 0;
   const bool a16 = (reinterpret_cast<uintptr_t>(rows) % 16) == 0;
+  const unsigned wgrid = unsigned((n + 8 * kUpdateRowsPerWarp - 1) / (8 * kUpdateRowsPerWarp));
   if (c.d % 8 == 0 && a32)
-    k_update_write<8><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
+    k_update_write<8><<<wgrid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
   else if (c.d % 4 == 0 && a16)
-    k_update_write<4><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
+    k_update_write<4><<<wgrid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
   else
-    k_update_write<1><<<grid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
+    k_update_write<1><<<wgrid, 256, 0, st>>>(c, rows, n, slot_of, winner, block_hits, grid, written);
   check_launch("update", 2);
 }
 

@@ -72,8 +72,9 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
   lookup_marks_locked(0);  // allocated up front: lookups may be graph-captured
-  HPSB_CUDA(cudaMalloc(&winner_, slots * 4));  // update: last position per slot
-  HPSB_CUDA(cudaMemsetAsync(winner_, 0, slots * 4, stream_));
+  // update: last position per slot, two arrays (consecutive updates alternate)
+  HPSB_CUDA(cudaMalloc(&winner_, 2 * slots * 4));
+  HPSB_CUDA(cudaMemsetAsync(winner_, 0, 2 * slots * 4, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.keys, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.counters, 0, slots * 8, stream_));
   HPSB_CUDA(cudaMemsetAsync(dev_.masks, 0, slabs * 4, stream_));
@@ -348,8 +349,8 @@ size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,
   } else {
     join_from(user);
   }
-  launch_update(dev_, d_keys, n, d_rows, scratch_u, winner_, d_small_ + 2, /*after_lookup=*/false,
-                stream_);
+  launch_update(dev_, d_keys, n, d_rows, scratch_u, next_winner(), d_small_ + 2,
+                /*after_lookup=*/false, stream_);
   HPSB_CUDA(cudaMemcpyAsync(h_small_ + 2, d_small_ + 2, 8, cudaMemcpyDeviceToHost, stream_));
   HPSB_CUDA(cudaStreamSynchronize(stream_));
   if (!host) join_to(user);
@@ -369,19 +370,22 @@ void DeviceCache::update_device(const uint64_t* keys, size_t n, const float* vec
   DeviceGuard g(device_);
   join_from(user);
   bool chain = after_lookup;
+  // two scratch halves: the next update's probe may overlap this write
   if (n > ucap_) {
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
-    ubuf_.ensure(align256(update_scratch_bytes(cap)) + 256, stream_);
+    ubuf_.ensure(2 * (align256(update_scratch_bytes(cap)) + 256), stream_);
     ucap_ = cap;
     chain = false;  // (re)allocation enqueued work in between
   }
+  uint32_t* winner = next_winner();
+  const uint64_t half = align256(update_scratch_bytes(ucap_)) + 256;
+  char* ub = static_cast<char*>(ubuf_.get()) + (winner == winner_ ? 0 : half);
   unsigned long long* w = written != nullptr
                               ? reinterpret_cast<unsigned long long*>(written)
                               : reinterpret_cast<unsigned long long*>(
-                                    static_cast<char*>(ubuf_.get()) +
-                                    align256(update_scratch_bytes(ucap_)));
-  launch_update(dev_, keys, n, vectors, ubuf_.get(), winner_, w, chain, stream_);
+                                    ub + align256(update_scratch_bytes(ucap_)));
+  launch_update(dev_, keys, n, vectors, ub, winner, w, chain, stream_);
   last_op_update_ = n > 0 && (user == nullptr || user == stream_);
   join_to(user);
 }

@@ -158,8 +158,14 @@ class DeviceCache {
   // per slot (see LookupView::marks), valid for stamps of epoch marks_epoch_
   uint32_t* marks_ = nullptr;
   uint64_t marks_epoch_ = 0;
-  // update: per-slot winning position + 1 (all-zero between calls)
+  // update: per-slot winning position + 1 (all-zero between calls); two
+  // arrays, consecutive updates alternate (the next update's probe may run
+  // while this update's write kernel is in flight)
   uint32_t* winner_ = nullptr;
+  uint64_t updates_ = 0;
+  uint32_t* next_winner() {
+    return winner_ + ((updates_++ & 1u) ? cfg_.slabset_count * cfg_.slabs_per_set * 32ull : 0ull);
+  }
   DeviceBuffer ubuf_;  // update_device scratch
   uint64_t ucap_ = 0;
   // diagnostic lookup timeline ring (HPSB_TRACE=1): kTraceRing calls x 8

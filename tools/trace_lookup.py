@@ -31,6 +31,11 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--hit", type=float, default=0.9)
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--isolated", action="store_true",
+                    help="one call at a time (host sync between calls): single-call timeline")
+    ap.add_argument("--update-frac", type=float, default=0.0,
+                    help="cfg 4: stream-ordered update of this fraction of the resident rows "
+                         "after every lookup")
     a = ap.parse_args()
     wl = bench.Workload()
     d, n = wl.dim, wl.batch
@@ -39,7 +44,17 @@ def main():
     for i in range(0, len(wl.preload), n):
         k = wl.preload[i:i + n]
         cache.replace(k, bench.table_rows(k, d))
-    wl.set_resident(cache.dump_all())
+    resident = cache.dump_all()
+    wl.set_resident(resident)
+    upd = []
+    if a.update_frac > 0:
+        u = max(1, int(len(resident) * a.update_frac))
+        rng = np.random.default_rng(77)
+        for j in range(8):
+            idx = rng.choice(len(resident), u, replace=False)
+            upd.append((torch.from_numpy(resident[idx].view(np.int64)).cuda(),
+                        torch.empty(u * d, device="cuda").uniform_(-1, 1), u))
+    written = torch.zeros(1, dtype=torch.int64, device="cuda")
     batches, _, _ = wl.batches(a.hit, 32, 7)
     dk = [torch.from_numpy(b.view(np.int64)).cuda() for b in batches]
     outs = [torch.empty(n * d, device="cuda") for _ in range(8)]
@@ -52,16 +67,43 @@ def main():
     for s in range(10):
         cache.lookup_device(dk[s % 32].data_ptr(), n, outs[s % 8].data_ptr(), fl.data_ptr(),
                             dr.data_ptr(), mk.data_ptr(), mf.data_ptr(), cnt.data_ptr(), sp)
+        if upd:
+            k, r, u = upd[s % 8]
+            cache.update_device_async(k.data_ptr(), u, r.data_ptr(), written.data_ptr(), sp)
     torch.cuda.synchronize()
     cache.debug_trace()
-    g = hps.StreamGraph(sp)
-    with g:
+    if a.isolated:
+        st = torch.cuda.ExternalStream(sp)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(a.steps)]
         for s in range(a.steps):
+            ev[s][0].record(st)
             cache.lookup_device(dk[s % 32].data_ptr(), n, outs[s % 8].data_ptr(), fl.data_ptr(),
                                 dr.data_ptr(), mk.data_ptr(), mf.data_ptr(),
                                 cnt[2 * s:].data_ptr(), sp)
-    g.launch()
-    torch.cuda.synchronize()
+            ev[s][1].record(st)
+            torch.cuda.synchronize()
+        el = np.array([x.elapsed_time(y) for x, y in ev]) * 1e3
+        print(f"isolated calls: event-bracketed median {np.median(el):.2f} us "
+              f"[p10 {np.percentile(el, 10):.2f}, p90 {np.percentile(el, 90):.2f}]")
+    else:
+        g = hps.StreamGraph(sp)
+        with g:
+            for s in range(a.steps):
+                cache.lookup_device(dk[s % 32].data_ptr(), n, outs[s % 8].data_ptr(), fl.data_ptr(),
+                                    dr.data_ptr(), mk.data_ptr(), mf.data_ptr(),
+                                    cnt[2 * s:].data_ptr(), sp)
+                if upd:
+                    k, r, u = upd[s % 8]
+                    cache.update_device_async(k.data_ptr(), u, r.data_ptr(), written.data_ptr(), sp)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = torch.cuda.ExternalStream(sp)
+        t0.record(st)
+        g.launch()
+        t1.record(st)
+        torch.cuda.synchronize()
+        print(f"graph: {t0.elapsed_time(t1) * 1e3 / a.steps:.2f} us per step")
+        torch.cuda.synchronize()
     if a.no_trace:
         return
     t = cache.debug_trace()[-a.steps:]
