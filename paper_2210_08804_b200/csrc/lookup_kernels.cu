@@ -565,7 +565,7 @@ __device__ __forceinline__ void warp_copy_rows(const CacheDev& c, uint32_t res, 
 // The body of one table's lookup for block `blk` of its `nblocks` blocks
 // (the single-table kernel passes blockIdx / gridDim; the multi-table
 // kernel the block's rank within its table).
-template <int CH, int WARPS>
+template <int CH, int WARPS, bool SF>
 __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* __restrict__ keys,
                                             uint64_t n, float* __restrict__ out,
                                             uint8_t* __restrict__ flags,
@@ -595,8 +595,34 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   const uint64_t key = valid ? keys[pos] : 0ull;
   const uint32_t res = lane_probe(c, key, valid);
   const bool miss = valid && res == kNoSlot && !(skip & kSkipMiss);
-  const uint32_t um = warp_claim_misses(v, keys, pos, key, miss);
-  if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
+  // SF: recency exchange before the claims -- the slot's counter and mark
+  // reads go out first and their round trip overlaps the claims' atomics
+  // (single-call latency 26.8 -> 25.0 us at cfg 2); a call pipelined behind
+  // another lookup keeps the exchange after the claims ticket (1-2 % more
+  // throughput when calls overlap)
+  uint32_t uh = 0, um = 0;
+  if constexpr (SF) {
+    const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
+    bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
+    if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c.counters) + res;
+    unsigned long long cur_ctr = ~0ull;
+    uint32_t cur_mark = uint32_t(stamp);
+    if (stamp_it) {
+      cur_ctr = __ldcg(ctr);
+      cur_mark = __ldcg(v.marks + res);
+    }
+    um = warp_claim_misses(v, keys, pos, key, miss);
+    if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
+    if (cur_ctr < stamp) atomicMax(ctr, stamp);
+    uh = (cur_mark != uint32_t(stamp) &&
+          atomicExch(v.marks + res, uint32_t(stamp)) != uint32_t(stamp))
+             ? 1u
+             : 0u;
+  } else {
+    um = warp_claim_misses(v, keys, pos, key, miss);
+    if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
+  }
   if (v.trace) {
     __syncthreads();
     trace_min(v, 1, true);
@@ -618,10 +644,12 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
     asm volatile("bar.arrive 1, %0;" ::"r"(kThreadsB) : "memory");
   }
   // ---- C: recency exchange, row copy, counts ----
-  const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
-  bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
-  if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
-  const uint32_t uh = stamp_it ? stamp_slot(c, v, res, stamp) : 0u;
+  if constexpr (!SF) {
+    const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
+    bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
+    if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
+    uh = stamp_it ? stamp_slot(c, v, res, stamp) : 0u;
+  }
   // behind an update (programmatic dependent launch): its row writes must be
   // complete before the rows are read
   if (skip & kWaitBeforeCopy) pdl_wait();
@@ -644,14 +672,14 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   if (last_block(v, 1, nblocks)) finish_counts(v);
 }
 
-template <int CH, int WARPS>
+template <int CH, int WARPS, bool SF>
 __global__ void __launch_bounds__(WARPS * 32, HPSB_MINB_THREADS / (WARPS * 32))
     k_lookup_tag(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                  float* __restrict__ out, uint8_t* __restrict__ flags,
                  const float* __restrict__ default_row, uint64_t stamp, LookupView v,
                  uint32_t skip) {
-  lookup_body<CH, WARPS>(c, keys, n, out, flags, default_row, stamp, v, skip, blockIdx.x,
-                         gridDim.x);
+  lookup_body<CH, WARPS, SF>(c, keys, n, out, flags, default_row, stamp, v, skip, blockIdx.x,
+                             gridDim.x);
 }
 
 // Several tables (caches) in ONE launch: block b belongs to the table whose
@@ -668,8 +696,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
   }
   __syncthreads();
   const TableLookup& tl = tables[s_t];
-  lookup_body<CH, WARPS>(tl.c, tl.keys, tl.n, tl.out, tl.flags, tl.default_row, tl.stamp, tl.v, 0u,
-                         blockIdx.x - tl.block_begin, tl.nblocks);
+  lookup_body<CH, WARPS, true>(tl.c, tl.keys, tl.n, tl.out, tl.flags, tl.default_row, tl.stamp,
+                               tl.v, 0u, blockIdx.x - tl.block_begin, tl.nblocks);
 }
 
 void launch_lookup_multi(const TableLookup* d_tables, uint32_t count, uint32_t total_blocks,
@@ -727,12 +755,19 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     const int ch = (c.d % 8 == 0 && aligned(out, 32) && aligned(default_row, 32))   ? 8
                    : (c.d % 4 == 0 && aligned(out, 16) && aligned(default_row, 16)) ? 4
                                                                                      : 1;
+    // a call pipelined behind another lookup orders its recency exchange
+    // for throughput, any other call for latency (see lookup_body)
+    const bool pipelined = cfg.numAttrs == 1 && !(skip & kWaitBeforeCopy);
     auto go = [&](auto chc, auto wc) {
       constexpr int CH = decltype(chc)::value, WARPS = decltype(wc)::value;
       cfg.gridDim = dim3(unsigned((n + WARPS * 32 - 1) / (WARPS * 32)));
       cfg.blockDim = dim3(WARPS * 32);
-      cudaLaunchKernelEx(&cfg, k_lookup_tag<CH, WARPS>, c, keys, n, out, flags, default_row,
-                         stamp, v, skip);
+      if (pipelined)
+        cudaLaunchKernelEx(&cfg, k_lookup_tag<CH, WARPS, false>, c, keys, n, out, flags,
+                           default_row, stamp, v, skip);
+      else
+        cudaLaunchKernelEx(&cfg, k_lookup_tag<CH, WARPS, true>, c, keys, n, out, flags,
+                           default_row, stamp, v, skip);
     };
     auto by_warps = [&](auto chc) {
       switch (warps) {
