@@ -519,6 +519,12 @@ __global__ void __launch_bounds__(kThreads)
 #ifndef HPSB_COPY_U
 #define HPSB_COPY_U 2
 #endif
+#ifndef HPSB_SINGLE_COPY_U
+#define HPSB_SINGLE_COPY_U 4
+#endif
+#ifndef HPSB_SINGLE_MINB_THREADS
+#define HPSB_SINGLE_MINB_THREADS 1024
+#endif
 #ifndef HPSB_MINB_THREADS
 #define HPSB_MINB_THREADS 1536
 #endif
@@ -654,9 +660,12 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   // complete before the rows are read
   if (skip & kWaitBeforeCopy) pdl_wait();
   const uint32_t nrows = n > base + 32 ? 32u : uint32_t(n > base ? n - base : 0);
+  // a lone call has the SMs to itself: twice the chunks in flight per lane
+  // (single-call latency -1.7 us at cfg 2); pipelined calls keep registers
+  // low so several calls stay resident
+  constexpr int kU = SF ? HPSB_SINGLE_COPY_U : HPSB_COPY_U;
   if (!(skip & kSkipCopy))
-    warp_copy_rows<CH, CH == 8 ? HPSB_COPY_U : 2 * HPSB_COPY_U>(c, res, nrows, default_row,
-                                                              out + base * c.d);
+    warp_copy_rows<CH, CH == 8 ? kU : 2 * kU>(c, res, nrows, default_row, out + base * c.d);
   warp_add_counts(v, uh, um, blk * WARPS + (threadIdx.x >> 5));
   if (v.trace) {
     __syncthreads();
@@ -673,7 +682,8 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
 }
 
 template <int CH, int WARPS, bool SF>
-__global__ void __launch_bounds__(WARPS * 32, HPSB_MINB_THREADS / (WARPS * 32))
+__global__ void __launch_bounds__(WARPS * 32,
+                                  (SF ? HPSB_SINGLE_MINB_THREADS : HPSB_MINB_THREADS) / (WARPS * 32))
     k_lookup_tag(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                  float* __restrict__ out, uint8_t* __restrict__ flags,
                  const float* __restrict__ default_row, uint64_t stamp, LookupView v,
