@@ -240,6 +240,84 @@ __global__ void k_replace_validate(const uint64_t* __restrict__ keys, ReplaceScr
   if (__any_sync(0xFFFFFFFFu, dup) && lane == 0) atomicOr(rs.dup_flag, 1u);
 }
 
+// One key of a set, applied by a whole warp (slab_cache.cpp:261-326): ballot
+// probe of the set's slabs in probe order; resident -> recency refresh only;
+// else insert at the lowest free slot of the first non-full probed slab; else
+// evict the minimum counter of the set, ties to the lowest (slab, slot).
+__device__ __forceinline__ void warp_replace_key(const CacheDev& c, uint64_t set, uint64_t key,
+                                                 const float* __restrict__ row, uint64_t stamp) {
+  const uint32_t lane = lane_id();
+  volatile uint32_t* vmask = c.masks;
+  volatile uint64_t* vkeys = c.keys;
+  volatile uint64_t* vctr = c.counters;
+  const uint64_t per_set = uint64_t(c.W) * kSlotsPerSlab;
+  const uint32_t first = first_slab_of(c, key);
+  int64_t found = -1;
+  int64_t ins_slab = -1;
+  for (uint32_t step = 0; step < c.W; ++step) {
+    uint32_t sl = first + step;
+    sl = (sl >= c.W) ? sl - c.W : sl;
+    const uint64_t slab = set * c.W + sl;
+    const uint32_t m = vmask[slab];
+    const uint64_t k = vkeys[slab * kSlotsPerSlab + lane];
+    const uint32_t hitb = __ballot_sync(0xFFFFFFFFu, ((m >> lane) & 1u) && k == key);
+    if (hitb) {
+      found = int64_t(slab * kSlotsPerSlab + (__ffs(hitb) - 1));
+      break;
+    }
+    if (m != kFullSlab) {
+      ins_slab = int64_t(slab);
+      break;
+    }
+  }
+  if (found >= 0) {
+    // resident: recency refresh only, vector kept (slab_cache.cpp:283-288)
+    if (lane == 0) vctr[found] = stamp;
+    __syncwarp();
+    return;
+  }
+  uint64_t slot;
+  if (ins_slab >= 0) {
+    const uint32_t m = vmask[ins_slab];
+    const uint32_t j = __ffs(~m) - 1;  // countr_one(mask) (slab_cache.cpp:299)
+    slot = uint64_t(ins_slab) * kSlotsPerSlab + j;
+    if (lane == 0) {
+      vmask[ins_slab] = m | (1u << j);
+      atomicAdd(c.occupied, 1ull);
+    }
+  } else {
+    // all slabs full: evict min counter, ties to lowest (slab, slot)
+    const uint64_t base = set * per_set;
+    uint64_t best_c = ~0ull;
+    uint32_t best_i = 0xFFFFFFFFu;
+    for (uint32_t s = lane; s < per_set; s += 32) {
+      const uint64_t cv = vctr[base + s];
+      if (cv < best_c) {
+        best_c = cv;
+        best_i = s;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, best_c, o);
+      const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, best_i, o);
+      if (oc < best_c || (oc == best_c && oi < best_i)) {
+        best_c = oc;
+        best_i = oi;
+      }
+    }
+    slot = base + best_i;
+  }
+  if (lane == 0) {
+    vkeys[slot] = key;
+    vctr[slot] = stamp;
+    c.tags[slot] = key_tag(xxh64_key(key, kSlabSeed));
+  }
+  warp_copy_row(row, c.rows + slot * c.d, c.d);
+  __threadfence_block();
+  __syncwarp();
+}
+
 __global__ void k_replace_apply(CacheDev c, const uint64_t* __restrict__ keys,
                                 const float* __restrict__ rows, uint64_t stamp,
                                 ReplaceScratch rs) {
@@ -250,86 +328,96 @@ __global__ void k_replace_apply(CacheDev c, const uint64_t* __restrict__ keys,
   if (*reinterpret_cast<volatile uint32_t*>(rs.dup_flag)) return;  // rejected before mutation
   uint32_t* b = rs.bucket + rs.tab_off[t];
   warp_sort_group(b, cnt);
-  const uint32_t lane = lane_id();
   const uint64_t set = rs.tab_set[t];
-  volatile uint32_t* vmask = c.masks;
-  volatile uint64_t* vkeys = c.keys;
-  volatile uint64_t* vctr = c.counters;
-  const uint64_t per_set = uint64_t(c.W) * kSlotsPerSlab;
   for (uint32_t g = 0; g < cnt; ++g) {
     const uint32_t i = b[g];
-    const uint64_t key = keys[i];
-    const uint32_t first = first_slab_of(c, key);
-    int64_t found = -1;
-    int64_t ins_slab = -1;
-    for (uint32_t step = 0; step < c.W; ++step) {
-      uint32_t sl = first + step;
-      sl = (sl >= c.W) ? sl - c.W : sl;
-      const uint64_t slab = set * c.W + sl;
-      const uint32_t m = vmask[slab];
-      const uint64_t k = vkeys[slab * kSlotsPerSlab + lane];
-      const uint32_t hitb = __ballot_sync(0xFFFFFFFFu, ((m >> lane) & 1u) && k == key);
-      if (hitb) {
-        found = int64_t(slab * kSlotsPerSlab + (__ffs(hitb) - 1));
-        break;
-      }
-      if (m != kFullSlab) {
-        ins_slab = int64_t(slab);
-        break;
-      }
-    }
-    if (found >= 0) {
-      // resident: recency refresh only, vector kept (slab_cache.cpp:283-288)
-      if (lane == 0) vctr[found] = stamp;
-      __syncwarp();
-      continue;
-    }
-    uint64_t slot;
-    if (ins_slab >= 0) {
-      const uint32_t m = vmask[ins_slab];
-      const uint32_t j = __ffs(~m) - 1;  // countr_one(mask) (slab_cache.cpp:299)
-      slot = uint64_t(ins_slab) * kSlotsPerSlab + j;
-      if (lane == 0) {
-        vmask[ins_slab] = m | (1u << j);
-        atomicAdd(c.occupied, 1ull);
-      }
-    } else {
-      // all slabs full: evict min counter, ties to lowest (slab, slot)
-      const uint64_t base = set * per_set;
-      uint64_t best_c = ~0ull;
-      uint32_t best_i = 0xFFFFFFFFu;
-      for (uint32_t s = lane; s < per_set; s += 32) {
-        const uint64_t cv = vctr[base + s];
-        if (cv < best_c) {
-          best_c = cv;
-          best_i = s;
+    warp_replace_key(c, set, keys[i], rows + uint64_t(i) * c.d, stamp);
+  }
+}
+
+// Small batches (the engine's per-call unique misses at small batch sizes;
+// n <= kSmallReplaceMax) in ONE single-block launch without scratch
+// memsets -- 32 warps take the touched sets 32 at a time, so beyond a few
+// hundred keys the multi-kernel path's warp per set wins: (set, index) pairs
+// bitonic-sorted in shared memory (input order within each set), one warp per
+// set applying its keys serially as above; the duplicate check (device-mode
+// replace) runs over each set's keys before any mutation.
+constexpr uint32_t kSmallReplace = 1024;   // block size (and sort capacity)
+constexpr uint32_t kSmallReplaceMax = 256;  // dispatch limit
+
+__global__ void __launch_bounds__(kSmallReplace)
+    k_replace_small(CacheDev c, const uint64_t* __restrict__ keys, uint32_t n,
+                    const float* __restrict__ rows, uint64_t stamp, uint32_t validate,
+                    ReplaceScratch rs) {
+  __shared__ unsigned long long sk[kSmallReplace];
+  __shared__ uint32_t s_heads[kSmallReplace];
+  __shared__ uint32_t s_nheads, s_dup;
+  const uint32_t t = threadIdx.x;
+  uint32_t P = 1;
+  while (P < n) P <<= 1;
+  if (t == 0) {
+    s_nheads = 0;
+    s_dup = 0;
+  }
+  if (t < P) sk[t] = t < n ? (slabset_of(c, keys[t]) << 10) | t : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t x = t ^ j;
+      if (t < P && x > t) {
+        const unsigned long long a = sk[t], b = sk[x];
+        if ((a > b) == ((t & k) == 0)) {
+          sk[t] = b;
+          sk[x] = a;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, best_c, o);
-        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, best_i, o);
-        if (oc < best_c || (oc == best_c && oi < best_i)) {
-          best_c = oc;
-          best_i = oi;
-        }
+      __syncthreads();
+    }
+  }
+  if (t < n && (t == 0 || (sk[t] >> 10) != (sk[t - 1] >> 10))) s_heads[atomicAdd(&s_nheads, 1u)] = t;
+  __syncthreads();
+  const uint32_t warp = t >> 5, lane = t & 31u, nh = s_nheads;
+  if (validate) {
+    for (uint32_t h = warp; h < nh; h += kSmallReplace / 32) {
+      const uint32_t s0 = s_heads[h];
+      const unsigned long long set = sk[s0] >> 10;
+      uint32_t e = s0 + 1;
+      while (e < n && (sk[e] >> 10) == set) ++e;
+      bool dup = false;
+      for (uint32_t x = s0 + lane; x < e; x += 32) {
+        const uint64_t kx = keys[sk[x] & 1023u];
+        for (uint32_t y = x + 1; y < e; ++y) dup |= keys[sk[y] & 1023u] == kx;
       }
-      slot = base + best_i;
+      if (__any_sync(0xFFFFFFFFu, dup) && lane == 0) atomicOr(&s_dup, 1u);
     }
-    if (lane == 0) {
-      vkeys[slot] = key;
-      vctr[slot] = stamp;
-      c.tags[slot] = key_tag(xxh64_key(key, kSlabSeed));
+    __syncthreads();
+  }
+  if (!s_dup) {
+    for (uint32_t h = warp; h < nh; h += kSmallReplace / 32) {
+      const uint32_t s0 = s_heads[h];
+      const unsigned long long set = sk[s0] >> 10;
+      for (uint32_t g = s0; g < n && (sk[g] >> 10) == set; ++g) {
+        const uint32_t i = uint32_t(sk[g] & 1023u);
+        warp_replace_key(c, set, keys[i], rows + uint64_t(i) * c.d, stamp);
+      }
     }
-    warp_copy_row(rows + uint64_t(i) * c.d, c.rows + slot * c.d, c.d);
-    __threadfence_block();
-    __syncwarp();
+  }
+  if (t == 0) {
+    rs.cursor[0] = 0u;
+    rs.dup_flag[0] = s_dup;
   }
 }
 
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st) {
   if (n == 0) return;
+  static const bool no_small = std::getenv("HPSB_REPLACE_NO_SMALL") != nullptr;
+  if (n <= kSmallReplaceMax && !no_small) {
+    k_replace_small<<<1, kSmallReplace, 0, st>>>(c, keys, uint32_t(n), rows, stamp,
+                                                 validate ? 1u : 0u, rs);
+    check_launch("replace", 1);
+    return;
+  }
   cudaMemsetAsync(rs.tab_set, 0xFF, rs.cap * 8, st);
   // tab_cnt, tab_fill are contiguous (carve order); cursor + dup_flag after buckets
   cudaMemsetAsync(rs.tab_cnt, 0, rs.cap * 4, st);

@@ -186,8 +186,9 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   uint64_t cap = 1024;
   while (cap < n) cap <<= 1;
   const uint64_t ls_bytes = lookup_scratch_bytes(cap);
+  const uint64_t hdr_bytes = 16 + cap * 4 + 8 + cap * 8 + cap;
   const uint64_t dev_bytes = a256(cap * 8) * 3 + a256(cap * uint64_t(d) * 4) * 2 + a256(cap) +
-                             a256(cap * 4) + a256(ls_bytes);
+                             a256(cap * 4) + a256(ls_bytes) + a256(hdr_bytes);
   HPSB_CUDA(cudaStreamSynchronize(st));
   char* p = static_cast<char*>(dbuf.ensure(dev_bytes, st));
   auto take = [&](uint64_t bytes) {
@@ -201,12 +202,13 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   d_row_of = reinterpret_cast<int32_t*>(take(cap * 4));
   d_staged = reinterpret_cast<float*>(take(cap * uint64_t(d) * 4));
   d_found_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
+  d_hdr = take(hdr_bytes);
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);
 
   const uint64_t host_bytes = a256(cap * 8) * 5 + a256(16) + a256(cap * 4) * 3 +
-                              a256(cap * uint64_t(d) * 4) * 2 + a256(cap);
+                              a256(cap * uint64_t(d) * 4) * 2 + a256(cap) + a256(hdr_bytes);
   char* h = static_cast<char*>(hbuf.ensure(host_bytes));
   auto htake = [&](uint64_t bytes) {
     char* r = h;
@@ -225,6 +227,7 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   h_claim_keys = reinterpret_cast<uint64_t*>(htake(cap * 8));
   h_claim_firsts = reinterpret_cast<uint32_t*>(htake(cap * 4));
   h_row_of_claim = reinterpret_cast<int32_t*>(htake(cap * 4));
+  h_hdr = htake(hdr_bytes);
   HPSB_CUDA(cudaStreamSynchronize(st));
   capacity = cap;
   dim = d;
@@ -401,23 +404,51 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
       }
       ws->lv = lookup_next_view(ws->ls, /*chain=*/false);
       ws->lv.marks = cache_->lookup_marks_locked(stamp);
+      // small host-mode call: counts, claims and flags written into one
+      // packed region [counts | first positions | keys | flags] that comes
+      // back in one copy (three or four small copies otherwise)
+      c.packed = host && n <= kPackedMax;
+      uint64_t packed_bytes = 0;
+      if (c.packed) {
+        const uint64_t fo = 16, ko = 16 + (n * 4 + 7) / 8 * 8, flo = ko + n * 8;
+        packed_bytes = flo + n;
+        ws->lv.counts_out = reinterpret_cast<unsigned long long*>(ws->d_hdr);
+        ws->lv.list_firsts = reinterpret_cast<uint32_t*>(ws->d_hdr + fo);
+        ws->lv.list_keys = reinterpret_cast<uint64_t*>(ws->d_hdr + ko);
+        c.d_flags = reinterpret_cast<uint8_t*>(ws->d_hdr + flo);
+        c.hc = reinterpret_cast<const unsigned long long*>(ws->h_hdr);
+        c.hcf = reinterpret_cast<const uint32_t*>(ws->h_hdr + fo);
+        c.hck = reinterpret_cast<const uint64_t*>(ws->h_hdr + ko);
+        c.hfl = reinterpret_cast<const uint8_t*>(ws->h_hdr + flo);
+      }
       cache_->note_stream_op();  // the engine's own copies follow on the stream
       launch_lookup_probe(cache_->dev(), c.d_keys, n, c.d_out, c.d_flags, d_default_, stamp,
                           ws->lv, /*after_lookup=*/false, st);
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->lv.counts_out, 16, cudaMemcpyDeviceToHost, st));
-      // One host round trip on the common path: the first claims and -- when
-      // the previous call took the async branch, whose rows are final as the
-      // kernel leaves them -- the rows and flags come back with the counts.
-      c.spec_claims = std::min<uint64_t>(n, kSpeculativeClaims);
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, c.spec_claims * 8,
-                                cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, c.spec_claims * 4,
-                                cudaMemcpyDeviceToHost, st));
-      if (host && c.spec_rows) {
-        HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, c.d_out, n * uint64_t(d) * 4,
+      if (c.packed) {
+        HPSB_CUDA(cudaMemcpyAsync(ws->h_hdr, ws->d_hdr, packed_bytes, cudaMemcpyDeviceToHost, st));
+        c.spec_claims = n;
+        if (c.spec_rows)
+          HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, c.d_out, n * uint64_t(d) * 4,
+                                    cudaMemcpyDeviceToHost, st));
+      } else {
+        HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->lv.counts_out, 16, cudaMemcpyDeviceToHost, st));
+        // One host round trip on the common path: the first claims and -- when
+        // the previous call took the async branch, whose rows are final as the
+        // kernel leaves them -- the rows and flags come back with the counts.
+        c.spec_claims = std::min<uint64_t>(n, kSpeculativeClaims);
+        c.hc = ws->h_counts;
+        c.hcf = ws->h_claim_firsts;
+        c.hck = ws->h_claim_keys;
+        HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys, ws->lv.list_keys, c.spec_claims * 8,
                                   cudaMemcpyDeviceToHost, st));
-        HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, c.d_flags, n,
+        HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, c.spec_claims * 4,
                                   cudaMemcpyDeviceToHost, st));
+        if (host && c.spec_rows) {
+          HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, c.d_out, n * uint64_t(d) * 4,
+                                    cudaMemcpyDeviceToHost, st));
+          HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, c.d_flags, n,
+                                    cudaMemcpyDeviceToHost, st));
+        }
       }
       HPSB_CUDA(cudaEventRecord(ws->done, st));
     }
@@ -452,8 +483,8 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   uint64_t uh = 0, um = 0;
   if (n > 0) {
     HPSB_CUDA(cudaEventSynchronize(ws->done));
-    uh = ws->h_counts[0];
-    um = ws->h_counts[1];
+    uh = c.hc[0];
+    um = c.hc[1];
     if (um > c.spec_claims) {
       HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys + c.spec_claims,
                                 ws->lv.list_keys + c.spec_claims, (um - c.spec_claims) * 8,
@@ -469,10 +500,10 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
       // (types.cpp:20-34 + slab_cache.cpp:84-89)
       ws->order.resize(um);
       for (uint32_t e = 0; e < um; ++e) ws->order[e] = e;
-      const uint32_t* fp = ws->h_claim_firsts;
+      const uint32_t* fp = c.hcf;
       std::sort(ws->order.begin(), ws->order.end(),
                 [fp](uint32_t a, uint32_t b) { return fp[a] < fp[b]; });
-      for (uint64_t k = 0; k < um; ++k) ws->h_miss_keys[k] = ws->h_claim_keys[ws->order[k]];
+      for (uint64_t k = 0; k < um; ++k) ws->h_miss_keys[k] = c.hck[ws->order[k]];
     }
   }
   const uint64_t n_unique = uh + um;
@@ -508,17 +539,23 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   last_async_.store(!sync_branch, std::memory_order_relaxed);
   if (n > 0) {
     if (host) {
+      // packed async-branch calls: the flags in the packed copy are final
+      const bool packed_flags = c.packed && !sync_branch;
       if (sync_branch || !c.spec_rows) {
         HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
                                   cudaMemcpyDeviceToHost, st));
-        HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
-                                  cudaMemcpyDeviceToHost, st));
+        if (!packed_flags)
+          HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
+                                    cudaMemcpyDeviceToHost, st));
         HPSB_CUDA(cudaEventRecord(ws->done, st));
         HPSB_CUDA(cudaEventSynchronize(ws->done));
       }
       ws->pending = false;
       if (!c.out_pinned) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
-      if (!c.flags_pinned) std::memcpy(flags, ws->h_flags, n);
+      if (packed_flags)
+        std::memcpy(flags, c.hfl, n);
+      else if (!c.flags_pinned)
+        std::memcpy(flags, ws->h_flags, n);
     } else {
       cache_->join_to(c.user);
     }

@@ -90,6 +90,7 @@ struct Workspace {
   int32_t* d_row_of = nullptr;
   float* d_staged = nullptr;
   uint64_t* d_found_keys = nullptr;
+  char* d_hdr = nullptr;  // packed per-call results (small host-mode calls)
   LookupScratch ls;
   LookupView lv;  // the view of the last lookup
   // pinned host
@@ -106,6 +107,7 @@ struct Workspace {
   uint64_t* h_claim_keys = nullptr;    // unique misses in claim order
   uint32_t* h_claim_firsts = nullptr;  // their first positions
   int32_t* h_row_of_claim = nullptr;   // staged row per claim (sync branch)
+  char* h_hdr = nullptr;               // pinned mirror of d_hdr
   std::vector<uint32_t> order;         // claims sorted by first position
   // batch state (for the async task)
   std::vector<uint64_t> missing_keys;
@@ -178,6 +180,7 @@ class LookupEngine {
   // claims copied back speculatively with the counts (one round trip when a
   // call has at most this many unique misses)
   static constexpr uint64_t kSpeculativeClaims = 4096;
+  static constexpr uint64_t kPackedMax = 4096;
   // one lookup split at its first host wait (begin enqueues, finish waits)
   struct LookupCall {
     LookupEngine* engine = nullptr;
@@ -189,6 +192,13 @@ class LookupEngine {
     cudaStream_t user = nullptr;
     bool host = true, spec_rows = false, out_pinned = false, flags_pinned = false;
     uint64_t spec_claims = 0;
+    // packed: counts, every claim (first positions, keys) and the flags come
+    // back in ONE device-to-host copy (host-mode calls of <= kPackedMax keys)
+    bool packed = false;
+    const unsigned long long* hc = nullptr;
+    const uint32_t* hcf = nullptr;
+    const uint64_t* hck = nullptr;
+    const uint8_t* hfl = nullptr;
     const uint64_t* d_keys = nullptr;
     float* d_out = nullptr;
     uint8_t* d_flags = nullptr;
