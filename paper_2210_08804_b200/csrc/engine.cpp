@@ -13,6 +13,17 @@ namespace hpsb {
 namespace {
 inline uint64_t a256(uint64_t v) { return (v + 255) / 256 * 256; }
 
+// Device-accessible address of pinned host memory (cudaHostAlloc'd or
+// registered), nullptr for pageable memory.
+const void* mapped(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -389,7 +400,22 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
     std::lock_guard<std::mutex> lk(cache_->mutex());
     const uint64_t stamp = cache_->bump_clock();  // query ticks even when empty
     if (n > 0) {
-      if (host) {
+      // small host-mode call (packed): zero-copy -- the kernel reads the keys
+      // from pinned host memory and writes rows, flags, counts and every
+      // claim straight into pinned host memory ([counts | first positions |
+      // keys | flags] in h_hdr); no copies, one host wait on the kernel
+      c.packed = host && n <= kPackedMax;
+      if (c.packed) {
+        const void* mk = mapped(keys);
+        if (mk == nullptr) {
+          std::memcpy(ws->h_keys, keys, n * 8);
+          mk = ws->h_keys;
+        }
+        c.d_keys = static_cast<const uint64_t*>(mk);
+        float* mo = c.out_pinned ? static_cast<float*>(const_cast<void*>(mapped(out))) : nullptr;
+        c.out_direct = mo != nullptr;
+        c.d_out = c.out_direct ? mo : ws->h_out;
+      } else if (host) {
         if (is_pinned(keys)) {
           HPSB_CUDA(cudaMemcpyAsync(ws->d_keys, keys, n * 8, cudaMemcpyHostToDevice, st));
         } else {
@@ -404,33 +430,22 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
       }
       ws->lv = lookup_next_view(ws->ls, /*chain=*/false);
       ws->lv.marks = cache_->lookup_marks_locked(stamp);
-      // small host-mode call: counts, claims and flags written into one
-      // packed region [counts | first positions | keys | flags] that comes
-      // back in one copy (three or four small copies otherwise)
-      c.packed = host && n <= kPackedMax;
-      uint64_t packed_bytes = 0;
       if (c.packed) {
         const uint64_t fo = 16, ko = 16 + (n * 4 + 7) / 8 * 8, flo = ko + n * 8;
-        packed_bytes = flo + n;
-        ws->lv.counts_out = reinterpret_cast<unsigned long long*>(ws->d_hdr);
-        ws->lv.list_firsts = reinterpret_cast<uint32_t*>(ws->d_hdr + fo);
-        ws->lv.list_keys = reinterpret_cast<uint64_t*>(ws->d_hdr + ko);
-        c.d_flags = reinterpret_cast<uint8_t*>(ws->d_hdr + flo);
+        ws->lv.counts_out = reinterpret_cast<unsigned long long*>(ws->h_hdr);
+        ws->lv.list_firsts = reinterpret_cast<uint32_t*>(ws->h_hdr + fo);
+        ws->lv.list_keys = reinterpret_cast<uint64_t*>(ws->h_hdr + ko);
+        c.d_flags = reinterpret_cast<uint8_t*>(ws->h_hdr + flo);
         c.hc = reinterpret_cast<const unsigned long long*>(ws->h_hdr);
         c.hcf = reinterpret_cast<const uint32_t*>(ws->h_hdr + fo);
         c.hck = reinterpret_cast<const uint64_t*>(ws->h_hdr + ko);
         c.hfl = reinterpret_cast<const uint8_t*>(ws->h_hdr + flo);
+        c.spec_claims = n;
       }
       cache_->note_stream_op();  // the engine's own copies follow on the stream
       launch_lookup_probe(cache_->dev(), c.d_keys, n, c.d_out, c.d_flags, d_default_, stamp,
                           ws->lv, /*after_lookup=*/false, st);
-      if (c.packed) {
-        HPSB_CUDA(cudaMemcpyAsync(ws->h_hdr, ws->d_hdr, packed_bytes, cudaMemcpyDeviceToHost, st));
-        c.spec_claims = n;
-        if (c.spec_rows)
-          HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, c.d_out, n * uint64_t(d) * 4,
-                                    cudaMemcpyDeviceToHost, st));
-      } else {
+      if (!c.packed) {
         HPSB_CUDA(cudaMemcpyAsync(ws->h_counts, ws->lv.counts_out, 16, cudaMemcpyDeviceToHost, st));
         // One host round trip on the common path: the first claims and -- when
         // the previous call took the async branch, whose rows are final as the
@@ -520,15 +535,32 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
     if (nf > 0) {
       // row_of is in miss order; the scatter kernel indexes by claim
       for (uint64_t k = 0; k < um; ++k) ws->h_row_of_claim[ws->order[k]] = ws->h_row_of[k];
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, um * 4, cudaMemcpyHostToDevice,
-                                st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
-                                cudaMemcpyHostToDevice, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
-                                cudaMemcpyHostToDevice, st));
-      cache_->note_stream_op();
-      launch_lookup_scatter(n, d, d_flags, ws->lv, ws->d_row_of, ws->d_staged, d_out, st);
-      cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+      if (c.packed) {
+        // zero-copy: the scatter reads the staged rows from pinned host
+        // memory and writes the caller's rows / flags there; a small replace
+        // (one single-block kernel) reads its keys and rows from it too
+        cache_->note_stream_op();
+        launch_lookup_scatter(n, d, d_flags, ws->lv, ws->h_row_of_claim, ws->h_staged, d_out, st);
+        if (nf <= kZeroCopyReplaceMax) {
+          cache_->replace_device_locked(ws->h_found_keys, nf, ws->h_staged);
+        } else {
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                    cudaMemcpyHostToDevice, st));
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                    cudaMemcpyHostToDevice, st));
+          cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+        }
+      } else {
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, um * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                  cudaMemcpyHostToDevice, st));
+        cache_->note_stream_op();
+        launch_lookup_scatter(n, d, d_flags, ws->lv, ws->d_row_of, ws->d_staged, d_out, st);
+        cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+      }
     }
     HPSB_CUDA(cudaEventRecord(ws->done, st));
     ws->pending = true;
@@ -538,24 +570,25 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
 
   last_async_.store(!sync_branch, std::memory_order_relaxed);
   if (n > 0) {
-    if (host) {
-      // packed async-branch calls: the flags in the packed copy are final
-      const bool packed_flags = c.packed && !sync_branch;
+    if (host && c.packed) {
+      // zero-copy call: rows and flags are already in host memory once the
+      // kernels are done (the sync branch's scatter + replace waited here)
+      if (sync_branch) HPSB_CUDA(cudaEventSynchronize(ws->done));
+      ws->pending = false;
+      if (!c.out_direct) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
+      std::memcpy(flags, c.hfl, n);
+    } else if (host) {
       if (sync_branch || !c.spec_rows) {
         HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
                                   cudaMemcpyDeviceToHost, st));
-        if (!packed_flags)
-          HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
-                                    cudaMemcpyDeviceToHost, st));
+        HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
+                                  cudaMemcpyDeviceToHost, st));
         HPSB_CUDA(cudaEventRecord(ws->done, st));
         HPSB_CUDA(cudaEventSynchronize(ws->done));
       }
       ws->pending = false;
       if (!c.out_pinned) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
-      if (packed_flags)
-        std::memcpy(flags, c.hfl, n);
-      else if (!c.flags_pinned)
-        std::memcpy(flags, ws->h_flags, n);
+      if (!c.flags_pinned) std::memcpy(flags, ws->h_flags, n);
     } else {
       cache_->join_to(c.user);
     }

@@ -181,6 +181,7 @@ class LookupEngine {
   // call has at most this many unique misses)
   static constexpr uint64_t kSpeculativeClaims = 4096;
   static constexpr uint64_t kPackedMax = 4096;
+  static constexpr uint64_t kZeroCopyReplaceMax = 256;  // = the single-block replace limit
   // one lookup split at its first host wait (begin enqueues, finish waits)
   struct LookupCall {
     LookupEngine* engine = nullptr;
@@ -192,9 +193,11 @@ class LookupEngine {
     cudaStream_t user = nullptr;
     bool host = true, spec_rows = false, out_pinned = false, flags_pinned = false;
     uint64_t spec_claims = 0;
-    // packed: counts, every claim (first positions, keys) and the flags come
-    // back in ONE device-to-host copy (host-mode calls of <= kPackedMax keys)
-    bool packed = false;
+    // packed: zero-copy call (host mode, <= kPackedMax keys): the kernels read
+    // keys and write rows, flags, counts and every claim (first positions,
+    // keys) in pinned host memory; out_direct = rows go to the caller's own
+    // pinned `out`
+    bool packed = false, out_direct = false;
     const unsigned long long* hc = nullptr;
     const uint32_t* hcf = nullptr;
     const uint64_t* hck = nullptr;
