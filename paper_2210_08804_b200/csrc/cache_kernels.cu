@@ -252,6 +252,71 @@ __device__ __forceinline__ void warp_replace_key(const CacheDev& c, uint64_t set
   volatile uint64_t* vctr = c.counters;
   const uint64_t per_set = uint64_t(c.W) * kSlotsPerSlab;
   const uint32_t first = first_slab_of(c, key);
+  // rows of up to 128 floats: prefetched into registers with everything else
+  const bool pre = (c.d & 3u) == 0 && c.d <= 128 && (reinterpret_cast<uintptr_t>(row) & 15u) == 0;
+  float4 rv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (pre && lane < (c.d >> 2)) rv = reinterpret_cast<const float4*>(row)[lane];
+  if (c.W == 2) {
+    // both slabs' masks and keys and the set's 64 counters in ONE round trip
+    const uint64_t sa = set * 2 + first, sb = set * 2 + (first ^ 1u);
+    const uint32_t ma = vmask[sa], mb = vmask[sb];
+    const uint64_t ka = vkeys[sa * kSlotsPerSlab + lane], kb = vkeys[sb * kSlotsPerSlab + lane];
+    const uint64_t c0 = vctr[set * 64 + lane], c1 = vctr[set * 64 + 32 + lane];
+    uint64_t slot;
+    int64_t found = -1;
+    const uint32_t ha = __ballot_sync(0xFFFFFFFFu, ((ma >> lane) & 1u) && ka == key);
+    const uint32_t hb = __ballot_sync(0xFFFFFFFFu, ((mb >> lane) & 1u) && kb == key);
+    if (ha) {
+      found = int64_t(sa * kSlotsPerSlab + (__ffs(ha) - 1));
+    } else if (ma == kFullSlab && hb) {
+      found = int64_t(sb * kSlotsPerSlab + (__ffs(hb) - 1));
+    }
+    if (found >= 0) {
+      if (lane == 0) vctr[found] = stamp;  // resident: recency refresh only
+      __syncwarp();
+      return;
+    }
+    if (ma != kFullSlab || mb != kFullSlab) {
+      const uint64_t ins = ma != kFullSlab ? sa : sb;
+      const uint32_t m = ma != kFullSlab ? ma : mb;
+      const uint32_t j = __ffs(~m) - 1;  // countr_one(mask) (slab_cache.cpp:299)
+      slot = ins * kSlotsPerSlab + j;
+      if (lane == 0) {
+        vmask[ins] = m | (1u << j);
+        atomicAdd(c.occupied, 1ull);
+      }
+    } else {
+      uint64_t best_c = c0;
+      uint32_t best_i = lane;
+      if (c1 < best_c) {
+        best_c = c1;
+        best_i = lane + 32;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, best_c, o);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, best_i, o);
+        if (oc < best_c || (oc == best_c && oi < best_i)) {
+          best_c = oc;
+          best_i = oi;
+        }
+      }
+      slot = set * 64 + best_i;
+    }
+    if (lane == 0) {
+      vkeys[slot] = key;
+      vctr[slot] = stamp;
+      c.tags[slot] = key_tag(xxh64_key(key, kSlabSeed));
+    }
+    if (pre) {
+      if (lane < (c.d >> 2)) reinterpret_cast<float4*>(c.rows + slot * c.d)[lane] = rv;
+    } else {
+      warp_copy_row(row, c.rows + slot * c.d, c.d);
+    }
+    __threadfence_block();
+    __syncwarp();
+    return;
+  }
   int64_t found = -1;
   int64_t ins_slab = -1;
   for (uint32_t step = 0; step < c.W; ++step) {

@@ -182,6 +182,7 @@ Workspace::~Workspace() {
     cudaEventSynchronize(done);
     cudaEventDestroy(done);
   }
+  if (rows_ready) cudaEventDestroy(rows_ready);
 }
 
 void Workspace::wait_idle() {
@@ -193,6 +194,8 @@ void Workspace::wait_idle() {
 
 void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   if (done == nullptr) HPSB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  if (rows_ready == nullptr)
+    HPSB_CUDA(cudaEventCreateWithFlags(&rows_ready, cudaEventDisableTiming));
   if (n <= capacity && d == dim && dbuf.get() != nullptr) return;
   uint64_t cap = 1024;
   while (cap < n) cap <<= 1;
@@ -527,6 +530,7 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   const bool sync_branch = h < cfg_.hit_rate_threshold;
   TierCounters counters;
   uint64_t defaults = 0;
+  bool rows_event = false;
   if (sync_branch) {
     size_t nf = 0;
     const size_t absent = fetch_and_upload(*ws, ws->h_miss_keys, um, &counters, &nf);
@@ -541,6 +545,11 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
         // (one single-block kernel) reads its keys and rows from it too
         cache_->note_stream_op();
         launch_lookup_scatter(n, d, d_flags, ws->lv, ws->h_row_of_claim, ws->h_staged, d_out, st);
+        // the caller waits for the rows only; the replace runs on behind the
+        // return (stream-ordered before any later operation on the cache; the
+        // workspace is reused only after it, ws->done)
+        HPSB_CUDA(cudaEventRecord(ws->rows_ready, st));
+        rows_event = true;
         if (nf <= kZeroCopyReplaceMax) {
           cache_->replace_device_locked(ws->h_found_keys, nf, ws->h_staged);
         } else {
@@ -573,8 +582,8 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
     if (host && c.packed) {
       // zero-copy call: rows and flags are already in host memory once the
       // kernels are done (the sync branch's scatter + replace waited here)
-      if (sync_branch) HPSB_CUDA(cudaEventSynchronize(ws->done));
-      ws->pending = false;
+      if (rows_event) HPSB_CUDA(cudaEventSynchronize(ws->rows_ready));
+      if (!sync_branch) ws->pending = false;
       if (!c.out_direct) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
       std::memcpy(flags, c.hfl, n);
     } else if (host) {

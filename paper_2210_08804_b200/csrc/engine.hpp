@@ -112,6 +112,7 @@ struct Workspace {
   // batch state (for the async task)
   std::vector<uint64_t> missing_keys;
   cudaEvent_t done = nullptr;
+  cudaEvent_t rows_ready = nullptr;  // zero-copy sync branch: rows final (replace may run on)
   bool pending = false;  // `done` recorded, not yet waited
 
   ~Workspace();
