@@ -473,10 +473,48 @@ __global__ void __launch_bounds__(kSmallReplace)
   }
 }
 
+// Small batches without the duplicate check (the engine's fills: unique
+// misses): no sort at all -- one warp per key across as many blocks as
+// needed; the warp owning the FIRST key of a set (in input order) applies
+// every key of that set in input order, the others have nothing to do, so
+// all touched sets proceed in parallel.
+__global__ void __launch_bounds__(256)
+    k_replace_tiny(CacheDev c, const uint64_t* __restrict__ keys, uint32_t n,
+                   const float* __restrict__ rows, uint64_t stamp, ReplaceScratch rs) {
+  __shared__ unsigned long long s_set[kSmallReplaceMax];
+  __shared__ unsigned long long s_key[kSmallReplaceMax];
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+    const uint64_t k = keys[t];
+    s_key[t] = k;
+    s_set[t] = slabset_of(c, k);
+  }
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rs.cursor[0] = 0u;
+    rs.dup_flag[0] = 0u;
+  }
+  if (i >= n) return;
+  const unsigned long long set = s_set[i];
+  bool earlier = false;
+  for (uint32_t j = lane; j < i; j += 32) earlier |= s_set[j] == set;
+  if (__any_sync(0xFFFFFFFFu, earlier)) return;  // not the set's first key
+  for (uint32_t j = i; j < n; ++j) {
+    if (s_set[j] != set) continue;
+    warp_replace_key(c, set, s_key[j], rows + uint64_t(j) * c.d, stamp);
+  }
+}
+
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st) {
   if (n == 0) return;
   static const bool no_small = std::getenv("HPSB_REPLACE_NO_SMALL") != nullptr;
+  if (n <= kSmallReplaceMax && !no_small && !validate) {
+    k_replace_tiny<<<unsigned((n + 7) / 8), 256, 0, st>>>(c, keys, uint32_t(n), rows, stamp, rs);
+    check_launch("replace", 1);
+    return;
+  }
   if (n <= kSmallReplaceMax && !no_small) {
     k_replace_small<<<1, kSmallReplace, 0, st>>>(c, keys, uint32_t(n), rows, stamp,
                                                  validate ? 1u : 0u, rs);

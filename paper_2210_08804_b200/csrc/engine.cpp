@@ -443,6 +443,7 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
         c.hcf = reinterpret_cast<const uint32_t*>(ws->h_hdr + fo);
         c.hck = reinterpret_cast<const uint64_t*>(ws->h_hdr + ko);
         c.hfl = reinterpret_cast<const uint8_t*>(ws->h_hdr + flo);
+        ws->lv.flags_dev = ws->d_flags;
         c.spec_claims = n;
       }
       cache_->note_stream_op();  // the engine's own copies follow on the stream

@@ -113,6 +113,9 @@ struct LookupView {
   // as a unique hit (one array per concurrently running call, see
   // DeviceCache::lookup_marks_locked)
   uint32_t* marks = nullptr;
+  // zero-copy engine calls: a device copy of the miss flags (the output flags
+  // live in pinned host memory; the sync branch's scatter reads this copy)
+  uint8_t* flags_dev = nullptr;
 };
 // A ring of views: consecutive lookups on one stream take consecutive views,
 // so up to kLookupViews calls can be in flight (programmatic dependent

@@ -458,7 +458,10 @@ __global__ void __launch_bounds__(kThreads)
     tslot = miss_insert(v.miss_table, v.cap, keys, key, uint32_t(pos), &claimed);
     v.miss_slot[pos] = tslot;
   }
-  if (valid && sub == 0) flags[pos] = res == kNoSlot ? 1 : 0;
+  if (valid && sub == 0) {
+    flags[pos] = res == kNoSlot ? 1 : 0;
+    if (v.flags_dev != nullptr) v.flags_dev[pos] = res == kNoSlot ? 1 : 0;
+  }
   pdl_trigger();
   // recency exchange by the group's lane 0, issued before the copy
   bool stamp_it = valid && sub == 0 && res != kNoSlot;
@@ -619,7 +622,10 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
       cur_mark = __ldcg(v.marks + res);
     }
     um = warp_claim_misses(v, keys, pos, key, miss);
-    if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
+    if (valid) {
+      flags[pos] = res == kNoSlot ? 1 : 0;
+      if (v.flags_dev != nullptr) v.flags_dev[pos] = res == kNoSlot ? 1 : 0;
+    }
     if (cur_ctr < stamp) atomicMax(ctr, stamp);
     uh = (cur_mark != uint32_t(stamp) &&
           atomicExch(v.marks + res, uint32_t(stamp)) != uint32_t(stamp))
@@ -627,7 +633,10 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
              : 0u;
   } else {
     um = warp_claim_misses(v, keys, pos, key, miss);
-    if (valid) flags[pos] = res == kNoSlot ? 1 : 0;
+    if (valid) {
+      flags[pos] = res == kNoSlot ? 1 : 0;
+      if (v.flags_dev != nullptr) v.flags_dev[pos] = res == kNoSlot ? 1 : 0;
+    }
   }
   if (v.trace) {
     __syncthreads();
@@ -810,7 +819,7 @@ __global__ void __launch_bounds__(256)
                      float* __restrict__ out) {
   const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
-  if (flags[i] == 0) return;
+  if ((v.flags_dev != nullptr ? v.flags_dev[i] : flags[i]) == 0) return;
   const uint32_t e = v.claim_of_slot[v.miss_slot[i]];
   const int32_t r = row_of_claim[e];
   if (r < 0) return;  // absent from every tier: keep default + flag
