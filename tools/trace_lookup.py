@@ -30,6 +30,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--hit", type=float, default=0.9)
+    ap.add_argument("--batch", type=int, default=65536)
+    ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--isolated", action="store_true",
                     help="one call at a time (host sync between calls): single-call timeline")
@@ -37,7 +39,7 @@ def main():
                     help="cfg 4: stream-ordered update of this fraction of the resident rows "
                          "after every lookup")
     a = ap.parse_args()
-    wl = bench.Workload()
+    wl = bench.Workload(batch=a.batch, dim=a.dim)
     d, n = wl.dim, wl.batch
     cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=wl.S, slabs_per_set=wl.W, dimension=d),
                           device=0)
