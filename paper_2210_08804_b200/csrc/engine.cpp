@@ -663,21 +663,41 @@ void LookupEngine::finish_group(const GroupResult& r, LookupOutcome* outcome) {
     if (nf > 0) {
       std::lock_guard<std::mutex> lk(cache_->mutex());
       for (uint64_t k = 0; k < r.um; ++k) ws->h_row_of_claim[r.order[k]] = ws->h_row_of[k];
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, r.um * 4,
-                                cudaMemcpyHostToDevice, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
-                                cudaMemcpyHostToDevice, st));
-      HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
-                                cudaMemcpyHostToDevice, st));
-      cache_->note_stream_op();
-      launch_lookup_scatter(r.n, d, r.d_flags, r.v, ws->d_row_of, ws->d_staged, r.d_out, st);
-      cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
-      HPSB_CUDA(cudaMemcpyAsync(r.out, r.d_out, r.n * uint64_t(d) * 4, cudaMemcpyDeviceToHost,
-                                st));
-      HPSB_CUDA(cudaMemcpyAsync(r.flags, r.d_flags, r.n, cudaMemcpyDeviceToHost, st));
+      if (r.zero_copy) {
+        // rows, flags and staged rows all in pinned host memory
+        cache_->note_stream_op();
+        launch_lookup_scatter(r.n, d, r.d_flags, r.v, ws->h_row_of_claim, ws->h_staged, r.d_out,
+                              st);
+        if (nf <= kZeroCopyReplaceMax) {
+          cache_->replace_device_locked(ws->h_found_keys, nf, ws->h_staged);
+        } else {
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                    cudaMemcpyHostToDevice, st));
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                    cudaMemcpyHostToDevice, st));
+          cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+        }
+      } else {
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, r.um * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                  cudaMemcpyHostToDevice, st));
+        cache_->note_stream_op();
+        launch_lookup_scatter(r.n, d, r.d_flags, r.v, ws->d_row_of, ws->d_staged, r.d_out, st);
+        cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+        HPSB_CUDA(cudaMemcpyAsync(r.out, r.d_out, r.n * uint64_t(d) * 4, cudaMemcpyDeviceToHost,
+                                  st));
+        HPSB_CUDA(cudaMemcpyAsync(r.flags, r.d_flags, r.n, cudaMemcpyDeviceToHost, st));
+      }
     }
     HPSB_CUDA(cudaEventRecord(ws->done, st));
     HPSB_CUDA(cudaEventSynchronize(ws->done));
+    if (nf > 0 && r.zero_copy) {
+      std::memcpy(r.out, r.d_out, r.n * uint64_t(d) * 4);
+      std::memcpy(r.flags, r.d_flags, r.n);
+    }
   } else {
     defaults = r.um;
   }
@@ -804,6 +824,11 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
     roff[t + 1] = roff[t] + n[t] * eng_[t]->dim() + 7;  // keep 32 B alignment
     roff[t + 1] &= ~7ull;
   }
+  // small calls: zero-copy outputs -- the kernel writes counts, flags,
+  // claims and rows straight into the pinned mirror (same offsets), no
+  // device-to-host copies
+  const bool packed_rows = roff[T] * 4 <= kPackedRowBytes;
+  char* ob = packed_rows ? hb : db;
   uint32_t blocks = 0;
   std::vector<LookupView> views(T);
   for (uint64_t t = 0; t < T; ++t) {
@@ -814,16 +839,16 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
     c->note_stream_op();
     LookupView v = lookup_next_view(ls_[t], false);
     v.marks = c->lookup_marks_locked(stamp);
-    v.list_keys = reinterpret_cast<uint64_t*>(db + d_ckeys_) + koff[t];
-    v.list_firsts = reinterpret_cast<uint32_t*>(db + d_cfirsts_) + koff[t];
-    v.counts_out = reinterpret_cast<unsigned long long*>(db + d_counts_) + 2 * t;
+    v.list_keys = reinterpret_cast<uint64_t*>(ob + d_ckeys_) + koff[t];
+    v.list_firsts = reinterpret_cast<uint32_t*>(ob + d_cfirsts_) + koff[t];
+    v.counts_out = reinterpret_cast<unsigned long long*>(ob + d_counts_) + 2 * t;
     views[t] = v;
     TableLookup& tl = desc[t];
     tl.c = c->dev();
     tl.keys = reinterpret_cast<const uint64_t*>(db + d_keys_) + koff[t];
     tl.n = n[t];
-    tl.out = reinterpret_cast<float*>(db + d_rows_) + roff[t];
-    tl.flags = reinterpret_cast<uint8_t*>(db + d_flags_) + koff[t];
+    tl.out = reinterpret_cast<float*>(ob + d_rows_) + roff[t];
+    tl.flags = reinterpret_cast<uint8_t*>(ob + d_flags_) + koff[t];
     tl.default_row = eng_[t]->default_row();
     tl.stamp = stamp;
     tl.v = v;
@@ -840,16 +865,14 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
   auto d2h = [&](uint64_t off, uint64_t bytes) {
     if (bytes) HPSB_CUDA(cudaMemcpyAsync(hb + off, db + off, bytes, cudaMemcpyDeviceToHost, st));
   };
-  d2h(d_counts_, T * 16);
-  d2h(d_flags_, koff[T]);
-  d2h(d_ckeys_, koff[T] * 8);
-  d2h(d_cfirsts_, koff[T] * 4);
-  // rows: small batches in one packed copy (+ host scatter); large ones
-  // straight into each table's output (no extra host copy of big rows)
-  const bool packed_rows = roff[T] * 4 <= kPackedRowBytes;
-  if (packed_rows) {
-    d2h(d_rows_, roff[T] * 4);
-  } else {
+  // large calls: one D2H each for counts, flags, claims (whole packed
+  // regions), and the rows straight into each table's output (no extra host
+  // copy of big rows)
+  if (!packed_rows) {
+    d2h(d_counts_, T * 16);
+    d2h(d_flags_, koff[T]);
+    d2h(d_ckeys_, koff[T] * 8);
+    d2h(d_cfirsts_, koff[T] * 4);
     for (uint64_t t = 0; t < T; ++t)
       if (n[t])
         HPSB_CUDA(cudaMemcpyAsync(out[t], db + d_rows_ + roff[t] * 4,
@@ -881,8 +904,9 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
       r.miss_keys = miss_.data();
       r.order = order_.data();
       r.v = views[t];
-      r.d_out = reinterpret_cast<float*>(db + d_rows_) + roff[t];
-      r.d_flags = reinterpret_cast<uint8_t*>(db + d_flags_) + koff[t];
+      r.d_out = reinterpret_cast<float*>(ob + d_rows_) + roff[t];
+      r.d_flags = reinterpret_cast<uint8_t*>(ob + d_flags_) + koff[t];
+      r.zero_copy = packed_rows;
       r.out = out[t];
       r.flags = flags[t];
       eng_[t]->finish_group(r, outcomes ? outcomes + t : nullptr);
@@ -914,11 +938,17 @@ void LookupEngine::async_loop() {
       fetch_and_upload(ws, ws.missing_keys.data(), ws.missing_keys.size(), &counters, &nf);
       if (nf > 0) {
         std::lock_guard<std::mutex> lk(cache_->mutex());
-        HPSB_CUDA(cudaMemcpyAsync(ws.d_staged, ws.h_staged, nf * uint64_t(dim_) * 4,
-                                  cudaMemcpyHostToDevice, st));
-        HPSB_CUDA(cudaMemcpyAsync(ws.d_found_keys, ws.h_found_keys, nf * 8,
-                                  cudaMemcpyHostToDevice, st));
-        cache_->replace_device_locked(ws.d_found_keys, nf, ws.d_staged);
+        if (nf <= kZeroCopyReplaceMax) {
+          // small fill: the replace reads keys and rows from pinned host
+          // memory (no copies queued ahead of the next lookup on the stream)
+          cache_->replace_device_locked(ws.h_found_keys, nf, ws.h_staged);
+        } else {
+          HPSB_CUDA(cudaMemcpyAsync(ws.d_staged, ws.h_staged, nf * uint64_t(dim_) * 4,
+                                    cudaMemcpyHostToDevice, st));
+          HPSB_CUDA(cudaMemcpyAsync(ws.d_found_keys, ws.h_found_keys, nf * 8,
+                                    cudaMemcpyHostToDevice, st));
+          cache_->replace_device_locked(ws.d_found_keys, nf, ws.d_staged);
+        }
         HPSB_CUDA(cudaEventRecord(ws.done, st));
         ws.pending = true;
       }

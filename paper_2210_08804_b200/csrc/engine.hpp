@@ -174,6 +174,7 @@ class LookupEngine {
     uint8_t* d_flags = nullptr;
     float* out = nullptr;
     uint8_t* flags = nullptr;
+    bool zero_copy = false;  // d_out / d_flags are pinned host memory
   };
   void finish_group(const GroupResult& r, LookupOutcome* outcome);
 

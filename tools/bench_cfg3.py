@@ -96,9 +96,10 @@ def main():
         return time.perf_counter() - t0, o.unique_hit_rate
 
     # warm-up to steady state: every table sees ~2x its cache capacity of draws
+    wb = min(65536, maxb)
     for t in range(T):
-        for _ in range(max(2, (4 * S * 64) // 65536)):
-            call(t, 65536, draw(t, 65536))
+        for _ in range(max(2, (4 * S * 64) // wb)):
+            call(t, wb, draw(t, wb))
         engines[t].drain_async()
     result = {"config": {"workload": "cfg3: Criteo-shaped tables, power-law alpha 1.2, host VDB "
                                      "holds every table, threshold 0.8",
