@@ -455,3 +455,60 @@ def test_group_multi_lookup_one_launch_equals_per_table_lookups(dims):
     m.close()
     for e in ea + eb:
         e.close()
+
+
+@pytest.mark.parametrize("threshold", [0.7, 1.0])
+def test_zero_copy_small_calls_pinned_and_pageable_match_oracle(threshold):
+    """Host-buffer calls of <= 4,096 keys run zero-copy (the kernels read the
+    keys from and write rows, flags, counts and claims to pinned host memory;
+    the sync branch's scatter and fill read the host-staged rows). Pinned
+    caller buffers (rows written straight into the caller's memory), pageable
+    ones, and sizes across the zero-copy limit (4,096 / 4,097) must all match
+    the engine oracle call for call: outcomes, rows, flags, and the final
+    engine stats."""
+    import torch
+
+    d, S = 16, 96
+    eo = oracle.EngineOracle(S, 2, d, threshold=threshold, default_vector=[0.25, -1.0])
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vk = np.arange(0, 60000, 3, dtype=np.uint64)  # other keys are absent everywhere
+    vv = row_values(vk, d, 5)
+    vdb.insert("t", vk, vv)
+    for k, r in zip(vk, vv.reshape(-1, d)):
+        eo.vdb[int(k)] = r
+    c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
+    eng = hps.LookupEngine(table, c, vdb, None,
+                           hps.EngineConfig(hit_rate_threshold=threshold,
+                                            default_vector=[0.25, -1.0]))
+    maxn = 4097
+    pk = torch.empty(maxn, dtype=torch.int64).pin_memory()
+    po = torch.empty(maxn * d).pin_memory()
+    pf = torch.empty(maxn, dtype=torch.uint8).pin_memory()
+    sizes = [1, 7, 1024, 4096, 4097, 300, 4096, 2048, 33, 4097, 1500, 4000]
+    stream = hps.powerlaw_sample(1.15, 60000, 11, 12, sum(sizes))
+    at = 0
+    for b, n in enumerate(sizes):
+        keys = stream[at:at + n]
+        at += n
+        if b % 2 == 0:
+            pk.numpy().view(np.uint64)[:n] = keys
+            o = eng.lookup_ptrs(pk.data_ptr(), n, po.data_ptr(), pf.data_ptr(), hps.HPS_MEM_HOST)
+            got_rows, got_flags = po.numpy()[: n * d].copy(), pf.numpy()[:n].copy()
+            got = (o.sync_branch, o.unique_hit_rate, o.unique_count, o.defaults_returned)
+        else:
+            oo = hps.LookupOutcome()
+            r = eng.lookup(keys, oo)
+            got_rows, got_flags = r.vectors, r.miss_flags
+            got = (oo.sync_branch, oo.unique_hit_rate, oo.unique_count, oo.defaults_returned)
+        eng.drain_async()
+        out, flags, oc = eo.lookup(keys)
+        eo.drain_async()
+        assert got == (oc["sync_branch"], oc["unique_hit_rate"], oc["unique_count"],
+                       oc["defaults_returned"]), (b, n)
+        assert got_rows.tobytes() == out.tobytes(), (b, n)
+        assert (got_flags == flags).all(), (b, n)
+    assert eng.stats().__dict__ == eo.stats
+    c.check_invariants()
+    eng.close()
