@@ -732,6 +732,116 @@ void launch_lookup_multi(const TableLookup* d_tables, uint32_t count, uint32_t t
   check_launch("lookup_multi", 1);
 }
 
+// ============================================= small calls (one block) --
+// A lone call of at most kSmallLookup positions in ONE block, every step in
+// shared memory: the miss dedup (first position by atomicMin in a block hash
+// table over the batch's keys, staged in shared memory), the distinct-slot
+// set for recency stamps and unique hits, the per-call counts. No global
+// miss table, no block tickets, no finish passes: a 32-key call was ~15 us
+// event-bracketed through the multi-block kernel's dozen dependent global
+// round trips. Claims are emitted in table order (the host sorts them by
+// first position, as for the large kernel); miss_slot[pos] holds the claim
+// index and claim_of_slot the identity, so the sync-branch scatter works
+// unchanged. Used only when the call is not chained behind another lookup
+// (stream order then covers every view-ordering rule).
+constexpr uint32_t kSmallLookup = 1024;
+constexpr uint32_t kSmallTab = 2 * kSmallLookup;
+
+template <int CH>
+__global__ void __launch_bounds__(kSmallLookup)
+    k_lookup_small(CacheDev c, const uint64_t* __restrict__ keys, uint32_t n,
+                   float* __restrict__ out, uint8_t* __restrict__ flags,
+                   const float* __restrict__ default_row, uint64_t stamp, LookupView v) {
+  __shared__ unsigned long long s_key[kSmallLookup];
+  __shared__ uint32_t s_tab[kSmallTab];    // 0 = empty, else first position + 1
+  __shared__ uint32_t s_slots[kSmallTab];  // distinct hit slots
+  __shared__ uint32_t s_claim[kSmallTab];  // claim index of a table entry
+  __shared__ uint32_t s_nclaims, s_uh;
+  const uint32_t t = threadIdx.x;
+  const uint32_t lane = lane_id();
+  for (uint32_t i = t; i < kSmallTab; i += blockDim.x) {
+    s_tab[i] = 0u;
+    s_slots[i] = kNoSlot;
+  }
+  if (t == 0) {
+    s_nclaims = 0u;
+    s_uh = 0u;
+  }
+  const bool valid = t < n;
+  const uint64_t key = valid ? keys[t] : 0ull;
+  s_key[t] = key;
+  const uint32_t res = lane_probe(c, key, valid);
+  __syncthreads();
+  // hits: one recency exchange and one unique hit per distinct slot
+  uint32_t uh = 0;
+  bool first_hit = false;
+  if (res != kNoSlot) {
+    // exact distinct-slot set (at most kSmallLookup slots in 2x entries)
+    uint32_t q = (res * 0x9E3779B1u) >> 7;
+    while (true) {
+      q &= kSmallTab - 1;
+      const uint32_t cur = atomicCAS(&s_slots[q], kNoSlot, res);
+      if (cur == kNoSlot) {
+        first_hit = true;
+        break;
+      }
+      if (cur == res) break;
+      ++q;
+    }
+  }
+  if (first_hit) {
+    atomicMax(reinterpret_cast<unsigned long long*>(c.counters) + res,
+              (unsigned long long)stamp);
+    uh = 1;
+  }
+  // misses: dedup in the block table, first position kept
+  uint32_t h = 0;
+  if (valid && res == kNoSlot) {
+    h = uint32_t(fmix64(key ^ 0x9E3779B97F4A7C15ull)) & (kSmallTab - 1);
+    while (true) {
+      const uint32_t old = atomicCAS(&s_tab[h], 0u, t + 1);
+      if (old == 0u) break;
+      if (s_key[old - 1] == key) {
+        if (t + 1 < old) atomicMin(&s_tab[h], t + 1);
+        break;
+      }
+      h = (h + 1) & (kSmallTab - 1);
+    }
+  }
+  uh = __reduce_add_sync(0xFFFFFFFFu, uh);
+  if (lane == 0 && uh) atomicAdd(&s_uh, uh);
+  if (valid) {
+    flags[t] = res == kNoSlot ? 1 : 0;
+    if (v.flags_dev != nullptr) v.flags_dev[t] = res == kNoSlot ? 1 : 0;
+  }
+  __syncthreads();
+  // one claim per table entry (the entry's final value is the first position)
+  for (uint32_t i = t; i < kSmallTab; i += blockDim.x) {
+    const uint32_t f = s_tab[i];
+    if (f != 0u) {
+      const uint32_t e = atomicAdd(&s_nclaims, 1u);
+      s_claim[i] = e;
+      v.list_keys[e] = s_key[f - 1];
+      v.list_firsts[e] = f - 1;
+      v.claim_of_slot[e] = e;
+    }
+  }
+  __syncthreads();
+  if (valid && res == kNoSlot) v.miss_slot[t] = s_claim[h];
+  // rows: the warp's 32 consecutive positions as one contiguous block
+  const uint32_t base = t & ~31u;
+  const uint32_t nrows = n > base + 32 ? 32u : (n > base ? n - base : 0u);
+  if (nrows) warp_copy_rows<CH, CH == 8 ? 4 : 8>(c, res, nrows, default_row, out + uint64_t(base) * c.d);
+  __syncthreads();
+  if (t == 0) {
+    v.counts_out[0] = s_uh;
+    v.counts_out[1] = s_nclaims;
+    // the view is free for its next use (the large kernel's completion rule)
+    __threadfence();
+    st_release(v.completed, v.gen + 1);
+  }
+}
+
 // --------------------------------------------------------------- launch --
 unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n, float* out,
                              uint8_t* flags, const float* default_row, uint64_t stamp,
@@ -777,6 +887,21 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     // a call pipelined behind another lookup orders its recency exchange
     // for throughput, any other call for latency (see lookup_body)
     const bool pipelined = cfg.numAttrs == 1 && !(skip & kWaitBeforeCopy);
+    static const bool no_small = std::getenv("HPSB_LOOKUP_NO_SMALL") != nullptr;
+    if (cfg.numAttrs == 0 && n <= kSmallLookup && diag_skip == 0 && v.trace == nullptr &&
+        !no_small) {
+      if (ch == 8)
+        k_lookup_small<8><<<1, kSmallLookup, 0, st>>>(c, keys, uint32_t(n), out, flags,
+                                                      default_row, stamp, v);
+      else if (ch == 4)
+        k_lookup_small<4><<<1, kSmallLookup, 0, st>>>(c, keys, uint32_t(n), out, flags,
+                                                      default_row, stamp, v);
+      else
+        k_lookup_small<1><<<1, kSmallLookup, 0, st>>>(c, keys, uint32_t(n), out, flags,
+                                                      default_row, stamp, v);
+      check_launch("lookup", 1);
+      return 1;
+    }
     auto go = [&](auto chc, auto wc) {
       constexpr int CH = decltype(chc)::value, WARPS = decltype(wc)::value;
       cfg.gridDim = dim3(unsigned((n + WARPS * 32 - 1) / (WARPS * 32)));

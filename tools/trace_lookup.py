@@ -35,6 +35,10 @@ def main():
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--isolated", action="store_true",
                     help="one call at a time (host sync between calls): single-call timeline")
+    ap.add_argument("--graph-events", action="store_true",
+                    help="the bench's p50 arrangement: one graph, CUDA events around every "
+                         "lookup (no overlap); also times an empty event pair and a tiny "
+                         "kernel the same way (the launch floor)")
     ap.add_argument("--update-frac", type=float, default=0.0,
                     help="cfg 4: stream-ordered update of this fraction of the resident rows "
                          "after every lookup")
@@ -74,7 +78,37 @@ def main():
             cache.update_device_async(k.data_ptr(), u, r.data_ptr(), written.data_ptr(), sp)
     torch.cuda.synchronize()
     cache.debug_trace()
-    if a.isolated:
+    if a.graph_events:
+        st = torch.cuda.ExternalStream(sp)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(a.steps)]
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(a.steps)]
+        for x, y in kev + fev:
+            x.record(st)
+            y.record(st)
+        torch.cuda.synchronize()
+        g = hps.StreamGraph(sp)
+        if True:
+            with g:
+                for s in range(a.steps):
+                    cache.set_profile_events(kev[s][0].cuda_event, kev[s][1].cuda_event)
+                    cache.lookup_device(dk[s % 32].data_ptr(), n, outs[s % 8].data_ptr(),
+                                        fl.data_ptr(), dr.data_ptr(), mk.data_ptr(), mf.data_ptr(),
+                                        cnt[2 * s:].data_ptr(), sp)
+                    # the floor: the same event pair around a 32-key lookup (one block)
+                    cache.set_profile_events(fev[s][0].cuda_event, fev[s][1].cuda_event)
+                    cache.lookup_device(dk[s % 32].data_ptr(), 32, outs[s % 8].data_ptr(),
+                                        fl.data_ptr(), dr.data_ptr(), mk.data_ptr(), mf.data_ptr(),
+                                        cnt[2 * s:].data_ptr(), sp)
+                    cache.set_profile_events(0, 0)
+        g.launch()
+        torch.cuda.synchronize()
+        k1 = np.array([x.elapsed_time(y) for x, y in kev]) * 1e3
+        f1 = np.array([x.elapsed_time(y) for x, y in fev]) * 1e3
+        print(f"graph with events: lookup p50 {np.median(k1):.2f} us, 32-key lookup (floor) p50 "
+              f"{np.median(f1):.2f} us")
+    elif a.isolated:
         st = torch.cuda.ExternalStream(sp)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(a.steps)]
