@@ -202,7 +202,7 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   const uint64_t ls_bytes = lookup_scratch_bytes(cap);
   const uint64_t hdr_bytes = 16 + cap * 4 + 8 + cap * 8 + cap;
   const uint64_t dev_bytes = a256(cap * 8) * 3 + a256(cap * uint64_t(d) * 4) * 2 + a256(cap) +
-                             a256(cap * 4) + a256(ls_bytes) + a256(hdr_bytes);
+                             a256(cap * 4) + a256(ls_bytes);
   HPSB_CUDA(cudaStreamSynchronize(st));
   char* p = static_cast<char*>(dbuf.ensure(dev_bytes, st));
   auto take = [&](uint64_t bytes) {
@@ -216,7 +216,6 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   d_row_of = reinterpret_cast<int32_t*>(take(cap * 4));
   d_staged = reinterpret_cast<float*>(take(cap * uint64_t(d) * 4));
   d_found_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
-  d_hdr = take(hdr_bytes);
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
   ls = lookup_scratch_carve(ls_base, cap);

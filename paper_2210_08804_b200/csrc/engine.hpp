@@ -90,7 +90,6 @@ struct Workspace {
   int32_t* d_row_of = nullptr;
   float* d_staged = nullptr;
   uint64_t* d_found_keys = nullptr;
-  char* d_hdr = nullptr;  // packed per-call results (small host-mode calls)
   LookupScratch ls;
   LookupView lv;  // the view of the last lookup
   // pinned host
@@ -107,7 +106,7 @@ struct Workspace {
   uint64_t* h_claim_keys = nullptr;    // unique misses in claim order
   uint32_t* h_claim_firsts = nullptr;  // their first positions
   int32_t* h_row_of_claim = nullptr;   // staged row per claim (sync branch)
-  char* h_hdr = nullptr;               // pinned mirror of d_hdr
+  char* h_hdr = nullptr;               // zero-copy calls: [counts | firsts | keys | flags]
   std::vector<uint32_t> order;         // claims sorted by first position
   // batch state (for the async task)
   std::vector<uint64_t> missing_keys;
