@@ -4,6 +4,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <unordered_map>
@@ -406,7 +407,11 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
       // from pinned host memory and writes rows, flags, counts and every
       // claim straight into pinned host memory ([counts | first positions |
       // keys | flags] in h_hdr); no copies, one host wait on the kernel
-      c.packed = host && n <= kPackedMax;
+      static const uint64_t zero_copy_max = [] {
+        const char* e = std::getenv("HPSB_ZERO_COPY_MAX");  // A/B knob
+        return e ? uint64_t(std::strtoull(e, nullptr, 10)) : kPackedMax;
+      }();
+      c.packed = host && n <= zero_copy_max;
       if (c.packed) {
         const void* mk = mapped(keys);
         if (mk == nullptr) {
