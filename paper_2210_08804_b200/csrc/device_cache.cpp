@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <unordered_set>
 #include <vector>
 
@@ -161,6 +162,41 @@ size_t DeviceCache::query(const uint64_t* keys, size_t n, float* out, size_t out
   const uint64_t d = cfg_.dimension;
   const bool host = mem == kHostMem;
   ensure_scan_tiles((n + kScanTile - 1) / kScanTile);
+  if (host && n <= kZeroCopyQueryMax) {
+    // Zero-copy (the reference's batch sizes): the kernels read the keys from
+    // and write hit rows, hit flags, miss positions / keys and the miss count
+    // to pinned host memory -- the caller's own buffers when they are pinned,
+    // else a pinned staging area copied on the host (only HIT rows go back
+    // into `out`: miss rows stay untouched, slab_cache.cpp:84-89). One host
+    // wait, no copy-engine operations.
+    const uint64_t sb = align256(n * 8) + align256(n * d * 4) + align256(n) + align256(n * 4) +
+                        align256(n * 8);
+    Carver hv{static_cast<char*>(qstage_.ensure(sb))};
+    uint64_t* hk = hv.take<uint64_t>(n);
+    float* hrows = hv.take<float>(n * d);
+    uint8_t* hhit = hv.take<uint8_t>(n);
+    uint32_t* hpos = hv.take<uint32_t>(n);
+    uint64_t* hmk = hv.take<uint64_t>(n);
+    const uint64_t* zk = static_cast<const uint64_t*>(host_mapped(keys));
+    if (zk == nullptr) {
+      std::memcpy(hk, keys, n * 8);
+      zk = hk;
+    }
+    float* zo = static_cast<float*>(host_mapped(out));
+    uint32_t* zp = static_cast<uint32_t*>(host_mapped(miss_pos));
+    uint64_t* zm = static_cast<uint64_t*>(host_mapped(miss_keys));
+    launch_cache_query(dev_, zk, n, zo ? zo : hrows, hhit, stamp, keys_per_warp_, stream_);
+    launch_select_misses(zk, hhit, n, zp ? zp : hpos, zm ? zm : hmk, h_small_, scan_, stream_);
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+    const size_t n_miss = h_small_[0];
+    if (zo == nullptr) {
+      for (uint64_t i = 0; i < n; ++i)
+        if (hhit[i]) std::memcpy(out + i * d, hrows + i * d, d * 4);
+    }
+    if (zp == nullptr) std::memcpy(miss_pos, hpos, n_miss * 4);
+    if (zm == nullptr) std::memcpy(miss_keys, hmk, n_miss * 8);
+    return n_miss;
+  }
   const uint64_t bytes = align256(n) + (host ? align256(n * 8) * 2 + align256(n * d * 4) +
                                                    align256(n * 4)
                                              : 0);

@@ -167,6 +167,8 @@ class DeviceCache {
     return winner_ + ((updates_++ & 1u) ? cfg_.slabset_count * cfg_.slabs_per_set * 32ull : 0ull);
   }
   DeviceBuffer ubuf_;  // update_device scratch
+  PinnedBuffer qstage_;  // zero-copy host-mode query staging
+  static constexpr uint64_t kZeroCopyQueryMax = 65536;
   uint64_t ucap_ = 0;
   // diagnostic lookup timeline ring (HPSB_TRACE=1): kTraceRing calls x 8
   unsigned long long* trace_ = nullptr;

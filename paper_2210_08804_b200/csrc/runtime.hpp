@@ -87,6 +87,18 @@ class DeviceBuffer {
   size_t bytes_ = 0;
 };
 
+// Device-accessible address of pinned host memory (cudaHostAlloc'd or
+// registered; the same address under unified addressing), nullptr for
+// pageable memory.
+inline void* host_mapped(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 // Grow-only page-locked host buffer (for async copies).
 class PinnedBuffer {
  public:
