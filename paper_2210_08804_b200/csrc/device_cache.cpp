@@ -327,7 +327,24 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
   ReplaceScratch rs = replace_scratch_carve(cv.take<char>(rs_bytes), n);
   const uint64_t* d_keys = keys;
   const float* d_rows = vectors;
-  if (host) {
+  if (host && n <= kZeroCopyReplaceMax) {
+    // zero-copy: the one-launch small replace reads the keys and rows from
+    // pinned host memory (the caller's when pinned, else a pinned staging copy)
+    const uint64_t sb = align256(n * 8) + align256(n * d * 4);
+    Carver hv{static_cast<char*>(qstage_.ensure(sb))};
+    uint64_t* hk = hv.take<uint64_t>(n);
+    float* hr = hv.take<float>(n * d);
+    d_keys = static_cast<const uint64_t*>(host_mapped(keys));
+    d_rows = static_cast<const float*>(host_mapped(vectors));
+    if (d_keys == nullptr) {
+      std::memcpy(hk, keys, n * 8);
+      d_keys = hk;
+    }
+    if (d_rows == nullptr) {
+      std::memcpy(hr, vectors, n * d * 4);
+      d_rows = hr;
+    }
+  } else if (host) {
     uint64_t* k = cv.take<uint64_t>(n);
     float* r = cv.take<float>(n * d);
     HPSB_CUDA(cudaMemcpyAsync(k, keys, n * 8, cudaMemcpyHostToDevice, stream_));

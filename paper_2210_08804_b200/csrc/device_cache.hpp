@@ -169,6 +169,7 @@ class DeviceCache {
   DeviceBuffer ubuf_;  // update_device scratch
   PinnedBuffer qstage_;  // zero-copy host-mode query staging
   static constexpr uint64_t kZeroCopyQueryMax = 65536;
+  static constexpr uint64_t kZeroCopyReplaceMax = 256;  // the one-launch replace kernels' limit
   uint64_t ucap_ = 0;
   // diagnostic lookup timeline ring (HPSB_TRACE=1): kTraceRing calls x 8
   unsigned long long* trace_ = nullptr;
