@@ -153,7 +153,12 @@ class ThreadPool {
       return;
     }
     const size_t per = (n + chunks - 1) / chunks;
-    std::atomic<size_t> left{chunks - 1};
+    // The countdown lives on this frame: it is decremented UNDER done_mu, so
+    // the waiter (which reads it under done_mu) cannot see zero -- and return,
+    // destroying done_mu / done_cv -- before the last worker has finished
+    // notifying and released the lock. (Decrementing first and locking after
+    // let the waiter return in between: a rare use-after-scope of the mutex.)
+    size_t left = chunks - 1;
     std::mutex done_mu;
     std::condition_variable done_cv;
     {
@@ -162,17 +167,15 @@ class ThreadPool {
         const size_t b = c * per, e = std::min(n, b + per);
         q_.push_back([&, b, e] {
           if (b < e) fn(b, e);
-          if (left.fetch_sub(1) == 1) {
-            std::lock_guard<std::mutex> dl(done_mu);
-            done_cv.notify_all();
-          }
+          std::lock_guard<std::mutex> dl(done_mu);
+          if (--left == 0) done_cv.notify_all();
         });
       }
     }
     cv_.notify_all();
     fn(0, std::min(n, per));
     std::unique_lock<std::mutex> dl(done_mu);
-    done_cv.wait(dl, [&] { return left.load() == 0; });
+    done_cv.wait(dl, [&] { return left == 0; });
   }
 
  private:
