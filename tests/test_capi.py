@@ -198,3 +198,38 @@ def test_cache_config_validation_precedes_device_use():
                 hps.SlabCacheConfig(slabset_count=1, dimension=4, worker_pool_size=0)):
         with pytest.raises(hps.InvalidArgument):
             hps.SlabCache(cfg)
+
+
+def test_vdb_parallel_lookups_from_several_threads():
+    """Large lookups fan out over the store's thread pool (chunks of >= 512
+    keys); several caller threads at once (the engine's async fill next to a
+    sync-branch fetch) share that pool. Every result must be exact -- a
+    regression guard for the pool's completion countdown, which once let a
+    caller return while the last worker was still signalling it."""
+    import threading
+
+    d = 4
+    vdb = hps.VolatileStore(8)
+    vdb.register_table(T("t", d), hps.VolatileTableConfig(partition_count=16))
+    keys = np.arange(0, 200000, 2, dtype=np.uint64)
+    vdb.insert("t", keys, rows(keys, d))
+    errors = []
+
+    def worker(seed):
+        rng = np.random.default_rng(seed)
+        for _ in range(150):
+            q = rng.integers(0, 200000, 3000, dtype=np.uint64)
+            r = vdb.lookup("t", q)
+            want = q[q % 2 == 0]
+            if not (np.array_equal(r.found_keys, want) and
+                    r.found_vectors.tobytes() == rows(want, d).tobytes() and
+                    np.array_equal(r.missing_keys, q[q % 2 == 1])):
+                errors.append(seed)
+                return
+
+    ts = [threading.Thread(target=worker, args=(s,)) for s in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors
