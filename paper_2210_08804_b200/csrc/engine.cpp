@@ -699,8 +699,8 @@ void LookupEngine::finish_group(const GroupResult& r, LookupOutcome* outcome) {
     HPSB_CUDA(cudaEventRecord(ws->done, st));
     HPSB_CUDA(cudaEventSynchronize(ws->done));
     if (nf > 0 && r.zero_copy) {
-      std::memcpy(r.out, r.d_out, r.n * uint64_t(d) * 4);
-      std::memcpy(r.flags, r.d_flags, r.n);
+      if (r.out != r.d_out) std::memcpy(r.out, r.d_out, r.n * uint64_t(d) * 4);
+      if (r.flags != r.d_flags) std::memcpy(r.flags, r.d_flags, r.n);
     }
   } else {
     defaults = r.um;
@@ -832,7 +832,19 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
   // claims and rows straight into the pinned mirror (same offsets), no
   // device-to-host copies
   const bool packed_rows = roff[T] * 4 <= kPackedRowBytes;
-  char* ob = packed_rows ? hb : db;
+  // pinned caller outputs (any size up to kDirectRowBytes): the kernel writes
+  // each table's rows straight into the caller's buffer -- no row copies at
+  // all (one D2H per table before); counts, flags and claims as above
+  std::vector<float*> direct_out(T, nullptr);
+  bool direct = roff[T] * 4 <= kDirectRowBytes;
+  const uintptr_t align = ch_ == 8 ? 32 : (ch_ == 4 ? 16 : 4);
+  for (uint64_t t = 0; t < T && direct; ++t) {
+    if (n[t] == 0) continue;
+    direct_out[t] = static_cast<float*>(host_mapped(out[t]));
+    direct = direct_out[t] != nullptr && reinterpret_cast<uintptr_t>(direct_out[t]) % align == 0;
+  }
+  const bool zero_copy = packed_rows || direct;
+  char* ob = zero_copy ? hb : db;
   uint32_t blocks = 0;
   std::vector<LookupView> views(T);
   for (uint64_t t = 0; t < T; ++t) {
@@ -851,7 +863,7 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
     tl.c = c->dev();
     tl.keys = reinterpret_cast<const uint64_t*>(db + d_keys_) + koff[t];
     tl.n = n[t];
-    tl.out = reinterpret_cast<float*>(ob + d_rows_) + roff[t];
+    tl.out = direct ? direct_out[t] : reinterpret_cast<float*>(ob + d_rows_) + roff[t];
     tl.flags = reinterpret_cast<uint8_t*>(ob + d_flags_) + koff[t];
     tl.default_row = eng_[t]->default_row();
     tl.stamp = stamp;
@@ -872,7 +884,7 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
   // large calls: one D2H each for counts, flags, claims (whole packed
   // regions), and the rows straight into each table's output (no extra host
   // copy of big rows)
-  if (!packed_rows) {
+  if (!zero_copy) {
     d2h(d_counts_, T * 16);
     d2h(d_flags_, koff[T]);
     d2h(d_ckeys_, koff[T] * 8);
@@ -893,7 +905,7 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
   for (uint64_t t = 0; t < T; ++t) {
     try {
       const uint32_t d = eng_[t]->dim();
-      if (packed_rows) std::memcpy(out[t], hrows + roff[t], n[t] * uint64_t(d) * 4);
+      if (zero_copy && !direct) std::memcpy(out[t], hrows + roff[t], n[t] * uint64_t(d) * 4);
       std::memcpy(flags[t], hflags + koff[t], n[t]);
       LookupEngine::GroupResult r;
       r.n = n[t];
@@ -908,9 +920,9 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
       r.miss_keys = miss_.data();
       r.order = order_.data();
       r.v = views[t];
-      r.d_out = reinterpret_cast<float*>(ob + d_rows_) + roff[t];
+      r.d_out = direct ? direct_out[t] : reinterpret_cast<float*>(ob + d_rows_) + roff[t];
       r.d_flags = reinterpret_cast<uint8_t*>(ob + d_flags_) + koff[t];
-      r.zero_copy = packed_rows;
+      r.zero_copy = zero_copy;
       r.out = out[t];
       r.flags = flags[t];
       eng_[t]->finish_group(r, outcomes ? outcomes + t : nullptr);

@@ -263,6 +263,7 @@ class MultiLookup {
 
  private:
   static constexpr uint64_t kPackedRowBytes = 1 << 20;
+  static constexpr uint64_t kDirectRowBytes = 64ull << 20;
   std::vector<LookupEngine*> eng_;
   uint64_t maxb_;
   int ch_ = 1;

@@ -405,13 +405,17 @@ def test_native_refresh_tier_fault_keeps_finished_batches():
     assert got[200:].tobytes() == row_values(resident[200:], d, 0).tobytes()
 
 
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("dims", [(16, 16, 16, 16), (8, 12, 16, 20, 4), (3, 5)])
-def test_group_multi_lookup_one_launch_equals_per_table_lookups(dims):
+def test_group_multi_lookup_one_launch_equals_per_table_lookups(dims, pinned):
     """MultiLookup (cache group, ONE kernel launch for all tables) must give
     every table exactly what a per-table hps_engine_lookup gives on an
     identical twin: rows, flags, outcomes, cache contents, stats -- with
     different dims per table, ragged and empty per-table batches, and both
-    the sync and the async branch."""
+    the sync and the async branch; pinned caller outputs get the rows written
+    straight into them (zero-copy), pageable ones through the staging mirror."""
+    import torch
+
     T_ = len(dims)
 
     def build(grouped):
@@ -439,7 +443,16 @@ def test_group_multi_lookup_one_launch_equals_per_table_lookups(dims):
             ns[0] = 0
         batches = [hps.powerlaw_sample(1.1, 11000, t, 70 * r + t, ns[t]) + np.uint64(t * 100000)
                    for t in range(T_)]
-        got = m.lookup(batches)
+        if pinned:
+            pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
+            po = [torch.zeros(max(ns[t], 1) * dims[t]).pin_memory() for t in range(T_)]
+            pf = [torch.zeros(max(ns[t], 1), dtype=torch.uint8).pin_memory() for t in range(T_)]
+            m.lookup_ptrs([k.data_ptr() for k in pk], ns, [o.data_ptr() for o in po],
+                          [f.data_ptr() for f in pf])
+            got = [hps.LookupResult(dims[t], po[t].numpy()[: ns[t] * dims[t]].copy(),
+                                    pf[t].numpy()[: ns[t]].copy()) for t in range(T_)]
+        else:
+            got = m.lookup(batches)
         for t in range(T_):
             o = hps.LookupOutcome()
             want = eb[t].lookup(batches[t], o)
