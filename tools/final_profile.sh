@@ -13,7 +13,7 @@ timeout 600 python bench.py --impl reference > $out/bench_ref.json 2> $out/bench
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
   python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline --no-online > $out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"k_lookup_tag<8, 8, (0|false)>" -s 3 -c 1 \
+  -k regex:"k_lookup_tag<\(int\)8, \(int\)8, \(bool\)0>" -s 3 -c 1 \
   -o $out/prof python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline --no-online > $out/ncu_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"k_lookup_small" -s 20 -c 1 \
