@@ -162,6 +162,7 @@ class DeviceCache {
   // arrays, consecutive updates alternate (the next update's probe may run
   // while this update's write kernel is in flight)
   uint32_t* winner_ = nullptr;
+  void* probe_mem_ = nullptr;  // keys + fingerprints (one allocation)
   uint64_t updates_ = 0;
   uint32_t* next_winner() {
     return winner_ + ((updates_++ & 1u) ? cfg_.slabset_count * cfg_.slabs_per_set * 32ull : 0ull);
