@@ -67,14 +67,17 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
   dev_.d = cfg.dimension;
   dev_.mS = ~0ull / cfg.slabset_count;
   dev_.mW = ~0ull / cfg.slabs_per_set;
-  // keys and fingerprints in ONE allocation (one L2 persistence window
-  // covers both probe structures, below)
+  // keys, fingerprints, masks and counters in ONE allocation (one L2
+  // persistence window covers the probe structures, below)
   const uint64_t tags_off = (slots * 8 + 255) / 256 * 256;
-  HPSB_CUDA(cudaMalloc(&probe_mem_, tags_off + slots));
-  dev_.keys = static_cast<uint64_t*>(probe_mem_);
-  HPSB_CUDA(cudaMalloc(&dev_.counters, slots * 8));
-  HPSB_CUDA(cudaMalloc(&dev_.masks, slabs * 4));
-  dev_.tags = static_cast<uint8_t*>(probe_mem_) + tags_off;
+  const uint64_t masks_off = tags_off + (slots + 255) / 256 * 256;
+  const uint64_t ctr_off = masks_off + (slabs * 4 + 255) / 256 * 256;
+  HPSB_CUDA(cudaMalloc(&probe_mem_, ctr_off + slots * 8));
+  char* pm = static_cast<char*>(probe_mem_);
+  dev_.keys = reinterpret_cast<uint64_t*>(pm);
+  dev_.tags = reinterpret_cast<uint8_t*>(pm + tags_off);
+  dev_.masks = reinterpret_cast<decltype(dev_.masks)>(pm + masks_off);
+  dev_.counters = reinterpret_cast<decltype(dev_.counters)>(pm + ctr_off);
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
   lookup_marks_locked(0);  // allocated up front: lookups may be graph-captured
@@ -96,7 +99,9 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
       int maxp = 0, maxw = 0;
       cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device_);
       cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device_);
-      const size_t win = std::min<size_t>(tags_off + slots, size_t(maxw));
+      // default: keys + fingerprints + masks; HPSB_L2_PERSIST=all adds the counters
+      const bool all = e && std::string(e) == "all";
+      const size_t win = std::min<size_t>(all ? ctr_off + slots * 8 : ctr_off, size_t(maxw));
       if (maxp > 0 && win > 0) {
         const size_t persist = std::min<size_t>(win, size_t(maxp));
         size_t cur = 0;
@@ -128,8 +133,6 @@ DeviceCache::~DeviceCache() {
   DeviceGuard g(device_);
   cudaStreamSynchronize(stream_);
   cudaFree(probe_mem_);
-  cudaFree(dev_.counters);
-  cudaFree(dev_.masks);
   cudaFree(dev_.rows);
   cudaFree(dev_.occupied);
   cudaFree(d_small_);
