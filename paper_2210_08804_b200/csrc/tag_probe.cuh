@@ -31,16 +31,22 @@ __device__ __forceinline__ void st_cs_f4(float4* p, const float4& v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
+#ifndef HPSB_ROW_LOAD
+#define HPSB_ROW_LOAD ""
+#endif
 __device__ __forceinline__ void ld256_nc(const void* p, uint32_t (&r)[8]) {
-  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile("ld.global.nc" HPSB_ROW_LOAD ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                  "=r"(r[6]), "=r"(r[7])
                : "l"(p));
 }
+// Output rows are written once and never re-read here: no L1 allocation and
+// evict-first in L2 (vs .cs: cfg 2 +2 %, profiles/r01_ab_history.txt).
 __device__ __forceinline__ void st256_cs(void* p, const uint32_t (&r)[8]) {
-  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]),
-               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
+  asm volatile(
+      "st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
 }
 // Bit j set when byte j of the 32-byte fingerprint block may equal `tag`
 // (zero-byte test on w ^ tag; it can over-report -- verified against the
