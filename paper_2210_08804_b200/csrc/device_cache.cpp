@@ -91,8 +91,8 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
   // The probe structures (keys + fingerprints: 9 B per slot, 18 MB at cfg 2)
   // as a persisting L2 window on the cache stream, so the expanded output
   // streaming through L2 (33.5 MB per 65,536-key call) does not evict them
-  // between calls (cfg 2: +1.5-2 % lookups/s; HPSB_L2_PERSIST=off disables).
-  // Larger tables persist a hit-ratio share of the window.
+  // between calls (cfg 2: +3.5 % lookups/s; HPSB_L2_PERSIST=off disables).
+  // Tables whose probe structures exceed the persisting capacity get none.
   {
     const char* e = std::getenv("HPSB_L2_PERSIST");
     if (!(e && std::string(e) == "off")) {
@@ -101,8 +101,12 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
       cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device_);
       // default: keys + fingerprints + masks; HPSB_L2_PERSIST=all adds the counters
       const bool all = e && std::string(e) == "all";
-      const size_t win = std::min<size_t>(all ? ctr_off + slots * 8 : ctr_off, size_t(maxw));
-      if (maxp > 0 && win > 0) {
+      const size_t want = all ? ctr_off + slots * 8 : ctr_off;
+      const size_t win = std::min<size_t>(want, size_t(maxw));
+      // only when the whole region fits the persisting capacity: a random
+      // sliver of a much larger table (cfg 5: 1.8 GB) would only take L2
+      // away from everything else
+      if (maxp > 0 && win > 0 && want <= size_t(maxp) && want <= size_t(maxw)) {
         const size_t persist = std::min<size_t>(win, size_t(maxp));
         size_t cur = 0;
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
