@@ -233,13 +233,19 @@ def hbm_peak():
 
 
 def ncu_traffic():
+    """DRAM bytes (read + write) per step of the timed lookup stream, from the
+    committed whole-graph ncu capture (profiles/ncu_traffic.json): the output
+    rows reach DRAM as L2 evictions during later steps, so a single launch's
+    own counters under-report them."""
     f = ROOT / "profiles" / "ncu_traffic.json"
     if f.exists():
         try:
-            return json.loads(f.read_text()).get("lookup_dram_bytes_per_launch")
+            j = json.loads(f.read_text())
+            return j.get("graph_dram_bytes_per_step", j.get("lookup_dram_bytes_per_launch")), \
+                j.get("graph_source", j.get("source"))
         except Exception:
-            return None
-    return None
+            return None, None
+    return None, None
 
 
 def max_over_ranks(x: float, dist, dev) -> float:
@@ -306,102 +312,141 @@ def run_ours(args, rank, world, local_rank):
     mkeys = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(ring)]
     mfirsts = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(ring)]
 
-    def device_run(target, steps, warmup, seed):
+    resident_sorted = np.sort(resident)
+
+    def expected(keys):
+        """Query-only steps over a fixed resident set: a position's row is the
+        table row of its key when resident, else the default (zero) row."""
+        res = np.isin(keys, resident_sorted, assume_unique=False)
+        rows = table_rows(keys, d).reshape(-1, d)
+        rows[~res] = 0.0
+        u, first = np.unique(keys, return_index=True)
+        ures = np.isin(u, resident_sorted)
+        return rows.reshape(-1), (~res).astype(np.uint8), u, first, ures
+
+    def self_check(batches, steps, c):
+        """The timed launch's outputs (the last `ring` steps stay in the output
+        ring) byte-compared against the expected rows; every step's unique
+        counts; the claims (unique missing keys + first positions)."""
+        bad = []
+        for s in range(steps):
+            keys = batches[s % pool]
+            u = np.unique(keys)
+            ures = np.isin(u, resident_sorted)
+            if c[s].tolist() != [int(ures.sum()), int((~ures).sum())]:
+                bad.append(f"step {s}: counts {c[s].tolist()}")
+        checked = 0
+        for s in range(max(0, steps - ring), steps):
+            keys = batches[s % pool]
+            rows, fl, u, first, ures = expected(keys)
+            if outs[s % ring].cpu().numpy().tobytes() != rows.tobytes():
+                bad.append(f"step {s}: rows differ")
+            if not (flags[s % ring].cpu().numpy() == fl).all():
+                bad.append(f"step {s}: flags differ")
+            um = int((~ures).sum())
+            ck = mkeys[s % ring][:um].cpu().numpy().view(np.uint64)
+            cf = mfirsts[s % ring][:um].cpu().numpy().astype(np.int64)
+            o = np.argsort(ck)
+            if not ((ck[o] == u[~ures]).all() and (cf[o] == first[~ures]).all()):
+                bad.append(f"step {s}: claims differ")
+            checked += 1
+        return {"ok": not bad, "steps_rows_checked": checked, "steps_counts_checked": steps,
+                "errors": bad[:5]}
+
+    def device_run(target, steps, warmup, seed, check=False):
         batches, p, h_draw = wl.batches(target, pool, seed)
         ab = [wl.algorithmic_bytes(b, keys_state, masks_state) for b in batches]
         dkeys = [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
         counts = torch.zeros(max(steps, 1) * 2, dtype=torch.int64, device=dev)
         torch.cuda.synchronize()
         sp = st.cuda_stream
-        for s in range(warmup):
-            j = s % pool
-            cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
+
+        def issue(s, cnt_ptr):
+            cache.lookup_device(dkeys[s % pool].data_ptr(), n, outs[s % ring].data_ptr(),
                                 flags[s % ring].data_ptr(), default_row.data_ptr(),
                                 mkeys[s % ring].data_ptr(), mfirsts[s % ring].data_ptr(),
-                                counts.data_ptr(), sp)
-        # The K steps are captured into one CUDA graph and launched once, so
-        # host-side call overhead cannot starve the GPU between steps; per-step
-        # and per-kernel timestamps are external event records inside it.
-        # The library records the events around each lookup kernel (external
-        # records inside the capture, so they stay readable after launch).
+                                cnt_ptr, sp)
+
+        # the W untimed warm-up steps (eager; they also size the scratch)
+        for s in range(warmup):
+            issue(s, counts.data_ptr())
+        torch.cuda.synchronize()
+        # The K timed steps are captured into one CUDA graph bracketed by two
+        # event-record nodes, so the timed region holds exactly the K lookups
+        # (no host launch latency, no graph upload). A second graph records
+        # events around each lookup (no overlap between calls there): the
+        # single-call latencies. Captured lookups are replayable (fresh
+        # stamps per launch), so both graphs are launched once untimed first.
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps)]
-        for a, b in kev:  # materialise the cudaEvent_t handles
+        for a, b in kev + [(t0, t1)]:  # materialise the cudaEvent_t handles
             a.record(st)
             b.record(st)
         torch.cuda.synchronize()
-
-        def capture(with_events):
-            g = hps.StreamGraph(sp)
-            with g:
-                for s in range(steps):
-                    j = s % pool
-                    if with_events:
-                        cache.set_profile_events(kev[s][0].cuda_event, kev[s][1].cuda_event)
-                    cache.lookup_device(dkeys[j].data_ptr(), n, outs[s % ring].data_ptr(),
-                                        flags[s % ring].data_ptr(), default_row.data_ptr(),
-                                        mkeys[s % ring].data_ptr(), mfirsts[s % ring].data_ptr(),
-                                        counts[2 * s:].data_ptr(), sp)
-            cache.set_profile_events(0, 0)
-            return g
-
-        # graph 1: the timed region (no event nodes between steps);
-        # graph 2: the same steps with events around each lookup's kernels
         l0 = hps.kernel_launch_count()
-        graph = capture(False)
-        launches = hps.kernel_launch_count() - l0  # kernel nodes in the timed graph
-        graph_ev = capture(True)
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        graph = hps.StreamGraph(sp)
+        with graph:
+            hps.event_record(t0.cuda_event, sp)
+            for s in range(steps):
+                issue(s, counts[2 * s:].data_ptr())
+            hps.event_record(t1.cuda_event, sp)
+        captured = hps.kernel_launch_count() - l0  # kernel nodes in the timed graph
+        graph_ev = hps.StreamGraph(sp)
+        with graph_ev:
+            for s in range(steps):
+                cache.set_profile_events(kev[s][0].cuda_event, kev[s][1].cuda_event)
+                issue(s, counts[2 * s:].data_ptr())
+        cache.set_profile_events(0, 0)
+        graph.launch()
+        graph_ev.launch()
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        t0.record(st)
-        graph.launch()
-        t1.record(st)
+        l1 = hps.kernel_launch_count()
+        graph.launch()  # the timed launch
         torch.cuda.synchronize()
+        launches = captured + (hps.kernel_launch_count() - l1)  # + the rebase kernel
         if dist:
             dist.barrier()
         total_ms = t0.elapsed_time(t1)
         c = counts.cpu().numpy().reshape(-1, 2)[:steps].copy()
+        chk = self_check(batches, steps, c) if check else None
         graph_ev.launch()
         torch.cuda.synchronize()
-        k1 = np.array([a.elapsed_time(b) for a, b in kev])
-        per = k1
-        h_meas = float(np.mean(1.0 - c[:, 1] / np.maximum(c.sum(axis=1), 1)))
+        per = np.array([a.elapsed_time(b) for a, b in kev])
+        h_meas = float(np.mean(c[:, 0] / np.maximum(c.sum(axis=1), 1)))
         total_ms = max_over_ranks(total_ms, dist, dev)
         bytes_per = float(np.mean([ab[s % pool][0] for s in range(steps)]))
         # consecutive lookups overlap (programmatic dependent launch): the
         # kernel's average duration over the timed region is total / steps;
         # the event-bracketed per-call times above are single-call latencies
         return dict(total_ms=total_ms, p50_us=float(np.median(per) * 1e3),
-                    p99_us=float(np.percentile(per, 99) * 1e3), k1_us=float(k1.mean() * 1e3),
+                    p99_us=float(np.percentile(per, 99) * 1e3), k1_us=float(per.mean() * 1e3),
                     h=h_meas, h_draw=h_draw, p=p, bytes_per_batch=bytes_per,
                     unique_per_batch=float(np.mean([a[2] for a in ab])),
-                    probes_per_unique=float(np.mean([a[3] for a in ab])), launches=launches)
+                    probes_per_unique=float(np.mean([a[3] for a in ab])), launches=launches,
+                    check=chk)
 
     clocks = ClockSampler(dev)
-    main = device_run(args.hit, args.steps, args.warmup, seed=1000 + rank)
+    main = device_run(args.hit, args.steps, args.warmup, seed=1000 + rank, check=True)
     sweep = {}
-    if args.sweep:
-        for h in (0.5, 0.99):
-            r = device_run(h, max(args.steps // 4, 4), args.warmup, seed=2000 + rank + int(h * 100))
-            sweep[f"{h:.2f}"] = {
-                "keys_per_s": world * max(args.steps // 4, 4) * n / (r["total_ms"] / 1e3),
+
+    def leg(r):
+        kus = r["total_ms"] * 1e3 / args.steps
+        return {"keys_per_s": world * args.steps * n / (r["total_ms"] / 1e3),
                 "p50_batch_us": r["p50_us"], "measured_unique_hit_rate": r["h"],
-                "kernel_us": r["total_ms"] * 1e3 / max(args.steps // 4, 4),
-                "kernel_gbs": r["bytes_per_batch"] / (r["total_ms"] * 1e-3 / max(args.steps // 4, 4)) / 1e9,
-                "roofline_frac": r["bytes_per_batch"] / (r["total_ms"] * 1e-3 / max(args.steps // 4, 4))
-                / 1e9 / hbm_peak()[0],
+                "kernel_us": kus, "kernel_gbs": r["bytes_per_batch"] / (kus * 1e-6) / 1e9,
+                "roofline_frac": r["bytes_per_batch"] / (kus * 1e-6) / 1e9 / hbm_peak()[0],
                 "algorithmic_bytes_per_batch": r["bytes_per_batch"]}
-    sweep[f"{args.hit:.2f}"] = {
-        "keys_per_s": world * args.steps * n / (main["total_ms"] / 1e3),
-        "p50_batch_us": main["p50_us"], "measured_unique_hit_rate": main["h"],
-        "kernel_us": main["total_ms"] * 1e3 / args.steps,
-        "kernel_gbs": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9,
-        "roofline_frac": main["bytes_per_batch"] / (main["total_ms"] * 1e-3 / args.steps) / 1e9
-        / hbm_peak()[0],
-        "algorithmic_bytes_per_batch": main["bytes_per_batch"]}
+
+    if args.sweep:
+        # the sweep legs time the same number of steps as the headline
+        for h in (0.5, 0.99):
+            sweep[f"{h:.2f}"] = leg(device_run(h, args.steps, args.warmup,
+                                               seed=2000 + rank + int(h * 100)))
+    sweep[f"{args.hit:.2f}"] = leg(main)
 
     online = None
     if not args.no_online:
@@ -439,15 +484,20 @@ def run_ours(args, rank, world, local_rank):
             "hit_rate_sweep": sweep,
             "roofline": {"bound": "hbm", "kernel": "k_lookup_tag", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "frac": achieved / peak, "traffic": ncu_traffic()[0],
+                         "traffic_source": ncu_traffic()[1],
                          "algorithmic_bytes_per_launch": main["bytes_per_batch"],
                          "kernel_us": kernel_us,
                          "single_call_latency_us": main["k1_us"],
                          "frac_of_8tbs_spec": achieved / 8000.0},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "online": online,
             "gpu_launches": main["launches"],
+            "self_check": main["check"],
         }
         print(json.dumps(result))
+        if main["check"] is not None and not main["check"]["ok"]:
+            sys.exit("bench self-check FAILED: the timed lookups' outputs differ from the "
+                     "expected rows / counts / claims")
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -526,7 +576,7 @@ def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
     fl = torch.empty(n, dtype=torch.uint8, device=dev)
     mk = torch.empty(n, dtype=torch.int64, device=dev)
     mf = torch.empty(n, dtype=torch.int32, device=dev)
-    steps = max(args.steps // 4, 8)
+    steps = args.steps  # the same step count as the headline
     cnt = torch.zeros(2 * steps, dtype=torch.int64, device=dev)
     dr = torch.zeros(d, device=dev)
 
@@ -536,17 +586,18 @@ def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
         k, r = upd_sets[s % 8]
         cache.update_device_async(k.data_ptr(), u, r.data_ptr(), written.data_ptr(), sp)
 
-    for s in range(4):
+    for s in range(max(args.warmup, 4)):
         step(s)
     torch.cuda.synchronize()
     g = hps.StreamGraph(sp)
     with g:
+        hps.event_record(ev[0].cuda_event, sp)
         for s in range(steps):
             step(s)
+        hps.event_record(ev[1].cuda_event, sp)
+    g.launch()  # warm (replays are exact: fresh stamps per launch)
     torch.cuda.synchronize()
-    ev[0].record(st)
     g.launch()
-    ev[1].record(st)
     torch.cuda.synchronize()
     mixed_ms = ev[0].elapsed_time(ev[1]) / steps
     return {"update_all_resident": {"rows": R, "row_bytes": row_bytes, "ms": upd_ms,

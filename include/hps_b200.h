@@ -146,13 +146,25 @@ int hps_cache_set_profile_events(hps_cache* cache, void* start_event, void* end_
 
 /* CUDA graph capture through this library's runtime (device-mode calls
  * enqueued on `stream` between begin and end become graph nodes; no host
- * synchronising calls may be made in between). end_capture instantiates
- * the graph into *graph_exec; launch replays it on `stream`. A captured
- * lookup bakes in its recency stamp: launch such a graph once. */
+ * synchronising calls may be made in between, and a cache captured on one
+ * thread must not be used by other threads until end_capture). end_capture
+ * instantiates the graph into *graph_exec (an opaque handle of this
+ * library). Captured lookups are REPLAYABLE: each hps_graph_launch writes
+ * the caches' current recency clock and lookup-view uses into device words
+ * the graph's lookups read their stamps and view generations relative to
+ * (one small kernel before the graph), then advances them by what one replay
+ * consumes -- a replay is exactly the same lookups issued again (fresh
+ * stamps in stream order, unique hits counted). Replays
+ * must go through hps_graph_launch, which also orders each cache's own
+ * stream before and after the graph; destroy a graph before its caches. */
 int hps_stream_begin_capture(void* stream);
 int hps_stream_end_capture(void* stream, void** graph_exec);
 int hps_graph_launch(void* graph_exec, void* stream);
 int hps_graph_destroy(void* graph_exec);
+/* Records the cudaEvent_t `event` on `stream`; inside a capture as an
+ * external record node (its timestamp stays readable after each launch of
+ * the graph -- bench.py's timed region is bracketed this way). */
+int hps_event_record(void* event, void* stream);
 
 /* replaces SlabCache::replace (slab_cache.cpp:93-107). Rejects a wrong
  * vector size or duplicate keys before any mutation. */
@@ -275,7 +287,8 @@ typedef struct {
   uint32_t workspace_pool_size;
   uint32_t async_worker_count;
   int volatile_tier_enabled;
-  uint32_t max_batch; /* device workspace capacity in keys (0 = 131072) */
+  uint32_t max_batch; /* largest accepted batch in keys; larger calls fail with
+                         HPS_INVALID_ARGUMENT (0 = no limit below 2^32) */
 } hps_engine_config;
 
 /* Mirrors LookupOutcome (lookup_engine.hpp:145-150). */

@@ -239,9 +239,25 @@ void orc_cache_query(orc_cache* c, const uint64_t* keys, size_t n, float* out,
  * current clock (no increment). */
 int orc_cache_replace(orc_cache* c, const uint64_t* keys, size_t n,
                       const float* vecs) {
-  for (size_t i = 0; i < n; ++i)
-    for (size_t j = i + 1; j < n; ++j)
-      if (keys[i] == keys[j]) return 1;
+  if (n > 1) {
+    /* duplicate check before any mutation (slab_cache.cpp:95-101): one
+     * open-addressing pass instead of all pairs (million-key preloads) */
+    size_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    uint64_t* tk = (uint64_t*)malloc(cap * sizeof(uint64_t));
+    unsigned char* used = (unsigned char*)calloc(cap, 1);
+    int dup = 0;
+    for (size_t i = 0; i < n && !dup; ++i) {
+      size_t h = (size_t)orc_xxh64_key(keys[i], 0x0DDull) & (cap - 1);
+      while (used[h] && tk[h] != keys[i]) h = (h + 1) & (cap - 1);
+      if (used[h]) dup = 1;
+      used[h] = 1;
+      tk[h] = keys[i];
+    }
+    free(tk);
+    free(used);
+    if (dup) return 1;
+  }
   const size_t per_set = (size_t)c->W * 32;
   for (size_t i = 0; i < n; ++i) {
     const uint64_t k = keys[i];

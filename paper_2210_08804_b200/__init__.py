@@ -141,6 +141,7 @@ SIGNATURES = {
     "hps_stream_end_capture": (C.c_int, [_P, C.POINTER(_P)]),
     "hps_graph_launch": (C.c_int, [_P, _P]),
     "hps_graph_destroy": (C.c_int, [_P]),
+    "hps_event_record": (C.c_int, [_P, _P]),
     "hps_cache_replace": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, C.c_int, _P]),
     "hps_cache_update": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _SZP, C.c_int, _P]),
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
@@ -266,6 +267,12 @@ class StreamGraph:
                 lib().hps_graph_destroy(self.exec)
         except Exception:
             pass
+
+
+def event_record(event: int, stream: int) -> None:
+    """Records a cudaEvent_t on a stream (an external record node inside a
+    capture, so it can time a region of a replayed graph)."""
+    _check(lib().hps_event_record(event, stream))
 
 
 def partition_of(key: int, partition_count: int) -> int:
@@ -782,7 +789,7 @@ class EngineConfig:
     workspace_pool_size: int = 16
     async_worker_count: int = 2
     volatile_tier_enabled: bool = True
-    max_batch: int = 131072
+    max_batch: int = 0  # largest accepted batch (0 = no limit below 2^32)
 
 
 @dataclass

@@ -3,6 +3,7 @@
 // thread-local for hps_last_error().
 #include "hps_b200.h"
 
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -24,6 +25,11 @@ struct hps_engine {
 };
 struct hps_multi {
   std::unique_ptr<hpsb::MultiLookup> impl;
+};
+// A captured graph and what each of its caches consumes per replay.
+struct hps_graph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<hpsb::GraphCacheUse> uses;
 };
 
 namespace hpsb {
@@ -342,26 +348,79 @@ int hps_stream_begin_capture(void* stream) {
 int hps_stream_end_capture(void* stream, void** graph_exec) {
   return guarded([&] {
     need(stream != nullptr && graph_exec != nullptr, "null argument");
-    cudaGraph_t g = nullptr;
-    HPSB_CUDA(cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g));
-    cudaGraphExec_t ge = nullptr;
-    const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
-    cudaGraphDestroy(g);
-    HPSB_CUDA(e);
-    *graph_exec = ge;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    unsigned long long cid = 0;
+    HPSB_CUDA(cudaStreamGetCaptureInfo(st, &cs, &cid));
+    // close the caches' capture sessions whatever happens next (their host
+    // clocks and view uses go back to the values at capture start)
+    auto g = std::make_unique<hps_graph>();
+    g->uses = hpsb::DeviceCache::end_capture(cid);
+    cudaGraph_t gr = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(st, &gr);
+    if (ec != cudaSuccess) {
+      for (auto& u : g->uses)
+        if (hpsb::DeviceCache::alive(u.cache, u.serial)) u.cache->release_rebase_slot(u.slot);
+      g->uses.clear();
+      HPSB_CUDA(ec);
+    }
+    const cudaError_t e = cudaGraphInstantiate(&g->exec, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) {
+      for (auto& u : g->uses)
+        if (hpsb::DeviceCache::alive(u.cache, u.serial)) u.cache->release_rebase_slot(u.slot);
+      g->uses.clear();
+      HPSB_CUDA(e);
+    }
+    *graph_exec = g.release();
   });
 }
 
 int hps_graph_launch(void* graph_exec, void* stream) {
   return guarded([&] {
     need(graph_exec != nullptr, "null graph");
-    HPSB_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), as_stream(stream)));
+    auto* g = static_cast<hps_graph*>(graph_exec);
+    cudaStream_t x = as_stream(stream);
+    // every cache of the graph is held for the whole launch (address order:
+    // no lock-order inversion between concurrent launches)
+    std::vector<hpsb::GraphCacheUse*> us;
+    for (auto& u : g->uses) {
+      need(hpsb::DeviceCache::alive(u.cache, u.serial),
+           "a cache captured in this graph has been destroyed");
+      us.push_back(&u);
+    }
+    std::sort(us.begin(), us.end(),
+              [](const hpsb::GraphCacheUse* a, const hpsb::GraphCacheUse* b) { return a->cache < b->cache; });
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (size_t i = 0; i < us.size(); ++i)
+      if (i == 0 || us[i]->cache != us[i - 1]->cache) locks.emplace_back(us[i]->cache->mutex());
+    for (auto* u : us) u->cache->graph_before_launch_locked(*u, x);
+    HPSB_CUDA(cudaGraphLaunch(g->exec, x));
+    for (auto* u : us) u->cache->graph_after_launch_locked(x);
+  });
+}
+
+int hps_event_record(void* event, void* stream) {
+  return guarded([&] {
+    need(event != nullptr, "null event");
+    cudaStream_t st = as_stream(stream);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    HPSB_CUDA(cudaStreamIsCapturing(st, &cs));
+    HPSB_CUDA(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(event), st,
+                                       cs == cudaStreamCaptureStatusActive
+                                           ? cudaEventRecordExternal
+                                           : cudaEventRecordDefault));
   });
 }
 
 int hps_graph_destroy(void* graph_exec) {
   return guarded([&] {
-    if (graph_exec) HPSB_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)));
+    auto* g = static_cast<hps_graph*>(graph_exec);
+    if (g == nullptr) return;
+    for (auto& u : g->uses)
+      if (hpsb::DeviceCache::alive(u.cache, u.serial)) u.cache->release_rebase_slot(u.slot);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    delete g;
   });
 }
 
@@ -631,7 +690,7 @@ int hps_engine_create(const char* table, uint32_t dimension, hps_cache* cache, h
     c.workspace_pool_size = config->workspace_pool_size;
     c.async_worker_count = config->async_worker_count;
     c.volatile_tier_enabled = config->volatile_tier_enabled != 0;
-    c.max_batch = config->max_batch ? config->max_batch : 131072;
+    c.max_batch = config->max_batch;  // 0 = no limit (below 2^32)
     auto h = std::make_unique<hps_engine>();
     h->impl = std::make_unique<hpsb::LookupEngine>(table, dimension, cache->impl.get(),
                                                    vdb ? vdb->impl.get() : nullptr, cold,

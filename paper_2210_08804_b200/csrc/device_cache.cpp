@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -23,6 +24,12 @@ struct Carver {
     return r;
   }
 };
+
+// Live caches and the open capture sessions (capture id -> caches).
+std::mutex g_reg_mu;
+std::map<const DeviceCache*, uint64_t> g_alive;
+std::map<unsigned long long, std::vector<DeviceCache*>> g_sessions;
+uint64_t g_next_serial = 1;
 
 int keys_per_warp_for(uint32_t tasks_per_worker) {
   // SlabCacheConfig::tasks_per_worker (slab_cache.hpp:33) becomes the number
@@ -80,7 +87,11 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
   dev_.counters = reinterpret_cast<decltype(dev_.counters)>(pm + ctr_off);
   HPSB_CUDA(cudaMalloc(&dev_.rows, slots * uint64_t(cfg.dimension) * 4));
   HPSB_CUDA(cudaMalloc(&dev_.occupied, 8));
-  lookup_marks_locked(0);  // allocated up front: lookups may be graph-captured
+  // rebase slots of captured graphs (allocated up front: no allocation may
+  // happen while a stream is being captured)
+  HPSB_CUDA(cudaMalloc(&rebase_, kRebaseSlots * 16 * 8));
+  HPSB_CUDA(cudaMemsetAsync(rebase_, 0, kRebaseSlots * 16 * 8, stream_));
+  for (int i = kRebaseSlots - 1; i >= 0; --i) free_slots_.push_back(i);
   // update: last position per slot, two arrays (consecutive updates alternate)
   HPSB_CUDA(cudaMalloc(&winner_, 2 * slots * 4));
   HPSB_CUDA(cudaMemsetAsync(winner_, 0, 2 * slots * 4, stream_));
@@ -131,9 +142,23 @@ DeviceCache::DeviceCache(const CacheConfig& cfg, int device, const DeviceCache* 
   HPSB_CUDA(cudaMemsetAsync(scan_.tile_ctr, 0, 8, stream_));
   ensure_scan_tiles(1024);
   HPSB_CUDA(cudaStreamSynchronize(stream_));
+  std::lock_guard<std::mutex> rl(g_reg_mu);
+  serial_ = g_next_serial++;
+  g_alive[this] = serial_;
 }
 
 DeviceCache::~DeviceCache() {
+  {
+    std::lock_guard<std::mutex> rl(g_reg_mu);
+    g_alive.erase(this);
+    if (cap_.id != 0) {
+      auto it = g_sessions.find(cap_.id);
+      if (it != g_sessions.end()) {
+        auto& v = it->second;
+        v.erase(std::remove(v.begin(), v.end(), this), v.end());
+      }
+    }
+  }
   DeviceGuard g(device_);
   cudaStreamSynchronize(stream_);
   cudaFree(probe_mem_);
@@ -144,7 +169,7 @@ DeviceCache::~DeviceCache() {
   cudaFree(scan_.tile_ctr);
   cudaFree(scan_.status);
   cudaFree(trace_);
-  cudaFree(marks_);
+  cudaFree(rebase_);
   cudaFree(winner_);
   cudaEventDestroy(ev_in_);
   cudaEventDestroy(ev_out_);
@@ -280,9 +305,28 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
                                 const float* default_row, uint64_t* miss_keys,
                                 uint32_t* miss_firsts, uint64_t* counts, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(mu_);
-  const uint64_t stamp = bump_clock();
   DeviceGuard g(device_);
   join_from(user);
+  // inside a stream capture (the cache's stream joined it through join_from):
+  // the call's stamp and view generation become relative to the rebase words
+  // of this cache's capture session (graph_before_launch_locked)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long cid = 0;
+  HPSB_CUDA(cudaStreamGetCaptureInfo(stream_, &cs, &cid));
+  const bool capturing = cs == cudaStreamCaptureStatusActive;
+  if (capturing && cap_.id != cid) {
+    if (cap_.id != 0) throw invalid_argument("cache is already part of another stream capture");
+    if (free_slots_.empty()) throw invalid_argument("too many live captured graphs on this cache");
+    cap_.id = cid;
+    cap_.slot = free_slots_.back();
+    free_slots_.pop_back();
+    cap_.clock0 = clock_.load(std::memory_order_relaxed);
+    for (int k = 0; k < kLookupViews; ++k) cap_.uses0[k] = lws_.uses[k];
+    mark_other_op();  // the first captured lookup chains onto nothing
+    std::lock_guard<std::mutex> rl(g_reg_mu);
+    g_sessions[cid].push_back(this);
+  }
+  const uint64_t stamp = bump_clock();
   if (n == 0) {
     mark_other_op();
     HPSB_CUDA(cudaMemsetAsync(counts, 0, 16, stream_));
@@ -291,8 +335,10 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   }
   if (n >= (1ull << 32)) throw invalid_argument("lookup batch too large");
   if (n > lcap_) {
+    if (capturing)
+      throw invalid_argument("run one lookup of this batch size before capturing lookups");
     // (re)carve: miss table >= 2n entries, per-position slots, claim list,
-    // counters -- zeroed once, then kept clean by the kernels
+    // counters, hit tables -- zeroed once, then kept clean by the kernels
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
     const uint64_t bytes = lookup_scratch_bytes(cap);
@@ -305,13 +351,19 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   // programmatic dependent of the previous lookup when nothing else was
   // enqueued in between (the kernel orders itself against it)
   static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
-  // (never inside a cache group: other caches' work shares the stream)
-  uint32_t* marks = lookup_marks_locked(stamp);  // (may enqueue a reset first)
+  if (!capturing) prepare_hits(lws_, stamp);  // (may enqueue a clear first)
   const bool after_update = last_op_update_;
+  // (never inside a cache group: other caches' work shares the stream)
   const bool chain = (last_op_lookup_ || last_op_update_) && !no_pdl &&
                      stream_holder_.use_count() == 1;
   LookupView v = lookup_next_view(lws_, chain);
-  v.marks = marks + uint64_t(lws_.last) * capacity_slots();
+  uint64_t kstamp = stamp;
+  if (capturing) {
+    kstamp = stamp - cap_.clock0;
+    v.gen -= cap_.uses0[v.idx];
+    if (v.prev_completed != nullptr) v.prev_target -= cap_.uses0[v.prev_idx];
+    v.rebase = rebase_ + uint64_t(cap_.slot) * 16;
+  }
   static const bool tracing = std::getenv("HPSB_TRACE") != nullptr;
   if (tracing) {
     if (trace_ == nullptr) {
@@ -326,15 +378,12 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
   v.counts_out = reinterpret_cast<unsigned long long*>(counts);
   // profile events: external records when the stream is being captured into
   // a CUDA graph, so the timestamps stay readable after graph launches
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (prof_start_ || prof_end_) HPSB_CUDA(cudaStreamIsCapturing(stream_, &cap));
-  const unsigned rec_flags =
-      cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  const unsigned rec_flags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (prof_start_) {
     HPSB_CUDA(cudaEventRecordWithFlags(prof_start_, stream_, rec_flags));
     mark_other_op();
   }
-  launch_lookup_probe(dev_, keys, n, out, flags, default_row, stamp, v, chain, stream_,
+  launch_lookup_probe(dev_, keys, n, out, flags, default_row, kstamp, v, chain, stream_,
                       /*wait_before_copy=*/after_update);
   mark_other_op();
   last_op_lookup_ = true;
@@ -343,6 +392,93 @@ void DeviceCache::lookup_device(const uint64_t* keys, size_t n, float* out, uint
     mark_other_op();
   }
   join_to(user);
+}
+
+void DeviceCache::prepare_hits(LookupScratch& ls, uint64_t stamp) {
+  if ((stamp >> 32) == ls.hit_epoch) return;
+  // every 2^32 stamps: an entry of the previous epoch could carry this
+  // call's tag (stream-ordered after every earlier lookup)
+  HPSB_CUDA(cudaMemsetAsync(ls.hits_base, 0, ls.hits_bytes, stream_));
+  mark_other_op();
+  ls.hit_epoch = stamp >> 32;
+}
+
+std::vector<GraphCacheUse> DeviceCache::end_capture(unsigned long long capture_id) {
+  std::vector<DeviceCache*> caches;
+  {
+    std::lock_guard<std::mutex> rl(g_reg_mu);
+    auto it = g_sessions.find(capture_id);
+    if (it == g_sessions.end()) return {};
+    caches = std::move(it->second);
+    g_sessions.erase(it);
+  }
+  std::vector<GraphCacheUse> out;
+  for (DeviceCache* c : caches) {
+    std::lock_guard<std::mutex> lk(c->mu_);
+    GraphCacheUse u;
+    u.cache = c;
+    u.serial = c->serial_;
+    u.slot = c->cap_.slot;
+    // what one replay consumes; the capture itself consumed nothing
+    u.stamps = c->clock_.load(std::memory_order_relaxed) - c->cap_.clock0;
+    c->clock_.store(c->cap_.clock0, std::memory_order_relaxed);
+    for (int k = 0; k < kLookupViews; ++k) {
+      u.uses[k] = c->lws_.uses[k] - c->cap_.uses0[k];
+      c->lws_.uses[k] = c->cap_.uses0[k];
+    }
+    c->cap_ = CaptureSession{};
+    c->mark_other_op();
+    out.push_back(u);
+  }
+  return out;
+}
+
+void DeviceCache::graph_before_launch_locked(const GraphCacheUse& u, cudaStream_t x) {
+  DeviceGuard g(device_);
+  if (x != stream_) {
+    // earlier work of the cache precedes the graph
+    HPSB_CUDA(cudaEventRecord(ev_in_, stream_));
+    HPSB_CUDA(cudaStreamWaitEvent(x, ev_in_, 0));
+  }
+  if (u.stamps >= (1ull << 31)) throw invalid_argument("captured graph holds too many lookups");
+  uint64_t base = clock_.load(std::memory_order_relaxed);
+  if (u.stamps > 0) {
+    // the replay's stamps base+1 .. base+stamps share their high 32 bits and
+    // none has zero low bits (the tag value of a free hit-table entry)
+    if (((base + 1) >> 32) != ((base + u.stamps) >> 32)) base = ((base + u.stamps) >> 32) << 32;
+    const uint64_t epoch = (base + 1) >> 32;
+    if (lws_.hits_base != nullptr && lws_.hit_epoch != epoch) {
+      HPSB_CUDA(cudaMemsetAsync(lws_.hits_base, 0, lws_.hits_bytes, x));
+      lws_.hit_epoch = epoch;
+    }
+  }
+  unsigned long long ub[kLookupViews];
+  for (int k = 0; k < kLookupViews; ++k) ub[k] = lws_.uses[k];
+  launch_rebase(rebase_ + uint64_t(u.slot) * 16, base, ub, x);
+  clock_.store(base + u.stamps, std::memory_order_relaxed);
+  for (int k = 0; k < kLookupViews; ++k) lws_.uses[k] += u.uses[k];
+  mark_other_op();
+}
+
+void DeviceCache::graph_after_launch_locked(cudaStream_t x) {
+  DeviceGuard g(device_);
+  if (x != stream_) {
+    // later work of the cache follows the graph
+    HPSB_CUDA(cudaEventRecord(ev_out_, x));
+    HPSB_CUDA(cudaStreamWaitEvent(stream_, ev_out_, 0));
+  }
+  mark_other_op();
+}
+
+void DeviceCache::release_rebase_slot(int slot) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (slot >= 0) free_slots_.push_back(slot);
+}
+
+bool DeviceCache::alive(const DeviceCache* c, uint64_t serial) {
+  std::lock_guard<std::mutex> rl(g_reg_mu);
+  auto it = g_alive.find(c);
+  return it != g_alive.end() && it->second == serial;
 }
 
 void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
@@ -503,23 +639,6 @@ size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, si
   return n;
 }
 
-uint32_t* DeviceCache::lookup_marks_locked(uint64_t stamp) {
-  const uint64_t bytes = uint64_t(kLookupViews) * capacity_slots() * 4;
-  if (marks_ == nullptr) {
-    HPSB_CUDA(cudaMalloc(&marks_, bytes));
-    HPSB_CUDA(cudaMemsetAsync(marks_, 0, bytes, stream_));
-    mark_other_op();
-    marks_epoch_ = stamp >> 32;
-  } else if ((stamp >> 32) != marks_epoch_) {
-    // every 2^32 stamps: a mark from the previous epoch could equal this
-    // call's low bits (stream-ordered after every earlier lookup)
-    HPSB_CUDA(cudaMemsetAsync(marks_, 0, bytes, stream_));
-    mark_other_op();
-    marks_epoch_ = stamp >> 32;
-  }
-  return marks_;
-}
-
 uint64_t DeviceCache::trace(unsigned long long* out) {
   std::lock_guard<std::mutex> lk(mu_);
   if (trace_ == nullptr) return 0;
@@ -573,17 +692,26 @@ void DeviceCache::check_invariants() {
   const uint64_t slots = S * W * 32;
   std::vector<uint64_t> keys(slots), ctr(slots);
   std::vector<uint32_t> masks(S * W);
-  export_state(keys.data(), ctr.data(), masks.data(), nullptr);
   std::vector<uint8_t> tags(slots);
+  uint64_t occ = 0, clock_now = 0;
   {
+    // one consistent snapshot: keys, counters, masks, fingerprints, the
+    // occupancy counter and the clock under ONE hold of the cache mutex and
+    // one stream sync (the reference holds every set gate for the whole
+    // check, slab_cache.cpp:407-442), so a concurrent replace or engine fill
+    // cannot slip in between the copies
     std::lock_guard<std::mutex> lk(mu_);
     mark_other_op();
     DeviceGuard g(device_);
+    HPSB_CUDA(cudaMemcpyAsync(keys.data(), dev_.keys, slots * 8, cudaMemcpyDeviceToHost, stream_));
+    HPSB_CUDA(cudaMemcpyAsync(ctr.data(), dev_.counters, slots * 8, cudaMemcpyDeviceToHost, stream_));
+    HPSB_CUDA(cudaMemcpyAsync(masks.data(), dev_.masks, S * W * 4, cudaMemcpyDeviceToHost, stream_));
     HPSB_CUDA(cudaMemcpyAsync(tags.data(), dev_.tags, slots, cudaMemcpyDeviceToHost, stream_));
+    HPSB_CUDA(cudaMemcpyAsync(h_small_ + 7, dev_.occupied, 8, cudaMemcpyDeviceToHost, stream_));
     HPSB_CUDA(cudaStreamSynchronize(stream_));
+    occ = h_small_[7];
+    clock_now = recency_clock();
   }
-  const uint64_t clock_now = recency_clock();
-  const uint64_t occ = occupied();
   std::unordered_set<uint64_t> seen;
   seen.reserve(occ);
   uint64_t populated = 0;

@@ -15,6 +15,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.hpp"
 #include "runtime.hpp"
@@ -30,6 +31,19 @@ struct CacheConfig {
 };
 
 enum MemKind : int { kHostMem = 0, kDeviceMem = 1 };
+
+class DeviceCache;
+
+// One cache's lookups inside one captured CUDA graph: what every replay
+// consumes (clock ticks, uses of each lookup view) and the device words the
+// graph's lookups read their stamps / generations relative to.
+struct GraphCacheUse {
+  DeviceCache* cache = nullptr;
+  uint64_t serial = 0;  // the cache's identity (pointers may be reused)
+  int slot = -1;        // rebase slot of the cache
+  uint64_t stamps = 0;  // clock ticks per replay
+  uint64_t uses[kLookupViews] = {};
+};
 
 struct StreamHolder {
   cudaStream_t s = nullptr;
@@ -102,12 +116,12 @@ class DeviceCache {
   // Callers that enqueue their own work on stream() (the engine) call this
   // under mutex() so the next lookup does not chain onto a stale lookup.
   void note_stream_op() { mark_other_op(); }
-  // Mark arrays of the lookup kernels (call under mutex()) for a call with
-  // `stamp`; array i at + i * capacity_slots(). Marks hold the low 32 bits of
-  // stamps; they are reset when the high 32 bits change.
-  uint32_t* lookup_marks_locked(uint64_t stamp);
+  // Makes the distinct-hit tables of `ls` valid for a call with `stamp`
+  // (call under mutex(); enqueues a clear on stream() when the stamps' high
+  // 32 bits changed since the tables were last used).
+  void prepare_hits(LookupScratch& ls, uint64_t stamp);
   uint64_t capacity_slots() const { return cfg_.slabset_count * cfg_.slabs_per_set * 32ull; }
-  // Stamps never have zero low 32 bits (the reset value of the marks).
+  // Stamps never have zero low 32 bits (the tag of a free hit-table entry).
   uint64_t bump_clock() {
     uint64_t s = clock_.fetch_add(1, std::memory_order_relaxed) + 1;
     if (uint32_t(s) == 0) s = clock_.fetch_add(1, std::memory_order_relaxed) + 1;
@@ -121,6 +135,26 @@ class DeviceCache {
   // or identical), and the reverse.
   void join_from(cudaStream_t user);
   void join_to(cudaStream_t user);
+
+  // ---- CUDA graph replay (hps_stream_begin_capture / hps_graph_launch) ----
+  // Lookups captured into a graph take their stamps and view generations
+  // relative to device words (a rebase slot of the cache); every launch of
+  // the graph first writes the current clock and view uses there and
+  // advances them by what one replay consumes, so replays are exactly
+  // equivalent to issuing the same lookups again (fresh stamps in stream
+  // order, unique hits counted, views reused only after release).
+  // The sessions of capture `capture_id`, closed (the host clock and view
+  // uses restored to their values at capture start).
+  static std::vector<GraphCacheUse> end_capture(unsigned long long capture_id);
+  // Launch of a graph on `x`: before -- orders earlier cache work before the
+  // graph and writes the rebase words; after -- orders later cache work after
+  // it. Callers hold mutex() of every cache of the graph.
+  void graph_before_launch_locked(const GraphCacheUse& u, cudaStream_t x);
+  void graph_after_launch_locked(cudaStream_t x);
+  void release_rebase_slot(int slot);
+  uint64_t serial() const { return serial_; }
+  // true when `c` with `serial` is a live cache
+  static bool alive(const DeviceCache* c, uint64_t serial);
 
  private:
   void* scratch(size_t bytes) { return scratch_.ensure(bytes, stream_); }
@@ -154,10 +188,17 @@ class DeviceCache {
     last_op_update_ = false;
   }
   std::shared_ptr<StreamHolder> stream_holder_;
-  // unique-hit marks of the lookup kernels: kLookupViews arrays of one u32
-  // per slot (see LookupView::marks), valid for stamps of epoch marks_epoch_
-  uint32_t* marks_ = nullptr;
-  uint64_t marks_epoch_ = 0;
+  // graph capture: the open session of this cache (capture id 0 = none)
+  struct CaptureSession {
+    unsigned long long id = 0;
+    int slot = -1;
+    uint64_t clock0 = 0;
+    uint64_t uses0[kLookupViews] = {};
+  } cap_;
+  static constexpr int kRebaseSlots = 64;
+  unsigned long long* rebase_ = nullptr;  // kRebaseSlots x 16 words
+  std::vector<int> free_slots_;
+  uint64_t serial_ = 0;
   // update: per-slot winning position + 1 (all-zero between calls); two
   // arrays, consecutive updates alternate (the next update's probe may run
   // while this update's write kernel is in flight)

@@ -200,7 +200,8 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   if (n <= capacity && d == dim && dbuf.get() != nullptr) return;
   uint64_t cap = 1024;
   while (cap < n) cap <<= 1;
-  const uint64_t ls_bytes = lookup_scratch_bytes(cap);
+  // one lookup view: a workspace serves one call at a time (wait_idle)
+  const uint64_t ls_bytes = lookup_scratch_bytes(cap, 1);
   const uint64_t hdr_bytes = 16 + cap * 4 + 8 + cap * 8 + cap;
   const uint64_t dev_bytes = a256(cap * 8) * 3 + a256(cap * uint64_t(d) * 4) * 2 + a256(cap) +
                              a256(cap * 4) + a256(ls_bytes);
@@ -219,7 +220,7 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   d_found_keys = reinterpret_cast<uint64_t*>(take(cap * 8));
   char* ls_base = take(ls_bytes);
   HPSB_CUDA(cudaMemsetAsync(ls_base, 0, ls_bytes, st));
-  ls = lookup_scratch_carve(ls_base, cap);
+  ls = lookup_scratch_carve(ls_base, cap, 1);
 
   const uint64_t host_bytes = a256(cap * 8) * 5 + a256(16) + a256(cap * 4) * 3 +
                               a256(cap * uint64_t(d) * 4) * 2 + a256(cap) + a256(hdr_bytes);
@@ -349,8 +350,12 @@ void LookupEngine::lookup_multi(LookupEngine* const* engines, size_t count,
   calls.reserve(count);
   try {
     for (size_t t = 0; t < count; ++t)
+      // device mode orders against the legacy default stream, exactly as
+      // hps_engine_lookup with a NULL stream (join_from / join_to skip a
+      // null stream, which would leave the caller's keys and later reads
+      // unordered against the cache stream)
       calls.push_back(engines[t]->begin(keys[t], n[t], out[t], n[t] * engines[t]->dim_, flags[t],
-                                        mem, nullptr));
+                                        mem, cudaStreamLegacy));
   } catch (...) {
     for (auto& c : calls) c.engine->abandon(c);
     throw;
@@ -377,6 +382,10 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
                                              size_t out_len, uint8_t* flags, int mem,
                                              cudaStream_t user) {
   if (out_len != n * uint64_t(dim_)) throw invalid_argument("lookup output buffer has wrong size");
+  // positions and first occurrences are u32 on the device
+  if (n >= 0xFFFFFFFFull) throw invalid_argument("lookup batch too large");
+  if (cfg_.max_batch != 0 && n > cfg_.max_batch)
+    throw invalid_argument("lookup batch exceeds the engine's max_batch");
   LookupCall c;
   c.engine = this;
   c.n = n;
@@ -435,8 +444,8 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
       } else {
         cache_->join_from(user);
       }
+      cache_->prepare_hits(ws->ls, stamp);
       ws->lv = lookup_next_view(ws->ls, /*chain=*/false);
-      ws->lv.marks = cache_->lookup_marks_locked(stamp);
       if (c.packed) {
         const uint64_t fo = 16, ko = 16 + (n * 4 + 7) / 8 * 8, flo = ko + n * 8;
         ws->lv.counts_out = reinterpret_cast<unsigned long long*>(ws->h_hdr);
@@ -793,10 +802,12 @@ MultiLookup::MultiLookup(std::vector<LookupEngine*> engines, uint64_t max_batch)
   dev_.ensure(o, st);
   host_.ensure(o);
   h_rows_ = d_rows_;
-  const uint64_t sbytes = lookup_scratch_bytes(maxb_);
+  // one view per table: every group call completes before the next starts
+  const uint64_t sbytes = lookup_scratch_bytes(maxb_, 1);
   char* sp = static_cast<char*>(scratch_dev_.ensure(a256m(sbytes) * T, st));
   HPSB_CUDA(cudaMemsetAsync(sp, 0, a256m(sbytes) * T, st));
-  for (uint64_t t = 0; t < T; ++t) ls_.push_back(lookup_scratch_carve(sp + t * a256m(sbytes), maxb_));
+  for (uint64_t t = 0; t < T; ++t)
+    ls_.push_back(lookup_scratch_carve(sp + t * a256m(sbytes), maxb_, 1));
   HPSB_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
   HPSB_CUDA(cudaStreamSynchronize(st));
 }
@@ -853,13 +864,21 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
     std::lock_guard<std::mutex> clk(c->mutex());
     const uint64_t stamp = c->bump_clock();  // query ticks even when empty
     c->note_stream_op();
+    TableLookup& tl = desc[t];
+    if (n[t] == 0) {
+      // no blocks run for an empty table: it takes no view (a view handed
+      // out here would never be released, and its next use would wait
+      // forever on the device)
+      std::memset(static_cast<void*>(&tl), 0, sizeof(tl));
+      tl.block_begin = blocks;
+      continue;
+    }
+    c->prepare_hits(ls_[t], stamp);
     LookupView v = lookup_next_view(ls_[t], false);
-    v.marks = c->lookup_marks_locked(stamp);
     v.list_keys = reinterpret_cast<uint64_t*>(ob + d_ckeys_) + koff[t];
     v.list_firsts = reinterpret_cast<uint32_t*>(ob + d_cfirsts_) + koff[t];
     v.counts_out = reinterpret_cast<unsigned long long*>(ob + d_counts_) + 2 * t;
     views[t] = v;
-    TableLookup& tl = desc[t];
     tl.c = c->dev();
     tl.keys = reinterpret_cast<const uint64_t*>(db + d_keys_) + koff[t];
     tl.n = n[t];

@@ -61,7 +61,7 @@ struct EngineConfig {
   uint32_t workspace_pool_size = 16;
   uint32_t async_worker_count = 2;
   bool volatile_tier_enabled = true;
-  uint32_t max_batch = 131072;
+  uint32_t max_batch = 0;  // largest accepted batch (0 = any below 2^32)
 };
 
 struct LookupOutcome {

@@ -109,10 +109,19 @@ struct LookupView {
   // the previous call on the stream (its completion precedes this call's)
   const unsigned long long* prev_completed = nullptr;
   unsigned long long prev_target = 0;
-  // per-slot low 32 bits of the stamp of the last call that counted the slot
-  // as a unique hit (one array per concurrently running call, see
-  // DeviceCache::lookup_marks_locked)
-  uint32_t* marks = nullptr;
+  // distinct hit slots of the call (open addressing, `cap` entries, 2^log2cap):
+  // (low 32 bits of the call's stamp << 32) | slot. An entry whose tag is not
+  // this call's stamp is free (a previous use of the view), so the table needs
+  // no clearing between calls; inserting a slot for the first time counts one
+  // unique hit. Cleared only when the stamps' high 32 bits change
+  // (DeviceCache::prepare_hits).
+  unsigned long long* hits = nullptr;
+  uint32_t log2cap = 0;
+  // graph replay (DeviceCache capture sessions): stamp, gen and prev_target
+  // are relative to device words written before every launch of the graph
+  // ([0] stamp base, [1 + view] use base of view `view`); nullptr = absolute
+  const unsigned long long* rebase = nullptr;
+  uint32_t idx = 0, prev_idx = 0;  // this call's / the previous call's view index
   // zero-copy engine calls: a device copy of the miss flags (the output flags
   // live in pinned host memory; the sync branch's scatter reads this copy)
   uint8_t* flags_dev = nullptr;
@@ -128,17 +137,27 @@ constexpr int kLookupViews = HPSB_LOOKUP_VIEWS;
 struct LookupScratch {
   LookupView v[kLookupViews];
   uint64_t uses[kLookupViews] = {};  // host: uses handed out per view
+  int nviews = kLookupViews;         // views in the ring (1 for unchained users)
   int next = 0;
   int last = -1;
+  // hit tables of every view, contiguous (one memset clears them)
+  void* hits_base = nullptr;
+  uint64_t hits_bytes = 0;
+  uint64_t hit_epoch = ~0ull;  // stamp >> 32 the tables are valid for
 };
-// The view of the next call (host bookkeeping; marks not set). chain: the
-// call is launched as a programmatic dependent of the previous call taken
-// from this scratch, whose completion it then waits for before completing.
+// The view of the next call (host bookkeeping). chain: the call is launched
+// as a programmatic dependent of the previous call taken from this scratch,
+// whose completion it then waits for before completing.
 LookupView lookup_next_view(LookupScratch& ls, bool chain);
-// Bytes / carving of a LookupScratch for batches of up to `cap` keys (the
-// caller zero-fills the block once; carving resets the host bookkeeping).
-size_t lookup_scratch_bytes(uint64_t cap);
-LookupScratch lookup_scratch_carve(void* base, uint64_t cap);
+// Bytes / carving of a LookupScratch of `nviews` views for batches of up to
+// `cap` keys (the caller zero-fills the block once; carving resets the host
+// bookkeeping).
+size_t lookup_scratch_bytes(uint64_t cap, int nviews = kLookupViews);
+LookupScratch lookup_scratch_carve(void* base, uint64_t cap, int nviews = kLookupViews);
+// Writes the rebase words of a captured graph's lookups (one thread):
+// w[0] = stamp base, w[1 + k] = use base of view k.
+void launch_rebase(unsigned long long* w, unsigned long long stamp_base,
+                   const unsigned long long (&use_base)[kLookupViews], cudaStream_t st);
 // One launch per lookup (probe, claims, stamps, row gather / default rows,
 // and the call's completion by its last block). after_lookup: the previous
 // operation on `st` was a lookup or update kernel -> launched as its

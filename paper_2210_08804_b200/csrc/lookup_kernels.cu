@@ -85,23 +85,28 @@ uint64_t view_bytes(uint64_t cap) {
 }
 }  // namespace
 
-size_t lookup_scratch_bytes(uint64_t cap) { return kLookupViews * view_bytes(cap); }
+size_t lookup_scratch_bytes(uint64_t cap, int nviews) {
+  return uint64_t(nviews) * (view_bytes(cap) + a256(table_cap(cap) * 8));
+}
 
 LookupView lookup_next_view(LookupScratch& ls, bool chain) {
   const int i = ls.next;
   LookupView v = ls.v[i];
   v.gen = ls.uses[i]++;
+  v.idx = uint32_t(i);
   if (chain && ls.last >= 0) {
     v.prev_completed = ls.v[ls.last].completed;
     v.prev_target = ls.uses[ls.last];  // that call's gen + 1
+    v.prev_idx = uint32_t(ls.last);
   }
   ls.last = i;
-  ls.next = (i + 1) % kLookupViews;
+  ls.next = (i + 1) % ls.nviews;
   return v;
 }
 
-LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
+LookupScratch lookup_scratch_carve(void* base, uint64_t cap, int nviews) {
   LookupScratch ls;
+  ls.nviews = nviews;
   const uint64_t tcap = table_cap(cap);
   char* p = static_cast<char*>(base);
   auto take = [&](uint64_t b) {
@@ -109,7 +114,16 @@ LookupScratch lookup_scratch_carve(void* base, uint64_t cap) {
     p += a256(b);
     return r;
   };
-  for (int k = 0; k < kLookupViews; ++k) {
+  uint32_t lg = 0;
+  while ((1ull << lg) < tcap) ++lg;
+  // every view's hit table first, contiguous
+  ls.hits_base = p;
+  ls.hits_bytes = uint64_t(nviews) * a256(tcap * 8);
+  for (int k = 0; k < nviews; ++k) {
+    ls.v[k].hits = reinterpret_cast<unsigned long long*>(take(tcap * 8));
+    ls.v[k].log2cap = lg;
+  }
+  for (int k = 0; k < nviews; ++k) {
     LookupView& v = ls.v[k];
     v.cap = tcap;
     v.miss_table = reinterpret_cast<uint32_t*>(take(tcap * 4));
@@ -235,7 +249,8 @@ __device__ void finish_claims(const LookupView& v) {
   }
 }
 
-__device__ void finish_counts(const LookupView& v) {
+__device__ void finish_counts(const LookupView& v, unsigned long long gen,
+                              unsigned long long prev_target) {
   if (threadIdx.x < 32) {
     // 128 values, 4 per lane, loaded together
     const uint32_t i = threadIdx.x & 1u;
@@ -254,9 +269,9 @@ __device__ void finish_counts(const LookupView& v) {
       v.done[1] = 0u;
       // completion order = launch order: this call completes after the
       // previous one, so stream work after it sees every earlier lookup done
-      if (v.prev_completed != nullptr) spin_ge(v.prev_completed, v.prev_target);
+      if (v.prev_completed != nullptr) spin_ge(v.prev_completed, prev_target);
       __threadfence();
-      st_release(v.completed, v.gen + 1);  // the view is free for its next use
+      st_release(v.completed, gen + 1);  // the view is free for its next use
     }
   }
 }
@@ -323,9 +338,65 @@ __device__ __forceinline__ uint32_t warp_claim_misses(const LookupView& v,
   return claimed ? 1u : 0u;
 }
 
+// Per-call sequence values: a lookup captured into a CUDA graph carries them
+// relative to rebase words the library writes before every launch of the
+// graph (DeviceCache capture sessions), so replays take fresh stamps and
+// view generations in stream order.
+struct CallSeq {
+  unsigned long long stamp, gen, prev_target;
+};
+__device__ __forceinline__ CallSeq resolve_seq(const LookupView& v, uint64_t stamp) {
+  CallSeq q{stamp, v.gen, v.prev_target};
+  if (v.rebase != nullptr) {
+    q.stamp += __ldg(v.rebase);
+    q.gen += __ldg(v.rebase + 1 + v.idx);
+    q.prev_target += __ldg(v.rebase + 1 + v.prev_idx);
+  }
+  return q;
+}
+// The pieces separately, where the multi-block kernels need them (each
+// re-derived at its point of use instead of held in registers across the
+// probe: the pipelined kernel runs at a 40-register cap).
+__device__ __forceinline__ unsigned long long call_stamp(const LookupView& v, uint64_t stamp) {
+  return v.rebase != nullptr ? stamp + __ldg(v.rebase) : stamp;
+}
+__device__ __forceinline__ unsigned long long call_gen(const LookupView& v) {
+  return v.rebase != nullptr ? v.gen + __ldg(v.rebase + 1 + v.idx) : v.gen;
+}
+__device__ __forceinline__ unsigned long long call_prev_target(const LookupView& v) {
+  return v.rebase != nullptr ? v.prev_target + __ldg(v.rebase + 1 + v.prev_idx) : v.prev_target;
+}
+
+// Home entry of `slot` in the call's hit table.
+__device__ __forceinline__ uint64_t hit_home(const LookupView& v, uint32_t slot) {
+  return (uint64_t(slot) * 0x9E3779B97F4A7C15ull) >> (64 - v.log2cap);
+}
+// Inserts `slot` into the call's distinct-hit table, starting at entry h whose
+// current value `cur` the caller has already loaded (issued early, so the
+// round trip overlaps other work). Entries tagged with another stamp are free.
+// Returns 1 when this call inserted the slot (one unique hit), else 0.
+__device__ __forceinline__ uint32_t hit_insert(const LookupView& v, uint32_t slot, uint32_t tag,
+                                               uint64_t h, unsigned long long cur) {
+  const unsigned long long mine = (uint64_t(tag) << 32) | slot;
+  const uint64_t mask = v.cap - 1;
+  for (uint64_t probes = 0; probes <= mask;) {
+    if (uint32_t(cur >> 32) == tag) {
+      if (uint32_t(cur) == slot) return 0u;
+      h = (h + 1) & mask;
+      ++probes;
+      cur = __ldcg(v.hits + h);
+      continue;
+    }
+    const unsigned long long old = atomicCAS(v.hits + h, cur, mine);
+    if (old == cur) return 1u;
+    cur = old;
+  }
+  return 0u;
+}
+
 // Recency exchange of a hit slot: the call's stamp becomes the slot's
-// counter (max: calls may overlap, a later call's stamp wins), and the
-// exchange on the call's mark array tells whether this is the call's first
+// counter (max: calls may overlap, a later call's stamp wins), and inserting
+// the slot into the call's hit table tells whether this is the call's first
 // hit of the slot (one unique hit). Both are read first and only written
 // when not already done: a power-law batch's hot slot is hit by every block
 // of the call, and same-line read-modify-writes serialise in its L2 slice
@@ -333,11 +404,11 @@ __device__ __forceinline__ uint32_t warp_claim_misses(const LookupView& v,
 __device__ __forceinline__ uint32_t stamp_slot(const CacheDev& c, const LookupView& v,
                                                uint32_t slot, unsigned long long stamp) {
   unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c.counters) + slot;
-  const uint32_t s32 = uint32_t(stamp);  // never 0 (DeviceCache::bump_clock)
   const unsigned long long cur_ctr = __ldcg(ctr);
-  const uint32_t cur_mark = __ldcg(v.marks + slot);
+  const uint64_t h = hit_home(v, slot);
+  const unsigned long long cur = __ldcg(v.hits + h);
   if (cur_ctr < stamp) atomicMax(ctr, stamp);
-  return (cur_mark != s32 && atomicExch(v.marks + slot, s32) != s32) ? 1u : 0u;
+  return hit_insert(v, slot, uint32_t(stamp), h, cur);  // low 32 bits never 0
 }
 
 // Inserts `slot` into a block-shared open-addressing set; false when the
@@ -398,7 +469,9 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int RC = 32 / L;   // float4 chunks per lane per 128-float row segment
   __shared__ uint32_t s_stamped[1u << kSetBits];
   for (uint32_t i = threadIdx.x; i < (1u << kSetBits); i += kThreads) s_stamped[i] = kNoSlot;
-  if (threadIdx.x == 0) spin_ge_relaxed(v.completed, v.gen);
+  const CallSeq seq = resolve_seq(v, stamp);
+  stamp = seq.stamp;
+  if (threadIdx.x == 0) spin_ge_relaxed(v.completed, seq.gen);
   __syncthreads();
   const uint32_t lane = lane_id();
   const uint32_t q = lane / L, sub = lane % L;
@@ -512,7 +585,7 @@ __global__ void __launch_bounds__(kThreads)
   if (last_block(v, 0, gridDim.x)) finish_claims(v);
   if (valid) copy_row();
   warp_add_counts(v, uh, claimed ? 1u : 0u, blockIdx.x * kWarps + (threadIdx.x >> 5));
-  if (last_block(v, 1, gridDim.x)) finish_counts(v);
+  if (last_block(v, 1, gridDim.x)) finish_counts(v, seq.gen, seq.prev_target);
 }
 
 // ====================================================== lane-per-position --
@@ -586,7 +659,7 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   __shared__ uint32_t s_stamped[kSetSize];
   for (uint32_t i = threadIdx.x; i < kSetSize; i += kThreadsB) s_stamped[i] = kNoSlot;
   // the view's previous use must have completed (normally long ago)
-  if (threadIdx.x == 0) spin_ge_relaxed(v.completed, v.gen);
+  if (threadIdx.x == 0) spin_ge_relaxed(v.completed, call_gen(v));
   __syncthreads();
   trace_min(v, 0, false);
   trace_min(v, 2, true);
@@ -611,15 +684,17 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   // throughput when calls overlap)
   uint32_t uh = 0, um = 0;
   if constexpr (SF) {
+    stamp = call_stamp(v, stamp);
     const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
     bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
     if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c.counters) + res;
-    unsigned long long cur_ctr = ~0ull;
-    uint32_t cur_mark = uint32_t(stamp);
+    unsigned long long cur_ctr = ~0ull, cur_hit = 0ull;
+    uint64_t hh = 0;
     if (stamp_it) {
       cur_ctr = __ldcg(ctr);
-      cur_mark = __ldcg(v.marks + res);
+      hh = hit_home(v, res);
+      cur_hit = __ldcg(v.hits + hh);
     }
     um = warp_claim_misses(v, keys, pos, key, miss);
     if (valid) {
@@ -627,10 +702,7 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
       if (v.flags_dev != nullptr) v.flags_dev[pos] = res == kNoSlot ? 1 : 0;
     }
     if (cur_ctr < stamp) atomicMax(ctr, stamp);
-    uh = (cur_mark != uint32_t(stamp) &&
-          atomicExch(v.marks + res, uint32_t(stamp)) != uint32_t(stamp))
-             ? 1u
-             : 0u;
+    uh = stamp_it ? hit_insert(v, res, uint32_t(stamp), hh, cur_hit) : 0u;
   } else {
     um = warp_claim_misses(v, keys, pos, key, miss);
     if (valid) {
@@ -660,6 +732,7 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
   }
   // ---- C: recency exchange, row copy, counts ----
   if constexpr (!SF) {
+    stamp = call_stamp(v, stamp);
     const uint32_t same_slot = __match_any_sync(0xFFFFFFFFu, res);
     bool stamp_it = res != kNoSlot && (__ffs(same_slot) - 1) == lane && !(skip & kSkipStamp);
     if (stamp_it) stamp_it = block_set_insert(s_stamped, kSetSize, res);
@@ -687,7 +760,7 @@ __device__ __forceinline__ void lookup_body(const CacheDev& c, const uint64_t* _
     finish_claims(v);
     trace_min(v, 7, false);
   }
-  if (last_block(v, 1, nblocks)) finish_counts(v);
+  if (last_block(v, 1, nblocks)) finish_counts(v, call_gen(v), call_prev_target(v));
 }
 
 template <int CH, int WARPS, bool SF>
@@ -767,6 +840,7 @@ __global__ void __launch_bounds__(kSmallLookup)
     s_nclaims = 0u;
     s_uh = 0u;
   }
+  stamp = call_stamp(v, stamp);
   const bool valid = t < n;
   const uint64_t key = valid ? keys[t] : 0ull;
   s_key[t] = key;
@@ -838,8 +912,25 @@ __global__ void __launch_bounds__(kSmallLookup)
     v.counts_out[1] = s_nclaims;
     // the view is free for its next use (the large kernel's completion rule)
     __threadfence();
-    st_release(v.completed, v.gen + 1);
+    st_release(v.completed, call_gen(v) + 1);
   }
+}
+
+// --------------------------------------------------------------- rebase --
+struct RebaseWords {
+  unsigned long long w[1 + kLookupViews];
+};
+__global__ void k_rebase(unsigned long long* __restrict__ out, RebaseWords r) {
+  if (threadIdx.x <= kLookupViews) out[threadIdx.x] = r.w[threadIdx.x];
+}
+
+void launch_rebase(unsigned long long* w, unsigned long long stamp_base,
+                   const unsigned long long (&use_base)[kLookupViews], cudaStream_t st) {
+  RebaseWords r;
+  r.w[0] = stamp_base;
+  for (int k = 0; k < kLookupViews; ++k) r.w[1 + k] = use_base[k];
+  k_rebase<<<1, 32, 0, st>>>(w, r);
+  check_launch("rebase", 1);
 }
 
 // --------------------------------------------------------------- launch --

@@ -525,3 +525,112 @@ def test_zero_copy_small_calls_pinned_and_pageable_match_oracle(threshold):
     assert eng.stats().__dict__ == eo.stats
     c.check_invariants()
     eng.close()
+
+
+def test_group_multi_lookup_with_empty_tables_over_many_calls():
+    """An empty per-table batch takes no lookup view (no block would ever
+    release it): more than kLookupViews (8) group calls with table 0 empty
+    every time, and some calls with every table empty, must keep matching
+    the per-table twin (a leaked view would hang its next use on the device)."""
+    dims = (8, 16)
+    T_ = len(dims)
+
+    def build(grouped):
+        vdb = hps.VolatileStore(2)
+        caches, engines = [], []
+        for t, d in enumerate(dims):
+            table = T(f"e{t}", d)
+            vdb.register_table(table)
+            keys = np.arange(t * 100000, t * 100000 + 5000, dtype=np.uint64)
+            vdb.insert(table.name, keys, row_values(keys, d, t))
+            cfg = hps.SlabCacheConfig(slabset_count=16, slabs_per_set=2, dimension=d)
+            c = hps.SlabCache(cfg, share_stream_with=caches[0] if (grouped and caches) else None)
+            caches.append(c)
+            engines.append(hps.LookupEngine(table, c, vdb, None,
+                                            hps.EngineConfig(hit_rate_threshold=0.6)))
+        return vdb, caches, engines
+
+    va, ca, ea = build(True)
+    vb, cb, eb = build(False)
+    m = hps.MultiLookup(ea, max_batch=2048)
+    for r in range(20):
+        ns = [0, 0 if r % 5 == 4 else 200 + 37 * r]
+        batches = [hps.powerlaw_sample(1.1, 6000, t, 90 * r + t, ns[t]) + np.uint64(t * 100000)
+                   for t in range(T_)]
+        got = m.lookup(batches)
+        for t in range(T_):
+            want = eb[t].lookup(batches[t])
+            assert got[t].vectors.tobytes() == want.vectors.tobytes(), (r, t)
+            assert (got[t].miss_flags == want.miss_flags).all(), (r, t)
+        for e in ea + eb:
+            e.drain_async()
+    for t in range(T_):
+        assert ca[t].recency_clock() == cb[t].recency_clock()
+        assert ca[t].dump_all().tolist() == cb[t].dump_all().tolist()
+        assert ea[t].stats() == eb[t].stats()
+    m.close()
+    for e in ea + eb:
+        e.close()
+
+
+def test_engine_lookup_multi_device_mode_orders_against_default_stream():
+    """hps_engine_lookup_multi with HPS_MEM_DEVICE orders against the legacy
+    default stream (like hps_engine_lookup with a NULL stream): keys written
+    by a default-stream kernel right before the call are the ones looked up,
+    and default-stream reads right after it see the final rows and flags --
+    including the sync branch's scatter."""
+    import torch
+
+    d, T_, n = 32, 3, 20000
+
+    def build():
+        vdb = hps.VolatileStore(4)
+        engines = []
+        for t in range(T_):
+            table = T(f"dm{t}", d)
+            vdb.register_table(table)
+            keys = np.arange(t * 100000, t * 100000 + 50000, dtype=np.uint64)
+            vdb.insert(table.name, keys, row_values(keys, d, t))
+            c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=128, slabs_per_set=2, dimension=d))
+            engines.append((c, hps.LookupEngine(table, c, vdb, None,
+                                                hps.EngineConfig(hit_rate_threshold=0.9))))
+        return vdb, engines
+
+    va, ea = build()
+    vb, eb = build()
+    for r in range(4):
+        batches = [hps.powerlaw_sample(1.05, 60000, t, 11 * r + t, n) + np.uint64(t * 100000)
+                   for t in range(T_)]
+        # keys land on the device through a default-stream kernel (x + 0)
+        src = [torch.from_numpy(b.view(np.int64)).cuda() for b in batches]
+        torch.cuda.synchronize()
+        torch.cuda.set_stream(torch.cuda.default_stream())
+        big = torch.empty(1 << 26, device="cuda")
+        big.uniform_()  # queue default-stream work ahead of the key writes
+        dk = [s + 0 for s in src]
+        out = [torch.full((n * d,), -7.0, device="cuda") for _ in range(T_)]
+        fl = [torch.full((n,), 9, dtype=torch.uint8, device="cuda") for _ in range(T_)]
+        hps.LookupEngine.lookup_multi_ptrs([e for _, e in ea], [k.data_ptr() for k in dk], [n] * T_,
+                                           [o.data_ptr() for o in out], [f.data_ptr() for f in fl],
+                                           hps.HPS_MEM_DEVICE)
+        got = [(o.cpu().numpy(), f.cpu().numpy()) for o, f in zip(out, fl)]  # default stream
+        for t in range(T_):
+            want = eb[t][1].lookup(batches[t])
+            assert got[t][0].tobytes() == want.vectors.tobytes(), (r, t)
+            assert (got[t][1] == want.miss_flags).all(), (r, t)
+        for (_, e) in ea + eb:
+            e.drain_async()
+    for (_, e) in ea + eb:
+        e.close()
+
+
+def test_max_batch_is_enforced():
+    fx = Fixture(200)
+    e = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig(max_batch=64))
+    e.lookup(np.arange(64, dtype=np.uint64) % 200)
+    with pytest.raises(hps.InvalidArgument):
+        e.lookup(np.arange(65, dtype=np.uint64) % 200)
+    e.close()
+    unlimited = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig())
+    assert unlimited.lookup(np.arange(5000, dtype=np.uint64) % 200).vectors.size == 5000 * 2
+    unlimited.close()
