@@ -171,6 +171,13 @@ int hps_event_record(void* event, void* stream);
 int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n,
                       const float* vectors, size_t vectors_len, int mem, void* stream);
 
+/* Stream-ordered SlabCache::replace on device pointers for keys the caller
+ * guarantees DISTINCT (the engine's miss fill: unique misses): no duplicate
+ * check and no host synchronisation; same placement, recency and eviction
+ * as hps_cache_replace. */
+int hps_cache_replace_device_async(hps_cache* cache, const uint64_t* keys, size_t n,
+                                   const float* vectors, size_t vectors_len, void* stream);
+
 /* replaces SlabCache::update (slab_cache.cpp:109-125). *written = number of
  * positions whose key was resident (duplicates count every time; the last
  * occurrence's row wins). */

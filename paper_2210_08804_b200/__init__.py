@@ -143,6 +143,7 @@ SIGNATURES = {
     "hps_graph_destroy": (C.c_int, [_P]),
     "hps_event_record": (C.c_int, [_P, _P]),
     "hps_cache_replace": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, C.c_int, _P]),
+    "hps_cache_replace_device_async": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P]),
     "hps_cache_update": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _SZP, C.c_int, _P]),
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
     "hps_cache_check_invariants": (C.c_int, [_P]),
@@ -419,6 +420,12 @@ class SlabCache:
     def replace_device(self, keys_ptr: int, n: int, rows_ptr: int, stream: int = 0) -> None:
         _check(lib().hps_cache_replace(self._h, keys_ptr, n, rows_ptr, n * self._dim,
                                        HPS_MEM_DEVICE, stream or None))
+
+    def replace_fill(self, keys_ptr: int, n: int, rows_ptr: int, stream: int = 0) -> None:
+        """Stream-ordered replace of DISTINCT device keys (the engine's miss
+        fill; hps_cache_replace_device_async): no duplicate check, no sync."""
+        _check(lib().hps_cache_replace_device_async(self._h, keys_ptr, n, rows_ptr, n * self._dim,
+                                                    stream or None))
 
     def update(self, keys, vectors) -> int:
         k = _u64(keys)

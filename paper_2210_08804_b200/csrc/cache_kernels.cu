@@ -136,82 +136,108 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
 // ---------------------------------------------------------------- replace --
 // Deterministic parity with the reference's grouped application
 // (slab_cache.cpp:131-142: keys grouped by slabset, input order inside a
-// group): (A) hash keys into a table of touched slabsets and count,
-// (B) give each touched set a bucket range, (C) scatter key indices into
-// the buckets, (D) one warp per touched set sorts its (few) indices and
-// applies them serially with ballot probes, lowest-free-slot insertion and
-// a warp argmin over the set's W*32 counters for eviction.
+// group) in two launches and no memsets (batches above kSmallReplaceMax):
+//   k_replace_bin    one thread per key: slabset, the set's entry in a
+//                    per-call table (CAS on the set id), the key's index
+//                    appended there (atomicAdd rank; the rank-0 key leads)
+//   [k_replace_dups] (validated calls) each leader compares its set's keys:
+//                    any duplicate rejects the whole call before mutation
+//   k_replace_sets   one warp per LEADER: the set's key indices sorted into
+//                    input order, the set's masks, keys and counters loaded
+//                    ONCE into registers (lane j holds slot j of every slab)
+//                    with the first rows prefetched, then every key of the set
+//                    applied serially against that register state -- probe by
+//                    ballot, lowest free slot of the first non-full probed
+//                    slab, else the argmin counter (ties to the lowest
+//                    (slab, slot)); only the changed words are stored; the
+//                    set's table entry is cleared (the table is clean again)
 size_t replace_scratch_bytes(uint64_t n) {
   const uint64_t cap = pow2_at_least(2 * n);
-  return align_up(cap * 8, 256) + 3 * align_up(cap * 4, 256) + 2 * align_up(n * 4, 256) + 256;
+  return align_up(cap * 4, 256) * 4 + align_up(cap * 4 * kReplaceInline, 256) +
+         align_up(n * 4, 256) * 3 + 256;
 }
 
 ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
   ReplaceScratch r;
   r.cap = pow2_at_least(2 * n);
+  r.ncap = n;
   char* p = static_cast<char*>(base);
-  r.tab_set = reinterpret_cast<uint64_t*>(p);
-  p += align_up(r.cap * 8, 256);
-  r.tab_cnt = reinterpret_cast<uint32_t*>(p);
-  p += align_up(r.cap * 4, 256);
-  r.tab_fill = reinterpret_cast<uint32_t*>(p);
-  p += align_up(r.cap * 4, 256);
-  r.tab_off = reinterpret_cast<uint32_t*>(p);
-  p += align_up(r.cap * 4, 256);
-  r.key_tab = reinterpret_cast<uint32_t*>(p);
-  p += align_up(n * 4, 256);
-  r.bucket = reinterpret_cast<uint32_t*>(p);
-  p += align_up(n * 4, 256);
-  r.cursor = reinterpret_cast<uint32_t*>(p);
+  auto take = [&](uint64_t bytes) {
+    uint32_t* q = reinterpret_cast<uint32_t*>(p);
+    p += align_up(bytes, 256);
+    return q;
+  };
+  // zero-initialised part first, then the all-ones part (two memsets once)
+  r.set1 = take(r.cap * 4);
+  r.cnt = take(r.cap * 4);
+  r.cursor = take(256);
   r.dup_flag = r.cursor + 1;
+  r.ovf = take(r.cap * 4);
+  r.boff = take(r.cap * 4);
+  r.idx = take(r.cap * 4 * kReplaceInline);
+  r.next = take(n * 4);
+  r.entry = take(n * 4);
+  r.bucket = take(n * 4);
   return r;
 }
 
-__global__ void k_replace_group(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
-                                ReplaceScratch rs) {
+void replace_scratch_init(const ReplaceScratch& rs, cudaStream_t st) {
+  const char* z0 = reinterpret_cast<const char*>(rs.set1);
+  const char* o0 = reinterpret_cast<const char*>(rs.ovf);
+  const char* o1 = reinterpret_cast<const char*>(rs.idx);
+  cudaMemsetAsync(rs.set1, 0, size_t(o0 - z0), st);
+  cudaMemsetAsync(rs.ovf, 0xFF, size_t(o1 - o0), st);
+}
+
+constexpr uint32_t kLeaderBit = 0x80000000u;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+__global__ void __launch_bounds__(256)
+    k_replace_bin(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t s = slabset_of(c, keys[i]);
-  uint64_t t = fmix64(s) & (rs.cap - 1);
-  while (true) {
-    const unsigned long long old =
-        atomicCAS(reinterpret_cast<unsigned long long*>(rs.tab_set + t), ~0ull, s);
-    if (old == ~0ull || old == s) break;
-    t = (t + 1) & (rs.cap - 1);
+  if (i == 0) {
+    rs.cursor[0] = 0u;
+    rs.dup_flag[0] = 0u;
   }
-  rs.key_tab[i] = uint32_t(t);
-  atomicAdd(rs.tab_cnt + t, 1u);
-}
-
-__global__ void k_replace_offsets(ReplaceScratch rs) {
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rs.cap) return;
-  const uint32_t cnt = rs.tab_cnt[t];
-  if (cnt) rs.tab_off[t] = atomicAdd(rs.cursor, cnt);
-}
-
-__global__ void k_replace_bucket(uint64_t n, ReplaceScratch rs) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint32_t t = rs.key_tab[i];
-  const uint32_t pos = atomicAdd(rs.tab_fill + t, 1u);
-  rs.bucket[rs.tab_off[t] + pos] = uint32_t(i);
+  const uint32_t s1 = uint32_t(slabset_of(c, keys[i])) + 1u;
+  const uint64_t mask = rs.cap - 1;
+  uint64_t e = fmix64(s1) & mask;
+  while (true) {
+    const uint32_t old = atomicCAS(rs.set1 + e, 0u, s1);
+    if (old == 0u || old == s1) break;
+    e = (e + 1) & mask;
+  }
+  const uint32_t r = atomicAdd(rs.cnt + e, 1u);
+  if (r < kReplaceInline) {
+    rs.idx[e * kReplaceInline + r] = uint32_t(i);
+  } else {
+    rs.next[i] = atomicExch(rs.ovf + e, uint32_t(i));
+  }
+  rs.entry[i] = uint32_t(e) | (r == 0 ? kLeaderBit : 0u);
 }
 
-// Sorts bucket[off, off+cnt) ascending. cnt <= 32: rank sort in registers;
-// larger groups (tiny caches) fall back to a lane-0 insertion sort.
-__device__ __forceinline__ void warp_sort_group(uint32_t* b, uint32_t cnt) {
-  const uint32_t lane = lane_id();
-  if (cnt <= 32) {
-    const uint32_t v = lane < cnt ? b[lane] : 0xFFFFFFFFu;
-    uint32_t rank = 0;
-    for (uint32_t j = 0; j < cnt; ++j) {
-      const uint32_t o = __shfl_sync(0xFFFFFFFFu, v, j);
-      rank += (o < v) ? 1u : 0u;
+// Sets of more than 32 keys (tiny caches): the indices in a sorted bucket
+// range, built once per call by whichever kernel needs it first.
+__device__ __forceinline__ const uint32_t* big_bucket(const ReplaceScratch& rs, uint64_t e,
+                                                      uint32_t cnt) {
+  uint32_t off = 0;
+  if (lane_id() == 0) {
+    off = rs.boff[e];
+    if (off == kNone) {
+      off = atomicAdd(rs.cursor, cnt);
+      uint32_t* b = rs.bucket + off;
+      uint32_t j = 0;
+      for (; j < kReplaceInline; ++j) b[j] = rs.idx[e * kReplaceInline + j];
+      for (uint32_t x = rs.ovf[e]; x != kNone; x = rs.next[x]) b[j++] = x;
+      rs.boff[e] = off;
     }
-    __syncwarp();
-    if (lane < cnt) b[rank] = v;
-  } else if (lane == 0) {
+  }
+  off = __shfl_sync(0xFFFFFFFFu, off, 0);
+  __syncwarp();
+  uint32_t* b = rs.bucket + off;
+  // rank sort / insertion sort (already sorted on the second call: linear)
+  if (lane_id() == 0) {
     for (uint32_t a = 1; a < cnt; ++a) {
       const uint32_t x = b[a];
       uint32_t j = a;
@@ -223,21 +249,264 @@ __device__ __forceinline__ void warp_sort_group(uint32_t* b, uint32_t cnt) {
     }
   }
   __syncwarp();
+  return b;
 }
 
-__global__ void k_replace_validate(const uint64_t* __restrict__ keys, ReplaceScratch rs) {
-  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (t >= rs.cap) return;
-  const uint32_t cnt = rs.tab_cnt[t];
+// Indices of a set with at most 32 keys into lanes, sorted: lane j holds the
+// j-th smallest (kNone past cnt). `sw` = 32 words of per-warp shared memory.
+__device__ __forceinline__ uint32_t small_group(const ReplaceScratch& rs, uint64_t e, uint32_t cnt,
+                                                uint32_t* sw) {
+  const uint32_t lane = lane_id();
+  uint32_t v = kNone;
+  if (lane < kReplaceInline && lane < cnt) v = rs.idx[e * kReplaceInline + lane];
+  if (cnt > kReplaceInline) {
+    if (lane == 0) {
+      uint32_t j = kReplaceInline;
+      for (uint32_t x = rs.ovf[e]; x != kNone && j < 32; x = rs.next[x]) sw[j++] = x;
+    }
+    __syncwarp();
+    if (lane >= kReplaceInline && lane < cnt) v = sw[lane];
+    __syncwarp();
+  }
+  uint32_t rank = 0;
+  for (uint32_t j = 0; j < cnt; ++j) {
+    const uint32_t o = __shfl_sync(0xFFFFFFFFu, v, j);
+    rank += (o < v) ? 1u : 0u;
+  }
+  if (lane < cnt) sw[rank] = v;
+  __syncwarp();
+  v = lane < cnt ? sw[lane] : kNone;
+  __syncwarp();
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+    k_replace_dups(const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
+  __shared__ uint32_t s_w[8][32];
+  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const uint32_t ent = rs.entry[i];
+  if (!(ent & kLeaderBit)) return;
+  const uint64_t e = ent & ~kLeaderBit;
+  const uint32_t cnt = rs.cnt[e];
   if (cnt < 2) return;
-  const uint32_t* b = rs.bucket + rs.tab_off[t];
   const uint32_t lane = lane_id();
   bool dup = false;
-  for (uint32_t x = lane; x < cnt; x += 32) {
-    const uint64_t kx = keys[b[x]];
-    for (uint32_t y = x + 1; y < cnt; ++y) dup |= (keys[b[y]] == kx);
+  if (cnt <= 32) {
+    const uint32_t v = small_group(rs, e, cnt, s_w[threadIdx.x >> 5]);
+    const uint64_t k = v != kNone ? keys[v] : 0ull;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint64_t o = __shfl_sync(0xFFFFFFFFu, k, j);
+      dup |= (lane < cnt && j != lane && o == k);
+    }
+  } else {
+    const uint32_t* b = big_bucket(rs, e, cnt);
+    for (uint32_t x = lane; x < cnt; x += 32) {
+      const uint64_t kx = keys[b[x]];
+      for (uint32_t y = x + 1; y < cnt; ++y) dup |= (keys[b[y]] == kx);
+    }
   }
   if (__any_sync(0xFFFFFFFFu, dup) && lane == 0) atomicOr(rs.dup_flag, 1u);
+}
+
+// The set's state in registers: lane j holds slot j of each of its W slabs.
+template <int W>
+struct SetRegs {
+  uint64_t k[W];
+  uint64_t ct[W];
+  uint32_t m[W];
+};
+
+template <int W>
+__device__ __forceinline__ void replace_apply_set(const CacheDev& c, uint64_t set,
+                                                  const uint64_t* __restrict__ keys,
+                                                  const float* __restrict__ rows, uint64_t stamp,
+                                                  uint32_t cnt, uint32_t my_idx,
+                                                  const uint32_t* __restrict__ big) {
+  constexpr int kPre = 4;  // rows prefetched (d <= 128, 16 B aligned)
+  const uint32_t lane = lane_id();
+  const uint32_t d = c.d;
+  const uint64_t sbase = set * W;
+  SetRegs<W> st;
+  uint32_t m0[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    st.m[w] = c.masks[sbase + w];
+    m0[w] = st.m[w];
+    st.k[w] = c.keys[(sbase + w) * kSlotsPerSlab + lane];
+    st.ct[w] = c.counters[(sbase + w) * kSlotsPerSlab + lane];
+  }
+  // lane j < cnt: key and first-slab hash of the j-th key (small groups)
+  uint64_t my_key = 0, my_h2 = 0;
+  if (big == nullptr && my_idx != kNone) {
+    my_key = keys[my_idx];
+    my_h2 = xxh64_key(my_key, kSlabSeed);
+  }
+  const bool vec = (d & 3u) == 0 && d <= 128 && (reinterpret_cast<uintptr_t>(rows) & 15u) == 0;
+  float4 pre[kPre];
+  if (vec && big == nullptr) {
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) {
+      const uint32_t ij = __shfl_sync(0xFFFFFFFFu, my_idx, j);
+      pre[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (uint32_t(j) < cnt && lane < (d >> 2))
+        pre[j] = reinterpret_cast<const float4*>(rows + uint64_t(ij) * d)[lane];
+    }
+  }
+  uint32_t inserted = 0;
+  for (uint32_t j = 0; j < cnt; ++j) {
+    uint32_t ij;
+    uint64_t key, h2;
+    if (big == nullptr) {
+      ij = __shfl_sync(0xFFFFFFFFu, my_idx, j);
+      key = __shfl_sync(0xFFFFFFFFu, my_key, j);
+      h2 = __shfl_sync(0xFFFFFFFFu, my_h2, j);
+    } else {
+      ij = big[j];
+      key = keys[ij];
+      h2 = xxh64_key(key, kSlabSeed);
+    }
+    const uint32_t first = W == 1 ? 0u : (W == 2 ? uint32_t(h2 & 1u) : uint32_t(fastmod(h2, W, c.mW)));
+    // probe in slab order from `first` (slab_cache.cpp:292-310)
+    int hit_w = -1, ins_w = -1;
+    uint32_t hit_j = 0;
+#pragma unroll
+    for (int step = 0; step < W; ++step) {
+      int w = int(first) + step;
+      if (w >= W) w -= W;
+      if (hit_w >= 0 || ins_w >= 0) continue;
+      uint64_t kw = 0;
+      uint32_t mw = 0;
+#pragma unroll
+      for (int x = 0; x < W; ++x)
+        if (x == w) {
+          kw = st.k[x];
+          mw = st.m[x];
+        }
+      const uint32_t hb = __ballot_sync(0xFFFFFFFFu, ((mw >> lane) & 1u) && kw == key);
+      if (hb) {
+        hit_w = w;
+        hit_j = __ffs(hb) - 1;
+      } else if (mw != kFullSlab) {
+        ins_w = w;
+      }
+    }
+    if (hit_w >= 0) {
+      // resident: recency refresh only, the vector is kept (:283-288)
+      if (lane == hit_j) {
+#pragma unroll
+        for (int x = 0; x < W; ++x)
+          if (x == hit_w) st.ct[x] = stamp;
+        c.counters[(sbase + hit_w) * kSlotsPerSlab + lane] = stamp;
+      }
+      continue;
+    }
+    int tw;
+    uint32_t tj;
+    if (ins_w >= 0) {
+      uint32_t mw = 0;
+#pragma unroll
+      for (int x = 0; x < W; ++x)
+        if (x == ins_w) mw = st.m[x];
+      tj = __ffs(~mw) - 1;  // countr_one(mask) (:299)
+#pragma unroll
+      for (int x = 0; x < W; ++x)
+        if (x == ins_w) st.m[x] = mw | (1u << tj);
+      tw = ins_w;
+      ++inserted;
+    } else {
+      // every probed slab full: evict the minimum counter of the set, ties
+      // to the lowest (slab, slot) in slab-major order (:312-324)
+      uint64_t bc = st.ct[0];
+      uint32_t bi = lane;
+#pragma unroll
+      for (int x = 1; x < W; ++x)
+        if (st.ct[x] < bc) {
+          bc = st.ct[x];
+          bi = uint32_t(x) * 32 + lane;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, bc, o);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+        if (oc < bc || (oc == bc && oi < bi)) {
+          bc = oc;
+          bi = oi;
+        }
+      }
+      tw = int(bi >> 5);
+      tj = bi & 31u;
+    }
+    const uint64_t slot = (sbase + tw) * kSlotsPerSlab + tj;
+    if (lane == tj) {
+#pragma unroll
+      for (int x = 0; x < W; ++x)
+        if (x == tw) {
+          st.k[x] = key;
+          st.ct[x] = stamp;
+        }
+      c.keys[slot] = key;
+      c.counters[slot] = stamp;
+      c.tags[slot] = key_tag(h2);
+    }
+    const float* src = rows + uint64_t(ij) * d;
+    float* dst = c.rows + slot * d;
+    if (vec && big == nullptr && j < uint32_t(kPre)) {
+      float4 x = pre[0];
+#pragma unroll
+      for (int q = 1; q < kPre; ++q)
+        if (uint32_t(q) == j) x = pre[q];
+      if (lane < (d >> 2)) reinterpret_cast<float4*>(dst)[lane] = x;
+    } else {
+      warp_copy_row(src, dst, d);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      if (st.m[w] != m0[w]) c.masks[sbase + w] = st.m[w];
+    if (inserted) atomicAdd(c.occupied, (unsigned long long)inserted);
+  }
+}
+
+__device__ __forceinline__ void warp_replace_key(const CacheDev& c, uint64_t set, uint64_t key,
+                                                 const float* __restrict__ row, uint64_t stamp);
+
+// W = 0: any slab count, the set re-read for every key (warp_replace_key)
+template <int W>
+__global__ void __launch_bounds__(256)
+    k_replace_sets(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                   const float* __restrict__ rows, uint64_t stamp, uint32_t validate,
+                   ReplaceScratch rs) {
+  __shared__ uint32_t s_w[8][32];
+  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const uint32_t ent = rs.entry[i];
+  if (!(ent & kLeaderBit)) return;
+  const uint64_t e = ent & ~kLeaderBit;
+  const uint32_t cnt = rs.cnt[e];
+  const uint64_t set = rs.set1[e] - 1u;
+  const bool rejected = validate && *reinterpret_cast<volatile uint32_t*>(rs.dup_flag) != 0u;
+  if (!rejected) {
+    const uint32_t v = cnt <= 32 ? small_group(rs, e, cnt, s_w[threadIdx.x >> 5]) : kNone;
+    const uint32_t* b = cnt <= 32 ? nullptr : big_bucket(rs, e, cnt);
+    if constexpr (W == 0) {
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint32_t ij = b ? b[j] : __shfl_sync(0xFFFFFFFFu, v, j);
+        warp_replace_key(c, set, keys[ij], rows + uint64_t(ij) * c.d, stamp);
+      }
+    } else {
+      replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, b);
+    }
+  }
+  __syncwarp();
+  if (lane_id() == 0) {
+    // the table is clean again for the next call
+    rs.set1[e] = 0u;
+    rs.cnt[e] = 0u;
+    rs.ovf[e] = kNone;
+    rs.boff[e] = kNone;
+  }
 }
 
 // One key of a set, applied by a whole warp (slab_cache.cpp:261-326): ballot
@@ -383,23 +652,6 @@ __device__ __forceinline__ void warp_replace_key(const CacheDev& c, uint64_t set
   __syncwarp();
 }
 
-__global__ void k_replace_apply(CacheDev c, const uint64_t* __restrict__ keys,
-                                const float* __restrict__ rows, uint64_t stamp,
-                                ReplaceScratch rs) {
-  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (t >= rs.cap) return;
-  const uint32_t cnt = rs.tab_cnt[t];
-  if (cnt == 0) return;
-  if (*reinterpret_cast<volatile uint32_t*>(rs.dup_flag)) return;  // rejected before mutation
-  uint32_t* b = rs.bucket + rs.tab_off[t];
-  warp_sort_group(b, cnt);
-  const uint64_t set = rs.tab_set[t];
-  for (uint32_t g = 0; g < cnt; ++g) {
-    const uint32_t i = b[g];
-    warp_replace_key(c, set, keys[i], rows + uint64_t(i) * c.d, stamp);
-  }
-}
-
 // Small batches (the engine's per-call unique misses at small batch sizes;
 // n <= kSmallReplaceMax) in ONE single-block launch without scratch
 // memsets -- 32 warps take the touched sets 32 at a time, so beyond a few
@@ -521,22 +773,18 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
     check_launch("replace", 1);
     return;
   }
-  cudaMemsetAsync(rs.tab_set, 0xFF, rs.cap * 8, st);
-  // tab_cnt, tab_fill are contiguous (carve order); cursor + dup_flag after buckets
-  cudaMemsetAsync(rs.tab_cnt, 0, rs.cap * 4, st);
-  cudaMemsetAsync(rs.tab_fill, 0, rs.cap * 4, st);
-  cudaMemsetAsync(rs.cursor, 0, 8, st);
   const unsigned tb = 256;
-  k_replace_group<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(c, keys, n, rs);
-  k_replace_offsets<<<unsigned((rs.cap + tb - 1) / tb), tb, 0, st>>>(rs);
-  k_replace_bucket<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(n, rs);
-  const uint64_t warp_threads = rs.cap * 32;
-  if (validate) {
-    k_replace_validate<<<unsigned((warp_threads + tb - 1) / tb), tb, 0, st>>>(keys, rs);
+  k_replace_bin<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(c, keys, n, rs);
+  const unsigned wgrid = unsigned((n * 32 + tb - 1) / tb);
+  if (validate) k_replace_dups<<<wgrid, tb, 0, st>>>(keys, n, rs);
+  switch (c.W) {
+    case 1: k_replace_sets<1><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 2: k_replace_sets<2><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 3: k_replace_sets<3><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 4: k_replace_sets<4><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    default: k_replace_sets<0><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
   }
-  k_replace_apply<<<unsigned((warp_threads + tb - 1) / tb), tb, 0, st>>>(c, keys, rows, stamp,
-                                                                          rs);
-  check_launch("replace", validate ? 5 : 4);
+  check_launch("replace", validate ? 3 : 2);
 }
 
 // ----------------------------------------------------------------- update --

@@ -432,6 +432,17 @@ int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n, const fl
   });
 }
 
+int hps_cache_replace_device_async(hps_cache* cache, const uint64_t* keys, size_t n,
+                                   const float* vectors, size_t vectors_len, void* stream) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    need(vectors_len == n * uint64_t(cache->impl->dimension()),
+         "replace vector buffer has wrong size");
+    need(n == 0 || (keys && vectors), "null argument");
+    cache->impl->replace_device_async(keys, n, vectors, as_stream(stream));
+  });
+}
+
 int hps_cache_update(hps_cache* cache, const uint64_t* keys, size_t n, const float* vectors,
                      size_t vectors_len, size_t* written, int mem, void* stream) {
   return guarded([&] {

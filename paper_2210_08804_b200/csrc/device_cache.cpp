@@ -496,10 +496,9 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
   DeviceGuard g(device_);
   const uint64_t d = cfg_.dimension;
   const uint64_t stamp = clock_.load(std::memory_order_relaxed);  // no increment
-  const uint64_t rs_bytes = replace_scratch_bytes(n);
-  const uint64_t bytes = align256(rs_bytes) + (host ? align256(n * 8) + align256(n * d * 4) : 0);
+  const ReplaceScratch& rs = replace_scratch_locked(n);
+  const uint64_t bytes = host ? align256(n * 8) + align256(n * d * 4) : 256;
   Carver cv{static_cast<char*>(scratch(bytes))};
-  ReplaceScratch rs = replace_scratch_carve(cv.take<char>(rs_bytes), n);
   const uint64_t* d_keys = keys;
   const float* d_rows = vectors;
   if (host && n <= kZeroCopyReplaceMax) {
@@ -541,12 +540,36 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
   join_to(user);
 }
 
+void DeviceCache::replace_device_async(const uint64_t* keys, size_t n, const float* rows,
+                                       cudaStream_t user) {
+  std::lock_guard<std::mutex> lk(mu_);
+  DeviceGuard g(device_);
+  join_from(user);
+  replace_device_locked(keys, n, rows);
+  join_to(user);
+}
+
+const ReplaceScratch& DeviceCache::replace_scratch_locked(uint64_t n) {
+  if (n >= (1ull << 31)) throw invalid_argument("replace batch too large");
+  if (n > rcap_) {
+    // persistent: the replace kernels leave it clean, so calls need no
+    // memsets; (re)initialised only when it grows
+    uint64_t cap = 1024;
+    while (cap < n) cap <<= 1;
+    void* b = rbuf_.ensure(replace_scratch_bytes(cap), stream_);
+    rs_ = replace_scratch_carve(b, cap);
+    replace_scratch_init(rs_, stream_);
+    rcap_ = cap;
+    mark_other_op();
+  }
+  return rs_;
+}
+
 void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const float* d_rows) {
   mark_other_op();
   if (n == 0) return;
   const uint64_t stamp = clock_.load(std::memory_order_relaxed);
-  const uint64_t rs_bytes = replace_scratch_bytes(n);
-  ReplaceScratch rs = replace_scratch_carve(scratch2_.ensure(rs_bytes, stream_), n);
+  const ReplaceScratch& rs = replace_scratch_locked(n);
   launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/false, rs, stream_);
 }
 

@@ -70,6 +70,9 @@ class DeviceCache {
   // slab_cache.cpp:109-125
   size_t update(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
                 int mem, cudaStream_t user);
+  // Stream-ordered replace of DISTINCT keys on device pointers (the engine's
+  // fill primitive): no duplicate check, no host synchronisation.
+  void replace_device_async(const uint64_t* keys, size_t n, const float* rows, cudaStream_t user);
   // Stream-ordered update on device pointers (online training path): no
   // host sync; *written (device u64, may be null) gets the count.
   void update_device(const uint64_t* keys, size_t n, const float* vectors, uint64_t* written,
@@ -171,7 +174,11 @@ class DeviceCache {
   std::atomic<uint64_t> clock_{0};
   ScanState scan_;
   DeviceBuffer scratch_;
-  DeviceBuffer scratch2_;
+  // replace: persistent per-call set table (kernels.hpp ReplaceScratch)
+  DeviceBuffer rbuf_;
+  ReplaceScratch rs_;
+  uint64_t rcap_ = 0;
+  const ReplaceScratch& replace_scratch_locked(uint64_t n);
   PinnedBuffer pinned_;
   // lookup_device scratch
   DeviceBuffer lbuf_;

@@ -38,20 +38,32 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
                           uint32_t* miss_pos, uint64_t* miss_keys,
                           unsigned long long* n_miss, ScanState& scan, cudaStream_t st);
 
+// Replace scratch (persistent: the kernels leave it in its initial state --
+// set1 / cnt zero, ovf / boff all-ones -- so calls need no memsets).
+// A per-call table of the touched slabsets (open addressing on the set id):
+// each key finds its set's entry and appends its index there (the first
+// kReplaceInline inline, the rest on an overflow list); the key that arrived
+// first leads the set.
+constexpr uint32_t kReplaceInline = 8;
 struct ReplaceScratch {
-  uint64_t cap = 0;          // power of two >= 2n
-  uint64_t* tab_set = nullptr;
-  uint32_t* tab_cnt = nullptr;
-  uint32_t* tab_off = nullptr;
-  uint32_t* tab_fill = nullptr;
-  uint32_t* key_tab = nullptr;  // n
-  uint32_t* bucket = nullptr;   // n
-  uint32_t* cursor = nullptr;
+  uint64_t cap = 0;      // set-table entries (power of two >= 2 * ncap)
+  uint64_t ncap = 0;     // keys per call
+  uint32_t* set1 = nullptr;   // cap: slabset + 1 (0 = free)
+  uint32_t* cnt = nullptr;    // cap: keys of the set in this call
+  uint32_t* idx = nullptr;    // cap * kReplaceInline: key indices, arrival order
+  uint32_t* ovf = nullptr;    // cap: overflow list head (~0 = none)
+  uint32_t* boff = nullptr;   // cap: sorted bucket of a set with > 32 keys (~0 = none)
+  uint32_t* next = nullptr;   // ncap: overflow list links
+  uint32_t* entry = nullptr;  // ncap: key -> entry | kLeaderBit
+  uint32_t* bucket = nullptr; // ncap: buckets of sets with > 32 keys
+  uint32_t* cursor = nullptr; // [0] bucket cursor, [1] duplicate flag
   uint32_t* dup_flag = nullptr;
 };
-// Needed bytes for n keys, and carving of a raw buffer.
+// Bytes of a scratch for calls of up to n keys; carving; the one-time
+// initialisation (enqueued on st).
 size_t replace_scratch_bytes(uint64_t n);
 ReplaceScratch replace_scratch_carve(void* base, uint64_t n);
+void replace_scratch_init(const ReplaceScratch& rs, cudaStream_t st);
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st);
 
