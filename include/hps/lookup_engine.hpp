@@ -4,17 +4,18 @@
 // libhps_b200.so (hps_engine_* in include/hps_b200.h).
 //
 // The dedup -> cache query -> hit-rate switch -> expansion runs on the GPU
-// (one kernel per lookup, lookup_kernels.cu); the misses are fetched from
-// the caller's own storage tiers -- the reference's VolatileStore and
-// PersistentStore, which a reference build keeps -- through the engine's
-// cold-tier callback, in the reference's tier order (tier_fetch below,
-// lookup_engine.cpp:50-89), and admitted with the GPU replace.
+// (one kernel per lookup, lookup_kernels.cu); the misses are fetched
+// in-process from the NATIVE volatile DB (include/hps/volatile_store.hpp,
+// the drop-in hps::VolatileStore) straight into the engine's pinned staging,
+// then from the reference's PersistentStore (kept; reached through the
+// engine's cold-tier callback) for the rest, in the reference's tier order
+// (lookup_engine.cpp:50-89), and admitted with the GPU replace.
 //
 // Use: this repo's include/ ahead of core/include, link libhps_b200.so and
-// the reference's tier sources (types.cpp, volatile_store.cpp,
-// persistent_store.cpp) instead of slab_cache.cpp / lookup_engine.cpp. The
-// reference's tests/unit/test_lookup_engine.cpp compiles unchanged against
-// it (oracle/Makefile target _ref/test_lookup_engine_b200).
+// the reference's types.cpp + persistent_store.cpp instead of
+// slab_cache.cpp / lookup_engine.cpp / volatile_store.cpp. The reference's
+// tests/unit/test_lookup_engine.cpp compiles unchanged against it
+// (oracle/Makefile target _ref/test_lookup_engine_b200).
 #pragma once
 
 #include <atomic>
@@ -48,37 +49,57 @@ struct TierCounters {
   std::uint64_t missing = 0;
 };
 
-// lookup_engine.cpp:50-89: volatile tier first, persistent for the rest,
-// persistent hits promoted to the volatile tier asynchronously; found rows
-// in (volatile-found, persistent-found) order.
+namespace b200_detail {
+// hps_cold_fetch_fn over the reference's PersistentStore::get
+// (persistent_store.cpp:405-439): the tier below the native volatile DB.
+struct PdbTier {
+  PersistentStore* pdb;
+  const std::string* table;
+};
+inline int pdb_fetch(void* ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
+                     float* found_vectors, size_t* n_found, uint64_t* missing_keys,
+                     size_t* n_missing) {
+  auto* t = static_cast<PdbTier*>(ctx);
+  try {
+    FetchResult f = t->pdb->get(*t->table, std::span<const EmbeddingKey>(keys, n));
+    std::copy(f.found_keys.begin(), f.found_keys.end(), found_keys);
+    std::copy(f.found_vectors.begin(), f.found_vectors.end(), found_vectors);
+    std::copy(f.missing_keys.begin(), f.missing_keys.end(), missing_keys);
+    *n_found = f.found_keys.size();
+    *n_missing = f.missing_keys.size();
+    return 0;
+  } catch (...) {
+    return 1;  // surfaces as TierFault (sync) or an async fault
+  }
+}
+}  // namespace b200_detail
+
+// lookup_engine.cpp:50-89 (tier order: volatile first, persistent for the
+// rest, persistent hits promoted to the volatile tier asynchronously; found
+// rows in (volatile-found, persistent-found) order) -- run by the native
+// hps_tier_fetch over the native volatile DB.
 inline FetchResult tier_fetch(const TableId& table, std::span<const EmbeddingKey> keys,
                               VolatileStore* vdb, PersistentStore& pdb,
                               TierCounters* counters = nullptr) {
   FetchResult out;
   if (keys.empty()) return out;
-  const bool use_vdb = vdb != nullptr && vdb->has_table(table.name);
-  std::vector<EmbeddingKey> remaining;
-  if (use_vdb) {
-    FetchResult v = vdb->lookup(table.name, keys);
-    if (counters) counters->vdb_hits += v.found_keys.size();
-    out.found_keys = std::move(v.found_keys);
-    out.found_vectors = std::move(v.found_vectors);
-    remaining = std::move(v.missing_keys);
-  } else {
-    remaining.assign(keys.begin(), keys.end());
-  }
-  if (!remaining.empty()) {
-    FetchResult p = pdb.get(table.name, remaining);
-    if (counters) {
-      counters->pdb_hits += p.found_keys.size();
-      counters->missing += p.missing_keys.size();
-    }
-    if (use_vdb && !p.found_keys.empty())
-      vdb->insert_async(table.name, p.found_keys, p.found_vectors);
-    out.found_keys.insert(out.found_keys.end(), p.found_keys.begin(), p.found_keys.end());
-    out.found_vectors.insert(out.found_vectors.end(), p.found_vectors.begin(),
-                             p.found_vectors.end());
-    out.missing_keys = std::move(p.missing_keys);
+  out.found_keys.resize(keys.size());
+  out.found_vectors.resize(keys.size() * table.dimension);
+  out.missing_keys.resize(keys.size());
+  b200_detail::PdbTier tier{&pdb, &table.name};
+  std::size_t nf = 0, nm = 0;
+  std::uint64_t c[3] = {0, 0, 0};
+  b200_detail::check(hps_tier_fetch(vdb ? vdb->handle() : nullptr, table.name.c_str(),
+                                    table.dimension, &b200_detail::pdb_fetch, &tier, keys.data(),
+                                    keys.size(), out.found_keys.data(), out.found_vectors.data(),
+                                    &nf, out.missing_keys.data(), &nm, c));
+  out.found_keys.resize(nf);
+  out.found_vectors.resize(nf * table.dimension);
+  out.missing_keys.resize(nm);
+  if (counters) {
+    counters->vdb_hits += c[0];
+    counters->pdb_hits += c[1];
+    counters->missing += c[2];
   }
   return out;
 }
@@ -131,7 +152,12 @@ class LookupEngine {
   // lookup_engine.cpp:91-117 (same validation, std::invalid_argument)
   LookupEngine(const TableId& table, SlabCache& cache, VolatileStore* vdb, PersistentStore& pdb,
                EngineConfig config)
-      : table_(table), cache_(cache), vdb_(vdb), pdb_(pdb), config_(std::move(config)) {
+      : table_(table),
+        cache_(cache),
+        vdb_(vdb),
+        pdb_(pdb),
+        config_(std::move(config)),
+        tier_{&pdb_, &table_.name} {
     if (config_.workspace_pool_size == 0)
       throw std::invalid_argument("workspace pool size must be positive");
     validate_table_id(table_);
@@ -141,10 +167,12 @@ class LookupEngine {
     c.default_vector_len = uint32_t(config_.default_vector.size());
     c.workspace_pool_size = uint32_t(config_.workspace_pool_size);
     c.async_worker_count = config_.async_worker_count;
-    c.volatile_tier_enabled = 0;  // the tiers are reached through cold_fetch
+    c.volatile_tier_enabled = config_.volatile_tier_enabled ? 1 : 0;
     c.max_batch = 0;
+    // misses: the native volatile DB in-process, then the persistent tier
     b200_detail::check(hps_engine_create(table_.name.c_str(), table_.dimension, cache_.handle(),
-                                         nullptr, &LookupEngine::cold_fetch, this, &c, &h_));
+                                         vdb_ ? vdb_->handle() : nullptr,
+                                         &b200_detail::pdb_fetch, &tier_, &c, &h_));
     pool_.engine_ = h_;
   }
   ~LookupEngine() { hps_engine_destroy(h_); }
@@ -186,48 +214,23 @@ class LookupEngine {
     o.async_batches = s.async_batches;
     o.defaults_returned = s.defaults_returned;
     o.async_faults = s.async_faults;
-    // tier split as seen by tier_fetch (sync and background fetches alike)
-    o.vdb_hits = vdb_hits_.load();
-    o.pdb_hits = pdb_hits_.load();
-    o.tier_missing = missing_.load();
+    o.vdb_hits = s.vdb_hits;  // sync and background fetches alike
+    o.pdb_hits = s.pdb_hits;
+    o.tier_missing = s.tier_missing;
     return o;
   }
   const TableId& table() const { return table_; }
   WorkspacePool& workspace_pool() { return pool_; }
 
  private:
-  // hps_cold_fetch_fn: the reference tiers behind the GPU engine
-  static int cold_fetch(void* ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
-                        float* found_vectors, size_t* n_found, uint64_t* missing_keys,
-                        size_t* n_missing) {
-    auto* self = static_cast<LookupEngine*>(ctx);
-    try {
-      TierCounters tc;
-      FetchResult f = tier_fetch(self->table_, std::span<const EmbeddingKey>(keys, n),
-                                 self->config_.volatile_tier_enabled ? self->vdb_ : nullptr,
-                                 self->pdb_, &tc);
-      self->vdb_hits_ += tc.vdb_hits;
-      self->pdb_hits_ += tc.pdb_hits;
-      self->missing_ += tc.missing;
-      std::copy(f.found_keys.begin(), f.found_keys.end(), found_keys);
-      std::copy(f.found_vectors.begin(), f.found_vectors.end(), found_vectors);
-      std::copy(f.missing_keys.begin(), f.missing_keys.end(), missing_keys);
-      *n_found = f.found_keys.size();
-      *n_missing = f.missing_keys.size();
-      return 0;
-    } catch (...) {
-      return 1;  // surfaces as TierFault (sync) or an async fault
-    }
-  }
-
   TableId table_;
   SlabCache& cache_;
   VolatileStore* vdb_;
   PersistentStore& pdb_;
   EngineConfig config_;
+  b200_detail::PdbTier tier_;
   hps_engine* h_ = nullptr;
   WorkspacePool pool_;
-  std::atomic<std::uint64_t> vdb_hits_{0}, pdb_hits_{0}, missing_{0};
 };
 
 }  // namespace hps

@@ -255,6 +255,17 @@ int hps_vdb_last_access(hps_vdb* vdb, const char* name, uint64_t key, uint64_t* 
 /* replaces evict (volatile_store.cpp:190-199) */
 int hps_vdb_evict(hps_vdb* vdb, const char* name, uint32_t partition,
                   uint64_t* evicted, size_t evicted_cap, size_t* n_evicted);
+/* The full evicted-key list of this thread's last hps_vdb_insert /
+ * hps_vdb_evict (for callers whose evicted_cap was too small): copies up to
+ * cap keys, *n = the list's length. */
+int hps_vdb_last_evicted(uint64_t* out, size_t cap, size_t* n);
+/* the table's registered dimension (TableId::dimension) */
+int hps_vdb_dimension(hps_vdb* vdb, const char* name, uint32_t* out);
+/* replaces partition_count (volatile_store.cpp:59-61) */
+int hps_vdb_partition_count(hps_vdb* vdb, const char* name, uint32_t* out);
+/* replaces keys (volatile_store.cpp:293-303): every resident key, partition
+ * by partition; copies up to cap keys (out may be NULL), *n = the count. */
+int hps_vdb_keys(hps_vdb* vdb, const char* name, uint64_t* out, size_t cap, size_t* n);
 
 /* ---- cold tier callback (stands in for hps::PersistentStore::get,
  *      persistent_store.cpp:405-439, which stays CPU code) ---- */
@@ -388,11 +399,6 @@ int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_p
 int hps_wire_lookup_frame(int device, const float* rows, const uint8_t* miss_flags,
                           uint32_t count, uint32_t dim, int mem, uint8_t* frame, size_t cap,
                           size_t* frame_len, void* stream);
-
-/* ---- workload (harness input; replaces PowerLawSampler::sample,
- *      workload.cpp:24-70, bit-exact) ---- */
-int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,
-                        uint64_t draw_seed, size_t count, uint64_t* out);
 
 #ifdef __cplusplus
 }

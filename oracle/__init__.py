@@ -34,6 +34,8 @@ REF_CACHE_TEST = HERE / "_ref" / "test_slab_cache_b200"
 REF_ENGINE_TEST = HERE / "_ref" / "test_lookup_engine_b200"
 # tests/unit/test_refresh_engine.cpp + the reference's refresh_engine.cpp over the B200 cache
 REF_REFRESH_TEST = HERE / "_ref" / "test_refresh_engine_b200"
+# tests/unit/test_volatile_store.cpp built against include/hps/volatile_store.hpp
+REF_VDB_TEST = HERE / "_ref" / "test_volatile_store_b200"
 # the reference's acceptance suite (c1-c10) against the B200 cache + engine
 REF_ACCEPTANCE = HERE / "_ref" / "acceptance_b200"
 REF_SRC = Path("/root/reference/proj")

@@ -178,6 +178,10 @@ SIGNATURES = {
     "hps_vdb_table_clock": (C.c_int, [_P, C.c_char_p, _U64P]),
     "hps_vdb_last_access": (C.c_int, [_P, C.c_char_p, C.c_uint64, _U64P, C.POINTER(C.c_int)]),
     "hps_vdb_evict": (C.c_int, [_P, C.c_char_p, C.c_uint32, _P, C.c_size_t, _SZP]),
+    "hps_vdb_last_evicted": (C.c_int, [_P, C.c_size_t, _SZP]),
+    "hps_vdb_dimension": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_uint32)]),
+    "hps_vdb_partition_count": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_uint32)]),
+    "hps_vdb_keys": (C.c_int, [_P, C.c_char_p, _P, C.c_size_t, _SZP]),
     "hps_tier_fetch": (C.c_int, [_P, C.c_char_p, C.c_uint32, COLD_FETCH_FN, _P, _P, C.c_size_t,
                                  _P, _P, _SZP, _P, _SZP, _P]),
     "hps_engine_create": (C.c_int, [C.c_char_p, C.c_uint32, _P, _P, COLD_FETCH_FN, _P,
@@ -188,8 +192,6 @@ SIGNATURES = {
     "hps_engine_drain_async": (C.c_int, [_P]),
     "hps_engine_get_stats": (C.c_int, [_P, C.POINTER(_Stats)]),
     "hps_engine_pool_info": (C.c_int, [_P, _U64P, _U64P, _U64P]),
-    "hps_powerlaw_sample": (C.c_int, [C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t,
-                                      _P]),
 }
 
 
@@ -582,8 +584,6 @@ class VolatileStore:
     def __init__(self, lookup_threads: int = 0):
         self._h = C.c_void_p()
         _check(lib().hps_vdb_create(lookup_threads, C.byref(self._h)))
-        self._dims = {}
-        self._parts = {}
 
     def close(self):
         if getattr(self, "_h", None):
@@ -603,33 +603,47 @@ class VolatileStore:
     def register_table(self, table: TableId, config: VolatileTableConfig = VolatileTableConfig()):
         _check(lib().hps_vdb_register_table(self._h, table.name.encode(), table.dimension,
                                             config.partition_count, config.overflow_margin))
-        self._dims.setdefault(table.name, table.dimension)
-        self._parts.setdefault(table.name, config.partition_count)
 
     def has_table(self, name: str) -> bool:
         return bool(lib().hps_vdb_has_table(self._h, name.encode()))
 
     def partition_count(self, name: str) -> int:
-        if name not in self._parts:
-            raise InvalidArgument("volatile store has no table named " + name)
-        return self._parts[name]
+        v = C.c_uint32(0)
+        _check(lib().hps_vdb_partition_count(self._h, name.encode(), C.byref(v)))
+        return v.value
 
     def _dim(self, name: str) -> int:
-        if name not in self._dims:
-            raise InvalidArgument("volatile store has no table named " + name)
-        return self._dims[name]
+        v = C.c_uint32(0)
+        _check(lib().hps_vdb_dimension(self._h, name.encode(), C.byref(v)))
+        return v.value
+
+    @staticmethod
+    def _evicted(ev: np.ndarray, n: int) -> np.ndarray:
+        if n > len(ev):
+            ev = np.empty(n, dtype=np.uint64)
+            ne = C.c_size_t(0)
+            _check(lib().hps_vdb_last_evicted(_ptr(ev), n, C.byref(ne)))
+        return ev[:n].copy()
 
     def insert(self, name: str, keys, vectors) -> np.ndarray:
         k = _u64(keys)
         v = _f32(vectors)
-        cap = max(len(k) * 4, 1024)
+        cap = len(k) + 64
         ev = np.empty(cap, dtype=np.uint64)
         ne = C.c_size_t(0)
         _check(lib().hps_vdb_insert(self._h, name.encode(), _ptr(k), len(k), _ptr(v), v.size,
                                     _ptr(ev), cap, C.byref(ne)))
-        if ne.value > cap:
-            raise HpsError("evicted key buffer too small")
-        return ev[: ne.value].copy()
+        return self._evicted(ev, ne.value)
+
+    def keys(self, name: str) -> np.ndarray:
+        n = C.c_size_t(0)
+        _check(lib().hps_vdb_keys(self._h, name.encode(), None, 0, C.byref(n)))
+        out = np.empty(n.value + 1024, dtype=np.uint64)
+        _check(lib().hps_vdb_keys(self._h, name.encode(), _ptr(out), len(out), C.byref(n)))
+        if n.value > len(out):
+            out = np.empty(n.value, dtype=np.uint64)
+            _check(lib().hps_vdb_keys(self._h, name.encode(), _ptr(out), len(out), C.byref(n)))
+        return out[: min(n.value, len(out))].copy()
 
     def insert_async(self, name: str, keys, vectors) -> None:
         k = _u64(keys)
@@ -639,7 +653,7 @@ class VolatileStore:
 
     def lookup(self, name: str, keys) -> FetchResult:
         k = _u64(keys)
-        d = self._dim(name) if name in self._dims else 1
+        d = self._dim(name)
         n = len(k)
         fk = np.empty(max(n, 1), dtype=np.uint64)
         fv = np.empty(max(n, 1) * d, dtype=np.float32)
@@ -650,11 +664,11 @@ class VolatileStore:
         return FetchResult(fk[: nf.value].copy(), fv[: nf.value * d].copy(), mk[: nm.value].copy())
 
     def evict(self, name: str, partition: int) -> np.ndarray:
-        cap = 1 << 16
+        cap = 1024
         ev = np.empty(cap, dtype=np.uint64)
         ne = C.c_size_t(0)
         _check(lib().hps_vdb_evict(self._h, name.encode(), partition, _ptr(ev), cap, C.byref(ne)))
-        return ev[: min(ne.value, cap)].copy()
+        return self._evicted(ev, ne.value)
 
     def drain(self) -> None:
         _check(lib().hps_vdb_drain(self._h))
@@ -986,14 +1000,6 @@ def wire_lookup_frame_device(rows_ptr: int, flags_ptr: int, count: int, dim: int
     _check(lib().hps_wire_lookup_frame(device, rows_ptr, flags_ptr, count, dim, HPS_MEM_DEVICE,
                                        frame_ptr, cap, C.byref(n), stream or None))
     return n.value
-
-
-def powerlaw_sample(alpha: float, keyspace: int, permute_seed: int, draw_seed: int,
-                    count: int) -> np.ndarray:
-    """PowerLawSampler::sample (workload.cpp:24-70), bit-exact."""
-    out = np.empty(count, dtype=np.uint64)
-    _check(lib().hps_powerlaw_sample(alpha, keyspace, permute_seed, draw_seed, count, _ptr(out)))
-    return out
 
 
 def bench_draw_seed(seed: int) -> int:

@@ -32,13 +32,10 @@ struct hps_graph {
   std::vector<hpsb::GraphCacheUse> uses;
 };
 
-namespace hpsb {
-void powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed, uint64_t draw_seed,
-                     size_t count, uint64_t* out);
-}
-
 namespace {
 thread_local std::string g_error;
+// keys evicted by this thread's last hps_vdb_insert / hps_vdb_evict
+thread_local std::vector<uint64_t> g_evicted;
 
 template <class F>
 int guarded(F&& f) {
@@ -601,7 +598,8 @@ int hps_vdb_insert(hps_vdb* vdb, const char* name, const uint64_t* keys, size_t 
                    size_t evicted_cap, size_t* n_evicted) {
   return guarded([&] {
     need(vdb && name, "null argument");
-    auto ev = vdb->impl->insert(name, keys, n, vectors, vectors_len);
+    g_evicted = vdb->impl->insert(name, keys, n, vectors, vectors_len);
+    const auto& ev = g_evicted;
     if (evicted) std::copy(ev.begin(), ev.begin() + std::min(ev.size(), evicted_cap), evicted);
     if (n_evicted) *n_evicted = ev.size();
   });
@@ -646,9 +644,37 @@ int hps_vdb_last_access(hps_vdb* vdb, const char* name, uint64_t key, uint64_t* 
 int hps_vdb_evict(hps_vdb* vdb, const char* name, uint32_t partition, uint64_t* evicted,
                   size_t evicted_cap, size_t* n_evicted) {
   return guarded([&] {
-    auto ev = vdb->impl->evict(name, partition);
+    g_evicted = vdb->impl->evict(name, partition);
+    const auto& ev = g_evicted;
     if (evicted) std::copy(ev.begin(), ev.begin() + std::min(ev.size(), evicted_cap), evicted);
     if (n_evicted) *n_evicted = ev.size();
+  });
+}
+int hps_vdb_last_evicted(uint64_t* out, size_t cap, size_t* n) {
+  return guarded([&] {
+    need(n != nullptr, "null argument");
+    if (out) std::copy(g_evicted.begin(), g_evicted.begin() + std::min(g_evicted.size(), cap), out);
+    *n = g_evicted.size();
+  });
+}
+int hps_vdb_dimension(hps_vdb* vdb, const char* name, uint32_t* out) {
+  return guarded([&] {
+    need(vdb && name && out, "null argument");
+    *out = vdb->impl->dimension(name);
+  });
+}
+int hps_vdb_partition_count(hps_vdb* vdb, const char* name, uint32_t* out) {
+  return guarded([&] {
+    need(vdb && name && out, "null argument");
+    *out = vdb->impl->partition_count(name);
+  });
+}
+int hps_vdb_keys(hps_vdb* vdb, const char* name, uint64_t* out, size_t cap, size_t* n) {
+  return guarded([&] {
+    need(vdb && name && n, "null argument");
+    auto k = vdb->impl->keys(name);
+    if (out) std::copy(k.begin(), k.begin() + std::min(k.size(), cap), out);
+    *n = k.size();
   });
 }
 
@@ -809,9 +835,5 @@ int hps_engine_pool_info(hps_engine* engine, uint64_t* size, uint64_t* outstandi
   });
 }
 
-int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,
-                        uint64_t draw_seed, size_t count, uint64_t* out) {
-  return guarded([&] { hpsb::powerlaw_sample(alpha, keyspace, permute_seed, draw_seed, count, out); });
-}
 
 }  // extern "C"

@@ -103,6 +103,21 @@ VolatileStore::Table& VolatileStore::table_ref(const std::string& name) const {
 
 uint32_t VolatileStore::dimension(const std::string& name) const { return table_ref(name).dim; }
 
+uint32_t VolatileStore::partition_count(const std::string& name) const {
+  return table_ref(name).partition_count;
+}
+
+std::vector<uint64_t> VolatileStore::keys(const std::string& name) const {
+  Table& t = table_ref(name);
+  std::vector<uint64_t> out;
+  for (auto& p : t.parts) {
+    std::shared_lock<std::shared_mutex> lk(p->mu);
+    for (uint32_t s : p->index)
+      if (s) out.push_back(p->keys[s - 1]);
+  }
+  return out;
+}
+
 void VolatileStore::upsert(Partition& p, uint32_t dim, uint64_t key, const float* row,
                            uint64_t stamp) {
   int64_t e = p.find(key);

@@ -40,6 +40,9 @@ class VolatileStore {
                       uint64_t overflow_margin);
   bool has_table(const std::string& name) const;
   uint32_t dimension(const std::string& name) const;
+  uint32_t partition_count(const std::string& name) const;
+  // Every resident key, partition by partition (volatile_store.cpp:293-303).
+  std::vector<uint64_t> keys(const std::string& name) const;
 
   // Upsert + prune touched partitions; returns evicted keys.
   std::vector<uint64_t> insert(const std::string& name, const uint64_t* keys, size_t n,

@@ -24,6 +24,7 @@ def _built():
 
     if not oracle.ORACLE_SO.exists() or (oracle.REF_SRC.exists() and not (
             oracle.REF_SO.exists() and oracle.REF_CACHE_TEST.exists()
-            and oracle.REF_ENGINE_TEST.exists() and oracle.REF_REFRESH_TEST.exists())):
+            and oracle.REF_ENGINE_TEST.exists() and oracle.REF_REFRESH_TEST.exists()
+            and oracle.REF_VDB_TEST.exists())):
         oracle.build()
     yield

@@ -1,8 +1,10 @@
-"""The drop-in C++ surface: include/hps/slab_cache.hpp and
-include/hps/lookup_engine.hpp re-expose the reference's hps::SlabCache
-(slab_cache.hpp:23-178) and hps::LookupEngine / tier_fetch
+"""The drop-in C++ surface: include/hps/slab_cache.hpp,
+include/hps/volatile_store.hpp and include/hps/lookup_engine.hpp re-expose
+the reference's hps::SlabCache (slab_cache.hpp:23-178), hps::VolatileStore
+(volatile_store.hpp:27-89) and hps::LookupEngine / tier_fetch
 (lookup_engine.hpp:29-196) over the C ABI, and the reference's OWN unit
-tests, tests/unit/test_slab_cache.cpp and test_lookup_engine.cpp -- and the
+tests, tests/unit/test_slab_cache.cpp, test_volatile_store.cpp and
+test_lookup_engine.cpp -- and the
 reference's refresh loop (refresh_engine.cpp, a caller of the cache) with
 test_refresh_engine.cpp -- compiled unchanged against them (oracle/Makefile targets _ref/test_*_b200; doctest is
 the local stand-in oracle/doctest_stub), must pass on the GPU; so must the
@@ -42,6 +44,22 @@ BINARIES = [oracle.REF_CACHE_TEST, oracle.REF_ENGINE_TEST, oracle.REF_REFRESH_TE
             oracle.REF_ACCEPTANCE]
 
 
+def test_reference_volatile_store_test_passes_on_the_native_store():
+    """The reference's test_volatile_store.cpp, unchanged, over the native
+    host VDB (host code: runs without a GPU)."""
+    exe = oracle.REF_VDB_TEST
+    if not exe.exists():
+        pytest.skip("reference sources absent and no prebuilt binary")
+    nm = subprocess.run(["nm", "-C", str(exe)], capture_output=True, text=True).stdout
+    # the reference's own store is NOT linked in
+    assert "hps::VolatileStore::background_loop" not in nm
+    assert "hps::VolatileStore::prune_partition" not in nm
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    tail = "\n".join(r.stderr.splitlines()[-40:])
+    assert r.returncode == 0, tail
+    assert "0 failed" in r.stderr, tail
+
+
 @pytest.mark.parametrize("exe", BINARIES, ids=lambda p: p.name)
 def test_reference_unit_test_binary_is_built_against_the_library(exe):
     if not exe.exists():
@@ -51,7 +69,7 @@ def test_reference_unit_test_binary_is_built_against_the_library(exe):
     # the reference's own cache / engine implementation is NOT linked in
     nm = subprocess.run(["nm", "-C", str(exe)], capture_output=True, text=True).stdout
     for sym in ("hps::SlabCache::apply_query", "hps::SlabCache::run_grouped",
-                "hps::LookupEngine::async_loop"):
+                "hps::LookupEngine::async_loop", "hps::VolatileStore::background_loop"):
         assert sym not in nm
 
 

@@ -9,6 +9,8 @@ import json
 from pathlib import Path
 
 import numpy as np
+
+from tools import workload
 import pytest
 
 import oracle
@@ -226,7 +228,7 @@ def test_lockstep_with_engine_oracle_power_law(threshold):
     c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
     eng = hps.LookupEngine(table, c, vdb, None,
                            hps.EngineConfig(hit_rate_threshold=threshold, default_vector=[1.5]))
-    stream = hps.powerlaw_sample(1.2, 40000, 7, 8, 30 * 2048)
+    stream = workload.powerlaw_sample(1.2, 40000, 7, 8, 30 * 2048)
     for b in range(30):
         keys = stream[b * 2048:(b + 1) * 2048]
         o = hps.LookupOutcome()
@@ -259,7 +261,7 @@ def test_device_and_pinned_pointer_lookups_match_host_lookup():
     ch, eh = mk()
     cd, ed = mk()
     cp, ep = mk()
-    stream = hps.powerlaw_sample(1.2, 100000, 1, 2, 8 * 16384)
+    stream = workload.powerlaw_sample(1.2, 100000, 1, 2, 8 * 16384)
     for b in range(8):
         keys = stream[b * 16384:(b + 1) * 16384]
         r = eh.lookup(keys)
@@ -310,7 +312,7 @@ def test_multi_table_lookup_equals_per_table_lookups():
     vb, cb, eb = build()
     rng = np.random.default_rng(9)
     for r in range(6):
-        batches = [hps.powerlaw_sample(1.1, 26000, t, 50 * r + t, n) + np.uint64(t * 100000)
+        batches = [workload.powerlaw_sample(1.1, 26000, t, 50 * r + t, n) + np.uint64(t * 100000)
                    for t in range(T_)]
         pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
         po = [torch.empty(n * d).pin_memory() for _ in range(T_)]
@@ -441,7 +443,7 @@ def test_group_multi_lookup_one_launch_equals_per_table_lookups(dims, pinned):
         ns = [(700 + 311 * t + 97 * r) % 4097 for t in range(T_)]
         if r == 2:
             ns[0] = 0
-        batches = [hps.powerlaw_sample(1.1, 11000, t, 70 * r + t, ns[t]) + np.uint64(t * 100000)
+        batches = [workload.powerlaw_sample(1.1, 11000, t, 70 * r + t, ns[t]) + np.uint64(t * 100000)
                    for t in range(T_)]
         if pinned:
             pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
@@ -500,7 +502,7 @@ def test_zero_copy_small_calls_pinned_and_pageable_match_oracle(threshold):
     po = torch.empty(maxn * d).pin_memory()
     pf = torch.empty(maxn, dtype=torch.uint8).pin_memory()
     sizes = [1, 7, 1024, 4096, 4097, 300, 4096, 2048, 33, 4097, 1500, 4000]
-    stream = hps.powerlaw_sample(1.15, 60000, 11, 12, sum(sizes))
+    stream = workload.powerlaw_sample(1.15, 60000, 11, 12, sum(sizes))
     at = 0
     for b, n in enumerate(sizes):
         keys = stream[at:at + n]
@@ -555,7 +557,7 @@ def test_group_multi_lookup_with_empty_tables_over_many_calls():
     m = hps.MultiLookup(ea, max_batch=2048)
     for r in range(20):
         ns = [0, 0 if r % 5 == 4 else 200 + 37 * r]
-        batches = [hps.powerlaw_sample(1.1, 6000, t, 90 * r + t, ns[t]) + np.uint64(t * 100000)
+        batches = [workload.powerlaw_sample(1.1, 6000, t, 90 * r + t, ns[t]) + np.uint64(t * 100000)
                    for t in range(T_)]
         got = m.lookup(batches)
         for t in range(T_):
@@ -599,7 +601,7 @@ def test_engine_lookup_multi_device_mode_orders_against_default_stream():
     va, ea = build()
     vb, eb = build()
     for r in range(4):
-        batches = [hps.powerlaw_sample(1.05, 60000, t, 11 * r + t, n) + np.uint64(t * 100000)
+        batches = [workload.powerlaw_sample(1.05, 60000, t, 11 * r + t, n) + np.uint64(t * 100000)
                    for t in range(T_)]
         # keys land on the device through a default-stream kernel (x + 0)
         src = [torch.from_numpy(b.view(np.int64)).cuda() for b in batches]

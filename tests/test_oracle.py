@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
+from tools import workload
 from opstream import ops, row_values, run_stream
 
 GOLD = Path(__file__).resolve().parent / "golden"
@@ -158,7 +159,7 @@ def test_product_sampler_matches_reference_fixture():
     s = _load("sampler.json")
     for name in ("cfg1", "cfg2"):
         f = s[name]
-        keys = hps.powerlaw_sample(f["alpha"], f["keyspace"], f["permute_seed"], f["draw_seed"],
+        keys = workload.powerlaw_sample(f["alpha"], f["keyspace"], f["permute_seed"], f["draw_seed"],
                                    f["count"])
         assert keys[:64].tolist() == f["head"]
         assert hashlib.sha256(keys.tobytes()).hexdigest() == f["sha256"]

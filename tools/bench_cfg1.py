@@ -13,7 +13,7 @@ engines on the IDENTICAL key stream:
 
 The stream is the reference sampler's (PowerLawSampler, permute seed 42,
 draw seed 42 ^ 0x9E3779B97F4A7C15, bench.cpp:33-35, restated bit-exactly
-by hps.powerlaw_sample). Both volatile DBs hold the whole table up front
+by workload.powerlaw_sample). Both volatile DBs hold the whole table up front
 (run_bench starts with the rows in its persistent store and promotes them
 into the VDB on first miss; which tier serves a miss does not change the
 cache's trajectory). Per threshold (1.0: every batch with a miss takes the
@@ -43,13 +43,15 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
+from tools import workload  # noqa: E402
+
 KEYS, DIM, BATCH, ALPHA, SEED = 1_000_000, 16, 1024, 1.2, 42
 
 
 def cfg1_stream(batches: int) -> np.ndarray:
     import paper_2210_08804_b200 as hps
 
-    return hps.powerlaw_sample(ALPHA, KEYS, SEED, SEED ^ 0x9E3779B97F4A7C15, batches * BATCH)
+    return workload.powerlaw_sample(ALPHA, KEYS, SEED, SEED ^ 0x9E3779B97F4A7C15, batches * BATCH)
 
 
 def run(threshold: float, batches: int, compare_rows: bool, stream: np.ndarray,

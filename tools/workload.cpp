@@ -1,26 +1,23 @@
-// workload.cpp -- synthetic power-law key streams (harness input).
+// workload.cpp -- synthetic power-law key streams: HARNESS INPUT for the
+// bench and the tests (tools/libhps_workload.so), not part of the product
+// library.
 //
 // Bit-exact restatement of PowerLawSampler (workload.cpp:18-20, 24-70 of the
-// reference): inverse CDF over r^-alpha (running sum of std::pow, normalised,
-// last entry forced to 1.0), mt19937_64 Fisher-Yates rank -> key permutation
-// (`gen() % (i + 1)`), uniform = top 53 bits * 2^-53, upper_bound search.
-// The CDF build and the permutation are O(keyspace); the draws fan out over
-// threads with per-draw generator positions reproduced by discarding.
+// reference; SURVEY.md §2 marks the sampler "reused verbatim" so the streams
+// match the reference's bit for bit): inverse CDF over r^-alpha (running sum
+// of std::pow, normalised, last entry forced to 1.0), mt19937_64
+// Fisher-Yates rank -> key permutation (`gen() % (i + 1)`), uniform = top 53
+// bits * 2^-53, upper_bound search. Serial, O(keyspace + count log keyspace).
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <random>
-#include <stdexcept>
 #include <vector>
 
-#include "runtime.hpp"
-
-namespace hpsb {
-
-void powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed, uint64_t draw_seed,
-                     size_t count, uint64_t* out) {
-  if (keyspace == 0) throw invalid_argument("keyspace must be positive");
-  if (!(alpha > 0.0)) throw invalid_argument("alpha must be positive");
+extern "C" int hps_powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed,
+                                   uint64_t draw_seed, size_t count, uint64_t* out) {
+  if (keyspace == 0 || !(alpha > 0.0) || (count > 0 && out == nullptr)) return 1;
   std::vector<double> cdf(keyspace);
   double running = 0.0;
   for (uint64_t r = 1; r <= keyspace; ++r) {
@@ -44,6 +41,5 @@ void powerlaw_sample(double alpha, uint64_t keyspace, uint64_t permute_seed, uin
     rank = std::min(rank, keyspace);
     out[i] = rank_to_key[rank - 1];
   }
+  return 0;
 }
-
-}  // namespace hpsb
