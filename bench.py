@@ -454,6 +454,12 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, hps, torch, cache, wl, dev, rank, dist)
+        # next to the pinned headline: the same call with pageable buffers,
+        # and the synchronous miss path (h 0.5 under threshold 0.8)
+        e2e["pageable"] = run_e2e(args, hps, torch, cache, wl, dev, rank, dist, pageable=True)
+        e2e["sync_h050"] = run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=0.5)
+        if world == 1:
+            e2e["dropin_cpp"] = run_dropin(args, wl)
     clk = clocks.stop()
 
     value = world * args.steps * n / (main["total_ms"] / 1e3)
@@ -615,9 +621,16 @@ def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
                                              "ms_per_batch": mixed_ms}}
 
 
-def run_e2e(args, hps, torch, cache, wl, dev, rank, dist):
+def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=False,
+            threshold=0.8):
+    """hps_engine_lookup with HOST buffers, copies inside the timed region.
+    pinned (default): page-locked keys / rows / flags (the headline e2e);
+    pageable: plain numpy buffers (rows come back through the engine's
+    chunked staging + parallel copy-on); `hit` / `threshold` pick the branch
+    mix (h 0.5 at threshold 0.8 = every batch on the synchronous miss path)."""
     d, n = wl.dim, wl.batch
-    batches, p, _ = wl.batches(args.hit, 32, seed=3000 + rank)
+    hit = args.hit if hit is None else hit
+    batches, p, _ = wl.batches(hit, 32, seed=3000 + rank + int(hit * 100))
     vdb = hps.VolatileStore(8)
     table = hps.TableId("bench", d)
     vdb.register_table(table, hps.VolatileTableConfig(partition_count=16,
@@ -628,25 +641,39 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist):
         k = miss_keys[i:i + (1 << 18)]
         vdb.insert("bench", k, table_rows(k, d))
     eng = hps.LookupEngine(table, cache, vdb, None,
-                           hps.EngineConfig(hit_rate_threshold=0.8, workspace_pool_size=16,
+                           hps.EngineConfig(hit_rate_threshold=threshold, workspace_pool_size=16,
                                             async_worker_count=2))
-    pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
     ring = 4
-    po = [torch.empty(n * d).pin_memory() for _ in range(ring)]
-    pf = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(ring)]
+    if pageable:
+        pk = [np.ascontiguousarray(b) for b in batches]
+        po = [np.empty(n * d, dtype=np.float32) for _ in range(ring)]
+        pf = [np.empty(n, dtype=np.uint8) for _ in range(ring)]
+        for a in po + pf:
+            a.fill(0)  # resident pages (as a reused caller buffer would be)
+        kp = [a.ctypes.data for a in pk]
+        op = [a.ctypes.data for a in po]
+        fp = [a.ctypes.data for a in pf]
+    else:
+        pk = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
+        po = [torch.empty(n * d).pin_memory() for _ in range(ring)]
+        pf = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(ring)]
+        kp = [t.data_ptr() for t in pk]
+        op = [t.data_ptr() for t in po]
+        fp = [t.data_ptr() for t in pf]
     for s in range(args.warmup):
-        eng.lookup_ptrs(pk[s % 32].data_ptr(), n, po[s % ring].data_ptr(), pf[s % ring].data_ptr(),
-                        hps.HPS_MEM_HOST)
+        eng.lookup_ptrs(kp[s % 32], n, op[s % ring], fp[s % ring], hps.HPS_MEM_HOST)
     eng.drain_async()
     torch.cuda.synchronize()
+    st0 = eng.stats()
     if dist:
         dist.barrier()
     l0 = hps.kernel_launch_count()
-    hs = []
+    hs, lat = [], []
     t0 = time.perf_counter()
     for s in range(args.steps):
-        o = eng.lookup_ptrs(pk[s % 32].data_ptr(), n, po[s % ring].data_ptr(),
-                            pf[s % ring].data_ptr(), hps.HPS_MEM_HOST)
+        c0 = time.perf_counter()
+        o = eng.lookup_ptrs(kp[s % 32], n, op[s % ring], fp[s % ring], hps.HPS_MEM_HOST)
+        lat.append(time.perf_counter() - c0)
         hs.append(o.unique_hit_rate)
     eng.drain_async()
     torch.cuda.synchronize()
@@ -656,13 +683,46 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist):
     world = dist.get_world_size() if dist else 1
     st = eng.stats()
     eng.close()
+    lat_us = np.array(lat) * 1e6
     return {"value": world * args.steps * n / el, "unit": "keys/s",
             "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * d * 4 + n,
             "ms_per_step": el * 1e3 / args.steps, "mean_unique_hit_rate": float(np.mean(hs)),
-            "api": "hps_engine_lookup (LookupEngine::lookup), pinned host buffers, "
-                   "threshold 0.8, async VDB fill + replace inside the timed region",
-            "sync_batches": st.sync_batches, "async_batches": st.async_batches,
+            "p50_call_us": float(np.percentile(lat_us, 50)),
+            "p99_call_us": float(np.percentile(lat_us, 99)),
+            "call_us": [round(float(x), 1) for x in lat_us],
+            "api": "hps_engine_lookup (LookupEngine::lookup), "
+                   + ("PAGEABLE" if pageable else "pinned") + " host buffers, "
+                   f"threshold {threshold}, target unique hit {hit}; VDB fetch + scatter + "
+                   "replace of misses (sync branch) or async fill inside the timed region",
+            "sync_batches": st.sync_batches - st0.sync_batches,
+            "async_batches": st.async_batches - st0.async_batches,
             "gpu_launches": launches}
+
+
+def run_dropin(args, wl):
+    """The same e2e through the DROP-IN C++ API (tools/bench_dropin.cpp):
+    hps::LookupEngine::lookup returning the reference's std::vector
+    LookupResult (pageable), over the drop-in SlabCache + VolatileStore, in a
+    separate process with its own cache replica of the same geometry."""
+    import tempfile
+
+    exe = ROOT / "tools" / "_build" / "bench_dropin_b200"
+    if not exe.exists():
+        return {"unavailable": "tools/_build/bench_dropin_b200 not built"}
+    batches, _, _ = wl.batches(args.hit, 32, seed=3000)
+    allk = np.concatenate(batches).astype(np.uint64)
+    miss = np.unique(allk)
+    miss = miss[~np.isin(miss, wl.R)]
+    with tempfile.TemporaryDirectory() as td:
+        wl.preload.astype(np.uint64).tofile(os.path.join(td, "preload.u64"))
+        miss.tofile(os.path.join(td, "vdb.u64"))
+        allk.tofile(os.path.join(td, "batches.u64"))
+        r = subprocess.run([str(exe), td, str(wl.S), str(wl.W), str(wl.dim), str(wl.batch),
+                            str(args.steps), str(args.warmup), "0.8"],
+                           capture_output=True, text=True, timeout=900)
+    if r.returncode != 0:
+        return {"failed": r.stderr[-500:] + r.stdout[-500:]}
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 # ------------------------------------------------------ reference arm -----

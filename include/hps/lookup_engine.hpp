@@ -31,6 +31,10 @@
 #include "hps/volatile_store.hpp"
 #include "hps_b200.h"
 
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
+
 namespace hps {
 
 // lookup_engine.hpp:29-37
@@ -50,6 +54,25 @@ struct TierCounters {
 };
 
 namespace b200_detail {
+// A value-initialised vector of n elements, as std::vector(n) gives, but with
+// its storage advised onto transparent huge pages before the zero-fill: a
+// 33.5 MB result (cfg 2: 65,536 x 128 floats) then takes ~17 page faults
+// instead of ~8,200 -- the fault path dominates a fresh result's cost.
+template <class T>
+std::vector<T> sized_vector(std::size_t n) {
+  std::vector<T> v;
+  v.reserve(n);
+#if defined(__linux__) && defined(MADV_HUGEPAGE)
+  constexpr std::uintptr_t kHuge = std::uintptr_t(2) << 20;
+  const auto a = reinterpret_cast<std::uintptr_t>(v.data());
+  const std::uintptr_t lo = (a + kHuge - 1) & ~(kHuge - 1);
+  const std::uintptr_t hi = (a + n * sizeof(T)) & ~(kHuge - 1);
+  if (hi > lo) (void)::madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+#endif
+  v.resize(n);
+  return v;
+}
+
 // hps_cold_fetch_fn over the reference's PersistentStore::get
 // (persistent_store.cpp:405-439): the tier below the native volatile DB.
 struct PdbTier {
@@ -184,7 +207,7 @@ class LookupEngine {
   LookupResult lookup(std::span<const EmbeddingKey> keys, LookupOutcome* outcome = nullptr) {
     LookupResult r;
     r.dimension = table_.dimension;
-    r.vectors.resize(keys.size() * table_.dimension);
+    r.vectors = b200_detail::sized_vector<float>(keys.size() * table_.dimension);
     r.miss_flags.resize(keys.size());
     hps_lookup_outcome o{};
     b200_detail::check(hps_engine_lookup(h_, keys.data(), keys.size(), r.vectors.data(),

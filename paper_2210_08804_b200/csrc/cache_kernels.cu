@@ -138,23 +138,29 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
 // (slab_cache.cpp:131-142: keys grouped by slabset, input order inside a
 // group) in two launches and no memsets (batches above kSmallReplaceMax):
 //   k_replace_bin    one thread per key: slabset, the set's entry in a
-//                    per-call table (CAS on the set id), the key's index
-//                    appended there (atomicAdd rank; the rank-0 key leads)
-//   [k_replace_dups] (validated calls) each leader compares its set's keys:
-//                    any duplicate rejects the whole call before mutation
-//   k_replace_sets   one warp per LEADER: the set's key indices sorted into
-//                    input order, the set's masks, keys and counters loaded
-//                    ONCE into registers (lane j holds slot j of every slab)
-//                    with the first rows prefetched, then every key of the set
-//                    applied serially against that register state -- probe by
-//                    ballot, lowest free slot of the first non-full probed
-//                    slab, else the argmin counter (ties to the lowest
-//                    (slab, slot)); only the changed words are stored; the
-//                    set's table entry is cleared (the table is clean again)
+//                    per-call table (CAS on the set id), the key's index and
+//                    the key itself appended there (atomicAdd rank); the
+//                    rank-0 key publishes (entry, set) into a compact list of
+//                    touched sets (one warp-aggregated add per warp)
+//   [k_replace_dups] (validated calls) a warp per touched set compares its
+//                    keys: any duplicate rejects the whole call before mutation
+//   k_replace_sets   a warp per TOUCHED SET (the compact list; warps past its
+//                    end exit on the list's sentinel): the set's masks, keys
+//                    and counters loaded ONCE into registers (lane j holds slot
+//                    j of every slab) together with the set's key indices and
+//                    keys, the indices sorted into input order, the first rows
+//                    prefetched; then every key of the set applied serially
+//                    against that register state -- probe by ballot, lowest
+//                    free slot of the first non-full probed slab, else the
+//                    argmin counter (ties to the lowest (slab, slot)); only the
+//                    changed words are stored; the set's table entry and list
+//                    slot are cleared (the scratch is clean again). Dependent
+//                    round trips per set: list -> (set state, indices, keys)
+//                    -> rows.
 size_t replace_scratch_bytes(uint64_t n) {
   const uint64_t cap = pow2_at_least(2 * n);
   return align_up(cap * 4, 256) * 4 + align_up(cap * 4 * kReplaceInline, 256) +
-         align_up(n * 4, 256) * 3 + 256;
+         align_up(cap * 8 * kReplaceInline, 256) + align_up(n * 4, 256) * 4 + 256;
 }
 
 ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
@@ -174,9 +180,11 @@ ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
   r.dup_flag = r.cursor + 1;
   r.ovf = take(r.cap * 4);
   r.boff = take(r.cap * 4);
+  r.lead_e = take(n * 4);
   r.idx = take(r.cap * 4 * kReplaceInline);
+  r.kin = reinterpret_cast<uint64_t*>(take(r.cap * 8 * kReplaceInline));
   r.next = take(n * 4);
-  r.entry = take(n * 4);
+  r.lead_s = take(n * 4);
   r.bucket = take(n * 4);
   return r;
 }
@@ -189,7 +197,6 @@ void replace_scratch_init(const ReplaceScratch& rs, cudaStream_t st) {
   cudaMemsetAsync(rs.ovf, 0xFF, size_t(o1 - o0), st);
 }
 
-constexpr uint32_t kLeaderBit = 0x80000000u;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 __global__ void __launch_bounds__(256)
@@ -199,22 +206,40 @@ __global__ void __launch_bounds__(256)
     rs.cursor[0] = 0u;
     rs.dup_flag[0] = 0u;
   }
-  if (i >= n) return;
-  const uint32_t s1 = uint32_t(slabset_of(c, keys[i])) + 1u;
-  const uint64_t mask = rs.cap - 1;
-  uint64_t e = fmix64(s1) & mask;
-  while (true) {
-    const uint32_t old = atomicCAS(rs.set1 + e, 0u, s1);
-    if (old == 0u || old == s1) break;
-    e = (e + 1) & mask;
+  bool lead = false;
+  uint32_t e32 = 0, s1 = 0;
+  if (i < n) {
+    const uint64_t key = keys[i];
+    s1 = uint32_t(slabset_of(c, key)) + 1u;
+    const uint64_t mask = rs.cap - 1;
+    uint64_t e = fmix64(s1) & mask;
+    while (true) {
+      const uint32_t old = atomicCAS(rs.set1 + e, 0u, s1);
+      if (old == 0u || old == s1) break;
+      e = (e + 1) & mask;
+    }
+    const uint32_t r = atomicAdd(rs.cnt + e, 1u);
+    if (r < kReplaceInline) {
+      rs.idx[e * kReplaceInline + r] = uint32_t(i);
+      rs.kin[e * kReplaceInline + r] = key;
+    } else {
+      rs.next[i] = atomicExch(rs.ovf + e, uint32_t(i));
+    }
+    lead = r == 0;
+    e32 = uint32_t(e);
   }
-  const uint32_t r = atomicAdd(rs.cnt + e, 1u);
-  if (r < kReplaceInline) {
-    rs.idx[e * kReplaceInline + r] = uint32_t(i);
-  } else {
-    rs.next[i] = atomicExch(rs.ovf + e, uint32_t(i));
+  __syncwarp();
+  const uint32_t lm = __ballot_sync(0xFFFFFFFFu, lead);
+  if (lm == 0u) return;
+  const uint32_t lane = lane_id();
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(rs.cursor + 2, uint32_t(__popc(lm)));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (lead) {
+    const uint32_t k = base + uint32_t(__popc(lm & ((1u << lane) - 1u)));
+    rs.lead_e[k] = e32;
+    rs.lead_s[k] = s1 - 1u;
   }
-  rs.entry[i] = uint32_t(e) | (r == 0 ? kLeaderBit : 0u);
 }
 
 // Sets of more than 32 keys (tiny caches): the indices in a sorted bucket
@@ -253,48 +278,64 @@ __device__ __forceinline__ const uint32_t* big_bucket(const ReplaceScratch& rs, 
 }
 
 // Indices of a set with at most 32 keys into lanes, sorted: lane j holds the
-// j-th smallest (kNone past cnt). `sw` = 32 words of per-warp shared memory.
+// j-th smallest (kNone past cnt) and, in *key, that key. `sw` = 32 words and
+// `sk` = 32 keys of per-warp shared memory.
 __device__ __forceinline__ uint32_t small_group(const ReplaceScratch& rs, uint64_t e, uint32_t cnt,
-                                                uint32_t* sw) {
+                                                const uint64_t* __restrict__ keys, uint32_t* sw,
+                                                uint64_t* sk, uint64_t* key) {
   const uint32_t lane = lane_id();
   uint32_t v = kNone;
-  if (lane < kReplaceInline && lane < cnt) v = rs.idx[e * kReplaceInline + lane];
+  uint64_t k = 0;
+  if (lane < kReplaceInline && lane < cnt) {
+    v = rs.idx[e * kReplaceInline + lane];
+    k = rs.kin[e * kReplaceInline + lane];
+  }
   if (cnt > kReplaceInline) {
     if (lane == 0) {
       uint32_t j = kReplaceInline;
       for (uint32_t x = rs.ovf[e]; x != kNone && j < 32; x = rs.next[x]) sw[j++] = x;
     }
     __syncwarp();
-    if (lane >= kReplaceInline && lane < cnt) v = sw[lane];
+    if (lane >= kReplaceInline && lane < cnt) {
+      v = sw[lane];
+      k = keys[v];
+    }
     __syncwarp();
   }
-  uint32_t rank = 0;
-  for (uint32_t j = 0; j < cnt; ++j) {
-    const uint32_t o = __shfl_sync(0xFFFFFFFFu, v, j);
-    rank += (o < v) ? 1u : 0u;
+  if (cnt > 1) {
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint32_t o = __shfl_sync(0xFFFFFFFFu, v, j);
+      rank += (o < v) ? 1u : 0u;
+    }
+    if (lane < cnt) {
+      sw[rank] = v;
+      sk[rank] = k;
+    }
+    __syncwarp();
+    v = lane < cnt ? sw[lane] : kNone;
+    k = lane < cnt ? sk[lane] : 0ull;
+    __syncwarp();
   }
-  if (lane < cnt) sw[rank] = v;
-  __syncwarp();
-  v = lane < cnt ? sw[lane] : kNone;
-  __syncwarp();
+  *key = k;
   return v;
 }
 
 __global__ void __launch_bounds__(256)
     k_replace_dups(const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
   __shared__ uint32_t s_w[8][32];
-  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const uint32_t ent = rs.entry[i];
-  if (!(ent & kLeaderBit)) return;
-  const uint64_t e = ent & ~kLeaderBit;
+  __shared__ uint64_t s_k[8][32];
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  const uint32_t e = rs.lead_e[w];
+  if (e == kNone) return;
   const uint32_t cnt = rs.cnt[e];
   if (cnt < 2) return;
   const uint32_t lane = lane_id();
   bool dup = false;
   if (cnt <= 32) {
-    const uint32_t v = small_group(rs, e, cnt, s_w[threadIdx.x >> 5]);
-    const uint64_t k = v != kNone ? keys[v] : 0ull;
+    uint64_t k;
+    (void)small_group(rs, e, cnt, keys, s_w[threadIdx.x >> 5], s_k[threadIdx.x >> 5], &k);
     for (uint32_t j = 0; j < cnt; ++j) {
       const uint64_t o = __shfl_sync(0xFFFFFFFFu, k, j);
       dup |= (lane < cnt && j != lane && o == k);
@@ -322,6 +363,7 @@ __device__ __forceinline__ void replace_apply_set(const CacheDev& c, uint64_t se
                                                   const uint64_t* __restrict__ keys,
                                                   const float* __restrict__ rows, uint64_t stamp,
                                                   uint32_t cnt, uint32_t my_idx,
+                                                  uint64_t my_key_in,
                                                   const uint32_t* __restrict__ big) {
   constexpr int kPre = 4;  // rows prefetched (d <= 128, 16 B aligned)
   const uint32_t lane = lane_id();
@@ -339,7 +381,7 @@ __device__ __forceinline__ void replace_apply_set(const CacheDev& c, uint64_t se
   // lane j < cnt: key and first-slab hash of the j-th key (small groups)
   uint64_t my_key = 0, my_h2 = 0;
   if (big == nullptr && my_idx != kNone) {
-    my_key = keys[my_idx];
+    my_key = my_key_in;
     my_h2 = xxh64_key(my_key, kSlabSeed);
   }
   const bool vec = (d & 3u) == 0 && d <= 128 && (reinterpret_cast<uintptr_t>(rows) & 15u) == 0;
@@ -479,16 +521,21 @@ __global__ void __launch_bounds__(256)
                    const float* __restrict__ rows, uint64_t stamp, uint32_t validate,
                    ReplaceScratch rs) {
   __shared__ uint32_t s_w[8][32];
-  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const uint32_t ent = rs.entry[i];
-  if (!(ent & kLeaderBit)) return;
-  const uint64_t e = ent & ~kLeaderBit;
+  __shared__ uint64_t s_k[8][32];
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  // the list is consumed through its sentinels; its count restarts here
+  if (blockIdx.x == 0 && threadIdx.x == 0) rs.cursor[2] = 0u;
+  if (w >= n) return;
+  const uint32_t e = rs.lead_e[w];
+  if (e == kNone) return;
+  const uint64_t set = rs.lead_s[w];
   const uint32_t cnt = rs.cnt[e];
-  const uint64_t set = rs.set1[e] - 1u;
   const bool rejected = validate && *reinterpret_cast<volatile uint32_t*>(rs.dup_flag) != 0u;
   if (!rejected) {
-    const uint32_t v = cnt <= 32 ? small_group(rs, e, cnt, s_w[threadIdx.x >> 5]) : kNone;
+    uint64_t k = 0;
+    const uint32_t v =
+        cnt <= 32 ? small_group(rs, e, cnt, keys, s_w[threadIdx.x >> 5], s_k[threadIdx.x >> 5], &k)
+                  : kNone;
     const uint32_t* b = cnt <= 32 ? nullptr : big_bucket(rs, e, cnt);
     if constexpr (W == 0) {
       for (uint32_t j = 0; j < cnt; ++j) {
@@ -496,16 +543,17 @@ __global__ void __launch_bounds__(256)
         warp_replace_key(c, set, keys[ij], rows + uint64_t(ij) * c.d, stamp);
       }
     } else {
-      replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, b);
+      replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b);
     }
   }
   __syncwarp();
   if (lane_id() == 0) {
-    // the table is clean again for the next call
+    // the scratch is clean again for the next call
     rs.set1[e] = 0u;
     rs.cnt[e] = 0u;
     rs.ovf[e] = kNone;
     rs.boff[e] = kNone;
+    rs.lead_e[w] = kNone;
   }
 }
 

@@ -183,7 +183,14 @@ Workspace::~Workspace() {
     cudaEventSynchronize(done);
     cudaEventDestroy(done);
   }
+  if (uploaded) {
+    cudaEventSynchronize(uploaded);
+    cudaEventDestroy(uploaded);
+  }
   if (rows_ready) cudaEventDestroy(rows_ready);
+  if (counts_ready) cudaEventDestroy(counts_ready);
+  for (auto& e : chunk_ev)
+    if (e) cudaEventDestroy(e);
 }
 
 void Workspace::wait_idle() {
@@ -197,6 +204,12 @@ void Workspace::ensure(uint64_t n, uint32_t d, cudaStream_t st) {
   if (done == nullptr) HPSB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
   if (rows_ready == nullptr)
     HPSB_CUDA(cudaEventCreateWithFlags(&rows_ready, cudaEventDisableTiming));
+  if (counts_ready == nullptr)
+    HPSB_CUDA(cudaEventCreateWithFlags(&counts_ready, cudaEventDisableTiming));
+  if (uploaded == nullptr)
+    HPSB_CUDA(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
+  for (auto& e : chunk_ev)
+    if (e == nullptr) HPSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (n <= capacity && d == dim && dbuf.get() != nullptr) return;
   uint64_t cap = 1024;
   while (cap < n) cap <<= 1;
@@ -296,7 +309,8 @@ LookupEngine::LookupEngine(const std::string& table, uint32_t dim, DeviceCache* 
       cold_(cold),
       cold_ctx_(cold_ctx),
       cfg_(std::move(cfg)),
-      pool_(cfg_.workspace_pool_size, cache ? cache->device() : 0) {
+      pool_(cfg_.workspace_pool_size, cache ? cache->device() : 0),
+      copy_threads_(std::min(8u, std::max(1u, std::thread::hardware_concurrency()))) {
   if (table.empty()) throw invalid_argument("table name must not be empty");
   if (table.size() > 255) throw invalid_argument("table name exceeds 255 bytes: " + table);
   if (dim == 0) throw invalid_argument("table dimension must be positive: " + table);
@@ -310,6 +324,7 @@ LookupEngine::LookupEngine(const std::string& table, uint32_t dim, DeviceCache* 
   DeviceGuard g(cache->device());
   HPSB_CUDA(cudaMalloc(&d_default_, dim * 4));
   HPSB_CUDA(cudaMemcpy(d_default_, def.data(), dim * 4, cudaMemcpyHostToDevice));
+  HPSB_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
   for (uint32_t i = 0; i < cfg_.async_worker_count; ++i)
     workers_.emplace_back([this] { async_loop(); });
 }
@@ -323,6 +338,54 @@ LookupEngine::~LookupEngine() {
   for (auto& w : workers_) w.join();
   DeviceGuard g(cache_->device());
   cudaFree(d_default_);
+  if (copy_stream_) {
+    cudaStreamSynchronize(copy_stream_);
+    cudaStreamDestroy(copy_stream_);
+  }
+}
+
+void LookupEngine::rows_d2h(Workspace& ws, const LookupCall& c, cudaStream_t st) {
+  const uint64_t bytes = c.n * uint64_t(dim_) * 4;
+  if (c.out_pinned) {
+    ws.out_chunks = 0;
+    HPSB_CUDA(cudaMemcpyAsync(c.out, c.d_out, bytes, cudaMemcpyDeviceToHost, st));
+    return;
+  }
+  // ~2 MB chunks: the copy-on of chunk i runs while chunk i+1 crosses PCIe
+  const uint64_t nch = std::clamp<uint64_t>(bytes >> 21, 1, Workspace::kOutChunks);
+  const uint64_t per = (bytes / nch + 255) / 256 * 256;
+  ws.out_chunks = 0;
+  for (uint64_t off = 0; off < bytes; off += per) {
+    const uint64_t len = std::min(per, bytes - off);
+    HPSB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ws.h_out) + off,
+                              reinterpret_cast<const char*>(c.d_out) + off, len,
+                              cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaEventRecord(ws.chunk_ev[ws.out_chunks++], st));
+  }
+}
+
+void LookupEngine::rows_to_pageable(Workspace& ws, const LookupCall& c) {
+  const uint64_t bytes = c.n * uint64_t(dim_) * 4;
+  const int nch = ws.out_chunks;
+  if (nch == 0) return;
+  const uint64_t per = (bytes / uint64_t(nch) + 255) / 256 * 256;
+  auto copy_chunk = [&](size_t i) {
+    HPSB_CUDA(cudaEventSynchronize(ws.chunk_ev[i]));
+    const uint64_t off = i * per;
+    if (off >= bytes) return;
+    std::memcpy(reinterpret_cast<char*>(c.out) + off, reinterpret_cast<const char*>(ws.h_out) + off,
+                std::min(per, bytes - off));
+  };
+  if (nch == 1) {
+    copy_chunk(0);
+    return;
+  }
+  // thread t takes chunks t, t + T, ...: every thread starts on an early chunk
+  const size_t T = std::min<size_t>(copy_threads_.size(), size_t(nch));
+  copy_threads_.parallel_for(T, 1, [&](size_t tb, size_t te) {
+    for (size_t t = tb; t < te; ++t)
+      for (size_t i = t; i < size_t(nch); i += T) copy_chunk(i);
+  });
 }
 
 size_t LookupEngine::fetch_and_upload(Workspace& ws, const uint64_t* miss_keys, size_t n_miss,
@@ -475,14 +538,19 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
                                   cudaMemcpyDeviceToHost, st));
         HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts, ws->lv.list_firsts, c.spec_claims * 4,
                                   cudaMemcpyDeviceToHost, st));
+        // the host decides the branch as soon as the counts land; the rows
+        // copy on behind them
+        HPSB_CUDA(cudaEventRecord(ws->counts_ready, st));
         if (host && c.spec_rows) {
-          HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, c.d_out, n * uint64_t(d) * 4,
-                                    cudaMemcpyDeviceToHost, st));
           HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, c.d_flags, n,
                                     cudaMemcpyDeviceToHost, st));
+          rows_d2h(*ws, c, st);
         }
+      } else {
+        HPSB_CUDA(cudaEventRecord(ws->counts_ready, st));
       }
       HPSB_CUDA(cudaEventRecord(ws->done, st));
+      ws->pending = true;  // rows may still be crossing after the counts land
     }
   } catch (...) {
     pool_.release(ws);
@@ -514,18 +582,20 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   cudaStream_t st = cache_->stream();
   uint64_t uh = 0, um = 0;
   if (n > 0) {
-    HPSB_CUDA(cudaEventSynchronize(ws->done));
+    HPSB_CUDA(cudaEventSynchronize(ws->counts_ready));
     uh = c.hc[0];
     um = c.hc[1];
     if (um > c.spec_claims) {
+      // the rest of the claims, on the side stream (the kernel is done: the
+      // copy need not queue behind the speculative rows on the cache stream)
       HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_keys + c.spec_claims,
                                 ws->lv.list_keys + c.spec_claims, (um - c.spec_claims) * 8,
-                                cudaMemcpyDeviceToHost, st));
+                                cudaMemcpyDeviceToHost, copy_stream_));
       HPSB_CUDA(cudaMemcpyAsync(ws->h_claim_firsts + c.spec_claims,
                                 ws->lv.list_firsts + c.spec_claims, (um - c.spec_claims) * 4,
-                                cudaMemcpyDeviceToHost, st));
-      HPSB_CUDA(cudaEventRecord(ws->done, st));
-      HPSB_CUDA(cudaEventSynchronize(ws->done));
+                                cudaMemcpyDeviceToHost, copy_stream_));
+      HPSB_CUDA(cudaEventRecord(ws->uploaded, copy_stream_));
+      HPSB_CUDA(cudaEventSynchronize(ws->uploaded));
     }
     if (um > 0) {
       // the reference's miss order: unique misses by first occurrence
@@ -602,15 +672,15 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
       std::memcpy(flags, c.hfl, n);
     } else if (host) {
       if (sync_branch || !c.spec_rows) {
-        HPSB_CUDA(cudaMemcpyAsync(c.out_pinned ? out : ws->h_out, d_out, n * uint64_t(d) * 4,
-                                  cudaMemcpyDeviceToHost, st));
         HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
                                   cudaMemcpyDeviceToHost, st));
+        rows_d2h(*ws, c, st);
         HPSB_CUDA(cudaEventRecord(ws->done, st));
-        HPSB_CUDA(cudaEventSynchronize(ws->done));
       }
+      // pageable rows: copied on chunk by chunk as they land
+      if (!c.out_pinned) rows_to_pageable(*ws, c);
+      HPSB_CUDA(cudaEventSynchronize(ws->done));
       ws->pending = false;
-      if (!c.out_pinned) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
       if (!c.flags_pinned) std::memcpy(flags, ws->h_flags, n);
     } else {
       cache_->join_to(c.user);
@@ -971,6 +1041,17 @@ void LookupEngine::async_loop() {
       ws.wait_idle();
       size_t nf = 0;
       fetch_and_upload(ws, ws.missing_keys.data(), ws.missing_keys.size(), &counters, &nf);
+      if (nf > kZeroCopyReplaceMax) {
+        // the upload runs on the side stream and is waited for HERE, before
+        // the replace is enqueued: lookups queued on the cache stream in the
+        // meantime never wait behind the copy
+        HPSB_CUDA(cudaMemcpyAsync(ws.d_staged, ws.h_staged, nf * uint64_t(dim_) * 4,
+                                  cudaMemcpyHostToDevice, copy_stream_));
+        HPSB_CUDA(cudaMemcpyAsync(ws.d_found_keys, ws.h_found_keys, nf * 8,
+                                  cudaMemcpyHostToDevice, copy_stream_));
+        HPSB_CUDA(cudaEventRecord(ws.uploaded, copy_stream_));
+        HPSB_CUDA(cudaEventSynchronize(ws.uploaded));
+      }
       if (nf > 0) {
         std::lock_guard<std::mutex> lk(cache_->mutex());
         if (nf <= kZeroCopyReplaceMax) {
@@ -978,10 +1059,6 @@ void LookupEngine::async_loop() {
           // memory (no copies queued ahead of the next lookup on the stream)
           cache_->replace_device_locked(ws.h_found_keys, nf, ws.h_staged);
         } else {
-          HPSB_CUDA(cudaMemcpyAsync(ws.d_staged, ws.h_staged, nf * uint64_t(dim_) * 4,
-                                    cudaMemcpyHostToDevice, st));
-          HPSB_CUDA(cudaMemcpyAsync(ws.d_found_keys, ws.h_found_keys, nf * 8,
-                                    cudaMemcpyHostToDevice, st));
           cache_->replace_device_locked(ws.d_found_keys, nf, ws.d_staged);
         }
         HPSB_CUDA(cudaEventRecord(ws.done, st));

@@ -112,6 +112,14 @@ struct Workspace {
   std::vector<uint64_t> missing_keys;
   cudaEvent_t done = nullptr;
   cudaEvent_t rows_ready = nullptr;  // zero-copy sync branch: rows final (replace may run on)
+  cudaEvent_t counts_ready = nullptr;  // the lookup's counts and first claims are in host memory
+  cudaEvent_t uploaded = nullptr;      // async fill: staged rows copied to the device (copy stream)
+  // pageable output: the rows come back in chunks into h_out, one event per
+  // chunk, and are copied on to the caller's memory by several threads as
+  // each chunk lands
+  static constexpr int kOutChunks = 16;
+  cudaEvent_t chunk_ev[kOutChunks] = {};
+  int out_chunks = 0;
   bool pending = false;  // `done` recorded, not yet waited
 
   ~Workspace();
@@ -223,6 +231,12 @@ class LookupEngine {
   // and (optionally) scatter into the output + replace into the cache.
   size_t fetch_and_upload(Workspace& ws, const uint64_t* miss_keys, size_t n_miss,
                           TierCounters* counters, size_t* n_found);
+  // rows (n * dim floats at d_out) back to the host: straight into the
+  // caller's `out` when it is pinned, else chunked into ws.h_out
+  void rows_d2h(Workspace& ws, const LookupCall& c, cudaStream_t st);
+  // completes rows_d2h for a pageable `out`: waits chunk by chunk and copies
+  // each on to `out` over the copy threads
+  void rows_to_pageable(Workspace& ws, const LookupCall& c);
 
   std::string table_;
   uint32_t dim_;
@@ -233,6 +247,10 @@ class LookupEngine {
   EngineConfig cfg_;
   float* d_default_ = nullptr;
   WorkspacePool pool_;
+  // the miss path's side stream: background fills upload their staged rows
+  // here, so the copies never sit in front of a lookup on the cache stream
+  cudaStream_t copy_stream_ = nullptr;
+  ThreadPool copy_threads_;  // pageable-output copies
 
   mutable std::mutex stats_mu_;
   EngineStats stats_;

@@ -51,12 +51,14 @@ struct ReplaceScratch {
   uint32_t* set1 = nullptr;   // cap: slabset + 1 (0 = free)
   uint32_t* cnt = nullptr;    // cap: keys of the set in this call
   uint32_t* idx = nullptr;    // cap * kReplaceInline: key indices, arrival order
+  uint64_t* kin = nullptr;    // cap * kReplaceInline: the keys themselves
   uint32_t* ovf = nullptr;    // cap: overflow list head (~0 = none)
   uint32_t* boff = nullptr;   // cap: sorted bucket of a set with > 32 keys (~0 = none)
   uint32_t* next = nullptr;   // ncap: overflow list links
-  uint32_t* entry = nullptr;  // ncap: key -> entry | kLeaderBit
+  uint32_t* lead_e = nullptr; // ncap: touched sets' table entries, compact (~0 = none)
+  uint32_t* lead_s = nullptr; // ncap: their slabsets
   uint32_t* bucket = nullptr; // ncap: buckets of sets with > 32 keys
-  uint32_t* cursor = nullptr; // [0] bucket cursor, [1] duplicate flag
+  uint32_t* cursor = nullptr; // [0] bucket cursor, [1] duplicate flag, [2] touched-set count
   uint32_t* dup_flag = nullptr;
 };
 // Bytes of a scratch for calls of up to n keys; carving; the one-time

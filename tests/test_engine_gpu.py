@@ -636,3 +636,71 @@ def test_max_batch_is_enforced():
     unlimited = hps.LookupEngine(fx.table, fx.cache, None, fx.pdb, hps.EngineConfig())
     assert unlimited.lookup(np.arange(5000, dtype=np.uint64) % 200).vectors.size == 5000 * 2
     unlimited.close()
+
+
+@pytest.mark.parametrize("threshold", [0.5, 0.95])
+def test_large_pageable_batches_lockstep_with_engine_oracle(threshold):
+    """Batches whose rows come back through the chunked staging + parallel
+    copy-on (pageable numpy output, 40,000 x 64 floats = 10 MB, 5 chunks),
+    both branches, in lock-step with the engine oracle."""
+    d, S = 64, 512
+    eo = oracle.EngineOracle(S, 2, d, threshold=threshold, default_vector=[0.5])
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vk = np.arange(0, 60000, 3, dtype=np.uint64)
+    vv = row_values(vk, d, 5)
+    vdb.insert("t", vk, vv)
+    for k, r in zip(vk, vv.reshape(-1, d)):
+        eo.vdb[int(k)] = r
+    c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
+    eng = hps.LookupEngine(table, c, vdb, None,
+                           hps.EngineConfig(hit_rate_threshold=threshold, default_vector=[0.5]))
+    stream = workload.powerlaw_sample(1.05, 60000, 3, 4, 6 * 40000)
+    branches = set()
+    for b in range(6):
+        keys = stream[b * 40000:(b + 1) * 40000]
+        o = hps.LookupOutcome()
+        r = eng.lookup(keys, o)
+        eng.drain_async()
+        out, flags, oc = eo.lookup(keys)
+        eo.drain_async()
+        branches.add(o.sync_branch)
+        assert o.__dict__ == oc
+        assert r.vectors.tobytes() == out.tobytes()
+        assert (r.miss_flags == flags).all()
+    assert eng.stats().__dict__ == eo.stats
+    c.check_invariants()
+
+
+def test_async_fills_on_the_side_stream_interleave_with_lookups():
+    """Back-to-back large lookups with background fills in flight (their
+    uploads on the engine's copy stream, replaces enqueued after): every
+    unflagged row is the stored row, every flagged row the default, and the
+    cache ends consistent with every fetched key resident or evicted."""
+    d, S = 128, 1024
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vk = np.arange(200000, dtype=np.uint64)
+    vv = row_values(vk, d, 9)
+    vdb.insert("t", vk, vv)
+    vv = vv.reshape(-1, d)
+    c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
+    eng = hps.LookupEngine(table, c, vdb, None,
+                           hps.EngineConfig(hit_rate_threshold=0.0, default_vector=[-2.0]))
+    stream = workload.powerlaw_sample(1.1, 200000, 11, 12, 12 * 32768)
+    for b in range(12):
+        keys = stream[b * 32768:(b + 1) * 32768]
+        o = hps.LookupOutcome()
+        r = eng.lookup(keys, o)
+        assert not o.sync_branch
+        got = r.vectors.reshape(-1, d)
+        hit = r.miss_flags == 0
+        assert (got[hit] == vv[keys[hit].astype(np.int64)]).all()
+        dv = np.zeros(d, np.float32)
+        dv[0] = -2.0  # the default vector, zero-padded to the dimension
+        assert (got[~hit] == dv).all()
+    eng.drain_async()
+    c.check_invariants()
+    assert eng.stats().async_faults == 0

@@ -21,6 +21,7 @@ import pytest
 import bench
 import oracle
 import paper_2210_08804_b200 as hps
+from tools import workload
 
 pytestmark = pytest.mark.gpu
 
@@ -96,7 +97,7 @@ def test_captured_graph_replays_like_reissued_lookups(own_stream):
     o.replace(keys, v)
     default = np.full(d, 0.5, np.float32)
     dr = torch.from_numpy(default).cuda()
-    qs = [hps.powerlaw_sample(1.2, 100000, 3, 40 + b, n) for b in range(K)]
+    qs = [workload.powerlaw_sample(1.2, 100000, 3, 40 + b, n) for b in range(K)]
     qt = [torch.from_numpy(q.view(np.int64)).cuda() for q in qs]
     b = Bufs(torch, K, n, d)
     user = torch.cuda.Stream()
@@ -110,7 +111,7 @@ def test_captured_graph_replays_like_reissued_lookups(own_stream):
             b.issue(c, j, qt[j], n, dr, sp)
     # the capture itself consumed no clock ticks
     assert c.recency_clock() == o.clock()
-    extra = hps.powerlaw_sample(1.2, 100000, 9, 9, n)
+    extra = workload.powerlaw_sample(1.2, 100000, 9, 9, n)
     et = torch.from_numpy(extra.view(np.int64)).cuda()
     hits = []
     for rep in range(3):
@@ -207,7 +208,7 @@ def test_cfg5_scale_geometry_pipelined_lookups():
     assert c.occupied() == o.occupied()
     qs = []
     for j in range(K):
-        idx = hps.powerlaw_sample(1.2, len(pre), 11, 100 + j, n).astype(np.int64)
+        idx = workload.powerlaw_sample(1.2, len(pre), 11, 100 + j, n).astype(np.int64)
         q = pre[idx]
         absent = rng.random(n) < 0.3
         q[absent] = rng.integers(1_000_000_000, 2_000_000_000, int(absent.sum()), dtype=np.uint64)
