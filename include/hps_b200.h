@@ -50,6 +50,7 @@ typedef struct hps_cache hps_cache;
 typedef struct hps_vdb hps_vdb;
 typedef struct hps_engine hps_engine;
 typedef struct hps_multi hps_multi;
+typedef struct hps_pdb hps_pdb;
 
 /* ---- vocabulary ------------------------------------------------------- */
 
@@ -273,6 +274,37 @@ typedef int (*hps_cold_fetch_fn)(void* ctx, const uint64_t* keys, size_t n,
                                  uint64_t* found_keys, float* found_vectors,
                                  size_t* n_found, uint64_t* missing_keys,
                                  size_t* n_missing);
+
+/* ---- batched cold reads over the reference's persistent store files
+ *      (replaces PersistentStore::get,
+ *      persistent_store.cpp:405-439, one pread per key, for the read path).
+ *      A read-only reader of <root>/<escaped table>/{MANIFEST, seg-<n>.log}
+ *      (persistent_store.hpp:5-15): the newest-record-wins index is rebuilt
+ *      as the reference's open does (persistent_store.cpp:229-268), the
+ *      segments are memory-mapped, and a batch's probes and row copies fan
+ *      out over `threads` host threads (0 = all cores). Records still in the
+ *      writer's unflushed tail are invisible until flushed + refreshed. ---- */
+int hps_pdb_open(const char* root, uint32_t threads, hps_pdb** out);
+int hps_pdb_destroy(hps_pdb* pdb);
+/* indexes the table (HPS_INVALID_ARGUMENT "persistent store has no table
+ * named <t>" when absent; HPS_TIER_FAULT for a malformed MANIFEST) */
+int hps_pdb_attach(hps_pdb* pdb, const char* table);
+/* picks up flushed appends, new segments and compactions */
+int hps_pdb_refresh(hps_pdb* pdb, const char* table);
+int hps_pdb_info(hps_pdb* pdb, const char* table, uint32_t* dimension, uint64_t* keys,
+                 uint64_t* segments);
+/* PersistentStore::get: found keys / rows and missing keys in input order;
+ * each output holds n entries (rows: n * dim) */
+int hps_pdb_get(hps_pdb* pdb, const char* table, const uint64_t* keys, size_t n,
+                uint64_t* found_keys, float* found_vectors, size_t* n_found,
+                uint64_t* missing_keys, size_t* n_missing);
+/* the engine's cold tier over one table: pass hps_pdb_cold_fetch as `cold`
+ * and the context from hps_pdb_table_ctx (attaches the table; owned by pdb)
+ * as `cold_ctx` to hps_engine_create / hps_tier_fetch / hps_refresh_cache */
+int hps_pdb_table_ctx(hps_pdb* pdb, const char* table, void** ctx);
+int hps_pdb_cold_fetch(void* ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
+                       float* found_vectors, size_t* n_found, uint64_t* missing_keys,
+                       size_t* n_missing);
 
 /* replaces hps::tier_fetch (lookup_engine.cpp:50-89): VDB first (if vdb and
  * the table are present), then the cold tier for the rest; cold hits are

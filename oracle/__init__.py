@@ -109,6 +109,18 @@ def rlib() -> C.CDLL:
         l.ref_last_error.restype = C.c_char_p
         l.ref_wire_lookup_frame.restype = _SZ
         l.ref_wire_lookup_frame.argtypes = [_P, _P, C.c_uint32, C.c_uint32, _P, _SZ]
+        l.ref_pdb_open.argtypes = [C.c_char_p, C.POINTER(_P)]
+        l.ref_pdb_destroy.argtypes = [_P]
+        l.ref_pdb_create_table.argtypes = [_P, C.c_char_p, C.c_uint32]
+        l.ref_pdb_put.argtypes = [_P, C.c_char_p, _P, _SZ, _P]
+        l.ref_pdb_flush.argtypes = [_P, C.c_char_p]
+        l.ref_pdb_compact.argtypes = [_P, C.c_char_p]
+        l.ref_pdb_get.argtypes = [_P, C.c_char_p, _P, _SZ, _P, _P, C.POINTER(_SZ), _P,
+                                  C.POINTER(_SZ)]
+        l.ref_pdb_segment_count.restype = _SZ
+        l.ref_pdb_segment_count.argtypes = [_P, C.c_char_p]
+        l.ref_pdb_key_count.restype = _SZ
+        l.ref_pdb_key_count.argtypes = [_P, C.c_char_p]
         l.ref_xxh64.restype = C.c_uint64
         l.ref_xxh64.argtypes = [_P, _SZ, C.c_uint64]
         l.ref_xxh64_key.restype = C.c_uint64
@@ -554,3 +566,50 @@ def ref_dedup(keys):
     inv = np.empty(max(len(k), 1), dtype=np.uint32)
     n = rlib().ref_dedup(_p(k), len(k), _p(u), _p(inv))
     return u[:n].copy(), inv[: len(k)].copy()
+
+
+class RefPersistentStore:
+    """The reference's own hps::PersistentStore (oracle/_ref) -- the writer of
+    the segment files and the parity partner of the native batched reader."""
+
+    def __init__(self, root):
+        self._h = C.c_void_p()
+        _rcheck(rlib().ref_pdb_open(str(root).encode(), C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            rlib().ref_pdb_destroy(self._h)
+            self._h = None
+
+    def create_table(self, name, dim):
+        _rcheck(rlib().ref_pdb_create_table(self._h, name.encode(), dim))
+        self.dims = getattr(self, "dims", {})
+        self.dims[name] = dim
+
+    def put(self, name, keys, rows):
+        k = np.ascontiguousarray(keys, dtype=np.uint64)
+        v = np.ascontiguousarray(rows, dtype=np.float32)
+        _rcheck(rlib().ref_pdb_put(self._h, name.encode(), k.ctypes.data, len(k), v.ctypes.data))
+
+    def flush(self, name):
+        _rcheck(rlib().ref_pdb_flush(self._h, name.encode()))
+
+    def compact(self, name):
+        _rcheck(rlib().ref_pdb_compact(self._h, name.encode()))
+
+    def segment_count(self, name):
+        return rlib().ref_pdb_segment_count(self._h, name.encode())
+
+    def key_count(self, name):
+        return rlib().ref_pdb_key_count(self._h, name.encode())
+
+    def get(self, name, keys, dim):
+        k = np.ascontiguousarray(keys, dtype=np.uint64)
+        n = len(k)
+        fk = np.empty(max(n, 1), np.uint64)
+        fv = np.empty(max(n, 1) * dim, np.float32)
+        mk = np.empty(max(n, 1), np.uint64)
+        nf, nm = _SZ(0), _SZ(0)
+        _rcheck(rlib().ref_pdb_get(self._h, name.encode(), k.ctypes.data, n, fk.ctypes.data,
+                                   fv.ctypes.data, C.byref(nf), mk.ctypes.data, C.byref(nm)))
+        return fk[: nf.value].copy(), fv[: nf.value * dim].copy(), mk[: nm.value].copy()

@@ -15,6 +15,7 @@
 //   hps::PowerLawSampler      core/src/workload.cpp:24-70
 //   hps::VolatileStore        core/include/hps/volatile_store.hpp:45-137
 //   hps::LookupEngine         core/include/hps/lookup_engine.hpp:152-196
+//   hps::PersistentStore      core/include/hps/persistent_store.hpp:39-95
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
@@ -298,6 +299,45 @@ size_t ref_wire_lookup_frame(const float* rows, const uint8_t* flags, uint32_t c
   const auto f = hps::encode_response_frame(hps::Opcode::Lookup, resp);
   std::memcpy(out, f.data(), std::min(cap, f.size()));
   return f.size();
+}
+
+// ---- PersistentStore (the f4 row's parity partner) ----
+int ref_pdb_open(const char* root, void** out) {
+  return guard([&] { *out = new hps::PersistentStore(root); });
+}
+void ref_pdb_destroy(void* p) { delete static_cast<hps::PersistentStore*>(p); }
+int ref_pdb_create_table(void* p, const char* name, uint32_t dim) {
+  return guard([&] { static_cast<hps::PersistentStore*>(p)->create_table({name, dim}); });
+}
+int ref_pdb_put(void* p, const char* name, const uint64_t* keys, size_t n, const float* v) {
+  return guard([&] {
+    auto* s = static_cast<hps::PersistentStore*>(p);
+    const uint32_t d = s->table(name).dimension;
+    s->put(name, std::span<const uint64_t>(keys, n), std::span<const float>(v, n * d));
+  });
+}
+int ref_pdb_flush(void* p, const char* name) {
+  return guard([&] { static_cast<hps::PersistentStore*>(p)->flush(name); });
+}
+int ref_pdb_compact(void* p, const char* name) {
+  return guard([&] { static_cast<hps::PersistentStore*>(p)->compact(name); });
+}
+int ref_pdb_get(void* p, const char* name, const uint64_t* keys, size_t n, uint64_t* fk,
+                float* fv, size_t* nf, uint64_t* mk, size_t* nm) {
+  return guard([&] {
+    auto r = static_cast<hps::PersistentStore*>(p)->get(name, std::span<const uint64_t>(keys, n));
+    std::copy(r.found_keys.begin(), r.found_keys.end(), fk);
+    std::copy(r.found_vectors.begin(), r.found_vectors.end(), fv);
+    std::copy(r.missing_keys.begin(), r.missing_keys.end(), mk);
+    *nf = r.found_keys.size();
+    *nm = r.missing_keys.size();
+  });
+}
+size_t ref_pdb_segment_count(void* p, const char* name) {
+  return static_cast<hps::PersistentStore*>(p)->segment_count(name);
+}
+size_t ref_pdb_key_count(void* p, const char* name) {
+  return static_cast<hps::PersistentStore*>(p)->key_count(name);
 }
 
 }  // extern "C"

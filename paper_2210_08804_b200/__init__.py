@@ -179,6 +179,14 @@ SIGNATURES = {
     "hps_vdb_last_access": (C.c_int, [_P, C.c_char_p, C.c_uint64, _U64P, C.POINTER(C.c_int)]),
     "hps_vdb_evict": (C.c_int, [_P, C.c_char_p, C.c_uint32, _P, C.c_size_t, _SZP]),
     "hps_vdb_last_evicted": (C.c_int, [_P, C.c_size_t, _SZP]),
+    "hps_pdb_open": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(_P)]),
+    "hps_pdb_destroy": (C.c_int, [_P]),
+    "hps_pdb_attach": (C.c_int, [_P, C.c_char_p]),
+    "hps_pdb_refresh": (C.c_int, [_P, C.c_char_p]),
+    "hps_pdb_info": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_uint32), _U64P, _U64P]),
+    "hps_pdb_get": (C.c_int, [_P, C.c_char_p, _P, C.c_size_t, _P, _P, _SZP, _P, _SZP]),
+    "hps_pdb_table_ctx": (C.c_int, [_P, C.c_char_p, C.POINTER(_P)]),
+    "hps_pdb_cold_fetch": (C.c_int, [_P, _P, C.c_size_t, _P, _P, _SZP, _P, _SZP]),
     "hps_vdb_dimension": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_uint32)]),
     "hps_vdb_partition_count": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_uint32)]),
     "hps_vdb_keys": (C.c_int, [_P, C.c_char_p, _P, C.c_size_t, _SZP]),
@@ -726,6 +734,92 @@ class ColdTier:
         self.fn = COLD_FETCH_FN(_cb)
 
 
+class SegmentStore:
+    """Batched cold reads over the reference's persistent-store files
+    (hps_pdb_*): <root>/<escaped table>/{MANIFEST,
+    seg-<n>.log} indexed the way PersistentStore's open does
+    (persistent_store.cpp:229-268), memory-mapped, a batch's probes and row
+    copies spread over host threads -- in place of PersistentStore::get's one
+    pread per key (persistent_store.cpp:405-439). Read-only."""
+
+    def __init__(self, root, threads: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().hps_pdb_open(str(root).encode(), threads, C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hps_pdb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def attach(self, name: str) -> None:
+        _check(lib().hps_pdb_attach(self._h, name.encode()))
+
+    def refresh(self, name: str) -> None:
+        _check(lib().hps_pdb_refresh(self._h, name.encode()))
+
+    def _info(self, name: str):
+        d, k, sg = C.c_uint32(0), C.c_uint64(0), C.c_uint64(0)
+        _check(lib().hps_pdb_info(self._h, name.encode(), C.byref(d), C.byref(k), C.byref(sg)))
+        return d.value, k.value, sg.value
+
+    def dimension(self, name: str) -> int:
+        return self._info(name)[0]
+
+    def key_count(self, name: str) -> int:
+        return self._info(name)[1]
+
+    def segment_count(self, name: str) -> int:
+        return self._info(name)[2]
+
+    def get(self, name: str, keys) -> FetchResult:
+        k = _u64(keys)
+        n = len(k)
+        d = self.dimension(name)
+        fk = np.empty(max(n, 1), dtype=np.uint64)
+        fv = np.empty(max(n, 1) * d, dtype=np.float32)
+        mk = np.empty(max(n, 1), dtype=np.uint64)
+        nf, nm = C.c_size_t(0), C.c_size_t(0)
+        _check(lib().hps_pdb_get(self._h, name.encode(), _ptr(k), n, _ptr(fk), _ptr(fv),
+                                 C.byref(nf), _ptr(mk), C.byref(nm)))
+        return FetchResult(fk[: nf.value].copy(), fv[: nf.value * d].copy(), mk[: nm.value].copy())
+
+    def table(self, name: str) -> "SegmentTable":
+        return SegmentTable(self, name)
+
+
+class SegmentTable:
+    """One table of a SegmentStore as an engine cold tier: passed as `pdb`
+    to LookupEngine / tier_fetch / refresh_cache it is called NATIVELY
+    (hps_pdb_cold_fetch), no Python callback on the miss path."""
+
+    def __init__(self, store: SegmentStore, name: str):
+        self.store = store
+        self.name = name
+        self.ctx = C.c_void_p()
+        _check(lib().hps_pdb_table_ctx(store._h, name.encode(), C.byref(self.ctx)))
+        self.fn = C.cast(lib().hps_pdb_cold_fetch, COLD_FETCH_FN)
+
+    def get(self, keys) -> FetchResult:
+        return self.store.get(self.name, keys)
+
+
+def _cold(pdb, dim):
+    """(callback, ctx, keep-alive) of a cold tier: native for a SegmentTable,
+    a ctypes adapter for any object with get(keys) -> FetchResult."""
+    if pdb is None:
+        return _NULL_COLD, None, None
+    if isinstance(pdb, SegmentTable):
+        return pdb.fn, pdb.ctx, pdb
+    ct = ColdTier(pdb, dim)
+    return ct.fn, None, ct
+
+
 class DictStore:
     """Minimal in-memory cold tier with the PersistentStore::get contract
     (found keys / rows and missing keys in input order)."""
@@ -762,14 +856,14 @@ def tier_fetch(table: TableId, keys, vdb: Optional[VolatileStore], pdb=None,
     k = _u64(keys)
     n = len(k)
     d = table.dimension
-    cold = ColdTier(pdb, d) if pdb is not None else None
+    cfn, cctx, _keep = _cold(pdb, d)
     fk = np.empty(max(n, 1), dtype=np.uint64)
     fv = np.empty(max(n, 1) * d, dtype=np.float32)
     mk = np.empty(max(n, 1), dtype=np.uint64)
     nf, nm = C.c_size_t(0), C.c_size_t(0)
     cnt = np.zeros(3, dtype=np.uint64)
     _check(lib().hps_tier_fetch(vdb.handle if vdb else None, table.name.encode(), d,
-                                cold.fn if cold else _NULL_COLD, None, _ptr(k), n, _ptr(fk),
+                                cfn, cctx, _ptr(k), n, _ptr(fk),
                                 _ptr(fv), C.byref(nf), _ptr(mk), C.byref(nm), _ptr(cnt)))
     if counters is not None:
         counters["vdb_hits"] = counters.get("vdb_hits", 0) + int(cnt[0])
@@ -790,13 +884,13 @@ def refresh_cache(cache: "SlabCache", table: TableId, vdb: Optional[VolatileStor
     """refresh_engine.cpp:5-22 on the B200 cache (hps_refresh_cache): dump,
     tier fetch (VDB, then pdb), non-admitting update; the host fetch of one
     batch overlaps the device update of the previous one."""
-    cold = ColdTier(pdb, table.dimension) if pdb is not None else None
+    cfn, cctx, _keep = _cold(pdb, table.dimension)
     cap = cache.capacity()
     un = np.empty(max(cap, 1), dtype=np.uint64)
     refreshed = C.c_uint64(0)
     nu = C.c_size_t(0)
     _check(lib().hps_refresh_cache(cache.handle, vdb.handle if vdb else None,
-                                   table.name.encode(), cold.fn if cold else _NULL_COLD, None,
+                                   table.name.encode(), cfn, cctx,
                                    dump_batch_size, C.byref(refreshed), _ptr(un), cap,
                                    C.byref(nu)))
     return RefreshOutcome(int(refreshed.value), un[: nu.value].copy())
@@ -860,7 +954,7 @@ class LookupEngine:
         self.table = table
         self.cache = cache
         self.vdb = vdb
-        self._cold = ColdTier(pdb, table.dimension) if pdb is not None else None
+        cfn, cctx, self._cold = _cold(pdb, table.dimension)
         dv = _f32(list(config.default_vector))
         self._dv = dv
         cfg = _EngineConfig(float(config.hit_rate_threshold),
@@ -869,8 +963,7 @@ class LookupEngine:
                             1 if config.volatile_tier_enabled else 0, config.max_batch)
         _check(lib().hps_engine_create(table.name.encode(), table.dimension, cache.handle,
                                        vdb.handle if vdb else None,
-                                       self._cold.fn if self._cold else _NULL_COLD, None,
-                                       C.byref(cfg), C.byref(self._h)))
+                                       cfn, cctx, C.byref(cfg), C.byref(self._h)))
 
     def close(self):
         if getattr(self, "_h", None):

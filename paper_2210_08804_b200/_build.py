@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 
-SOURCES = ["cache_kernels.cu", "lookup_kernels.cu", "shard_kernels.cu", "wire.cu", "device_cache.cpp", "volatile_store.cpp",
+SOURCES = ["cache_kernels.cu", "lookup_kernels.cu", "shard_kernels.cu", "wire.cu", "device_cache.cpp", "volatile_store.cpp", "segment_store.cpp",
            "engine.cpp", "capi.cpp"]
 
 

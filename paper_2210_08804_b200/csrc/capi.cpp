@@ -12,6 +12,7 @@
 
 #include "device_cache.hpp"
 #include "engine.hpp"
+#include "segment_store.hpp"
 #include "volatile_store.hpp"
 
 struct hps_cache {
@@ -19,6 +20,12 @@ struct hps_cache {
 };
 struct hps_vdb {
   std::unique_ptr<hpsb::VolatileStore> impl;
+};
+struct hps_pdb {
+  std::unique_ptr<hpsb::SegmentStore> impl;
+  std::mutex mu;
+  // cold-callback contexts handed out by hps_pdb_table_ctx (stable addresses)
+  std::map<std::string, std::unique_ptr<std::pair<hps_pdb*, std::string>>> ctx;
 };
 struct hps_engine {
   std::unique_ptr<hpsb::LookupEngine> impl;
@@ -676,6 +683,66 @@ int hps_vdb_keys(hps_vdb* vdb, const char* name, uint64_t* out, size_t cap, size
     if (out) std::copy(k.begin(), k.begin() + std::min(k.size(), cap), out);
     *n = k.size();
   });
+}
+
+// ------------------------------------------------------------- cold tier --
+int hps_pdb_open(const char* root, uint32_t threads, hps_pdb** out) {
+  return guarded([&] {
+    need(root && out, "null argument");
+    auto h = std::make_unique<hps_pdb>();
+    h->impl = std::make_unique<hpsb::SegmentStore>(root, threads);
+    *out = h.release();
+  });
+}
+int hps_pdb_destroy(hps_pdb* pdb) {
+  return guarded([&] { delete pdb; });
+}
+int hps_pdb_attach(hps_pdb* pdb, const char* table) {
+  return guarded([&] {
+    need(pdb && table, "null argument");
+    pdb->impl->attach(table);
+  });
+}
+int hps_pdb_refresh(hps_pdb* pdb, const char* table) {
+  return guarded([&] {
+    need(pdb && table, "null argument");
+    pdb->impl->refresh(table);
+  });
+}
+int hps_pdb_info(hps_pdb* pdb, const char* table, uint32_t* dimension, uint64_t* keys,
+                 uint64_t* segments) {
+  return guarded([&] {
+    need(pdb && table, "null argument");
+    if (dimension) *dimension = pdb->impl->dimension(table);
+    if (keys) *keys = pdb->impl->key_count(table);
+    if (segments) *segments = pdb->impl->segment_count(table);
+  });
+}
+int hps_pdb_get(hps_pdb* pdb, const char* table, const uint64_t* keys, size_t n,
+                uint64_t* found_keys, float* found_vectors, size_t* n_found,
+                uint64_t* missing_keys, size_t* n_missing) {
+  return guarded([&] {
+    need(pdb && table && n_found && n_missing, "null argument");
+    pdb->impl->get(table, keys, n, found_keys, found_vectors, nullptr, n_found, missing_keys,
+                   n_missing);
+  });
+}
+int hps_pdb_table_ctx(hps_pdb* pdb, const char* table, void** ctx) {
+  return guarded([&] {
+    need(pdb && table && ctx, "null argument");
+    pdb->impl->attach(table);
+    std::lock_guard<std::mutex> lk(pdb->mu);
+    auto& c = pdb->ctx[table];
+    if (!c) c = std::make_unique<std::pair<hps_pdb*, std::string>>(pdb, table);
+    *ctx = c.get();
+  });
+}
+int hps_pdb_cold_fetch(void* ctx, const uint64_t* keys, size_t n, uint64_t* found_keys,
+                       float* found_vectors, size_t* n_found, uint64_t* missing_keys,
+                       size_t* n_missing) {
+  auto* c = static_cast<std::pair<hps_pdb*, std::string>*>(ctx);
+  return hps_pdb_get(c->first, c->second.c_str(), keys, n, found_keys, found_vectors, n_found,
+                     missing_keys, n_missing);
 }
 
 int hps_tier_fetch(hps_vdb* vdb, const char* table, uint32_t dimension, hps_cold_fetch_fn cold,
