@@ -643,6 +643,7 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=Fal
     eng = hps.LookupEngine(table, cache, vdb, None,
                            hps.EngineConfig(hit_rate_threshold=threshold, workspace_pool_size=16,
                                             async_worker_count=2))
+    eng.reserve(n)  # serving setup: every workspace allocated before traffic
     ring = 4
     if pageable:
         pk = [np.ascontiguousarray(b) for b in batches]

@@ -224,6 +224,10 @@ class LookupEngine {
 
   void drain_async() { b200_detail::check(hps_engine_drain_async(h_)); }
 
+  // B200 extension: allocate every workspace for batches of up to max_keys
+  // now (pinned staging included), so no lookup pays a first-use allocation.
+  void reserve(std::size_t max_keys) { b200_detail::check(hps_engine_reserve(h_, max_keys)); }
+
   EngineStatsSnapshot stats() const {
     hps_engine_stats s{};
     b200_detail::check(hps_engine_get_stats(h_, &s));

@@ -391,6 +391,11 @@ int hps_multi_destroy(hps_multi* multi);
 int hps_multi_lookup(hps_multi* multi, const uint64_t* const* keys, const size_t* n,
                      float* const* out, uint8_t* const* miss_flags, hps_lookup_outcome* outcomes);
 
+/* B200 extension: allocates every workspace (device + pinned staging) and
+ * the cache's replace scratch for batches of up to max_keys now, so no lookup
+ * pays a first-use allocation (also done at creation when
+ * hps_engine_config.max_batch is set). Call before serving. */
+int hps_engine_reserve(hps_engine* engine, size_t max_keys);
 /* replaces drain_async (lookup_engine.cpp:286-289) */
 int hps_engine_drain_async(hps_engine* engine);
 /* replaces stats (lookup_engine.cpp:291-294) */

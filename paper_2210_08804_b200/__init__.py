@@ -199,6 +199,7 @@ SIGNATURES = {
                                     C.c_int, _P]),
     "hps_engine_drain_async": (C.c_int, [_P]),
     "hps_engine_get_stats": (C.c_int, [_P, C.POINTER(_Stats)]),
+    "hps_engine_reserve": (C.c_int, [_P, C.c_size_t]),
     "hps_engine_pool_info": (C.c_int, [_P, _U64P, _U64P, _U64P]),
 }
 
@@ -1017,6 +1018,10 @@ class LookupEngine:
 
     def drain_async(self) -> None:
         _check(lib().hps_engine_drain_async(self._h))
+
+    def reserve(self, max_keys: int) -> None:
+        """Allocate every workspace for batches of up to max_keys now."""
+        _check(lib().hps_engine_reserve(self._h, max_keys))
 
     def stats(self) -> EngineStatsSnapshot:
         s = _Stats()

@@ -138,14 +138,17 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
 // (slab_cache.cpp:131-142: keys grouped by slabset, input order inside a
 // group) in two launches and no memsets (batches above kSmallReplaceMax):
 //   k_replace_bin    one thread per key: slabset, the set's entry in a
-//                    per-call table (CAS on the set id), the key's index and
-//                    the key itself appended there (atomicAdd rank); the
-//                    rank-0 key publishes (entry, set) into a compact list of
-//                    touched sets (one warp-aggregated add per warp)
+//                    per-call table (one 64-bit word: set id | key count; the
+//                    CAS that claims it ranks the first key, an add ranks the
+//                    rest), the key's index and the key itself appended there;
+//                    the rank-0 key publishes (entry, set) into a compact list
+//                    of touched sets (one warp-aggregated add per warp)
 //   [k_replace_dups] (validated calls) a warp per touched set compares its
 //                    keys: any duplicate rejects the whole call before mutation
-//   k_replace_sets   a warp per TOUCHED SET (the compact list; warps past its
-//                    end exit on the list's sentinel): the set's masks, keys
+//   k_replace_sets   persistent warps over the compact list of TOUCHED SETS
+//                    (each warp walks it with a stride, the next item's list
+//                    entry in flight while the current one is applied; the
+//                    walk ends on the list's sentinel): the set's masks, keys
 //                    and counters loaded ONCE into registers (lane j holds slot
 //                    j of every slab) together with the set's key indices and
 //                    keys, the indices sorted into input order, the first rows
@@ -155,11 +158,10 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
 //                    argmin counter (ties to the lowest (slab, slot)); only the
 //                    changed words are stored; the set's table entry and list
 //                    slot are cleared (the scratch is clean again). Dependent
-//                    round trips per set: list -> (set state, indices, keys)
-//                    -> rows.
+//                    round trips per set: (set state, indices, keys) -> rows.
 size_t replace_scratch_bytes(uint64_t n) {
   const uint64_t cap = pow2_at_least(2 * n);
-  return align_up(cap * 4, 256) * 4 + align_up(cap * 4 * kReplaceInline, 256) +
+  return align_up(cap * 8, 256) + align_up(cap * 4, 256) * 2 + align_up(cap * 4 * kReplaceInline, 256) +
          align_up(cap * 8 * kReplaceInline, 256) + align_up(n * 4, 256) * 4 + 256;
 }
 
@@ -174,8 +176,7 @@ ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
     return q;
   };
   // zero-initialised part first, then the all-ones part (two memsets once)
-  r.set1 = take(r.cap * 4);
-  r.cnt = take(r.cap * 4);
+  r.ent = reinterpret_cast<unsigned long long*>(take(r.cap * 8));
   r.cursor = take(256);
   r.dup_flag = r.cursor + 1;
   r.ovf = take(r.cap * 4);
@@ -190,14 +191,25 @@ ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
 }
 
 void replace_scratch_init(const ReplaceScratch& rs, cudaStream_t st) {
-  const char* z0 = reinterpret_cast<const char*>(rs.set1);
+  const char* z0 = reinterpret_cast<const char*>(rs.ent);
   const char* o0 = reinterpret_cast<const char*>(rs.ovf);
   const char* o1 = reinterpret_cast<const char*>(rs.idx);
-  cudaMemsetAsync(rs.set1, 0, size_t(o0 - z0), st);
+  cudaMemsetAsync(rs.ent, 0, size_t(o0 - z0), st);
   cudaMemsetAsync(rs.ovf, 0xFF, size_t(o1 - o0), st);
 }
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// The set kernel's register cap (4 blocks of 256 per SM: 32 warps) and the
+// rows it prefetches into registers per set. A/B on B200 (profiles/
+// r02_ab_replace.txt): the cap is worth ~30 %; L2 prefetches of the input
+// rows / set state from the bin kernel were measured and dropped (no gain).
+#ifndef HPSB_REPL_MINB
+#define HPSB_REPL_MINB 4
+#endif
+#ifndef HPSB_REPL_KPRE
+#define HPSB_REPL_KPRE 2
+#endif
 
 __global__ void __launch_bounds__(256)
     k_replace_bin(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
@@ -207,18 +219,28 @@ __global__ void __launch_bounds__(256)
     rs.dup_flag[0] = 0u;
   }
   bool lead = false;
-  uint32_t e32 = 0, s1 = 0;
+  uint32_t e32 = 0;
+  uint64_t set = 0;
   if (i < n) {
     const uint64_t key = keys[i];
-    s1 = uint32_t(slabset_of(c, key)) + 1u;
+    // the row the set kernel will copy (if the key is inserted), toward L2
+    set = slabset_of(c, key);
+    const unsigned long long tag = (set + 1ull) << 32;
     const uint64_t mask = rs.cap - 1;
-    uint64_t e = fmix64(s1) & mask;
+    uint64_t e = fmix64(set + 1ull) & mask;
+    uint32_t r;
     while (true) {
-      const uint32_t old = atomicCAS(rs.set1 + e, 0u, s1);
-      if (old == 0u || old == s1) break;
+      const unsigned long long old = atomicCAS(rs.ent + e, 0ull, tag | 1ull);
+      if (old == 0ull) {
+        r = 0;
+        break;
+      }
+      if ((old >> 32) == (tag >> 32)) {
+        r = uint32_t(atomicAdd(rs.ent + e, 1ull));  // the low word: this key's rank
+        break;
+      }
       e = (e + 1) & mask;
     }
-    const uint32_t r = atomicAdd(rs.cnt + e, 1u);
     if (r < kReplaceInline) {
       rs.idx[e * kReplaceInline + r] = uint32_t(i);
       rs.kin[e * kReplaceInline + r] = key;
@@ -238,7 +260,7 @@ __global__ void __launch_bounds__(256)
   if (lead) {
     const uint32_t k = base + uint32_t(__popc(lm & ((1u << lane) - 1u)));
     rs.lead_e[k] = e32;
-    rs.lead_s[k] = s1 - 1u;
+    rs.lead_s[k] = uint32_t(set);
   }
 }
 
@@ -329,7 +351,7 @@ __global__ void __launch_bounds__(256)
   if (w >= n) return;
   const uint32_t e = rs.lead_e[w];
   if (e == kNone) return;
-  const uint32_t cnt = rs.cnt[e];
+  const uint32_t cnt = uint32_t(rs.ent[e]);
   if (cnt < 2) return;
   const uint32_t lane = lane_id();
   bool dup = false;
@@ -358,14 +380,15 @@ struct SetRegs {
   uint32_t m[W];
 };
 
+// Returns the number of keys inserted into free slots (lane 0's value).
 template <int W>
-__device__ __forceinline__ void replace_apply_set(const CacheDev& c, uint64_t set,
+__device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_t set,
                                                   const uint64_t* __restrict__ keys,
                                                   const float* __restrict__ rows, uint64_t stamp,
                                                   uint32_t cnt, uint32_t my_idx,
                                                   uint64_t my_key_in,
                                                   const uint32_t* __restrict__ big) {
-  constexpr int kPre = 4;  // rows prefetched (d <= 128, 16 B aligned)
+  constexpr int kPre = HPSB_REPL_KPRE;  // rows prefetched (d <= 128, 16 B aligned)
   const uint32_t lane = lane_id();
   const uint32_t d = c.d;
   const uint64_t sbase = set * W;
@@ -507,8 +530,8 @@ __device__ __forceinline__ void replace_apply_set(const CacheDev& c, uint64_t se
 #pragma unroll
     for (int w = 0; w < W; ++w)
       if (st.m[w] != m0[w]) c.masks[sbase + w] = st.m[w];
-    if (inserted) atomicAdd(c.occupied, (unsigned long long)inserted);
   }
+  return inserted;
 }
 
 __device__ __forceinline__ void warp_replace_key(const CacheDev& c, uint64_t set, uint64_t key,
@@ -516,45 +539,61 @@ __device__ __forceinline__ void warp_replace_key(const CacheDev& c, uint64_t set
 
 // W = 0: any slab count, the set re-read for every key (warp_replace_key)
 template <int W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, HPSB_REPL_MINB)
     k_replace_sets(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                    const float* __restrict__ rows, uint64_t stamp, uint32_t validate,
                    ReplaceScratch rs) {
   __shared__ uint32_t s_w[8][32];
   __shared__ uint64_t s_k[8][32];
-  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  __shared__ unsigned long long s_ins;
+  if (threadIdx.x == 0) s_ins = 0ull;
+  __syncthreads();
+  const uint64_t stride = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   // the list is consumed through its sentinels; its count restarts here
   if (blockIdx.x == 0 && threadIdx.x == 0) rs.cursor[2] = 0u;
-  if (w >= n) return;
-  const uint32_t e = rs.lead_e[w];
-  if (e == kNone) return;
-  const uint64_t set = rs.lead_s[w];
-  const uint32_t cnt = rs.cnt[e];
   const bool rejected = validate && *reinterpret_cast<volatile uint32_t*>(rs.dup_flag) != 0u;
-  if (!rejected) {
-    uint64_t k = 0;
-    const uint32_t v =
-        cnt <= 32 ? small_group(rs, e, cnt, keys, s_w[threadIdx.x >> 5], s_k[threadIdx.x >> 5], &k)
-                  : kNone;
-    const uint32_t* b = cnt <= 32 ? nullptr : big_bucket(rs, e, cnt);
-    if constexpr (W == 0) {
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const uint32_t ij = b ? b[j] : __shfl_sync(0xFFFFFFFFu, v, j);
-        warp_replace_key(c, set, keys[ij], rows + uint64_t(ij) * c.d, stamp);
+  uint32_t e = w < n ? rs.lead_e[w] : kNone;
+  uint32_t sset = w < n ? rs.lead_s[w] : 0u;
+  uint32_t inserted = 0;
+  while (e != kNone) {
+    // the next item's list entry is in flight while this one is applied
+    const uint64_t wn = w + stride;
+    const uint32_t en = wn < n ? rs.lead_e[wn] : kNone;
+    const uint32_t sn = wn < n ? rs.lead_s[wn] : 0u;
+    const uint64_t set = sset;
+    const uint32_t cnt = uint32_t(rs.ent[e]);
+    if (!rejected) {
+      uint64_t k = 0;
+      const uint32_t v = cnt <= 32 ? small_group(rs, e, cnt, keys, s_w[threadIdx.x >> 5],
+                                                 s_k[threadIdx.x >> 5], &k)
+                                   : kNone;
+      const uint32_t* b = cnt <= 32 ? nullptr : big_bucket(rs, e, cnt);
+      if constexpr (W == 0) {
+        for (uint32_t j = 0; j < cnt; ++j) {
+          const uint32_t ij = b ? b[j] : __shfl_sync(0xFFFFFFFFu, v, j);
+          warp_replace_key(c, set, keys[ij], rows + uint64_t(ij) * c.d, stamp);
+        }
+      } else {
+        inserted += replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b);
       }
-    } else {
-      replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b);
     }
+    __syncwarp();
+    if (lane_id() == 0) {
+      // the scratch is clean again for the next call
+      rs.ent[e] = 0ull;
+      rs.ovf[e] = kNone;
+      rs.boff[e] = kNone;
+      rs.lead_e[w] = kNone;
+    }
+    w = wn;
+    e = en;
+    sset = sn;
   }
-  __syncwarp();
-  if (lane_id() == 0) {
-    // the scratch is clean again for the next call
-    rs.set1[e] = 0u;
-    rs.cnt[e] = 0u;
-    rs.ovf[e] = kNone;
-    rs.boff[e] = kNone;
-    rs.lead_e[w] = kNone;
-  }
+  // occupancy: one atomic per block (W = 0 counts per key in warp_replace_key)
+  if (lane_id() == 0 && inserted) atomicAdd(&s_ins, (unsigned long long)inserted);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_ins) atomicAdd(c.occupied, s_ins);
 }
 
 // One key of a set, applied by a whole warp (slab_cache.cpp:261-326): ballot
@@ -807,7 +846,8 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
-                    uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st) {
+                    uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st,
+                    int device) {
   if (n == 0) return;
   static const bool no_small = std::getenv("HPSB_REPLACE_NO_SMALL") != nullptr;
   if (n <= kSmallReplaceMax && !no_small && !validate) {
@@ -825,12 +865,22 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
   k_replace_bin<<<unsigned((n + tb - 1) / tb), tb, 0, st>>>(c, keys, n, rs);
   const unsigned wgrid = unsigned((n * 32 + tb - 1) / tb);
   if (validate) k_replace_dups<<<wgrid, tb, 0, st>>>(keys, n, rs);
+  // persistent set kernel: as many blocks as fit on the device at once
+  // (fewer when the call touches fewer sets than that many warps)
+  auto grid_for = [&](const void* fn) {
+    static int sms = 0, per_sm[5] = {0, 0, 0, 0, 0};
+    const int wi = c.W <= 4 ? int(c.W) : 0;
+    if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (per_sm[wi] == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[wi], fn, tb, 0);
+    const uint64_t full = uint64_t(std::max(sms, 1)) * uint64_t(std::max(per_sm[wi], 1));
+    return unsigned(std::min<uint64_t>(full, wgrid));
+  };
   switch (c.W) {
-    case 1: k_replace_sets<1><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    case 2: k_replace_sets<2><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    case 3: k_replace_sets<3><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    case 4: k_replace_sets<4><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    default: k_replace_sets<0><<<wgrid, tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 1: k_replace_sets<1><<<grid_for((const void*)k_replace_sets<1>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 2: k_replace_sets<2><<<grid_for((const void*)k_replace_sets<2>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 3: k_replace_sets<3><<<grid_for((const void*)k_replace_sets<3>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 4: k_replace_sets<4><<<grid_for((const void*)k_replace_sets<4>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    default: k_replace_sets<0><<<grid_for((const void*)k_replace_sets<0>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
   }
   check_launch("replace", validate ? 3 : 2);
 }

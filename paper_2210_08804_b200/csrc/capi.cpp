@@ -880,6 +880,12 @@ int hps_multi_lookup(hps_multi* multi, const uint64_t* const* keys, const size_t
   });
 }
 
+int hps_engine_reserve(hps_engine* engine, size_t max_keys) {
+  return guarded([&] {
+    need(engine != nullptr, "null argument");
+    engine->impl->reserve(max_keys);
+  });
+}
 int hps_engine_drain_async(hps_engine* engine) {
   return guarded([&] { engine->impl->drain_async(); });
 }

@@ -528,7 +528,7 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
   } else {
     join_from(user);
   }
-  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/!host, rs, stream_);
+  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/!host, rs, stream_, device_);
   if (host) {
     HPSB_CUDA(cudaStreamSynchronize(stream_));
     return;
@@ -547,6 +547,12 @@ void DeviceCache::replace_device_async(const uint64_t* keys, size_t n, const flo
   join_from(user);
   replace_device_locked(keys, n, rows);
   join_to(user);
+}
+
+void DeviceCache::reserve_replace(uint64_t n) {
+  std::lock_guard<std::mutex> lk(mu_);
+  DeviceGuard g(device_);
+  replace_scratch_locked(n);
 }
 
 const ReplaceScratch& DeviceCache::replace_scratch_locked(uint64_t n) {
@@ -570,7 +576,7 @@ void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const 
   if (n == 0) return;
   const uint64_t stamp = clock_.load(std::memory_order_relaxed);
   const ReplaceScratch& rs = replace_scratch_locked(n);
-  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/false, rs, stream_);
+  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/false, rs, stream_, device_);
 }
 
 size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,

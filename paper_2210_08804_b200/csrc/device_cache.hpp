@@ -116,6 +116,8 @@ class DeviceCache {
 
   // ---- engine-facing primitives (caller holds mutex()) ----
   std::mutex& mutex() { return mu_; }
+  // grows the replace scratch for calls of up to n keys now (engine reserve)
+  void reserve_replace(uint64_t n);
   // Callers that enqueue their own work on stream() (the engine) call this
   // under mutex() so the next lookup does not chain onto a stale lookup.
   void note_stream_op() { mark_other_op(); }

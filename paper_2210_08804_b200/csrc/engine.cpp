@@ -4,6 +4,8 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -13,6 +15,32 @@ namespace hpsb {
 
 namespace {
 inline uint64_t a256(uint64_t v) { return (v + 255) / 256 * 256; }
+
+// HPSB_ENGINE_TRACE=1: per-phase host timeline of lookups slower than 2 ms
+// (diagnostic, stderr).
+struct PhaseTrace {
+  static bool on() {
+    static const bool v = std::getenv("HPSB_ENGINE_TRACE") != nullptr;
+    return v;
+  }
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double at[8] = {};
+  const char* name[8] = {};
+  int k = 0;
+  void mark(const char* what) {
+    if (!on() || k >= 8) return;
+    name[k] = what;
+    at[k++] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                  .count();
+  }
+  void report(uint64_t n, uint64_t um, bool sync) {
+    if (!on() || k == 0 || at[k - 1] < 2000.0) return;
+    std::fprintf(stderr, "[hpsb trace] n=%llu misses=%llu sync=%d", (unsigned long long)n,
+                 (unsigned long long)um, int(sync));
+    for (int i = 0; i < k; ++i) std::fprintf(stderr, " %s=%.0fus", name[i], at[i]);
+    std::fprintf(stderr, "\n");
+  }
+};
 
 // Device-accessible address of pinned host memory (cudaHostAlloc'd or
 // registered), nullptr for pageable memory.
@@ -327,6 +355,7 @@ LookupEngine::LookupEngine(const std::string& table, uint32_t dim, DeviceCache* 
   HPSB_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
   for (uint32_t i = 0; i < cfg_.async_worker_count; ++i)
     workers_.emplace_back([this] { async_loop(); });
+  if (cfg_.max_batch) reserve(cfg_.max_batch);
 }
 
 LookupEngine::~LookupEngine() {
@@ -560,6 +589,7 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
 }
 
 void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
+  PhaseTrace tr;
   Workspace* ws = c.ws;
   bool handed_off = false;
   struct LeaseGuard {
@@ -583,6 +613,7 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   uint64_t uh = 0, um = 0;
   if (n > 0) {
     HPSB_CUDA(cudaEventSynchronize(ws->counts_ready));
+    tr.mark("counts");
     uh = c.hc[0];
     um = c.hc[1];
     if (um > c.spec_claims) {
@@ -618,8 +649,10 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   if (sync_branch) {
     size_t nf = 0;
     const size_t absent = fetch_and_upload(*ws, ws->h_miss_keys, um, &counters, &nf);
+    tr.mark("fetch");
     defaults = absent;
     std::lock_guard<std::mutex> lk(cache_->mutex());
+    tr.mark("lock");
     if (nf > 0) {
       // row_of is in miss order; the scatter kernel indexes by claim
       for (uint64_t k = 0; k < um; ++k) ws->h_row_of_claim[ws->order[k]] = ws->h_row_of[k];
@@ -657,6 +690,7 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
     }
     HPSB_CUDA(cudaEventRecord(ws->done, st));
     ws->pending = true;
+    tr.mark("enqueued");
   } else {
     defaults = um;
   }
@@ -680,6 +714,7 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
       // pageable rows: copied on chunk by chunk as they land
       if (!c.out_pinned) rows_to_pageable(*ws, c);
       HPSB_CUDA(cudaEventSynchronize(ws->done));
+      tr.mark("rows");
       ws->pending = false;
       if (!c.flags_pinned) std::memcpy(flags, ws->h_flags, n);
     } else {
@@ -687,6 +722,8 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
     }
   }
 
+  tr.mark("done");
+  tr.report(n, um, sync_branch);
   if (outcome) {
     outcome->sync_branch = sync_branch;
     outcome->unique_hit_rate = h;
@@ -1081,6 +1118,18 @@ void LookupEngine::async_loop() {
       if (queue_.empty() && active_ == 0) idle_cv_.notify_all();
     }
   }
+}
+
+void LookupEngine::reserve(uint64_t n) {
+  if (n == 0) return;
+  if (n >= 0xFFFFFFFFull) throw invalid_argument("lookup batch too large");
+  DeviceGuard g(cache_->device());
+  cudaStream_t st = cache_->stream();
+  pool_.for_each([&](Workspace& ws) {
+    ws.wait_idle();
+    ws.ensure(n, dim_, st);
+  });
+  cache_->reserve_replace(n);
 }
 
 void LookupEngine::drain_async() {

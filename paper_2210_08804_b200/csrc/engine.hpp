@@ -132,6 +132,19 @@ class WorkspacePool {
   WorkspacePool(size_t size, int device);
   Workspace* acquire();  // blocks until one is free
   void release(Workspace* ws);
+  // fn(ws) on every workspace, each taken out of the pool for the call
+  template <class F>
+  void for_each(F&& fn) {
+    std::vector<Workspace*> held;
+    for (size_t i = 0; i < slots_.size(); ++i) held.push_back(acquire());
+    try {
+      for (Workspace* w : held) fn(*w);
+    } catch (...) {
+      for (Workspace* w : held) release(w);
+      throw;
+    }
+    for (Workspace* w : held) release(w);
+  }
   size_t size() const { return slots_.size(); }
   size_t outstanding() const;
   size_t peak_outstanding() const;
@@ -159,6 +172,11 @@ class LookupEngine {
                            const uint64_t* const* keys, const size_t* n, float* const* out,
                            uint8_t* const* flags, LookupOutcome* outcomes, int mem);
   void drain_async();
+  // Allocates every workspace (device + pinned staging) and the cache's
+  // replace scratch for batches of up to n keys now, so no lookup pays a
+  // first-use allocation (a pinned staging set is ~100 MB at cfg 2). Also
+  // run at construction when EngineConfig::max_batch is set.
+  void reserve(uint64_t n);
   EngineStats stats() const;
   WorkspacePool& pool() { return pool_; }
   DeviceCache* cache() const { return cache_; }

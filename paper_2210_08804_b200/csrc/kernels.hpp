@@ -48,8 +48,7 @@ constexpr uint32_t kReplaceInline = 8;
 struct ReplaceScratch {
   uint64_t cap = 0;      // set-table entries (power of two >= 2 * ncap)
   uint64_t ncap = 0;     // keys per call
-  uint32_t* set1 = nullptr;   // cap: slabset + 1 (0 = free)
-  uint32_t* cnt = nullptr;    // cap: keys of the set in this call
+  unsigned long long* ent = nullptr;  // cap: (slabset + 1) << 32 | keys of the set (0 = free)
   uint32_t* idx = nullptr;    // cap * kReplaceInline: key indices, arrival order
   uint64_t* kin = nullptr;    // cap * kReplaceInline: the keys themselves
   uint32_t* ovf = nullptr;    // cap: overflow list head (~0 = none)
@@ -67,7 +66,8 @@ size_t replace_scratch_bytes(uint64_t n);
 ReplaceScratch replace_scratch_carve(void* base, uint64_t n);
 void replace_scratch_init(const ReplaceScratch& rs, cudaStream_t st);
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
-                    uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st);
+                    uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st,
+                    int device);
 
 // Update (slab_cache.cpp:109-125): scratch = update_scratch_bytes(n) of
 // device memory (per-position slots + per-block hit counts); winner = the

@@ -704,3 +704,70 @@ def test_async_fills_on_the_side_stream_interleave_with_lookups():
     eng.drain_async()
     c.check_invariants()
     assert eng.stats().async_faults == 0
+
+
+def test_native_segment_cold_tier_engine_matches_python_cold_tier(tmp_path):
+    """The engine with the native batched reader (hps_pdb_cold_fetch, §8 row
+    f4) behind a partial VDB behaves exactly like the engine over a Python
+    cold tier holding the same rows: outcomes, rows, flags, stats (PDB hits
+    promoted into the VDB included)."""
+    from test_segment_store import write_table
+
+    d, S = 16, 64
+    table = T("cold", d)
+    keys = np.arange(0, 30000, 3, dtype=np.uint64)
+    vals = row_values(keys, d, 4)
+    write_table(tmp_path, "cold", d, {0: [(int(k), d, v) for k, v in
+                                         zip(keys, vals.reshape(-1, d))]})
+    native = hps.SegmentStore(tmp_path).table("cold")
+    py = hps.DictStore(d)
+    py.put(keys, vals)
+    engines = []
+    for cold in (native, py):
+        vdb = hps.VolatileStore()
+        vdb.register_table(table)
+        vk = keys[::4]
+        vdb.insert("cold", vk, row_values(vk, d, 4))
+        c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
+        engines.append((hps.LookupEngine(table, c, vdb, cold,
+                                         hps.EngineConfig(hit_rate_threshold=0.9)), c, vdb))
+    stream = workload.powerlaw_sample(1.1, 33000, 5, 6, 10 * 4000)
+    for b in range(10):
+        q = stream[b * 4000:(b + 1) * 4000]
+        res = []
+        for e, _, vdb in engines:
+            o = hps.LookupOutcome()
+            r = e.lookup(q, o)
+            e.drain_async()
+            vdb.drain()
+            res.append((o.__dict__, r.vectors.tobytes(), r.miss_flags.tobytes()))
+        assert res[0] == res[1]
+    s0, s1 = engines[0][0].stats().__dict__, engines[1][0].stats().__dict__
+    assert s0 == s1 and s0["pdb_hits"] > 0
+    assert engines[0][2].table_size("cold") == engines[1][2].table_size("cold")
+
+
+def test_reserve_preallocates_and_lookups_are_unchanged():
+    d = 32
+    table = T("t", d)
+    vdb = hps.VolatileStore()
+    vdb.register_table(table)
+    vk = np.arange(50000, dtype=np.uint64)
+    vdb.insert("t", vk, row_values(vk, d, 1))
+    outs = []
+    for mode in ("lazy", "reserve", "max_batch"):
+        c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=256, slabs_per_set=2, dimension=d))
+        e = hps.LookupEngine(table, c, vdb, None, hps.EngineConfig(
+            hit_rate_threshold=0.7, workspace_pool_size=4,
+            max_batch=20000 if mode == "max_batch" else 0))
+        if mode == "reserve":
+            e.reserve(20000)
+        stream = workload.powerlaw_sample(1.1, 50000, 2, 3, 6 * 20000)
+        got = []
+        for b in range(6):
+            r = e.lookup(stream[b * 20000:(b + 1) * 20000])
+            e.drain_async()
+            got.append((r.vectors.tobytes(), r.miss_flags.tobytes()))
+        outs.append((got, e.stats().__dict__))
+        c.check_invariants()
+    assert outs[0] == outs[1] == outs[2]

@@ -105,6 +105,7 @@ int main(int argc, char** argv) {
     hps::EngineConfig ec;
     ec.hit_rate_threshold = threshold;
     hps::LookupEngine eng(table, cache, &vdb, pdb, ec);
+    eng.reserve(batch);  // serving setup (B200 extension)
     for (int s = 0; s < warmup; ++s)
       (void)eng.lookup(std::span(all.data() + (s % K) * batch, batch));
     eng.drain_async();
