@@ -51,6 +51,7 @@ typedef struct hps_vdb hps_vdb;
 typedef struct hps_engine hps_engine;
 typedef struct hps_multi hps_multi;
 typedef struct hps_pdb hps_pdb;
+typedef struct hps_replicas hps_replicas;
 
 /* ---- vocabulary ------------------------------------------------------- */
 
@@ -390,6 +391,19 @@ int hps_multi_create(hps_engine* const* engines, size_t count, size_t max_batch,
 int hps_multi_destroy(hps_multi* multi);
 int hps_multi_lookup(hps_multi* multi, const uint64_t* const* keys, const size_t* n,
                      float* const* out, uint8_t* const* miss_flags, hps_lookup_outcome* outcomes);
+
+/* The paper's concurrent deployment in one process (no
+ * reference counterpart -- the reference is single-GPU-less): engines[r] is
+ * replica r -- its own cache on its own GPU -- and the engines share ONE host
+ * VDB (create them all over the same hps_vdb). hps_replicas_lookup hands
+ * replica r the batch keys[r][0..n[r]) on its own persistent host thread
+ * (exactly hps_engine_lookup's semantics, NULL stream in device mode) and
+ * returns when every replica is done; no collective. */
+int hps_replicas_create(hps_engine* const* engines, size_t count, hps_replicas** out);
+int hps_replicas_destroy(hps_replicas* group);
+int hps_replicas_lookup(hps_replicas* group, const uint64_t* const* keys, const size_t* n,
+                        float* const* out, uint8_t* const* miss_flags,
+                        hps_lookup_outcome* outcomes, int mem);
 
 /* B200 extension: allocates every workspace (device + pinned staging) and
  * the cache's replace scratch for batches of up to max_keys now, so no lookup

@@ -200,6 +200,9 @@ SIGNATURES = {
     "hps_engine_drain_async": (C.c_int, [_P]),
     "hps_engine_get_stats": (C.c_int, [_P, C.POINTER(_Stats)]),
     "hps_engine_reserve": (C.c_int, [_P, C.c_size_t]),
+    "hps_replicas_create": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    "hps_replicas_destroy": (C.c_int, [_P]),
+    "hps_replicas_lookup": (C.c_int, [_P, _P, _P, _P, _P, _P, C.c_int]),
     "hps_engine_pool_info": (C.c_int, [_P, _U64P, _U64P, _U64P]),
 }
 
@@ -1032,6 +1035,59 @@ class LookupEngine:
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
         _check(lib().hps_engine_pool_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
         return PoolInfo(a.value, b.value, c.value)
+
+
+class ReplicaGroup:
+    """The paper's concurrent deployment in one process: one
+    cache replica + engine per GPU in `devices`, every engine over the SAME
+    host VolatileStore (and cold tier), each replica serving its own batch on
+    its own host thread (hps_replicas_*). No collective."""
+
+    def __init__(self, devices: Sequence[int], cache_config: "SlabCacheConfig", table: TableId,
+                 vdb: Optional[VolatileStore], pdb=None,
+                 config: EngineConfig = EngineConfig()):
+        self.caches = [SlabCache(cache_config, device=d) for d in devices]
+        self.engines = [LookupEngine(table, c, vdb, pdb, config) for c in self.caches]
+        self.table = table
+        PA = C.c_void_p * len(self.engines)
+        self._h = C.c_void_p()
+        _check(lib().hps_replicas_create(PA(*[e._h for e in self.engines]), len(self.engines),
+                                         C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hps_replicas_destroy(self._h)
+            self._h = None
+        for e in getattr(self, "engines", []):
+            e.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        return len(self.engines)
+
+    def lookup_ptrs(self, keys_ptrs, ns, out_ptrs, flags_ptrs, mem: int = HPS_MEM_HOST):
+        g = len(self.engines)
+        PA = C.c_void_p * g
+        outs = (_Outcome * g)()
+        _check(lib().hps_replicas_lookup(self._h, PA(*keys_ptrs), (C.c_size_t * g)(*ns),
+                                         PA(*out_ptrs), PA(*flags_ptrs), outs, mem))
+        return [LookupOutcome(bool(o.sync_branch), float(o.unique_hit_rate), int(o.unique_count),
+                              int(o.defaults_returned)) for o in outs]
+
+    def lookup(self, batches) -> List[LookupResult]:
+        """batches[r] = replica r's keys; returns one LookupResult each."""
+        ks = [_u64(b) for b in batches]
+        d = self.table.dimension
+        outs = [np.empty(max(len(k), 1) * d, dtype=np.float32) for k in ks]
+        fls = [np.empty(max(len(k), 1), dtype=np.uint8) for k in ks]
+        self.lookup_ptrs([k.ctypes.data for k in ks], [len(k) for k in ks],
+                         [o.ctypes.data for o in outs], [f.ctypes.data for f in fls])
+        return [LookupResult(d, o[: len(k) * d], f[: len(k)]) for k, o, f in zip(ks, outs, fls)]
 
 
 class MultiLookup:

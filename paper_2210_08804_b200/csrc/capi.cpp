@@ -30,6 +30,9 @@ struct hps_pdb {
 struct hps_engine {
   std::unique_ptr<hpsb::LookupEngine> impl;
 };
+struct hps_replicas {
+  std::unique_ptr<hpsb::ReplicaGroup> impl;
+};
 struct hps_multi {
   std::unique_ptr<hpsb::MultiLookup> impl;
 };
@@ -880,6 +883,36 @@ int hps_multi_lookup(hps_multi* multi, const uint64_t* const* keys, const size_t
   });
 }
 
+int hps_replicas_create(hps_engine* const* engines, size_t count, hps_replicas** out) {
+  return guarded([&] {
+    need(engines && out, "null argument");
+    std::vector<hpsb::LookupEngine*> e;
+    for (size_t i = 0; i < count; ++i) e.push_back(engines[i] ? engines[i]->impl.get() : nullptr);
+    auto h = std::make_unique<hps_replicas>();
+    h->impl = std::make_unique<hpsb::ReplicaGroup>(std::move(e));
+    *out = h.release();
+  });
+}
+int hps_replicas_destroy(hps_replicas* group) {
+  return guarded([&] { delete group; });
+}
+int hps_replicas_lookup(hps_replicas* group, const uint64_t* const* keys, const size_t* n,
+                        float* const* out, uint8_t* const* miss_flags,
+                        hps_lookup_outcome* outcomes, int mem) {
+  return guarded([&] {
+    need(group && keys && n && out && miss_flags, "null argument");
+    const size_t g = group->impl->size();
+    std::vector<hpsb::LookupOutcome> o(g);
+    group->impl->lookup(keys, n, out, miss_flags, o.data(), mem);
+    if (outcomes)
+      for (size_t r = 0; r < g; ++r) {
+        outcomes[r].sync_branch = o[r].sync_branch ? 1 : 0;
+        outcomes[r].unique_hit_rate = o[r].unique_hit_rate;
+        outcomes[r].unique_count = o[r].unique_count;
+        outcomes[r].defaults_returned = o[r].defaults_returned;
+      }
+  });
+}
 int hps_engine_reserve(hps_engine* engine, size_t max_keys) {
   return guarded([&] {
     need(engine != nullptr, "null argument");

@@ -1142,4 +1142,65 @@ EngineStats LookupEngine::stats() const {
   return stats_;
 }
 
+// ------------------------------------------------------------ replicas --
+ReplicaGroup::ReplicaGroup(std::vector<LookupEngine*> engines) : eng_(std::move(engines)) {
+  if (eng_.empty()) throw invalid_argument("a replica group needs at least one engine");
+  for (auto* e : eng_)
+    if (e == nullptr) throw invalid_argument("null engine in replica group");
+  jobs_.resize(eng_.size());
+  errs_.resize(eng_.size());
+  for (size_t r = 0; r < eng_.size(); ++r) threads_.emplace_back([this, r] { worker(r); });
+}
+
+ReplicaGroup::~ReplicaGroup() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : threads_) t.join();
+}
+
+void ReplicaGroup::worker(size_t r) {
+  uint64_t seen = 0;
+  for (;;) {
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+    }
+    const Job& j = jobs_[r];
+    try {
+      eng_[r]->lookup(j.keys, j.n, j.out, j.n * uint64_t(eng_[r]->dimension()), j.flags, j.outcome,
+                      j.mem, cudaStreamLegacy);
+    } catch (...) {
+      errs_[r] = std::current_exception();
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+}
+
+void ReplicaGroup::lookup(const uint64_t* const* keys, const size_t* n, float* const* out,
+                          uint8_t* const* flags, LookupOutcome* outcomes, int mem) {
+  std::lock_guard<std::mutex> call(call_mu_);
+  for (size_t r = 0; r < eng_.size(); ++r) {
+    jobs_[r] = Job{keys[r], n[r], out[r], flags[r], outcomes ? outcomes + r : nullptr, mem};
+    errs_[r] = nullptr;
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    pending_ = eng_.size();
+    ++gen_;
+  }
+  cv_.notify_all();
+  std::unique_lock<std::mutex> lk(mu_);
+  done_cv_.wait(lk, [&] { return pending_ == 0; });
+  for (auto& e : errs_)
+    if (e) std::rethrow_exception(e);
+}
+
 }  // namespace hpsb

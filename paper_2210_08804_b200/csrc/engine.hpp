@@ -178,6 +178,7 @@ class LookupEngine {
   // run at construction when EngineConfig::max_batch is set.
   void reserve(uint64_t n);
   EngineStats stats() const;
+  uint32_t dimension() const { return dim_; }
   WorkspacePool& pool() { return pool_; }
   DeviceCache* cache() const { return cache_; }
   uint32_t dim() const { return dim_; }
@@ -316,6 +317,46 @@ class MultiLookup {
   uint64_t h_rows_ = 0;
   std::vector<uint32_t> order_;
   std::vector<uint64_t> miss_;
+};
+
+// The paper's concurrent deployment in ONE process: one
+// cache replica per GPU, each with its own engine, all engines over the SAME
+// host volatile DB (its partitions shared, host RAM not multiplied by the GPU
+// count), each replica serving its own query stream. lookup() hands every
+// replica its batch on its own persistent host thread and returns when all
+// are done; there is no collective -- the replicas only meet in the VDB.
+class ReplicaGroup {
+ public:
+  explicit ReplicaGroup(std::vector<LookupEngine*> engines);
+  ~ReplicaGroup();
+  ReplicaGroup(const ReplicaGroup&) = delete;
+  ReplicaGroup& operator=(const ReplicaGroup&) = delete;
+  size_t size() const { return eng_.size(); }
+  // replica r looks up keys[r][0..n[r]) exactly as LookupEngine::lookup;
+  // the first failure (if any) is rethrown after every replica finished
+  void lookup(const uint64_t* const* keys, const size_t* n, float* const* out,
+              uint8_t* const* flags, LookupOutcome* outcomes, int mem);
+
+ private:
+  struct Job {
+    const uint64_t* keys = nullptr;
+    size_t n = 0;
+    float* out = nullptr;
+    uint8_t* flags = nullptr;
+    LookupOutcome* outcome = nullptr;
+    int mem = 0;
+  };
+  void worker(size_t r);
+  std::vector<LookupEngine*> eng_;
+  std::vector<Job> jobs_;
+  std::vector<std::exception_ptr> errs_;
+  std::vector<std::thread> threads_;
+  std::mutex call_mu_;  // one group call at a time
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  size_t pending_ = 0;
+  bool stop_ = false;
 };
 
 }  // namespace hpsb

@@ -51,3 +51,25 @@ def test_max_over_ranks_single_process_is_identity():
     import bench
 
     assert bench.max_over_ranks(3.25, None, "cpu") == 3.25
+
+
+def test_cpu_replica_baseline_runs_n_concurrent_reference_engines():
+    """N > 1: the CPU baseline is N independent reference replicas served
+    concurrently, value = their aggregate keys/s."""
+    import types
+
+    import pytest
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import oracle
+
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    wl = bench.Workload(keyspace=100_000, dim=16, cache_frac=0.2, batch=2048)
+    args = types.SimpleNamespace(hit=0.9)
+    one = bench.cpu_baseline(args, wl, replicas=1)
+    two = bench.cpu_baseline(args, wl, replicas=2)
+    assert one["value"] > 0 and two["value"] > 0, (one, two)
+    assert two["replicas"] == 2 and one["replicas"] == 1
+    assert two["kind"] == "reference" and "2 concurrent reference" in two["sample"]

@@ -771,3 +771,43 @@ def test_reserve_preallocates_and_lookups_are_unchanged():
         outs.append((got, e.stats().__dict__))
         c.check_invariants()
     assert outs[0] == outs[1] == outs[2]
+
+
+def test_replica_group_shares_one_vdb_and_matches_independent_engines():
+    """ReplicaGroup (hps_replicas_*): replicas on their own threads over ONE
+    shared VDB give every replica exactly what an independent engine gives
+    for its own stream (the GPU box has one GPU: both replicas on device 0)."""
+    d, S = 32, 128
+    table = T("t", d)
+    vk = np.arange(0, 60000, 2, dtype=np.uint64)
+    vv = row_values(vk, d, 7)
+
+    def vdb_full():
+        v = hps.VolatileStore()
+        v.register_table(table)
+        v.insert("t", vk, vv)
+        return v
+
+    shared = vdb_full()
+    cfg = hps.EngineConfig(hit_rate_threshold=0.85, default_vector=[0.5])
+    grp = hps.ReplicaGroup([0, 0], hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2,
+                                                       dimension=d), table, shared, None, cfg)
+    solo = []
+    for r in range(2):
+        c = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=2, dimension=d))
+        solo.append((c, hps.LookupEngine(table, c, vdb_full(), None, cfg)))
+    streams = [workload.powerlaw_sample(1.15, 60000, 20 + r, 30 + r, 8 * 6000) for r in range(2)]
+    for b in range(8):
+        batches = [s[b * 6000:(b + 1) * 6000] for s in streams]
+        got = grp.lookup(batches)
+        for e in grp.engines:
+            e.drain_async()
+        for r in range(2):
+            want = solo[r][1].lookup(batches[r])
+            solo[r][1].drain_async()
+            assert got[r].vectors.tobytes() == want.vectors.tobytes()
+            assert (got[r].miss_flags == want.miss_flags).all()
+    for r in range(2):
+        assert grp.engines[r].stats().__dict__ == solo[r][1].stats().__dict__
+        grp.caches[r].check_invariants()
+    grp.close()
