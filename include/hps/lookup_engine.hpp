@@ -34,6 +34,9 @@
 #if defined(__linux__)
 #include <sys/mman.h>
 #endif
+#if defined(__GLIBC__)
+#include <malloc.h>
+#endif
 
 namespace hps {
 
@@ -226,7 +229,23 @@ class LookupEngine {
 
   // B200 extension: allocate every workspace for batches of up to max_keys
   // now (pinned staging included), so no lookup pays a first-use allocation.
-  void reserve(std::size_t max_keys) { b200_detail::check(hps_engine_reserve(h_, max_keys)); }
+  // Also keeps LookupResult storage of that size on the malloc heap: glibc
+  // serves blocks above M_MMAP_THRESHOLD (at most 32 MiB by default) with a
+  // fresh mmap and unmaps them on free, so every result of a large batch
+  // (cfg 2: 33.5 MB) would page-fault its whole buffer again while
+  // resize() zero-fills it; with the threshold raised the freed block of
+  // the previous result is reused, already faulted in. Process-wide
+  // allocator tuning, done only here (serving setup).
+  void reserve(std::size_t max_keys) {
+    b200_detail::check(hps_engine_reserve(h_, max_keys));
+#if defined(__GLIBC__)
+    const std::size_t bytes = max_keys * std::size_t(table_.dimension) * sizeof(float);
+    if (bytes >= (std::size_t(16) << 20) && bytes < (std::size_t(256) << 20)) {
+      (void)::mallopt(M_MMAP_THRESHOLD, int(bytes + bytes / 4 + (std::size_t(1) << 20)));
+      (void)::mallopt(M_TRIM_THRESHOLD, int(4 * bytes));
+    }
+#endif
+  }
 
   EngineStatsSnapshot stats() const {
     hps_engine_stats s{};

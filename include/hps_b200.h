@@ -180,6 +180,25 @@ int hps_cache_replace(hps_cache* cache, const uint64_t* keys, size_t n,
 int hps_cache_replace_device_async(hps_cache* cache, const uint64_t* keys, size_t n,
                                    const float* vectors, size_t vectors_len, void* stream);
 
+/* B200 extension (SURVEY §7 "Hard parts": the opt-in relaxed mode). mode
+ * HPS_REPLACE_EXACT (default): every replace is slot-exact with the
+ * reference -- a set's keys applied in input order (slab_cache.cpp:131-142,
+ * 261-326). HPS_REPLACE_RELAXED: replaces whose keys are known distinct
+ * (host-mode hps_cache_replace after its CPU duplicate check,
+ * hps_cache_replace_device_async, the engine's miss fills) apply every key
+ * at once, winning slots with atomicOr on the slab mask / atomicCAS on the
+ * slot counter; same probe / insert / LRU rules, but same-set keys race, so
+ * slots and the survivors of an over-subscribed set may differ from the
+ * exact mode, and a key whose set has no slot left that this call has not
+ * already stamped is not admitted (counted). A device-mode hps_cache_replace
+ * (which must reject duplicates) stays exact. W > 4 stays exact. */
+#define HPS_REPLACE_EXACT 0
+#define HPS_REPLACE_RELAXED 1
+int hps_cache_set_replace_mode(hps_cache* cache, int mode);
+/* mode and the number of keys the relaxed mode has not admitted so far
+ * (either may be NULL; reading `dropped` synchronises the cache stream) */
+int hps_cache_get_replace_mode(hps_cache* cache, int* mode, uint64_t* dropped);
+
 /* replaces SlabCache::update (slab_cache.cpp:109-125). *written = number of
  * positions whose key was resident (duplicates count every time; the last
  * occurrence's row wins). */

@@ -54,6 +54,8 @@ kPartitionSeed = 0
 
 HPS_MEM_HOST = 0
 HPS_MEM_DEVICE = 1
+HPS_REPLACE_EXACT = 0
+HPS_REPLACE_RELAXED = 1
 
 
 class HpsError(RuntimeError):
@@ -144,6 +146,8 @@ SIGNATURES = {
     "hps_event_record": (C.c_int, [_P, _P]),
     "hps_cache_replace": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, C.c_int, _P]),
     "hps_cache_replace_device_async": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P]),
+    "hps_cache_set_replace_mode": (C.c_int, [_P, C.c_int]),
+    "hps_cache_get_replace_mode": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "hps_cache_update": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _SZP, C.c_int, _P]),
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
     "hps_cache_check_invariants": (C.c_int, [_P]),
@@ -440,6 +444,23 @@ class SlabCache:
         fill; hps_cache_replace_device_async): no duplicate check, no sync."""
         _check(lib().hps_cache_replace_device_async(self._h, keys_ptr, n, rows_ptr, n * self._dim,
                                                     stream or None))
+
+    def set_replace_mode(self, mode: int) -> None:
+        """HPS_REPLACE_EXACT (default, slot-exact with the reference) or
+        HPS_REPLACE_RELAXED (atomicCAS slot claims for distinct-key replaces;
+        see include/hps_b200.h)."""
+        _check(lib().hps_cache_set_replace_mode(self._h, int(mode)))
+
+    def replace_mode(self) -> int:
+        m = C.c_int(0)
+        _check(lib().hps_cache_get_replace_mode(self._h, C.byref(m), None))
+        return m.value
+
+    def relaxed_dropped(self) -> int:
+        """Keys the relaxed mode has not admitted so far."""
+        d = C.c_uint64(0)
+        _check(lib().hps_cache_get_replace_mode(self._h, None, C.byref(d)))
+        return d.value
 
     def update(self, keys, vectors) -> int:
         k = _u64(keys)

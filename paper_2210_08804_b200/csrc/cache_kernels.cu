@@ -845,6 +845,235 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------- relaxed replace --
+// Opt-in (SURVEY §7 "Hard parts": a relaxed atomicCAS-claim mode where the
+// north star's tolerance clause applies): every key of the call is applied
+// by its own warp, all keys at once -- no grouping by set, no per-set
+// serialisation. Placement rules are the reference's (probe the W slabs from
+// the first slab; resident -> recency refresh only; else the lowest free slot
+// of the first non-full probed slab; else evict the minimum counter of the
+// set, ties to the lowest (slab, slot), slab_cache.cpp:283-324), but keys of
+// the same set race for slots and win them with atomics instead of being
+// applied in input order. A won slot's counter holds stamp | kClaimBit until
+// the call's second kernel clears the bit, so within the call
+//   * no other key can claim it again (a claimed counter is never the
+//     minimum, and every claim is an atomicCAS from the value observed),
+//   * so every slot is written by at most one key: rows are never torn.
+//   free slot  atomicOr of the slot's bit into the slab mask (the claimer
+//              whose OR found the bit clear owns the mask bit; a loser
+//              retries on the mask the OR returned, so masks still fill
+//              from bit 0), then atomicCAS(counter, observed, stamp|claim)
+//              -- an evictor that saw the slab full may have taken it first
+//   eviction   argmin over the set's unclaimed counters, won by
+//              atomicCAS(counter, min, stamp|claim); a lost CAS updates the
+//              one observed counter (it only ever grows: a refresh raises it
+//              to the stamp, a claim sets the bit) and retries
+//   refresh    atomicMax(counter, stamp) (keeps a concurrent claim's bit)
+// Keys of one call therefore never evict each other: a key whose set has no
+// unclaimed slot left is not admitted (counted in *dropped), where the exact
+// mode would evict a key this call inserted. Keys must be DISTINCT. Slots,
+// and which keys of an over-subscribed set survive, can differ from the
+// exact mode; invariants and every stored row's bytes are the same.
+constexpr unsigned long long kClaimBit = 1ull << 63;
+
+#ifndef HPSB_RELAX_MINB
+#define HPSB_RELAX_MINB 1
+#endif
+
+template <int W>
+__global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
+    k_replace_relaxed(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
+                      const float* __restrict__ rows, uint64_t stamp,
+                      uint64_t* __restrict__ claimed, unsigned long long* __restrict__ dropped) {
+  __shared__ unsigned long long s_ins, s_drop;
+  if (threadIdx.x == 0) {
+    s_ins = 0ull;
+    s_drop = 0ull;
+  }
+  __syncthreads();
+  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  unsigned long long* const ctr = reinterpret_cast<unsigned long long*>(c.counters);
+  const unsigned long long mine = stamp | kClaimBit;
+  if (i < n) {
+    const uint32_t d = c.d;
+    const uint64_t key = keys[i];
+    const float* src = rows + i * d;
+    const bool vec = (d & 3u) == 0 && d <= 128 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
+    float4 rv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (vec && lane < (d >> 2)) rv = reinterpret_cast<const float4*>(src)[lane];
+    const uint64_t set = slabset_of(c, key);
+    const uint64_t h2 = xxh64_key(key, kSlabSeed);
+    const uint32_t first = W == 1 ? 0u : (W == 2 ? uint32_t(h2 & 1u) : uint32_t(fastmod(h2, W, c.mW)));
+    const uint64_t sbase = set * W;
+    uint32_t m[W];
+    uint64_t k[W], ct[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      m[w] = c.masks[sbase + w];
+      k[w] = c.keys[(sbase + w) * kSlotsPerSlab + lane];
+      ct[w] = c.counters[(sbase + w) * kSlotsPerSlab + lane];
+    }
+    // probe in slab order from `first` (slab_cache.cpp:292-310)
+    int hit_w = -1, ins_step = -1;
+    uint32_t hit_j = 0;
+#pragma unroll
+    for (int step = 0; step < W; ++step) {
+      int w = int(first) + step;
+      if (w >= W) w -= W;
+      if (hit_w >= 0 || ins_step >= 0) continue;
+      uint64_t kw = 0;
+      uint32_t mw = 0;
+#pragma unroll
+      for (int x = 0; x < W; ++x)
+        if (x == w) {
+          kw = k[x];
+          mw = m[x];
+        }
+      const uint32_t hb = __ballot_sync(0xFFFFFFFFu, ((mw >> lane) & 1u) && kw == key);
+      if (hb) {
+        hit_w = w;
+        hit_j = __ffs(hb) - 1;
+      } else if (mw != kFullSlab) {
+        ins_step = step;
+      }
+    }
+    uint64_t slot = ~0ull;
+    if (hit_w >= 0) {
+      // resident: recency refresh only, the vector is kept (:283-288)
+      if (lane == hit_j) atomicMax(ctr + (sbase + hit_w) * kSlotsPerSlab + lane, (unsigned long long)stamp);
+    } else {
+      int tw = -1;
+      uint32_t tj = 0;
+      // free slots: the probed slabs from the first non-full one, in order
+      if (ins_step >= 0) {
+#pragma unroll
+        for (int step = 0; step < W; ++step) {
+          if (step < ins_step || tw >= 0) continue;
+          int w = int(first) + step;
+          if (w >= W) w -= W;
+          uint32_t mw = 0;
+          uint64_t cw = 0;
+#pragma unroll
+          for (int x = 0; x < W; ++x)
+            if (x == w) {
+              mw = m[x];
+              cw = ct[x];
+            }
+          // terminates: every lost OR returns a mask with more bits set
+          while (mw != kFullSlab) {
+            const uint32_t j = __ffs(~mw) - 1;  // countr_one(mask) (:299)
+            const uint64_t cj = __shfl_sync(0xFFFFFFFFu, cw, j);
+            uint32_t old = 0, won = 0;
+            if (lane == 0) {
+              old = atomicOr(c.masks + sbase + w, 1u << j);
+              if (((old >> j) & 1u) == 0u) {
+                // occupied from here on, by this key or by an evictor's
+                atomicAdd(&s_ins, 1ull);
+                won = atomicCAS(ctr + (sbase + w) * kSlotsPerSlab + j, (unsigned long long)cj,
+                                mine) == cj ? 1u : 0u;
+              }
+            }
+            old = __shfl_sync(0xFFFFFFFFu, old, 0);
+            won = __shfl_sync(0xFFFFFFFFu, won, 0);
+            if (won) {
+              tw = w;
+              tj = j;
+              break;
+            }
+            mw = old | (1u << j);
+          }
+#pragma unroll
+          for (int x = 0; x < W; ++x)
+            if (x == w) m[x] = mw;
+        }
+      }
+      // eviction: argmin over the set's unclaimed counters; terminates --
+      // a lost CAS shows a strictly larger value (at most two raises a slot)
+      for (uint32_t tries = 0; tw < 0 && tries <= 2u * uint32_t(W) * 32u; ++tries) {
+        uint64_t bc = ~0ull;
+        uint32_t bi = 0xFFFFFFFFu;
+#pragma unroll
+        for (int x = 0; x < W; ++x)
+          if ((ct[x] & kClaimBit) == 0ull && ct[x] < bc) {
+            bc = ct[x];
+            bi = uint32_t(x) * 32 + lane;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, bc, o);
+          const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+          if (oc < bc || (oc == bc && oi < bi)) {
+            bc = oc;
+            bi = oi;
+          }
+        }
+        if (bi == 0xFFFFFFFFu) break;  // every slot of the set claimed by this call
+        const uint32_t bw = bi >> 5, bj = bi & 31u;
+        unsigned long long old = 0;
+        if (lane == 0) old = atomicCAS(ctr + (sbase + bw) * kSlotsPerSlab + bj, (unsigned long long)bc, mine);
+        old = __shfl_sync(0xFFFFFFFFu, old, 0);
+        if (old == bc) {
+          tw = int(bw);
+          tj = bj;
+        } else if (lane == bj) {
+#pragma unroll
+          for (int x = 0; x < W; ++x)
+            if (uint32_t(x) == bw) ct[x] = old;
+        }
+      }
+      if (tw >= 0) {
+        slot = (sbase + uint64_t(tw)) * kSlotsPerSlab + tj;
+        if (lane == 0) {
+          c.keys[slot] = key;
+          c.tags[slot] = key_tag(h2);
+        }
+        float* dst = c.rows + slot * d;
+        if (vec) {
+          if (lane < (d >> 2)) reinterpret_cast<float4*>(dst)[lane] = rv;
+        } else {
+          warp_copy_row(src, dst, d);
+        }
+      } else if (lane == 0) {
+        atomicAdd(&s_drop, 1ull);
+      }
+    }
+    if (lane == 0) claimed[i] = slot;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_ins) atomicAdd(c.occupied, s_ins);
+    if (s_drop && dropped != nullptr) atomicAdd(dropped, s_drop);
+  }
+}
+
+// The call's claims become plain counters (= the stamp).
+__global__ void __launch_bounds__(256)
+    k_replace_relaxed_release(CacheDev c, const uint64_t* __restrict__ claimed, uint64_t n,
+                              uint64_t stamp) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t slot = claimed[i];
+  if (slot != ~0ull) c.counters[slot] = stamp;
+}
+
+bool launch_replace_relaxed(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
+                            uint64_t stamp, uint64_t* claimed, unsigned long long* dropped,
+                            cudaStream_t st) {
+  if (n == 0) return true;
+  if (c.W == 0 || c.W > 4) return false;  // wider sets: the exact path
+  const unsigned grid = unsigned((n * 32 + 255) / 256);
+  switch (c.W) {
+    case 1: k_replace_relaxed<1><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    case 2: k_replace_relaxed<2><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    case 3: k_replace_relaxed<3><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    default: k_replace_relaxed<4><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+  }
+  k_replace_relaxed_release<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, claimed, n, stamp);
+  check_launch("replace_relaxed", 2);
+  return true;
+}
+
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st,
                     int device) {

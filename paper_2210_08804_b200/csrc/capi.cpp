@@ -450,6 +450,21 @@ int hps_cache_replace_device_async(hps_cache* cache, const uint64_t* keys, size_
   });
 }
 
+int hps_cache_set_replace_mode(hps_cache* cache, int mode) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    cache->impl->set_replace_mode(mode);
+  });
+}
+
+int hps_cache_get_replace_mode(hps_cache* cache, int* mode, uint64_t* dropped) {
+  return guarded([&] {
+    need(cache != nullptr, "null argument");
+    if (mode) *mode = cache->impl->replace_mode();
+    if (dropped) *dropped = cache->impl->relaxed_dropped();
+  });
+}
+
 int hps_cache_update(hps_cache* cache, const uint64_t* keys, size_t n, const float* vectors,
                      size_t vectors_len, size_t* written, int mem, void* stream) {
   return guarded([&] {

@@ -528,7 +528,7 @@ void DeviceCache::replace(const uint64_t* keys, size_t n, const float* vectors,
   } else {
     join_from(user);
   }
-  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/!host, rs, stream_, device_);
+  launch_replace_mode(d_keys, n, d_rows, stamp, /*validate=*/!host, rs);
   if (host) {
     HPSB_CUDA(cudaStreamSynchronize(stream_));
     return;
@@ -565,6 +565,7 @@ const ReplaceScratch& DeviceCache::replace_scratch_locked(uint64_t n) {
     void* b = rbuf_.ensure(replace_scratch_bytes(cap), stream_);
     rs_ = replace_scratch_carve(b, cap);
     replace_scratch_init(rs_, stream_);
+    relaxed_buf_.ensure(cap * 8, stream_);
     rcap_ = cap;
     mark_other_op();
   }
@@ -576,7 +577,34 @@ void DeviceCache::replace_device_locked(const uint64_t* d_keys, size_t n, const 
   if (n == 0) return;
   const uint64_t stamp = clock_.load(std::memory_order_relaxed);
   const ReplaceScratch& rs = replace_scratch_locked(n);
-  launch_replace(dev_, d_keys, n, d_rows, stamp, /*validate=*/false, rs, stream_, device_);
+  launch_replace_mode(d_keys, n, d_rows, stamp, /*validate=*/false, rs);
+}
+
+void DeviceCache::launch_replace_mode(const uint64_t* d_keys, uint64_t n, const float* d_rows,
+                                      uint64_t stamp, bool validate, const ReplaceScratch& rs) {
+  // slot d_small_[6]: the relaxed mode's dropped-key count
+  if (!validate && replace_mode() == 1 && dev_.W <= 4) {
+    // each key's claimed slot (sized with the replace scratch)
+    uint64_t* claimed = static_cast<uint64_t*>(relaxed_buf_.get());
+    launch_replace_relaxed(dev_, d_keys, n, d_rows, stamp, claimed, d_small_ + 6, stream_);
+    return;
+  }
+  launch_replace(dev_, d_keys, n, d_rows, stamp, validate, rs, stream_, device_);
+}
+
+void DeviceCache::set_replace_mode(int mode) {
+  if (mode != 0 && mode != 1) throw invalid_argument("replace mode must be 0 (exact) or 1 (relaxed)");
+  std::lock_guard<std::mutex> lk(mu_);
+  replace_mode_.store(mode, std::memory_order_relaxed);
+}
+
+uint64_t DeviceCache::relaxed_dropped() {
+  std::lock_guard<std::mutex> lk(mu_);
+  mark_other_op();
+  DeviceGuard g(device_);
+  HPSB_CUDA(cudaMemcpyAsync(h_small_ + 6, d_small_ + 6, 8, cudaMemcpyDeviceToHost, stream_));
+  HPSB_CUDA(cudaStreamSynchronize(stream_));
+  return h_small_[6];
 }
 
 size_t DeviceCache::update(const uint64_t* keys, size_t n, const float* vectors,

@@ -70,6 +70,15 @@ class DeviceCache {
   // slab_cache.cpp:109-125
   size_t update(const uint64_t* keys, size_t n, const float* vectors, size_t vectors_len,
                 int mem, cudaStream_t user);
+  // Replace mode: 0 = exact (the reference's per-set input order, the
+  // default), 1 = relaxed (atomicCAS slot claims, every key at once; used by
+  // the calls whose keys are known distinct: host-mode replace, the device
+  // fill below and the engine's fills -- a device-mode replace that must
+  // reject duplicates stays exact).
+  void set_replace_mode(int mode);
+  int replace_mode() const { return replace_mode_.load(std::memory_order_relaxed); }
+  // keys the relaxed mode did not admit so far (syncs the stream)
+  uint64_t relaxed_dropped();
   // Stream-ordered replace of DISTINCT keys on device pointers (the engine's
   // fill primitive): no duplicate check, no host synchronisation.
   void replace_device_async(const uint64_t* keys, size_t n, const float* rows, cudaStream_t user);
@@ -174,10 +183,15 @@ class DeviceCache {
   cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
   std::mutex mu_;
   std::atomic<uint64_t> clock_{0};
+  std::atomic<int> replace_mode_{0};
+  // exact or relaxed replace of device keys / rows (distinct keys)
+  void launch_replace_mode(const uint64_t* d_keys, uint64_t n, const float* d_rows,
+                           uint64_t stamp, bool validate, const ReplaceScratch& rs);
   ScanState scan_;
   DeviceBuffer scratch_;
   // replace: persistent per-call set table (kernels.hpp ReplaceScratch)
   DeviceBuffer rbuf_;
+  DeviceBuffer relaxed_buf_;  // relaxed replace: each key's claimed slot
   ReplaceScratch rs_;
   uint64_t rcap_ = 0;
   const ReplaceScratch& replace_scratch_locked(uint64_t n);

@@ -68,6 +68,14 @@ void replace_scratch_init(const ReplaceScratch& rs, cudaStream_t st);
 void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
                     uint64_t stamp, bool validate, const ReplaceScratch& rs, cudaStream_t st,
                     int device);
+// The opt-in relaxed mode (atomicCAS slot claims, every key at once; keys
+// must be distinct): false when the geometry has no relaxed kernel (W > 4),
+// then the caller runs the exact path. `claimed` = n u64 of device scratch
+// (each key's won slot); *dropped (device) counts keys that found no
+// claimable slot.
+bool launch_replace_relaxed(const CacheDev& c, const uint64_t* keys, uint64_t n, const float* rows,
+                            uint64_t stamp, uint64_t* claimed, unsigned long long* dropped,
+                            cudaStream_t st);
 
 // Update (slab_cache.cpp:109-125): scratch = update_scratch_bytes(n) of
 // device memory (per-position slots + per-block hit counts); winner = the

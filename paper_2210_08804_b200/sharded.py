@@ -10,14 +10,21 @@ rank calls it with its own batch:
    positions ride along);
 2. exchange: the counts, then the keys (all-to-all; NCCL over NVLink on the
    GPU box, gloo in the CPU tests);
-3. each owner runs ONE lookup of everything it received
-   (``hps_cache_lookup_device``: probe, recency, rows, default rows for
-   misses, its unique misses -- the owner fills its own shard);
+3. each owner runs ONE lookup of everything it received -- either the bare
+   cache lookup (``cache_local_lookup``: ``hps_cache_lookup_device``, probe,
+   recency, rows, default rows for misses, the owner's unique misses handed
+   back), or the whole lookup engine (``engine_local_lookup``:
+   ``hps_engine_lookup`` on device pointers -- dedup, query, the hit-rate
+   switch, the tier fetch of the owner's unique misses from the host VDB,
+   scatter, replace or background fill: the owner fills its own shard with
+   the reference's LookupEngine semantics, lookup_engine.cpp:130-241);
 4. exchange back: rows and miss flags (reverse all-to-all);
 5. unroute: rows to the requester's original positions
    (``hps_shard_unroute``).
 
-The only collectives are these exchanges; the replica mode (one full cache
+One host synchronisation per lookup: the per-owner counts are exchanged on
+the device and read back together (the all-to-all split sizes must be host
+values). The only collectives are these exchanges; the replica mode (one full cache
 per GPU, ``bench.py --gpus N``) has none. There is no reference counterpart:
 the reference is single-process and the paper deploys replicas
 (PAPER.md:809).
@@ -100,6 +107,29 @@ def cache_local_lookup(cache, device: int = 0) -> Callable:
     return run
 
 
+def engine_local_lookup(engine, device: int = 0) -> Callable:
+    """The owner-side lookup through a full LookupEngine over the owner's
+    shard cache (hps_engine_lookup, HPS_MEM_DEVICE): misses are fetched from
+    the engine's tiers and admitted into the owner's shard (sync branch) or
+    filled in the background (async branch), exactly as a single-GPU engine
+    does (lookup_engine.cpp:130-241). The engine's configured default vector
+    is used for absent keys. Returns (rows, flags, outcome)."""
+
+    def run(keys, default_row):
+        import torch
+
+        n = keys.numel()
+        d = engine.table.dimension
+        rows = torch.empty(max(n, 1) * d, device=keys.device)
+        flags = torch.empty(max(n, 1), dtype=torch.uint8, device=keys.device)
+        st = torch.cuda.current_stream(device).cuda_stream
+        o = engine.lookup_ptrs(keys.data_ptr(), n, rows.data_ptr(), flags.data_ptr(),
+                               HPS_MEM_DEVICE, st)
+        return rows[: n * d], flags[:n], o
+
+    return run
+
+
 class ShardedLookup:
     """Collective lookup over a key-hash-sharded cache (see module doc)."""
 
@@ -116,25 +146,28 @@ class ShardedLookup:
 
     def lookup(self, keys, default_row):
         """keys: int64 tensor of this rank's batch. Returns (rows [n*dim],
-        miss flags [n], owner_side) where owner_side = (miss_keys,
-        miss_firsts, counts) of THIS rank's shard lookup (its unique misses,
-        to be fetched from the tiers and replaced by this rank)."""
+        miss flags [n], owner_side) where owner_side is what THIS rank's
+        shard lookup returned besides rows and flags: (miss_keys,
+        miss_firsts, counts) for cache_local_lookup (its unique misses, to be
+        fetched and replaced by this rank), (outcome,) for
+        engine_local_lookup (misses already fetched / admitted)."""
         import torch
 
         dist, G, d = self.dist, self.world, self.dim
         n = keys.numel()
         counts = self.ops.count(keys, G)
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
         offsets = torch.zeros_like(counts)
         if G > 1:
             offsets[1:] = torch.cumsum(counts, 0)[:-1]
         send_keys, send_pos = self.ops.scatter(keys, G, offsets)
-        send_splits = counts.cpu().tolist()
-        recv_counts = torch.empty_like(counts)
-        dist.all_to_all_single(recv_counts, counts, group=self.group)
-        recv_splits = recv_counts.cpu().tolist()
+        # the one host synchronisation: both split vectors at once
+        splits = torch.cat([counts, recv_counts]).cpu().tolist()
+        send_splits, recv_splits = splits[:G], splits[G:]
         recv_keys = torch.empty(sum(recv_splits), dtype=keys.dtype, device=keys.device)
         dist.all_to_all_single(recv_keys, send_keys, recv_splits, send_splits, group=self.group)
-        rows, flags, mk, mf, cnt = self.local_lookup(recv_keys, default_row)
+        rows, flags, *owner_side = self.local_lookup(recv_keys, default_row)
         back_rows = torch.empty(n * d, dtype=rows.dtype, device=keys.device)
         dist.all_to_all_single(back_rows.view(-1, d) if n else back_rows,
                                rows.view(-1, d) if rows.numel() else rows,
@@ -145,4 +178,4 @@ class ShardedLookup:
         out = torch.empty(n * d, dtype=rows.dtype, device=keys.device)
         flags_out = torch.empty(n, dtype=torch.uint8, device=keys.device)
         self.ops.unroute(send_pos, back_rows, back_flags, out, flags_out, d)
-        return out, flags_out, (mk, mf, cnt)
+        return out, flags_out, tuple(owner_side)

@@ -109,6 +109,72 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def engine_oracle_lookup(eo: "oracle.EngineOracle"):
+    """CPU stand-in for engine_local_lookup: the owner's whole LookupEngine
+    (EngineOracle: dedup, query, hit-rate switch, tier fetch, replace)."""
+    def run(keys, default_row):
+        out, flags, oc = eo.lookup(keys.numpy().view(np.uint64))
+        eo.drain_async()
+        return torch.from_numpy(out.copy()), torch.from_numpy(flags.astype(np.uint8)), oc
+    return run
+
+
+def _engine_worker(rank, world, port, threshold, q):
+    """Owner-side miss fill: every owner runs an engine over its shard with
+    the VDB behind it; the requester's rows must be the VDB rows (flag 0) or
+    the default (flag 1: absent, or an async-branch miss), and the owners
+    must have admitted the keys they fetched."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        default = np.full(D, -2.0, np.float32)
+        eo = oracle.EngineOracle(256, 2, D, threshold=threshold, default_vector=list(default))
+        vdb_keys = np.arange(0, KEYSPACE, 2, dtype=np.uint64)  # odd keys absent everywhere
+        mine = vdb_keys[sharded.shard_of(vdb_keys, world) == rank]
+        for k, r in zip(mine, key_rows(mine).reshape(-1, D)):
+            eo.vdb[int(k)] = r
+        sl = sharded.ShardedLookup(D, engine_oracle_lookup(eo), ops=CpuOps())
+        ok = True
+        for b in range(4):
+            brng = np.random.default_rng(1000 * rank + b)
+            batch = brng.integers(0, KEYSPACE, 500 + 61 * rank, dtype=np.uint64)
+            out, flags, (oc,) = sl.lookup(torch.from_numpy(batch.view(np.int64)),
+                                          torch.from_numpy(default))
+            got = out.numpy().reshape(-1, D)
+            fl = flags.numpy()
+            want = key_rows(batch).reshape(-1, D)
+            present = batch % 2 == 0
+            ok &= bool((got[fl == 0] == want[fl == 0]).all())
+            ok &= bool((got[fl == 1] == default).all())
+            ok &= bool((fl[~present] == 1).all())
+            if threshold >= 1.0:  # every batch with a miss takes the sync branch
+                ok &= bool((fl[present] == 0).all())
+        # owner-side fill: every present key this rank owns that was looked
+        # up (by anyone) is resident in its shard now (no eviction at 512 slots)
+        ok &= eo.cache.occupied() > 0 and eo.stats["vdb_hits"] == eo.cache.occupied()
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("threshold", [1.0, 0.6])
+def test_sharded_engine_owner_side_fill_gloo(threshold):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = free_port()
+    procs = [ctx.Process(target=_engine_worker, args=(r, world, port, threshold, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get() for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_lookup_orchestration_gloo(world):
     ctx = mp.get_context("spawn")
@@ -196,5 +262,47 @@ def test_sharded_lookup_world_one_nccl_matches_oracle():
             assert (fl.cpu().numpy() == (1 - hit)[inv]).all()
             um = int((hit == 0).sum())
             assert cnt.cpu().tolist() == [len(uniq) - um, um]
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_engine_lookup_world_one_nccl_matches_engine_oracle():
+    """engine_local_lookup on B200 (NCCL, world 1): the owner's engine
+    fetches its misses from the host VDB and admits them; outcomes, rows and
+    flags equal the engine oracle's (no eviction, so the routing order inside
+    a segment does not change which keys are resident)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        S, W, thr = 256, 2, 0.7
+        table = hps.TableId("t", D)
+        vdb = hps.VolatileStore()
+        vdb.register_table(table)
+        vk = np.arange(0, KEYSPACE, 2, dtype=np.uint64)
+        vdb.insert("t", vk, key_rows(vk))
+        eo = oracle.EngineOracle(S, W, D, threshold=thr, default_vector=[4.0])
+        for k, r in zip(vk, key_rows(vk).reshape(-1, D)):
+            eo.vdb[int(k)] = r
+        cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=S, slabs_per_set=W, dimension=D))
+        eng = hps.LookupEngine(table, cache, vdb, None,
+                               hps.EngineConfig(hit_rate_threshold=thr, default_vector=[4.0]))
+        sl = sharded.ShardedLookup(D, sharded.engine_local_lookup(eng))
+        rng = np.random.default_rng(9)
+        dflt = torch.zeros(D, device="cuda")
+        for b in range(6):
+            q = rng.integers(0, KEYSPACE // 4, 2000, dtype=np.uint64)
+            out, fl, (oc,) = sl.lookup(torch.from_numpy(q.view(np.int64)).cuda(), dflt)
+            eng.drain_async()
+            torch.cuda.synchronize()
+            want, wflags, woc = eo.lookup(q)
+            eo.drain_async()
+            assert oc.__dict__ == woc
+            assert out.cpu().numpy().tobytes() == want.tobytes()
+            assert (fl.cpu().numpy() == wflags).all()
+        cache.check_invariants()
+        assert cache.occupied() == eo.cache.occupied()
     finally:
         dist.destroy_process_group()

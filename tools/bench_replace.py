@@ -13,6 +13,11 @@ with CUDA events on the cache stream:
                     keys hashing into sets other keys of the call also touch
   replace_user   -- the same through hps_cache_replace (device mode: duplicate
                     check before mutation, host reads the flag)
+  replace_relaxed -- the engine-fill replace in the opt-in relaxed mode
+                    (hps_cache_set_replace_mode(HPS_REPLACE_RELAXED):
+                    atomicCAS slot claims, every key at once), same batch
+                    shape, then the invariants checked and the dropped keys
+                    counted (run after everything else)
   update_all     -- hps_cache_update_device of every resident row
 and the cache state is checked against the oracle at the end when --check.
 """
@@ -63,7 +68,7 @@ def main():
     rng = np.random.default_rng(5)
     fresh = wl.rank_to_key[len(wl.preload):]
     batches = []
-    for b in range(a.reps + 2):
+    for b in range(2 * a.reps + 3):
         f = fresh[b * n: b * n + n // 2 + n // 4]
         rres = rng.choice(resident, n // 4, replace=False)
         k = np.concatenate([f, rres])
@@ -94,8 +99,9 @@ def main():
             o.replace(*batches[1 + j])
     res["replace_fill_us"] = t_fill
     res["replace_fill_row_gbs"] = n * d * 4 * 2 / (t_fill * 1e-6) / 1e9
-    k, r = batches[-1]
-    t_user = timed(lambda j: cache.replace_device(dk[-1][0].data_ptr(), len(k), dk[-1][1].data_ptr(),
+    u = a.reps + 1
+    k, r = batches[u]
+    t_user = timed(lambda j: cache.replace_device(dk[u][0].data_ptr(), len(k), dk[u][1].data_ptr(),
                                                   sp), 1)
     if o is not None:
         o.replace(k, r)
@@ -117,6 +123,18 @@ def main():
         res["state_equal"] = bool((gm == om).all() and (gk[occ] == ok[occ]).all()
                                   and (gc[occ] == oc[occ]).all()
                                   and gr.reshape(-1, d)[occ].tobytes() == orow.reshape(-1, d)[occ].tobytes())
+    # relaxed mode last (the exact-mode state check above is done)
+    cache.set_replace_mode(hps.HPS_REPLACE_RELAXED)
+    base = a.reps + 2
+    cache.replace_fill(dk[base][0].data_ptr(), len(batches[base][0]), dk[base][1].data_ptr(), sp)
+    t_rel = timed(lambda j: cache.replace_fill(dk[base + 1 + j][0].data_ptr(),
+                                               len(batches[base + 1 + j][0]),
+                                               dk[base + 1 + j][1].data_ptr(), sp), a.reps)
+    cache.check_invariants()
+    res["replace_relaxed_us"] = t_rel
+    res["replace_relaxed_row_gbs"] = n * d * 4 * 2 / (t_rel * 1e-6) / 1e9
+    res["replace_relaxed_dropped"] = cache.relaxed_dropped()
+    res["replace_relaxed_keys"] = int(sum(len(batches[base + j][0]) for j in range(a.reps + 1)))
     print(json.dumps(res))
 
 
