@@ -566,6 +566,11 @@ def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
     for i in range(0, R, 1 << 18):
         k = resident[i:i + (1 << 18)]
         rvdb.insert("refresh", k, table_rows(k, d))
+    # the first pass allocates the refresh staging (kept by the cache for
+    # later passes); the steady-state figure is the second pass
+    t0 = time.perf_counter()
+    hps.refresh_cache(cache, rtable, rvdb, None, dump_batch_size=65536)
+    refresh_first_ms = (time.perf_counter() - t0) * 1e3
     t0 = time.perf_counter()
     ref_out = hps.refresh_cache(cache, rtable, rvdb, None, dump_batch_size=65536)
     refresh_ms = (time.perf_counter() - t0) * 1e3
@@ -613,6 +618,7 @@ def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
             "dump_all": {"keys": R, "ms": dump_ms, "api": "SlabCache::dump_all (device kernel + D2H)",
                          "device_dump_ms": dump_dev_ms, "paper_a100_ms_1gb": 0.064},
             "refresh_full_cache": {"rows": R, "refreshed": ref_out.refreshed, "ms": refresh_ms,
+                                   "first_pass_ms": refresh_first_ms,
                                    "gb_per_s": row_bytes / (refresh_ms * 1e-3) / 1e9,
                                    "api": "hps_refresh_cache: dump -> host VDB fetch (pinned) "
                                           "-> H2D -> update, batches of 65536, pipelined"},

@@ -211,6 +211,9 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #define HPSB_REPL_KPRE 2
 #endif
 
+#ifndef HPSB_REPL_BINAGG
+#define HPSB_REPL_BINAGG 1
+#endif
 __global__ void __launch_bounds__(256)
     k_replace_bin(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -223,7 +226,6 @@ __global__ void __launch_bounds__(256)
   uint64_t set = 0;
   if (i < n) {
     const uint64_t key = keys[i];
-    // the row the set kernel will copy (if the key is inserted), toward L2
     set = slabset_of(c, key);
     const unsigned long long tag = (set + 1ull) << 32;
     const uint64_t mask = rs.cap - 1;
@@ -250,6 +252,26 @@ __global__ void __launch_bounds__(256)
     lead = r == 0;
     e32 = uint32_t(e);
   }
+#if HPSB_REPL_BINAGG
+  // the touched-set list: one global cursor add per BLOCK (every warp adding
+  // on the same word serialised ~2,000 same-address atomics in one L2 slice)
+  __shared__ uint32_t s_cnt, s_base;
+  if (threadIdx.x == 0) s_cnt = 0u;
+  __syncthreads();
+  const uint32_t lm = __ballot_sync(0xFFFFFFFFu, lead);
+  const uint32_t lane = lane_id();
+  uint32_t woff = 0;
+  if (lane == 0 && lm) woff = atomicAdd(&s_cnt, uint32_t(__popc(lm)));
+  woff = __shfl_sync(0xFFFFFFFFu, woff, 0);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) s_base = atomicAdd(rs.cursor + 2, s_cnt);
+  __syncthreads();
+  if (lead) {
+    const uint32_t k = s_base + woff + uint32_t(__popc(lm & ((1u << lane) - 1u)));
+    rs.lead_e[k] = e32;
+    rs.lead_s[k] = uint32_t(set);
+  }
+#else
   __syncwarp();
   const uint32_t lm = __ballot_sync(0xFFFFFFFFu, lead);
   if (lm == 0u) return;
@@ -262,6 +284,7 @@ __global__ void __launch_bounds__(256)
     rs.lead_e[k] = e32;
     rs.lead_s[k] = uint32_t(set);
   }
+#endif
 }
 
 // Sets of more than 32 keys (tiny caches): the indices in a sorted bucket
@@ -877,22 +900,33 @@ __global__ void __launch_bounds__(256)
 constexpr unsigned long long kClaimBit = 1ull << 63;
 
 #ifndef HPSB_RELAX_MINB
-#define HPSB_RELAX_MINB 1
+#define HPSB_RELAX_MINB 5
 #endif
 
-template <int W>
-__global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
+// A key is applied by a GROUP of G lanes (G = 32 / keys per warp): lane l
+// of the group holds slots l, l + G, ... of each slab (SPL = 32 / G slots
+// per slab per lane); every collective op is masked to the group, so the
+// groups of a warp proceed independently (2 keys in flight per warp at
+// G = 16 -- the kernel is bound by its dependent round trips, not by issue).
+template <int W, int G>
+__global__ void __launch_bounds__(256, W <= 2 ? HPSB_RELAX_MINB : 4)
     k_replace_relaxed(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n,
                       const float* __restrict__ rows, uint64_t stamp,
                       uint64_t* __restrict__ claimed, unsigned long long* __restrict__ dropped) {
+  constexpr int SPL = 32 / G;
+  constexpr uint32_t kGroupBits = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
+  constexpr int RV = (32 + G - 1) / G;  // float4 of a <= 128-float row per lane
   __shared__ unsigned long long s_ins, s_drop;
   if (threadIdx.x == 0) {
     s_ins = 0ull;
     s_drop = 0ull;
   }
   __syncthreads();
-  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
+  const uint32_t l = lane % G;             // lane within the group
+  const uint32_t gb = lane - l;            // the group's first lane
+  const uint32_t gm = kGroupBits << gb;    // the group's lanes
+  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
   unsigned long long* const ctr = reinterpret_cast<unsigned long long*>(c.counters);
   const unsigned long long mine = stamp | kClaimBit;
   if (i < n) {
@@ -900,19 +934,27 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
     const uint64_t key = keys[i];
     const float* src = rows + i * d;
     const bool vec = (d & 3u) == 0 && d <= 128 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
-    float4 rv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (vec && lane < (d >> 2)) rv = reinterpret_cast<const float4*>(src)[lane];
+    float4 rv[RV];
+#pragma unroll
+    for (int r = 0; r < RV; ++r) {
+      const uint32_t q = uint32_t(r) * G + l;
+      rv[r] = (vec && q < (d >> 2)) ? reinterpret_cast<const float4*>(src)[q]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     const uint64_t set = slabset_of(c, key);
     const uint64_t h2 = xxh64_key(key, kSlabSeed);
     const uint32_t first = W == 1 ? 0u : (W == 2 ? uint32_t(h2 & 1u) : uint32_t(fastmod(h2, W, c.mW)));
     const uint64_t sbase = set * W;
     uint32_t m[W];
-    uint64_t k[W], ct[W];
+    uint64_t k[W][SPL], ct[W][SPL];
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       m[w] = c.masks[sbase + w];
-      k[w] = c.keys[(sbase + w) * kSlotsPerSlab + lane];
-      ct[w] = c.counters[(sbase + w) * kSlotsPerSlab + lane];
+#pragma unroll
+      for (int r = 0; r < SPL; ++r) {
+        k[w][r] = c.keys[(sbase + w) * kSlotsPerSlab + r * G + l];
+        ct[w][r] = c.counters[(sbase + w) * kSlotsPerSlab + r * G + l];
+      }
     }
     // probe in slab order from `first` (slab_cache.cpp:292-310)
     int hit_w = -1, ins_step = -1;
@@ -922,15 +964,20 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
       int w = int(first) + step;
       if (w >= W) w -= W;
       if (hit_w >= 0 || ins_step >= 0) continue;
-      uint64_t kw = 0;
       uint32_t mw = 0;
 #pragma unroll
       for (int x = 0; x < W; ++x)
-        if (x == w) {
-          kw = k[x];
-          mw = m[x];
-        }
-      const uint32_t hb = __ballot_sync(0xFFFFFFFFu, ((mw >> lane) & 1u) && kw == key);
+        if (x == w) mw = m[x];
+      uint32_t hb = 0;
+#pragma unroll
+      for (int r = 0; r < SPL; ++r) {
+        uint64_t kw = 0;
+#pragma unroll
+        for (int x = 0; x < W; ++x)
+          if (x == w) kw = k[x][r];
+        const uint32_t b = __ballot_sync(gm, ((mw >> (r * G + l)) & 1u) && kw == key);
+        hb |= ((b >> gb) & kGroupBits) << (r * G);
+      }
       if (hb) {
         hit_w = w;
         hit_j = __ffs(hb) - 1;
@@ -941,7 +988,7 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
     uint64_t slot = ~0ull;
     if (hit_w >= 0) {
       // resident: recency refresh only, the vector is kept (:283-288)
-      if (lane == hit_j) atomicMax(ctr + (sbase + hit_w) * kSlotsPerSlab + lane, (unsigned long long)stamp);
+      if (l == 0) atomicMax(ctr + (sbase + hit_w) * kSlotsPerSlab + hit_j, (unsigned long long)stamp);
     } else {
       int tw = -1;
       uint32_t tj = 0;
@@ -953,19 +1000,21 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
           int w = int(first) + step;
           if (w >= W) w -= W;
           uint32_t mw = 0;
-          uint64_t cw = 0;
 #pragma unroll
           for (int x = 0; x < W; ++x)
-            if (x == w) {
-              mw = m[x];
-              cw = ct[x];
-            }
+            if (x == w) mw = m[x];
           // terminates: every lost OR returns a mask with more bits set
           while (mw != kFullSlab) {
             const uint32_t j = __ffs(~mw) - 1;  // countr_one(mask) (:299)
-            const uint64_t cj = __shfl_sync(0xFFFFFFFFu, cw, j);
+            uint64_t cv = 0;
+#pragma unroll
+            for (int x = 0; x < W; ++x)
+#pragma unroll
+              for (int r = 0; r < SPL; ++r)
+                if (x == w && uint32_t(r) == j / G) cv = ct[x][r];
+            const uint64_t cj = __shfl_sync(gm, cv, gb + j % G);
             uint32_t old = 0, won = 0;
-            if (lane == 0) {
+            if (l == 0) {
               old = atomicOr(c.masks + sbase + w, 1u << j);
               if (((old >> j) & 1u) == 0u) {
                 // occupied from here on, by this key or by an evictor's
@@ -974,8 +1023,8 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
                                 mine) == cj ? 1u : 0u;
               }
             }
-            old = __shfl_sync(0xFFFFFFFFu, old, 0);
-            won = __shfl_sync(0xFFFFFFFFu, won, 0);
+            old = __shfl_sync(gm, old, gb);
+            won = __shfl_sync(gm, won, gb);
             if (won) {
               tw = w;
               tj = j;
@@ -995,14 +1044,16 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
         uint32_t bi = 0xFFFFFFFFu;
 #pragma unroll
         for (int x = 0; x < W; ++x)
-          if ((ct[x] & kClaimBit) == 0ull && ct[x] < bc) {
-            bc = ct[x];
-            bi = uint32_t(x) * 32 + lane;
-          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, bc, o);
-          const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+          for (int r = 0; r < SPL; ++r)
+            if ((ct[x][r] & kClaimBit) == 0ull && ct[x][r] < bc) {
+              bc = ct[x][r];
+              bi = uint32_t(x) * 32 + uint32_t(r) * G + l;
+            }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          const uint64_t oc = __shfl_xor_sync(gm, bc, o);
+          const uint32_t oi = __shfl_xor_sync(gm, bi, o);
           if (oc < bc || (oc == bc && oi < bi)) {
             bc = oc;
             bi = oi;
@@ -1011,34 +1062,40 @@ __global__ void __launch_bounds__(256, HPSB_RELAX_MINB)
         if (bi == 0xFFFFFFFFu) break;  // every slot of the set claimed by this call
         const uint32_t bw = bi >> 5, bj = bi & 31u;
         unsigned long long old = 0;
-        if (lane == 0) old = atomicCAS(ctr + (sbase + bw) * kSlotsPerSlab + bj, (unsigned long long)bc, mine);
-        old = __shfl_sync(0xFFFFFFFFu, old, 0);
+        if (l == 0) old = atomicCAS(ctr + (sbase + bw) * kSlotsPerSlab + bj, (unsigned long long)bc, mine);
+        old = __shfl_sync(gm, old, gb);
         if (old == bc) {
           tw = int(bw);
           tj = bj;
-        } else if (lane == bj) {
+        } else if (l == bj % G) {
 #pragma unroll
           for (int x = 0; x < W; ++x)
-            if (uint32_t(x) == bw) ct[x] = old;
+#pragma unroll
+            for (int r = 0; r < SPL; ++r)
+              if (uint32_t(x) == bw && uint32_t(r) == bj / G) ct[x][r] = old;
         }
       }
       if (tw >= 0) {
         slot = (sbase + uint64_t(tw)) * kSlotsPerSlab + tj;
-        if (lane == 0) {
+        if (l == 0) {
           c.keys[slot] = key;
           c.tags[slot] = key_tag(h2);
         }
         float* dst = c.rows + slot * d;
         if (vec) {
-          if (lane < (d >> 2)) reinterpret_cast<float4*>(dst)[lane] = rv;
+#pragma unroll
+          for (int r = 0; r < RV; ++r) {
+            const uint32_t q = uint32_t(r) * G + l;
+            if (q < (d >> 2)) reinterpret_cast<float4*>(dst)[q] = rv[r];
+          }
         } else {
-          warp_copy_row(src, dst, d);
+          for (uint32_t x = l; x < d; x += G) dst[x] = src[x];
         }
-      } else if (lane == 0) {
+      } else if (l == 0) {
         atomicAdd(&s_drop, 1ull);
       }
     }
-    if (lane == 0) claimed[i] = slot;
+    if (l == 0) claimed[i] = slot;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1062,12 +1119,17 @@ bool launch_replace_relaxed(const CacheDev& c, const uint64_t* keys, uint64_t n,
                             cudaStream_t st) {
   if (n == 0) return true;
   if (c.W == 0 || c.W > 4) return false;  // wider sets: the exact path
-  const unsigned grid = unsigned((n * 32 + 255) / 256);
+#ifndef HPSB_RELAX_G
+#define HPSB_RELAX_G 16
+#endif
+  // lanes per key: HPSB_RELAX_G for W <= 2, a whole warp for wider sets
+  constexpr int G2 = HPSB_RELAX_G;
+  const unsigned g12 = unsigned((n * G2 + 255) / 256), g34 = unsigned((n * 32 + 255) / 256);
   switch (c.W) {
-    case 1: k_replace_relaxed<1><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
-    case 2: k_replace_relaxed<2><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
-    case 3: k_replace_relaxed<3><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
-    default: k_replace_relaxed<4><<<grid, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    case 1: k_replace_relaxed<1, G2><<<g12, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    case 2: k_replace_relaxed<2, G2><<<g12, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    case 3: k_replace_relaxed<3, 32><<<g34, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
+    default: k_replace_relaxed<4, 32><<<g34, 256, 0, st>>>(c, keys, n, rows, stamp, claimed, dropped); break;
   }
   k_replace_relaxed_release<<<unsigned((n + 255) / 256), 256, 0, st>>>(c, claimed, n, stamp);
   check_launch("replace_relaxed", 2);

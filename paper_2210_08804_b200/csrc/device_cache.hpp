@@ -123,6 +123,18 @@ class DeviceCache {
   const CacheDev& dev() const { return dev_; }
   int keys_per_warp() const { return keys_per_warp_; }
 
+  // Staging of the refresh loop (refresh_cache, engine.cpp), kept across
+  // calls: a periodic refresh reuses its pinned / device buffers (a fresh
+  // 2 x 33.5 MB cudaHostAlloc per pass cost more than the pass's host fetch).
+  struct RefreshBuffers {
+    std::mutex mu;  // one refresh pass of this cache at a time
+    PinnedBuffer h[2];
+    DeviceBuffer dv[2];
+    DeviceBuffer written;
+    std::vector<uint64_t> keys;
+  };
+  RefreshBuffers& refresh_buffers() { return refresh_; }
+
   // ---- engine-facing primitives (caller holds mutex()) ----
   std::mutex& mutex() { return mu_; }
   // grows the replace scratch for calls of up to n keys now (engine reserve)
@@ -232,6 +244,7 @@ class DeviceCache {
     return winner_ + ((updates_++ & 1u) ? cfg_.slabset_count * cfg_.slabs_per_set * 32ull : 0ull);
   }
   DeviceBuffer ubuf_;  // update_device scratch
+  RefreshBuffers refresh_;
   PinnedBuffer qstage_;  // zero-copy host-mode query staging
   static constexpr uint64_t kZeroCopyQueryMax = 65536;
   static constexpr uint64_t kZeroCopyReplaceMax = 256;  // the one-launch replace kernels' limit

@@ -142,15 +142,16 @@ RefreshResult refresh_cache(DeviceCache& cache, VolatileStore* vdb, const std::s
   RefreshResult r;
   const uint32_t d = cache.dimension();
   const uint64_t S = cache.slabset_count();
-  std::vector<uint64_t> keys(S * cache.slabs_per_set() * 32ull);
+  DeviceCache::RefreshBuffers& rb = cache.refresh_buffers();
+  std::lock_guard<std::mutex> lk(rb.mu);
+  std::vector<uint64_t>& keys = rb.keys;
+  keys.resize(S * cache.slabs_per_set() * 32ull);
   keys.resize(cache.dump(0, S, keys.data(), keys.size()));
   if (keys.empty()) return r;
   DeviceGuard g(cache.device());
   cudaStream_t st = cache.stream();
   const uint64_t nb = (keys.size() + dump_batch - 1) / dump_batch;
   struct Stage {
-    PinnedBuffer h;
-    DeviceBuffer dv;
     cudaEvent_t done = nullptr;
     uint64_t* h_keys = nullptr;
     float* h_rows = nullptr;
@@ -159,15 +160,15 @@ RefreshResult refresh_cache(DeviceCache& cache, VolatileStore* vdb, const std::s
   } stage[2];
   std::vector<uint64_t> missing(dump_batch);
   std::vector<int32_t> row_of(dump_batch);
-  DeviceBuffer written_buf;
-  uint64_t* written = static_cast<uint64_t*>(written_buf.ensure(nb * 8, st));
+  uint64_t* written = static_cast<uint64_t*>(rb.written.ensure(nb * 8, st));
   HPSB_CUDA(cudaMemsetAsync(written, 0, nb * 8, st));
-  for (auto& sg : stage) {
+  for (int x = 0; x < 2; ++x) {
+    Stage& sg = stage[x];
     HPSB_CUDA(cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming));
-    char* hp = static_cast<char*>(sg.h.ensure(dump_batch * (8 + uint64_t(d) * 4)));
+    char* hp = static_cast<char*>(rb.h[x].ensure(dump_batch * (8 + uint64_t(d) * 4)));
     sg.h_keys = reinterpret_cast<uint64_t*>(hp);
     sg.h_rows = reinterpret_cast<float*>(hp + dump_batch * 8);
-    char* dp = static_cast<char*>(sg.dv.ensure(dump_batch * (8 + uint64_t(d) * 4) + 256, st));
+    char* dp = static_cast<char*>(rb.dv[x].ensure(dump_batch * (8 + uint64_t(d) * 4) + 256, st));
     sg.d_keys = reinterpret_cast<uint64_t*>(dp);
     sg.d_rows = reinterpret_cast<float*>(dp + (dump_batch * 8 + 255) / 256 * 256);
   }

@@ -125,7 +125,7 @@ void VolatileStore::upsert(Partition& p, uint32_t dim, uint64_t key, const float
     // grow the index to keep load <= 1/2
     if ((p.live + 1) * 2 > p.index.size()) {
       const size_t cap = std::max<size_t>(64, p.index.size() * 2);
-      std::vector<uint32_t> idx(cap, 0);
+      Arena<uint32_t> idx(cap, 0);
       for (size_t s = 0; s < p.index.size(); ++s) {
         const uint32_t v = p.index[s];
         if (!v) continue;

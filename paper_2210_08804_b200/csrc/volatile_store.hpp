@@ -14,7 +14,11 @@
 #pragma once
 
 #include <atomic>
+#include <sys/mman.h>
+
 #include <condition_variable>
+#include <cstdlib>
+#include <new>
 #include <cstdint>
 #include <deque>
 #include <memory>
@@ -66,13 +70,43 @@ class VolatileStore {
   bool last_access(const std::string& name, uint64_t key, uint64_t* out) const;
 
  private:
+  // Arena storage on transparent huge pages (2 MB): a table of 10 M rows of
+  // 512 B is 5 GB, and a miss batch touches its rows at random -- with 4 KB
+  // pages nearly every row copy is also a TLB miss.
+  template <class T>
+  struct HugePageAllocator {
+    using value_type = T;
+    static constexpr size_t kHuge = size_t(2) << 20;
+    HugePageAllocator() = default;
+    template <class U>
+    HugePageAllocator(const HugePageAllocator<U>&) {}
+    T* allocate(size_t n) {
+      const size_t bytes = n * sizeof(T);
+      if (bytes < kHuge) return static_cast<T*>(::operator new(bytes));
+      const size_t rounded = (bytes + kHuge - 1) & ~(kHuge - 1);
+      void* p = std::aligned_alloc(kHuge, rounded);
+      if (p == nullptr) throw std::bad_alloc();
+      (void)::madvise(p, rounded, MADV_HUGEPAGE);
+      return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t n) {
+      if (n * sizeof(T) < kHuge)
+        ::operator delete(p);
+      else
+        std::free(p);
+    }
+    template <class U>
+    bool operator==(const HugePageAllocator<U>&) const { return true; }
+  };
+  template <class T>
+  using Arena = std::vector<T, HugePageAllocator<T>>;
   struct Partition {
     mutable std::shared_mutex mu;
     // open addressing: slot -> entry index + 1 (0 = empty)
-    std::vector<uint32_t> index;
-    std::vector<uint64_t> keys;             // per entry
-    std::vector<uint64_t> last_access;      // per entry (updated with atomic_ref max)
-    std::vector<float> rows;                // entry * dim
+    Arena<uint32_t> index;
+    Arena<uint64_t> keys;                   // per entry
+    Arena<uint64_t> last_access;            // per entry (updated with atomic_ref max)
+    Arena<float> rows;                      // entry * dim
     std::vector<uint32_t> free_entries;
     uint64_t live = 0;
     int64_t find(uint64_t key) const;       // entry or -1
