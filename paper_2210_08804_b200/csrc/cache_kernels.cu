@@ -327,13 +327,15 @@ __device__ __forceinline__ const uint32_t* big_bucket(const ReplaceScratch& rs, 
 // `sk` = 32 keys of per-warp shared memory.
 __device__ __forceinline__ uint32_t small_group(const ReplaceScratch& rs, uint64_t e, uint32_t cnt,
                                                 const uint64_t* __restrict__ keys, uint32_t* sw,
-                                                uint64_t* sk, uint64_t* key) {
+                                                uint64_t* sk, uint64_t* key,
+                                                bool preloaded = false, uint32_t v_in = kNone,
+                                                uint64_t k_in = 0) {
   const uint32_t lane = lane_id();
   uint32_t v = kNone;
   uint64_t k = 0;
   if (lane < kReplaceInline && lane < cnt) {
-    v = rs.idx[e * kReplaceInline + lane];
-    k = rs.kin[e * kReplaceInline + lane];
+    v = preloaded ? v_in : rs.idx[e * kReplaceInline + lane];
+    k = preloaded ? k_in : rs.kin[e * kReplaceInline + lane];
   }
   if (cnt > kReplaceInline) {
     if (lane == 0) {
@@ -405,25 +407,33 @@ struct SetRegs {
 
 // Returns the number of keys inserted into free slots (lane 0's value).
 template <int W>
+__device__ __forceinline__ void load_set(const CacheDev& c, uint64_t set, SetRegs<W>& st) {
+  const uint32_t lane = lane_id();
+  const uint64_t sbase = set * W;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    st.m[w] = c.masks[sbase + w];
+    st.k[w] = c.keys[(sbase + w) * kSlotsPerSlab + lane];
+    st.ct[w] = c.counters[(sbase + w) * kSlotsPerSlab + lane];
+  }
+}
+
+template <int W>
 __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_t set,
                                                   const uint64_t* __restrict__ keys,
                                                   const float* __restrict__ rows, uint64_t stamp,
                                                   uint32_t cnt, uint32_t my_idx,
                                                   uint64_t my_key_in,
-                                                  const uint32_t* __restrict__ big) {
+                                                  const uint32_t* __restrict__ big,
+                                                  const SetRegs<W>& loaded) {
   constexpr int kPre = HPSB_REPL_KPRE;  // rows prefetched (d <= 128, 16 B aligned)
   const uint32_t lane = lane_id();
   const uint32_t d = c.d;
   const uint64_t sbase = set * W;
-  SetRegs<W> st;
+  SetRegs<W> st = loaded;  // loaded with the set's count and inline keys
   uint32_t m0[W];
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    st.m[w] = c.masks[sbase + w];
-    m0[w] = st.m[w];
-    st.k[w] = c.keys[(sbase + w) * kSlotsPerSlab + lane];
-    st.ct[w] = c.counters[(sbase + w) * kSlotsPerSlab + lane];
-  }
+  for (int w = 0; w < W; ++w) m0[w] = st.m[w];
   // lane j < cnt: key and first-slab hash of the j-th key (small groups)
   uint64_t my_key = 0, my_h2 = 0;
   if (big == nullptr && my_idx != kNone) {
@@ -585,11 +595,25 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
     const uint32_t en = wn < n ? rs.lead_e[wn] : kNone;
     const uint32_t sn = wn < n ? rs.lead_s[wn] : 0u;
     const uint64_t set = sset;
+    // ONE round trip: the set's key count, its inline key indices and keys
+    // (read whatever the count; entries past it are ignored) and the set's
+    // masks / keys / counters -- all depend only on the list entry
     const uint32_t cnt = uint32_t(rs.ent[e]);
+    const uint32_t lane = lane_id();
+    uint32_t v_in = kNone;
+    uint64_t k_in = 0;
+    if (lane < kReplaceInline) {
+      v_in = rs.idx[uint64_t(e) * kReplaceInline + lane];
+      k_in = rs.kin[uint64_t(e) * kReplaceInline + lane];
+    }
+    SetRegs<W == 0 ? 1 : W> pre;
+    if constexpr (W > 0) {
+      if (!rejected) load_set<W>(c, set, pre);
+    }
     if (!rejected) {
       uint64_t k = 0;
       const uint32_t v = cnt <= 32 ? small_group(rs, e, cnt, keys, s_w[threadIdx.x >> 5],
-                                                 s_k[threadIdx.x >> 5], &k)
+                                                 s_k[threadIdx.x >> 5], &k, true, v_in, k_in)
                                    : kNone;
       const uint32_t* b = cnt <= 32 ? nullptr : big_bucket(rs, e, cnt);
       if constexpr (W == 0) {
@@ -598,7 +622,7 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
           warp_replace_key(c, set, keys[ij], rows + uint64_t(ij) * c.d, stamp);
         }
       } else {
-        inserted += replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b);
+        inserted += replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b, pre);
       }
     }
     __syncwarp();

@@ -1,0 +1,11 @@
+#!/bin/bash
+# exact replace: set state + count + inline keys in one round trip (A/B vs prev); replace parity
+tag=${1:-r02m}
+out=gpurun_out/$tag; mkdir -p $out
+timeout 900 python -m pytest tests/test_cache_gpu.py tests/test_headline_gpu.py -x -q -m gpu > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log
+for v in base prev base prev; do
+  if [ $v = base ]; then timeout 600 python tools/bench_replace.py --reps 40 >> $out/replace_$v.json 2>> $out/replace.err;
+  else HPSB_LIB_VARIANT=$v timeout 600 python tools/bench_replace.py --reps 40 >> $out/replace_$v.json 2>> $out/replace.err; fi
+done
+timeout 600 python tools/bench_replace.py --reps 40 --check > $out/replace_check.json 2>> $out/replace.err
+ls -la $out
