@@ -394,6 +394,49 @@ void LookupEngine::rows_d2h(Workspace& ws, const LookupCall& c, cudaStream_t st)
   }
 }
 
+void LookupEngine::host_scatter(Workspace& ws, const LookupCall& c, uint64_t um, uint8_t* hflags) {
+  // found misses (ws.h_miss_keys in miss order, ws.h_row_of: staged row or -1)
+  uint64_t cap = 16;
+  while (cap < 2 * um) cap <<= 1;
+  if (ws.hs_keys.size() < cap) {
+    ws.hs_keys.resize(cap);
+    ws.hs_rows.resize(cap);
+    ws.hs_used.resize(cap);
+  }
+  std::fill(ws.hs_used.begin(), ws.hs_used.begin() + cap, uint8_t(0));
+  const uint64_t mask = cap - 1;
+  bool any = false;
+  for (uint64_t k = 0; k < um; ++k) {
+    if (ws.h_row_of[k] < 0) continue;
+    any = true;
+    const uint64_t key = ws.h_miss_keys[k];
+    uint64_t h = fmix64(key) & mask;
+    while (ws.hs_used[h]) h = (h + 1) & mask;
+    ws.hs_used[h] = 1;
+    ws.hs_keys[h] = key;
+    ws.hs_rows[h] = ws.h_row_of[k];
+  }
+  if (!any) return;
+  const uint32_t d = dim_;
+  const size_t n = c.n;
+  const size_t chunks = std::min<size_t>(copy_threads_.size(), (n + 4095) / 4096);
+  const size_t per = (n + chunks - 1) / chunks;
+  copy_threads_.parallel_for(chunks, 1, [&](size_t cb, size_t ce) {
+    for (size_t ch = cb; ch < ce; ++ch) {
+      const size_t e = std::min(n, (ch + 1) * per);
+      for (size_t p = ch * per; p < e; ++p) {
+        if (!hflags[p]) continue;
+        const uint64_t key = c.h_keys[p];
+        uint64_t h = fmix64(key) & mask;
+        while (ws.hs_used[h] && ws.hs_keys[h] != key) h = (h + 1) & mask;
+        if (!ws.hs_used[h]) continue;  // absent from every tier: default row, flagged
+        std::memcpy(c.out + p * d, ws.h_staged + uint64_t(ws.hs_rows[h]) * d, d * 4ull);
+        hflags[p] = 0;
+      }
+    }
+  });
+}
+
 void LookupEngine::rows_to_pageable(Workspace& ws, const LookupCall& c) {
   const uint64_t bytes = c.n * uint64_t(dim_) * 4;
   const int nch = ws.out_chunks;
@@ -496,7 +539,12 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
     DeviceGuard g(cache_->device());
     cudaStream_t st = cache_->stream();
     ws->ensure(std::max<size_t>(n, 1), d, st);
-    c.spec_rows = host && last_async_.load(std::memory_order_relaxed);
+    // host mode: rows and flags always come back with the counts -- an
+    // async call's rows are final as the kernel leaves them, and a sync
+    // call's fetched rows are scattered into the host output on the host
+    // (host_scatter) while the cache fill runs on
+    c.spec_rows = host;
+    c.h_keys = host ? keys : nullptr;
     c.out_pinned = host && n > 0 && is_pinned(out);
     c.flags_pinned = host && n > 0 && is_pinned(flags);
     c.d_keys = keys;
@@ -575,6 +623,7 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
           HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, c.d_flags, n,
                                     cudaMemcpyDeviceToHost, st));
           rows_d2h(*ws, c, st);
+          HPSB_CUDA(cudaEventRecord(ws->rows_ready, st));
         }
       } else {
         HPSB_CUDA(cudaEventRecord(ws->counts_ready, st));
@@ -654,7 +703,17 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
     defaults = absent;
     std::lock_guard<std::mutex> lk(cache_->mutex());
     tr.mark("lock");
-    if (nf > 0) {
+    if (host && !c.packed && c.spec_rows) {
+      // rows and flags are already crossing to the host: the fetched rows go
+      // into the host output there (below); on the device only the fill
+      if (nf > 0) {
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                  cudaMemcpyHostToDevice, st));
+        HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                  cudaMemcpyHostToDevice, st));
+        cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+      }
+    } else if (nf > 0) {
       // row_of is in miss order; the scatter kernel indexes by claim
       for (uint64_t k = 0; k < um; ++k) ws->h_row_of_claim[ws->order[k]] = ws->h_row_of[k];
       if (c.packed) {
@@ -706,17 +765,26 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
       if (!c.out_direct) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
       std::memcpy(flags, c.hfl, n);
     } else if (host) {
-      if (sync_branch || !c.spec_rows) {
+      if (!c.spec_rows) {
         HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
                                   cudaMemcpyDeviceToHost, st));
         rows_d2h(*ws, c, st);
+        HPSB_CUDA(cudaEventRecord(ws->rows_ready, st));
         HPSB_CUDA(cudaEventRecord(ws->done, st));
       }
       // pageable rows: copied on chunk by chunk as they land
       if (!c.out_pinned) rows_to_pageable(*ws, c);
-      HPSB_CUDA(cudaEventSynchronize(ws->done));
+      HPSB_CUDA(cudaEventSynchronize(ws->rows_ready));
       tr.mark("rows");
-      ws->pending = false;
+      uint8_t* hf = c.flags_pinned ? flags : ws->h_flags;
+      if (sync_branch && um > 0) {
+        host_scatter(*ws, c, um, hf);
+        tr.mark("scatter");
+      }
+      if (!sync_branch) {
+        HPSB_CUDA(cudaEventSynchronize(ws->done));
+        ws->pending = false;
+      }  // sync: the fill runs on behind the return (ws->done, wait_idle)
       if (!c.flags_pinned) std::memcpy(flags, ws->h_flags, n);
     } else {
       cache_->join_to(c.user);

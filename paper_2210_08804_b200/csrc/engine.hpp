@@ -108,6 +108,11 @@ struct Workspace {
   int32_t* h_row_of_claim = nullptr;   // staged row per claim (sync branch)
   char* h_hdr = nullptr;               // zero-copy calls: [counts | firsts | keys | flags]
   std::vector<uint32_t> order;         // claims sorted by first position
+  // sync branch of a host-mode call: found miss key -> staged row (open
+  // addressing; hs_used marks occupied entries, every u64 is a legal key)
+  std::vector<uint64_t> hs_keys;
+  std::vector<int32_t> hs_rows;
+  std::vector<uint8_t> hs_used;
   // batch state (for the async task)
   std::vector<uint64_t> missing_keys;
   cudaEvent_t done = nullptr;
@@ -231,9 +236,14 @@ class LookupEngine {
     const uint64_t* hck = nullptr;
     const uint8_t* hfl = nullptr;
     const uint64_t* d_keys = nullptr;
+    const uint64_t* h_keys = nullptr;  // host mode: the caller's keys
     float* d_out = nullptr;
     uint8_t* d_flags = nullptr;
   };
+  // Sync branch of a host-mode call whose rows came back with the counts:
+  // the fetched rows are written straight into the host output at every
+  // position of their key (and those flags cleared) by the copy threads.
+  void host_scatter(Workspace& ws, const LookupCall& c, uint64_t um, uint8_t* hflags);
   LookupCall begin(const uint64_t* keys, size_t n, float* out, size_t out_len, uint8_t* flags,
                    int mem, cudaStream_t user);
   void finish(LookupCall& c, LookupOutcome* outcome);
