@@ -49,7 +49,7 @@ def test_mode_switch_and_validation():
     assert c.occupied() == 0
 
 
-@pytest.mark.parametrize("W,d", [(1, 8), (2, 32), (3, 16), (4, 128)])
+@pytest.mark.parametrize("W,d", [(1, 8), (2, 32), (3, 16), (4, 128), (2, 3), (2, 200), (1, 130)])
 def test_relaxed_fill_admits_every_key_when_sets_have_room(W, d):
     S = 97
     rng = np.random.default_rng(W)
@@ -69,14 +69,15 @@ def test_relaxed_fill_admits_every_key_when_sets_have_room(W, d):
     assert len(pos) == 0 and out.tobytes() == rows.tobytes()
 
 
-def test_relaxed_eviction_under_contention():
+@pytest.mark.parametrize("d", [16, 200])
+def test_relaxed_eviction_under_contention(d):
     """A full, tiny cache (16 sets) and a replace 3x its capacity: every set
     over-subscribed. Keys of one call never evict each other, so each set
     ends with min(64, its keys) new keys -- exactly the number the exact mode
     keeps (its last 64 in input order); rows stay bit-exact."""
     import torch
 
-    S, W, d = 16, 2, 16
+    S, W = 16, 2
     c = mk(S, W, d)
     old = np.arange(10_000, 10_000 + S * W * 32 * 2, dtype=np.uint64)
     c.replace(old, row_values(old, d, 2))  # fills (the rest of `old` is dropped)
