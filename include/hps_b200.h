@@ -52,6 +52,7 @@ typedef struct hps_engine hps_engine;
 typedef struct hps_multi hps_multi;
 typedef struct hps_pdb hps_pdb;
 typedef struct hps_replicas hps_replicas;
+typedef struct hps_peer_group hps_peer_group;
 
 /* ---- vocabulary ------------------------------------------------------- */
 
@@ -457,6 +458,35 @@ int hps_shard_scatter(int device, const uint64_t* keys, size_t n, uint32_t world
 int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_pos,
                       const float* rows, const uint8_t* flags_in, float* out, uint8_t* flags_out,
                       void* stream);
+
+/* ---- key-hash-sharded lookup over PEER MEMORY (the B200-native
+ *      alternative to the two all-to-alls; no reference counterpart). Every
+ *      rank exports its shard cache (CUDA IPC handles of its probe
+ *      structures, rows and a miss inbox; the caller ships the blob to the
+ *      other ranks over any transport), then maps every rank's shard. A
+ *      lookup is ONE kernel: each key's owner shard is probed through mapped
+ *      (NVLink peer) memory, the owner's counter stamped, its row copied
+ *      straight into `out`; misses get default_row + flag and are appended
+ *      to the owner's inbox. Owners admit their inbox keys between lookup
+ *      phases (hps_cache_peer_drain, then a fetch + replace of their own);
+ *      no peer may look up while an owner mutates its shard. Recency: the
+ *      requester's own shard clock ticks once per call and stamps every
+ *      owner's hits (ranks step together). ---- */
+size_t hps_peer_blob_size(void);
+/* inbox_cap: miss keys the inbox holds between drains (first export only) */
+int hps_cache_peer_export(hps_cache* cache, uint64_t inbox_cap, void* blob, size_t blob_cap,
+                          size_t* blob_len);
+/* blobs: world blobs of blob_len bytes each, rank order; self = this rank's cache */
+int hps_peer_group_create(hps_cache* self, uint32_t rank, uint32_t world, const void* blobs,
+                          size_t blob_len, hps_peer_group** out);
+int hps_peer_group_destroy(hps_peer_group* group);
+/* device pointers: keys[n], out[n * dim], miss_flags[n], default_row[dim] */
+int hps_peer_lookup_device(hps_peer_group* group, const uint64_t* keys, size_t n, float* out,
+                           uint8_t* miss_flags, const float* default_row, void* stream);
+/* this shard's inbox: up to cap keys into keys_out (host), *n_appended = keys
+ * appended since the last drain (beyond the inbox capacity they were
+ * dropped); empties the inbox */
+int hps_cache_peer_drain(hps_cache* cache, uint64_t* keys_out, size_t cap, size_t* n_appended);
 
 /* ---- wire LOOKUP response frame (replaces encode_response_frame for
  *      Opcode::Lookup, wire.cpp:174-188; layout wire.hpp:18-21, byte-exact:

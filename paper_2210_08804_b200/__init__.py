@@ -147,6 +147,13 @@ SIGNATURES = {
     "hps_cache_replace": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, C.c_int, _P]),
     "hps_cache_replace_device_async": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P]),
     "hps_cache_set_replace_mode": (C.c_int, [_P, C.c_int]),
+    "hps_peer_blob_size": (C.c_size_t, []),
+    "hps_cache_peer_export": (C.c_int, [_P, C.c_uint64, _P, C.c_size_t, _SZP]),
+    "hps_peer_group_create": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, C.c_size_t,
+                                        C.POINTER(_P)]),
+    "hps_peer_group_destroy": (C.c_int, [_P]),
+    "hps_peer_lookup_device": (C.c_int, [_P, _P, C.c_size_t, _P, _P, _P, _P]),
+    "hps_cache_peer_drain": (C.c_int, [_P, _P, C.c_size_t, _SZP]),
     "hps_cache_get_replace_mode": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "hps_cache_update": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _SZP, C.c_int, _P]),
     "hps_cache_dump": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_size_t, _SZP]),
@@ -455,6 +462,23 @@ class SlabCache:
         m = C.c_int(0)
         _check(lib().hps_cache_get_replace_mode(self._h, C.byref(m), None))
         return m.value
+
+    def peer_export(self, inbox_cap: int = 1 << 20) -> bytes:
+        """This shard's peer-mapping blob (CUDA IPC handles + geometry + a miss
+        inbox of inbox_cap keys): ship it to the other ranks."""
+        n = lib().hps_peer_blob_size()
+        buf = C.create_string_buffer(n)
+        ln = C.c_size_t(0)
+        _check(lib().hps_cache_peer_export(self._h, inbox_cap, buf, n, C.byref(ln)))
+        return buf.raw[: ln.value]
+
+    def peer_drain(self, cap: int = 1 << 20) -> np.ndarray:
+        """Keys peers appended to this shard's miss inbox since the last
+        drain (input order unspecified, duplicates possible); empties it."""
+        out = np.empty(max(cap, 1), dtype=np.uint64)
+        n = C.c_size_t(0)
+        _check(lib().hps_cache_peer_drain(self._h, _ptr(out), cap, C.byref(n)))
+        return out[: min(n.value, cap)].copy()
 
     def relaxed_dropped(self) -> int:
         """Keys the relaxed mode has not admitted so far."""

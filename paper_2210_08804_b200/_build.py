@@ -25,7 +25,7 @@ FLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 
 SOURCES = ["cache_kernels.cu", "lookup_kernels.cu", "shard_kernels.cu", "wire.cu", "device_cache.cpp", "volatile_store.cpp", "segment_store.cpp",
-           "engine.cpp", "capi.cpp"]
+           "peer.cpp", "engine.cpp", "capi.cpp"]
 
 
 def _newest_header() -> float:

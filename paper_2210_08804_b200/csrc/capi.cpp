@@ -10,13 +10,19 @@
 #include <string>
 #include <vector>
 
+#include <cstring>
+
 #include "device_cache.hpp"
+#include "peer.hpp"
 #include "engine.hpp"
 #include "segment_store.hpp"
 #include "volatile_store.hpp"
 
 struct hps_cache {
   std::unique_ptr<hpsb::DeviceCache> impl;
+};
+struct hps_peer_group {
+  std::unique_ptr<hpsb::PeerGroup> impl;
 };
 struct hps_vdb {
   std::unique_ptr<hpsb::VolatileStore> impl;
@@ -447,6 +453,55 @@ int hps_cache_replace_device_async(hps_cache* cache, const uint64_t* keys, size_
          "replace vector buffer has wrong size");
     need(n == 0 || (keys && vectors), "null argument");
     cache->impl->replace_device_async(keys, n, vectors, as_stream(stream));
+  });
+}
+
+size_t hps_peer_blob_size(void) { return sizeof(hpsb::PeerBlob); }
+
+int hps_cache_peer_export(hps_cache* cache, uint64_t inbox_cap, void* blob, size_t blob_cap,
+                          size_t* blob_len) {
+  return guarded([&] {
+    need(cache && blob && blob_len, "null argument");
+    need(blob_cap >= sizeof(hpsb::PeerBlob), "peer blob buffer too small");
+    hpsb::PeerBlob b;
+    cache->impl->peer_export(inbox_cap, &b);
+    std::memcpy(blob, &b, sizeof(b));
+    *blob_len = sizeof(b);
+  });
+}
+
+int hps_peer_group_create(hps_cache* self, uint32_t rank, uint32_t world, const void* blobs,
+                          size_t blob_len, hps_peer_group** out) {
+  return guarded([&] {
+    need(self && blobs && out, "null argument");
+    need(blob_len == sizeof(hpsb::PeerBlob), "peer blob size mismatch");
+    std::vector<hpsb::PeerBlob> v(world);
+    for (uint32_t r = 0; r < world; ++r)
+      std::memcpy(&v[r], static_cast<const char*>(blobs) + size_t(r) * blob_len, blob_len);
+    auto g = std::make_unique<hps_peer_group>();
+    g->impl = std::make_unique<hpsb::PeerGroup>(*self->impl, rank, v);
+    *out = g.release();
+  });
+}
+
+int hps_peer_group_destroy(hps_peer_group* group) {
+  return guarded([&] { delete group; });
+}
+
+int hps_peer_lookup_device(hps_peer_group* group, const uint64_t* keys, size_t n, float* out,
+                           uint8_t* miss_flags, const float* default_row, void* stream) {
+  return guarded([&] {
+    need(group != nullptr, "null argument");
+    need(n == 0 || (keys && out && miss_flags && default_row), "null argument");
+    need(n < 0xFFFFFFFFull, "lookup batch too large");
+    group->impl->lookup(keys, n, out, miss_flags, default_row, as_stream(stream));
+  });
+}
+
+int hps_cache_peer_drain(hps_cache* cache, uint64_t* keys_out, size_t cap, size_t* n_appended) {
+  return guarded([&] {
+    need(cache && n_appended && (cap == 0 || keys_out), "null argument");
+    *n_appended = cache->impl->peer_drain(keys_out, cap);
   });
 }
 

@@ -166,6 +166,7 @@ DeviceCache::~DeviceCache() {
   cudaFree(dev_.occupied);
   cudaFree(d_small_);
   cudaFreeHost(h_small_);
+  cudaFree(inbox_);
   cudaFree(scan_.tile_ctr);
   cudaFree(scan_.status);
   cudaFree(trace_);
@@ -590,6 +591,57 @@ void DeviceCache::launch_replace_mode(const uint64_t* d_keys, uint64_t n, const 
     return;
   }
   launch_replace(dev_, d_keys, n, d_rows, stamp, validate, rs, stream_, device_);
+}
+
+void DeviceCache::peer_export(uint64_t inbox_cap, PeerBlob* out) {
+  std::lock_guard<std::mutex> lk(mu_);
+  DeviceGuard g(device_);
+  if (inbox_ == nullptr) {
+    if (inbox_cap == 0) throw invalid_argument("peer inbox capacity must be positive");
+    HPSB_CUDA(cudaMalloc(&inbox_, 256 + inbox_cap * 8));
+    HPSB_CUDA(cudaMemsetAsync(inbox_, 0, 256, stream_));
+    HPSB_CUDA(cudaStreamSynchronize(stream_));
+    inbox_cap_ = inbox_cap;
+  }
+  PeerBlob b;
+  b.magic = kPeerBlobMagic;
+  b.S = cfg_.slabset_count;
+  b.W = cfg_.slabs_per_set;
+  b.d = cfg_.dimension;
+  const char* pm = static_cast<const char*>(probe_mem_);
+  b.tags_off = uint64_t(reinterpret_cast<const char*>(dev_.tags) - pm);
+  b.masks_off = uint64_t(reinterpret_cast<const char*>(dev_.masks) - pm);
+  b.ctr_off = uint64_t(reinterpret_cast<const char*>(dev_.counters) - pm);
+  b.inbox_cap = inbox_cap_;
+  b.device = device_;
+  HPSB_CUDA(cudaIpcGetMemHandle(&b.probe, probe_mem_));
+  HPSB_CUDA(cudaIpcGetMemHandle(&b.rows, dev_.rows));
+  HPSB_CUDA(cudaIpcGetMemHandle(&b.inbox, inbox_));
+  *out = b;
+}
+
+void DeviceCache::peer_inbox(unsigned long long** count, uint64_t** keys, uint64_t* cap) const {
+  if (inbox_ == nullptr) throw invalid_argument("cache is not exported for peers");
+  *count = static_cast<unsigned long long*>(inbox_);
+  *keys = reinterpret_cast<uint64_t*>(static_cast<char*>(inbox_) + 256);
+  *cap = inbox_cap_;
+}
+
+size_t DeviceCache::peer_drain(uint64_t* out, size_t cap) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (inbox_ == nullptr) throw invalid_argument("cache is not exported for peers");
+  mark_other_op();
+  DeviceGuard g(device_);
+  // the peers' appends are done (caller's contract); the device is
+  // synchronised so appends from other streams / processes have landed
+  HPSB_CUDA(cudaDeviceSynchronize());
+  HPSB_CUDA(cudaMemcpy(h_small_ + 5, inbox_, 8, cudaMemcpyDeviceToHost));
+  const uint64_t appended = h_small_[5];
+  const uint64_t m = std::min<uint64_t>({appended, inbox_cap_, uint64_t(cap)});
+  if (m > 0)
+    HPSB_CUDA(cudaMemcpy(out, static_cast<char*>(inbox_) + 256, m * 8, cudaMemcpyDeviceToHost));
+  HPSB_CUDA(cudaMemset(inbox_, 0, 8));
+  return size_t(appended);
 }
 
 void DeviceCache::set_replace_mode(int mode) {

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "kernels.hpp"
+#include "peer.hpp"
 #include "runtime.hpp"
 
 namespace hpsb {
@@ -135,6 +136,17 @@ class DeviceCache {
   };
   RefreshBuffers& refresh_buffers() { return refresh_; }
 
+  // ---- peer-memory sharded mode (peer.hpp) ----
+  // Exports this shard for peers: IPC handles of the probe structures, the
+  // rows and a miss inbox of inbox_cap keys (allocated on the first export).
+  void peer_export(uint64_t inbox_cap, PeerBlob* out);
+  void peer_inbox(unsigned long long** count, uint64_t** keys, uint64_t* cap) const;
+  // Takes the keys peers appended to this shard's inbox since the last
+  // drain (up to cap into out; returns how many were appended, which may
+  // exceed the inbox capacity -- the rest were dropped) and empties it. Call
+  // only between lookup phases (no peer may be appending).
+  size_t peer_drain(uint64_t* out, size_t cap);
+
   // ---- engine-facing primitives (caller holds mutex()) ----
   std::mutex& mutex() { return mu_; }
   // grows the replace scratch for calls of up to n keys now (engine reserve)
@@ -244,6 +256,8 @@ class DeviceCache {
     return winner_ + ((updates_++ & 1u) ? cfg_.slabset_count * cfg_.slabs_per_set * 32ull : 0ull);
   }
   DeviceBuffer ubuf_;  // update_device scratch
+  void* inbox_ = nullptr;  // peer miss inbox: [u64 count | 248 B pad | keys]
+  uint64_t inbox_cap_ = 0;
   RefreshBuffers refresh_;
   PinnedBuffer qstage_;  // zero-copy host-mode query staging
   static constexpr uint64_t kZeroCopyQueryMax = 65536;

@@ -18,7 +18,9 @@
 
 #include "common.cuh"
 #include "kernels.hpp"
+#include "peer.hpp"
 #include "probe.cuh"
+#include "tag_probe.cuh"
 
 namespace hpsb {
 
@@ -107,6 +109,108 @@ void launch_shard_unroute(uint64_t m, uint32_t d, const uint32_t* send_pos, cons
   k_shard_unroute<<<unsigned((m * 32 + 255) / 256), 256, 0, st>>>(m, d, send_pos, rows, flags_in,
                                                                   out, flags_out);
   check_launch("shard_unroute", 1);
+}
+
+// ------------------------------------------------ peer-memory lookup --
+// Lane per position (peer.hpp): owner = shard_of(key); the owner's slabs are
+// probed through its mapped memory (fingerprints + masks in one round trip,
+// key verification -- tag_probe.cuh), a hit stamps the owner's counter
+// (atomicMax, one lane per distinct (owner, slot) of the warp) and the
+// owner's row is read straight into the local output (a warp streams its 32
+// rows, 4 rows in flight); a miss writes the default row, sets the flag and
+// appends the key once per warp to the owner's inbox.
+__global__ void __launch_bounds__(256)
+    k_peer_lookup(const PeerShard* __restrict__ shards, uint32_t world,
+                  const uint64_t* __restrict__ keys, uint64_t n, float* __restrict__ out,
+                  uint8_t* __restrict__ flags, const float* __restrict__ default_row, uint32_t d,
+                  uint64_t stamp) {
+  __shared__ PeerShard s_sh[kMaxPeers];
+  for (uint32_t i = threadIdx.x; i < world; i += blockDim.x) s_sh[i] = shards[i];
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint64_t pos = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t base = pos - lane;
+  if (base >= n) return;  // whole warp past the end
+  const bool valid = pos < n;
+  const uint64_t key = valid ? keys[pos] : 0ull;
+  const uint32_t owner = valid ? shard_of_key(key, world) : 0u;
+  const PeerShard& sh = s_sh[owner];
+  const uint32_t res = lane_probe(sh.c, key, valid);
+  const bool hit = res != kNoSlot;
+  // recency: one atomic per distinct (owner, slot) of the warp
+  const uint64_t tag = hit ? ((uint64_t(owner) << 32) | res) : ~0ull;
+  const uint32_t same = __match_any_sync(0xFFFFFFFFu, tag);
+  if (hit && (__ffs(same) - 1) == lane)
+    atomicMax(reinterpret_cast<unsigned long long*>(sh.c.counters) + res,
+              (unsigned long long)stamp);
+  // misses: one inbox append per distinct key of the warp
+  const bool miss = valid && !hit;
+  // (every lane runs both warp-collective calls: no short-circuit around them)
+  const uint32_t same_key = __match_any_sync(0xFFFFFFFFu, miss ? key : 0ull);
+  const uint32_t missing = __ballot_sync(0xFFFFFFFFu, miss);
+  if (miss && (__ffs(same_key & missing) - 1) == lane) {
+    const unsigned long long at = atomicAdd(sh.inbox_count, 1ull);
+    if (at < sh.inbox_cap) sh.inbox_keys[at] = key;
+  }
+  if (valid) flags[pos] = miss ? 1 : 0;
+  // rows: the warp's 32 rows, each row by all lanes, 4 rows in flight
+  const float* src = hit ? sh.c.rows + uint64_t(res) * d : default_row;
+  const uint32_t nrows = n - base < 32 ? uint32_t(n - base) : 32u;
+  const bool vec = (d & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(default_row) & 15u) == 0;
+  if (vec) {
+    const uint32_t q4 = d >> 2;
+    for (uint32_t r0 = 0; r0 < nrows; r0 += 4) {
+      float4 x[4][2];
+      const float4* sp[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = r0 + u;
+        sp[u] = reinterpret_cast<const float4*>(__shfl_sync(0xFFFFFFFFu,
+                                                            reinterpret_cast<uintptr_t>(src), r & 31u));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t q = lane + 32u * h;
+          if (r < nrows && q < q4) x[u][h] = sp[u][q];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = r0 + u;
+        float4* dp = reinterpret_cast<float4*>(out + (base + r) * d);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t q = lane + 32u * h;
+          if (r < nrows && q < q4) dp[q] = x[u][h];
+        }
+      }
+      // rows wider than 256 floats: the rest, row by row
+      if (q4 > 64) {
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t r = r0 + u;
+          if (r >= nrows) break;
+          float4* dp = reinterpret_cast<float4*>(out + (base + r) * d);
+          for (uint32_t q = 64 + lane; q < q4; q += 32) dp[q] = sp[u][q];
+        }
+      }
+    }
+  } else {
+    for (uint32_t r = 0; r < nrows; ++r) {
+      const float* sr = reinterpret_cast<const float*>(
+          __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(src), r));
+      float* dr = out + (base + r) * d;
+      for (uint32_t x = lane; x < d; x += 32) dr[x] = sr[x];
+    }
+  }
+}
+
+void launch_peer_lookup(const PeerShard* d_shards, uint32_t world, const uint64_t* keys,
+                        uint64_t n, float* out, uint8_t* flags, const float* default_row,
+                        uint32_t d, uint64_t stamp, cudaStream_t st) {
+  if (n == 0) return;
+  k_peer_lookup<<<unsigned((n + 255) / 256), 256, 0, st>>>(d_shards, world, keys, n, out, flags,
+                                                          default_row, d, stamp);
+  check_launch("peer_lookup", 1);
 }
 
 }  // namespace hpsb

@@ -179,3 +179,80 @@ class ShardedLookup:
         flags_out = torch.empty(n, dtype=torch.uint8, device=keys.device)
         self.ops.unroute(send_pos, back_rows, back_flags, out, flags_out, d)
         return out, flags_out, tuple(owner_side)
+
+
+class PeerShardedLookup:
+    """The key-hash-sharded lookup over PEER MEMORY (SURVEY §8e's B200-native
+    alternative; include/hps_b200.h hps_peer_*): each rank exports its shard
+    cache, the blobs are exchanged once (``all_gather_object``), and every
+    rank maps every shard. A lookup is then ONE kernel on the requester --
+    route, probe the owner's slabs, stamp, copy the owner's row over NVLink
+    into the local output, append misses to the owner's inbox -- with no
+    collective on the data path. ``fill`` is the owner side: between lookup
+    phases (a barrier on each side) every owner drains its inbox, fetches the
+    keys from its tiers and admits them into its shard."""
+
+    def __init__(self, cache, group=None, inbox_cap: int = 1 << 20, device: int = 0):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.cache = cache
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = device
+        self.inbox_cap = inbox_cap
+        blob = cache.peer_export(inbox_cap)
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, blob, group=group)
+        self._blobs = b"".join(blobs)
+        self._h = C.c_void_p()
+        _check(lib().hps_peer_group_create(cache.handle, self.rank, self.world, self._blobs,
+                                           len(blob), C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hps_peer_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def lookup(self, keys, default_row, stream: int = 0):
+        """keys: int64 CUDA tensor of this rank's batch; default_row: float32
+        CUDA tensor of dim floats. Returns (rows [n*dim], miss flags [n]) --
+        stream-ordered on `stream` (default: the current stream)."""
+        import torch
+
+        n = keys.numel()
+        d = self.cache.dimension()
+        out = torch.empty(max(n, 1) * d, device=keys.device)
+        flags = torch.empty(max(n, 1), dtype=torch.uint8, device=keys.device)
+        st = stream or torch.cuda.current_stream(self.device).cuda_stream
+        _check(lib().hps_peer_lookup_device(self._h, keys.data_ptr(), n, out.data_ptr(),
+                                            flags.data_ptr(), default_row.data_ptr(), st))
+        return out[: n * d], flags[:n]
+
+    def fill(self, fetch: Callable) -> int:
+        """Owner side, collective: after every rank's lookups (barrier), drain
+        this shard's inbox, fetch its unique keys (``fetch(keys) -> (found
+        keys, rows)``, e.g. a VolatileStore lookup) and admit them; a second
+        barrier before anyone looks up again. Returns the keys admitted."""
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)
+        keys = np.unique(self.cache.peer_drain(self.inbox_cap))
+        admitted = 0
+        if len(keys):
+            fk, rows = fetch(keys)
+            if len(fk):
+                self.cache.replace(fk, rows)
+                admitted = len(fk)
+        self.dist.barrier(group=self.group)
+        return admitted

@@ -306,3 +306,89 @@ def test_sharded_engine_lookup_world_one_nccl_matches_engine_oracle():
         assert cache.occupied() == eo.cache.occupied()
     finally:
         dist.destroy_process_group()
+
+
+def _peer_worker(rank, world, port, q):
+    """Peer-memory sharded lookup (hps_peer_*): `world` processes on cuda:0,
+    each owning one shard; the shards are mapped through CUDA IPC (NVLink peer
+    memory on a multi-GPU node). Every position's row / flag must equal what
+    its owner shard holds; the owners admit their inboxes between steps."""
+    import faulthandler
+    import sys
+    import traceback
+
+    # a stuck worker dumps its stack and exits instead of hanging the suite
+    faulthandler.dump_traceback_later(150, exit=True, file=sys.stderr)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=__import__("datetime").timedelta(seconds=120))
+    try:
+        torch.cuda.set_device(0)
+        cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=64, slabs_per_set=2, dimension=D))
+        peer = sharded.PeerShardedLookup(cache, inbox_cap=1 << 14)
+        vdb = {int(k): r for k, r in zip(range(0, KEYSPACE, 2),
+                                         key_rows(np.arange(0, KEYSPACE, 2)).reshape(-1, D))}
+
+        def fetch(keys):
+            fk = np.array([k for k in keys if int(k) in vdb], dtype=np.uint64)
+            rows = (np.concatenate([vdb[int(k)] for k in fk]) if len(fk)
+                    else np.empty(0, np.float32))
+            return fk, rows.astype(np.float32)
+
+        default = torch.full((D,), -7.0, device="cuda")
+        resident = set()
+        ok = True
+        for step in range(4):
+            rng = np.random.default_rng(500 * rank + step)
+            batch = rng.integers(0, KEYSPACE, 1500 + 111 * rank, dtype=np.uint64)
+            batch[:4] = [0, 2, 4, 6]  # shared across ranks: duplicates across requesters
+            out, fl = peer.lookup(torch.from_numpy(batch.view(np.int64)).cuda(), default)
+            torch.cuda.synchronize()
+            got = out.cpu().numpy().reshape(-1, D)
+            flags = fl.cpu().numpy()
+            res = np.array([int(k) in resident for k in batch])
+            want = key_rows(batch).reshape(-1, D)
+            want[~res] = -7.0
+            ok &= got.tobytes() == want.tobytes()
+            ok &= bool((flags == (~res).astype(np.uint8)).all())
+            admitted = peer.fill(fetch)
+            every = [None] * world
+            dist.all_gather_object(every, [int(k) for k in batch])
+            new_even = set(k for b in every for k in b if k % 2 == 0) - resident
+            owners = sharded.shard_of(np.array(sorted(new_even), dtype=np.uint64), world)
+            ok &= admitted == int((owners == rank).sum())
+            resident |= new_even
+        cache.check_invariants()
+        # the shard holds exactly the even keys it owns that anyone asked for
+        mine = set(int(k) for k in cache.dump_all())
+        ok &= mine == set(k for k in resident
+                          if sharded.shard_of(np.array([k], np.uint64), world)[0] == rank)
+        peer.close()
+        q.put((rank, bool(ok)))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2])
+def test_peer_memory_sharded_lookup_two_processes_one_gpu(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, v = q.get(timeout=240)
+            res[r] = v
+    finally:
+        for p in procs:
+            p.join(30)
+            if p.is_alive():
+                p.kill()
+    assert all(res.get(r) is True for r in range(world)), res
+    assert all(p.exitcode == 0 for p in procs)
