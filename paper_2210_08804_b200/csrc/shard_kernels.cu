@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 
 #include "common.cuh"
@@ -119,7 +120,7 @@ void launch_shard_unroute(uint64_t m, uint32_t d, const uint32_t* send_pos, cons
 // owner's row is read straight into the local output (a warp streams its 32
 // rows, 4 rows in flight); a miss writes the default row, sets the flag and
 // appends the key once per warp to the owner's inbox.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     k_peer_lookup(const PeerShard* __restrict__ shards, uint32_t world,
                   const uint64_t* __restrict__ keys, uint64_t n, float* __restrict__ out,
                   uint8_t* __restrict__ flags, const float* __restrict__ default_row, uint32_t d,
@@ -153,55 +154,45 @@ __global__ void __launch_bounds__(256)
     if (at < sh.inbox_cap) sh.inbox_keys[at] = key;
   }
   if (valid) flags[pos] = miss ? 1 : 0;
-  // rows: the warp's 32 rows, each row by all lanes, 4 rows in flight
+  // rows: the warp's 32 output rows are one contiguous block; lane i's row
+  // comes from its owner's shard (or the default row). 256-bit chunks, U in
+  // flight per lane (d % 8 == 0), else 128-bit / scalar.
   const float* src = hit ? sh.c.rows + uint64_t(res) * d : default_row;
   const uint32_t nrows = n - base < 32 ? uint32_t(n - base) : 32u;
-  const bool vec = (d & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0 &&
-                   (reinterpret_cast<uintptr_t>(default_row) & 15u) == 0;
-  if (vec) {
-    const uint32_t q4 = d >> 2;
-    for (uint32_t r0 = 0; r0 < nrows; r0 += 4) {
-      float4 x[4][2];
-      const float4* sp[4];
+  float* obase = out + base * d;
+  const uintptr_t sp = reinterpret_cast<uintptr_t>(src);
+  auto copy = [&](auto chunk_tag, auto u_tag) {
+    using Ch = decltype(chunk_tag);
+    constexpr int CH = sizeof(Ch) / 4;
+    constexpr int U = decltype(u_tag)::value;
+    const uint32_t cpr = d / CH;
+    const uint32_t total = nrows * cpr;
+    for (uint32_t c0 = 0; c0 < total; c0 += 32 * U) {
+      Ch x[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t r = r0 + u;
-        sp[u] = reinterpret_cast<const float4*>(__shfl_sync(0xFFFFFFFFu,
-                                                            reinterpret_cast<uintptr_t>(src), r & 31u));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t q = lane + 32u * h;
-          if (r < nrows && q < q4) x[u][h] = sp[u][q];
-        }
+      for (int u = 0; u < U; ++u) {
+        const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
+        const uint32_t row = min(ch / cpr, 31u);
+        const float* rs = reinterpret_cast<const float*>(__shfl_sync(0xFFFFFFFFu, sp, row));
+        if (ch < total) x[u].load(rs + (ch - row * cpr) * CH);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t r = r0 + u;
-        float4* dp = reinterpret_cast<float4*>(out + (base + r) * d);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t q = lane + 32u * h;
-          if (r < nrows && q < q4) dp[q] = x[u][h];
-        }
-      }
-      // rows wider than 256 floats: the rest, row by row
-      if (q4 > 64) {
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t r = r0 + u;
-          if (r >= nrows) break;
-          float4* dp = reinterpret_cast<float4*>(out + (base + r) * d);
-          for (uint32_t q = 64 + lane; q < q4; q += 32) dp[q] = sp[u][q];
-        }
+      for (int u = 0; u < U; ++u) {
+        const uint32_t ch = c0 + uint32_t(u) * 32 + lane;
+        if (ch < total) x[u].store(obase + uint64_t(ch) * CH);
       }
     }
-  } else {
-    for (uint32_t r = 0; r < nrows; ++r) {
-      const float* sr = reinterpret_cast<const float*>(
-          __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(src), r));
-      float* dr = out + (base + r) * d;
-      for (uint32_t x = lane; x < d; x += 32) dr[x] = sr[x];
-    }
-  }
+  };
+  const bool al32 = (d & 7u) == 0 && (reinterpret_cast<uintptr_t>(out) & 31u) == 0 &&
+                    (reinterpret_cast<uintptr_t>(default_row) & 31u) == 0;
+  const bool al16 = (d & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0 &&
+                    (reinterpret_cast<uintptr_t>(default_row) & 15u) == 0;
+  if (al32)
+    copy(Chunk<8>{}, std::integral_constant<int, 4>{});
+  else if (al16)
+    copy(Chunk<4>{}, std::integral_constant<int, 8>{});
+  else
+    copy(Chunk<1>{}, std::integral_constant<int, 8>{});
 }
 
 void launch_peer_lookup(const PeerShard* d_shards, uint32_t world, const uint64_t* keys,

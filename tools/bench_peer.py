@@ -61,9 +61,13 @@ def worker(rank, a, port, q):
     torch.cuda.synchronize(dev)
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
+
     e0.record(st)
+    h0 = time.perf_counter()
     for s in range(a.steps):
         out, fl = peer.lookup(dk[s % 16], default)
+    host_us = (time.perf_counter() - h0) * 1e6 / a.steps
     e1.record(st)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / a.steps
@@ -71,6 +75,7 @@ def worker(rank, a, port, q):
     dist.barrier()
     peer.close()
     q.put({"rank": rank, "device": dev, "ms_per_step": ms, "keys_per_s": n / (ms * 1e-3),
+           "host_issue_us_per_call": host_us,
            "miss_fraction_positions": miss})
     dist.destroy_process_group()
 
