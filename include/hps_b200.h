@@ -469,9 +469,11 @@ int hps_shard_unroute(int device, size_t m, uint32_t dim, const uint32_t* send_p
  *      straight into `out`; misses get default_row + flag and are appended
  *      to the owner's inbox. Owners admit their inbox keys between lookup
  *      phases (hps_cache_peer_drain, then a fetch + replace of their own);
- *      no peer may look up while an owner mutates its shard. Recency: the
- *      requester's own shard clock ticks once per call and stamps every
- *      owner's hits (ranks step together). ---- */
+ *      no peer may look up while an owner mutates its shard. Recency: while
+ *      exported, a shard's clock lives in device memory; every lookup call
+ *      ticks each owner's clock once and stamps that owner's hits with it,
+ *      and a drain reads it back for the owner's replaces (use an exported
+ *      shard only through its peer group). ---- */
 size_t hps_peer_blob_size(void);
 /* inbox_cap: miss keys the inbox holds between drains (first export only) */
 int hps_cache_peer_export(hps_cache* cache, uint64_t inbox_cap, void* blob, size_t blob_cap,

@@ -600,6 +600,11 @@ void DeviceCache::peer_export(uint64_t inbox_cap, PeerBlob* out) {
     if (inbox_cap == 0) throw invalid_argument("peer inbox capacity must be positive");
     HPSB_CUDA(cudaMalloc(&inbox_, 256 + inbox_cap * 8));
     HPSB_CUDA(cudaMemsetAsync(inbox_, 0, 256, stream_));
+    // from here on the recency clock lives in device memory ([1] of the
+    // inbox header): peers tick it, drains read it back
+    h_small_[4] = clock_.load(std::memory_order_relaxed);
+    HPSB_CUDA(cudaMemcpyAsync(static_cast<char*>(inbox_) + 8, h_small_ + 4, 8,
+                              cudaMemcpyHostToDevice, stream_));
     HPSB_CUDA(cudaStreamSynchronize(stream_));
     inbox_cap_ = inbox_cap;
   }
@@ -635,8 +640,16 @@ size_t DeviceCache::peer_drain(uint64_t* out, size_t cap) {
   // the peers' appends are done (caller's contract); the device is
   // synchronised so appends from other streams / processes have landed
   HPSB_CUDA(cudaDeviceSynchronize());
-  HPSB_CUDA(cudaMemcpy(h_small_ + 5, inbox_, 8, cudaMemcpyDeviceToHost));
-  const uint64_t appended = h_small_[5];
+  HPSB_CUDA(cudaMemcpy(h_small_ + 4, inbox_, 16, cudaMemcpyDeviceToHost));
+  const uint64_t appended = h_small_[4];
+  // the shard's clock as the peers ticked it: this owner's replaces stamp
+  // with it (slab_cache.cpp:105)
+  uint64_t cur = clock_.load(std::memory_order_relaxed);
+  while (cur < h_small_[5] && !clock_.compare_exchange_weak(cur, h_small_[5])) {
+  }
+  // and back: ticks of this cache's own host-side queries reach the peers
+  h_small_[5] = clock_.load(std::memory_order_relaxed);
+  HPSB_CUDA(cudaMemcpy(static_cast<char*>(inbox_) + 8, h_small_ + 5, 8, cudaMemcpyHostToDevice));
   const uint64_t m = std::min<uint64_t>({appended, inbox_cap_, uint64_t(cap)});
   if (m > 0)
     HPSB_CUDA(cudaMemcpy(out, static_cast<char*>(inbox_) + 256, m * 8, cudaMemcpyDeviceToHost));

@@ -25,6 +25,7 @@ PeerGroup::PeerGroup(DeviceCache& self, uint32_t rank, const std::vector<PeerBlo
       if (r == rank_) {
         s.c = self.dev();
         self.peer_inbox(&s.inbox_count, &s.inbox_keys, &s.inbox_cap);
+        s.clock = s.inbox_count + 1;
         continue;
       }
       void *probe = nullptr, *rows = nullptr, *inbox = nullptr;
@@ -49,10 +50,12 @@ PeerGroup::PeerGroup(DeviceCache& self, uint32_t rank, const std::vector<PeerBlo
       c.mW = ~0ull / b.W;
       s.c = c;
       s.inbox_count = static_cast<unsigned long long*>(inbox);
+      s.clock = s.inbox_count + 1;
       s.inbox_keys = reinterpret_cast<uint64_t*>(static_cast<char*>(inbox) + 256);
       s.inbox_cap = b.inbox_cap;
     }
     HPSB_CUDA(cudaMalloc(&d_shards_, world_ * sizeof(PeerShard)));
+    HPSB_CUDA(cudaMalloc(&d_stamps_, world_ * 8));
     HPSB_CUDA(cudaMemcpy(d_shards_, shards.data(), world_ * sizeof(PeerShard),
                          cudaMemcpyHostToDevice));
   } catch (...) {
@@ -67,20 +70,18 @@ PeerGroup::~PeerGroup() {
   cudaDeviceSynchronize();
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   cudaFree(d_shards_);
+  cudaFree(d_stamps_);
 }
 
 void PeerGroup::lookup(const uint64_t* keys, size_t n, float* out, uint8_t* flags,
                        const float* default_row, cudaStream_t user) {
   std::lock_guard<std::mutex> lk(self_.mutex());
   DeviceGuard g(self_.device());
-  // recency: the requester's own shard clock ticks once per call and stamps
-  // every owner's hit slots (ranks step together, so the shards' clocks
-  // advance at the same rate; an approximation of the per-cache clock)
-  const uint64_t stamp = self_.bump_clock();
+  // recency: each owner's device clock ticks once for this call (peer.hpp)
   self_.note_stream_op();
   self_.join_from(user);
-  launch_peer_lookup(d_shards_, world_, keys, n, out, flags, default_row, self_.dimension(), stamp,
-                     self_.stream());
+  launch_peer_lookup(d_shards_, world_, keys, n, out, flags, default_row, self_.dimension(),
+                     d_stamps_, self_.stream());
   self_.join_to(user);
 }
 

@@ -8,6 +8,11 @@
 // No collective, no staging, no host synchronisation on the data path; the
 // owners admit their inboxes' keys between lookup phases (PeerGroup users
 // run a barrier around the fill, see paper_2210_08804_b200/sharded.py).
+// Recency: while a shard is peer-mapped its clock lives in device memory
+// next to its inbox; every lookup call ticks each owner's clock once
+// (slab_cache.cpp:73-74: one tick per query) and stamps that owner's hits
+// with it, and the owner's replace stamps with the same clock (it is read
+// back at the drain), so the LRU order is the reference's per shard.
 // No reference counterpart: the reference is single-process and the paper
 // deploys one replica per GPU.
 #pragma once
@@ -41,15 +46,18 @@ constexpr uint64_t kPeerBlobMagic = 0x48505342504545ull;  // "HPSBPEE"
 // One shard as the lookup kernel sees it.
 struct PeerShard {
   CacheDev c;
-  unsigned long long* inbox_count;  // inbox: [count | keys...]
+  unsigned long long* inbox_count;  // inbox: [count | clock | pad | keys...]
+  unsigned long long* clock;        // the shard's recency clock while peer-mapped
   uint64_t* inbox_keys;
   uint64_t inbox_cap;
 };
 
 // Kernel launcher (shard_kernels.cu).
+// (two launches: each owner's clock ticks once for the call -- the stamps --
+// then the lookup)
 void launch_peer_lookup(const PeerShard* d_shards, uint32_t world, const uint64_t* keys,
                         uint64_t n, float* out, uint8_t* flags, const float* default_row,
-                        uint32_t d, uint64_t stamp, cudaStream_t st);
+                        uint32_t d, unsigned long long* d_stamps, cudaStream_t st);
 
 class PeerGroup {
  public:
@@ -71,6 +79,7 @@ class PeerGroup {
   uint32_t rank_, world_;
   std::vector<void*> opened_;
   PeerShard* d_shards_ = nullptr;
+  unsigned long long* d_stamps_ = nullptr;  // this call's stamp per owner
 };
 
 }  // namespace hpsb

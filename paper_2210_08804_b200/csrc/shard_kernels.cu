@@ -120,11 +120,21 @@ void launch_shard_unroute(uint64_t m, uint32_t d, const uint32_t* send_pos, cons
 // owner's row is read straight into the local output (a warp streams its 32
 // rows, 4 rows in flight); a miss writes the default row, sets the flag and
 // appends the key once per warp to the owner's inbox.
+// One tick of every owner's clock for a call (slab_cache.cpp:73-74).
+// The lookup is launched as its programmatic dependent: it may start at once
+// and waits for the stamps only after its probe.
+__global__ void k_peer_stamps(const PeerShard* __restrict__ shards, uint32_t world,
+                              unsigned long long* __restrict__ stamps) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t g = threadIdx.x;
+  if (g < world) stamps[g] = atomicAdd(shards[g].clock, 1ull) + 1ull;
+}
+
 __global__ void __launch_bounds__(256, 3)
     k_peer_lookup(const PeerShard* __restrict__ shards, uint32_t world,
                   const uint64_t* __restrict__ keys, uint64_t n, float* __restrict__ out,
                   uint8_t* __restrict__ flags, const float* __restrict__ default_row, uint32_t d,
-                  uint64_t stamp) {
+                  const unsigned long long* __restrict__ stamps) {
   __shared__ PeerShard s_sh[kMaxPeers];
   for (uint32_t i = threadIdx.x; i < world; i += blockDim.x) s_sh[i] = shards[i];
   __syncthreads();
@@ -138,12 +148,14 @@ __global__ void __launch_bounds__(256, 3)
   const PeerShard& sh = s_sh[owner];
   const uint32_t res = lane_probe(sh.c, key, valid);
   const bool hit = res != kNoSlot;
-  // recency: one atomic per distinct (owner, slot) of the warp
+  // recency: one atomic per distinct (owner, slot) of the warp, with the
+  // call's tick of the owner's clock (the stamps kernel has completed and
+  // its writes are visible after the grid-dependency wait)
   const uint64_t tag = hit ? ((uint64_t(owner) << 32) | res) : ~0ull;
   const uint32_t same = __match_any_sync(0xFFFFFFFFu, tag);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (hit && (__ffs(same) - 1) == lane)
-    atomicMax(reinterpret_cast<unsigned long long*>(sh.c.counters) + res,
-              (unsigned long long)stamp);
+    atomicMax(reinterpret_cast<unsigned long long*>(sh.c.counters) + res, stamps[owner]);
   // misses: one inbox append per distinct key of the warp
   const bool miss = valid && !hit;
   // (every lane runs both warp-collective calls: no short-circuit around them)
@@ -197,11 +209,27 @@ __global__ void __launch_bounds__(256, 3)
 
 void launch_peer_lookup(const PeerShard* d_shards, uint32_t world, const uint64_t* keys,
                         uint64_t n, float* out, uint8_t* flags, const float* default_row,
-                        uint32_t d, uint64_t stamp, cudaStream_t st) {
-  if (n == 0) return;
-  k_peer_lookup<<<unsigned((n + 255) / 256), 256, 0, st>>>(d_shards, world, keys, n, out, flags,
-                                                          default_row, d, stamp);
-  check_launch("peer_lookup", 1);
+                        uint32_t d, unsigned long long* d_stamps, cudaStream_t st) {
+  // every call ticks the owners' clocks, even an empty one (a query bumps
+  // the clock before anything else, slab_cache.cpp:73-74)
+  k_peer_stamps<<<1, kMaxPeers, 0, st>>>(d_shards, world, d_stamps);
+  if (n == 0) {
+    check_launch("peer_lookup", 1);
+    return;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned((n + 255) / 256));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_peer_lookup, static_cast<const PeerShard*>(d_shards), world, keys, n,
+                     out, flags, default_row, d,
+                     static_cast<const unsigned long long*>(d_stamps));
+  check_launch("peer_lookup", 2);
 }
 
 }  // namespace hpsb

@@ -352,6 +352,18 @@ def _peer_worker(rank, world, port, q):
             ok &= got.tobytes() == want.tobytes()
             ok &= bool((flags == (~res).astype(np.uint8)).all())
             admitted = peer.fill(fetch)
+            # recency: every call ticked this shard's clock once (all ranks
+            # looked up `step + 1` times), the fill stamped with it, and no
+            # counter is newer than the clock
+            ok &= cache.recency_clock() == world * (step + 1)
+            _, ctrs, masks, _ = cache.export_state()
+            occ = (np.repeat(masks, 32).reshape(-1, 32)
+                   >> np.arange(32, dtype=np.uint32) & 1).reshape(-1) == 1
+            if occ.any():
+                top = int(ctrs[occ].max())
+                ok &= top <= cache.recency_clock()
+                if admitted:
+                    ok &= top == cache.recency_clock()
             every = [None] * world
             dist.all_gather_object(every, [int(k) for k in batch])
             new_even = set(k for b in every for k in b if k % 2 == 0) - resident
