@@ -1337,66 +1337,56 @@ void launch_update(const CacheDev& c, const uint64_t* keys, uint64_t n, const fl
 
 // ------------------------------------------------------------------- dump --
 // Resident keys of slabs [set_begin*W, set_end*W) in slab order, slot order
-// inside a slab (slab_cache.cpp:380-392). A tile = kScanTile slabs: (1) each
-// thread reads kScanItems masks, a block scan of their popcounts plus a
-// decoupled look-back give every slab its output offset; (2) the warps copy
-// the keys slab by slab -- occupancy grows contiguously from bit 0, so lane j
-// of an occupied slab writes out[offset + j]: coalesced 256 B loads and
-// contiguous stores, four slabs in flight per warp.
+// inside a slab (slab_cache.cpp:380-392). A tile = kDumpTile slabs, one per
+// thread: (1) a block scan of the masks' popcounts plus a decoupled
+// look-back give every slab its output offset; (2) each warp copies its 32
+// slabs' keys -- occupancy grows contiguously from bit 0, so lane j of an
+// occupied slab writes out[offset + j]: coalesced 256 B loads and contiguous
+// stores, 8 slabs in flight per warp. (Tiles of 1,024 slabs -- 61 blocks at
+// cfg 2 -- left the copy latency-bound: 26 us for 2 M slots.)
 __global__ void __launch_bounds__(kScanBlock)
     k_dump_keys(CacheDev c, uint64_t slab_begin, uint64_t n_slabs, uint64_t* __restrict__ out,
                 unsigned long long* n_out, ScanState scan) {
+  static_assert(kDumpTile == kScanBlock, "one slab per thread");
   __shared__ uint32_t s_warp[kScanBlock / 32];
   __shared__ uint64_t s_tile;
   __shared__ uint64_t s_prefix;
-  __shared__ uint32_t s_off[kScanTile];
-  __shared__ uint32_t s_cnt[kScanTile];
   if (threadIdx.x == 0) s_tile = atomicAdd(scan.tile_ctr, 1ull) - scan.tile_base;
   __syncthreads();
   const uint64_t tile = s_tile;
-  const uint64_t first = tile * kScanTile;
-  uint32_t m[kScanItems];
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t sl = first + uint64_t(threadIdx.x) * kScanItems + k;
-    m[k] = (sl < n_slabs) ? c.masks[slab_begin + sl] : 0u;
-    cnt += __popc(m[k]);
-  }
+  const uint64_t first = tile * kDumpTile;
+  const uint64_t sl = first + threadIdx.x;
+  const uint32_t m = (sl < n_slabs) ? c.masks[slab_begin + sl] : 0u;
+  const uint32_t cnt = __popc(m);
   uint32_t block_total;
-  uint32_t excl = block_exclusive_scan<kScanBlock>(cnt, s_warp, &block_total);
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint32_t i = threadIdx.x * kScanItems + k;
-    s_off[i] = excl;
-    s_cnt[i] = __popc(m[k]);
-    excl += __popc(m[k]);
-  }
+  const uint32_t excl = block_exclusive_scan<kScanBlock>(cnt, s_warp, &block_total);
   if (threadIdx.x < 32) {
     const uint64_t pre = lb_exclusive_prefix(scan.status, uint32_t(tile), scan.epoch, block_total);
     if (threadIdx.x == 0) {
       s_prefix = pre;
-      const uint64_t tiles = (n_slabs + kScanTile - 1) / kScanTile;
+      const uint64_t tiles = (n_slabs + kDumpTile - 1) / kDumpTile;
       if (tile == tiles - 1) *n_out = pre + block_total;
     }
   }
   __syncthreads();
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  constexpr uint32_t kWarpsB = kScanBlock / 32;
+  const uint32_t lane = lane_id();
   const uint64_t prefix = s_prefix;
-  const uint64_t* kbase = c.keys + (slab_begin + first) * kSlotsPerSlab;
-  for (uint32_t i0 = warp; i0 < kScanTile; i0 += 4 * kWarpsB) {
-    uint64_t k[4];
+  // this warp's 32 slabs: slab (warp base + i) held by lane i (count, offset)
+  const uint64_t wslab = first + (threadIdx.x & ~31u);
+  const uint64_t* kbase = c.keys + (slab_begin + wslab) * kSlotsPerSlab;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = i0 + u * kWarpsB;
-      k[u] = (i < kScanTile && lane < s_cnt[i]) ? kbase[uint64_t(i) * kSlotsPerSlab + lane] : 0ull;
+  for (int i0 = 0; i0 < 32; i0 += 8) {
+    uint64_t k[8];
+    uint32_t ci[8], oi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      ci[u] = __shfl_sync(0xFFFFFFFFu, cnt, i0 + u);
+      oi[u] = __shfl_sync(0xFFFFFFFFu, excl, i0 + u);
+      k[u] = lane < ci[u] ? kbase[uint64_t(i0 + u) * kSlotsPerSlab + lane] : 0ull;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = i0 + u * kWarpsB;
-      if (i < kScanTile && lane < s_cnt[i]) out[prefix + s_off[i] + lane] = k[u];
-    }
+    for (int u = 0; u < 8; ++u)
+      if (lane < ci[u]) out[prefix + oi[u] + lane] = k[u];
   }
 }
 
@@ -1407,7 +1397,7 @@ void launch_dump(const CacheDev& c, uint64_t set_begin, uint64_t set_end, uint64
     cudaMemsetAsync(n_out, 0, 8, st);
     return;
   }
-  const uint64_t tiles = (n_slabs + kScanTile - 1) / kScanTile;
+  const uint64_t tiles = (n_slabs + kDumpTile - 1) / kDumpTile;
   scan_begin(scan, tiles, st);
   k_dump_keys<<<unsigned(tiles), kScanBlock, 0, st>>>(c, set_begin * c.W, n_slabs, out, n_out,
                                                       scan);

@@ -747,7 +747,7 @@ size_t DeviceCache::dump(uint64_t set_begin, uint64_t set_end, uint64_t* out, si
   if (set_begin >= set_end) return 0;
   DeviceGuard g(device_);
   const uint64_t slots = (set_end - set_begin) * cfg_.slabs_per_set * 32ull;
-  ensure_scan_tiles(((set_end - set_begin) * cfg_.slabs_per_set + kScanTile - 1) / kScanTile);
+  ensure_scan_tiles(((set_end - set_begin) * cfg_.slabs_per_set + kDumpTile - 1) / kDumpTile);
   uint64_t* d_out = static_cast<uint64_t*>(scratch(slots * 8));
   launch_dump(dev_, set_begin, set_end, d_out, d_small_ + 3, scan_, stream_);
   HPSB_CUDA(cudaMemcpyAsync(h_small_ + 3, d_small_ + 3, 8, cudaMemcpyDeviceToHost, stream_));
@@ -784,7 +784,7 @@ void DeviceCache::dump_device(uint64_t set_begin, uint64_t set_end, uint64_t* ou
   if (set_begin >= set_end) {
     HPSB_CUDA(cudaMemsetAsync(n_out, 0, 8, stream_));
   } else {
-    ensure_scan_tiles(((set_end - set_begin) * cfg_.slabs_per_set + kScanTile - 1) / kScanTile);
+    ensure_scan_tiles(((set_end - set_begin) * cfg_.slabs_per_set + kDumpTile - 1) / kDumpTile);
     launch_dump(dev_, set_begin, set_end, out, reinterpret_cast<unsigned long long*>(n_out),
                 scan_, stream_);
   }

@@ -26,6 +26,7 @@ struct ScanState {
 constexpr int kScanBlock = 256;
 constexpr int kScanItems = 4;
 constexpr uint64_t kScanTile = uint64_t(kScanBlock) * kScanItems;
+constexpr uint64_t kDumpTile = uint64_t(kScanBlock);  // slabs per dump tile
 
 // Prepares `s` for one launch of `tiles` tiles; returns false if the status
 // array had to be cleared (epoch wrap) -- handled internally.
