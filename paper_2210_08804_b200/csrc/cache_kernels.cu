@@ -216,6 +216,8 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #endif
 __global__ void __launch_bounds__(256)
     k_replace_bin(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
+  // the set kernel may launch now (it waits for this grid before reading)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i == 0) {
     rs.cursor[0] = 0u;
@@ -581,6 +583,9 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
   __shared__ unsigned long long s_ins;
   if (threadIdx.x == 0) s_ins = 0ull;
   __syncthreads();
+  // launched as the bin kernel's programmatic dependent: everything below
+  // reads what bin wrote
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint64_t stride = uint64_t(gridDim.x) * (blockDim.x >> 5);
   uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   // the list is consumed through its sentinels; its count restarts here
@@ -1190,12 +1195,28 @@ void launch_replace(const CacheDev& c, const uint64_t* keys, uint64_t n, const f
     const uint64_t full = uint64_t(std::max(sms, 1)) * uint64_t(std::max(per_sm[wi], 1));
     return unsigned(std::min<uint64_t>(full, wgrid));
   };
+  // the set kernel as a programmatic dependent of the kernel before it (bin,
+  // or the duplicate check): its launch and prologue overlap that tail
+  static const bool no_pdl = std::getenv("HPSB_NO_PDL") != nullptr;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(tb);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  const uint32_t vflag = validate ? 1u : 0u;
+  auto sets = [&](auto kern) {
+    cfg.gridDim = dim3(grid_for((const void*)kern));
+    cudaLaunchKernelEx(&cfg, kern, c, keys, n, rows, stamp, vflag, rs);
+  };
   switch (c.W) {
-    case 1: k_replace_sets<1><<<grid_for((const void*)k_replace_sets<1>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    case 2: k_replace_sets<2><<<grid_for((const void*)k_replace_sets<2>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    case 3: k_replace_sets<3><<<grid_for((const void*)k_replace_sets<3>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    case 4: k_replace_sets<4><<<grid_for((const void*)k_replace_sets<4>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
-    default: k_replace_sets<0><<<grid_for((const void*)k_replace_sets<0>), tb, 0, st>>>(c, keys, n, rows, stamp, validate, rs); break;
+    case 1: sets(k_replace_sets<1>); break;
+    case 2: sets(k_replace_sets<2>); break;
+    case 3: sets(k_replace_sets<3>); break;
+    case 4: sets(k_replace_sets<4>); break;
+    default: sets(k_replace_sets<0>); break;
   }
   check_launch("replace", validate ? 3 : 2);
 }

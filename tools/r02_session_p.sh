@@ -8,6 +8,6 @@ for v in base prev base prev; do
   else HPSB_LIB_VARIANT=$v timeout 600 python tools/bench_replace.py --reps 40 >> $out/replace_$v.json 2>> $out/replace.err; fi
 done
 timeout 600 python tools/bench_replace.py --reps 40 --check > $out/replace_check.json 2>> $out/replace.err
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_replace_sets" -s 34 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_replace_sets<" -s 34 -c 1 \
   -o $out/sets python tools/bench_replace.py --reps 2 > $out/ncu_sets.log 2>&1
 ls -la $out
