@@ -977,7 +977,8 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
                                                                                      : 1;
     // a call pipelined behind another lookup orders its recency exchange
     // for throughput, any other call for latency (see lookup_body)
-    const bool pipelined = cfg.numAttrs == 1 && !(skip & kWaitBeforeCopy);
+    static const bool all_pipelined = std::getenv("HPSB_LOOKUP_ALL_PIPELINED") != nullptr;  // A/B
+    const bool pipelined = (cfg.numAttrs == 1 || all_pipelined) && !(skip & kWaitBeforeCopy);
     static const bool no_small = std::getenv("HPSB_LOOKUP_NO_SMALL") != nullptr;
     if (cfg.numAttrs == 0 && n <= kSmallLookup && diag_skip == 0 && v.trace == nullptr &&
         !no_small) {
