@@ -750,6 +750,19 @@ def ref_session(args, wl, workers):
     return eng
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (state nproc and the CPU model)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(args, wl, replicas=1):
     """Reference LookupEngine on a bounded sample of the same workload, on
     rank 0: 8 batches of 65,536 keys at the headline hit rate. With N > 1
@@ -784,7 +797,8 @@ def cpu_baseline(args, wl, replicas=1):
             t.join()
         el = time.perf_counter() - t0
         return {"value": replicas * len(batches) * wl.batch / el, "unit": "keys/s",
-                "cores": per * replicas, "kind": "reference", "replicas": replicas,
+                "cores": per * replicas, "cpu_model": cpu_model(), "kind": "reference",
+                "replicas": replicas,
                 "sample": f"{replicas} x {len(batches)} batches x {wl.batch} keys through "
                           f"{replicas} concurrent reference LookupEngine(s) (worker_pool_size = "
                           f"{per} each, threshold 0.8, VDB-backed misses), cfg2 geometry, "
@@ -830,7 +844,8 @@ def run_reference(args, rank, world):
                                   "batch 65536, unique-hit 0.9",
                       "target_unique_hit": args.hit, "parallelism": "CPU reference, rank 0"},
            "measured_unique_hit_rate": float(np.mean(hs)),
-           "cpu_baseline": {"value": v, "unit": "keys/s", "cores": cores, "kind": "reference",
+           "cpu_baseline": {"value": v, "unit": "keys/s", "cores": cores, "cpu_model": cpu_model(),
+                            "kind": "reference",
                             "sample": f"{args.steps} batches x {wl.batch} keys through the "
                                       "reference LookupEngine (oracle/_ref), threshold 0.8"},
            "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0,

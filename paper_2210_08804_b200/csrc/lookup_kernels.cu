@@ -975,10 +975,15 @@ unsigned launch_lookup_probe(const CacheDev& c, const uint64_t* keys, uint64_t n
     const int ch = (c.d % 8 == 0 && aligned(out, 32) && aligned(default_row, 32))   ? 8
                    : (c.d % 4 == 0 && aligned(out, 16) && aligned(default_row, 16)) ? 4
                                                                                      : 1;
-    // a call pipelined behind another lookup orders its recency exchange
-    // for throughput, any other call for latency (see lookup_body)
-    static const bool all_pipelined = std::getenv("HPSB_LOOKUP_ALL_PIPELINED") != nullptr;  // A/B
-    const bool pipelined = (cfg.numAttrs == 1 || all_pipelined) && !(skip & kWaitBeforeCopy);
+    // The throughput-ordered variant for every call except one chained
+    // behind an update (which waits before its copies): the latency-ordered
+    // variant (SF, recency exchange before the claims) measured no lower
+    // single-call latency on the round-2 kernel and made the first call of a
+    // pipelined sequence slower (20-step cfg-2 graph: 7.62 vs 7.49 G keys/s,
+    // 3 reps each, profiles/r02_ab_lookup.txt). HPSB_LOOKUP_LONE_VARIANT=1
+    // restores it for unchained calls.
+    static const bool lone_variant = std::getenv("HPSB_LOOKUP_LONE_VARIANT") != nullptr;
+    const bool pipelined = (cfg.numAttrs == 1 || !lone_variant) && !(skip & kWaitBeforeCopy);
     static const bool no_small = std::getenv("HPSB_LOOKUP_NO_SMALL") != nullptr;
     if (cfg.numAttrs == 0 && n <= kSmallLookup && diag_skip == 0 && v.trace == nullptr &&
         !no_small) {
