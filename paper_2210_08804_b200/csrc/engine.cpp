@@ -18,23 +18,33 @@ inline uint64_t a256(uint64_t v) { return (v + 255) / 256 * 256; }
 
 // HPSB_ENGINE_TRACE=1: per-phase host timeline of lookups slower than 2 ms
 // (diagnostic, stderr).
+// HPSB_ENGINE_TRACE=1: calls slower than 2 ms print their phase timeline
+// (from the start of begin); HPSB_ENGINE_TRACE=<us>: calls slower than that.
 struct PhaseTrace {
   static bool on() {
     static const bool v = std::getenv("HPSB_ENGINE_TRACE") != nullptr;
     return v;
   }
+  static double min_us() {
+    static const double v = [] {
+      const char* e = std::getenv("HPSB_ENGINE_TRACE");
+      const double x = e ? std::atof(e) : 0.0;
+      return (e == nullptr || x == 1.0) ? 2000.0 : x;
+    }();
+    return v;
+  }
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  double at[8] = {};
-  const char* name[8] = {};
+  double at[10] = {};
+  const char* name[10] = {};
   int k = 0;
   void mark(const char* what) {
-    if (!on() || k >= 8) return;
+    if (!on() || k >= 10) return;
     name[k] = what;
     at[k++] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
                   .count();
   }
   void report(uint64_t n, uint64_t um, bool sync) {
-    if (!on() || k == 0 || at[k - 1] < 2000.0) return;
+    if (!on() || k == 0 || at[k - 1] < min_us()) return;
     std::fprintf(stderr, "[hpsb trace] n=%llu misses=%llu sync=%d", (unsigned long long)n,
                  (unsigned long long)um, int(sync));
     for (int i = 0; i < k; ++i) std::fprintf(stderr, " %s=%.0fus", name[i], at[i]);
@@ -339,7 +349,11 @@ LookupEngine::LookupEngine(const std::string& table, uint32_t dim, DeviceCache* 
       cold_ctx_(cold_ctx),
       cfg_(std::move(cfg)),
       pool_(cfg_.workspace_pool_size, cache ? cache->device() : 0),
-      copy_threads_(std::min(8u, std::max(1u, std::thread::hardware_concurrency()))) {
+      copy_threads_([] {
+        const char* e = std::getenv("HPSB_COPY_THREADS");  // A/B knob
+        const unsigned want = e ? unsigned(std::max(1, std::atoi(e))) : 8u;
+        return std::min(want, std::max(1u, std::thread::hardware_concurrency()));
+      }()) {
   if (table.empty()) throw invalid_argument("table name must not be empty");
   if (table.size() > 255) throw invalid_argument("table name exceeds 255 bytes: " + table);
   if (dim == 0) throw invalid_argument("table dimension must be positive: " + table);
@@ -381,8 +395,15 @@ void LookupEngine::rows_d2h(Workspace& ws, const LookupCall& c, cudaStream_t st)
     HPSB_CUDA(cudaMemcpyAsync(c.out, c.d_out, bytes, cudaMemcpyDeviceToHost, st));
     return;
   }
-  // ~2 MB chunks: the copy-on of chunk i runs while chunk i+1 crosses PCIe
-  const uint64_t nch = std::clamp<uint64_t>(bytes >> 21, 1, Workspace::kOutChunks);
+  // ~512 KB chunks (HPSB_OUT_CHUNK_SHIFT): the copy-on of chunk i runs while
+  // later chunks cross PCIe; small chunks keep the tail after the last chunk
+  // lands short (2 MB chunks left a ~0.2 ms single-thread copy after the DMA)
+  static const int shift = [] {
+    const char* e = std::getenv("HPSB_OUT_CHUNK_SHIFT");
+    const int v = e ? std::atoi(e) : 19;
+    return std::clamp(v, 16, 24);
+  }();
+  const uint64_t nch = std::clamp<uint64_t>(bytes >> shift, 1, Workspace::kOutChunks);
   const uint64_t per = (bytes / nch + 255) / 256 * 256;
   ws.out_chunks = 0;
   for (uint64_t off = 0; off < bytes; off += per) {
@@ -523,6 +544,7 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
   if (cfg_.max_batch != 0 && n > cfg_.max_batch)
     throw invalid_argument("lookup batch exceeds the engine's max_batch");
   LookupCall c;
+  c.t0 = std::chrono::steady_clock::now();
   c.engine = this;
   c.n = n;
   c.out = out;
@@ -576,7 +598,17 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
         if (is_pinned(keys)) {
           HPSB_CUDA(cudaMemcpyAsync(ws->d_keys, keys, n * 8, cudaMemcpyHostToDevice, st));
         } else {
-          std::memcpy(ws->h_keys, keys, n * 8);
+          // pageable keys: staged by the copy threads (a 0.5 MB single-thread
+          // memcpy was most of this call's 0.1 ms before the upload)
+          const size_t bytes = n * 8;
+          const size_t chunks = bytes >= (size_t(256) << 10) ? copy_threads_.size() : 1;
+          const size_t per = (n + chunks - 1) / chunks;
+          copy_threads_.parallel_for(chunks, 1, [&](size_t cb, size_t ce) {
+            for (size_t ch = cb; ch < ce; ++ch) {
+              const size_t b = ch * per, e = std::min(n, b + per);
+              if (b < e) std::memcpy(ws->h_keys + b, keys + b, (e - b) * 8);
+            }
+          });
           HPSB_CUDA(cudaMemcpyAsync(ws->d_keys, ws->h_keys, n * 8, cudaMemcpyHostToDevice, st));
         }
         c.d_keys = ws->d_keys;
@@ -640,6 +672,8 @@ LookupEngine::LookupCall LookupEngine::begin(const uint64_t* keys, size_t n, flo
 
 void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   PhaseTrace tr;
+  tr.t0 = c.t0;
+  tr.mark("finish");
   Workspace* ws = c.ws;
   bool handed_off = false;
   struct LeaseGuard {

@@ -13,6 +13,7 @@
 #pragma once
 
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
@@ -122,7 +123,7 @@ struct Workspace {
   // pageable output: the rows come back in chunks into h_out, one event per
   // chunk, and are copied on to the caller's memory by several threads as
   // each chunk lands
-  static constexpr int kOutChunks = 16;
+  static constexpr int kOutChunks = 64;
   cudaEvent_t chunk_ev[kOutChunks] = {};
   int out_chunks = 0;
   bool pending = false;  // `done` recorded, not yet waited
@@ -217,6 +218,7 @@ class LookupEngine {
   static constexpr uint64_t kZeroCopyReplaceMax = 256;  // = the single-block replace limit
   // one lookup split at its first host wait (begin enqueues, finish waits)
   struct LookupCall {
+    std::chrono::steady_clock::time_point t0;  // start of begin (phase trace)
     LookupEngine* engine = nullptr;
     Workspace* ws = nullptr;
     size_t n = 0;
