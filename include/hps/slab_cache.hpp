@@ -188,6 +188,13 @@ class SlabCache {
 
   // B200 extras: the C handle (device-pointer / stream-ordered calls).
   hps_cache* handle() const { return h_; }
+  // The opt-in relaxed replace mode (atomicCAS slot claims for replaces of
+  // distinct keys; include/hps_b200.h hps_cache_set_replace_mode). The
+  // default, exact mode is slot-exact with the reference.
+  void set_relaxed_replace(bool relaxed) {
+    b200_detail::check(
+        hps_cache_set_replace_mode(h_, relaxed ? HPS_REPLACE_RELAXED : HPS_REPLACE_EXACT));
+  }
 
  private:
   hps_cache_info info() const {
