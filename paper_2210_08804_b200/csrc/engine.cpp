@@ -729,7 +729,6 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   const bool sync_branch = h < cfg_.hit_rate_threshold;
   TierCounters counters;
   uint64_t defaults = 0;
-  bool rows_event = false;
   if (sync_branch) {
     size_t nf = 0;
     const size_t absent = fetch_and_upload(*ws, ws->h_miss_keys, um, &counters, &nf);
@@ -737,7 +736,23 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
     defaults = absent;
     std::lock_guard<std::mutex> lk(cache_->mutex());
     tr.mark("lock");
-    if (host && !c.packed && c.spec_rows) {
+    if (host && c.packed) {
+      // zero-copy call: the kernel has written rows and flags to host memory
+      // already; the fetched rows go into the caller's output on the host
+      // (below) and the fill's replace reads its keys and rows straight from
+      // the pinned staging (small fills) or after an upload
+      if (nf > 0) {
+        if (nf <= kZeroCopyReplaceMax) {
+          cache_->replace_device_locked(ws->h_found_keys, nf, ws->h_staged);
+        } else {
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                    cudaMemcpyHostToDevice, st));
+          HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                    cudaMemcpyHostToDevice, st));
+          cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
+        }
+      }
+    } else if (host && c.spec_rows) {
       // rows and flags are already crossing to the host: the fetched rows go
       // into the host output there (below); on the device only the fill
       if (nf > 0) {
@@ -748,39 +763,18 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
         cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
       }
     } else if (nf > 0) {
-      // row_of is in miss order; the scatter kernel indexes by claim
+      // device mode: the scatter kernel (row_of is in miss order; the kernel
+      // indexes by claim) writes the caller's device rows / flags
       for (uint64_t k = 0; k < um; ++k) ws->h_row_of_claim[ws->order[k]] = ws->h_row_of[k];
-      if (c.packed) {
-        // zero-copy: the scatter reads the staged rows from pinned host
-        // memory and writes the caller's rows / flags there; a small replace
-        // (one single-block kernel) reads its keys and rows from it too
-        cache_->note_stream_op();
-        launch_lookup_scatter(n, d, d_flags, ws->lv, ws->h_row_of_claim, ws->h_staged, d_out, st);
-        // the caller waits for the rows only; the replace runs on behind the
-        // return (stream-ordered before any later operation on the cache; the
-        // workspace is reused only after it, ws->done)
-        HPSB_CUDA(cudaEventRecord(ws->rows_ready, st));
-        rows_event = true;
-        if (nf <= kZeroCopyReplaceMax) {
-          cache_->replace_device_locked(ws->h_found_keys, nf, ws->h_staged);
-        } else {
-          HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
-                                    cudaMemcpyHostToDevice, st));
-          HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
-                                    cudaMemcpyHostToDevice, st));
-          cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
-        }
-      } else {
-        HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, um * 4,
-                                  cudaMemcpyHostToDevice, st));
-        HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
-                                  cudaMemcpyHostToDevice, st));
-        HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
-                                  cudaMemcpyHostToDevice, st));
-        cache_->note_stream_op();
-        launch_lookup_scatter(n, d, d_flags, ws->lv, ws->d_row_of, ws->d_staged, d_out, st);
-        cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
-      }
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, um * 4,
+                                cudaMemcpyHostToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
+                                cudaMemcpyHostToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
+                                cudaMemcpyHostToDevice, st));
+      cache_->note_stream_op();
+      launch_lookup_scatter(n, d, d_flags, ws->lv, ws->d_row_of, ws->d_staged, d_out, st);
+      cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
     }
     HPSB_CUDA(cudaEventRecord(ws->done, st));
     ws->pending = true;
@@ -792,12 +786,16 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
   last_async_.store(!sync_branch, std::memory_order_relaxed);
   if (n > 0) {
     if (host && c.packed) {
-      // zero-copy call: rows and flags are already in host memory once the
-      // kernels are done (the sync branch's scatter + replace waited here)
-      if (rows_event) HPSB_CUDA(cudaEventSynchronize(ws->rows_ready));
+      // zero-copy call: rows and flags are in host memory since the kernel
+      // completed (counts_ready); a sync branch's fetched rows are written
+      // into the caller's output here while its fill runs on
       if (!sync_branch) ws->pending = false;
       if (!c.out_direct) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
       std::memcpy(flags, c.hfl, n);
+      if (sync_branch && um > 0) {
+        host_scatter(*ws, c, um, flags);
+        tr.mark("scatter");
+      }
     } else if (host) {
       if (!c.spec_rows) {
         HPSB_CUDA(cudaMemcpyAsync(c.flags_pinned ? flags : ws->h_flags, d_flags, n,
