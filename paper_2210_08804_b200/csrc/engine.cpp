@@ -415,7 +415,8 @@ void LookupEngine::rows_d2h(Workspace& ws, const LookupCall& c, cudaStream_t st)
   }
 }
 
-void LookupEngine::host_scatter(Workspace& ws, const LookupCall& c, uint64_t um, uint8_t* hflags) {
+void LookupEngine::host_scatter(Workspace& ws, size_t n, const uint64_t* keys, float* out,
+                                uint64_t um, uint8_t* hflags) {
   // found misses (ws.h_miss_keys in miss order, ws.h_row_of: staged row or -1)
   uint64_t cap = 16;
   while (cap < 2 * um) cap <<= 1;
@@ -430,7 +431,7 @@ void LookupEngine::host_scatter(Workspace& ws, const LookupCall& c, uint64_t um,
   for (uint64_t k = 0; k < um; ++k) {
     if (ws.h_row_of[k] < 0) continue;
     any = true;
-    const uint64_t key = ws.h_miss_keys[k];
+    const uint64_t key = ws.scatter_keys[k];
     uint64_t h = fmix64(key) & mask;
     while (ws.hs_used[h]) h = (h + 1) & mask;
     ws.hs_used[h] = 1;
@@ -439,7 +440,6 @@ void LookupEngine::host_scatter(Workspace& ws, const LookupCall& c, uint64_t um,
   }
   if (!any) return;
   const uint32_t d = dim_;
-  const size_t n = c.n;
   const size_t chunks = std::min<size_t>(copy_threads_.size(), (n + 4095) / 4096);
   const size_t per = (n + chunks - 1) / chunks;
   copy_threads_.parallel_for(chunks, 1, [&](size_t cb, size_t ce) {
@@ -447,11 +447,11 @@ void LookupEngine::host_scatter(Workspace& ws, const LookupCall& c, uint64_t um,
       const size_t e = std::min(n, (ch + 1) * per);
       for (size_t p = ch * per; p < e; ++p) {
         if (!hflags[p]) continue;
-        const uint64_t key = c.h_keys[p];
+        const uint64_t key = keys[p];
         uint64_t h = fmix64(key) & mask;
         while (ws.hs_used[h] && ws.hs_keys[h] != key) h = (h + 1) & mask;
         if (!ws.hs_used[h]) continue;  // absent from every tier: default row, flagged
-        std::memcpy(c.out + p * d, ws.h_staged + uint64_t(ws.hs_rows[h]) * d, d * 4ull);
+        std::memcpy(out + p * d, ws.h_staged + uint64_t(ws.hs_rows[h]) * d, d * 4ull);
         hflags[p] = 0;
       }
     }
@@ -793,7 +793,8 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
       if (!c.out_direct) std::memcpy(out, ws->h_out, n * uint64_t(d) * 4);
       std::memcpy(flags, c.hfl, n);
       if (sync_branch && um > 0) {
-        host_scatter(*ws, c, um, flags);
+        ws->scatter_keys = ws->h_miss_keys;
+        host_scatter(*ws, n, c.h_keys, out, um, flags);
         tr.mark("scatter");
       }
     } else if (host) {
@@ -810,7 +811,8 @@ void LookupEngine::finish(LookupCall& c, LookupOutcome* outcome) {
       tr.mark("rows");
       uint8_t* hf = c.flags_pinned ? flags : ws->h_flags;
       if (sync_branch && um > 0) {
-        host_scatter(*ws, c, um, hf);
+        ws->scatter_keys = ws->h_miss_keys;
+        host_scatter(*ws, n, c.h_keys, c.out, um, hf);
         tr.mark("scatter");
       }
       if (!sync_branch) {
@@ -882,13 +884,12 @@ void LookupEngine::finish_group(const GroupResult& r, LookupOutcome* outcome) {
     size_t nf = 0;
     defaults = fetch_and_upload(*ws, r.miss_keys, r.um, &counters, &nf);
     if (nf > 0) {
-      std::lock_guard<std::mutex> lk(cache_->mutex());
-      for (uint64_t k = 0; k < r.um; ++k) ws->h_row_of_claim[r.order[k]] = ws->h_row_of[k];
-      if (r.zero_copy) {
-        // rows, flags and staged rows all in pinned host memory
-        cache_->note_stream_op();
-        launch_lookup_scatter(r.n, d, r.d_flags, r.v, ws->h_row_of_claim, ws->h_staged, r.d_out,
-                              st);
+      // the table's rows and flags are in the caller's host buffers already:
+      // the fetched rows are written there by the host, and the fill's
+      // replace runs on behind the return (the workspace is reused only
+      // after it, ws->done)
+      {
+        std::lock_guard<std::mutex> lk(cache_->mutex());
         if (nf <= kZeroCopyReplaceMax) {
           cache_->replace_device_locked(ws->h_found_keys, nf, ws->h_staged);
         } else {
@@ -898,26 +899,11 @@ void LookupEngine::finish_group(const GroupResult& r, LookupOutcome* outcome) {
                                     cudaMemcpyHostToDevice, st));
           cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
         }
-      } else {
-        HPSB_CUDA(cudaMemcpyAsync(ws->d_row_of, ws->h_row_of_claim, r.um * 4,
-                                  cudaMemcpyHostToDevice, st));
-        HPSB_CUDA(cudaMemcpyAsync(ws->d_staged, ws->h_staged, nf * uint64_t(d) * 4,
-                                  cudaMemcpyHostToDevice, st));
-        HPSB_CUDA(cudaMemcpyAsync(ws->d_found_keys, ws->h_found_keys, nf * 8,
-                                  cudaMemcpyHostToDevice, st));
-        cache_->note_stream_op();
-        launch_lookup_scatter(r.n, d, r.d_flags, r.v, ws->d_row_of, ws->d_staged, r.d_out, st);
-        cache_->replace_device_locked(ws->d_found_keys, nf, ws->d_staged);
-        HPSB_CUDA(cudaMemcpyAsync(r.out, r.d_out, r.n * uint64_t(d) * 4, cudaMemcpyDeviceToHost,
-                                  st));
-        HPSB_CUDA(cudaMemcpyAsync(r.flags, r.d_flags, r.n, cudaMemcpyDeviceToHost, st));
+        HPSB_CUDA(cudaEventRecord(ws->done, st));
+        ws->pending = true;
       }
-    }
-    HPSB_CUDA(cudaEventRecord(ws->done, st));
-    HPSB_CUDA(cudaEventSynchronize(ws->done));
-    if (nf > 0 && r.zero_copy) {
-      if (r.out != r.d_out) std::memcpy(r.out, r.d_out, r.n * uint64_t(d) * 4);
-      if (r.flags != r.d_flags) std::memcpy(r.flags, r.d_flags, r.n);
+      ws->scatter_keys = r.miss_keys;
+      host_scatter(*ws, r.n, r.h_keys, r.out, r.um, r.flags);
     }
   } else {
     defaults = r.um;
@@ -1145,13 +1131,9 @@ void MultiLookup::lookup(const uint64_t* const* keys, const size_t* n, float* co
       std::sort(order_.begin(), order_.end(), [fp](uint32_t a, uint32_t b) { return fp[a] < fp[b]; });
       for (uint64_t k = 0; k < r.um; ++k) miss_[k] = hck[koff[t] + order_[k]];
       r.miss_keys = miss_.data();
-      r.order = order_.data();
-      r.v = views[t];
-      r.d_out = direct ? direct_out[t] : reinterpret_cast<float*>(ob + d_rows_) + roff[t];
-      r.d_flags = reinterpret_cast<uint8_t*>(ob + d_flags_) + koff[t];
-      r.zero_copy = zero_copy;
       r.out = out[t];
       r.flags = flags[t];
+      r.h_keys = keys[t];
       eng_[t]->finish_group(r, outcomes ? outcomes + t : nullptr);
     } catch (...) {
       if (!first_error) first_error = std::current_exception();

@@ -111,6 +111,7 @@ struct Workspace {
   std::vector<uint32_t> order;         // claims sorted by first position
   // sync branch of a host-mode call: found miss key -> staged row (open
   // addressing; hs_used marks occupied entries, every u64 is a legal key)
+  const uint64_t* scatter_keys = nullptr;
   std::vector<uint64_t> hs_keys;
   std::vector<int32_t> hs_rows;
   std::vector<uint8_t> hs_used;
@@ -200,13 +201,9 @@ class LookupEngine {
     size_t n = 0;
     uint64_t uh = 0, um = 0;
     const uint64_t* miss_keys = nullptr;  // um keys, reference order
-    const uint32_t* order = nullptr;      // claim index of each miss (sync scatter)
-    LookupView v;
-    float* d_out = nullptr;
-    uint8_t* d_flags = nullptr;
     float* out = nullptr;
     uint8_t* flags = nullptr;
-    bool zero_copy = false;  // d_out / d_flags are pinned host memory
+    const uint64_t* h_keys = nullptr;  // the table's keys (host)
   };
   void finish_group(const GroupResult& r, LookupOutcome* outcome);
 
@@ -245,7 +242,9 @@ class LookupEngine {
   // Sync branch of a host-mode call whose rows came back with the counts:
   // the fetched rows are written straight into the host output at every
   // position of their key (and those flags cleared) by the copy threads.
-  void host_scatter(Workspace& ws, const LookupCall& c, uint64_t um, uint8_t* hflags);
+  // (ws.scatter_keys: the unique misses in the order of ws.h_row_of)
+  void host_scatter(Workspace& ws, size_t n, const uint64_t* keys, float* out, uint64_t um,
+                    uint8_t* hflags);
   LookupCall begin(const uint64_t* keys, size_t n, float* out, size_t out_len, uint8_t* flags,
                    int mem, cudaStream_t user);
   void finish(LookupCall& c, LookupOutcome* outcome);
