@@ -233,3 +233,28 @@ def test_vdb_parallel_lookups_from_several_threads():
     for t in ts:
         t.join()
     assert not errors
+
+
+def test_round2_entry_points_validate_arguments_without_a_gpu():
+    """Replace-mode, peer-memory and drain entry points reject null handles /
+    bad sizes with HPS_INVALID_ARGUMENT and a thread-local message, before
+    touching a device (the C ABI's error contract, hps_b200.h)."""
+    import ctypes as C
+
+    L = hps.lib()
+    assert L.hps_peer_blob_size() >= 64
+    assert L.hps_cache_set_replace_mode(None, 1) == 1  # HPS_INVALID_ARGUMENT
+    assert b"null" in L.hps_last_error()
+    assert L.hps_cache_get_replace_mode(None, None, None) == 1
+    n = C.c_size_t(0)
+    assert L.hps_cache_peer_drain(None, None, 0, C.byref(n)) == 1
+    blob = C.create_string_buffer(L.hps_peer_blob_size())
+    ln = C.c_size_t(0)
+    assert L.hps_cache_peer_export(None, 16, blob, len(blob), C.byref(ln)) == \
+        1
+    g = C.c_void_p()
+    assert L.hps_peer_group_create(None, 0, 1, blob, len(blob), C.byref(g)) == \
+        1
+    assert L.hps_peer_lookup_device(None, None, 0, None, None, None, None) == \
+        1
+    assert L.hps_peer_group_destroy(None) == 0
