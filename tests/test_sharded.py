@@ -384,7 +384,7 @@ def _peer_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [1, 2])
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_peer_memory_sharded_lookup_two_processes_one_gpu(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -404,3 +404,32 @@ def test_peer_memory_sharded_lookup_two_processes_one_gpu(world):
                 p.kill()
     assert all(res.get(r) is True for r in range(world)), res
     assert all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.gpu
+def test_peer_inbox_overflow_is_counted_and_bounded():
+    """An owner's inbox holds inbox_cap keys between drains: appends beyond it
+    are dropped but counted (the drain reports how many were appended), and
+    the inbox is empty again after the drain."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        cache = hps.SlabCache(hps.SlabCacheConfig(slabset_count=8, slabs_per_set=2, dimension=D))
+        peer = sharded.PeerShardedLookup(cache, inbox_cap=16)
+        keys = torch.arange(1000, dtype=torch.int64, device="cuda") * 7 + 3
+        default = torch.zeros(D, device="cuda")
+        out, fl = peer.lookup(keys, default)
+        torch.cuda.synchronize()
+        assert int(fl.sum().item()) == 1000  # empty shard: every key misses
+        import ctypes as C
+
+        buf = np.empty(16, dtype=np.uint64)
+        n = C.c_size_t(0)
+        assert hps.lib().hps_cache_peer_drain(cache.handle, buf.ctypes.data, 16, C.byref(n)) == 0
+        assert n.value == 1000  # one append per distinct key of a warp: all distinct here
+        assert set(int(k) for k in buf) <= set(range(3, 7000, 7))
+        assert len(cache.peer_drain(16)) == 0  # empty after the drain
+        peer.close()
+    finally:
+        dist.destroy_process_group()
