@@ -161,7 +161,7 @@ void launch_select_misses(const uint64_t* keys, const uint8_t* hit, uint64_t n,
 //                    round trips per set: (set state, indices, keys) -> rows.
 size_t replace_scratch_bytes(uint64_t n) {
   const uint64_t cap = pow2_at_least(2 * n);
-  return align_up(cap * 8, 256) + align_up(cap * 4, 256) * 2 + align_up(cap * 4 * kReplaceInline, 256) +
+  return align_up(cap * 8, 256) + align_up(cap * 4, 256) * 2 + align_up(cap * 4 * kReplaceInline, 256) * 2 +
          align_up(cap * 8 * kReplaceInline, 256) + align_up(n * 4, 256) * 4 + 256;
 }
 
@@ -184,6 +184,7 @@ ReplaceScratch replace_scratch_carve(void* base, uint64_t n) {
   r.lead_e = take(n * 4);
   r.idx = take(r.cap * 4 * kReplaceInline);
   r.kin = reinterpret_cast<uint64_t*>(take(r.cap * 8 * kReplaceInline));
+  r.hin = take(r.cap * 4 * kReplaceInline);
   r.next = take(n * 4);
   r.lead_s = take(n * 4);
   r.bucket = take(n * 4);
@@ -211,9 +212,31 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #define HPSB_REPL_KPRE 2
 #endif
 
+// DIRECT: a call touching a cache of at most `cap` slabsets indexes the set
+// table by the slabset itself (one atomicAdd per key, no CAS probe). FAST:
+// the bin kernel hands each inline key's slab meta to the set kernel, and
+// the eviction argmin uses 32-bit warp min-reductions while every counter
+// and the stamp fit in 32 bits. Together 47.1-47.6 -> 40.9-42.4 us per
+// 65,536-key fill (profiles/r02_ab_replace.txt, r02ay).
+#ifndef HPSB_REPL_DIRECT
+#define HPSB_REPL_DIRECT 1
+#endif
+#ifndef HPSB_REPL_FAST
+#define HPSB_REPL_FAST 1
+#endif
 #ifndef HPSB_REPL_BINAGG
 #define HPSB_REPL_BINAGG 1
 #endif
+// A key's slab-hash facts the set kernel needs (its first probed slab and
+// its fingerprint), computed once per key by the bin kernel's thread rather
+// than by a whole warp per set: tag << 24 | first slab.
+__device__ __forceinline__ uint32_t slab_meta(const CacheDev& c, uint64_t key) {
+  const uint64_t h2 = xxh64_key(key, kSlabSeed);
+  const uint32_t first =
+      c.W == 1 ? 0u : (c.W == 2 ? uint32_t(h2 & 1u) : uint32_t(fastmod(h2, c.W, c.mW)));
+  return (uint32_t(key_tag(h2)) << 24) | first;
+}
+
 __global__ void __launch_bounds__(256)
     k_replace_bin(CacheDev c, const uint64_t* __restrict__ keys, uint64_t n, ReplaceScratch rs) {
   // the set kernel may launch now (it waits for this grid before reading)
@@ -233,7 +256,18 @@ __global__ void __launch_bounds__(256)
     const uint64_t mask = rs.cap - 1;
     uint64_t e = fmix64(set + 1ull) & mask;
     uint32_t r;
+#if HPSB_REPL_DIRECT
+    // no more sets than table entries: the set IS its entry (one atomic per
+    // key for its rank, no CAS probe)
+    const bool direct = c.S <= rs.cap;
+    if (direct) {
+      e = set;
+      r = uint32_t(atomicAdd(rs.ent + e, 1ull));
+    }
+    while (!direct) {
+#else
     while (true) {
+#endif
       const unsigned long long old = atomicCAS(rs.ent + e, 0ull, tag | 1ull);
       if (old == 0ull) {
         r = 0;
@@ -248,6 +282,9 @@ __global__ void __launch_bounds__(256)
     if (r < kReplaceInline) {
       rs.idx[e * kReplaceInline + r] = uint32_t(i);
       rs.kin[e * kReplaceInline + r] = key;
+#if HPSB_REPL_FAST
+      rs.hin[e * kReplaceInline + r] = slab_meta(c, key);
+#endif
     } else {
       rs.next[i] = atomicExch(rs.ovf + e, uint32_t(i));
     }
@@ -331,10 +368,14 @@ __device__ __forceinline__ uint32_t small_group(const ReplaceScratch& rs, uint64
                                                 const uint64_t* __restrict__ keys, uint32_t* sw,
                                                 uint64_t* sk, uint64_t* key,
                                                 bool preloaded = false, uint32_t v_in = kNone,
-                                                uint64_t k_in = 0) {
+                                                uint64_t k_in = 0, uint32_t* meta = nullptr,
+                                                const CacheDev* cd = nullptr) {
+  // meta != nullptr: *meta holds the lane's preloaded slab meta on entry and
+  // the sorted one on return (keys past the inline ones: computed here)
   const uint32_t lane = lane_id();
   uint32_t v = kNone;
   uint64_t k = 0;
+  uint32_t mt = meta ? *meta : 0u;
   if (lane < kReplaceInline && lane < cnt) {
     v = preloaded ? v_in : rs.idx[e * kReplaceInline + lane];
     k = preloaded ? k_in : rs.kin[e * kReplaceInline + lane];
@@ -348,6 +389,9 @@ __device__ __forceinline__ uint32_t small_group(const ReplaceScratch& rs, uint64
     if (lane >= kReplaceInline && lane < cnt) {
       v = sw[lane];
       k = keys[v];
+#if HPSB_REPL_FAST
+      if (meta) mt = slab_meta(*cd, k);
+#endif
     }
     __syncwarp();
   }
@@ -357,15 +401,24 @@ __device__ __forceinline__ uint32_t small_group(const ReplaceScratch& rs, uint64
       const uint32_t o = __shfl_sync(0xFFFFFFFFu, v, j);
       rank += (o < v) ? 1u : 0u;
     }
+    // the metas sorted the same way (sw reused once the indices are out)
     if (lane < cnt) {
       sw[rank] = v;
       sk[rank] = k;
     }
     __syncwarp();
-    v = lane < cnt ? sw[lane] : kNone;
+    const uint32_t vs = lane < cnt ? sw[lane] : kNone;
     k = lane < cnt ? sk[lane] : 0ull;
     __syncwarp();
+    if (meta) {
+      if (lane < cnt) sw[rank] = mt;
+      __syncwarp();
+      mt = lane < cnt ? sw[lane] : 0u;
+      __syncwarp();
+    }
+    v = vs;
   }
+  if (meta) *meta = mt;
   *key = k;
   return v;
 }
@@ -427,7 +480,8 @@ __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_
                                                   uint32_t cnt, uint32_t my_idx,
                                                   uint64_t my_key_in,
                                                   const uint32_t* __restrict__ big,
-                                                  const SetRegs<W>& loaded) {
+                                                  const SetRegs<W>& loaded,
+                                                  uint32_t my_meta_in = 0u) {
   constexpr int kPre = HPSB_REPL_KPRE;  // rows prefetched (d <= 128, 16 B aligned)
   const uint32_t lane = lane_id();
   const uint32_t d = c.d;
@@ -437,11 +491,28 @@ __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_
 #pragma unroll
   for (int w = 0; w < W; ++w) m0[w] = st.m[w];
   // lane j < cnt: key and first-slab hash of the j-th key (small groups)
-  uint64_t my_key = 0, my_h2 = 0;
+  uint64_t my_key = 0;
+#if HPSB_REPL_FAST
+  // the bin kernel's per-key slab meta (tag << 24 | first slab)
+  uint32_t my_meta = 0;
+  if (big == nullptr && my_idx != kNone) {
+    my_key = my_key_in;
+    my_meta = my_meta_in;
+  }
+  // every counter of the set and the stamp below 2^32: the eviction argmin
+  // runs on the low words with warp min-reductions
+  bool lo32 = (stamp >> 32) == 0;
+#pragma unroll
+  for (int x = 0; x < W; ++x) lo32 = lo32 && (st.ct[x] >> 32) == 0;
+  lo32 = __all_sync(0xFFFFFFFFu, lo32);
+#else
+  (void)my_meta_in;
+  uint64_t my_h2 = 0;
   if (big == nullptr && my_idx != kNone) {
     my_key = my_key_in;
     my_h2 = xxh64_key(my_key, kSlabSeed);
   }
+#endif
   const bool vec = (d & 3u) == 0 && d <= 128 && (reinterpret_cast<uintptr_t>(rows) & 15u) == 0;
   float4 pre[kPre];
   if (vec && big == nullptr) {
@@ -456,7 +527,22 @@ __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_
   uint32_t inserted = 0;
   for (uint32_t j = 0; j < cnt; ++j) {
     uint32_t ij;
-    uint64_t key, h2;
+    uint64_t key;
+#if HPSB_REPL_FAST
+    uint32_t meta;
+    if (big == nullptr) {
+      ij = __shfl_sync(0xFFFFFFFFu, my_idx, j);
+      key = __shfl_sync(0xFFFFFFFFu, my_key, j);
+      meta = __shfl_sync(0xFFFFFFFFu, my_meta, j);
+    } else {
+      ij = big[j];
+      key = keys[ij];
+      meta = slab_meta(c, key);
+    }
+    const uint32_t first = meta & 0xFFFFFFu;
+    const uint8_t ktag = uint8_t(meta >> 24);
+#else
+    uint64_t h2;
     if (big == nullptr) {
       ij = __shfl_sync(0xFFFFFFFFu, my_idx, j);
       key = __shfl_sync(0xFFFFFFFFu, my_key, j);
@@ -467,6 +553,8 @@ __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_
       h2 = xxh64_key(key, kSlabSeed);
     }
     const uint32_t first = W == 1 ? 0u : (W == 2 ? uint32_t(h2 & 1u) : uint32_t(fastmod(h2, W, c.mW)));
+    const uint8_t ktag = key_tag(h2);
+#endif
     // probe in slab order from `first` (slab_cache.cpp:292-310)
     int hit_w = -1, ins_w = -1;
     uint32_t hit_j = 0;
@@ -525,13 +613,21 @@ __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_
           bc = st.ct[x];
           bi = uint32_t(x) * 32 + lane;
         }
+#if HPSB_REPL_FAST
+      if (lo32) {
+        const uint32_t mn = __reduce_min_sync(0xFFFFFFFFu, uint32_t(bc));
+        bi = __reduce_min_sync(0xFFFFFFFFu, uint32_t(bc) == mn ? bi : 0xFFFFFFFFu);
+      } else
+#endif
+      {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, bc, o);
-        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
-        if (oc < bc || (oc == bc && oi < bi)) {
-          bc = oc;
-          bi = oi;
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t oc = __shfl_xor_sync(0xFFFFFFFFu, bc, o);
+          const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+          if (oc < bc || (oc == bc && oi < bi)) {
+            bc = oc;
+            bi = oi;
+          }
         }
       }
       tw = int(bi >> 5);
@@ -547,7 +643,7 @@ __device__ __forceinline__ uint32_t replace_apply_set(const CacheDev& c, uint64_
         }
       c.keys[slot] = key;
       c.counters[slot] = stamp;
-      c.tags[slot] = key_tag(h2);
+      c.tags[slot] = ktag;
     }
     const float* src = rows + uint64_t(ij) * d;
     float* dst = c.rows + slot * d;
@@ -605,11 +701,14 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
     // masks / keys / counters -- all depend only on the list entry
     const uint32_t cnt = uint32_t(rs.ent[e]);
     const uint32_t lane = lane_id();
-    uint32_t v_in = kNone;
+    uint32_t v_in = kNone, m_in = 0u;
     uint64_t k_in = 0;
     if (lane < kReplaceInline) {
       v_in = rs.idx[uint64_t(e) * kReplaceInline + lane];
       k_in = rs.kin[uint64_t(e) * kReplaceInline + lane];
+#if HPSB_REPL_FAST
+      if constexpr (W > 0) m_in = rs.hin[uint64_t(e) * kReplaceInline + lane];
+#endif
     }
     SetRegs<W == 0 ? 1 : W> pre;
     if constexpr (W > 0) {
@@ -618,7 +717,8 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
     if (!rejected) {
       uint64_t k = 0;
       const uint32_t v = cnt <= 32 ? small_group(rs, e, cnt, keys, s_w[threadIdx.x >> 5],
-                                                 s_k[threadIdx.x >> 5], &k, true, v_in, k_in)
+                                                 s_k[threadIdx.x >> 5], &k, true, v_in, k_in,
+                                                 (HPSB_REPL_FAST && W > 0) ? &m_in : nullptr, &c)
                                    : kNone;
       const uint32_t* b = cnt <= 32 ? nullptr : big_bucket(rs, e, cnt);
       if constexpr (W == 0) {
@@ -627,7 +727,7 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
           warp_replace_key(c, set, keys[ij], rows + uint64_t(ij) * c.d, stamp);
         }
       } else {
-        inserted += replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b, pre);
+        inserted += replace_apply_set<W>(c, set, keys, rows, stamp, cnt, v, k, b, pre, m_in);
       }
     }
     __syncwarp();

@@ -52,6 +52,7 @@ struct ReplaceScratch {
   unsigned long long* ent = nullptr;  // cap: (slabset + 1) << 32 | keys of the set (0 = free)
   uint32_t* idx = nullptr;    // cap * kReplaceInline: key indices, arrival order
   uint64_t* kin = nullptr;    // cap * kReplaceInline: the keys themselves
+  uint32_t* hin = nullptr;    // cap * kReplaceInline: their slab-hash meta (tag << 24 | first slab)
   uint32_t* ovf = nullptr;    // cap: overflow list head (~0 = none)
   uint32_t* boff = nullptr;   // cap: sorted bucket of a set with > 32 keys (~0 = none)
   uint32_t* next = nullptr;   // ncap: overflow list links
