@@ -227,6 +227,11 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #ifndef HPSB_REPL_BINAGG
 #define HPSB_REPL_BINAGG 1
 #endif
+// DYN: items handed out per block from a shared counter (40.3-40.9 -> 39.2-39.8 us,
+// r02bb; one global counter was slower: r02q)
+#ifndef HPSB_REPL_DYN
+#define HPSB_REPL_DYN 1
+#endif
 // A key's slab-hash facts the set kernel needs (its first probed slab and
 // its fingerprint), computed once per key by the bin kernel's thread rather
 // than by a whole warp per set: tag << 24 | first slab.
@@ -677,13 +682,24 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
   __shared__ uint32_t s_w[8][32];
   __shared__ uint64_t s_k[8][32];
   __shared__ unsigned long long s_ins;
+#if HPSB_REPL_DYN
+  // the block's items are list entries blockIdx + gridDim * k; its warps
+  // take k = 0..7 first, then grab the next k from a shared counter (sets
+  // carry 1..10 keys: a static share leaves warps idle at the end)
+  __shared__ uint32_t s_next;
+  if (threadIdx.x == 0) s_next = blockDim.x >> 5;
+#endif
   if (threadIdx.x == 0) s_ins = 0ull;
   __syncthreads();
   // launched as the bin kernel's programmatic dependent: everything below
   // reads what bin wrote
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if HPSB_REPL_DYN
+  uint64_t w = uint64_t(blockIdx.x) + uint64_t(gridDim.x) * (threadIdx.x >> 5);
+#else
   const uint64_t stride = uint64_t(gridDim.x) * (blockDim.x >> 5);
   uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+#endif
   // the list is consumed through its sentinels; its count restarts here
   if (blockIdx.x == 0 && threadIdx.x == 0) rs.cursor[2] = 0u;
   const bool rejected = validate && *reinterpret_cast<volatile uint32_t*>(rs.dup_flag) != 0u;
@@ -692,7 +708,14 @@ __global__ void __launch_bounds__(256, HPSB_REPL_MINB)
   uint32_t inserted = 0;
   while (e != kNone) {
     // the next item's list entry is in flight while this one is applied
+#if HPSB_REPL_DYN
+    uint32_t kn = 0;
+    if (lane_id() == 0) kn = atomicAdd(&s_next, 1u);
+    const uint64_t wn =
+        uint64_t(blockIdx.x) + uint64_t(gridDim.x) * __shfl_sync(0xFFFFFFFFu, kn, 0);
+#else
     const uint64_t wn = w + stride;
+#endif
     const uint32_t en = wn < n ? rs.lead_e[wn] : kNone;
     const uint32_t sn = wn < n ? rs.lead_s[wn] : 0u;
     const uint64_t set = sset;
