@@ -696,7 +696,9 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=Fal
             "ms_per_step": el * 1e3 / args.steps, "mean_unique_hit_rate": float(np.mean(hs)),
             "p50_call_us": float(np.percentile(lat_us, 50)),
             "p99_call_us": float(np.percentile(lat_us, 99)),
-            "call_us": [round(float(x), 1) for x in lat_us],
+            # the first 64 calls (the full list made the line ~50 KB at 2,000 steps)
+            "call_us_first64": [round(float(x), 1) for x in lat_us[:64]],
+            "max_call_us": float(np.max(lat_us)),
             "api": "hps_engine_lookup (LookupEngine::lookup), "
                    + ("PAGEABLE" if pageable else "pinned") + " host buffers, "
                    f"threshold {threshold}, target unique hit {hit}; VDB fetch + scatter + "

@@ -42,6 +42,9 @@ def main():
     ap.add_argument("--update-frac", type=float, default=0.0,
                     help="cfg 4: stream-ordered update of this fraction of the resident rows "
                          "after every lookup")
+    ap.add_argument("--per-call", action="store_true",
+                    help="also print every call's first block start, last phase A, last copy "
+                         "and finish end relative to the first call's start (fill / drain)")
     a = ap.parse_args()
     wl = bench.Workload(batch=a.batch, dim=a.dim)
     d, n = wl.dim, wl.batch
@@ -150,6 +153,12 @@ def main():
     for j, nm in enumerate(names):
         col = rel[:, j]
         print(f"  {nm:16s} {np.median(col):7.2f}  [{np.percentile(col, 10):6.2f}, {np.percentile(col, 90):6.2f}]")
+    if a.per_call:
+        z = t[0, 0]
+        print("  call   start  lastA  lastcopy  finish_end  (us from call 0 start)")
+        for i in range(len(t)):
+            print(f"  {i:4d} {(t[i, 0] - z) / 1e3:7.2f} {(t[i, 1] - z) / 1e3:6.2f} "
+                  f"{(t[i, 5] - z) / 1e3:8.2f} {(t[i, 7] - z) / 1e3:10.2f}")
     gap = np.diff(t[:, 0]) / 1e3
     end_to_start = (t[1:, 0] - t[:-1, 7]) / 1e3
     print(f"  start-to-start gap      {np.median(gap):7.2f}  [{np.percentile(gap, 10):6.2f}, {np.percentile(gap, 90):6.2f}]")
