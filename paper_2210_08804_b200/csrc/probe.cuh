@@ -188,12 +188,32 @@ __device__ __forceinline__ uint32_t dedup_insert(uint64_t* table, uint64_t cap,
 // positions of the same key compare through the immutable input and keep
 // the minimum position with a fire-and-forget atomicMin. The ordering tail
 // clears every claimed entry, so the table is all-zero between calls.
+// READ_FIRST: the entry is read (L2, never a stale L1 line) before the CAS, and
+// an entry already holding this key is joined without one -- a power-law
+// batch's hottest missing keys sit in nearly every warp, and ~2,000 CASes per
+// call on one entry serialise in its L2 slice (the recency counters had the
+// same problem, §5).
+#ifndef HPSB_CLAIM_READ_FIRST
+#define HPSB_CLAIM_READ_FIRST 1
+#endif
 __device__ __forceinline__ uint32_t miss_insert(uint32_t* table, uint64_t cap,
                                                 const uint64_t* __restrict__ keys, uint64_t key,
                                                 uint32_t pos, bool* claimed) {
   uint64_t t = fmix64(key ^ 0x9E3779B97F4A7C15ull) & (cap - 1);
   const uint32_t mine = pos + 1;
   while (true) {
+#if HPSB_CLAIM_READ_FIRST
+    const uint32_t seen = __ldcg(table + t);
+    if (seen != 0u) {
+      if (keys[seen - 1] == key) {
+        *claimed = false;
+        if (mine < seen) atomicMin(table + t, mine);
+        return uint32_t(t);
+      }
+      t = (t + 1) & (cap - 1);
+      continue;
+    }
+#endif
     const uint32_t old = atomicCAS(table + t, 0u, mine);
     if (old == 0u) {
       *claimed = true;
