@@ -457,7 +457,11 @@ def run_ours(args, rank, world, local_rank):
         # next to the pinned headline: the same call with pageable buffers,
         # and the synchronous miss path (h 0.5 under threshold 0.8)
         e2e["pageable"] = run_e2e(args, hps, torch, cache, wl, dev, rank, dist, pageable=True)
-        e2e["sync_h050"] = run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=0.5)
+        # (the sync leg's misses are admitted as it runs, so the cycle of 32
+        # batches drifts to the async branch: it times at most 20 calls after
+        # at most 3 warm-up calls, while the misses still force the sync path)
+        e2e["sync_h050"] = run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=0.5,
+                                   max_steps=20, max_warmup=3)
         if world == 1:
             e2e["dropin_cpp"] = run_dropin(args, wl)
     clk = clocks.stop()
@@ -628,7 +632,7 @@ def run_online(args, hps, torch, cache, wl, dev, st, dkeys):
 
 
 def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=False,
-            threshold=0.8):
+            threshold=0.8, max_steps=None, max_warmup=None):
     """hps_engine_lookup with HOST buffers, copies inside the timed region.
     pinned (default): page-locked keys / rows / flags (the headline e2e);
     pageable: plain numpy buffers (rows come back through the engine's
@@ -636,6 +640,8 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=Fal
     mix (h 0.5 at threshold 0.8 = every batch on the synchronous miss path)."""
     d, n = wl.dim, wl.batch
     hit = args.hit if hit is None else hit
+    steps = args.steps if max_steps is None else min(args.steps, max_steps)
+    warmup = args.warmup if max_warmup is None else min(args.warmup, max_warmup)
     batches, p, _ = wl.batches(hit, 32, seed=3000 + rank + int(hit * 100))
     vdb = hps.VolatileStore(8)
     table = hps.TableId("bench", d)
@@ -667,7 +673,7 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=Fal
         kp = [t.data_ptr() for t in pk]
         op = [t.data_ptr() for t in po]
         fp = [t.data_ptr() for t in pf]
-    for s in range(args.warmup):
+    for s in range(warmup):
         eng.lookup_ptrs(kp[s % 32], n, op[s % ring], fp[s % ring], hps.HPS_MEM_HOST)
     eng.drain_async()
     torch.cuda.synchronize()
@@ -677,7 +683,7 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=Fal
     l0 = hps.kernel_launch_count()
     hs, lat = [], []
     t0 = time.perf_counter()
-    for s in range(args.steps):
+    for s in range(steps):
         c0 = time.perf_counter()
         o = eng.lookup_ptrs(kp[s % 32], n, op[s % ring], fp[s % ring], hps.HPS_MEM_HOST)
         lat.append(time.perf_counter() - c0)
@@ -691,9 +697,9 @@ def run_e2e(args, hps, torch, cache, wl, dev, rank, dist, hit=None, pageable=Fal
     st = eng.stats()
     eng.close()
     lat_us = np.array(lat) * 1e6
-    return {"value": world * args.steps * n / el, "unit": "keys/s",
+    return {"value": world * steps * n / el, "unit": "keys/s", "steps": steps,
             "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * d * 4 + n,
-            "ms_per_step": el * 1e3 / args.steps, "mean_unique_hit_rate": float(np.mean(hs)),
+            "ms_per_step": el * 1e3 / steps, "mean_unique_hit_rate": float(np.mean(hs)),
             "p50_call_us": float(np.percentile(lat_us, 50)),
             "p99_call_us": float(np.percentile(lat_us, 99)),
             # the first 64 calls (the full list made the line ~50 KB at 2,000 steps)
