@@ -154,15 +154,27 @@ __global__ void __launch_bounds__(256, 3)
   const uint64_t tag = hit ? ((uint64_t(owner) << 32) | res) : ~0ull;
   const uint32_t same = __match_any_sync(0xFFFFFFFFu, tag);
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (hit && (__ffs(same) - 1) == lane)
-    atomicMax(reinterpret_cast<unsigned long long*>(sh.c.counters) + res, stamps[owner]);
-  // misses: one inbox append per distinct key of the warp
+  if (hit && (__ffs(same) - 1) == lane) {
+    // read first: a hot slot is hit by nearly every warp of the call, and
+    // same-line atomics serialise in its L2 slice (as in the local lookup)
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(sh.c.counters) + res;
+    const unsigned long long st = stamps[owner];
+    if (__ldcg(ctr) < st) atomicMax(ctr, st);
+  }
+  // misses: one inbox entry per distinct key of the warp, reserved with one
+  // add per (warp, owner) on the owner's inbox counter
   const bool miss = valid && !hit;
-  // (every lane runs both warp-collective calls: no short-circuit around them)
+  // (every lane runs the warp-collective calls: no short-circuit around them)
   const uint32_t same_key = __match_any_sync(0xFFFFFFFFu, miss ? key : 0ull);
   const uint32_t missing = __ballot_sync(0xFFFFFFFFu, miss);
-  if (miss && (__ffs(same_key & missing) - 1) == lane) {
-    const unsigned long long at = atomicAdd(sh.inbox_count, 1ull);
+  const bool lead_miss = miss && (__ffs(same_key & missing) - 1) == lane;
+  const uint32_t same_owner = __match_any_sync(0xFFFFFFFFu, lead_miss ? owner : ~0u);
+  const uint32_t grp = same_owner & __ballot_sync(0xFFFFFFFFu, lead_miss);
+  if (lead_miss) {
+    const uint32_t first = __ffs(grp) - 1;
+    unsigned long long at = 0;
+    if (lane == first) at = atomicAdd(sh.inbox_count, (unsigned long long)__popc(grp));
+    at = __shfl_sync(grp, at, first) + __popc(grp & ((1u << lane) - 1u));
     if (at < sh.inbox_cap) sh.inbox_keys[at] = key;
   }
   if (valid) flags[pos] = miss ? 1 : 0;
