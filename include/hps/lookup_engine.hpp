@@ -19,10 +19,13 @@
 #pragma once
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "hps/persistent_store.hpp"
@@ -201,7 +204,15 @@ class LookupEngine {
                                          &b200_detail::pdb_fetch, &tier_, &c, &h_));
     pool_.engine_ = h_;
   }
-  ~LookupEngine() { hps_engine_destroy(h_); }
+  ~LookupEngine() {
+    {
+      std::lock_guard<std::mutex> lk(spare_mu_);
+      spare_stop_ = true;
+    }
+    spare_cv_.notify_all();
+    if (spare_thr_.joinable()) spare_thr_.join();
+    hps_engine_destroy(h_);
+  }
 
   LookupEngine(const LookupEngine&) = delete;
   LookupEngine& operator=(const LookupEngine&) = delete;
@@ -210,7 +221,7 @@ class LookupEngine {
   LookupResult lookup(std::span<const EmbeddingKey> keys, LookupOutcome* outcome = nullptr) {
     LookupResult r;
     r.dimension = table_.dimension;
-    r.vectors = b200_detail::sized_vector<float>(keys.size() * table_.dimension);
+    r.vectors = take_result_storage(keys.size() * table_.dimension);
     r.miss_flags.resize(keys.size());
     hps_lookup_outcome o{};
     b200_detail::check(hps_engine_lookup(h_, keys.data(), keys.size(), r.vectors.data(),
@@ -269,6 +280,54 @@ class LookupEngine {
   WorkspacePool& workspace_pool() { return pool_; }
 
  private:
+  // Result storage (B200 extension, no API change): LookupResult::vectors is
+  // a std::vector<float> the call hands to the caller, and sizing one
+  // zero-fills it (33.5 MB per cfg-2 call, serial, before any row can land).
+  // Large results are instead taken from a spare vector a background thread
+  // has already sized for the previous call's shape, and the thread sizes
+  // the next spare while the caller works -- the zero-fill leaves the call's
+  // critical path. Other sizes, or a spare not ready yet, size in the call
+  // as before. Every element is overwritten by the lookup either way.
+  static constexpr std::size_t kSpareMinFloats = std::size_t(1) << 18;  // 1 MB
+  std::vector<float> take_result_storage(std::size_t n) {
+    if (n < kSpareMinFloats) return b200_detail::sized_vector<float>(n);
+    std::vector<float> v;
+    {
+      std::lock_guard<std::mutex> lk(spare_mu_);
+      if (spare_ready_ && spare_.size() == n) {
+        v.swap(spare_);
+        spare_ready_ = false;
+      }
+      spare_want_ = n;
+      if (!spare_thr_.joinable()) spare_thr_ = std::thread([this] { spare_loop(); });
+    }
+    spare_cv_.notify_one();
+    if (v.size() != n) v = b200_detail::sized_vector<float>(n);
+    return v;
+  }
+  void spare_loop() {
+    std::unique_lock<std::mutex> lk(spare_mu_);
+    while (true) {
+      spare_cv_.wait(lk, [this] { return spare_stop_ || (!spare_ready_ && spare_want_ != 0); });
+      if (spare_stop_) return;
+      const std::size_t n = spare_want_;
+      lk.unlock();
+      std::vector<float> v = b200_detail::sized_vector<float>(n);
+      lk.lock();
+      if (spare_want_ == n) {
+        spare_ = std::move(v);
+        spare_ready_ = true;
+      }
+    }
+  }
+  std::mutex spare_mu_;
+  std::condition_variable spare_cv_;
+  std::vector<float> spare_;
+  std::size_t spare_want_ = 0;
+  bool spare_ready_ = false;
+  bool spare_stop_ = false;
+  std::thread spare_thr_;
+
   TableId table_;
   SlabCache& cache_;
   VolatileStore* vdb_;
